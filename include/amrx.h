@@ -1,0 +1,195 @@
+/* amrx -- B200-native dual-mesh / iso-surface extraction for structured AMR.
+ *
+ * The C ABI every host binding goes through (the C++ drop-in shim in
+ * paper_2004_08475_b200/shim/, the Python host mirror over ctypes, and any
+ * FFI a maintainer adds).  Plain pointers and sizes only.
+ *
+ * Which reference interface each entry point replaces (paths relative to the
+ * reference checkout, /root/reference/):
+ *
+ *   amrx_index_create     build_index(vector<CellCoord>, vector<double>)
+ *                         proj/include/amriso/locator.hpp:52-53,
+ *                         proj/src/locator.cpp:26-92
+ *   amrx_index_download   CellIndex.data.{cells,scalars} / .levels / bounds
+ *                         proj/include/amriso/locator.hpp:38-45,
+ *                         proj/include/amriso/core.hpp:143-148
+ *   amrx_find_exact       find_exact   proj/src/locator.cpp:94-101
+ *   amrx_snap             snap         proj/src/locator.cpp:122-134
+ *   amrx_try_build_duals  try_build_dual (batched) proj/src/dual.cpp:41-72
+ *   amrx_extract_dual     extract_dual_mesh  proj/include/amriso/pipeline.hpp:70-71,
+ *                         proj/src/pipeline.cpp:160-194
+ *   amrx_extract_iso      extract_isosurface passes 1+2 (the fat soup, before
+ *                         weld) proj/include/amriso/pipeline.hpp:65-66,
+ *                         proj/src/pipeline.cpp:67-146
+ *   amrx_stats            ExtractionStats proj/include/amriso/pipeline.hpp:29-49
+ *   amrx_status codes     LoadError / invalid_argument / length_error /
+ *                         logic_error (core.hpp:62-74, locator.cpp:29-50,
+ *                         pipeline.cpp:70-71,116-118)
+ *
+ * Memory: every pointer argument may be host memory (pageable or pinned) or
+ * CUDA device memory on the index's device; the library detects which with
+ * cudaPointerGetAttributes and copies as needed.  Calls are synchronous with
+ * respect to the host (they run on the index's stream and synchronise it
+ * before returning).  Output order is the reference's candidate order
+ * (owning cell major, delta minor, table order within a hex), independent of
+ * launch configuration and of the multi-GPU partition.
+ */
+#ifndef AMRX_H
+#define AMRX_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define AMRX_API __attribute__((visibility("default")))
+#else
+#define AMRX_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum amrx_status {
+  AMRX_OK = 0,
+  AMRX_ERR_LOAD = 1,          /* malformed input -> LoadError ("record n: ...") */
+  AMRX_ERR_INVALID_ARG = 2,   /* empty dataset / bad argument -> invalid_argument */
+  AMRX_ERR_LENGTH = 3,        /* output too large for 32-bit indices -> length_error */
+  AMRX_ERR_INTERNAL = 4,      /* internal consistency check failed -> logic_error */
+  AMRX_ERR_CUDA = 5,          /* CUDA runtime failure (message names the call) */
+  AMRX_ERR_CAPACITY = 6,      /* caller buffer too small; *count holds the need */
+  AMRX_ERR_UNSUPPORTED = 7,   /* dataset outside this build's limits */
+  AMRX_ERR_NO_DEVICE = 8      /* no CUDA device / kernel image for this GPU */
+} amrx_status;
+
+typedef struct amrx_index amrx_index;
+
+/* index construction options (NULL = defaults) */
+typedef struct amrx_index_opts {
+  int device;        /* CUDA device ordinal; -1 = current device */
+  void *stream;      /* cudaStream_t to run on; NULL = library-owned stream */
+  uint32_t flags;    /* AMRX_FLAG_* */
+} amrx_index_opts;
+
+/* input is already in (i,j,k,level) order with stable ties (e.g. the arrays
+ * of an existing CellIndex): the library verifies this on the device and
+ * skips the radix sort */
+#define AMRX_FLAG_PRESORTED 0x1u
+
+typedef struct amrx_index_info {
+  uint64_t cell_count;
+  int32_t max_level;
+  int32_t level_count;
+  int32_t levels[31];       /* distinct levels present, finest first */
+  int64_t bounds_lo[3];     /* hull of all cell boxes (locator.cpp:70-83) */
+  int64_t bounds_hi[3];
+  int32_t key_bits;         /* bits of the packed 64-bit sort key in use */
+  int32_t directory_bits;   /* log2 of the search directory size */
+  uint64_t duplicate_keys;  /* adjacent equal keys after the sort */
+  uint64_t device_bytes;    /* HBM held by the index */
+  double seconds_ingest;    /* device time of pack + sort + gather + directory */
+} amrx_index_info;
+
+typedef struct amrx_stats {
+  uint64_t cell_count;
+  uint64_t duals_accepted;
+  uint64_t duals_missing_corner;
+  uint64_t duals_finer_corner;
+  uint64_t duals_lower_key_corner;
+  uint64_t pass1_triangle_count;  /* counted before the emit pass */
+  uint64_t fat_triangle_count;    /* written by the emit pass */
+  uint64_t dual_count;            /* duals emitted (== duals_accepted) */
+  double seconds_pass1;           /* device time, search + count phase */
+  double seconds_pass2;           /* device time, emit phase (fused: 0) */
+  uint64_t kernel_launches;       /* kernels this call launched */
+} amrx_stats;
+
+/* Build a device index: pack (i,j,k,level) into 64-bit keys, radix-sort
+ * them with the input position as a stable tie-break, gather the scalars,
+ * build the search directory.  Errors mirror build_index: empty input,
+ * length mismatch, > 2^32-1 cells, level outside [0,30], misaligned anchor
+ * (message names "record n" like locator.cpp:37-49). */
+AMRX_API amrx_status amrx_index_create(const int32_t *cells4, const double *scalars,
+                              uint64_t n_cells, uint64_t n_scalars,
+                              const amrx_index_opts *opts, amrx_index **out);
+
+AMRX_API amrx_status amrx_index_destroy(amrx_index *index);
+
+AMRX_API amrx_status amrx_index_get_info(const amrx_index *index, amrx_index_info *out);
+
+/* the sorted cells (4 x int32 each) and scalars; either pointer may be NULL */
+AMRX_API amrx_status amrx_index_download(const amrx_index *index, int32_t *cells4,
+                                double *scalars);
+
+/* device pointers of the sorted packed keys (u64) and scalars (f64) --
+ * what the multi-GPU path broadcasts */
+AMRX_API amrx_status amrx_index_device_arrays(const amrx_index *index, void **keys,
+                                     void **scalars);
+
+/* Adopt already-sorted packed keys + scalars (e.g. received by NCCL
+ * broadcast) with the geometry of a source index: no sort, directory only.
+ * geometry: the 16 int64 words from amrx_index_geometry(). */
+AMRX_API amrx_status amrx_index_geometry(const amrx_index *index, int64_t *geometry16);
+AMRX_API amrx_status amrx_index_adopt(const void *keys_dev, const double *scalars_dev,
+                             uint64_t n_cells, const int64_t *geometry16,
+                             const amrx_index_opts *opts, amrx_index **out);
+
+/* find_exact for n cells (4 x int32 each): out_ids = CellId or -1 */
+AMRX_API amrx_status amrx_find_exact(amrx_index *index, const int32_t *cells4,
+                            uint64_t n, int64_t *out_ids);
+
+/* snap for n points (3 x int64 each), one hint level per point (or a single
+ * hint if hints == NULL: *hint_all) */
+AMRX_API amrx_status amrx_snap(amrx_index *index, const int64_t *points3,
+                      const int32_t *hints, int32_t hint_all, uint64_t n,
+                      int64_t *out_ids);
+
+/* try_build_dual for n candidates given as task ids (cell*8 + delta):
+ * reject codes (0 accepted, 1 missing, 2 finer, 3 lower key) and, when
+ * accepted, the 8 corner CellIds */
+AMRX_API amrx_status amrx_try_build_duals(amrx_index *index, const uint64_t *tasks,
+                                 uint64_t n, uint8_t *out_reject,
+                                 uint32_t *out_corners8);
+
+/* Cell range [cell_begin, cell_end) of the candidate order; {0, UINT64_MAX}
+ * = all cells.  Used by the multi-GPU range partition. */
+typedef struct amrx_range {
+  uint64_t cell_begin;
+  uint64_t cell_end;
+} amrx_range;
+
+/* extract_dual_mesh: the accepted duals in candidate order.  corners8 gets
+ * 8 CellIds per dual; task_ids (optional) gets owner*8+delta, from which
+ * DualCell.{owner,base,level} follow (dual.hpp:61-67).  If the caller's cap
+ * is too small returns AMRX_ERR_CAPACITY with *count = the total. */
+AMRX_API amrx_status amrx_extract_dual(amrx_index *index, const amrx_range *range,
+                              uint32_t *corners8, uint64_t *task_ids,
+                              uint64_t cap, uint64_t *count,
+                              amrx_stats *stats);
+
+/* extract_isosurface passes 1+2: the fat triangle soup (9 coordinates per
+ * triangle, FP64 bit-exact with the reference; xyz_is_f32 = 1 rounds the
+ * FP64 results to float after the FP64 sliver test).  Also fills the dual
+ * counters.  AMRX_ERR_CAPACITY as above; AMRX_ERR_LENGTH when the total
+ * exceeds UINT32_MAX/3 (pipeline.cpp:116-118) and check_length is set. */
+typedef struct amrx_iso_params {
+  double iso;
+  int32_t xyz_is_f32;
+  int32_t check_length;
+} amrx_iso_params;
+
+AMRX_API amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range,
+                             const amrx_iso_params *params, void *xyz9,
+                             uint64_t cap, uint64_t *count,
+                             amrx_stats *stats);
+
+/* thread-local text of the last error on this thread */
+AMRX_API const char *amrx_last_error(void);
+
+/* library version string */
+AMRX_API const char *amrx_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AMRX_H */

@@ -1,0 +1,459 @@
+"""Python host mirror of the reference's operator API over the amrx C ABI.
+
+Names, argument meaning and error behaviour follow the reference's free
+functions in namespace ``amriso`` (paths under /root/reference/):
+
+  build_index(cells, scalars)          proj/include/amriso/locator.hpp:52-53
+  find_exact(index, coord)             proj/include/amriso/locator.hpp:55-57
+  snap(index, p, hint_level=-1)        proj/include/amriso/locator.hpp:59-66
+  try_build_dual(index, base...)       proj/include/amriso/dual.hpp:78-81
+  extract_dual_mesh(index, threads=0)  proj/include/amriso/pipeline.hpp:70-71
+  extract_isosurface(index, params)    proj/include/amriso/pipeline.hpp:65-66
+
+Errors map to the reference's exception types: ``LoadError`` (a
+RuntimeError, core.hpp:62-65), ``ValueError`` for std::invalid_argument,
+``OverflowError`` for std::length_error and ``InternalError`` (a
+RuntimeError standing for std::logic_error).
+
+Everything computes on the GPU through libamrx.so.  There is no CPU
+fallback: importing works anywhere, but any call raises if the library or a
+CUDA device is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libamrx.so")
+
+AMRX_OK = 0
+AMRX_ERR_LOAD = 1
+AMRX_ERR_INVALID_ARG = 2
+AMRX_ERR_LENGTH = 3
+AMRX_ERR_INTERNAL = 4
+AMRX_ERR_CUDA = 5
+AMRX_ERR_CAPACITY = 6
+AMRX_ERR_UNSUPPORTED = 7
+AMRX_ERR_NO_DEVICE = 8
+
+MAX_LEVEL = 30
+
+# DualReject (dual.hpp:38-43)
+ACCEPTED, MISSING_CORNER, FINER_CORNER, LOWER_KEY_CORNER = 0, 1, 2, 3
+
+
+class LoadError(RuntimeError):
+    """malformed input (core.hpp:62-65)"""
+
+
+class InternalError(RuntimeError):
+    """internal consistency failure (std::logic_error, core.hpp:67-74)"""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class CapacityError(RuntimeError):
+    def __init__(self, msg, count):
+        super().__init__(msg)
+        self.count = count
+
+
+class UnsupportedError(RuntimeError):
+    pass
+
+
+class _IndexInfo(C.Structure):
+    _fields_ = [("cell_count", C.c_uint64), ("max_level", C.c_int32),
+                ("level_count", C.c_int32), ("levels", C.c_int32 * 31),
+                ("bounds_lo", C.c_int64 * 3), ("bounds_hi", C.c_int64 * 3),
+                ("key_bits", C.c_int32), ("directory_bits", C.c_int32),
+                ("duplicate_keys", C.c_uint64), ("device_bytes", C.c_uint64),
+                ("seconds_ingest", C.c_double)]
+
+
+class _Opts(C.Structure):
+    _fields_ = [("device", C.c_int), ("stream", C.c_void_p), ("flags", C.c_uint32)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("cell_count", C.c_uint64), ("duals_accepted", C.c_uint64),
+                ("duals_missing_corner", C.c_uint64), ("duals_finer_corner", C.c_uint64),
+                ("duals_lower_key_corner", C.c_uint64),
+                ("pass1_triangle_count", C.c_uint64), ("fat_triangle_count", C.c_uint64),
+                ("dual_count", C.c_uint64), ("seconds_pass1", C.c_double),
+                ("seconds_pass2", C.c_double), ("kernel_launches", C.c_uint64)]
+
+
+class _Range(C.Structure):
+    _fields_ = [("cell_begin", C.c_uint64), ("cell_end", C.c_uint64)]
+
+
+class _IsoParams(C.Structure):
+    _fields_ = [("iso", C.c_double), ("xyz_is_f32", C.c_int32), ("check_length", C.c_int32)]
+
+
+_lib = None
+
+
+def library():
+    """Load libamrx.so (raises if it was never built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `make -C {_HERE}` "
+            "(or __graft_entry__.build()); there is no CPU fallback")
+    lib = C.CDLL(LIB_PATH)
+    P, U64, I64, I32 = C.c_void_p, C.c_uint64, C.c_int64, C.c_int32
+    sig = {
+        "amrx_index_create": [P, P, U64, U64, P, P],
+        "amrx_index_destroy": [P],
+        "amrx_index_get_info": [P, P],
+        "amrx_index_download": [P, P, P],
+        "amrx_index_device_arrays": [P, P, P],
+        "amrx_index_geometry": [P, P],
+        "amrx_index_adopt": [P, P, U64, P, P, P],
+        "amrx_find_exact": [P, P, U64, P],
+        "amrx_snap": [P, P, P, I32, U64, P],
+        "amrx_try_build_duals": [P, P, U64, P, P],
+        "amrx_extract_dual": [P, P, P, P, U64, P, P],
+        "amrx_extract_iso": [P, P, P, P, U64, P, P],
+    }
+    for name, args in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = C.c_int
+    lib.amrx_last_error.restype = C.c_char_p
+    lib.amrx_last_error.argtypes = []
+    lib.amrx_version.restype = C.c_char_p
+    _lib = lib
+    return lib
+
+
+def _check(status, count=None):
+    if status == AMRX_OK:
+        return
+    msg = library().amrx_last_error().decode()
+    if status == AMRX_ERR_LOAD:
+        raise LoadError(msg)
+    if status == AMRX_ERR_INVALID_ARG:
+        raise ValueError(msg)
+    if status == AMRX_ERR_LENGTH:
+        raise OverflowError(msg)
+    if status == AMRX_ERR_INTERNAL:
+        raise InternalError(msg)
+    if status == AMRX_ERR_CAPACITY:
+        raise CapacityError(msg, count)
+    if status == AMRX_ERR_UNSUPPORTED:
+        raise UnsupportedError(msg)
+    raise CudaError(msg)
+
+
+def _ptr(a):
+    """ctypes pointer of a numpy array or a torch tensor (host or CUDA)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return C.c_void_p(a.ctypes.data)
+    return C.c_void_p(a.data_ptr())
+
+
+@dataclass
+class IndexInfo:
+    cell_count: int
+    max_level: int
+    levels: list
+    bounds_lo: tuple
+    bounds_hi: tuple
+    key_bits: int
+    directory_bits: int
+    duplicate_keys: int
+    device_bytes: int
+    seconds_ingest: float
+
+
+class CellIndex:
+    """Device-resident search structure (CellIndex, locator.hpp:38-45).
+
+    ``cells``/``scalars`` (sorted, like CellIndex.data) are downloaded
+    lazily on first access."""
+
+    def __init__(self, handle, lib):
+        self._h = C.c_void_p(handle)
+        self._lib = lib
+        self._cells = None
+        self._scalars = None
+        info = _IndexInfo()
+        _check(lib.amrx_index_get_info(self._h, C.byref(info)))
+        self.info = IndexInfo(
+            info.cell_count, info.max_level, list(info.levels[: info.level_count]),
+            tuple(info.bounds_lo), tuple(info.bounds_hi), info.key_bits,
+            info.directory_bits, info.duplicate_keys, info.device_bytes,
+            info.seconds_ingest)
+
+    # -- CellIndex surface
+    def size(self):
+        return self.info.cell_count
+
+    def __len__(self):
+        return self.info.cell_count
+
+    @property
+    def levels(self):
+        return self.info.levels
+
+    @property
+    def max_level(self):
+        return self.info.max_level
+
+    @property
+    def bounds(self):
+        return self.info.bounds_lo, self.info.bounds_hi
+
+    def _download(self):
+        n = self.size()
+        cells = np.empty((n, 4), np.int32)
+        scal = np.empty(n, np.float64)
+        _check(self._lib.amrx_index_download(self._h, _ptr(cells), _ptr(scal)))
+        self._cells, self._scalars = cells, scal
+
+    @property
+    def cells(self):
+        if self._cells is None:
+            self._download()
+        return self._cells
+
+    @property
+    def scalars(self):
+        if self._scalars is None:
+            self._download()
+        return self._scalars
+
+    def device_arrays(self):
+        k, s = C.c_void_p(), C.c_void_p()
+        _check(self._lib.amrx_index_device_arrays(self._h, C.byref(k), C.byref(s)))
+        return k.value, s.value
+
+    def geometry(self):
+        g = np.zeros(16, np.int64)
+        _check(self._lib.amrx_index_geometry(self._h, _ptr(g)))
+        return g
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            self._lib.amrx_index_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def build_index(cells, scalars, device=-1, presorted=False):
+    """Sort cells (with their scalars) into a device CellIndex
+    (build_index, locator.cpp:26-92).  ``cells`` is (n,4) int32 (i,j,k,level),
+    numpy or torch (host or CUDA)."""
+    lib = library()
+    if isinstance(cells, np.ndarray) or not hasattr(cells, "data_ptr"):
+        cells = np.ascontiguousarray(np.asarray(cells, dtype=np.int32).reshape(-1, 4))
+        n_cells = len(cells)
+    else:
+        n_cells = cells.shape[0] if cells.numel() else 0
+    if isinstance(scalars, np.ndarray) or not hasattr(scalars, "data_ptr"):
+        scalars = np.ascontiguousarray(np.asarray(scalars, dtype=np.float64).reshape(-1))
+        n_s = len(scalars)
+    else:
+        n_s = scalars.numel()
+    opts = _Opts(device, None, 1 if presorted else 0)
+    h = C.c_void_p()
+    _check(lib.amrx_index_create(_ptr(cells) if n_cells else C.c_void_p(1),
+                                 _ptr(scalars) if n_s else C.c_void_p(1),
+                                 n_cells, n_s, C.byref(opts), C.byref(h)))
+    return CellIndex(h.value, lib)
+
+
+def adopt_index(keys_dev_ptr, scalars_dev_ptr, n_cells, geometry, device=-1):
+    """Index over already-sorted packed keys + scalars on this device (the
+    multi-GPU replica path: no sort, directory only)."""
+    lib = library()
+    g = np.ascontiguousarray(geometry, np.int64)
+    opts = _Opts(device, None, 0)
+    h = C.c_void_p()
+    _check(lib.amrx_index_adopt(C.c_void_p(keys_dev_ptr), C.c_void_p(scalars_dev_ptr),
+                                n_cells, _ptr(g), C.byref(opts), C.byref(h)))
+    return CellIndex(h.value, lib)
+
+
+def find_exact(index: CellIndex, coords):
+    """CellId per (i,j,k,level) row, -1 = absent (locator.cpp:94-101)."""
+    c = np.ascontiguousarray(np.asarray(coords, np.int32).reshape(-1, 4))
+    out = np.empty(len(c), np.int64)
+    _check(index._lib.amrx_find_exact(index.handle, _ptr(c), len(c), _ptr(out)))
+    return out
+
+
+def snap(index: CellIndex, points, hint_level=-1):
+    """CellId containing each int64 point, -1 = none (locator.cpp:122-134).
+    ``hint_level`` is one int or one per point."""
+    p = np.ascontiguousarray(np.asarray(points, np.int64).reshape(-1, 3))
+    out = np.empty(len(p), np.int64)
+    if np.ndim(hint_level) == 0:
+        _check(index._lib.amrx_snap(index.handle, _ptr(p), None, int(hint_level),
+                                    len(p), _ptr(out)))
+    else:
+        h = np.ascontiguousarray(np.asarray(hint_level, np.int32).reshape(-1))
+        _check(index._lib.amrx_snap(index.handle, _ptr(p), _ptr(h), -1, len(p), _ptr(out)))
+    return out
+
+
+def try_build_duals(index: CellIndex, tasks):
+    """try_build_dual for candidate tasks (cell*8+delta): (reject codes,
+    corners[n,8]) (dual.cpp:41-72)."""
+    t = np.ascontiguousarray(np.asarray(tasks, np.uint64).reshape(-1))
+    rej = np.empty(len(t), np.uint8)
+    cor = np.empty((len(t), 8), np.uint32)
+    _check(index._lib.amrx_try_build_duals(index.handle, _ptr(t), len(t), _ptr(rej), _ptr(cor)))
+    return rej, cor
+
+
+@dataclass
+class ExtractionStats:
+    """ExtractionStats (pipeline.hpp:29-49); times are device seconds."""
+    cell_count: int = 0
+    duals_accepted: int = 0
+    duals_missing_corner: int = 0
+    duals_finer_corner: int = 0
+    duals_lower_key_corner: int = 0
+    pass1_triangle_count: int = 0
+    fat_triangle_count: int = 0
+    dual_count: int = 0
+    seconds_pass1: float = 0.0
+    seconds_pass2: float = 0.0
+    kernel_launches: int = 0
+
+    @staticmethod
+    def _from(s: _Stats):
+        return ExtractionStats(*[getattr(s, f) for f, _ in _Stats._fields_])
+
+
+@dataclass
+class IsoParams:
+    """IsoParams (pipeline.hpp:23-27); thread_count is accepted and ignored."""
+    iso: float = 0.0
+    emit_dual_mesh: bool = False
+    thread_count: int = 0
+    f32: bool = False
+
+
+@dataclass
+class DualMesh:
+    """extract_dual_mesh's result as arrays: corners[n,8] CellIds and the
+    candidate task id owner*8+delta (owner/base/level follow)."""
+    corners: np.ndarray
+    tasks: np.ndarray
+    stats: ExtractionStats = None
+
+    @property
+    def owner(self):
+        return (self.tasks >> np.uint64(3)).astype(np.uint32)
+
+    @property
+    def delta(self):
+        return (self.tasks & np.uint64(7)).astype(np.int32)
+
+    def __len__(self):
+        return len(self.corners)
+
+
+@dataclass
+class ExtractionResult:
+    fat: np.ndarray                      # [n,9] triangle soup (emission order)
+    stats: ExtractionStats
+    duals: DualMesh = None
+    extra: dict = field(default_factory=dict)
+
+
+def _range(r):
+    if r is None:
+        return None
+    return C.byref(_Range(int(r[0]), int(r[1])))
+
+
+def extract_dual_mesh(index: CellIndex, thread_count=0, cell_range=None, out=None):
+    """The accepted duals in candidate order (pipeline.cpp:160-194).
+    ``out`` = (corners, tasks) preallocated device tensors to write into."""
+    lib = index._lib
+    st = _Stats()
+    cnt = C.c_uint64(0)
+    if out is not None:
+        corners, tasks = out
+        cap = corners.shape[0]
+        rc = lib.amrx_extract_dual(index.handle, _range(cell_range), _ptr(corners), _ptr(tasks),
+                                   cap, C.byref(cnt), C.byref(st))
+        _check(rc, cnt.value)
+        return DualMesh(corners[: cnt.value], tasks[: cnt.value], ExtractionStats._from(st))
+    _check(lib.amrx_extract_dual(index.handle, _range(cell_range), None, None, 0,
+                                 C.byref(cnt), C.byref(st)))
+    n = cnt.value
+    corners = np.empty((n, 8), np.uint32)
+    tasks = np.empty(n, np.uint64)
+    if n:
+        _check(lib.amrx_extract_dual(index.handle, _range(cell_range), _ptr(corners), _ptr(tasks),
+                                     n, C.byref(cnt), C.byref(st)))
+    return DualMesh(corners, tasks, ExtractionStats._from(st))
+
+
+def extract_isosurface(index: CellIndex, params: IsoParams = None, cell_range=None,
+                       out=None, check_length=True):
+    """Passes 1+2 of extract_isosurface (pipeline.cpp:67-146): the fat
+    triangle soup in emission order plus ExtractionStats.  The weld
+    (weld.cpp:31-64) is not part of this path; see DESIGN.md."""
+    if params is None:
+        params = IsoParams()
+    elif isinstance(params, (int, float)):
+        params = IsoParams(iso=float(params))
+    lib = index._lib
+    p = _IsoParams(float(params.iso), 1 if params.f32 else 0, 1 if check_length else 0)
+    st = _Stats()
+    cnt = C.c_uint64(0)
+    dtype = np.float32 if params.f32 else np.float64
+    if out is not None:
+        rc = lib.amrx_extract_iso(index.handle, _range(cell_range), C.byref(p), _ptr(out),
+                                  out.shape[0], C.byref(cnt), C.byref(st))
+        _check(rc, cnt.value)
+        fat = out[: cnt.value]
+    else:
+        _check(lib.amrx_extract_iso(index.handle, _range(cell_range), C.byref(p), None, 0,
+                                    C.byref(cnt), C.byref(st)))
+        fat = np.empty((cnt.value, 9), dtype)
+        if cnt.value:
+            _check(lib.amrx_extract_iso(index.handle, _range(cell_range), C.byref(p),
+                                        _ptr(fat), cnt.value, C.byref(cnt), C.byref(st)))
+    res = ExtractionResult(fat, ExtractionStats._from(st))
+    if params.emit_dual_mesh:
+        res.duals = extract_dual_mesh(index, cell_range=cell_range)
+    return res
+
+
+def dual_bases(index: CellIndex, tasks):
+    """DualCell.base / .level for task ids (dual_base_of, dual.hpp:61-67)."""
+    t = np.asarray(tasks, np.uint64)
+    owner = (t >> np.uint64(3)).astype(np.int64)
+    delta = (t & np.uint64(7)).astype(np.int64)
+    c = index.cells[owner].astype(np.int64)
+    w = np.left_shift(np.int64(1), c[:, 3])
+    base = np.stack([c[:, a] - np.where((delta >> a) & 1, 0, w) for a in range(3)], axis=1)
+    return base, c[:, 3].astype(np.int32)

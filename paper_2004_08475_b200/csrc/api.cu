@@ -1,0 +1,772 @@
+// C ABI (include/amrx.h): the device index handle, host/device pointer
+// handling, error mapping and the orchestration of the ingest/extract
+// kernels.  Every entry point catches everything and returns a status; the
+// message is kept per thread for amrx_last_error().
+#include "amrx.h"
+#include "internal.h"
+
+#include <algorithm>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace amrx {
+
+namespace {
+thread_local std::string g_last_error;
+
+struct ApiError : std::runtime_error {
+  int code;
+  ApiError(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void fail(int code, const std::string &msg)
+{
+  throw ApiError(code, msg);
+}
+
+template <typename Fn>
+amrx_status guarded(Fn &&fn)
+{
+  try {
+    fn();
+    g_last_error.clear();
+    return AMRX_OK;
+  } catch (const ApiError &e) {
+    g_last_error = e.what();
+    return amrx_status(e.code);
+  } catch (const std::bad_alloc &) {
+    g_last_error = "host allocation failed";
+    return AMRX_ERR_CUDA;
+  } catch (const std::exception &e) {
+    g_last_error = e.what();
+    return AMRX_ERR_INTERNAL;
+  }
+}
+
+bool is_device_ptr(const void *p)
+{
+  if (!p) return false;
+  cudaPointerAttributes attr;
+  const cudaError_t e = cudaPointerGetAttributes(&attr, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();  // clear sticky-free error state
+    return false;
+  }
+  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+int bit_width(uint64_t v)
+{
+  int b = 0;
+  while (v) {
+    b++;
+    v >>= 1;
+  }
+  return b;
+}
+
+/// a device view of a caller pointer: the pointer itself or a staged copy
+template <typename T>
+struct DevIn {
+  const T *ptr = nullptr;
+  DevBuf stage;
+  DevIn(const T *p, size_t count, cudaStream_t st)
+  {
+    if (!p || count == 0) return;
+    if (is_device_ptr(p)) {
+      ptr = p;
+      return;
+    }
+    stage.reserve(count * sizeof(T));
+    AMRX_CUDA(cudaMemcpyAsync(stage.ptr, p, count * sizeof(T),
+                              cudaMemcpyHostToDevice, st));
+    ptr = stage.as<T>();
+  }
+};
+
+template <typename T>
+struct DevOut {
+  T *user = nullptr;
+  T *ptr = nullptr;
+  size_t count = 0;
+  bool staged = false;
+  DevBuf stage;
+  DevOut(T *p, size_t n) : user(p), count(n)
+  {
+    if (!p || n == 0) return;
+    if (is_device_ptr(p)) {
+      ptr = p;
+      return;
+    }
+    staged = true;
+    stage.reserve(n * sizeof(T));
+    ptr = stage.as<T>();
+  }
+  void finish(cudaStream_t st)
+  {
+    if (staged)
+      AMRX_CUDA(cudaMemcpyAsync(user, ptr, count * sizeof(T),
+                                cudaMemcpyDeviceToHost, st));
+  }
+};
+
+}  // namespace
+
+[[noreturn]] void throw_cuda(cudaError_t e, const char *what, const char *file,
+                             int line)
+{
+  const char *base = std::strrchr(file, '/');
+  std::string msg = std::string("CUDA error ") + cudaGetErrorName(e) + " (" +
+                    cudaGetErrorString(e) + ") in " + what + " at " +
+                    (base ? base + 1 : file) + ":" + std::to_string(line);
+  const int code = (e == cudaErrorNoDevice || e == cudaErrorNoKernelImageForDevice ||
+                    e == cudaErrorInsufficientDriver)
+                     ? AMRX_ERR_NO_DEVICE
+                     : AMRX_ERR_CUDA;
+  throw ApiError(code, msg);
+}
+
+DevBuf::~DevBuf() { release(); }
+
+void DevBuf::reserve(size_t n)
+{
+  if (n <= bytes && ptr) return;
+  release();
+  if (n == 0) n = 16;
+  AMRX_CUDA(cudaMalloc(&ptr, n));
+  bytes = n;
+}
+
+void DevBuf::release()
+{
+  if (ptr) cudaFree(ptr);
+  ptr = nullptr;
+  bytes = 0;
+}
+
+int device_sm_count()
+{
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static int cached[64] = {0};
+  if (dev < 64 && cached[dev]) return cached[dev];
+  int sms = 0;
+  AMRX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (dev < 64) cached[dev] = sms;
+  return sms;
+}
+
+}  // namespace amrx
+
+using namespace amrx;
+
+struct amrx_index {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  uint64_t n = 0;
+  KeyGeom g{};
+  int64_t bounds_hi[3] = {0, 0, 0};
+  DevBuf keys, scal, dir, scratch, scratch2;
+  amrx_index_info info{};
+  // last extraction kept on the device for the count-then-copy pattern
+  struct Cached {
+    bool valid = false;
+    int kind = 0;  // 1 dual, 2 iso
+    uint64_t begin = 0, end = 0;
+    double iso = 0;
+    int f32 = 0;
+    uint64_t count = 0;
+    amrx_stats stats{};
+  } cache;
+  DevBuf out_a, out_b;  // arena: corners/xyz, tasks
+  std::mutex mu;
+
+  SearchCtx ctx() const
+  {
+    SearchCtx s;
+    s.keys = keys.as<uint64_t>();
+    s.dir = dir.as<uint32_t>();
+    s.n = n;
+    s.dir_shift = g.dir_shift;
+    return s;
+  }
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev)
+  {
+    cudaGetDevice(&prev);
+    if (dev != prev) AMRX_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard()
+  {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+KeyGeom make_geometry(const int64_t mn[3], const int64_t mx[3],
+                      uint32_t level_mask, uint64_t n)
+{
+  KeyGeom g{};
+  int lo_level = 0, hi_level = 0;
+  for (int l = 0; l <= kMaxLevel; l++)
+    if ((level_mask >> l) & 1u) {
+      lo_level = l;
+      break;
+    }
+  for (int l = kMaxLevel; l >= 0; l--)
+    if ((level_mask >> l) & 1u) {
+      hi_level = l;
+      break;
+    }
+  g.shift = lo_level;
+  for (int a = 0; a < 3; a++) {
+    g.mn[a] = mn[a];
+    g.mx[a] = mx[a];
+    g.bits[a] = bit_width(uint64_t(mx[a] - mn[a]) >> g.shift);
+  }
+  g.lbits = bit_width(uint64_t(hi_level - lo_level));
+  g.total = g.bits[0] + g.bits[1] + g.bits[2] + g.lbits;
+  if (g.total > 64)
+    fail(AMRX_ERR_UNSUPPORTED,
+         "dataset extent needs a " + std::to_string(g.total) +
+           "-bit cell key; this build packs keys into 64 bits");
+  g.sh[2] = g.lbits;
+  g.sh[1] = g.sh[2] + g.bits[2];
+  g.sh[0] = g.sh[1] + g.bits[1];
+  g.level_mask = level_mask;
+  g.nlevels = 0;
+  for (int l = 0; l <= kMaxLevel; l++)
+    if ((level_mask >> l) & 1u) g.levels[g.nlevels++] = int8_t(l);
+  // directory: about two buckets per cell, 2^10 .. 2^30 entries
+  const int want = std::min(30, std::max(10, bit_width(n) + 1));
+  g.dir_bits = std::min(g.total, want);
+  g.dir_shift = g.total - g.dir_bits;
+  return g;
+}
+
+void finish_info(amrx_index *ix, uint64_t equal_pairs, double ms)
+{
+  amrx_index_info &in = ix->info;
+  in.cell_count = ix->n;
+  in.level_count = ix->g.nlevels;
+  in.max_level = ix->g.nlevels ? ix->g.levels[ix->g.nlevels - 1] : 0;
+  for (int l = 0; l < ix->g.nlevels; l++) in.levels[l] = ix->g.levels[l];
+  for (int a = 0; a < 3; a++) {
+    in.bounds_lo[a] = ix->g.mn[a];
+    in.bounds_hi[a] = ix->bounds_hi[a];
+  }
+  in.key_bits = ix->g.total;
+  in.directory_bits = ix->g.dir_bits;
+  in.duplicate_keys = equal_pairs;
+  in.device_bytes = ix->keys.bytes + ix->scal.bytes + ix->dir.bytes;
+  in.seconds_ingest = ms / 1000.0;
+}
+
+void setup_stream(amrx_index *ix, const amrx_index_opts *opts)
+{
+  int dev = opts && opts->device >= 0 ? opts->device : -1;
+  if (dev < 0) AMRX_CUDA(cudaGetDevice(&dev));
+  int count = 0;
+  const cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    fail(AMRX_ERR_NO_DEVICE, "no CUDA device available");
+  }
+  ix->device = dev;
+  AMRX_CUDA(cudaSetDevice(dev));
+  if (opts && opts->stream) {
+    ix->stream = static_cast<cudaStream_t>(opts->stream);
+  } else {
+    AMRX_CUDA(cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking));
+    ix->own_stream = true;
+  }
+}
+
+/// bring the device-side directory + padding up for sorted keys
+void finalize_index(amrx_index *ix)
+{
+  pad_keys(ix->keys.as<uint64_t>(), ix->n, ix->stream);
+  ix->dir.reserve(((uint64_t(1) << ix->g.dir_bits) + 1) * sizeof(uint32_t));
+  build_directory(ix->keys.as<uint64_t>(), ix->n, ix->g, ix->dir.as<uint32_t>(),
+                  ix->scratch, ix->stream);
+}
+
+void check_range(const amrx_index *ix, const amrx_range *range, uint64_t &b,
+                 uint64_t &e)
+{
+  b = range ? range->cell_begin : 0;
+  e = range ? std::min<uint64_t>(range->cell_end, ix->n) : ix->n;
+  if (b > e) fail(AMRX_ERR_INVALID_ARG, "cell range begins after it ends");
+}
+
+void fill_stats(amrx_stats *st, const ExtractResult &r, uint64_t cells)
+{
+  if (!st) return;
+  std::memset(st, 0, sizeof *st);
+  st->cell_count = cells;
+  st->duals_accepted = r.counters[0];
+  st->duals_missing_corner = r.counters[1];
+  st->duals_finer_corner = r.counters[2];
+  st->duals_lower_key_corner = r.counters[3];
+  st->pass1_triangle_count = r.tris_counted;
+  st->fat_triangle_count = r.tris_written;
+  st->dual_count = r.duals;
+  st->seconds_pass1 = r.ms / 1000.0;
+  st->seconds_pass2 = 0;
+  st->kernel_launches = r.launches;
+}
+
+/// internal-consistency checks of pipeline.cpp:106-107,130-138
+void check_result(const ExtractResult &r, uint64_t cells, bool tri)
+{
+  if (r.error_flags & 1u)
+    fail(AMRX_ERR_INTERNAL, "contour_hex: case table selected a collapsed edge");
+  if (r.error_flags & 2u)
+    fail(AMRX_ERR_INTERNAL, "extract: candidate left undecided");
+  const uint64_t total = r.counters[0] + r.counters[1] + r.counters[2] + r.counters[3];
+  if (total != cells * 8)
+    fail(AMRX_ERR_INTERNAL, "extract_isosurface: candidate accounting broken");
+  if (tri && r.tris_counted != r.tris_written)
+    fail(AMRX_ERR_INTERNAL,
+         "extract_isosurface: pass 2 emitted a different number of "
+         "triangles than pass 1 counted");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *amrx_last_error(void) { return g_last_error.c_str(); }
+
+const char *amrx_version(void) { return "amrx 0.1 (sm_100a)"; }
+
+amrx_status amrx_index_create(const int32_t *cells4, const double *scalars,
+                              uint64_t n_cells, uint64_t n_scalars,
+                              const amrx_index_opts *opts, amrx_index **out)
+{
+  return guarded([&] {
+    if (!out) fail(AMRX_ERR_INVALID_ARG, "out is null");
+    *out = nullptr;
+    // locator.cpp:29-36, same order and wording
+    if (n_cells == 0) fail(AMRX_ERR_LOAD, "dataset is empty");
+    if (n_cells != n_scalars)
+      fail(AMRX_ERR_LOAD, "cell count " + std::to_string(n_cells) +
+                            " does not match scalar count " +
+                            std::to_string(n_scalars));
+    if (n_cells > uint64_t(std::numeric_limits<uint32_t>::max()))
+      fail(AMRX_ERR_LOAD, "dataset too large for 32-bit cell ids");
+    if (!cells4 || !scalars) fail(AMRX_ERR_INVALID_ARG, "null input array");
+
+    auto ix = std::make_unique<amrx_index>();
+    setup_stream(ix.get(), opts);
+    cudaStream_t st = ix->stream;
+    const uint64_t n = n_cells;
+    ix->n = n;
+
+    cudaEvent_t e0, e1;
+    AMRX_CUDA(cudaEventCreate(&e0));
+    AMRX_CUDA(cudaEventCreate(&e1));
+    AMRX_CUDA(cudaEventRecord(e0, st));
+
+    DevIn<int4> cells(reinterpret_cast<const int4 *>(cells4), n, st);
+    DevIn<double> sc(scalars, n, st);
+
+    const PrepassResult pre = ingest_prepass(cells.ptr, n, ix->scratch, st);
+    if (pre.first_bad != ~0ull) {
+      int4 c;
+      AMRX_CUDA(cudaMemcpy(&c, cells.ptr + pre.first_bad, sizeof c,
+                           cudaMemcpyDeviceToHost));
+      const std::string rec = "record " + std::to_string(pre.first_bad);
+      if (c.w < 0 || c.w > kMaxLevel)
+        fail(AMRX_ERR_LOAD, rec + ": level " + std::to_string(c.w) +
+                              " out of range [0," + std::to_string(kMaxLevel) + "]");
+      fail(AMRX_ERR_LOAD, rec + ": anchor (" + std::to_string(c.x) + " " +
+                            std::to_string(c.y) + " " + std::to_string(c.z) +
+                            ") is not a multiple of the level-" +
+                            std::to_string(c.w) + " cell width");
+    }
+    const int64_t mn[3] = {pre.mn[0], pre.mn[1], pre.mn[2]};
+    const int64_t mx[3] = {pre.mx[0], pre.mx[1], pre.mx[2]};
+    ix->g = make_geometry(mn, mx, pre.level_mask, n);
+    for (int a = 0; a < 3; a++) ix->bounds_hi[a] = pre.hi[a];
+
+    ix->keys.reserve((n + kKeyPad) * sizeof(uint64_t));
+    DevBuf idx, keys_alt, idx_alt;
+    idx.reserve(n * sizeof(uint32_t));
+    ingest_pack(cells.ptr, n, ix->g, ix->keys.as<uint64_t>(), idx.as<uint32_t>(), st);
+    cells.stage.release();
+
+    uint64_t desc = 0, eq = 0;
+    ingest_order_check(ix->keys.as<uint64_t>(), n, ix->scratch, &desc, &eq, st);
+    ix->scal.reserve(n * sizeof(double));
+    if (desc == 0) {
+      // already in (i,j,k,level) order; stable ties mean identity
+      AMRX_CUDA(cudaMemcpyAsync(ix->scal.ptr, sc.ptr, n * sizeof(double),
+                                cudaMemcpyDeviceToDevice, st));
+    } else {
+      if (opts && (opts->flags & AMRX_FLAG_PRESORTED))
+        fail(AMRX_ERR_INVALID_ARG, "input flagged presorted is not sorted");
+      keys_alt.reserve(n * sizeof(uint64_t));
+      idx_alt.reserve(n * sizeof(uint32_t));
+      int passes = 0;
+      radix_sort_pairs(ix->keys.as<uint64_t>(), idx.as<uint32_t>(),
+                       keys_alt.as<uint64_t>(), idx_alt.as<uint32_t>(), n,
+                       ix->g.total, ix->scratch, st, &passes);
+      keys_alt.release();
+      idx_alt.release();
+      gather_f64(idx.as<uint32_t>(), sc.ptr, ix->scal.as<double>(), n, st);
+      uint64_t d2 = 0;
+      ingest_order_check(ix->keys.as<uint64_t>(), n, ix->scratch, &d2, &eq, st);
+      if (d2 != 0) fail(AMRX_ERR_INTERNAL, "radix sort left keys out of order");
+    }
+    finalize_index(ix.get());
+    AMRX_CUDA(cudaEventRecord(e1, st));
+    AMRX_CUDA(cudaStreamSynchronize(st));
+    float ms = 0;
+    AMRX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    finish_info(ix.get(), eq, ms);
+    *out = ix.release();
+  });
+}
+
+amrx_status amrx_index_destroy(amrx_index *index)
+{
+  return guarded([&] {
+    if (!index) return;
+    {
+      DeviceGuard dg(index->device);
+      if (index->stream) cudaStreamSynchronize(index->stream);
+      index->keys.release();
+      index->scal.release();
+      index->dir.release();
+      index->scratch.release();
+      index->scratch2.release();
+      index->out_a.release();
+      index->out_b.release();
+      if (index->own_stream) cudaStreamDestroy(index->stream);
+    }
+    delete index;
+  });
+}
+
+amrx_status amrx_index_get_info(const amrx_index *index, amrx_index_info *out)
+{
+  return guarded([&] {
+    if (!index || !out) fail(AMRX_ERR_INVALID_ARG, "null argument");
+    *out = index->info;
+  });
+}
+
+amrx_status amrx_index_download(const amrx_index *cindex, int32_t *cells4,
+                                double *scalars)
+{
+  return guarded([&] {
+    auto *index = const_cast<amrx_index *>(cindex);
+    if (!index) fail(AMRX_ERR_INVALID_ARG, "null index");
+    DeviceGuard dg(index->device);
+    cudaStream_t st = index->stream;
+    if (cells4) {
+      DevOut<int4> o(reinterpret_cast<int4 *>(cells4), index->n);
+      unpack_cells(index->keys.as<uint64_t>(), index->n, index->g, o.ptr, st);
+      o.finish(st);
+      AMRX_CUDA(cudaStreamSynchronize(st));
+    }
+    if (scalars)
+      AMRX_CUDA(cudaMemcpyAsync(scalars, index->scal.ptr, index->n * sizeof(double),
+                                cudaMemcpyDefault, st));
+    AMRX_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+amrx_status amrx_index_device_arrays(const amrx_index *index, void **keys,
+                                     void **scalars)
+{
+  return guarded([&] {
+    if (!index) fail(AMRX_ERR_INVALID_ARG, "null index");
+    if (keys) *keys = index->keys.ptr;
+    if (scalars) *scalars = index->scal.ptr;
+  });
+}
+
+amrx_status amrx_index_geometry(const amrx_index *index, int64_t *g16)
+{
+  return guarded([&] {
+    if (!index || !g16) fail(AMRX_ERR_INVALID_ARG, "null argument");
+    const KeyGeom &g = index->g;
+    for (int a = 0; a < 3; a++) {
+      g16[a] = g.mn[a];
+      g16[3 + a] = g.mx[a];
+      g16[6 + a] = index->bounds_hi[a];
+    }
+    g16[9] = g.level_mask;
+    g16[10] = int64_t(index->n);
+    g16[11] = int64_t(index->info.duplicate_keys);
+    for (int i = 12; i < 16; i++) g16[i] = 0;
+  });
+}
+
+amrx_status amrx_index_adopt(const void *keys_dev, const double *scalars_dev,
+                             uint64_t n_cells, const int64_t *g16,
+                             const amrx_index_opts *opts, amrx_index **out)
+{
+  return guarded([&] {
+    if (!out || !keys_dev || !scalars_dev || !g16)
+      fail(AMRX_ERR_INVALID_ARG, "null argument");
+    if (n_cells == 0) fail(AMRX_ERR_LOAD, "dataset is empty");
+    if (uint64_t(g16[10]) != n_cells)
+      fail(AMRX_ERR_INVALID_ARG, "geometry describes a different cell count");
+    auto ix = std::make_unique<amrx_index>();
+    setup_stream(ix.get(), opts);
+    cudaStream_t st = ix->stream;
+    ix->n = n_cells;
+    const int64_t mn[3] = {g16[0], g16[1], g16[2]};
+    const int64_t mx[3] = {g16[3], g16[4], g16[5]};
+    ix->g = make_geometry(mn, mx, uint32_t(g16[9]), n_cells);
+    for (int a = 0; a < 3; a++) ix->bounds_hi[a] = g16[6 + a];
+    cudaEvent_t e0, e1;
+    AMRX_CUDA(cudaEventCreate(&e0));
+    AMRX_CUDA(cudaEventCreate(&e1));
+    AMRX_CUDA(cudaEventRecord(e0, st));
+    ix->keys.reserve((n_cells + kKeyPad) * sizeof(uint64_t));
+    ix->scal.reserve(n_cells * sizeof(double));
+    AMRX_CUDA(cudaMemcpyAsync(ix->keys.ptr, keys_dev, n_cells * 8,
+                              cudaMemcpyDefault, st));
+    AMRX_CUDA(cudaMemcpyAsync(ix->scal.ptr, scalars_dev, n_cells * 8,
+                              cudaMemcpyDefault, st));
+    finalize_index(ix.get());
+    AMRX_CUDA(cudaEventRecord(e1, st));
+    AMRX_CUDA(cudaStreamSynchronize(st));
+    float ms = 0;
+    AMRX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    finish_info(ix.get(), uint64_t(g16[11]), ms);
+    *out = ix.release();
+  });
+}
+
+amrx_status amrx_find_exact(amrx_index *index, const int32_t *cells4,
+                            uint64_t n, int64_t *out_ids)
+{
+  return guarded([&] {
+    if (!index) fail(AMRX_ERR_INVALID_ARG, "null index");
+    if (n == 0) return;
+    DeviceGuard dg(index->device);
+    cudaStream_t st = index->stream;
+    DevIn<int4> in(reinterpret_cast<const int4 *>(cells4), n, st);
+    DevOut<int64_t> o(out_ids, n);
+    run_find_exact(index->ctx(), index->g, in.ptr, n, o.ptr, st);
+    o.finish(st);
+    AMRX_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+amrx_status amrx_snap(amrx_index *index, const int64_t *points3,
+                      const int32_t *hints, int32_t hint_all, uint64_t n,
+                      int64_t *out_ids)
+{
+  return guarded([&] {
+    if (!index) fail(AMRX_ERR_INVALID_ARG, "null index");
+    if (n == 0) return;
+    DeviceGuard dg(index->device);
+    cudaStream_t st = index->stream;
+    DevIn<int64_t> p(points3, 3 * n, st);
+    DevIn<int32_t> h(hints, hints ? n : 0, st);
+    DevOut<int64_t> o(out_ids, n);
+    run_snap(index->ctx(), index->g, p.ptr, h.ptr, hint_all, n, o.ptr, st);
+    o.finish(st);
+    AMRX_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+amrx_status amrx_try_build_duals(amrx_index *index, const uint64_t *tasks,
+                                 uint64_t n, uint8_t *out_reject,
+                                 uint32_t *out_corners8)
+{
+  return guarded([&] {
+    if (!index) fail(AMRX_ERR_INVALID_ARG, "null index");
+    if (n == 0) return;
+    DeviceGuard dg(index->device);
+    cudaStream_t st = index->stream;
+    DevIn<uint64_t> t(tasks, n, st);
+    DevOut<uint8_t> r(out_reject, n);
+    DevOut<uint32_t> c(out_corners8, out_corners8 ? 8 * n : 0);
+    run_try_build(index->ctx(), index->g, t.ptr, n, r.ptr, c.ptr, st);
+    r.finish(st);
+    c.finish(st);
+    AMRX_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+amrx_status amrx_extract_dual(amrx_index *index, const amrx_range *range,
+                              uint32_t *corners8, uint64_t *task_ids,
+                              uint64_t cap, uint64_t *count, amrx_stats *stats)
+{
+  return guarded([&] {
+    if (!index || !count) fail(AMRX_ERR_INVALID_ARG, "null argument");
+    std::lock_guard<std::mutex> lock(index->mu);
+    DeviceGuard dg(index->device);
+    cudaStream_t st = index->stream;
+    uint64_t b, e;
+    check_range(index, range, b, e);
+    const uint64_t cells = e - b;
+    auto &C = index->cache;
+    const bool dev_out = corners8 && is_device_ptr(corners8);
+    if (dev_out && task_ids && !is_device_ptr(task_ids))
+      fail(AMRX_ERR_INVALID_ARG, "corners8 and task_ids must both be device or host");
+
+    ExtractRequest rq{};
+    rq.s = index->ctx();
+    rq.g = index->g;
+    rq.scal = index->scal.as<double>();
+    rq.cell_begin = b;
+    rq.cell_end = e;
+    rq.emit_dual = true;
+    if (dev_out) {
+      rq.corners = corners8;
+      rq.tasks = task_ids;
+      rq.dual_cap = cap;
+      const ExtractResult r = run_extract(rq, index->scratch, st);
+      check_result(r, cells, false);
+      fill_stats(stats, r, cells);
+      *count = r.duals;
+      C.valid = false;
+      if (r.duals > cap)
+        fail(AMRX_ERR_CAPACITY, "output capacity " + std::to_string(cap) +
+                                  " < " + std::to_string(r.duals) + " duals");
+      return;
+    }
+    // host (or absent) output: run into the device arena, keep it cached
+    const bool hit = C.valid && C.kind == 1 && C.begin == b && C.end == e;
+    if (!hit) {
+      uint64_t arena = std::max<uint64_t>(1024, cells + cells / 4);
+      for (int attempt = 0; attempt < 2; attempt++) {
+        index->out_a.reserve(arena * 32);
+        index->out_b.reserve(arena * 8);
+        rq.corners = index->out_a.as<uint32_t>();
+        rq.tasks = index->out_b.as<uint64_t>();
+        rq.dual_cap = arena;
+        const ExtractResult r = run_extract(rq, index->scratch, st);
+        check_result(r, cells, false);
+        if (r.duals <= arena) {
+          C.valid = true;
+          C.kind = 1;
+          C.begin = b;
+          C.end = e;
+          C.count = r.duals;
+          fill_stats(&C.stats, r, cells);
+          break;
+        }
+        arena = r.duals;
+      }
+    }
+    *count = C.count;
+    if (stats) *stats = C.stats;
+    if (!corners8 && !task_ids) return;  // count query
+    if (C.count > cap)
+      fail(AMRX_ERR_CAPACITY, "output capacity " + std::to_string(cap) + " < " +
+                                std::to_string(C.count) + " duals");
+    if (corners8)
+      AMRX_CUDA(cudaMemcpyAsync(corners8, index->out_a.ptr, C.count * 32,
+                                cudaMemcpyDefault, st));
+    if (task_ids)
+      AMRX_CUDA(cudaMemcpyAsync(task_ids, index->out_b.ptr, C.count * 8,
+                                cudaMemcpyDefault, st));
+    AMRX_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range,
+                             const amrx_iso_params *params, void *xyz9,
+                             uint64_t cap, uint64_t *count, amrx_stats *stats)
+{
+  return guarded([&] {
+    if (!index || !count || !params) fail(AMRX_ERR_INVALID_ARG, "null argument");
+    std::lock_guard<std::mutex> lock(index->mu);
+    DeviceGuard dg(index->device);
+    cudaStream_t st = index->stream;
+    uint64_t b, e;
+    check_range(index, range, b, e);
+    const uint64_t cells = e - b;
+    const size_t tri_bytes = params->xyz_is_f32 ? 36 : 72;
+    auto &C = index->cache;
+    const bool dev_out = xyz9 && is_device_ptr(xyz9);
+
+    ExtractRequest rq{};
+    rq.s = index->ctx();
+    rq.g = index->g;
+    rq.scal = index->scal.as<double>();
+    rq.cell_begin = b;
+    rq.cell_end = e;
+    rq.emit_tri = true;
+    rq.tri_f32 = params->xyz_is_f32 != 0;
+    rq.iso = params->iso;
+    const auto length_check = [&](uint64_t tris) {
+      if (params->check_length &&
+          tris > uint64_t(std::numeric_limits<uint32_t>::max()) / 3)
+        fail(AMRX_ERR_LENGTH, "extract_isosurface: mesh too large for 32-bit indices");
+    };
+    if (dev_out) {
+      rq.xyz = xyz9;
+      rq.tri_cap = cap;
+      const ExtractResult r = run_extract(rq, index->scratch, st);
+      check_result(r, cells, true);
+      fill_stats(stats, r, cells);
+      *count = r.tris_written;
+      C.valid = false;
+      length_check(r.tris_written);
+      if (r.tris_written > cap)
+        fail(AMRX_ERR_CAPACITY, "output capacity " + std::to_string(cap) +
+                                  " < " + std::to_string(r.tris_written) + " triangles");
+      return;
+    }
+    const bool hit = C.valid && C.kind == 2 && C.begin == b && C.end == e &&
+                     C.iso == params->iso && C.f32 == params->xyz_is_f32;
+    if (!hit) {
+      uint64_t arena = std::max<uint64_t>(4096, cells / 2);
+      for (int attempt = 0; attempt < 2; attempt++) {
+        index->out_a.reserve(arena * tri_bytes);
+        rq.xyz = index->out_a.ptr;
+        rq.tri_cap = arena;
+        const ExtractResult r = run_extract(rq, index->scratch, st);
+        check_result(r, cells, true);
+        if (r.tris_written <= arena) {
+          C.valid = true;
+          C.kind = 2;
+          C.begin = b;
+          C.end = e;
+          C.iso = params->iso;
+          C.f32 = params->xyz_is_f32;
+          C.count = r.tris_written;
+          fill_stats(&C.stats, r, cells);
+          break;
+        }
+        arena = r.tris_written;
+      }
+    }
+    *count = C.count;
+    if (stats) *stats = C.stats;
+    length_check(C.count);
+    if (!xyz9) return;  // count query
+    if (C.count > cap)
+      fail(AMRX_ERR_CAPACITY, "output capacity " + std::to_string(cap) + " < " +
+                                std::to_string(C.count) + " triangles");
+    AMRX_CUDA(cudaMemcpyAsync(xyz9, index->out_a.ptr, C.count * tri_bytes,
+                              cudaMemcpyDefault, st));
+    AMRX_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+}  // extern "C"

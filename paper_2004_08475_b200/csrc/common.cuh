@@ -1,0 +1,291 @@
+// Device-side building blocks shared by the amrx kernels (sm_100a).
+//
+// Key geometry: a cell (i,j,k,level) packs into one u64 whose integer order
+// IS the reference's CellCoord order -- lexicographic (i,j,k,level), the
+// defaulted operator<=> of proj/include/amriso/core.hpp:82-88.  Per axis the
+// anchor is biased by the dataset minimum and shifted right by the finest
+// level present (every anchor is a multiple of 2^finest, core.hpp:98-110), and
+// the level field is level-finest.  Field widths come from the data, so a
+// sorted position is a CellId exactly as in locator.hpp:25-33.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace amrx {
+
+constexpr int kMaxLevel = 30;  // core.hpp:28
+constexpr int kWin = 128;      // keys per warp search window (1 KB of smem)
+constexpr int kKeyPad = 256;   // u64 sentinel padding after the key array
+constexpr uint32_t kFull = 0xffffffffu;
+
+struct KeyGeom {
+  int64_t mn[3];        // min anchor per axis
+  int64_t mx[3];        // max anchor per axis
+  int32_t shift;        // finest level present
+  int32_t bits[3];      // field width per axis
+  int32_t lbits;        // width of the level field
+  int32_t total;        // key bits in use
+  int32_t sh[3];        // left shift of the x/y/z fields
+  int32_t dir_bits;     // directory has 2^dir_bits + 1 entries
+  int32_t dir_shift;    // bucket = key >> dir_shift
+  uint32_t level_mask;  // bit l set iff level l present
+  int32_t nlevels;
+  int8_t levels[32];    // present levels, finest first (locator.cpp:85-89)
+};
+
+__host__ __device__ inline int64_t anchor_mask(int64_t x, int32_t level)
+{
+  return x & ~((int64_t(1) << level) - 1);  // core.hpp:98-103
+}
+
+__host__ __device__ inline bool level_present(const KeyGeom &g, int32_t l)
+{
+  return l >= 0 && l <= kMaxLevel && ((g.level_mask >> l) & 1u);
+}
+
+/// pack an aligned anchor on a present level (caller has range-checked)
+__host__ __device__ inline uint64_t pack_unchecked(const KeyGeom &g, int64_t i,
+                                                   int64_t j, int64_t k,
+                                                   int32_t level)
+{
+  uint64_t key = uint64_t(level - g.shift);
+  if (g.bits[0]) key |= uint64_t((i - g.mn[0]) >> g.shift) << g.sh[0];
+  if (g.bits[1]) key |= uint64_t((j - g.mn[1]) >> g.shift) << g.sh[1];
+  if (g.bits[2]) key |= uint64_t((k - g.mn[2]) >> g.shift) << g.sh[2];
+  return key;
+}
+
+/*! snap_on_level's key (locator.cpp:107-119): mask the point to the level,
+    reject anchors outside the stored range (which also covers the int32
+    guard: the stored range is int32), pack.  false = cannot exist. */
+__host__ __device__ inline bool query_key(const KeyGeom &g, int64_t px,
+                                          int64_t py, int64_t pz,
+                                          int32_t level, uint64_t &key)
+{
+  if (!level_present(g, level)) return false;
+  const int64_t ax = anchor_mask(px, level);
+  const int64_t ay = anchor_mask(py, level);
+  const int64_t az = anchor_mask(pz, level);
+  if (ax < g.mn[0] || ax > g.mx[0] || ay < g.mn[1] || ay > g.mx[1] ||
+      az < g.mn[2] || az > g.mx[2])
+    return false;
+  key = pack_unchecked(g, ax, ay, az, level);
+  return true;
+}
+
+struct Cell {
+  int64_t i, j, k;
+  int32_t level;
+};
+
+__host__ __device__ inline Cell unpack(const KeyGeom &g, uint64_t key)
+{
+  Cell c;
+  c.level = int32_t(key & ((uint64_t(1) << g.lbits) - 1)) + g.shift;
+  const auto field = [&](int a) -> int64_t {
+    if (!g.bits[a]) return g.mn[a];
+    const uint64_t u = (key >> g.sh[a]) & ((uint64_t(1) << g.bits[a]) - 1);
+    return g.mn[a] + int64_t(u << g.shift);
+  };
+  c.i = field(0);
+  c.j = field(1);
+  c.k = field(2);
+  return c;
+}
+
+// ------------------------------------------------------------------------
+// device helpers
+
+__device__ __forceinline__ uint32_t lane_id()
+{
+  uint32_t l;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));
+  return l;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt()
+{
+  uint32_t m;
+  asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ uint64_t ldg_u64(const uint64_t *p)
+{
+  return __ldg(reinterpret_cast<const unsigned long long *>(p));
+}
+
+__device__ __forceinline__ ulonglong2 ldg_u64x2(const uint64_t *p)
+{
+  return __ldg(reinterpret_cast<const ulonglong2 *>(p));
+}
+
+__device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src,
+                                             uint32_t mask = kFull)
+{
+  return __shfl_sync(mask, (unsigned long long)v, src);
+}
+
+/// lower_bound over a sorted u64 span in shared memory
+__device__ __forceinline__ int smem_lower_bound(const uint64_t *a, int n,
+                                                uint64_t q)
+{
+  int lo = 0;
+  while (n > 0) {
+    const int half = n >> 1;
+    if (a[lo + half] < q) {
+      lo += half + 1;
+      n -= half + 1;
+    } else {
+      n = half;
+    }
+  }
+  return lo;
+}
+
+/// lower_bound over [lo, hi) of the global key array
+__device__ __forceinline__ uint64_t global_lower_bound(const uint64_t *keys,
+                                                       uint64_t lo,
+                                                       uint64_t hi,
+                                                       uint64_t q)
+{
+  uint64_t n = hi - lo;
+  while (n > 0) {
+    const uint64_t half = n >> 1;
+    if (ldg_u64(keys + lo + half) < q) {
+      lo += half + 1;
+      n -= half + 1;
+    } else {
+      n = half;
+    }
+  }
+  return lo;
+}
+
+struct SearchCtx {
+  const uint64_t *keys;  // sorted packed keys, kKeyPad sentinels after n
+  const uint32_t *dir;   // 2^dir_bits + 1 bucket starts
+  uint64_t n;
+  int32_t dir_shift;
+};
+
+/*! Warp-cooperative exact lookup of up to NQ keys per lane (find_exact,
+    locator.cpp:94-101: the FIRST position holding the key, or miss).
+
+    1. Each lane reads the directory bucket bounds of its smallest and
+       largest query: every key of the bucket range lies in [lo, hi).
+    2. The warp takes the lowest pending lane as leader, narrows the
+       leader's range with a 32-ary search (one coalesced probe of 32 keys
+       per step) until it fits one window, and stages that window of kWin
+       keys in shared memory with 16-byte vector loads.
+    3. Every pending lane resolves each query it can prove from the window
+       (found, or absent because the window brackets it); the rest go
+       round again with the next leader, then fall back to a per-lane
+       binary search of their own bucket.
+
+    out[q] = CellId, -1 = absent.  Inactive queries (valid[q] false) are
+    left untouched.  All 32 lanes must call this together. */
+template <int NQ>
+__device__ void warp_find(const SearchCtx &s, const uint64_t (&q)[NQ],
+                          const bool (&valid)[NQ], int64_t (&out)[NQ],
+                          uint64_t *win)
+{
+  const uint32_t lane = lane_id();
+  bool any = false;
+  uint64_t qmin = ~0ull, qmax = 0;
+#pragma unroll
+  for (int t = 0; t < NQ; t++)
+    if (valid[t]) {
+      any = true;
+      qmin = q[t] < qmin ? q[t] : qmin;
+      qmax = q[t] > qmax ? q[t] : qmax;
+    }
+  uint64_t lo = 0, hi = 0;
+  if (any) {
+    lo = __ldg(s.dir + (qmin >> s.dir_shift));
+    hi = __ldg(s.dir + (qmax >> s.dir_shift) + 1);
+  }
+  uint32_t unresolved = 0;  // bit t: query t still open
+#pragma unroll
+  for (int t = 0; t < NQ; t++)
+    if (valid[t]) {
+      if (lo == hi)
+        out[t] = -1;  // empty bucket range: absent
+      else
+        unresolved |= 1u << t;
+    }
+
+  for (int round = 0; round < 3; round++) {
+    const uint32_t pend = __ballot_sync(kFull, unresolved != 0);
+    if (!pend) break;
+    const int leader = __ffs(pend) - 1;
+    // leader's smallest open query
+    uint64_t lq = ~0ull;
+#pragma unroll
+    for (int t = 0; t < NQ; t++)
+      if ((unresolved >> t) & 1) lq = q[t] < lq ? q[t] : lq;
+    lq = shfl_u64(lq, leader);
+    uint64_t L = shfl_u64(lo, leader);
+    uint64_t H = shfl_u64(hi, leader);
+    // 32-ary narrowing of [L, H) around lower_bound(lq)
+    // leave 4 keys of slack so the window below brackets lower_bound(lq)
+    while (H - L > uint64_t(kWin - 4)) {
+      const uint64_t step = (H - L + 31) >> 5;
+      const uint64_t pos = L + lane * step;
+      const bool below = pos < H && ldg_u64(s.keys + pos) < lq;
+      const int c = __popc(__ballot_sync(kFull, below));
+      const uint64_t nl = c > 0 ? L + uint64_t(c - 1) * step + 1 : L;
+      const uint64_t pc = L + uint64_t(c) * step;
+      const uint64_t nh = (c < 32 && pc < H) ? pc + 1 : H;
+      L = nl;
+      H = nh;
+    }
+    // stage the window [ws, ws + kWin): 16-byte aligned, starting at or
+    // before L-1 so the leader's key[L-1] < lq proof lies inside it
+    const uint64_t ws = L >= 1 ? ((L - 1) & ~1ull) : 0;
+    __syncwarp();
+#pragma unroll
+    for (int v = 0; v < kWin / 64; v++) {
+      const uint64_t at = ws + 2 * lane + 64 * v;
+      const ulonglong2 kv = ldg_u64x2(s.keys + at);  // padded: never OOB
+      win[2 * lane + 64 * v] = kv.x;
+      win[2 * lane + 64 * v + 1] = kv.y;
+    }
+    __syncwarp();
+    const uint64_t wend = ws + kWin < s.n ? ws + kWin : s.n;
+    const int cnt = int(wend - ws);
+#pragma unroll
+    for (int t = 0; t < NQ; t++) {
+      if (!((unresolved >> t) & 1)) continue;
+      const int p = smem_lower_bound(win, cnt, q[t]);
+      bool done = false;
+      int64_t res = -1;
+      if (p < cnt && win[p] == q[t]) {
+        if (p > 0 || ws <= lo) {
+          done = true;
+          res = int64_t(ws + p);
+        }
+      } else if (p == 0) {
+        done = ws <= lo;
+      } else if (p == cnt) {
+        done = wend >= hi;
+      } else {
+        done = true;  // bracketed by two window keys, not equal
+      }
+      if (done) {
+        out[t] = res;
+        unresolved &= ~(1u << t);
+      }
+    }
+  }
+  // fallback: per-lane binary search of the own bucket range
+#pragma unroll
+  for (int t = 0; t < NQ; t++)
+    if ((unresolved >> t) & 1) {
+      const uint64_t p = global_lower_bound(s.keys, lo, hi, q[t]);
+      out[t] = (p < hi && ldg_u64(s.keys + p) == q[t]) ? int64_t(p) : -1;
+    }
+}
+
+}  // namespace amrx

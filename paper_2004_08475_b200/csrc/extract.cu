@@ -1,0 +1,731 @@
+// The fused hot path: per-cell dual enumeration + ownership rules + marching
+// cubes on degenerate hexes + ordered emission, in one persistent kernel.
+//
+// Reference behaviour restated here (paths under /root/reference/):
+//   candidate order, task t -> cell t>>3, delta t&7   proj/src/pipeline.cpp:40-57
+//   dual_base_of                                      proj/include/amriso/dual.hpp:61-67
+//   try_build_dual rules #1/#2/#3, first failing
+//   corner decides the reject reason                  proj/src/dual.cpp:41-72
+//   snap: hint level first, then levels finest first  proj/src/locator.cpp:107-134
+//   strict '>' case mask, table_corner, tri_table     proj/src/contour.cpp:22-28,
+//                                                     proj/src/mc_tables.cpp:318-330
+//   interpolation (lower CellId first, no FMA)        proj/src/contour.cpp:30-50
+//   sliver drop on exact equality                     proj/src/contour.cpp:80-84
+//   two-pass count -> prefix -> emit                  proj/src/pipeline.cpp:80-146
+//
+// B200 design: one warp owns 32 consecutive cells (a "tile",
+// handed out in order by an atomic ticket).  Instead of 8 independent
+// candidates x 8 corner snaps, the warp resolves the cell's 27-point stencil
+// {-w,0,w}^3 column by column: one column = the three points (dx,dy,{-1,0,1})
+// whose keys are adjacent in the (i,j,k,level) order, so the 32 lanes' 96
+// queries of a column land in one or two 1 KB key windows staged in shared
+// memory (warp_find).  Round 1 resolves the 4 columns holding every
+// candidate's corner 0 (82-86% of candidates die there); round 2 resolves the
+// remaining columns the survivors need.  The rules are then applied corner by
+// corner in the reference's order, so the reported reason is the reference's.
+// Counting and emitting happen in the same kernel: a warp-scan gives
+// per-lane offsets and a decoupled look-back over tile aggregates gives the
+// tile's global offset -- the reference's "pass 1 / prefix sum / pass 2"
+// with the prefix sum made single-pass, so candidate order is preserved
+// without running the search twice.
+#include "internal.h"
+#include "mc_tables.inc"
+
+namespace amrx {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+// point index p = (ox+1) + 3(oy+1) + 9(oz+1), o in {-1,0,1}^3; self = 13
+constexpr uint32_t kCorner0Points = (1u << 0) | (1u << 1) | (1u << 3) |
+                                    (1u << 4) | (1u << 9) | (1u << 10) |
+                                    (1u << 12) | (1u << 13);
+constexpr uint32_t col_bits(int col)
+{
+  return (1u << col) | (1u << (col + 9)) | (1u << (col + 18));
+}
+
+enum : uint32_t { kOk = 0, kMiss = 1, kFiner = 2, kLower = 3 };
+
+// case rows, staged into shared memory per CTA (lanes index them divergently)
+__constant__ uint64_t c_mc_rows[256] = {AMRX_MC_PACKED_ROWS};
+
+/// stencil point of corner d of candidate delta (dual.hpp:61-67 + dual.cpp:49-53)
+__device__ __forceinline__ int point_of(int delta, int d)
+{
+  return ((d & 1) + (delta & 1)) + 3 * (((d >> 1) & 1) + ((delta >> 1) & 1)) +
+         9 * (((d >> 2) & 1) + ((delta >> 2) & 1));
+}
+
+constexpr unsigned long long kFlagAgg = 1ull << 62;
+constexpr unsigned long long kFlagPre = 2ull << 62;
+constexpr unsigned long long kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long ld_relaxed(
+  const unsigned long long *p)
+{
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p)
+               : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_relaxed(unsigned long long *p,
+                                           unsigned long long v)
+{
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v)
+               : "memory");
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v)
+{
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+    v += __shfl_xor_sync(kFull, (unsigned long long)v, off);
+  return v;
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v)
+{
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, v, off);
+    if (lane >= off) v += y;
+  }
+  return v;
+}
+
+/*! decoupled look-back over warp tiles (ticket order): publish this tile's
+    aggregate, sum predecessors 32 at a time until an inclusive prefix shows
+    up, publish the inclusive prefix; returns the exclusive prefix */
+__device__ uint64_t lookback(unsigned long long *state, uint32_t tile,
+                             uint64_t aggregate)
+{
+  const uint32_t lane = lane_id();
+  if (tile == 0) {
+    if (lane == 0) st_relaxed(state, kFlagPre | aggregate);
+    return 0;
+  }
+  if (lane == 0) st_relaxed(state + tile, kFlagAgg | aggregate);
+  uint64_t excl = 0;
+  int64_t j = int64_t(tile) - 1;
+  while (true) {
+    const int64_t idx = j - int64_t(lane);
+    unsigned long long s = kFlagPre;  // before tile 0: an inclusive 0
+    if (idx >= 0) {
+      do {
+        s = ld_relaxed(state + idx);
+      } while ((s & ~kValMask) == 0);
+    }
+    const uint32_t pre = __ballot_sync(kFull, (s & ~kValMask) == kFlagPre);
+    const int first = pre ? __ffs(pre) - 1 : 32;
+    excl += warp_sum_u64(int(lane) <= first ? (s & kValMask) : 0);
+    if (pre) break;
+    j -= 32;
+  }
+  if (lane == 0) st_relaxed(state + tile, kFlagPre | (excl + aggregate));
+  return excl;
+}
+
+struct KArgs {
+  SearchCtx s;
+  KeyGeom g;
+  const double *scal;
+  uint64_t cell_begin, cell_end;
+  uint32_t num_tiles;
+  double iso;
+  uint32_t *corners;
+  uint64_t *tasks;
+  uint64_t dual_cap;
+  void *xyz;
+  uint64_t tri_cap;
+  unsigned long long *dual_state;
+  unsigned long long *tri_state;
+  unsigned int *ticket;
+  unsigned long long *out;  // [0..3] counters, [4] duals, [5] tris counted,
+                            // [6] tris written, [7] error flags
+};
+
+struct Smem {
+  uint64_t win[kWarps][kWin];
+  uint32_t id[kWarps][27][32];
+  uint8_t lev[kWarps][27][32];
+  uint64_t mc_rows[256];
+};
+
+/// centre of the corner cell: anchor + half width, in double (core.hpp:113-118)
+__device__ __forceinline__ double centre(int64_t anchor, int level)
+{
+  return __dadd_rn(double(anchor), __dmul_rn(0.5, double(int64_t(1) << level)));
+}
+
+/*! marching cubes over one accepted dual (contour.cpp:52-87): count (and,
+    when out != null, write) its non-sliver triangles.  FP64 with explicit
+    round-to-nearest intrinsics: no FMA contraction, matching the
+    reference's -ffp-contract=off build. */
+template <bool WRITE, bool F32>
+__device__ int mc_dual(const KArgs &a, const Smem &sm, int warp, int lane,
+                       const Cell &c, int delta, double iso, void *out,
+                       uint64_t at, uint64_t cap, uint32_t &err)
+{
+  const int64_t w = int64_t(1) << c.level;
+  uint32_t ids[8];
+  double val[8];
+  int lv[8];
+  int mask = 0;
+#pragma unroll
+  for (int d = 0; d < 8; d++) {
+    const int p = point_of(delta, d);
+    ids[d] = sm.id[warp][p][lane];
+    lv[d] = sm.lev[warp][p][lane];
+    val[d] = __ldg(a.scal + ids[d]);
+    if (val[d] > iso) mask |= 1 << d;
+  }
+  // slot mask -> table row (mc_tables.cpp:324-330)
+  int row = 0;
+#pragma unroll
+  for (int t = 0; t < 8; t++)
+    if (mask & (1 << ((AMRX_MC_TABLE_CORNER >> (3 * t)) & 7))) row |= 1 << t;
+  const uint64_t word = sm.mc_rows[row];
+  const int ntab = int(word & 15);
+  if (ntab == 0) return 0;
+
+  const auto edge_point = [&](int e, double (&pt)[3]) {
+    const uint32_t ends = e < 8 ? uint32_t(AMRX_MC_EDGE_LO >> (8 * e))
+                                : uint32_t(AMRX_MC_EDGE_HI >> (8 * (e - 8)));
+    int u = int(ends & 15), v = int((ends >> 4) & 15);
+    if (ids[u] == ids[v]) err |= 1u;  // collapsed edge selected (contour.cpp:67-70)
+    if (ids[v] < ids[u]) {            // lower CellId first (contour.cpp:42-44)
+      const int t = u;
+      u = v;
+      v = t;
+    }
+    const double t = __ddiv_rn(__dsub_rn(iso, val[u]), __dsub_rn(val[v], val[u]));
+    const int ou[3] = {((u & 1) + (delta & 1)) - 1, (((u >> 1) & 1) + ((delta >> 1) & 1)) - 1,
+                       (((u >> 2) & 1) + ((delta >> 2) & 1)) - 1};
+    const int ov[3] = {((v & 1) + (delta & 1)) - 1, (((v >> 1) & 1) + ((delta >> 1) & 1)) - 1,
+                       (((v >> 2) & 1) + ((delta >> 2) & 1)) - 1};
+    const int64_t self[3] = {c.i, c.j, c.k};
+#pragma unroll
+    for (int ax = 0; ax < 3; ax++) {
+      const double pa = centre(anchor_mask(self[ax] + ou[ax] * w, lv[u]), lv[u]);
+      const double pb = centre(anchor_mask(self[ax] + ov[ax] * w, lv[v]), lv[v]);
+      pt[ax] = __dadd_rn(pa, __dmul_rn(t, __dsub_rn(pb, pa)));
+    }
+  };
+
+  int count = 0;
+  for (int tri = 0; tri < ntab; tri++) {
+    double p0[3], p1[3], p2[3];
+    edge_point(int((word >> (4 + 12 * tri)) & 15), p0);
+    edge_point(int((word >> (8 + 12 * tri)) & 15), p1);
+    edge_point(int((word >> (12 + 12 * tri)) & 15), p2);
+    const bool e01 = p0[0] == p1[0] && p0[1] == p1[1] && p0[2] == p1[2];
+    const bool e12 = p1[0] == p2[0] && p1[1] == p2[1] && p1[2] == p2[2];
+    const bool e02 = p0[0] == p2[0] && p0[1] == p2[1] && p0[2] == p2[2];
+    if (e01 || e12 || e02) continue;
+    if (WRITE) {
+      const uint64_t slot = at + uint64_t(count);
+      if (slot < cap) {
+        if (F32) {
+          float *o = static_cast<float *>(out) + slot * 9;
+          o[0] = float(p0[0]); o[1] = float(p0[1]); o[2] = float(p0[2]);
+          o[3] = float(p1[0]); o[4] = float(p1[1]); o[5] = float(p1[2]);
+          o[6] = float(p2[0]); o[7] = float(p2[1]); o[8] = float(p2[2]);
+        } else {
+          double *o = static_cast<double *>(out) + slot * 9;
+          o[0] = p0[0]; o[1] = p0[1]; o[2] = p0[2];
+          o[3] = p1[0]; o[4] = p1[1]; o[5] = p1[2];
+          o[6] = p2[0]; o[7] = p2[1]; o[8] = p2[2];
+        }
+      }
+    }
+    count++;
+  }
+  return count;
+}
+
+/*! resolve the three stencil points of column COL (dx, dy fixed; dz =
+    -1,0,+1) for the lanes flagged 'mine': hint level first in one
+    warp_find, then for misses the other present levels finest first
+    (locator.cpp:125-133), one warp_find per probe round */
+__device__ __noinline__ void resolve_column(const KArgs &a, Smem &sm,
+                                            int warp, int lane, const Cell &c,
+                                            uint32_t self, int COL, bool mine,
+                                            uint32_t &resolved,
+                                            uint64_t &status)
+{
+  const int ox = COL % 3 - 1, oy = COL / 3 - 1;
+  const int64_t w = int64_t(1) << c.level;
+  const int64_t px = c.i + ox * w, py = c.j + oy * w;
+  uint64_t q[3];
+  bool v[3];
+  int64_t out[3] = {-1, -1, -1};
+  int lvl[3] = {c.level, c.level, c.level};
+#pragma unroll
+  for (int t = 0; t < 3; t++)
+    v[t] = mine && query_key(a.g, px, py, c.k + (t - 1) * w, c.level, q[t]);
+  warp_find<3>(a.s, q, v, out, sm.win[warp]);
+
+  // misses at the hint level probe the other levels, finest first
+  bool pend[3];
+#pragma unroll
+  for (int t = 0; t < 3; t++) pend[t] = mine && out[t] < 0;
+  int li = 0;
+  while (__any_sync(kFull, pend[0] || pend[1] || pend[2])) {
+    while (li < a.g.nlevels && a.g.levels[li] == c.level) li++;
+    const bool have = li < a.g.nlevels;
+    const int L = have ? a.g.levels[li] : 0;
+    bool v2[3];
+    int64_t o2[3] = {-1, -1, -1};
+#pragma unroll
+    for (int t = 0; t < 3; t++)
+      v2[t] = pend[t] && have &&
+              query_key(a.g, px, py, c.k + (t - 1) * w, L, q[t]);
+    warp_find<3>(a.s, q, v2, o2, sm.win[warp]);
+#pragma unroll
+    for (int t = 0; t < 3; t++) {
+      if (pend[t] && v2[t] && o2[t] >= 0) {
+        out[t] = o2[t];
+        lvl[t] = L;
+        pend[t] = false;
+      }
+      if (!have) pend[t] = false;
+    }
+    li++;
+  }
+  if (mine) {
+#pragma unroll
+    for (int t = 0; t < 3; t++) {
+      const int p = COL + 9 * t;
+      uint32_t st;
+      if (out[t] < 0)
+        st = kMiss;
+      else if (lvl[t] < c.level)
+        st = kFiner;
+      else if (lvl[t] == c.level && uint32_t(out[t]) < self)
+        st = kLower;
+      else
+        st = kOk;
+      status |= uint64_t(st) << (2 * p);
+      resolved |= 1u << p;
+      sm.id[warp][p][lane] = uint32_t(out[t]);
+      sm.lev[warp][p][lane] = uint8_t(lvl[t]);
+    }
+  }
+}
+
+__device__ __forceinline__ void resolve_needed(const KArgs &a, Smem &sm,
+                                               int warp, int lane,
+                                               const Cell &c, uint32_t self,
+                                               uint32_t need,
+                                               uint32_t &resolved,
+                                               uint64_t &status)
+{
+  uint32_t cols = 0;
+#pragma unroll
+  for (int col = 0; col < 9; col++)
+    if (need & col_bits(col)) cols |= 1u << col;
+  uint32_t wcols = __reduce_or_sync(kFull, cols);
+  while (wcols) {
+    const int col = __ffs(wcols) - 1;
+    wcols &= wcols - 1;
+    resolve_column(a, sm, warp, lane, c, self, col, (cols >> col) & 1,
+                   resolved, status);
+  }
+}
+
+/// walk each live candidate's corners in order while they are resolved
+__device__ __forceinline__ void advance(uint32_t resolved, uint64_t status,
+                                        uint32_t &alive, uint32_t &curd,
+                                        uint32_t &accepted, uint32_t (&cnt)[4])
+{
+#pragma unroll
+  for (int delta = 0; delta < 8; delta++) {
+    if (!((alive >> delta) & 1)) continue;
+    int d = int((curd >> (4 * delta)) & 15);
+    while (d < 8) {
+      const int p = point_of(delta, d);
+      if (!((resolved >> p) & 1)) break;
+      const uint32_t st = uint32_t(status >> (2 * p)) & 3;
+      if (st != kOk) {
+        alive &= ~(1u << delta);
+        cnt[st]++;
+        break;
+      }
+      d++;
+    }
+    if (d == 8) {
+      accepted |= 1u << delta;
+      alive &= ~(1u << delta);
+      cnt[0]++;
+    }
+    curd = (curd & ~(15u << (4 * delta))) | (uint32_t(d) << (4 * delta));
+  }
+}
+
+template <bool EMIT_DUAL, bool EMIT_TRI, bool F32>
+__global__ void __launch_bounds__(kThreads, 3)
+extract_kernel(const KArgs a)
+{
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem &sm = *reinterpret_cast<Smem *>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (EMIT_TRI) {
+    for (int i = threadIdx.x; i < 256; i += kThreads) sm.mc_rows[i] = c_mc_rows[i];
+    __syncthreads();
+  }
+
+  uint32_t cnt[4] = {0, 0, 0, 0};
+  uint64_t tot_dual = 0, tot_counted = 0, tot_written = 0;
+  uint32_t err = 0;
+
+  for (;;) {
+    uint32_t tile = 0;
+    if (lane == 0) tile = atomicAdd(a.ticket, 1u);
+    tile = __shfl_sync(kFull, tile, 0);
+    if (tile >= a.num_tiles) break;
+
+    const uint64_t cell = a.cell_begin + uint64_t(tile) * 32 + lane;
+    const bool valid = cell < a.cell_end;
+    const uint32_t self = uint32_t(cell);
+    Cell c = unpack(a.g, valid ? ldg_u64(a.s.keys + cell) : 0);
+
+    uint32_t resolved = 0, alive = valid ? 0xffu : 0u, curd = 0, accepted = 0;
+    uint64_t status = 0;
+    // round 1: every candidate's corner 0 ({-w,0}^3, 4 columns)
+    resolve_needed(a, sm, warp, lane, c, self, valid ? kCorner0Points : 0,
+                   resolved, status);
+    advance(resolved, status, alive, curd, accepted, cnt);
+    // round 2: everything the survivors still need
+    uint32_t need = 0;
+#pragma unroll
+    for (int delta = 0; delta < 8; delta++)
+      if ((alive >> delta) & 1)
+        for (int d = int((curd >> (4 * delta)) & 15); d < 8; d++)
+          need |= 1u << point_of(delta, d);
+    need &= ~resolved;
+    resolve_needed(a, sm, warp, lane, c, self, need, resolved, status);
+    advance(resolved, status, alive, curd, accepted, cnt);
+    if (alive) err |= 2u;
+
+    // ---- count, scan, look-back, emit
+    const uint32_t nd = __popc(accepted);
+    uint32_t nt = 0;
+    if (EMIT_TRI)
+      for (uint32_t m = accepted; m; m &= m - 1)
+        nt += mc_dual<false, F32>(a, sm, warp, lane, c, __ffs(m) - 1, a.iso,
+                                  nullptr, 0, 0, err);
+    __syncwarp();
+    if (EMIT_DUAL) {
+      const uint32_t incl = warp_incl_scan(nd);
+      const uint32_t agg = __shfl_sync(kFull, incl, 31);
+      const uint64_t base = lookback(a.dual_state, tile, agg) + (incl - nd);
+      tot_dual += nd;
+      uint32_t k = 0;
+      for (uint32_t m = accepted; m; m &= m - 1, k++) {
+        const int delta = __ffs(m) - 1;
+        const uint64_t slot = base + k;
+        if (slot >= a.dual_cap) continue;
+        uint32_t ids[8];
+#pragma unroll
+        for (int d = 0; d < 8; d++) ids[d] = sm.id[warp][point_of(delta, d)][lane];
+        uint4 *dst = reinterpret_cast<uint4 *>(a.corners + slot * 8);
+        dst[0] = make_uint4(ids[0], ids[1], ids[2], ids[3]);
+        dst[1] = make_uint4(ids[4], ids[5], ids[6], ids[7]);
+        if (a.tasks) a.tasks[slot] = cell * 8 + uint64_t(delta);
+      }
+    } else {
+      tot_dual += nd;
+    }
+    if (EMIT_TRI) {
+      const uint32_t incl = warp_incl_scan(nt);
+      const uint32_t agg = __shfl_sync(kFull, incl, 31);
+      const uint64_t base = lookback(a.tri_state, tile, agg) + (incl - nt);
+      tot_counted += nt;
+      uint64_t at = base;
+      for (uint32_t m = accepted; m; m &= m - 1)
+        at += mc_dual<true, F32>(a, sm, warp, lane, c, __ffs(m) - 1, a.iso,
+                                 a.xyz, at, a.tri_cap, err);
+      tot_written += at - base;
+    }
+    __syncwarp();
+  }
+
+  // per-warp totals -> global
+  uint64_t v[8] = {cnt[0], cnt[1], cnt[2], cnt[3], tot_dual, tot_counted,
+                   tot_written, 0};
+#pragma unroll
+  for (int i = 0; i < 7; i++) v[i] = warp_sum_u64(v[i]);
+  err = __reduce_or_sync(kFull, err);
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < 7; i++)
+      if (v[i]) atomicAdd(a.out + i, (unsigned long long)v[i]);
+    if (err) atomicOr(a.out + 7, (unsigned long long)err);
+  }
+}
+
+// ------------------------------------------------------- query kernels
+
+/*! snap (locator.cpp:122-134) for one point per lane, warp-cooperatively:
+    probe sequence = hint (if in [0,30]) then present levels finest first
+    skipping the hint */
+__device__ int64_t warp_snap(const SearchCtx &s, const KeyGeom &g, bool active,
+                             int64_t px, int64_t py, int64_t pz, int32_t hint,
+                             uint64_t *win)
+{
+  int64_t result = -1;
+  bool pend = active;
+  int probe = (hint >= 0 && hint <= kMaxLevel) ? -1 : 0;
+  while (__any_sync(kFull, pend)) {
+    if (probe >= 0)
+      while (probe < g.nlevels && g.levels[probe] == hint) probe++;
+    const bool have = pend && (probe < 0 || probe < g.nlevels);
+    const int L = probe < 0 ? hint : (have ? g.levels[probe] : 0);
+    uint64_t q[1];
+    bool v[1];
+    int64_t o[1] = {-1};
+    v[0] = have && query_key(g, px, py, pz, L, q[0]);
+    warp_find<1>(s, q, v, o, win);
+    if (pend && v[0] && o[0] >= 0) {
+      result = o[0];
+      pend = false;
+    }
+    if (!have) pend = false;
+    probe++;
+  }
+  return result;
+}
+
+__global__ void __launch_bounds__(kThreads)
+find_exact_kernel(const SearchCtx s, const KeyGeom g,
+                  const int4 *__restrict__ cells, uint64_t n,
+                  int64_t *__restrict__ out)
+{
+  __shared__ uint64_t win[kWarps][kWin];
+  const int warp = threadIdx.x >> 5;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x - (threadIdx.x & 31) +
+                       (threadIdx.x & ~31u);
+       base < n; base += stride) {
+    const uint64_t r = base + (threadIdx.x & 31);
+    const bool in = r < n;
+    int4 cc = in ? cells[r] : make_int4(0, 0, 0, 0);
+    uint64_t q[1];
+    bool v[1];
+    int64_t o[1] = {-1};
+    // find_exact matches the full key: the anchor must be the stored one
+    v[0] = in && anchor_mask(cc.x, cc.w) == cc.x &&
+           anchor_mask(cc.y, cc.w) == cc.y &&
+           anchor_mask(cc.z, cc.w) == cc.z &&
+           query_key(g, cc.x, cc.y, cc.z, cc.w, q[0]);
+    warp_find<1>(s, q, v, o, win[warp]);
+    if (in) out[r] = v[0] ? o[0] : -1;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+snap_kernel(const SearchCtx s, const KeyGeom g,
+            const int64_t *__restrict__ points, const int32_t *__restrict__ hints,
+            int32_t hint_all, uint64_t n, int64_t *__restrict__ out)
+{
+  __shared__ uint64_t win[kWarps][kWin];
+  const int warp = threadIdx.x >> 5;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u);
+       base < n; base += stride) {
+    const uint64_t r = base + (threadIdx.x & 31);
+    const bool in = r < n;
+    const int64_t px = in ? points[3 * r] : 0, py = in ? points[3 * r + 1] : 0,
+                  pz = in ? points[3 * r + 2] : 0;
+    const int32_t h = in ? (hints ? hints[r] : hint_all) : -1;
+    const int64_t res = warp_snap(s, g, in, px, py, pz, h, win[warp]);
+    if (in) out[r] = res;
+  }
+}
+
+/// try_build_dual (dual.cpp:41-72) for one task (cell*8+delta) per lane
+__global__ void __launch_bounds__(kThreads)
+try_build_kernel(const SearchCtx s, const KeyGeom g,
+                 const uint64_t *__restrict__ tasks, uint64_t n,
+                 uint8_t *__restrict__ reject, uint32_t *__restrict__ corners)
+{
+  __shared__ uint64_t win[kWarps][kWin];
+  const int warp = threadIdx.x >> 5;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u);
+       base < n; base += stride) {
+    const uint64_t r = base + (threadIdx.x & 31);
+    bool live = r < n;
+    const uint64_t task = live ? tasks[r] : 0;
+    const uint64_t cell = task >> 3;
+    const int delta = int(task & 7);
+    live = live && cell < s.n;
+    const Cell c = unpack(g, live ? ldg_u64(s.keys + cell) : 0);
+    const int64_t w = int64_t(1) << c.level;
+    const int64_t bx = c.i - ((delta & 1) ? 0 : w);
+    const int64_t by = c.j - ((delta & 2) ? 0 : w);
+    const int64_t bz = c.k - ((delta & 4) ? 0 : w);
+    uint32_t code = live ? 0u : 1u;
+    uint32_t ids[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    bool going = live;
+    for (int d = 0; d < 8; d++) {
+      const int64_t hit =
+        warp_snap(s, g, going, bx + ((d & 1) ? w : 0), by + ((d & 2) ? w : 0),
+                  bz + ((d & 4) ? w : 0), c.level, win[warp]);
+      if (going) {
+        if (hit < 0) {
+          code = kMiss;
+          going = false;
+        } else {
+          const int hl = unpack(g, ldg_u64(s.keys + hit)).level;
+          if (hl < c.level) {
+            code = kFiner;
+            going = false;
+          } else if (hl == c.level && uint64_t(hit) < cell) {
+            code = kLower;
+            going = false;
+          } else {
+            ids[d] = uint32_t(hit);
+          }
+        }
+      }
+    }
+    if (r < n) {
+      reject[r] = uint8_t(code);
+      if (corners)
+        for (int d = 0; d < 8; d++) corners[8 * r + d] = code == 0 ? ids[d] : 0;
+    }
+  }
+}
+
+int grid_query(uint64_t n)
+{
+  const uint64_t blocks = (n + kThreads - 1) / kThreads;
+  return int(std::max<uint64_t>(1, std::min<uint64_t>(blocks,
+                                                       uint64_t(device_sm_count()) * 8)));
+}
+
+template <bool D, bool T, bool F>
+void launch_extract(const KArgs &k, int grid, cudaStream_t st)
+{
+  static bool attr = false;
+  if (!attr) {
+    AMRX_CUDA(cudaFuncSetAttribute(extract_kernel<D, T, F>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(sizeof(Smem))));
+    attr = true;
+  }
+  extract_kernel<D, T, F><<<grid, kThreads, sizeof(Smem), st>>>(k);
+  AMRX_LAUNCH_CHECK();
+}
+
+template <bool D, bool T, bool F>
+int occupancy_grid()
+{
+  static int grid = 0;
+  if (!grid) {
+    AMRX_CUDA(cudaFuncSetAttribute(extract_kernel<D, T, F>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(sizeof(Smem))));
+    int per_sm = 0;
+    AMRX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, extract_kernel<D, T, F>, kThreads, sizeof(Smem)));
+    grid = std::max(1, per_sm) * device_sm_count();
+  }
+  return grid;
+}
+
+}  // namespace
+
+ExtractResult run_extract(const ExtractRequest &r, DevBuf &scratch,
+                          cudaStream_t st)
+{
+  ExtractResult res{};
+  const uint64_t cells = r.cell_end > r.cell_begin ? r.cell_end - r.cell_begin : 0;
+  const uint64_t tiles = (cells + 31) / 32;
+  const size_t state_bytes = size_t(tiles) * 8;
+  scratch.reserve(2 * state_bytes + 256);
+  auto *base = scratch.as<unsigned char>();
+  KArgs k;
+  k.s = r.s;
+  k.g = r.g;
+  k.scal = r.scal;
+  k.cell_begin = r.cell_begin;
+  k.cell_end = r.cell_end;
+  k.num_tiles = uint32_t(tiles);
+  k.iso = r.iso;
+  k.corners = r.corners;
+  k.tasks = r.tasks;
+  k.dual_cap = r.corners ? r.dual_cap : 0;
+  k.xyz = r.xyz;
+  k.tri_cap = r.xyz ? r.tri_cap : 0;
+  k.out = reinterpret_cast<unsigned long long *>(base);
+  k.ticket = reinterpret_cast<unsigned int *>(base + 64);
+  k.dual_state = reinterpret_cast<unsigned long long *>(base + 256);
+  k.tri_state = reinterpret_cast<unsigned long long *>(base + 256 + state_bytes);
+  AMRX_CUDA(cudaMemsetAsync(base, 0, 2 * state_bytes + 256, st));
+
+  cudaEvent_t e0, e1;
+  AMRX_CUDA(cudaEventCreate(&e0));
+  AMRX_CUDA(cudaEventCreate(&e1));
+  AMRX_CUDA(cudaEventRecord(e0, st));
+  if (tiles) {
+    int grid;
+    const bool D = r.emit_dual, T = r.emit_tri, F = r.tri_f32;
+    if (D && T && F) { grid = occupancy_grid<true, true, true>(); launch_extract<true, true, true>(k, grid, st); }
+    else if (D && T) { grid = occupancy_grid<true, true, false>(); launch_extract<true, true, false>(k, grid, st); }
+    else if (D) { grid = occupancy_grid<true, false, false>(); launch_extract<true, false, false>(k, grid, st); }
+    else if (T && F) { grid = occupancy_grid<false, true, true>(); launch_extract<false, true, true>(k, grid, st); }
+    else if (T) { grid = occupancy_grid<false, true, false>(); launch_extract<false, true, false>(k, grid, st); }
+    else { grid = occupancy_grid<false, false, false>(); launch_extract<false, false, false>(k, grid, st); }
+    res.launches = 1;
+  }
+  AMRX_CUDA(cudaEventRecord(e1, st));
+  unsigned long long h[8];
+  AMRX_CUDA(cudaMemcpyAsync(h, base, sizeof h, cudaMemcpyDeviceToHost, st));
+  AMRX_CUDA(cudaStreamSynchronize(st));
+  AMRX_CUDA(cudaEventElapsedTime(&res.ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  for (int i = 0; i < 4; i++) res.counters[i] = h[i];
+  res.duals = h[4];
+  res.tris_counted = h[5];
+  res.tris_written = h[6];
+  res.error_flags = uint32_t(h[7]);
+  return res;
+}
+
+void run_find_exact(const SearchCtx &s, const KeyGeom &g, const int4 *cells,
+                    uint64_t n, int64_t *out, cudaStream_t st)
+{
+  if (!n) return;
+  find_exact_kernel<<<grid_query(n), kThreads, 0, st>>>(s, g, cells, n, out);
+  AMRX_LAUNCH_CHECK();
+}
+
+void run_snap(const SearchCtx &s, const KeyGeom &g, const int64_t *points,
+              const int32_t *hints, int32_t hint_all, uint64_t n, int64_t *out,
+              cudaStream_t st)
+{
+  if (!n) return;
+  snap_kernel<<<grid_query(n), kThreads, 0, st>>>(s, g, points, hints, hint_all,
+                                                  n, out);
+  AMRX_LAUNCH_CHECK();
+}
+
+void run_try_build(const SearchCtx &s, const KeyGeom &g, const uint64_t *tasks,
+                   uint64_t n, uint8_t *reject, uint32_t *corners,
+                   cudaStream_t st)
+{
+  if (!n) return;
+  try_build_kernel<<<grid_query(n), kThreads, 0, st>>>(s, g, tasks, n, reject,
+                                                       corners);
+  AMRX_LAUNCH_CHECK();
+}
+
+}  // namespace amrx

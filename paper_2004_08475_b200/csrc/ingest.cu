@@ -1,0 +1,362 @@
+// Ingest kernels: validation prepass, key packing, order check, scalar
+// gather, search directory, device scan.  Replaces build_index's serial
+// loops (proj/src/locator.cpp:26-92) with HBM-streaming passes.
+#include "internal.h"
+
+#include <algorithm>
+#include <climits>
+#include <vector>
+
+namespace amrx {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+int grid_for(uint64_t n, int threads, int per_thread = 1)
+{
+  const uint64_t blocks = (n + uint64_t(threads) * per_thread - 1) /
+                          (uint64_t(threads) * per_thread);
+  const uint64_t cap = uint64_t(device_sm_count()) * 32;
+  return int(std::max<uint64_t>(1, std::min(blocks, cap)));
+}
+
+struct PrepassAcc {
+  unsigned long long first_bad;
+  int mn[3];
+  int mx[3];
+  long long hi[3];
+  unsigned int level_mask;
+};
+
+/*! locator.cpp:33-50 per record (level in [0,30], anchor aligned) fused
+    with the bounds/level reductions of locator.cpp:70-89.  The first bad
+    record in INPUT order wins (atomicMin on its position), so the host can
+    name "record n" exactly like the serial loop. */
+__global__ void __launch_bounds__(kThreads)
+prepass_kernel(const int4 *__restrict__ cells, uint64_t n, PrepassAcc *acc)
+{
+  int mn[3] = {INT_MAX, INT_MAX, INT_MAX};
+  int mx[3] = {INT_MIN, INT_MIN, INT_MIN};
+  long long hi[3] = {LLONG_MIN, LLONG_MIN, LLONG_MIN};
+  unsigned int mask = 0;
+  unsigned long long bad = ~0ull;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += stride) {
+    const int4 c = __ldg(cells + r);
+    const int v[3] = {c.x, c.y, c.z};
+    bool ok = c.w >= 0 && c.w <= kMaxLevel;
+    if (ok) {
+      const int64_t w = int64_t(1) << c.w;
+#pragma unroll
+      for (int a = 0; a < 3; a++) {
+        ok = ok && anchor_mask(v[a], c.w) == v[a];
+        mn[a] = min(mn[a], v[a]);
+        mx[a] = max(mx[a], v[a]);
+        hi[a] = max(hi[a], (long long)(v[a] + w));
+      }
+      mask |= 1u << c.w;
+    }
+    if (!ok && r < bad) bad = r;
+  }
+  // warp reduce, then one atomic per warp
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      mn[a] = min(mn[a], __shfl_xor_sync(kFull, mn[a], off));
+      mx[a] = max(mx[a], __shfl_xor_sync(kFull, mx[a], off));
+      hi[a] = max(hi[a], (long long)__shfl_xor_sync(kFull, hi[a], off));
+    }
+    mask |= __shfl_xor_sync(kFull, mask, off);
+    const unsigned long long ob = __shfl_xor_sync(kFull, bad, off);
+    bad = ob < bad ? ob : bad;
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      atomicMin(&acc->mn[a], mn[a]);
+      atomicMax(&acc->mx[a], mx[a]);
+      atomicMax(&acc->hi[a], hi[a]);
+    }
+    atomicOr(&acc->level_mask, mask);
+    if (bad != ~0ull) atomicMin(&acc->first_bad, bad);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+pack_kernel(const int4 *__restrict__ cells, uint64_t n, const KeyGeom g,
+            uint64_t *__restrict__ keys, uint32_t *__restrict__ idx)
+{
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += stride) {
+    const int4 c = __ldg(cells + r);
+    keys[r] = pack_unchecked(g, c.x, c.y, c.z, c.w);
+    idx[r] = uint32_t(r);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+order_check_kernel(const uint64_t *__restrict__ keys, uint64_t n,
+                   unsigned long long *out2)
+{
+  unsigned long long desc = 0, eq = 0;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+       r + 1 < n; r += stride) {
+    const uint64_t a = ldg_u64(keys + r), b = ldg_u64(keys + r + 1);
+    desc += a > b;
+    eq += a == b;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    desc += __shfl_xor_sync(kFull, desc, off);
+    eq += __shfl_xor_sync(kFull, eq, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (desc) atomicAdd(out2, desc);
+    if (eq) atomicAdd(out2 + 1, eq);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+gather_kernel(const uint32_t *__restrict__ perm, const double *__restrict__ in,
+              double *__restrict__ out, uint64_t n)
+{
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += stride)
+    out[r] = __ldg(in + __ldg(perm + r));
+}
+
+__global__ void pad_kernel(uint64_t *keys, uint64_t n)
+{
+  keys[n + threadIdx.x] = ~0ull;
+}
+
+/*! bucket histogram over sorted keys: equal buckets form runs, so each
+    warp issues one atomic per distinct bucket it holds */
+__global__ void __launch_bounds__(kThreads)
+bucket_count_kernel(const uint64_t *__restrict__ keys, uint64_t n, int shift,
+                    uint32_t *__restrict__ cnt)
+{
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  const uint64_t start = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  // whole warps iterate together so the match below sees all lanes
+  for (uint64_t base = start - (threadIdx.x & 31); base < n; base += stride) {
+    const uint64_t r = base + (threadIdx.x & 31);
+    const bool in = r < n;
+    const uint64_t b = in ? (ldg_u64(keys + r) >> shift) : ~0ull;
+    const uint32_t peers = __match_any_sync(kFull, b);
+    if (in && (__ffs(peers) - 1) == int(threadIdx.x & 31))
+      atomicAdd(cnt + b, __popc(peers));
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+unpack_kernel(const uint64_t *__restrict__ keys, uint64_t n, const KeyGeom g,
+              int4 *__restrict__ cells)
+{
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += stride) {
+    const Cell c = unpack(g, ldg_u64(keys + r));
+    cells[r] = make_int4(int(c.i), int(c.j), int(c.k), c.level);
+  }
+}
+
+// --------------------------------------------------- reduce-then-scan
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ uint32_t block_exclusive_sum(uint32_t v,
+                                                        uint32_t *smem,
+                                                        uint32_t *total)
+{
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, off);
+    if (lane >= off) x += y;
+  }
+  if (lane == 31) smem[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    uint32_t s = lane < nw ? smem[lane] : 0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, s, off);
+      if (lane >= off) s += y;
+    }
+    if (lane < nw) smem[lane] = s;
+  }
+  __syncthreads();
+  const uint32_t warp_excl = warp ? smem[warp - 1] : 0;
+  if (total) *total = smem[(blockDim.x >> 5) - 1];
+  return warp_excl + x - v;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+scan_reduce_kernel(const uint32_t *__restrict__ in, uint64_t n,
+                   uint32_t *__restrict__ sums)
+{
+  __shared__ uint32_t sm[32];
+  const uint64_t base = uint64_t(blockIdx.x) * kScanTile;
+  uint32_t s = 0;
+#pragma unroll
+  for (int t = 0; t < kScanItems; t++) {
+    const uint64_t r = base + uint64_t(t) * kScanThreads + threadIdx.x;
+    if (r < n) s += in[r];
+  }
+  uint32_t total;
+  block_exclusive_sum(s, sm, &total);
+  if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+scan_downsweep_kernel(const uint32_t *in, uint32_t *out, uint64_t n,
+                      const uint32_t *__restrict__ block_offsets)
+{
+  __shared__ uint32_t sm[32];
+  const uint64_t base = uint64_t(blockIdx.x) * kScanTile +
+                        uint64_t(threadIdx.x) * kScanItems;
+  uint32_t v[kScanItems];
+  uint32_t s = 0;
+#pragma unroll
+  for (int t = 0; t < kScanItems; t++) {
+    const uint64_t r = base + t;
+    v[t] = r < n ? in[r] : 0;
+    s += v[t];
+  }
+  uint32_t run = block_exclusive_sum(s, sm, nullptr) +
+                 (block_offsets ? block_offsets[blockIdx.x] : 0);
+#pragma unroll
+  for (int t = 0; t < kScanItems; t++) {
+    const uint64_t r = base + t;
+    if (r < n) out[r] = run;
+    run += v[t];
+  }
+}
+
+}  // namespace
+
+PrepassResult ingest_prepass(const int4 *cells, uint64_t n, DevBuf &scratch,
+                             cudaStream_t st)
+{
+  PrepassAcc init;
+  init.first_bad = ~0ull;
+  for (int a = 0; a < 3; a++) {
+    init.mn[a] = INT_MAX;
+    init.mx[a] = INT_MIN;
+    init.hi[a] = LLONG_MIN;
+  }
+  init.level_mask = 0;
+  scratch.reserve(sizeof(PrepassAcc));
+  PrepassAcc *acc = scratch.as<PrepassAcc>();
+  AMRX_CUDA(cudaMemcpyAsync(acc, &init, sizeof init, cudaMemcpyHostToDevice, st));
+  prepass_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(cells, n, acc);
+  AMRX_LAUNCH_CHECK();
+  PrepassAcc h;
+  AMRX_CUDA(cudaMemcpyAsync(&h, acc, sizeof h, cudaMemcpyDeviceToHost, st));
+  AMRX_CUDA(cudaStreamSynchronize(st));
+  PrepassResult r;
+  r.first_bad = h.first_bad;
+  for (int a = 0; a < 3; a++) {
+    r.mn[a] = h.mn[a];
+    r.mx[a] = h.mx[a];
+    r.hi[a] = h.hi[a];
+  }
+  r.level_mask = h.level_mask;
+  return r;
+}
+
+void ingest_pack(const int4 *cells, uint64_t n, const KeyGeom &g,
+                 uint64_t *keys, uint32_t *idx, cudaStream_t st)
+{
+  pack_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(cells, n, g, keys,
+                                                            idx);
+  AMRX_LAUNCH_CHECK();
+}
+
+void ingest_order_check(const uint64_t *keys, uint64_t n, DevBuf &scratch,
+                        uint64_t *descents, uint64_t *equal_pairs,
+                        cudaStream_t st)
+{
+  scratch.reserve(16);
+  auto *out = scratch.as<unsigned long long>();
+  AMRX_CUDA(cudaMemsetAsync(out, 0, 16, st));
+  order_check_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(keys, n,
+                                                                   out);
+  AMRX_LAUNCH_CHECK();
+  unsigned long long h[2];
+  AMRX_CUDA(cudaMemcpyAsync(h, out, 16, cudaMemcpyDeviceToHost, st));
+  AMRX_CUDA(cudaStreamSynchronize(st));
+  *descents = h[0];
+  *equal_pairs = h[1];
+}
+
+void gather_f64(const uint32_t *perm, const double *in, double *out,
+                uint64_t n, cudaStream_t st)
+{
+  gather_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(perm, in, out,
+                                                              n);
+  AMRX_LAUNCH_CHECK();
+}
+
+void pad_keys(uint64_t *keys, uint64_t n, cudaStream_t st)
+{
+  pad_kernel<<<1, kKeyPad, 0, st>>>(keys, n);
+  AMRX_LAUNCH_CHECK();
+}
+
+void build_directory(const uint64_t *keys, uint64_t n, const KeyGeom &g,
+                     uint32_t *dir, DevBuf &scratch, cudaStream_t st)
+{
+  const uint64_t entries = (uint64_t(1) << g.dir_bits) + 1;
+  AMRX_CUDA(cudaMemsetAsync(dir, 0, entries * sizeof(uint32_t), st));
+  bucket_count_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(
+    keys, n, g.dir_shift, dir);
+  AMRX_LAUNCH_CHECK();
+  scan_exclusive_u32(dir, dir, entries, scratch, st);
+}
+
+void unpack_cells(const uint64_t *keys, uint64_t n, const KeyGeom &g,
+                  int4 *cells, cudaStream_t st)
+{
+  unpack_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(keys, n, g,
+                                                              cells);
+  AMRX_LAUNCH_CHECK();
+}
+
+void scan_exclusive_u32(const uint32_t *in, uint32_t *out, uint64_t n,
+                        DevBuf &scratch, cudaStream_t st, int depth)
+{
+  if (n == 0) return;
+  const uint64_t blocks = (n + kScanTile - 1) / kScanTile;
+  if (blocks == 1) {
+    scan_downsweep_kernel<<<1, kScanThreads, 0, st>>>(in, out, n, nullptr);
+    AMRX_LAUNCH_CHECK();
+    return;
+  }
+  // block sums live in a per-depth slice of the scratch buffer
+  const uint64_t slot = (blocks + 1 + 255) & ~uint64_t(255);
+  const size_t need = size_t(slot) * sizeof(uint32_t);
+  DevBuf local;
+  local.reserve(need);
+  uint32_t *sums = local.as<uint32_t>();
+  scan_reduce_kernel<<<unsigned(blocks), kScanThreads, 0, st>>>(in, n, sums);
+  AMRX_LAUNCH_CHECK();
+  scan_exclusive_u32(sums, sums, blocks, scratch, st, depth + 1);
+  scan_downsweep_kernel<<<unsigned(blocks), kScanThreads, 0, st>>>(in, out, n,
+                                                                  sums);
+  AMRX_LAUNCH_CHECK();
+  // keep the block-sum buffer alive until the stream has consumed it
+  AMRX_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace amrx

@@ -1,0 +1,130 @@
+// Host-side interfaces shared between the amrx translation units.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace amrx {
+
+/// status + message carried out of the implementation to the C ABI
+struct Error {
+  int code;  // amrx_status
+  std::string message;
+};
+
+[[noreturn]] void throw_cuda(cudaError_t e, const char *what, const char *file,
+                             int line);
+
+#define AMRX_CUDA(call)                                                  \
+  do {                                                                   \
+    const cudaError_t amrx_e_ = (call);                                  \
+    if (amrx_e_ != cudaSuccess)                                          \
+      ::amrx::throw_cuda(amrx_e_, #call, __FILE__, __LINE__);            \
+  } while (0)
+
+#define AMRX_LAUNCH_CHECK() AMRX_CUDA(cudaGetLastError())
+
+/// device allocation with RAII; grows on demand
+struct DevBuf {
+  void *ptr = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf &) = delete;
+  DevBuf &operator=(const DevBuf &) = delete;
+  ~DevBuf();
+  void reserve(size_t n);   // at least n bytes, contents not kept
+  void release();
+  template <typename T> T *as() const { return static_cast<T *>(ptr); }
+};
+
+// ------------------------------------------------------------ ingest.cu
+struct PrepassResult {
+  uint64_t first_bad;   // UINT64_MAX if every record is valid
+  int32_t mn[3], mx[3];
+  int64_t hi[3];        // max anchor + width per axis
+  uint32_t level_mask;
+};
+
+/// validation + bounds + level mask over n input records (device pointer)
+PrepassResult ingest_prepass(const int4 *cells, uint64_t n, DevBuf &scratch,
+                             cudaStream_t st);
+
+/// key = pack(cell), idx = position
+void ingest_pack(const int4 *cells, uint64_t n, const KeyGeom &g,
+                 uint64_t *keys, uint32_t *idx, cudaStream_t st);
+
+/// number of i with key[i] > key[i+1] (0 = already sorted), and equal pairs
+void ingest_order_check(const uint64_t *keys, uint64_t n, DevBuf &scratch,
+                        uint64_t *descents, uint64_t *equal_pairs,
+                        cudaStream_t st);
+
+void gather_f64(const uint32_t *perm, const double *in, double *out,
+                uint64_t n, cudaStream_t st);
+
+/// fill kKeyPad sentinels (all ones) after the n sorted keys
+void pad_keys(uint64_t *keys, uint64_t n, cudaStream_t st);
+
+/// dir[b] = first position whose key >> g.dir_shift >= b, b in [0, 2^D]
+void build_directory(const uint64_t *keys, uint64_t n, const KeyGeom &g,
+                     uint32_t *dir, DevBuf &scratch, cudaStream_t st);
+
+/// unpack sorted keys into 4 x int32 cells
+void unpack_cells(const uint64_t *keys, uint64_t n, const KeyGeom &g,
+                  int4 *cells, cudaStream_t st);
+
+/// exclusive scan of n u32 values (in place allowed); returns nothing
+void scan_exclusive_u32(const uint32_t *in, uint32_t *out, uint64_t n,
+                        DevBuf &scratch, cudaStream_t st, int depth = 0);
+
+// -------------------------------------------------------------- sort.cu
+/// stable LSD radix sort of (keys, vals) over bits [0, key_bits); the
+/// result ends in keys/vals (alt buffers are scratch of the same size)
+void radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
+                      uint32_t *vals_alt, uint64_t n, int key_bits,
+                      DevBuf &scratch, cudaStream_t st, int *passes_run);
+
+// ----------------------------------------------------------- extract.cu
+struct ExtractRequest {
+  SearchCtx s;
+  KeyGeom g;
+  const double *scal;
+  uint64_t cell_begin, cell_end;
+  bool emit_dual;
+  bool emit_tri;
+  bool tri_f32;
+  double iso;
+  uint32_t *corners;    // [dual_cap][8] or null
+  uint64_t *tasks;      // [dual_cap] or null
+  uint64_t dual_cap;
+  void *xyz;            // [tri_cap][9] f64/f32 or null
+  uint64_t tri_cap;
+};
+
+struct ExtractResult {
+  uint64_t counters[4];  // accepted, missing, finer, lower_key
+  uint64_t duals;        // emitted by the scan (== accepted)
+  uint64_t tris_counted; // count phase
+  uint64_t tris_written; // emit phase
+  uint32_t error_flags;  // bit0 collapsed edge, bit1 undecided candidate
+  float ms;              // device time of the extraction kernel
+  uint64_t launches;
+};
+
+ExtractResult run_extract(const ExtractRequest &r, DevBuf &scratch,
+                          cudaStream_t st);
+
+void run_find_exact(const SearchCtx &s, const KeyGeom &g, const int4 *cells,
+                    uint64_t n, int64_t *out, cudaStream_t st);
+void run_snap(const SearchCtx &s, const KeyGeom &g, const int64_t *points,
+              const int32_t *hints, int32_t hint_all, uint64_t n,
+              int64_t *out, cudaStream_t st);
+void run_try_build(const SearchCtx &s, const KeyGeom &g, const uint64_t *tasks,
+                   uint64_t n, uint8_t *reject, uint32_t *corners,
+                   cudaStream_t st);
+
+int device_sm_count();
+
+}  // namespace amrx

@@ -1,0 +1,290 @@
+// Stable LSD radix sort of (u64 key, u32 value) pairs, onesweep style:
+// one histogram sweep for every digit pass up front, then per 8-bit pass a
+// single kernel that ranks a tile in shared memory (warp __match_any_sync
+// multisplit), obtains the tile's global digit offsets through a decoupled
+// look-back over its predecessors, and scatters digit-sorted runs so the
+// stores coalesce.  Replaces the std::sort over a permutation in
+// build_index (proj/src/locator.cpp:52-68); stability keeps duplicate keys
+// in input order exactly like its (key, input index) comparator.
+#include "internal.h"
+
+#include <algorithm>
+#include <vector>
+
+namespace amrx {
+
+namespace {
+
+constexpr int kRadixBits = 8;
+constexpr int kDigits = 1 << kRadixBits;
+constexpr int kSortThreads = 512;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kSortItems = 8;  // keys per thread
+constexpr int kSortTile = kSortThreads * kSortItems;
+constexpr int kMaxPasses = 8;
+
+constexpr unsigned long long kFlagAgg = 1ull << 62;
+constexpr unsigned long long kFlagPre = 2ull << 62;
+constexpr unsigned long long kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long ld_relaxed(
+  const unsigned long long *p)
+{
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p)
+               : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_relaxed(unsigned long long *p,
+                                           unsigned long long v)
+{
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v)
+               : "memory");
+}
+
+/// all passes' digit histograms in one sweep over the keys
+__global__ void __launch_bounds__(256)
+histogram_kernel(const uint64_t *__restrict__ keys, uint64_t n, int passes,
+                 unsigned int *__restrict__ hist)
+{
+  __shared__ unsigned int h[kMaxPasses][kDigits];
+  for (int i = threadIdx.x; i < kMaxPasses * kDigits; i += blockDim.x)
+    (&h[0][0])[i] = 0;
+  __syncthreads();
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += stride) {
+    const uint64_t k = ldg_u64(keys + r);
+    for (int p = 0; p < passes; p++)
+      atomicAdd(&h[p][(k >> (p * kRadixBits)) & (kDigits - 1)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * kDigits; i += blockDim.x) {
+    const unsigned int v = (&h[0][0])[i];
+    if (v) atomicAdd(hist + i, v);
+  }
+}
+
+/// exclusive scan of each pass's 256 bins (one block, one warp per pass)
+__global__ void digit_offsets_kernel(const unsigned int *hist, int passes,
+                                     unsigned long long *offs)
+{
+  const int lane = threadIdx.x & 31, p = threadIdx.x >> 5;
+  if (p >= passes) return;
+  unsigned long long run = 0;
+  for (int base = 0; base < kDigits; base += 32) {
+    unsigned long long v = hist[p * kDigits + base + lane];
+    unsigned long long x = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned long long y = __shfl_up_sync(kFull, x, off);
+      if (lane >= off) x += y;
+    }
+    offs[p * kDigits + base + lane] = run + x - v;
+    run += __shfl_sync(kFull, x, 31);
+  }
+}
+
+struct PassSmem {
+  uint64_t keys[kSortTile];
+  uint32_t vals[kSortTile];
+  uint32_t whist[kSortWarps][kDigits];  // per-warp counts -> warp offsets
+  uint32_t bexcl[kDigits];              // tile-local digit start
+  unsigned long long gofs[kDigits];     // global start of this tile's run
+  uint32_t tile;
+};
+
+__global__ void __launch_bounds__(kSortThreads)
+onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
+                     const uint32_t *__restrict__ vals_in,
+                     uint64_t *__restrict__ keys_out,
+                     uint32_t *__restrict__ vals_out, uint64_t n, int shift,
+                     const unsigned long long *__restrict__ digit_start,
+                     unsigned long long *state, unsigned int *ticket)
+{
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PassSmem &sm = *reinterpret_cast<PassSmem *>(smem_raw);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  if (threadIdx.x == 0) sm.tile = atomicAdd(ticket, 1u);
+  for (int i = threadIdx.x; i < kSortWarps * kDigits; i += kSortThreads)
+    (&sm.whist[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t tile = sm.tile;
+  const uint64_t base = uint64_t(tile) * kSortTile;
+
+  // warp-striped load: item t of lane l in warp w is tile position
+  // w*256 + t*32 + l, so (w, t, l) order is input order
+  uint64_t k[kSortItems];
+  uint32_t v[kSortItems];
+  uint32_t dig[kSortItems];
+  uint32_t rank[kSortItems];
+#pragma unroll
+  for (int t = 0; t < kSortItems; t++) {
+    const uint64_t r = base + uint64_t(warp) * (32 * kSortItems) + t * 32 + lane;
+    const bool in = r < n;
+    k[t] = in ? ldg_u64(keys_in + r) : ~0ull;
+    v[t] = in ? __ldg(vals_in + r) : 0u;
+    dig[t] = in ? uint32_t((k[t] >> shift) & (kDigits - 1)) : uint32_t(kDigits);
+  }
+  // warp multisplit: rank within (warp, digit) in input order
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int t = 0; t < kSortItems; t++) {
+    const uint32_t peers = __match_any_sync(kFull, dig[t]);
+    const bool leader = (__ffs(peers) - 1) == lane;
+    uint32_t before = 0;
+    if (dig[t] < kDigits) before = sm.whist[warp][dig[t]];
+    rank[t] = before + __popc(peers & lt);
+    __syncwarp();
+    if (leader && dig[t] < kDigits) sm.whist[warp][dig[t]] = before + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+
+  // per digit: exclusive over warps, tile total
+  uint32_t total = 0;
+  if (threadIdx.x < kDigits) {
+    const int d = threadIdx.x;
+    for (int w = 0; w < kSortWarps; w++) {
+      const uint32_t c = sm.whist[w][d];
+      sm.whist[w][d] = total;
+      total += c;
+    }
+  }
+  // tile-local digit starts (exclusive scan of totals over 256 digits)
+  if (threadIdx.x < kDigits) sm.bexcl[threadIdx.x] = total;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t run = 0;
+    for (int b = 0; b < kDigits; b += 32) {
+      const uint32_t c = sm.bexcl[b + lane];
+      uint32_t x = c;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, off);
+        if (lane >= off) x += y;
+      }
+      sm.bexcl[b + lane] = run + x - c;
+      run += __shfl_sync(kFull, x, 31);
+    }
+  }
+
+  // decoupled look-back per digit: publish the aggregate, sum the
+  // predecessors' until an inclusive prefix appears, publish ours
+  if (threadIdx.x < kDigits) {
+    const int d = threadIdx.x;
+    unsigned long long *me = state + uint64_t(tile) * kDigits + d;
+    unsigned long long excl = 0;
+    if (tile == 0) {
+      st_relaxed(me, kFlagPre | total);
+    } else {
+      st_relaxed(me, kFlagAgg | total);
+      int64_t j = int64_t(tile) - 1;
+      while (true) {
+        unsigned long long s;
+        do {
+          s = ld_relaxed(state + uint64_t(j) * kDigits + d);
+        } while ((s & ~kValMask) == 0);
+        excl += s & kValMask;
+        if ((s & ~kValMask) == kFlagPre) break;
+        j--;
+      }
+      st_relaxed(me, kFlagPre | (excl + total));
+    }
+    sm.gofs[d] = digit_start[d] + excl;
+  }
+  __syncthreads();
+
+  // local shuffle into digit order
+#pragma unroll
+  for (int t = 0; t < kSortItems; t++)
+    if (dig[t] < kDigits) {
+      const uint32_t pos = sm.bexcl[dig[t]] + sm.whist[warp][dig[t]] + rank[t];
+      sm.keys[pos] = k[t];
+      sm.vals[pos] = v[t];
+    }
+  __syncthreads();
+  const uint64_t valid = n - base < uint64_t(kSortTile) ? n - base : kSortTile;
+  for (int pos = threadIdx.x; pos < int(valid); pos += kSortThreads) {
+    const uint64_t kk = sm.keys[pos];
+    const uint32_t d = uint32_t((kk >> shift) & (kDigits - 1));
+    const uint64_t dst = sm.gofs[d] + (pos - sm.bexcl[d]);
+    keys_out[dst] = kk;
+    vals_out[dst] = sm.vals[pos];
+  }
+}
+
+}  // namespace
+
+void radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
+                      uint32_t *vals_alt, uint64_t n, int key_bits,
+                      DevBuf &scratch, cudaStream_t st, int *passes_run)
+{
+  if (passes_run) *passes_run = 0;
+  if (n <= 1 || key_bits <= 0) return;
+  const int passes = (key_bits + kRadixBits - 1) / kRadixBits;
+  const uint64_t tiles = (n + kSortTile - 1) / kSortTile;
+
+  // scratch: hist (passes*256 u32) | offsets (passes*256 u64) | ticket |
+  // look-back state (tiles*256 u64)
+  const size_t hist_bytes = size_t(kMaxPasses) * kDigits * 4;
+  const size_t offs_bytes = size_t(kMaxPasses) * kDigits * 8;
+  const size_t state_bytes = size_t(tiles) * kDigits * 8;
+  scratch.reserve(hist_bytes + offs_bytes + 256 + state_bytes);
+  auto *base = scratch.as<unsigned char>();
+  auto *hist = reinterpret_cast<unsigned int *>(base);
+  auto *offs = reinterpret_cast<unsigned long long *>(base + hist_bytes);
+  auto *ticket = reinterpret_cast<unsigned int *>(base + hist_bytes + offs_bytes);
+  auto *state = reinterpret_cast<unsigned long long *>(base + hist_bytes +
+                                                       offs_bytes + 256);
+
+  AMRX_CUDA(cudaMemsetAsync(hist, 0, hist_bytes, st));
+  const int hgrid = int(std::min<uint64_t>((n + 1023) / 1024,
+                                           uint64_t(device_sm_count()) * 8));
+  histogram_kernel<<<std::max(1, hgrid), 256, 0, st>>>(keys, n, passes, hist);
+  AMRX_LAUNCH_CHECK();
+  digit_offsets_kernel<<<1, 32 * kMaxPasses, 0, st>>>(hist, passes, offs);
+  AMRX_LAUNCH_CHECK();
+
+  // passes whose digit is constant over all keys permute nothing: skip
+  std::vector<unsigned int> h(size_t(passes) * kDigits);
+  AMRX_CUDA(cudaMemcpyAsync(h.data(), hist, h.size() * 4,
+                            cudaMemcpyDeviceToHost, st));
+  AMRX_CUDA(cudaStreamSynchronize(st));
+
+  static bool attr_set = false;
+  const size_t smem = sizeof(PassSmem);
+  if (!attr_set) {
+    AMRX_CUDA(cudaFuncSetAttribute(onesweep_pass_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(smem)));
+    attr_set = true;
+  }
+  uint64_t *kin = keys, *kout = keys_alt;
+  uint32_t *vin = vals, *vout = vals_alt;
+  int run = 0;
+  for (int p = 0; p < passes; p++) {
+    bool trivial = false;
+    for (int d = 0; d < kDigits; d++)
+      if (h[size_t(p) * kDigits + d] == n) trivial = true;
+    if (trivial) continue;
+    AMRX_CUDA(cudaMemsetAsync(state, 0, state_bytes, st));
+    AMRX_CUDA(cudaMemsetAsync(ticket, 0, 4, st));
+    onesweep_pass_kernel<<<unsigned(tiles), kSortThreads, smem, st>>>(
+      kin, vin, kout, vout, n, p * kRadixBits, offs + size_t(p) * kDigits,
+      state, ticket);
+    AMRX_LAUNCH_CHECK();
+    std::swap(kin, kout);
+    std::swap(vin, vout);
+    run++;
+  }
+  if (kin != keys) {
+    AMRX_CUDA(cudaMemcpyAsync(keys, kin, n * 8, cudaMemcpyDeviceToDevice, st));
+    AMRX_CUDA(cudaMemcpyAsync(vals, vin, n * 4, cudaMemcpyDeviceToDevice, st));
+  }
+  if (passes_run) *passes_run = run;
+}
+
+}  // namespace amrx
