@@ -1,0 +1,439 @@
+"""Benchmark: dual cells/s and iso triangles/s of the full hot path on the
+626M-cell C4 soup (BASELINE.json configs[3], the configuration the metric is
+quoted on; it fits one B200).
+
+One step = the reference's build_index + extract_isosurface passes 1+2 on
+one batch of synthetic input: pack (i,j,k,level) into 64-bit keys, radix
+sort, gather scalars, build the search directory, then the fused dual
+enumeration + ownership rules + marching cubes + ordered emission kernel.
+`value` times that step with the unsorted cell soup already resident in HBM;
+`e2e` times the same public call with pinned HOST input and output buffers
+(H2D of 24 B/cell and D2H of the 72 B/triangle soup inside the timed region).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl amrx|reference]
+
+Multi-GPU (torchrun, one rank per GPU, NCCL): rank 0 builds the index, the
+sorted keys + scalars are broadcast over NVLink, every rank adopts them and
+extracts its contiguous cell range; an all-gather of per-rank triangle
+counts gives global output offsets.  Strong scaling: the 626M cells are
+fixed, per-rank work shrinks with N.
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref, the unmodified amriso sources) on a bounded sample of the same
+workload with all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "dual cells/sec & iso triangles/sec (626M-cell synthetic AMR), 1/2/4/8 B200"
+HBM_FALLBACK = 6650.0
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region"""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- workload
+def make_workload(cfg_name, device):
+    """device-resident synthetic input: (cells int32[n,4], scalars f64[n]) torch CUDA"""
+    from paper_2004_08475_b200 import synth
+    cfg = synth.CONFIGS[cfg_name]
+    if cfg["kind"] == "bricks":
+        b3 = cfg["bricks"]
+        ds = synth.bricks(b3, seed=cfg["seed"], shuffle=cfg["shuffle"], knobs=synth.C4_KNOBS,
+                          holes=synth.body_holes(b3))
+        return ds.cells, ds.scalars, dict(bricks=list(b3), level_cells=ds.level_cells)
+    import torch
+    gen = getattr(synth, cfg["kind"])
+    cells, scal = gen(*cfg["args"])
+    return (torch.from_numpy(cells).to(device), torch.from_numpy(scal).to(device), {})
+
+
+def iso_of(cfg_name):
+    from paper_2004_08475_b200 import synth
+    iso = synth.CONFIGS[cfg_name]["iso"]
+    return synth.C4_ISO if iso is None else iso
+
+
+# ---------------------------------------------------------------- amrx arm
+def run_amrx(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2004_08475_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    iso = iso_of(args.config)
+
+    # every rank generates the same input deterministically (the "batch")
+    cells, scal, meta = make_workload(args.config, dev)
+    n = cells.shape[0]
+    stream = torch.cuda.Stream(device=dev)
+    sh = stream.cuda_stream
+
+    # output buffer sized from a first (untimed) run
+    idx = P.build_index(cells, scal, device=local, stream=sh)
+    probe = P.extract_isosurface(idx, P.IsoParams(iso=iso))
+    ntri_full = len(probe.fat)
+    duals_full = probe.stats.duals_accepted
+    geometry = idx.geometry()
+    idx.close()
+    del probe
+    cap = int(ntri_full * 1.05) + 1024
+    out = torch.empty((cap, 9), dtype=torch.float64, device=dev)
+
+    def step_single():
+        ix = P.build_index(cells, scal, device=local, stream=sh)
+        r = P.extract_isosurface(ix, P.IsoParams(iso=iso), out=out)
+        ingest = ix.info.seconds_ingest
+        ix.close()
+        return r.stats, ingest, len(r.fat)
+
+    keys_buf = scal_buf = None
+    if world > 1:
+        keys_buf = torch.empty(n + 256, dtype=torch.int64, device=dev)
+        scal_buf = torch.empty(n, dtype=torch.float64, device=dev)
+
+    def step_multi():
+        # rank 0 sorts; NCCL broadcast of the sorted keys + scalars; each
+        # rank adopts them and extracts its own contiguous cell range
+        ingest = 0.0
+        if rank == 0:
+            ix0 = P.build_index(cells, scal, device=local, stream=sh)
+            kp, sp = ix0.device_arrays()
+            ingest = ix0.info.seconds_ingest
+            P.library()  # noqa
+            torch.cuda.current_stream().wait_stream(stream)
+            _copy_dev(keys_buf, kp, n * 8)
+            _copy_dev(scal_buf, sp, n * 8)
+            ix0.close()
+        dist.broadcast(keys_buf, 0)
+        dist.broadcast(scal_buf, 0)
+        torch.cuda.synchronize()
+        ix = P.adopt_index(keys_buf.data_ptr(), scal_buf.data_ptr(), n, geometry, device=local,
+                           stream=sh)
+        lo, hi = n * rank // world, n * (rank + 1) // world
+        r = P.extract_isosurface(ix, P.IsoParams(iso=iso), cell_range=(lo, hi), out=out)
+        cnt = torch.tensor([len(r.fat)], dtype=torch.int64, device=dev)
+        counts = [torch.zeros_like(cnt) for _ in range(world)]
+        dist.all_gather(counts, cnt)
+        ix.close()
+        return r.stats, ingest, int(sum(c.item() for c in counts))
+
+    step = step_multi if world > 1 else step_single
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    launches0 = P.kernel_launches()
+    kernel_s, ingest_s, tris = [], [], 0
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ev0.record(stream)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            st, ing, nt = step()
+            kernel_s.append(st.seconds_pass1)
+            ingest_s.append(ing)
+            tris = nt
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        wall = time.perf_counter() - t0
+    launches = P.kernel_launches() - launches0
+    # the library syncs its stream per call, so the events on that stream
+    # bracket every step; host-side gaps between calls are included
+    ms_dev = ev0.elapsed_time(ev1) / args.steps
+    ms = max(ms_dev, 1000.0 * wall / args.steps)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+
+    # ---- e2e through the same public call with pinned host buffers
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        hcells = torch.empty(cells.shape, dtype=torch.int32, pin_memory=True)
+        hscal = torch.empty(scal.shape, dtype=torch.float64, pin_memory=True)
+        hcells.copy_(cells)
+        hscal.copy_(scal)
+        hout = torch.empty((cap, 9), dtype=torch.float64, pin_memory=True)
+
+        def step_e2e():
+            ix = P.build_index(hcells, hscal, device=local, stream=sh)
+            r = P.extract_isosurface(ix, P.IsoParams(iso=iso), out=hout)
+            ix.close()
+            return len(r.fat)
+
+        step_e2e()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        t0 = time.perf_counter()
+        k2 = max(1, min(args.steps, 3))
+        for _ in range(k2):
+            nt = step_e2e()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_e2e = max(e0.elapsed_time(e1) / k2, 1000 * (time.perf_counter() - t0) / k2)
+        e2e = {"value": duals_full / (ms_e2e / 1000.0), "unit": "dual cells/s",
+               "ms_per_step": ms_e2e, "triangles_per_s": nt / (ms_e2e / 1000.0),
+               "h2d_bytes_per_step": int(n * 16 + n * 8), "d2h_bytes_per_step": int(nt * 72)}
+        del hcells, hscal, hout
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    hbm, kind = peaks()
+    kern_ms = 1000.0 * statistics.mean(kernel_s)
+    alg_bytes = n * 16 / world + tris * 72 / world
+    achieved = alg_bytes / (kern_ms / 1000.0) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.config)
+        except Exception:
+            traffic = None
+    cpu = None
+    if not args.no_cpu and world == 1:
+        cpu = cpu_baseline(cells, scal, iso, args)
+    line = {
+        "metric": METRIC,
+        "value": duals_full / (ms / 1000.0),
+        "unit": "dual cells/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "int64 keys / f64 scalars",
+        "data": "synthetic (GPU generator: vortex-tube brick AMR, bijective-hash soup order)",
+        "config": {"workload": f"{args.config}: {n} cells, levels 0-3, iso {iso}",
+                   "cells": n, "triangles": tris, "duals": duals_full, "iso": iso,
+                   "parallelism": f"range-partition x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs (24 B/cell) far larger than L2", **meta},
+        "iso_triangles_per_s": tris / (ms / 1000.0),
+        "paper_split_ms": {"X_extract_kernel": kern_ms, "ingest_sort": 1000 * statistics.mean(ingest_s),
+                           "Y_step": ms},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": traffic,
+                     "kernel": "extract_kernel<iso, f64>", "peak_kind": kind,
+                     "alg_bytes_per_launch": alg_bytes},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _copy_dev(dst_tensor, src_ptr, nbytes):
+    from paper_2004_08475_b200 import synth
+    if synth.lib().amrxs_memcpy(dst_tensor.data_ptr(), src_ptr, nbytes):
+        raise RuntimeError("device copy failed")
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_sample(cells, scal, target):
+    """a contiguous sub-box (x slabs) of the workload with ~target cells"""
+    import torch
+    x = cells[:, 0]
+    xs = torch.sort(x).values
+    n = len(xs)
+    lo = int(xs[n // 3].item())
+    # grow the slab range until it holds ~target cells
+    hi_idx = min(n - 1, n // 3 + target)
+    hi = int(xs[hi_idx].item())
+    m = (x >= lo) & (x < hi)
+    return cells[m].cpu().numpy(), scal[m].cpu().numpy(), (lo, hi)
+
+
+def cpu_baseline(cells, scal, iso, args, impl_line=False):
+    """the reference (oracle/_ref) on a bounded sample; reports dual cells/s
+    over build_index (serial sort) + passes 1+2 (all host threads)"""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracles
+    R = oracles.reference()
+    kind = "reference"
+    if R is None:
+        R = oracles.restatement()
+        kind = "port"
+    hc, hs, slab = cpu_sample(cells, scal, args.cpu_sample)
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    h = R.build(hc, hs)
+    t_build = time.perf_counter() - t0
+    if kind == "reference":
+        # warm-up (first run per process is 2-7x slower)
+        R.extract_iso(h, iso, threads)
+        res = R.extract_iso(h, iso, threads)
+        st = res["stats"]
+        t_ext = st["seconds_pass1"] + st["seconds_pass2"]
+        duals = st["duals_accepted"]
+        tris = st["fat_triangle_count"]
+        weld = st["seconds_weld"]
+        cores = threads
+    else:
+        t1 = time.perf_counter()
+        r = R.extract_iso(h, iso)
+        t_ext = time.perf_counter() - t1
+        duals = int(r["counters"][0])
+        tris = len(r["fat"])
+        weld = None
+        cores = 1
+    R.free(h)
+    total = t_build + t_ext
+    return {"value": duals / total, "unit": "dual cells/s", "cores": cores, "kind": kind,
+            "sample": f"{len(hc)} cells (x-slabs [{slab[0]},{slab[1]}) of the workload), "
+                      f"build_index {t_build:.2f} s (serial) + passes 1+2 {t_ext:.2f} s "
+                      f"({cores} threads); weld excluded ({weld})",
+            "triangles_per_s": tris / total, "seconds": total}
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU path on the same workload (rank 0)"""
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    iso = iso_of(args.config)
+    cells, scal, meta = make_workload(args.config, torch.device("cuda"))
+    n = cells.shape[0]
+    vals = []
+    cb = None
+    for _ in range(args.warmup):
+        cpu_baseline(cells, scal, iso, args)
+    for _ in range(args.steps):
+        cb = cpu_baseline(cells, scal, iso, args)
+        vals.append(cb["value"])
+    v = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "dual cells/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * cb["seconds"], "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int32 cells / f64 scalars", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {n} cells (bounded sample per step)", **meta},
+        "cpu_baseline": {**cb, "value": v},
+        "e2e": {"value": v, "unit": "dual cells/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="amrx", choices=["amrx", "reference"])
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--cpu-sample", type=int, default=12_000_000)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_amrx(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -182,6 +182,9 @@ AMRX_API amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range
                              uint64_t cap, uint64_t *count,
                              amrx_stats *stats);
 
+/* kernels this process has launched through the library so far */
+AMRX_API uint64_t amrx_kernel_launches(void);
+
 /* thread-local text of the last error on this thread */
 AMRX_API const char *amrx_last_error(void);
 

@@ -11,7 +11,7 @@ from .amrx import (  # noqa: F401
     CapacityError, CellIndex, CudaError, DualMesh, ExtractionResult,
     ExtractionStats, InternalError, IsoParams, LoadError, UnsupportedError,
     adopt_index, build_index, dual_bases, extract_dual_mesh,
-    extract_isosurface, find_exact, library, snap, try_build_duals,
+    extract_isosurface, find_exact, kernel_launches, library, snap, try_build_duals,
 )
 
 __all__ = [

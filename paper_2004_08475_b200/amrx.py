@@ -133,6 +133,8 @@ def library():
     lib.amrx_last_error.restype = C.c_char_p
     lib.amrx_last_error.argtypes = []
     lib.amrx_version.restype = C.c_char_p
+    lib.amrx_kernel_launches.restype = C.c_uint64
+    lib.amrx_kernel_launches.argtypes = []
     _lib = lib
     return lib
 
@@ -262,7 +264,12 @@ class CellIndex:
             pass
 
 
-def build_index(cells, scalars, device=-1, presorted=False):
+def kernel_launches():
+    """kernels launched through libamrx.so by this process so far"""
+    return int(library().amrx_kernel_launches())
+
+
+def build_index(cells, scalars, device=-1, presorted=False, stream=None):
     """Sort cells (with their scalars) into a device CellIndex
     (build_index, locator.cpp:26-92).  ``cells`` is (n,4) int32 (i,j,k,level),
     numpy or torch (host or CUDA)."""
@@ -277,7 +284,7 @@ def build_index(cells, scalars, device=-1, presorted=False):
         n_s = len(scalars)
     else:
         n_s = scalars.numel()
-    opts = _Opts(device, None, 1 if presorted else 0)
+    opts = _Opts(device, C.c_void_p(stream) if stream else None, 1 if presorted else 0)
     h = C.c_void_p()
     _check(lib.amrx_index_create(_ptr(cells) if n_cells else C.c_void_p(1),
                                  _ptr(scalars) if n_s else C.c_void_p(1),
@@ -285,12 +292,12 @@ def build_index(cells, scalars, device=-1, presorted=False):
     return CellIndex(h.value, lib)
 
 
-def adopt_index(keys_dev_ptr, scalars_dev_ptr, n_cells, geometry, device=-1):
+def adopt_index(keys_dev_ptr, scalars_dev_ptr, n_cells, geometry, device=-1, stream=None):
     """Index over already-sorted packed keys + scalars on this device (the
     multi-GPU replica path: no sort, directory only)."""
     lib = library()
     g = np.ascontiguousarray(geometry, np.int64)
-    opts = _Opts(device, None, 0)
+    opts = _Opts(device, C.c_void_p(stream) if stream else None, 0)
     h = C.c_void_p()
     _check(lib.amrx_index_adopt(C.c_void_p(keys_dev_ptr), C.c_void_p(scalars_dev_ptr),
                                 n_cells, _ptr(g), C.byref(opts), C.byref(h)))

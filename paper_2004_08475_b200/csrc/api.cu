@@ -6,6 +6,7 @@
 #include "internal.h"
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -148,6 +149,12 @@ void DevBuf::release()
   ptr = nullptr;
   bytes = 0;
 }
+
+namespace {
+std::atomic<uint64_t> g_launches{0};
+}
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int device_sm_count()
 {
@@ -349,6 +356,8 @@ extern "C" {
 const char *amrx_last_error(void) { return g_last_error.c_str(); }
 
 const char *amrx_version(void) { return "amrx 0.1 (sm_100a)"; }
+
+uint64_t amrx_kernel_launches(void) { return g_launches.load(); }
 
 amrx_status amrx_index_create(const int32_t *cells4, const double *scalars,
                               uint64_t n_cells, uint64_t n_scalars,

@@ -509,8 +509,7 @@ find_exact_kernel(const SearchCtx s, const KeyGeom g,
   __shared__ uint64_t win[kWarps][kWin];
   const int warp = threadIdx.x >> 5;
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x - (threadIdx.x & 31) +
-                       (threadIdx.x & ~31u);
+  for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u);
        base < n; base += stride) {
     const uint64_t r = base + (threadIdx.x & 31);
     const bool in = r < n;
@@ -519,7 +518,8 @@ find_exact_kernel(const SearchCtx s, const KeyGeom g,
     bool v[1];
     int64_t o[1] = {-1};
     // find_exact matches the full key: the anchor must be the stored one
-    v[0] = in && anchor_mask(cc.x, cc.w) == cc.x &&
+    v[0] = in && cc.w >= 0 && cc.w <= kMaxLevel &&
+           anchor_mask(cc.x, cc.w) == cc.x &&
            anchor_mask(cc.y, cc.w) == cc.y &&
            anchor_mask(cc.z, cc.w) == cc.z &&
            query_key(g, cc.x, cc.y, cc.z, cc.w, q[0]);

@@ -25,7 +25,13 @@ struct Error {
       ::amrx::throw_cuda(amrx_e_, #call, __FILE__, __LINE__);            \
   } while (0)
 
-#define AMRX_LAUNCH_CHECK() AMRX_CUDA(cudaGetLastError())
+void note_launch();
+
+#define AMRX_LAUNCH_CHECK()                                              \
+  do {                                                                   \
+    ::amrx::note_launch();                                               \
+    AMRX_CUDA(cudaGetLastError());                                       \
+  } while (0)
 
 /// device allocation with RAII; grows on demand
 struct DevBuf {

@@ -1,0 +1,144 @@
+"""Synthetic AMR inputs for tests and the benchmark (libamrx_synth.so).
+
+Small configurations reproduce the reference's own generators record for
+record (host C++, same libstdc++ <random>): ``octree_sphere`` = gen_octree
+with a sphere field (proj/src/synth.cpp:141-181), ``uniform_sphere`` =
+gen_uniform (synth.cpp:122-137), ``slots`` = random_slot_dataset
+(proj/tests/fixtures.hpp:38-69).  They return the generator's record order,
+i.e. the cell list a caller hands to build_index.
+
+``bricks`` is the GPU generator for the large configurations (SURVEY §8(d)
+C4/C5): a 4-level block-structured AMR around Gaussian vortex tubes with
+"aircraft body" holes and a vorticity-magnitude scalar, optionally in a
+bijective-hash "soup" order.  Its arrays stay on the device.
+
+Config registry: ``CONFIGS`` names every BASELINE.json configuration.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libamrx_synth.so")
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `make -C {_HERE}`")
+        L = C.CDLL(LIB_PATH)
+        P, U64, D, I32 = C.c_void_p, C.c_uint64, C.c_double, C.c_int32
+        L.amrxs_octree_sphere.restype = P
+        L.amrxs_octree_sphere.argtypes = [I32, D, D, D, D, D]
+        L.amrxs_uniform_sphere.restype = P
+        L.amrxs_uniform_sphere.argtypes = [I32, D, D, D, D]
+        L.amrxs_slots.restype = P
+        L.amrxs_slots.argtypes = [C.c_uint32, C.c_int, C.c_int, D]
+        L.amrxs_size.restype = U64
+        L.amrxs_size.argtypes = [P]
+        L.amrxs_get.argtypes = [P, P, P]
+        L.amrxs_free.argtypes = [P]
+        L.amrxs_bricks.restype = C.c_int
+        L.amrxs_bricks.argtypes = [P, U64, C.c_int, P, C.c_int, P, P, P, P, P]
+        L.amrxs_device_free.argtypes = [P]
+        L.amrxs_memcpy.restype = C.c_int
+        L.amrxs_memcpy.argtypes = [P, P, U64]
+        _lib = L
+    return _lib
+
+
+def _take(h):
+    L = lib()
+    n = L.amrxs_size(h)
+    cells = np.empty((n, 4), np.int32)
+    scal = np.empty(n, np.float64)
+    L.amrxs_get(h, cells.ctypes.data_as(C.c_void_p), scal.ctypes.data_as(C.c_void_p))
+    L.amrxs_free(h)
+    return cells, scal
+
+
+def octree_sphere(depth, centre, radius, threshold):
+    return _take(lib().amrxs_octree_sphere(depth, *map(float, centre), float(radius),
+                                           float(threshold)))
+
+
+def uniform_sphere(n, centre, radius):
+    return _take(lib().amrxs_uniform_sphere(n, *map(float, centre), float(radius)))
+
+
+def slots(seed, n_slots, max_level, hole_prob=0.15):
+    return _take(lib().amrxs_slots(seed, n_slots, max_level, hole_prob))
+
+
+class DeviceDataset:
+    """cells (n,4) int32 and scalars (n,) f64 as torch CUDA tensors."""
+
+    def __init__(self, cells, scalars, level_cells, ptrs):
+        self.cells = cells
+        self.scalars = scalars
+        self.level_cells = level_cells
+        self._ptrs = ptrs
+
+    def __len__(self):
+        return self.cells.shape[0]
+
+
+def bricks(bricks3, seed=1, shuffle=True, knobs=None, holes=()):
+    """Generate on the current CUDA device; returns torch tensors that own
+    copies of the generated arrays (the raw buffers are freed)."""
+    import torch
+    L = lib()
+    if knobs is None:
+        knobs = C4_KNOBS
+    b3 = np.asarray(bricks3, np.int32)
+    k8 = np.asarray(knobs, np.float64)
+    ho = np.ascontiguousarray(np.asarray(holes, np.int64).reshape(-1, 6))
+    cp, sp, n = C.c_void_p(), C.c_void_p(), C.c_uint64()
+    lc = np.zeros(4, np.uint64)
+    rc = L.amrxs_bricks(b3.ctypes.data_as(C.c_void_p), seed, int(shuffle),
+                        k8.ctypes.data_as(C.c_void_p), len(ho),
+                        ho.ctypes.data_as(C.c_void_p) if len(ho) else None,
+                        C.byref(cp), C.byref(sp), C.byref(n),
+                        lc.ctypes.data_as(C.c_void_p))
+    if rc != 0:
+        raise RuntimeError(f"amrxs_bricks failed ({rc})")
+    nn = n.value
+    cells = torch.empty((nn, 4), dtype=torch.int32, device="cuda")
+    scal = torch.empty(nn, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    if L.amrxs_memcpy(C.c_void_p(cells.data_ptr()), cp, nn * 16) or \
+            L.amrxs_memcpy(C.c_void_p(scal.data_ptr()), sp, nn * 8):
+        raise RuntimeError("amrxs_memcpy failed")
+    L.amrxs_device_free(cp)
+    L.amrxs_device_free(sp)
+    return DeviceDataset(cells, scal, [int(x) for x in lc], None)
+
+
+# knobs: ntubes, core radius min, max, indicator reach (core radii), level
+# thresholds t0 t1 t2, noise amplitude
+C4_KNOBS = [14, 24.0, 48.0, 1.41, 0.30, 0.08, 0.01, 8.0]
+C4_ISO = 4.0
+
+# "aircraft body": fuselage + wing boxes (finest units), scaled to the domain
+def body_holes(bricks3):
+    X, Y, Z = (8 * b for b in bricks3)
+    fus = [int(0.10 * X), int(0.46 * Y), int(0.46 * Z), int(0.55 * X), int(0.54 * Y), int(0.54 * Z)]
+    wing = [int(0.28 * X), int(0.20 * Y), int(0.49 * Z), int(0.38 * X), int(0.80 * Y), int(0.51 * Z)]
+    return [fus, wing]
+
+
+CONFIGS = {
+    # C1: SURVEY §8(d): gen_octree(6, sphere((25,27.5,30), 20), 3.2), iso 0
+    "c1": dict(kind="octree_sphere", args=(6, (25.0, 27.5, 30.0), 20.0, 3.2), iso=0.0),
+    # C2: random_slot_dataset(mt19937(seed), 23, 4, 0.15), iso 0.1
+    "c2": dict(kind="slots", args=(2026, 23, 4, 0.15), iso=0.1),
+    # C4: 626M-cell 4-level soup (bricks 512 x 256 x 256 -> tuned knobs)
+    "c4": dict(kind="bricks", bricks=(512, 256, 256), seed=1, shuffle=True, iso=None),
+    # C5: ~250M-cell mixed-level AMR, dual mesh only
+    "c5": dict(kind="bricks", bricks=(384, 192, 192), seed=5, shuffle=False, iso=None),
+}
