@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -83,7 +84,7 @@ struct DevIn {
       ptr = p;
       return;
     }
-    stage.reserve(count * sizeof(T));
+    stage.reserve(count * sizeof(T), st);
     AMRX_CUDA(cudaMemcpyAsync(stage.ptr, p, count * sizeof(T),
                               cudaMemcpyHostToDevice, st));
     ptr = stage.as<T>();
@@ -97,7 +98,7 @@ struct DevOut {
   size_t count = 0;
   bool staged = false;
   DevBuf stage;
-  DevOut(T *p, size_t n) : user(p), count(n)
+  DevOut(T *p, size_t n, cudaStream_t st) : user(p), count(n)
   {
     if (!p || n == 0) return;
     if (is_device_ptr(p)) {
@@ -105,7 +106,7 @@ struct DevOut {
       return;
     }
     staged = true;
-    stage.reserve(n * sizeof(T));
+    stage.reserve(n * sizeof(T), st);
     ptr = stage.as<T>();
   }
   void finish(cudaStream_t st)
@@ -134,20 +135,34 @@ struct DevOut {
 
 DevBuf::~DevBuf() { release(); }
 
-void DevBuf::reserve(size_t n)
+void DevBuf::reserve(size_t n, cudaStream_t st)
 {
   if (n <= bytes && ptr) return;
   release();
   if (n == 0) n = 16;
-  AMRX_CUDA(cudaMalloc(&ptr, n));
+  stream = st;
+  AMRX_CUDA(cudaMallocAsync(&ptr, n, st));
   bytes = n;
 }
 
 void DevBuf::release()
 {
-  if (ptr) cudaFree(ptr);
+  if (ptr) cudaFreeAsync(ptr, stream);
   ptr = nullptr;
   bytes = 0;
+}
+
+void enable_pool_caching(int device)
+{
+  static std::mutex mu;
+  static bool done[64] = {false};
+  std::lock_guard<std::mutex> lock(mu);
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  AMRX_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t keep = ~0ull;
+  AMRX_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  done[device] = true;
 }
 
 namespace {
@@ -179,7 +194,8 @@ struct amrx_index {
   uint64_t n = 0;
   KeyGeom g{};
   int64_t bounds_hi[3] = {0, 0, 0};
-  DevBuf keys, scal, dir, scratch, scratch2;
+  DevBuf keys, scal, dir, lmap, scratch;
+  ExtractScratch xs;
   amrx_index_info info{};
   // last extraction kept on the device for the count-then-copy pattern
   struct Cached {
@@ -201,6 +217,9 @@ struct amrx_index {
     s.dir = dir.as<uint32_t>();
     s.n = n;
     s.dir_shift = g.dir_shift;
+    s.shift = g.shift;
+    s.lmask = (uint64_t(1) << g.lbits) - 1;
+    s.dbg = nullptr;
     return s;
   }
 };
@@ -258,6 +277,17 @@ KeyGeom make_geometry(const int64_t mn[3], const int64_t mx[3],
   const int want = std::min(30, std::max(10, bit_width(n) + 1));
   g.dir_bits = std::min(g.total, want);
   g.dir_shift = g.total - g.dir_bits;
+  // block level map at the coarsest level's granularity, if it is small
+  g.map_shift = hi_level;
+  double blocks = 1;
+  for (int a = 0; a < 3; a++) {
+    g.map_base[a] = mn[a] >> hi_level;  // arithmetic shift: floor
+    g.map_dim[a] = (mx[a] >> hi_level) - g.map_base[a] + 1;
+    blocks *= double(g.map_dim[a]);
+  }
+  const double budget = std::max(double(1 << 26), 4.0 * double(n));
+  static const bool disabled = std::getenv("AMRX_NO_LEVEL_MAP") != nullptr;
+  g.map_on = !disabled && g.nlevels <= 8 && blocks <= budget;
   return g;
 }
 
@@ -291,6 +321,7 @@ void setup_stream(amrx_index *ix, const amrx_index_opts *opts)
   }
   ix->device = dev;
   AMRX_CUDA(cudaSetDevice(dev));
+  enable_pool_caching(dev);
   if (opts && opts->stream) {
     ix->stream = static_cast<cudaStream_t>(opts->stream);
   } else {
@@ -303,9 +334,17 @@ void setup_stream(amrx_index *ix, const amrx_index_opts *opts)
 void finalize_index(amrx_index *ix)
 {
   pad_keys(ix->keys.as<uint64_t>(), ix->n, ix->stream);
-  ix->dir.reserve(((uint64_t(1) << ix->g.dir_bits) + 1) * sizeof(uint32_t));
+  ix->dir.reserve(((uint64_t(1) << ix->g.dir_bits) + 1) * sizeof(uint32_t), ix->stream);
   build_directory(ix->keys.as<uint64_t>(), ix->n, ix->g, ix->dir.as<uint32_t>(),
                   ix->scratch, ix->stream);
+  if (ix->g.map_on) {
+    const uint64_t bytes =
+      ((uint64_t(ix->g.map_dim[0]) * uint64_t(ix->g.map_dim[1]) *
+          uint64_t(ix->g.map_dim[2]) + 3) & ~uint64_t(3));
+    ix->lmap.reserve(bytes, ix->stream);
+    build_level_map(ix->keys.as<uint64_t>(), ix->n, ix->g, ix->lmap.as<uint8_t>(),
+                    bytes, ix->stream);
+  }
 }
 
 void check_range(const amrx_index *ix, const amrx_range *range, uint64_t &b,
@@ -329,7 +368,7 @@ void fill_stats(amrx_stats *st, const ExtractResult &r, uint64_t cells)
   st->fat_triangle_count = r.tris_written;
   st->dual_count = r.duals;
   st->seconds_pass1 = r.ms / 1000.0;
-  st->seconds_pass2 = 0;
+  st->seconds_pass2 = r.ms2 / 1000.0;
   st->kernel_launches = r.launches;
 }
 
@@ -409,15 +448,15 @@ amrx_status amrx_index_create(const int32_t *cells4, const double *scalars,
     ix->g = make_geometry(mn, mx, pre.level_mask, n);
     for (int a = 0; a < 3; a++) ix->bounds_hi[a] = pre.hi[a];
 
-    ix->keys.reserve((n + kKeyPad) * sizeof(uint64_t));
+    ix->keys.reserve((n + kKeyPad) * sizeof(uint64_t), st);
     DevBuf idx, keys_alt, idx_alt;
-    idx.reserve(n * sizeof(uint32_t));
+    idx.reserve(n * sizeof(uint32_t), st);
     ingest_pack(cells.ptr, n, ix->g, ix->keys.as<uint64_t>(), idx.as<uint32_t>(), st);
     cells.stage.release();
 
     uint64_t desc = 0, eq = 0;
     ingest_order_check(ix->keys.as<uint64_t>(), n, ix->scratch, &desc, &eq, st);
-    ix->scal.reserve(n * sizeof(double));
+    ix->scal.reserve(n * sizeof(double), st);
     if (desc == 0) {
       // already in (i,j,k,level) order; stable ties mean identity
       AMRX_CUDA(cudaMemcpyAsync(ix->scal.ptr, sc.ptr, n * sizeof(double),
@@ -425,8 +464,8 @@ amrx_status amrx_index_create(const int32_t *cells4, const double *scalars,
     } else {
       if (opts && (opts->flags & AMRX_FLAG_PRESORTED))
         fail(AMRX_ERR_INVALID_ARG, "input flagged presorted is not sorted");
-      keys_alt.reserve(n * sizeof(uint64_t));
-      idx_alt.reserve(n * sizeof(uint32_t));
+      keys_alt.reserve(n * sizeof(uint64_t), st);
+      idx_alt.reserve(n * sizeof(uint32_t), st);
       int passes = 0;
       radix_sort_pairs(ix->keys.as<uint64_t>(), idx.as<uint32_t>(),
                        keys_alt.as<uint64_t>(), idx_alt.as<uint32_t>(), n,
@@ -460,10 +499,16 @@ amrx_status amrx_index_destroy(amrx_index *index)
       index->keys.release();
       index->scal.release();
       index->dir.release();
+      index->lmap.release();
       index->scratch.release();
-      index->scratch2.release();
+      index->xs.ctl.release();
+      index->xs.tiles.release();
+      index->xs.stage_a.release();
+      index->xs.stage_b.release();
+      index->xs.scan.release();
       index->out_a.release();
       index->out_b.release();
+      cudaStreamSynchronize(index->stream);
       if (index->own_stream) cudaStreamDestroy(index->stream);
     }
     delete index;
@@ -487,7 +532,7 @@ amrx_status amrx_index_download(const amrx_index *cindex, int32_t *cells4,
     DeviceGuard dg(index->device);
     cudaStream_t st = index->stream;
     if (cells4) {
-      DevOut<int4> o(reinterpret_cast<int4 *>(cells4), index->n);
+      DevOut<int4> o(reinterpret_cast<int4 *>(cells4), index->n, st);
       unpack_cells(index->keys.as<uint64_t>(), index->n, index->g, o.ptr, st);
       o.finish(st);
       AMRX_CUDA(cudaStreamSynchronize(st));
@@ -548,8 +593,8 @@ amrx_status amrx_index_adopt(const void *keys_dev, const double *scalars_dev,
     AMRX_CUDA(cudaEventCreate(&e0));
     AMRX_CUDA(cudaEventCreate(&e1));
     AMRX_CUDA(cudaEventRecord(e0, st));
-    ix->keys.reserve((n_cells + kKeyPad) * sizeof(uint64_t));
-    ix->scal.reserve(n_cells * sizeof(double));
+    ix->keys.reserve((n_cells + kKeyPad) * sizeof(uint64_t), st);
+    ix->scal.reserve(n_cells * sizeof(double), st);
     AMRX_CUDA(cudaMemcpyAsync(ix->keys.ptr, keys_dev, n_cells * 8,
                               cudaMemcpyDefault, st));
     AMRX_CUDA(cudaMemcpyAsync(ix->scal.ptr, scalars_dev, n_cells * 8,
@@ -575,7 +620,7 @@ amrx_status amrx_find_exact(amrx_index *index, const int32_t *cells4,
     DeviceGuard dg(index->device);
     cudaStream_t st = index->stream;
     DevIn<int4> in(reinterpret_cast<const int4 *>(cells4), n, st);
-    DevOut<int64_t> o(out_ids, n);
+    DevOut<int64_t> o(out_ids, n, st);
     run_find_exact(index->ctx(), index->g, in.ptr, n, o.ptr, st);
     o.finish(st);
     AMRX_CUDA(cudaStreamSynchronize(st));
@@ -593,7 +638,7 @@ amrx_status amrx_snap(amrx_index *index, const int64_t *points3,
     cudaStream_t st = index->stream;
     DevIn<int64_t> p(points3, 3 * n, st);
     DevIn<int32_t> h(hints, hints ? n : 0, st);
-    DevOut<int64_t> o(out_ids, n);
+    DevOut<int64_t> o(out_ids, n, st);
     run_snap(index->ctx(), index->g, p.ptr, h.ptr, hint_all, n, o.ptr, st);
     o.finish(st);
     AMRX_CUDA(cudaStreamSynchronize(st));
@@ -610,8 +655,8 @@ amrx_status amrx_try_build_duals(amrx_index *index, const uint64_t *tasks,
     DeviceGuard dg(index->device);
     cudaStream_t st = index->stream;
     DevIn<uint64_t> t(tasks, n, st);
-    DevOut<uint8_t> r(out_reject, n);
-    DevOut<uint32_t> c(out_corners8, out_corners8 ? 8 * n : 0);
+    DevOut<uint8_t> r(out_reject, n, st);
+    DevOut<uint32_t> c(out_corners8, out_corners8 ? 8 * n : 0, st);
     run_try_build(index->ctx(), index->g, t.ptr, n, r.ptr, c.ptr, st);
     r.finish(st);
     c.finish(st);
@@ -640,6 +685,7 @@ amrx_status amrx_extract_dual(amrx_index *index, const amrx_range *range,
     rq.s = index->ctx();
     rq.g = index->g;
     rq.scal = index->scal.as<double>();
+    rq.lmap = index->lmap.as<uint8_t>();
     rq.cell_begin = b;
     rq.cell_end = e;
     rq.emit_dual = true;
@@ -647,7 +693,7 @@ amrx_status amrx_extract_dual(amrx_index *index, const amrx_range *range,
       rq.corners = corners8;
       rq.tasks = task_ids;
       rq.dual_cap = cap;
-      const ExtractResult r = run_extract(rq, index->scratch, st);
+      const ExtractResult r = run_extract(rq, index->xs, st);
       check_result(r, cells, false);
       fill_stats(stats, r, cells);
       *count = r.duals;
@@ -662,12 +708,12 @@ amrx_status amrx_extract_dual(amrx_index *index, const amrx_range *range,
     if (!hit) {
       uint64_t arena = std::max<uint64_t>(1024, cells + cells / 4);
       for (int attempt = 0; attempt < 2; attempt++) {
-        index->out_a.reserve(arena * 32);
-        index->out_b.reserve(arena * 8);
+        index->out_a.reserve(arena * 32, st);
+        index->out_b.reserve(arena * 8, st);
         rq.corners = index->out_a.as<uint32_t>();
         rq.tasks = index->out_b.as<uint64_t>();
         rq.dual_cap = arena;
-        const ExtractResult r = run_extract(rq, index->scratch, st);
+        const ExtractResult r = run_extract(rq, index->xs, st);
         check_result(r, cells, false);
         if (r.duals <= arena) {
           C.valid = true;
@@ -717,6 +763,7 @@ amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range,
     rq.s = index->ctx();
     rq.g = index->g;
     rq.scal = index->scal.as<double>();
+    rq.lmap = index->lmap.as<uint8_t>();
     rq.cell_begin = b;
     rq.cell_end = e;
     rq.emit_tri = true;
@@ -730,7 +777,7 @@ amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range,
     if (dev_out) {
       rq.xyz = xyz9;
       rq.tri_cap = cap;
-      const ExtractResult r = run_extract(rq, index->scratch, st);
+      const ExtractResult r = run_extract(rq, index->xs, st);
       check_result(r, cells, true);
       fill_stats(stats, r, cells);
       *count = r.tris_written;
@@ -746,10 +793,10 @@ amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range,
     if (!hit) {
       uint64_t arena = std::max<uint64_t>(4096, cells / 2);
       for (int attempt = 0; attempt < 2; attempt++) {
-        index->out_a.reserve(arena * tri_bytes);
+        index->out_a.reserve(arena * tri_bytes, st);
         rq.xyz = index->out_a.ptr;
         rq.tri_cap = arena;
-        const ExtractResult r = run_extract(rq, index->scratch, st);
+        const ExtractResult r = run_extract(rq, index->xs, st);
         check_result(r, cells, true);
         if (r.tris_written <= arena) {
           C.valid = true;

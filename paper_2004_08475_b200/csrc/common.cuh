@@ -32,7 +32,32 @@ struct KeyGeom {
   uint32_t level_mask;  // bit l set iff level l present
   int32_t nlevels;
   int8_t levels[32];    // present levels, finest first (locator.cpp:85-89)
+  // block level map: one byte per 2^map_shift-aligned block (map_shift =
+  // coarsest level present), bit b set iff some cell of level levels[b]
+  // lies in the block.  A cell containing point p lies in p's block, so
+  // only those levels can hit.  map_on = 0 when > 8 levels or too large.
+  int32_t map_on;
+  int32_t map_shift;
+  int64_t map_base[3];  // block index of the lowest anchor per axis
+  int64_t map_dim[3];   // blocks per axis
 };
+
+/// candidate-level bits (index into g.levels) for point p from the map
+__device__ __forceinline__ uint32_t block_levels(const KeyGeom &g,
+                                                 const uint8_t *map,
+                                                 int64_t px, int64_t py,
+                                                 int64_t pz)
+{
+  if (!g.map_on) return (1u << g.nlevels) - 1;
+  const int64_t bx = (px >> g.map_shift) - g.map_base[0];
+  const int64_t by = (py >> g.map_shift) - g.map_base[1];
+  const int64_t bz = (pz >> g.map_shift) - g.map_base[2];
+  if (bx < 0 || by < 0 || bz < 0 || bx >= g.map_dim[0] || by >= g.map_dim[1] ||
+      bz >= g.map_dim[2])
+    return 0;
+  return __ldg(map + (uint64_t(bz) * uint64_t(g.map_dim[1]) + uint64_t(by)) *
+                       uint64_t(g.map_dim[0]) + uint64_t(bx));
+}
 
 __host__ __device__ inline int64_t anchor_mask(int64_t x, int32_t level)
 {
@@ -168,7 +193,84 @@ struct SearchCtx {
   const uint32_t *dir;   // 2^dir_bits + 1 bucket starts
   uint64_t n;
   int32_t dir_shift;
+  int32_t shift;         // finest level present (level field offset)
+  uint64_t lmask;        // mask of the level field
+  unsigned long long *dbg;  // optional event counters (AMRX_DEBUG_COUNTERS)
 };
+
+/// debug event counters, one atomic per warp-level event, lane 0 only
+enum DbgEvent {
+  kDbgTiles = 0, kDbgColumns, kDbgFindCalls, kDbgFindRounds, kDbgNarrow,
+  kDbgFallback, kDbgCoarser, kDbgMcTab, kDbgQueries, kDbgWinResolved,
+  kDbgCount
+};
+
+// counters are compiled in only for a diagnostic build (make DBG=1): the
+// atomics otherwise bloat the hot loop past the instruction cache
+#ifndef AMRX_DBG
+#define AMRX_DBG 0
+#endif
+
+__device__ __forceinline__ void dbg_add(const SearchCtx &s, int ev,
+                                        unsigned long long v = 1)
+{
+#if AMRX_DBG
+  if (s.dbg && (threadIdx.x & 31) == 0) atomicAdd(s.dbg + ev, v);
+#endif
+}
+
+/*! global-memory path of warp_find for one query: lower_bound over the
+    bucket range [lo, hi), then (finer) the run of same-anchor keys before
+    it.  Returns the CellId or -1; level receives the hit's level. */
+static __device__ __noinline__ int64_t find_in_bucket(const SearchCtx &s, uint64_t lo,
+                                               uint64_t hi, uint64_t q,
+                                               bool finer, int &level)
+{
+  const uint64_t p = global_lower_bound(s.keys, lo, hi, q);
+  int64_t res = -1;
+  int rl = 0;
+  if (p < hi && ldg_u64(s.keys + p) == q) {
+    res = int64_t(p);
+    rl = int(q & s.lmask);
+  } else if (finer) {
+    const uint64_t anchor = q & ~s.lmask;
+    uint64_t x = p;
+    while (x > lo && (ldg_u64(s.keys + x - 1) & ~s.lmask) == anchor) x--;
+    if (x < p) {
+      res = int64_t(x);
+      rl = int(ldg_u64(s.keys + x) & s.lmask);
+    }
+  }
+  level = rl + s.shift;
+  return res;
+}
+
+/// lower_bound of q in win[from, cnt), galloping from `from`
+__device__ __forceinline__ int gallop_lower_bound(const uint64_t *win, int from,
+                                                  int cnt, uint64_t q)
+{
+  int lo = from, n;
+  if (from == 0) {
+    n = cnt;  // first query of the window: plain binary search
+  } else {
+    int step = 1;
+    while (lo + step - 1 < cnt && win[lo + step - 1] < q) {
+      lo += step;
+      step <<= 1;
+    }
+    n = (lo + step - 1 < cnt ? lo + step - 1 : cnt) - lo;
+  }
+  while (n > 0) {
+    const int half = n >> 1;
+    if (win[lo + half] < q) {
+      lo += half + 1;
+      n -= half + 1;
+    } else {
+      n = half;
+    }
+  }
+  return lo;
+}
 
 /*! Warp-cooperative exact lookup of up to NQ keys per lane (find_exact,
     locator.cpp:94-101: the FIRST position holding the key, or miss).
@@ -182,23 +284,36 @@ struct SearchCtx {
     3. Every pending lane resolves each query it can prove from the window
        (found, or absent because the window brackets it); the rest go
        round again with the next leader, then fall back to a per-lane
-       binary search of their own bucket.
+       binary search of their own bucket.  A lane's queries are searched in
+       order, galloping from the previous one's position (the callers pass
+       them ascending).
 
-    out[q] = CellId, -1 = absent.  Inactive queries (valid[q] false) are
-    left untouched.  All 32 lanes must call this together. */
-template <int NQ>
+    FINER: when the exact key is absent, also report the first stored key
+    with the same anchor and a lower level.  Keys differ from the query
+    only in the level field then, so they sit directly before its
+    lower_bound: for a stencil point p (a multiple of the owner width w)
+    every finer cell containing p is anchored exactly at p, so this is
+    snap's "remaining levels finest first" probe over the finer levels
+    (locator.cpp:125-133) answered from the same window.
+
+    out[t] = CellId or -1, lvl[t] = level field of the hit (FINER hits
+    report their own level).  Inactive queries are left untouched.  All 32
+    lanes must call this together. */
+template <int NQ, bool FINER>
 __device__ void warp_find(const SearchCtx &s, const uint64_t (&q)[NQ],
                           const bool (&valid)[NQ], int64_t (&out)[NQ],
-                          uint64_t *win)
+                          int (&lvl)[NQ], uint64_t *win)
 {
   const uint32_t lane = lane_id();
+  const uint64_t amask = FINER ? ~s.lmask : ~0ull;
   bool any = false;
   uint64_t qmin = ~0ull, qmax = 0;
 #pragma unroll
   for (int t = 0; t < NQ; t++)
     if (valid[t]) {
       any = true;
-      qmin = q[t] < qmin ? q[t] : qmin;
+      const uint64_t lowest = q[t] & amask;  // same anchor, any level
+      qmin = lowest < qmin ? lowest : qmin;
       qmax = q[t] > qmax ? q[t] : qmax;
     }
   uint64_t lo = 0, hi = 0;
@@ -216,20 +331,31 @@ __device__ void warp_find(const SearchCtx &s, const uint64_t (&q)[NQ],
         unresolved |= 1u << t;
     }
 
+  if (AMRX_DBG && s.dbg) {
+    int nv = 0;
+#pragma unroll
+    for (int t = 0; t < NQ; t++) nv += valid[t];
+    dbg_add(s, kDbgFindCalls);
+    dbg_add(s, kDbgQueries, __reduce_add_sync(kFull, nv));
+  }
   for (int round = 0; round < 3; round++) {
     const uint32_t pend = __ballot_sync(kFull, unresolved != 0);
     if (!pend) break;
+    dbg_add(s, kDbgFindRounds);
     const int leader = __ffs(pend) - 1;
-    // leader's smallest open query
+    // leader's smallest open query (anchor-lowest under FINER)
     uint64_t lq = ~0ull;
 #pragma unroll
     for (int t = 0; t < NQ; t++)
-      if ((unresolved >> t) & 1) lq = q[t] < lq ? q[t] : lq;
+      if ((unresolved >> t) & 1) {
+        const uint64_t v = q[t] & amask;
+        lq = v < lq ? v : lq;
+      }
     lq = shfl_u64(lq, leader);
     uint64_t L = shfl_u64(lo, leader);
     uint64_t H = shfl_u64(hi, leader);
-    // 32-ary narrowing of [L, H) around lower_bound(lq)
-    // leave 4 keys of slack so the window below brackets lower_bound(lq)
+    // 32-ary narrowing of [L, H) around lower_bound(lq); 4 keys of slack
+    // so the window below brackets it
     while (H - L > uint64_t(kWin - 4)) {
       const uint64_t step = (H - L + 31) >> 5;
       const uint64_t pos = L + lane * step;
@@ -240,6 +366,7 @@ __device__ void warp_find(const SearchCtx &s, const uint64_t (&q)[NQ],
       const uint64_t nh = (c < 32 && pc < H) ? pc + 1 : H;
       L = nl;
       H = nh;
+      dbg_add(s, kDbgNarrow);
     }
     // stage the window [ws, ws + kWin): 16-byte aligned, starting at or
     // before L-1 so the leader's key[L-1] < lq proof lies inside it
@@ -249,22 +376,28 @@ __device__ void warp_find(const SearchCtx &s, const uint64_t (&q)[NQ],
     for (int v = 0; v < kWin / 64; v++) {
       const uint64_t at = ws + 2 * lane + 64 * v;
       const ulonglong2 kv = ldg_u64x2(s.keys + at);  // padded: never OOB
-      win[2 * lane + 64 * v] = kv.x;
-      win[2 * lane + 64 * v + 1] = kv.y;
+      reinterpret_cast<ulonglong2 *>(win)[lane + 32 * v] = kv;
     }
     __syncwarp();
     const uint64_t wend = ws + kWin < s.n ? ws + kWin : s.n;
     const int cnt = int(wend - ws);
+    int from = 0;
+    uint64_t prev = 0;
 #pragma unroll
     for (int t = 0; t < NQ; t++) {
       if (!((unresolved >> t) & 1)) continue;
-      const int p = smem_lower_bound(win, cnt, q[t]);
+      if (q[t] < prev) from = 0;
+      const int p = gallop_lower_bound(win, from, cnt, q[t]);
+      from = p;
+      prev = q[t];
       bool done = false;
       int64_t res = -1;
+      int rl = 0;
       if (p < cnt && win[p] == q[t]) {
         if (p > 0 || ws <= lo) {
           done = true;
           res = int64_t(ws + p);
+          rl = int(q[t] & s.lmask);
         }
       } else if (p == 0) {
         done = ws <= lo;
@@ -273,18 +406,34 @@ __device__ void warp_find(const SearchCtx &s, const uint64_t (&q)[NQ],
       } else {
         done = true;  // bracketed by two window keys, not equal
       }
+      if (FINER && done && res < 0) {
+        // same-anchor keys with lower levels end right before p
+        int x = p - 1;
+        const uint64_t anchor = q[t] & ~s.lmask;
+        while (x >= 0 && (win[x] & ~s.lmask) == anchor) x--;
+        if (x < 0 && ws > lo) {
+          done = false;  // the run may continue before the window
+        } else if (x + 1 < p) {
+          res = int64_t(ws + x + 1);
+          rl = int(win[x + 1] & s.lmask);
+        }
+      }
       if (done) {
         out[t] = res;
+        lvl[t] = rl + s.shift;
         unresolved &= ~(1u << t);
       }
     }
   }
-  // fallback: per-lane binary search of the own bucket range
+  if (AMRX_DBG && s.dbg) dbg_add(s, kDbgFallback, __reduce_add_sync(kFull, __popc(unresolved)));
+  // fallback: per-lane binary search of the own bucket range (rare; out of
+  // line to keep the hot loop inside the instruction cache)
 #pragma unroll
   for (int t = 0; t < NQ; t++)
     if ((unresolved >> t) & 1) {
-      const uint64_t p = global_lower_bound(s.keys, lo, hi, q[t]);
-      out[t] = (p < hi && ldg_u64(s.keys + p) == q[t]) ? int64_t(p) : -1;
+      int rl;
+      out[t] = find_in_bucket(s, lo, hi, q[t], FINER, rl);
+      lvl[t] = rl;
     }
 }
 

@@ -31,6 +31,9 @@
 #include "internal.h"
 #include "mc_tables.inc"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace amrx {
 
 namespace {
@@ -59,26 +62,6 @@ __device__ __forceinline__ int point_of(int delta, int d)
          9 * (((d >> 2) & 1) + ((delta >> 2) & 1));
 }
 
-constexpr unsigned long long kFlagAgg = 1ull << 62;
-constexpr unsigned long long kFlagPre = 2ull << 62;
-constexpr unsigned long long kValMask = (1ull << 62) - 1;
-
-__device__ __forceinline__ unsigned long long ld_relaxed(
-  const unsigned long long *p)
-{
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p)
-               : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void st_relaxed(unsigned long long *p,
-                                           unsigned long long v)
-{
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v)
-               : "memory");
-}
-
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v)
 {
 #pragma unroll
@@ -98,41 +81,67 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v)
   return v;
 }
 
-/*! decoupled look-back over warp tiles (ticket order): publish this tile's
-    aggregate, sum predecessors 32 at a time until an inclusive prefix shows
-    up, publish the inclusive prefix; returns the exclusive prefix */
-__device__ uint64_t lookback(unsigned long long *state, uint32_t tile,
-                             uint64_t aggregate)
+constexpr uint32_t kDualChunk = 1024;  // >= 8 * 32, the most one tile emits
+constexpr uint32_t kTriChunk = 2048;   // >= 40 * 32 (5 triangles x 8 duals)
+
+/*! staging space for `agg` items of this tile from the warp's private
+    chunk (cur_end[0], cur_end[1] in shared memory); a new chunk comes from
+    one atomicAdd on the arena cursor.  Warp-uniform. */
+__device__ __forceinline__ uint64_t reserve(uint64_t *cur_end, uint32_t agg,
+                                            uint32_t chunk,
+                                            unsigned long long *cursor)
 {
-  const uint32_t lane = lane_id();
-  if (tile == 0) {
-    if (lane == 0) st_relaxed(state, kFlagPre | aggregate);
-    return 0;
+  if (agg == 0) return 0;
+  uint64_t cur = cur_end[0], end = cur_end[1];
+  if (cur + agg > end) {
+    unsigned long long b = 0;
+    if (lane_id() == 0) b = atomicAdd(cursor, (unsigned long long)chunk);
+    b = __shfl_sync(kFull, b, 0);
+    cur = b;
+    end = b + chunk;
   }
-  if (lane == 0) st_relaxed(state + tile, kFlagAgg | aggregate);
-  uint64_t excl = 0;
-  int64_t j = int64_t(tile) - 1;
-  while (true) {
-    const int64_t idx = j - int64_t(lane);
-    unsigned long long s = kFlagPre;  // before tile 0: an inclusive 0
-    if (idx >= 0) {
-      do {
-        s = ld_relaxed(state + idx);
-      } while ((s & ~kValMask) == 0);
+  __syncwarp();
+  if (lane_id() == 0) {
+    cur_end[0] = cur + agg;
+    cur_end[1] = end;
+  }
+  __syncwarp();
+  return cur;
+}
+
+/*! move each tile's block from its staging position to its place in
+    candidate order (final offset = exclusive scan of tile counts): one warp
+    per tile, `words` 32-bit words per item, coalesced both ways */
+__global__ void __launch_bounds__(256)
+reorder_kernel(const uint32_t *__restrict__ cnt, const uint64_t *__restrict__ src_off,
+               const uint64_t *__restrict__ dst_off, uint32_t tiles, int words,
+               const uint32_t *__restrict__ src, uint32_t *__restrict__ dst,
+               uint64_t dst_cap, int words2, const uint32_t *__restrict__ src2,
+               uint32_t *__restrict__ dst2)
+{
+  const int lane = threadIdx.x & 31;
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < tiles;
+       t += warps) {
+    const uint32_t n = cnt[t];
+    if (!n) continue;
+    const uint64_t so = src_off[t], d0 = dst_off[t];
+    const uint64_t keep = d0 >= dst_cap ? 0 : (d0 + n > dst_cap ? dst_cap - d0 : n);
+    const uint64_t nw = keep * uint64_t(words);
+    for (uint64_t w = lane; w < nw; w += 32)
+      dst[d0 * words + w] = __ldg(src + so * words + w);
+    if (words2) {
+      const uint64_t nw2 = keep * uint64_t(words2);
+      for (uint64_t w = lane; w < nw2; w += 32)
+        dst2[d0 * words2 + w] = __ldg(src2 + so * words2 + w);
     }
-    const uint32_t pre = __ballot_sync(kFull, (s & ~kValMask) == kFlagPre);
-    const int first = pre ? __ffs(pre) - 1 : 32;
-    excl += warp_sum_u64(int(lane) <= first ? (s & kValMask) : 0);
-    if (pre) break;
-    j -= 32;
   }
-  if (lane == 0) st_relaxed(state + tile, kFlagPre | (excl + aggregate));
-  return excl;
 }
 
 struct KArgs {
   SearchCtx s;
   KeyGeom g;
+  const uint8_t *lmap;  // block level map (g.map_on)
   const double *scal;
   uint64_t cell_begin, cell_end;
   uint32_t num_tiles;
@@ -142,11 +151,14 @@ struct KArgs {
   uint64_t dual_cap;
   void *xyz;
   uint64_t tri_cap;
-  unsigned long long *dual_state;
-  unsigned long long *tri_state;
+  uint32_t *tile_dual_cnt;
+  uint64_t *tile_dual_off;
+  uint32_t *tile_tri_cnt;
+  uint64_t *tile_tri_off;
   unsigned int *ticket;
   unsigned long long *out;  // [0..3] counters, [4] duals, [5] tris counted,
-                            // [6] tris written, [7] error flags
+                            // [6] tris written, [7] error flags,
+                            // [8] dual arena cursor, [9] tri arena cursor
 };
 
 struct Smem {
@@ -154,6 +166,13 @@ struct Smem {
   uint32_t id[kWarps][27][32];
   uint8_t lev[kWarps][27][32];
   uint64_t mc_rows[256];
+  // per-warp accumulators (lane 0 writes): [0..3] reject counters, [4]
+  // duals, [5] triangles counted, [6] triangles written; staging chunk
+  // cursors (cur, end) for duals and triangles
+  unsigned long long acc[kWarps][8];
+  uint64_t chunk[kWarps][4];
+  // remain[delta][d]: stencil points of candidate delta's corners d..7
+  uint32_t remain[8][9];
 };
 
 /// centre of the corner cell: anchor + half width, in double (core.hpp:113-118)
@@ -166,9 +185,9 @@ __device__ __forceinline__ double centre(int64_t anchor, int level)
     when out != null, write) its non-sliver triangles.  FP64 with explicit
     round-to-nearest intrinsics: no FMA contraction, matching the
     reference's -ffp-contract=off build. */
-template <bool WRITE, bool F32>
-__device__ int mc_dual(const KArgs &a, const Smem &sm, int warp, int lane,
-                       const Cell &c, int delta, double iso, void *out,
+template <bool F32>
+__device__ __noinline__ int mc_dual(const KArgs &a, const Smem &sm, int warp, int lane,
+                       const Cell &c, int delta, double iso, bool write, void *out,
                        uint64_t at, uint64_t cap, uint32_t &err)
 {
   const int64_t w = int64_t(1) << c.level;
@@ -219,15 +238,16 @@ __device__ int mc_dual(const KArgs &a, const Smem &sm, int warp, int lane,
 
   int count = 0;
   for (int tri = 0; tri < ntab; tri++) {
-    double p0[3], p1[3], p2[3];
-    edge_point(int((word >> (4 + 12 * tri)) & 15), p0);
-    edge_point(int((word >> (8 + 12 * tri)) & 15), p1);
-    edge_point(int((word >> (12 + 12 * tri)) & 15), p2);
+    double pv[3][3];
+#pragma unroll 1
+    for (int k = 0; k < 3; k++)  // one copy of the edge code (I-cache)
+      edge_point(int((word >> (4 + 12 * tri + 4 * k)) & 15), pv[k]);
+    const double *p0 = pv[0], *p1 = pv[1], *p2 = pv[2];
     const bool e01 = p0[0] == p1[0] && p0[1] == p1[1] && p0[2] == p1[2];
     const bool e12 = p1[0] == p2[0] && p1[1] == p2[1] && p1[2] == p2[2];
     const bool e02 = p0[0] == p2[0] && p0[1] == p2[1] && p0[2] == p2[2];
     if (e01 || e12 || e02) continue;
-    if (WRITE) {
+    if (write) {
       const uint64_t slot = at + uint64_t(count);
       if (slot < cap) {
         if (F32) {
@@ -248,54 +268,92 @@ __device__ int mc_dual(const KArgs &a, const Smem &sm, int warp, int lane,
   return count;
 }
 
+/// warp_find for the coarser-level probes: rare, so out of line
+__device__ __noinline__ void find3_coarse(const SearchCtx &s, const uint64_t (&q)[3],
+                                          const bool (&v)[3], int64_t (&o)[3],
+                                          int (&l)[3], uint64_t *win)
+{
+  warp_find<3, false>(s, q, v, o, l, win);
+}
+
 /*! resolve the three stencil points of column COL (dx, dy fixed; dz =
-    -1,0,+1) for the lanes flagged 'mine': hint level first in one
-    warp_find, then for misses the other present levels finest first
-    (locator.cpp:125-133), one warp_find per probe round */
-__device__ __noinline__ void resolve_column(const KArgs &a, Smem &sm,
+    -1,0,+1) for the lanes flagged 'mine', in snap's probe order
+    (locator.cpp:122-134), skipping levels the block level map rules out
+    (exact: a cell containing p lies in p's coarsest-aligned block):
+      1. the hint level and every finer level in ONE warp_find (finer cells
+         containing a stencil point share its anchor, see warp_find);
+      2. the candidate coarser levels ascending, one warp_find per round --
+         in valid data the first coarser probe hits, and points with no
+         candidate level (holes, outside the domain) cost no search. */
+__device__ __forceinline__ void resolve_column(const KArgs &a, Smem &sm,
                                             int warp, int lane, const Cell &c,
                                             uint32_t self, int COL, bool mine,
                                             uint32_t &resolved,
                                             uint64_t &status)
 {
+  const KeyGeom &g = a.g;
   const int ox = COL % 3 - 1, oy = COL / 3 - 1;
   const int64_t w = int64_t(1) << c.level;
   const int64_t px = c.i + ox * w, py = c.j + oy * w;
+  // level bits: index of the hint level in g.levels
+  const int hint_bit = __popc(g.level_mask & ((1u << c.level) - 1));
+  const uint32_t le_hint = (2u << hint_bit) - 1;
+  // at the hint level the points are their own anchors: build the keys
+  // from one shared x/y part, no masking
+  const bool xy = mine && px >= g.mn[0] && px <= g.mx[0] && py >= g.mn[1] &&
+                  py <= g.mx[1];
+  uint64_t base = uint64_t(c.level - g.shift);
+  if (g.bits[0]) base |= uint64_t((px - g.mn[0]) >> g.shift) << g.sh[0];
+  if (g.bits[1]) base |= uint64_t((py - g.mn[1]) >> g.shift) << g.sh[1];
   uint64_t q[3];
   bool v[3];
   int64_t out[3] = {-1, -1, -1};
   int lvl[3] = {c.level, c.level, c.level};
+  uint32_t cand[3];
 #pragma unroll
-  for (int t = 0; t < 3; t++)
-    v[t] = mine && query_key(a.g, px, py, c.k + (t - 1) * w, c.level, q[t]);
-  warp_find<3>(a.s, q, v, out, sm.win[warp]);
+  for (int t = 0; t < 3; t++) {
+    const int64_t pz = c.k + (t - 1) * w;
+    cand[t] = mine ? block_levels(g, a.lmap, px, py, pz) : 0u;
+    v[t] = xy && pz >= g.mn[2] && pz <= g.mx[2] && (cand[t] & le_hint);
+    q[t] = base | (g.bits[2] ? uint64_t((pz - g.mn[2]) >> g.shift) << g.sh[2] : 0);
+    cand[t] &= ~le_hint;  // what is left for step 2
+  }
+  if (__any_sync(kFull, v[0] || v[1] || v[2]))
+    warp_find<3, true>(a.s, q, v, out, lvl, sm.win[warp]);
 
-  // misses at the hint level probe the other levels, finest first
+  // step 2: coarser candidate levels, ascending (= the reference's finest
+  // first order restricted to the levels above the hint)
   bool pend[3];
 #pragma unroll
-  for (int t = 0; t < 3; t++) pend[t] = mine && out[t] < 0;
-  int li = 0;
+  for (int t = 0; t < 3; t++) pend[t] = out[t] < 0 && cand[t] != 0;
   while (__any_sync(kFull, pend[0] || pend[1] || pend[2])) {
-    while (li < a.g.nlevels && a.g.levels[li] == c.level) li++;
-    const bool have = li < a.g.nlevels;
-    const int L = have ? a.g.levels[li] : 0;
+    dbg_add(a.s, kDbgCoarser);
     bool v2[3];
     int64_t o2[3] = {-1, -1, -1};
-#pragma unroll
-    for (int t = 0; t < 3; t++)
-      v2[t] = pend[t] && have &&
-              query_key(a.g, px, py, c.k + (t - 1) * w, L, q[t]);
-    warp_find<3>(a.s, q, v2, o2, sm.win[warp]);
+    int l2[3], L[3];
 #pragma unroll
     for (int t = 0; t < 3; t++) {
-      if (pend[t] && v2[t] && o2[t] >= 0) {
-        out[t] = o2[t];
-        lvl[t] = L;
-        pend[t] = false;
+      L[t] = 0;
+      v2[t] = false;
+      if (pend[t]) {
+        const int b = __ffs(cand[t]) - 1;
+        cand[t] &= cand[t] - 1;
+        L[t] = g.levels[b];
+        v2[t] = query_key(g, px, py, c.k + (t - 1) * w, L[t], q[t]);
       }
-      if (!have) pend[t] = false;
     }
-    li++;
+    find3_coarse(a.s, q, v2, o2, l2, sm.win[warp]);
+#pragma unroll
+    for (int t = 0; t < 3; t++)
+      if (pend[t]) {
+        if (v2[t] && o2[t] >= 0) {
+          out[t] = o2[t];
+          lvl[t] = L[t];
+          pend[t] = false;
+        } else if (!cand[t]) {
+          pend[t] = false;
+        }
+      }
   }
   if (mine) {
 #pragma unroll
@@ -333,6 +391,7 @@ __device__ __forceinline__ void resolve_needed(const KArgs &a, Smem &sm,
   while (wcols) {
     const int col = __ffs(wcols) - 1;
     wcols &= wcols - 1;
+    dbg_add(a.s, kDbgColumns);
     resolve_column(a, sm, warp, lane, c, self, col, (cols >> col) & 1,
                    resolved, status);
   }
@@ -341,9 +400,9 @@ __device__ __forceinline__ void resolve_needed(const KArgs &a, Smem &sm,
 /// walk each live candidate's corners in order while they are resolved
 __device__ __forceinline__ void advance(uint32_t resolved, uint64_t status,
                                         uint32_t &alive, uint32_t &curd,
-                                        uint32_t &accepted, uint32_t (&cnt)[4])
+                                        uint32_t &accepted, uint32_t &reasons)
 {
-#pragma unroll
+#pragma unroll 1
   for (int delta = 0; delta < 8; delta++) {
     if (!((alive >> delta) & 1)) continue;
     int d = int((curd >> (4 * delta)) & 15);
@@ -353,7 +412,7 @@ __device__ __forceinline__ void advance(uint32_t resolved, uint64_t status,
       const uint32_t st = uint32_t(status >> (2 * p)) & 3;
       if (st != kOk) {
         alive &= ~(1u << delta);
-        cnt[st]++;
+        reasons += 1u << (8 * st);  // one byte per outcome, <= 8 per cell
         break;
       }
       d++;
@@ -361,7 +420,7 @@ __device__ __forceinline__ void advance(uint32_t resolved, uint64_t status,
     if (d == 8) {
       accepted |= 1u << delta;
       alive &= ~(1u << delta);
-      cnt[0]++;
+      reasons += 1u;
     }
     curd = (curd & ~(15u << (4 * delta))) | (uint32_t(d) << (4 * delta));
   }
@@ -379,8 +438,16 @@ extract_kernel(const KArgs a)
     __syncthreads();
   }
 
-  uint32_t cnt[4] = {0, 0, 0, 0};
-  uint64_t tot_dual = 0, tot_counted = 0, tot_written = 0;
+  for (int i = threadIdx.x; i < 72; i += kThreads) {
+    const int delta = i / 9, d0 = i % 9;
+    uint32_t m = 0;
+    for (int d = d0; d < 8; d++) m |= 1u << point_of(delta, d);
+    sm.remain[delta][d0] = m;
+  }
+  __syncthreads();
+  if (lane < 8) sm.acc[warp][lane] = 0;
+  if (lane < 4) sm.chunk[warp][lane] = 0;
+  __syncwarp();
   uint32_t err = 0;
 
   for (;;) {
@@ -388,43 +455,69 @@ extract_kernel(const KArgs a)
     if (lane == 0) tile = atomicAdd(a.ticket, 1u);
     tile = __shfl_sync(kFull, tile, 0);
     if (tile >= a.num_tiles) break;
+    dbg_add(a.s, kDbgTiles);
 
     const uint64_t cell = a.cell_begin + uint64_t(tile) * 32 + lane;
     const bool valid = cell < a.cell_end;
     const uint32_t self = uint32_t(cell);
-    Cell c = unpack(a.g, valid ? ldg_u64(a.s.keys + cell) : 0);
+    const Cell c = unpack(a.g, valid ? ldg_u64(a.s.keys + cell) : 0);
 
     uint32_t resolved = 0, alive = valid ? 0xffu : 0u, curd = 0, accepted = 0;
+    uint32_t reasons = 0;
     uint64_t status = 0;
-    // round 1: every candidate's corner 0 ({-w,0}^3, 4 columns)
-    resolve_needed(a, sm, warp, lane, c, self, valid ? kCorner0Points : 0,
-                   resolved, status);
-    advance(resolved, status, alive, curd, accepted, cnt);
-    // round 2: everything the survivors still need
-    uint32_t need = 0;
-#pragma unroll
-    for (int delta = 0; delta < 8; delta++)
-      if ((alive >> delta) & 1)
-        for (int d = int((curd >> (4 * delta)) & 15); d < 8; d++)
-          need |= 1u << point_of(delta, d);
-    need &= ~resolved;
-    resolve_needed(a, sm, warp, lane, c, self, need, resolved, status);
-    advance(resolved, status, alive, curd, accepted, cnt);
+    // round 0: every candidate's corner 0 ({-w,0}^3, 4 columns); round 1:
+    // everything the survivors still need
+    uint32_t need = valid ? kCorner0Points : 0;
+#pragma unroll 1
+    for (int round = 0; round < 2; round++) {
+      if (round == 1) {
+        need = 0;
+#pragma unroll 1
+        for (uint32_t m = alive; m; m &= m - 1) {
+          const int delta = __ffs(m) - 1;
+          need |= sm.remain[delta][(curd >> (4 * delta)) & 15];
+        }
+        need &= ~resolved;
+      }
+      resolve_needed(a, sm, warp, lane, c, self, need, resolved, status);
+      advance(resolved, status, alive, curd, accepted, reasons);
+    }
     if (alive) err |= 2u;
 
-    // ---- count, scan, look-back, emit
+    // ---- count (pass 1), reserve staging space, emit (pass 2).  No
+    // waiting on other tiles: the tile's block goes to this warp's private
+    // chunk of the staging arena and (offset, count) to the tile table;
+    // reorder_kernel later moves blocks into candidate order.
     const uint32_t nd = __popc(accepted);
     uint32_t nt = 0;
     if (EMIT_TRI)
       for (uint32_t m = accepted; m; m &= m - 1)
-        nt += mc_dual<false, F32>(a, sm, warp, lane, c, __ffs(m) - 1, a.iso,
-                                  nullptr, 0, 0, err);
+        nt += mc_dual<F32>(a, sm, warp, lane, c, __ffs(m) - 1, a.iso, false,
+                              nullptr, 0, 0, err);
+    // tile totals into the warp's accumulators (16-bit fields cannot carry:
+    // 32 lanes x 8 candidates)
+    {
+      const uint32_t r01 = __reduce_add_sync(kFull, (reasons & 0xffu) | ((reasons & 0xff00u) << 8));
+      const uint32_t r23 = __reduce_add_sync(kFull, ((reasons >> 16) & 0xffu) | ((reasons >> 24) << 16));
+      const uint32_t tnd = __reduce_add_sync(kFull, nd);
+      if (lane == 0) {
+        sm.acc[warp][0] += r01 & 0xffffu;
+        sm.acc[warp][1] += r01 >> 16;
+        sm.acc[warp][2] += r23 & 0xffffu;
+        sm.acc[warp][3] += r23 >> 16;
+        sm.acc[warp][4] += tnd;
+      }
+    }
     __syncwarp();
     if (EMIT_DUAL) {
       const uint32_t incl = warp_incl_scan(nd);
       const uint32_t agg = __shfl_sync(kFull, incl, 31);
-      const uint64_t base = lookback(a.dual_state, tile, agg) + (incl - nd);
-      tot_dual += nd;
+      const uint64_t base =
+        reserve(&sm.chunk[warp][0], agg, kDualChunk, a.out + 8) + (incl - nd);
+      if (lane == 0) {
+        a.tile_dual_cnt[tile] = agg;
+        a.tile_dual_off[tile] = base;
+      }
       uint32_t k = 0;
       for (uint32_t m = accepted; m; m &= m - 1, k++) {
         const int delta = __ffs(m) - 1;
@@ -436,35 +529,38 @@ extract_kernel(const KArgs a)
         uint4 *dst = reinterpret_cast<uint4 *>(a.corners + slot * 8);
         dst[0] = make_uint4(ids[0], ids[1], ids[2], ids[3]);
         dst[1] = make_uint4(ids[4], ids[5], ids[6], ids[7]);
-        if (a.tasks) a.tasks[slot] = cell * 8 + uint64_t(delta);
+        a.tasks[slot] = cell * 8 + uint64_t(delta);
       }
-    } else {
-      tot_dual += nd;
     }
     if (EMIT_TRI) {
       const uint32_t incl = warp_incl_scan(nt);
       const uint32_t agg = __shfl_sync(kFull, incl, 31);
-      const uint64_t base = lookback(a.tri_state, tile, agg) + (incl - nt);
-      tot_counted += nt;
-      uint64_t at = base;
-      for (uint32_t m = accepted; m; m &= m - 1)
-        at += mc_dual<true, F32>(a, sm, warp, lane, c, __ffs(m) - 1, a.iso,
-                                 a.xyz, at, a.tri_cap, err);
-      tot_written += at - base;
+      const uint64_t base =
+        reserve(&sm.chunk[warp][2], agg, kTriChunk, a.out + 9) + (incl - nt);
+      if (lane == 0) {
+        a.tile_tri_cnt[tile] = agg;
+        a.tile_tri_off[tile] = base;
+      }
+      uint32_t wrote = 0;
+      if (agg)
+        for (uint32_t m = accepted; m; m &= m - 1)
+          wrote += mc_dual<F32>(a, sm, warp, lane, c, __ffs(m) - 1, a.iso, true,
+                                 a.xyz, base + wrote, a.tri_cap, err);
+      const uint32_t tw = __reduce_add_sync(kFull, wrote);
+      if (lane == 0) {
+        sm.acc[warp][5] += agg;
+        sm.acc[warp][6] += tw;
+      }
     }
     __syncwarp();
   }
 
   // per-warp totals -> global
-  uint64_t v[8] = {cnt[0], cnt[1], cnt[2], cnt[3], tot_dual, tot_counted,
-                   tot_written, 0};
-#pragma unroll
-  for (int i = 0; i < 7; i++) v[i] = warp_sum_u64(v[i]);
   err = __reduce_or_sync(kFull, err);
   if (lane == 0) {
 #pragma unroll
     for (int i = 0; i < 7; i++)
-      if (v[i]) atomicAdd(a.out + i, (unsigned long long)v[i]);
+      if (sm.acc[warp][i]) atomicAdd(a.out + i, sm.acc[warp][i]);
     if (err) atomicOr(a.out + 7, (unsigned long long)err);
   }
 }
@@ -489,8 +585,9 @@ __device__ int64_t warp_snap(const SearchCtx &s, const KeyGeom &g, bool active,
     uint64_t q[1];
     bool v[1];
     int64_t o[1] = {-1};
+    int l1[1];
     v[0] = have && query_key(g, px, py, pz, L, q[0]);
-    warp_find<1>(s, q, v, o, win);
+    warp_find<1, false>(s, q, v, o, l1, win);
     if (pend && v[0] && o[0] >= 0) {
       result = o[0];
       pend = false;
@@ -523,7 +620,8 @@ find_exact_kernel(const SearchCtx s, const KeyGeom g,
            anchor_mask(cc.y, cc.w) == cc.y &&
            anchor_mask(cc.z, cc.w) == cc.z &&
            query_key(g, cc.x, cc.y, cc.z, cc.w, q[0]);
-    warp_find<1>(s, q, v, o, win[warp]);
+    int l1[1];
+    warp_find<1, false>(s, q, v, o, l1, win[warp]);
     if (in) out[r] = v[0] ? o[0] : -1;
   }
 }
@@ -642,61 +740,134 @@ int occupancy_grid()
 
 }  // namespace
 
-ExtractResult run_extract(const ExtractRequest &r, DevBuf &scratch,
+ExtractResult run_extract(const ExtractRequest &r, ExtractScratch &x,
                           cudaStream_t st)
 {
   ExtractResult res{};
   const uint64_t cells = r.cell_end > r.cell_begin ? r.cell_end - r.cell_begin : 0;
   const uint64_t tiles = (cells + 31) / 32;
-  const size_t state_bytes = size_t(tiles) * 8;
-  scratch.reserve(2 * state_bytes + 256);
-  auto *base = scratch.as<unsigned char>();
+  const bool D = r.emit_dual, T = r.emit_tri, F = r.tri_f32;
+  int grid = 1;
+  if (D && T && F) grid = occupancy_grid<true, true, true>();
+  else if (D && T) grid = occupancy_grid<true, true, false>();
+  else if (D) grid = occupancy_grid<true, false, false>();
+  else if (T && F) grid = occupancy_grid<false, true, true>();
+  else if (T) grid = occupancy_grid<false, true, false>();
+  else grid = occupancy_grid<false, false, false>();
+  const uint64_t warps = uint64_t(grid) * kWarps;
+
+  // control block | tile tables (count u32 + staging offset u64 + final
+  // offset u64, per output kind)
+  x.ctl.reserve(256, st);
+  x.tiles.reserve(size_t(tiles + 1) * 40 + 64, st);
+  auto *ctl = x.ctl.as<unsigned long long>();
+  auto *tb = x.tiles.as<unsigned char>();
+  uint32_t *dual_cnt = reinterpret_cast<uint32_t *>(tb);
+  uint32_t *tri_cnt = dual_cnt + (tiles + 1);
+  uint64_t *dual_off = reinterpret_cast<uint64_t *>(tb + ((2 * (tiles + 1) * 4 + 15) & ~size_t(15)));
+  uint64_t *tri_off = dual_off + (tiles + 1);
+  uint64_t *final_off = tri_off + (tiles + 1);
+  AMRX_CUDA(cudaMemsetAsync(ctl, 0, 256, st));
+  if (tiles) AMRX_CUDA(cudaMemsetAsync(tb, 0, size_t(tiles + 1) * 8, st));
+
+  // staging capacity: what the caller can take plus one chunk per warp of
+  // slack for partially used chunks (so a fitting result never overflows)
+  const uint64_t dual_stage = D && r.corners ? r.dual_cap + warps * kDualChunk : 0;
+  const uint64_t tri_stage = T && r.xyz ? r.tri_cap + warps * kTriChunk : 0;
+  const int tri_words = F ? 9 : 18;  // 32-bit words per triangle
+  if (dual_stage) {
+    x.stage_a.reserve(dual_stage * 32, st);
+    x.stage_b.reserve(dual_stage * 8, st);
+  }
+  if (tri_stage) x.stage_a.reserve(tri_stage * tri_words * 4, st);
+
   KArgs k;
   k.s = r.s;
   k.g = r.g;
+  k.lmap = r.lmap;
   k.scal = r.scal;
   k.cell_begin = r.cell_begin;
   k.cell_end = r.cell_end;
   k.num_tiles = uint32_t(tiles);
   k.iso = r.iso;
-  k.corners = r.corners;
-  k.tasks = r.tasks;
-  k.dual_cap = r.corners ? r.dual_cap : 0;
-  k.xyz = r.xyz;
-  k.tri_cap = r.xyz ? r.tri_cap : 0;
-  k.out = reinterpret_cast<unsigned long long *>(base);
-  k.ticket = reinterpret_cast<unsigned int *>(base + 64);
-  k.dual_state = reinterpret_cast<unsigned long long *>(base + 256);
-  k.tri_state = reinterpret_cast<unsigned long long *>(base + 256 + state_bytes);
-  AMRX_CUDA(cudaMemsetAsync(base, 0, 2 * state_bytes + 256, st));
+  k.corners = dual_stage ? x.stage_a.as<uint32_t>() : nullptr;
+  k.tasks = dual_stage ? x.stage_b.as<uint64_t>() : nullptr;
+  k.dual_cap = dual_stage;
+  k.xyz = tri_stage ? x.stage_a.ptr : nullptr;
+  k.tri_cap = tri_stage;
+  k.tile_dual_cnt = dual_cnt;
+  k.tile_dual_off = dual_off;
+  k.tile_tri_cnt = tri_cnt;
+  k.tile_tri_off = tri_off;
+  k.out = ctl;
+  k.ticket = reinterpret_cast<unsigned int *>(ctl + 16);
+  static const bool debug = std::getenv("AMRX_DEBUG_COUNTERS") != nullptr;
+  k.s.dbg = debug ? ctl + 18 : nullptr;  // ctl holds 32 u64
 
-  cudaEvent_t e0, e1;
+  cudaEvent_t e0, e1, e2;
   AMRX_CUDA(cudaEventCreate(&e0));
   AMRX_CUDA(cudaEventCreate(&e1));
+  AMRX_CUDA(cudaEventCreate(&e2));
   AMRX_CUDA(cudaEventRecord(e0, st));
   if (tiles) {
-    int grid;
-    const bool D = r.emit_dual, T = r.emit_tri, F = r.tri_f32;
-    if (D && T && F) { grid = occupancy_grid<true, true, true>(); launch_extract<true, true, true>(k, grid, st); }
-    else if (D && T) { grid = occupancy_grid<true, true, false>(); launch_extract<true, true, false>(k, grid, st); }
-    else if (D) { grid = occupancy_grid<true, false, false>(); launch_extract<true, false, false>(k, grid, st); }
-    else if (T && F) { grid = occupancy_grid<false, true, true>(); launch_extract<false, true, true>(k, grid, st); }
-    else if (T) { grid = occupancy_grid<false, true, false>(); launch_extract<false, true, false>(k, grid, st); }
-    else { grid = occupancy_grid<false, false, false>(); launch_extract<false, false, false>(k, grid, st); }
+    if (D && T && F) launch_extract<true, true, true>(k, grid, st);
+    else if (D && T) launch_extract<true, true, false>(k, grid, st);
+    else if (D) launch_extract<true, false, false>(k, grid, st);
+    else if (T && F) launch_extract<false, true, true>(k, grid, st);
+    else if (T) launch_extract<false, true, false>(k, grid, st);
+    else launch_extract<false, false, false>(k, grid, st);
     res.launches = 1;
   }
   AMRX_CUDA(cudaEventRecord(e1, st));
-  unsigned long long h[8];
-  AMRX_CUDA(cudaMemcpyAsync(h, base, sizeof h, cudaMemcpyDeviceToHost, st));
+  unsigned long long h[10];
+  AMRX_CUDA(cudaMemcpyAsync(h, ctl, sizeof h, cudaMemcpyDeviceToHost, st));
   AMRX_CUDA(cudaStreamSynchronize(st));
-  AMRX_CUDA(cudaEventElapsedTime(&res.ms, e0, e1));
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   for (int i = 0; i < 4; i++) res.counters[i] = h[i];
   res.duals = h[4];
   res.tris_counted = h[5];
   res.tris_written = h[6];
   res.error_flags = uint32_t(h[7]);
+  if (debug) {
+    unsigned long long d[kDbgCount];
+    AMRX_CUDA(cudaMemcpy(d, ctl + 18, sizeof d, cudaMemcpyDeviceToHost));
+    const char *names[kDbgCount] = {"tiles", "columns", "find_calls", "find_rounds",
+                                    "narrow_steps", "fallback_queries", "coarser_calls",
+                                    "mc_tab", "queries", "win_resolved"};
+    std::fprintf(stderr, "[amrx dbg]");
+    for (int i = 0; i < kDbgCount; i++)
+      std::fprintf(stderr, " %s=%llu (%.2f/tile)", names[i], d[i],
+                   d[0] ? double(d[i]) / double(d[0]) : 0.0);
+    std::fprintf(stderr, "\n");
+  }
+
+  // pass 2 of the reference's scheme: exclusive scan of the tile counts
+  // gives every tile its final offset; blocks move into candidate order
+  const int rgrid = int(std::min<uint64_t>((tiles + 7) / 8, uint64_t(device_sm_count()) * 16));
+  if (tiles && dual_stage && res.duals > 0) {
+    res.launches += scan_exclusive_u32_u64(dual_cnt, final_off, tiles, x.scan, st);
+    reorder_kernel<<<std::max(1, rgrid), 256, 0, st>>>(
+      dual_cnt, dual_off, final_off, uint32_t(tiles), 8, x.stage_a.as<uint32_t>(),
+      r.corners, r.dual_cap, r.tasks ? 2 : 0, x.stage_b.as<uint32_t>(),
+      reinterpret_cast<uint32_t *>(r.tasks));
+    AMRX_LAUNCH_CHECK();
+    res.launches += 1;
+  }
+  if (tiles && tri_stage && res.tris_written > 0) {
+    res.launches += scan_exclusive_u32_u64(tri_cnt, final_off, tiles, x.scan, st);
+    reorder_kernel<<<std::max(1, rgrid), 256, 0, st>>>(
+      tri_cnt, tri_off, final_off, uint32_t(tiles), tri_words,
+      x.stage_a.as<uint32_t>(), static_cast<uint32_t *>(r.xyz), r.tri_cap, 0,
+      nullptr, nullptr);
+    AMRX_LAUNCH_CHECK();
+    res.launches += 1;
+  }
+  AMRX_CUDA(cudaEventRecord(e2, st));
+  AMRX_CUDA(cudaStreamSynchronize(st));
+  AMRX_CUDA(cudaEventElapsedTime(&res.ms, e0, e1));
+  AMRX_CUDA(cudaEventElapsedTime(&res.ms2, e1, e2));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
   return res;
 }
 

@@ -155,6 +155,40 @@ bucket_count_kernel(const uint64_t *__restrict__ keys, uint64_t n, int shift,
   }
 }
 
+/*! block level map: OR the cell's level bit into the byte of its
+    coarsest-aligned block; sorted neighbours share blocks, so a warp issues
+    one atomic per distinct (word, bits) it holds */
+__global__ void __launch_bounds__(kThreads)
+level_map_kernel(const uint64_t *__restrict__ keys, uint64_t n, const KeyGeom g,
+                 uint32_t *__restrict__ words)
+{
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  const uint64_t start = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (uint64_t base = start - (threadIdx.x & 31); base < n; base += stride) {
+    const uint64_t r = base + (threadIdx.x & 31);
+    const bool in = r < n;
+    uint64_t idx = ~0ull;
+    uint32_t bits = 0;
+    if (in) {
+      const Cell c = unpack(g, ldg_u64(keys + r));
+      const int b = __popc(g.level_mask & ((1u << c.level) - 1));
+      const uint64_t bx = uint64_t((c.i >> g.map_shift) - g.map_base[0]);
+      const uint64_t by = uint64_t((c.j >> g.map_shift) - g.map_base[1]);
+      const uint64_t bz = uint64_t((c.k >> g.map_shift) - g.map_base[2]);
+      idx = (bz * uint64_t(g.map_dim[1]) + by) * uint64_t(g.map_dim[0]) + bx;
+      bits = (1u << b) << (8 * (idx & 3));
+    }
+    const uint64_t word = idx >> 2;
+    const uint32_t peers = __match_any_sync(kFull, word);
+    // OR of the peers' bits, then one atomic by the first peer
+    uint32_t acc = 0;
+    for (uint32_t m = peers; m; m &= m - 1)
+      acc |= __shfl_sync(peers, bits, __ffs(m) - 1);
+    if (in && (__ffs(peers) - 1) == int(threadIdx.x & 31))
+      atomicOr(words + word, acc);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads)
 unpack_kernel(const uint64_t *__restrict__ keys, uint64_t n, const KeyGeom g,
               int4 *__restrict__ cells)
@@ -168,79 +202,102 @@ unpack_kernel(const uint64_t *__restrict__ keys, uint64_t n, const KeyGeom g,
 }
 
 // --------------------------------------------------- reduce-then-scan
+// T = element type, A = accumulator / output type (u32 -> u32 or u32 -> u64)
 constexpr int kScanThreads = 512;
 constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
-__device__ __forceinline__ uint32_t block_exclusive_sum(uint32_t v,
-                                                        uint32_t *smem,
-                                                        uint32_t *total)
+template <typename A>
+__device__ __forceinline__ A block_exclusive_sum(A v, A *smem, A *total)
 {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t x = v;
+  A x = v;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
-    const uint32_t y = __shfl_up_sync(kFull, x, off);
+    const A y = __shfl_up_sync(kFull, x, off);
     if (lane >= off) x += y;
   }
   if (lane == 31) smem[warp] = x;
   __syncthreads();
   if (warp == 0) {
     const int nw = blockDim.x >> 5;
-    uint32_t s = lane < nw ? smem[lane] : 0;
+    A s = lane < nw ? smem[lane] : A(0);
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, s, off);
+      const A y = __shfl_up_sync(kFull, s, off);
       if (lane >= off) s += y;
     }
     if (lane < nw) smem[lane] = s;
   }
   __syncthreads();
-  const uint32_t warp_excl = warp ? smem[warp - 1] : 0;
+  const A warp_excl = warp ? smem[warp - 1] : A(0);
   if (total) *total = smem[(blockDim.x >> 5) - 1];
   return warp_excl + x - v;
 }
 
+template <typename T, typename A>
 __global__ void __launch_bounds__(kScanThreads)
-scan_reduce_kernel(const uint32_t *__restrict__ in, uint64_t n,
-                   uint32_t *__restrict__ sums)
+scan_reduce_kernel(const T *__restrict__ in, uint64_t n, A *__restrict__ sums)
 {
-  __shared__ uint32_t sm[32];
+  __shared__ A sm[32];
   const uint64_t base = uint64_t(blockIdx.x) * kScanTile;
-  uint32_t s = 0;
+  A s = 0;
 #pragma unroll
   for (int t = 0; t < kScanItems; t++) {
     const uint64_t r = base + uint64_t(t) * kScanThreads + threadIdx.x;
-    if (r < n) s += in[r];
+    if (r < n) s += A(in[r]);
   }
-  uint32_t total;
-  block_exclusive_sum(s, sm, &total);
+  A total;
+  block_exclusive_sum<A>(s, sm, &total);
   if (threadIdx.x == 0) sums[blockIdx.x] = total;
 }
 
+template <typename T, typename A>
 __global__ void __launch_bounds__(kScanThreads)
-scan_downsweep_kernel(const uint32_t *in, uint32_t *out, uint64_t n,
-                      const uint32_t *__restrict__ block_offsets)
+scan_downsweep_kernel(const T *in, A *out, uint64_t n,
+                      const A *__restrict__ block_offsets)
 {
-  __shared__ uint32_t sm[32];
+  __shared__ A sm[32];
   const uint64_t base = uint64_t(blockIdx.x) * kScanTile +
                         uint64_t(threadIdx.x) * kScanItems;
-  uint32_t v[kScanItems];
-  uint32_t s = 0;
+  A v[kScanItems];
+  A s = 0;
 #pragma unroll
   for (int t = 0; t < kScanItems; t++) {
     const uint64_t r = base + t;
-    v[t] = r < n ? in[r] : 0;
+    v[t] = r < n ? A(in[r]) : A(0);
     s += v[t];
   }
-  uint32_t run = block_exclusive_sum(s, sm, nullptr) +
-                 (block_offsets ? block_offsets[blockIdx.x] : 0);
+  A run = block_exclusive_sum<A>(s, sm, nullptr) +
+          (block_offsets ? block_offsets[blockIdx.x] : A(0));
 #pragma unroll
   for (int t = 0; t < kScanItems; t++) {
     const uint64_t r = base + t;
     if (r < n) out[r] = run;
     run += v[t];
   }
+}
+
+/// recursive reduce-then-scan; block sums of each level in a pool buffer
+template <typename T, typename A>
+int scan_exclusive(const T *in, A *out, uint64_t n, cudaStream_t st)
+{
+  if (n == 0) return 0;
+  const uint64_t blocks = (n + kScanTile - 1) / kScanTile;
+  if (blocks == 1) {
+    scan_downsweep_kernel<T, A><<<1, kScanThreads, 0, st>>>(in, out, n, nullptr);
+    AMRX_LAUNCH_CHECK();
+    return 1;
+  }
+  DevBuf sums;  // stream-ordered pool allocation: freed in stream order
+  sums.reserve(size_t(blocks) * sizeof(A), st);
+  scan_reduce_kernel<T, A><<<unsigned(blocks), kScanThreads, 0, st>>>(in, n, sums.as<A>());
+  AMRX_LAUNCH_CHECK();
+  int launches = 2 + scan_exclusive<A, A>(sums.as<A>(), sums.as<A>(), blocks, st);
+  scan_downsweep_kernel<T, A><<<unsigned(blocks), kScanThreads, 0, st>>>(in, out, n,
+                                                                        sums.as<A>());
+  AMRX_LAUNCH_CHECK();
+  return launches;
 }
 
 }  // namespace
@@ -256,7 +313,7 @@ PrepassResult ingest_prepass(const int4 *cells, uint64_t n, DevBuf &scratch,
     init.hi[a] = LLONG_MIN;
   }
   init.level_mask = 0;
-  scratch.reserve(sizeof(PrepassAcc));
+  scratch.reserve(sizeof(PrepassAcc), st);
   PrepassAcc *acc = scratch.as<PrepassAcc>();
   AMRX_CUDA(cudaMemcpyAsync(acc, &init, sizeof init, cudaMemcpyHostToDevice, st));
   prepass_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(cells, n, acc);
@@ -287,7 +344,7 @@ void ingest_order_check(const uint64_t *keys, uint64_t n, DevBuf &scratch,
                         uint64_t *descents, uint64_t *equal_pairs,
                         cudaStream_t st)
 {
-  scratch.reserve(16);
+  scratch.reserve(16, st);
   auto *out = scratch.as<unsigned long long>();
   AMRX_CUDA(cudaMemsetAsync(out, 0, 16, st));
   order_check_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(keys, n,
@@ -325,6 +382,15 @@ void build_directory(const uint64_t *keys, uint64_t n, const KeyGeom &g,
   scan_exclusive_u32(dir, dir, entries, scratch, st);
 }
 
+void build_level_map(const uint64_t *keys, uint64_t n, const KeyGeom &g,
+                     uint8_t *map, uint64_t map_bytes, cudaStream_t st)
+{
+  AMRX_CUDA(cudaMemsetAsync(map, 0, map_bytes, st));
+  level_map_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(
+    keys, n, g, reinterpret_cast<uint32_t *>(map));
+  AMRX_LAUNCH_CHECK();
+}
+
 void unpack_cells(const uint64_t *keys, uint64_t n, const KeyGeom &g,
                   int4 *cells, cudaStream_t st)
 {
@@ -333,30 +399,17 @@ void unpack_cells(const uint64_t *keys, uint64_t n, const KeyGeom &g,
   AMRX_LAUNCH_CHECK();
 }
 
-void scan_exclusive_u32(const uint32_t *in, uint32_t *out, uint64_t n,
-                        DevBuf &scratch, cudaStream_t st, int depth)
+int scan_exclusive_u32(const uint32_t *in, uint32_t *out, uint64_t n,
+                       DevBuf &, cudaStream_t st)
 {
-  if (n == 0) return;
-  const uint64_t blocks = (n + kScanTile - 1) / kScanTile;
-  if (blocks == 1) {
-    scan_downsweep_kernel<<<1, kScanThreads, 0, st>>>(in, out, n, nullptr);
-    AMRX_LAUNCH_CHECK();
-    return;
-  }
-  // block sums live in a per-depth slice of the scratch buffer
-  const uint64_t slot = (blocks + 1 + 255) & ~uint64_t(255);
-  const size_t need = size_t(slot) * sizeof(uint32_t);
-  DevBuf local;
-  local.reserve(need);
-  uint32_t *sums = local.as<uint32_t>();
-  scan_reduce_kernel<<<unsigned(blocks), kScanThreads, 0, st>>>(in, n, sums);
-  AMRX_LAUNCH_CHECK();
-  scan_exclusive_u32(sums, sums, blocks, scratch, st, depth + 1);
-  scan_downsweep_kernel<<<unsigned(blocks), kScanThreads, 0, st>>>(in, out, n,
-                                                                  sums);
-  AMRX_LAUNCH_CHECK();
-  // keep the block-sum buffer alive until the stream has consumed it
-  AMRX_CUDA(cudaStreamSynchronize(st));
+  return scan_exclusive<uint32_t, uint32_t>(in, out, n, st);
+}
+
+int scan_exclusive_u32_u64(const uint32_t *in, uint64_t *out, uint64_t n,
+                           DevBuf &, cudaStream_t st)
+{
+  return scan_exclusive<uint32_t, unsigned long long>(
+    in, reinterpret_cast<unsigned long long *>(out), n, st);
 }
 
 }  // namespace amrx

@@ -33,17 +33,29 @@ void note_launch();
     AMRX_CUDA(cudaGetLastError());                                       \
   } while (0)
 
-/// device allocation with RAII; grows on demand
+/*! device allocation with RAII, grows on demand.  Memory comes from the
+    device's stream-ordered pool (cudaMallocAsync) whose release threshold is
+    raised at index creation, so a buffer freed by one step is handed to the
+    next step's allocation without touching the driver. */
 struct DevBuf {
   void *ptr = nullptr;
   size_t bytes = 0;
+  cudaStream_t stream = nullptr;
   DevBuf() = default;
   DevBuf(const DevBuf &) = delete;
   DevBuf &operator=(const DevBuf &) = delete;
   ~DevBuf();
-  void reserve(size_t n);   // at least n bytes, contents not kept
+  void reserve(size_t n, cudaStream_t st = nullptr);  // contents not kept
   void release();
   template <typename T> T *as() const { return static_cast<T *>(ptr); }
+};
+
+/// keep pool memory cached across frees on this device (idempotent)
+void enable_pool_caching(int device);
+
+/// scratch an extraction keeps between calls
+struct ExtractScratch {
+  DevBuf ctl, tiles, stage_a, stage_b, scan;
 };
 
 // ------------------------------------------------------------ ingest.cu
@@ -77,13 +89,21 @@ void pad_keys(uint64_t *keys, uint64_t n, cudaStream_t st);
 void build_directory(const uint64_t *keys, uint64_t n, const KeyGeom &g,
                      uint32_t *dir, DevBuf &scratch, cudaStream_t st);
 
+/// block level map (KeyGeom::map_*): fill map (map bytes, zeroed here)
+void build_level_map(const uint64_t *keys, uint64_t n, const KeyGeom &g,
+                     uint8_t *map, uint64_t map_bytes, cudaStream_t st);
+
 /// unpack sorted keys into 4 x int32 cells
 void unpack_cells(const uint64_t *keys, uint64_t n, const KeyGeom &g,
                   int4 *cells, cudaStream_t st);
 
-/// exclusive scan of n u32 values (in place allowed); returns nothing
-void scan_exclusive_u32(const uint32_t *in, uint32_t *out, uint64_t n,
-                        DevBuf &scratch, cudaStream_t st, int depth = 0);
+/// exclusive scan of n u32 values (in place allowed); returns launches
+int scan_exclusive_u32(const uint32_t *in, uint32_t *out, uint64_t n,
+                       DevBuf &scratch, cudaStream_t st);
+
+/// exclusive scan of n u32 counts into u64 offsets; returns launches
+int scan_exclusive_u32_u64(const uint32_t *in, uint64_t *out, uint64_t n,
+                           DevBuf &scratch, cudaStream_t st);
 
 // -------------------------------------------------------------- sort.cu
 /// stable LSD radix sort of (keys, vals) over bits [0, key_bits); the
@@ -96,6 +116,7 @@ void radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
 struct ExtractRequest {
   SearchCtx s;
   KeyGeom g;
+  const uint8_t *lmap;
   const double *scal;
   uint64_t cell_begin, cell_end;
   bool emit_dual;
@@ -116,10 +137,11 @@ struct ExtractResult {
   uint64_t tris_written; // emit phase
   uint32_t error_flags;  // bit0 collapsed edge, bit1 undecided candidate
   float ms;              // device time of the extraction kernel
+  float ms2;             // device time of scan + reorder into final order
   uint64_t launches;
 };
 
-ExtractResult run_extract(const ExtractRequest &r, DevBuf &scratch,
+ExtractResult run_extract(const ExtractRequest &r, ExtractScratch &x,
                           cudaStream_t st);
 
 void run_find_exact(const SearchCtx &s, const KeyGeom &g, const int4 *cells,

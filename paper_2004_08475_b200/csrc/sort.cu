@@ -232,7 +232,7 @@ void radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
   const size_t hist_bytes = size_t(kMaxPasses) * kDigits * 4;
   const size_t offs_bytes = size_t(kMaxPasses) * kDigits * 8;
   const size_t state_bytes = size_t(tiles) * kDigits * 8;
-  scratch.reserve(hist_bytes + offs_bytes + 256 + state_bytes);
+  scratch.reserve(hist_bytes + offs_bytes + 256 + state_bytes, st);
   auto *base = scratch.as<unsigned char>();
   auto *hist = reinterpret_cast<unsigned int *>(base);
   auto *offs = reinterpret_cast<unsigned long long *>(base + hist_bytes);
