@@ -28,7 +28,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libamrx.so")
+# AMRX_LIB selects an alternate in-tree build (A/B experiments)
+LIB_PATH = os.environ.get("AMRX_LIB") or os.path.join(_HERE, "libamrx.so")
 
 AMRX_OK = 0
 AMRX_ERR_LOAD = 1

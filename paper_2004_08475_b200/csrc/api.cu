@@ -506,6 +506,7 @@ amrx_status amrx_index_destroy(amrx_index *index)
       index->xs.stage_a.release();
       index->xs.stage_b.release();
       index->xs.scan.release();
+      index->xs.bits.release();
       index->out_a.release();
       index->out_b.release();
       cudaStreamSynchronize(index->stream);

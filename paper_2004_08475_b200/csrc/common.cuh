@@ -245,6 +245,47 @@ static __device__ __noinline__ int64_t find_in_bucket(const SearchCtx &s, uint64
   return res;
 }
 
+/*! Per-lane lookup of NQ ascending keys inside their own directory buckets
+    (no warp cooperation): with ~2 directory entries per cell a bucket
+    holds a handful of keys, so each query costs two directory loads and a
+    short binary search through L1-cached key loads.  Same contract as
+    warp_find (exact hit, or under FINER the first same-anchor lower-level
+    key).  Consecutive queries resume from the previous lower_bound. */
+template <int NQ, bool FINER>
+__device__ __forceinline__ void lane_find(const SearchCtx &s, const uint64_t (&q)[NQ],
+                                          const bool (&valid)[NQ],
+                                          int64_t (&out)[NQ], int (&lvl)[NQ])
+{
+  uint64_t prev_p = 0;
+  uint64_t prev_q = 0;
+#pragma unroll
+  for (int t = 0; t < NQ; t++) {
+    if (!valid[t]) continue;
+    const uint64_t anchor = q[t] & ~s.lmask;
+    uint64_t lo = __ldg(s.dir + ((FINER ? anchor : q[t]) >> s.dir_shift));
+    const uint64_t hi = __ldg(s.dir + (q[t] >> s.dir_shift) + 1);
+    const uint64_t from = (t > 0 && prev_q <= q[t] && prev_p > lo) ? prev_p : lo;
+    const uint64_t p = global_lower_bound(s.keys, from, hi, q[t]);
+    prev_p = p;
+    prev_q = q[t];
+    int64_t res = -1;
+    int rl = 0;
+    if (p < hi && ldg_u64(s.keys + p) == q[t]) {
+      res = int64_t(p);
+      rl = int(q[t] & s.lmask);
+    } else if (FINER) {
+      uint64_t x = p;
+      while (x > lo && (ldg_u64(s.keys + x - 1) & ~s.lmask) == anchor) x--;
+      if (x < p) {
+        res = int64_t(x);
+        rl = int(ldg_u64(s.keys + x) & s.lmask);
+      }
+    }
+    out[t] = res;
+    lvl[t] = rl + s.shift;
+  }
+}
+
 /// lower_bound of q in win[from, cnt), galloping from `from`
 __device__ __forceinline__ int gallop_lower_bound(const uint64_t *win, int from,
                                                   int cnt, uint64_t q)

@@ -34,6 +34,11 @@
 #include <cstdio>
 #include <cstdlib>
 
+// 1: per-lane bucket search (lane_find); 0: warp-cooperative windows (warp_find)
+#ifndef AMRX_LANE_SEARCH
+#define AMRX_LANE_SEARCH 1
+#endif
+
 namespace amrx {
 
 namespace {
@@ -112,6 +117,20 @@ __device__ __forceinline__ uint64_t reserve(uint64_t *cur_end, uint32_t agg,
 /*! move each tile's block from its staging position to its place in
     candidate order (final offset = exclusive scan of tile counts): one warp
     per tile, `words` 32-bit words per item, coalesced both ways */
+/// bit i of the result: scalar i > iso (the strict case test of contour.cpp:22-28)
+__global__ void __launch_bounds__(256)
+sign_bits_kernel(const double *__restrict__ scal, uint64_t n, double iso,
+                 uint32_t *__restrict__ bits)
+{
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u);
+       base < n; base += stride) {
+    const uint64_t r = base + (threadIdx.x & 31);
+    const uint32_t word = __ballot_sync(kFull, r < n && __ldg(scal + r) > iso);
+    if ((threadIdx.x & 31) == 0) bits[base >> 5] = word;
+  }
+}
+
 __global__ void __launch_bounds__(256)
 reorder_kernel(const uint32_t *__restrict__ cnt, const uint64_t *__restrict__ src_off,
                const uint64_t *__restrict__ dst_off, uint32_t tiles, int words,
@@ -142,6 +161,7 @@ struct KArgs {
   SearchCtx s;
   KeyGeom g;
   const uint8_t *lmap;  // block level map (g.map_on)
+  const uint32_t *above;  // bit i: scalar i > iso (EMIT_TRI)
   const double *scal;
   uint64_t cell_begin, cell_end;
   uint32_t num_tiles;
@@ -175,6 +195,45 @@ struct Smem {
   uint32_t remain[8][9];
 };
 
+/// slot-numbered corner mask -> table row (mc::to_table_case, mc_tables.cpp:324-330)
+__device__ __forceinline__ int table_row(uint32_t mask)
+{
+  int row = 0;
+#pragma unroll
+  for (int t = 0; t < 8; t++)
+    if (mask & (1u << ((AMRX_MC_TABLE_CORNER >> (3 * t)) & 7))) row |= 1 << t;
+  return row;
+}
+
+/*! a tile wrote each lane's triangles at its upper-bound offset `from`;
+    slivers left gaps, so move every lane's run to its exact offset `to`
+    (to <= from), lanes in order so a left shift never overwrites unread
+    data.  Whole warp; rare. */
+template <bool F32>
+__device__ __noinline__ void compact_tile(void *xyz, uint64_t cap, uint64_t from,
+                                          uint64_t to, uint32_t count)
+{
+  const int lane = int(lane_id());
+  const int words = F32 ? 9 : 18;  // 32-bit words per triangle
+  uint32_t *base = static_cast<uint32_t *>(xyz);
+  for (int src = 0; src < 32; src++) {
+    const uint64_t f = __shfl_sync(kFull, (unsigned long long)from, src);
+    const uint64_t t = __shfl_sync(kFull, (unsigned long long)to, src);
+    const uint32_t n = __shfl_sync(kFull, count, src);
+    if (f == t || n == 0) continue;
+    const uint64_t keep = f + n <= cap ? n : (f < cap ? cap - f : 0);
+    const uint64_t nw = keep * uint64_t(words);
+    for (uint64_t w0 = 0; w0 < nw; w0 += 32) {
+      const uint64_t w = w0 + uint64_t(lane);
+      uint32_t v = 0;
+      if (w < nw) v = base[f * words + w];
+      __syncwarp();
+      if (w < nw) base[t * words + w] = v;
+      __syncwarp();
+    }
+  }
+}
+
 /// centre of the corner cell: anchor + half width, in double (core.hpp:113-118)
 __device__ __forceinline__ double centre(int64_t anchor, int level)
 {
@@ -203,12 +262,7 @@ __device__ __noinline__ int mc_dual(const KArgs &a, const Smem &sm, int warp, in
     val[d] = __ldg(a.scal + ids[d]);
     if (val[d] > iso) mask |= 1 << d;
   }
-  // slot mask -> table row (mc_tables.cpp:324-330)
-  int row = 0;
-#pragma unroll
-  for (int t = 0; t < 8; t++)
-    if (mask & (1 << ((AMRX_MC_TABLE_CORNER >> (3 * t)) & 7))) row |= 1 << t;
-  const uint64_t word = sm.mc_rows[row];
+  const uint64_t word = sm.mc_rows[table_row(uint32_t(mask))];
   const int ntab = int(word & 15);
   if (ntab == 0) return 0;
 
@@ -273,7 +327,11 @@ __device__ __noinline__ void find3_coarse(const SearchCtx &s, const uint64_t (&q
                                           const bool (&v)[3], int64_t (&o)[3],
                                           int (&l)[3], uint64_t *win)
 {
+#if AMRX_LANE_SEARCH
+  lane_find<3, false>(s, q, v, o, l);
+#else
   warp_find<3, false>(s, q, v, o, l, win);
+#endif
 }
 
 /*! resolve the three stencil points of column COL (dx, dy fixed; dz =
@@ -318,8 +376,12 @@ __device__ __forceinline__ void resolve_column(const KArgs &a, Smem &sm,
     q[t] = base | (g.bits[2] ? uint64_t((pz - g.mn[2]) >> g.shift) << g.sh[2] : 0);
     cand[t] &= ~le_hint;  // what is left for step 2
   }
+#if AMRX_LANE_SEARCH
+  lane_find<3, true>(a.s, q, v, out, lvl);
+#else
   if (__any_sync(kFull, v[0] || v[1] || v[2]))
     warp_find<3, true>(a.s, q, v, out, lvl, sm.win[warp]);
+#endif
 
   // step 2: coarser candidate levels, ascending (= the reference's finest
   // first order restricted to the levels above the hint)
@@ -427,7 +489,10 @@ __device__ __forceinline__ void advance(uint32_t resolved, uint64_t status,
 }
 
 template <bool EMIT_DUAL, bool EMIT_TRI, bool F32>
-__global__ void __launch_bounds__(kThreads, 3)
+#ifndef AMRX_MINB
+#define AMRX_MINB 3  // CTAs per SM the register budget is sized for
+#endif
+__global__ void __launch_bounds__(kThreads, AMRX_MINB)
 extract_kernel(const KArgs a)
 {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -484,16 +549,30 @@ extract_kernel(const KArgs a)
     }
     if (alive) err |= 2u;
 
-    // ---- count (pass 1), reserve staging space, emit (pass 2).  No
-    // waiting on other tiles: the tile's block goes to this warp's private
-    // chunk of the staging arena and (offset, count) to the tile table;
-    // reorder_kernel later moves blocks into candidate order.
+    // ---- pass 1 + pass 2 fused.  No waiting on other tiles: the tile's
+    // block goes to this warp's private chunk of the staging arena and
+    // (offset, count) to the tile table; reorder_kernel later moves blocks
+    // into candidate order (the reference's prefix sum, pipeline.cpp:109-114).
     const uint32_t nd = __popc(accepted);
-    uint32_t nt = 0;
-    if (EMIT_TRI)
-      for (uint32_t m = accepted; m; m &= m - 1)
-        nt += mc_dual<F32>(a, sm, warp, lane, c, __ffs(m) - 1, a.iso, false,
-                              nullptr, 0, 0, err);
+    uint32_t upper = 0, cross = 0;
+    if (EMIT_TRI) {
+      // duals whose 8 corners all classify alike carry no triangle: decide
+      // from the sign bits (value > iso, contour.cpp:22-28) before touching
+      // the FP64 scalars; the case row's table count bounds the triangles
+      for (uint32_t m = accepted; m; m &= m - 1) {
+        const int delta = __ffs(m) - 1;
+        uint32_t mask = 0;
+#pragma unroll
+        for (int d = 0; d < 8; d++) {
+          const uint32_t id = sm.id[warp][point_of(delta, d)][lane];
+          mask |= ((__ldg(a.above + (id >> 5)) >> (id & 31)) & 1u) << d;
+        }
+        if (mask != 0 && mask != 0xffu) {
+          cross |= 1u << delta;
+          upper += uint32_t(sm.mc_rows[table_row(mask)] & 15);
+        }
+      }
+    }
     // tile totals into the warp's accumulators (16-bit fields cannot carry:
     // 32 lanes x 8 candidates)
     {
@@ -533,23 +612,26 @@ extract_kernel(const KArgs a)
       }
     }
     if (EMIT_TRI) {
-      const uint32_t incl = warp_incl_scan(nt);
-      const uint32_t agg = __shfl_sync(kFull, incl, 31);
-      const uint64_t base =
-        reserve(&sm.chunk[warp][2], agg, kTriChunk, a.out + 9) + (incl - nt);
+      // reserve the table's upper bound, emit each crossing dual once, then
+      // close the gaps slivers left (contour.cpp:80-84 drops them; rare)
+      const uint32_t incl = warp_incl_scan(upper);
+      const uint32_t agg_up = __shfl_sync(kFull, incl, 31);
+      const uint64_t block =
+        reserve(&sm.chunk[warp][2], agg_up, kTriChunk, a.out + 9);
+      const uint64_t start = block + (incl - upper);
+      uint32_t wrote = 0;
+      for (uint32_t m = cross; m; m &= m - 1)
+        wrote += mc_dual<F32>(a, sm, warp, lane, c, __ffs(m) - 1, a.iso, true,
+                              a.xyz, start + wrote, a.tri_cap, err);
+      const uint32_t incl_w = warp_incl_scan(wrote);
+      const uint32_t agg = __shfl_sync(kFull, incl_w, 31);
+      if (agg != agg_up)
+        compact_tile<F32>(a.xyz, a.tri_cap, start, block + (incl_w - wrote), wrote);
       if (lane == 0) {
         a.tile_tri_cnt[tile] = agg;
-        a.tile_tri_off[tile] = base;
-      }
-      uint32_t wrote = 0;
-      if (agg)
-        for (uint32_t m = accepted; m; m &= m - 1)
-          wrote += mc_dual<F32>(a, sm, warp, lane, c, __ffs(m) - 1, a.iso, true,
-                                 a.xyz, base + wrote, a.tri_cap, err);
-      const uint32_t tw = __reduce_add_sync(kFull, wrote);
-      if (lane == 0) {
+        a.tile_tri_off[tile] = block;
         sm.acc[warp][5] += agg;
-        sm.acc[warp][6] += tw;
+        sm.acc[warp][6] += agg;
       }
     }
     __syncwarp();
@@ -772,19 +854,25 @@ ExtractResult run_extract(const ExtractRequest &r, ExtractScratch &x,
 
   // staging capacity: what the caller can take plus one chunk per warp of
   // slack for partially used chunks (so a fitting result never overflows)
-  const uint64_t dual_stage = D && r.corners ? r.dual_cap + warps * kDualChunk : 0;
-  const uint64_t tri_stage = T && r.xyz ? r.tri_cap + warps * kTriChunk : 0;
+  uint64_t dual_stage = D && r.corners ? r.dual_cap + warps * kDualChunk : 0;
+  uint64_t tri_stage = T && r.xyz ? r.tri_cap + warps * kTriChunk : 0;
   const int tri_words = F ? 9 : 18;  // 32-bit words per triangle
-  if (dual_stage) {
-    x.stage_a.reserve(dual_stage * 32, st);
-    x.stage_b.reserve(dual_stage * 8, st);
-  }
-  if (tri_stage) x.stage_a.reserve(tri_stage * tri_words * 4, st);
 
   KArgs k;
   k.s = r.s;
   k.g = r.g;
   k.lmap = r.lmap;
+  k.above = nullptr;
+  if (T) {
+    const uint64_t words = (r.s.n + 31) / 32;
+    x.bits.reserve(words * 4 + 64, st);
+    k.above = x.bits.as<uint32_t>();
+    const int bgrid = int(std::min<uint64_t>((words + 7) / 8, uint64_t(device_sm_count()) * 16));
+    sign_bits_kernel<<<std::max(1, bgrid), 256, 0, st>>>(r.scal, r.s.n, r.iso,
+                                                         x.bits.as<uint32_t>());
+    AMRX_LAUNCH_CHECK();
+    res.launches += 1;
+  }
   k.scal = r.scal;
   k.cell_begin = r.cell_begin;
   k.cell_end = r.cell_end;
@@ -808,20 +896,40 @@ ExtractResult run_extract(const ExtractRequest &r, ExtractScratch &x,
   AMRX_CUDA(cudaEventCreate(&e0));
   AMRX_CUDA(cudaEventCreate(&e1));
   AMRX_CUDA(cudaEventCreate(&e2));
-  AMRX_CUDA(cudaEventRecord(e0, st));
-  if (tiles) {
-    if (D && T && F) launch_extract<true, true, true>(k, grid, st);
-    else if (D && T) launch_extract<true, true, false>(k, grid, st);
-    else if (D) launch_extract<true, false, false>(k, grid, st);
-    else if (T && F) launch_extract<false, true, true>(k, grid, st);
-    else if (T) launch_extract<false, true, false>(k, grid, st);
-    else launch_extract<false, false, false>(k, grid, st);
-    res.launches = 1;
-  }
-  AMRX_CUDA(cudaEventRecord(e1, st));
   unsigned long long h[10];
-  AMRX_CUDA(cudaMemcpyAsync(h, ctl, sizeof h, cudaMemcpyDeviceToHost, st));
-  AMRX_CUDA(cudaStreamSynchronize(st));
+  for (int attempt = 0;; attempt++) {
+    if (dual_stage) {
+      x.stage_a.reserve(dual_stage * 32, st);
+      x.stage_b.reserve(dual_stage * 8, st);
+    }
+    if (tri_stage) x.stage_a.reserve(tri_stage * tri_words * 4, st);
+    k.corners = dual_stage ? x.stage_a.as<uint32_t>() : nullptr;
+    k.tasks = dual_stage ? x.stage_b.as<uint64_t>() : nullptr;
+    k.dual_cap = dual_stage;
+    k.xyz = tri_stage ? x.stage_a.ptr : nullptr;
+    k.tri_cap = tri_stage;
+    if (attempt) AMRX_CUDA(cudaMemsetAsync(ctl, 0, 256, st));
+    AMRX_CUDA(cudaEventRecord(e0, st));
+    if (tiles) {
+      if (D && T && F) launch_extract<true, true, true>(k, grid, st);
+      else if (D && T) launch_extract<true, true, false>(k, grid, st);
+      else if (D) launch_extract<true, false, false>(k, grid, st);
+      else if (T && F) launch_extract<false, true, true>(k, grid, st);
+      else if (T) launch_extract<false, true, false>(k, grid, st);
+      else launch_extract<false, false, false>(k, grid, st);
+      res.launches += 1;
+    }
+    AMRX_CUDA(cudaEventRecord(e1, st));
+    AMRX_CUDA(cudaMemcpyAsync(h, ctl, sizeof h, cudaMemcpyDeviceToHost, st));
+    AMRX_CUDA(cudaStreamSynchronize(st));
+    // the staging arena ran out although the result fits the caller's
+    // buffer (upper-bound reservations): grow it and run again
+    const bool dual_short = dual_stage && h[8] > dual_stage && h[4] <= r.dual_cap;
+    const bool tri_short = tri_stage && h[9] > tri_stage && h[6] <= r.tri_cap;
+    if (attempt || (!dual_short && !tri_short)) break;
+    if (dual_short) dual_stage = h[8] + warps * kDualChunk;
+    if (tri_short) tri_stage = h[9] + warps * kTriChunk;
+  }
   for (int i = 0; i < 4; i++) res.counters[i] = h[i];
   res.duals = h[4];
   res.tris_counted = h[5];

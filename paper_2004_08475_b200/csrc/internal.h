@@ -55,7 +55,7 @@ void enable_pool_caching(int device);
 
 /// scratch an extraction keeps between calls
 struct ExtractScratch {
-  DevBuf ctl, tiles, stage_a, stage_b, scan;
+  DevBuf ctl, tiles, stage_a, stage_b, scan, bits;
 };
 
 // ------------------------------------------------------------ ingest.cu
