@@ -62,6 +62,29 @@ bool is_device_ptr(const void *p)
   return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
 }
 
+/// the pointer itself if it is device memory (inputs: staged otherwise)
+const void *device_view(const void *p)
+{
+  return is_device_ptr(p) ? p : nullptr;
+}
+
+/*! a device-writable alias of an output pointer: device memory, or pinned
+    (page-locked, mapped) host memory the kernels can stream into directly
+    over the host link; nullptr for pageable host memory */
+void *device_writable(void *p)
+{
+  if (!p) return nullptr;
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged)
+    return p;
+  if (attr.type == cudaMemoryTypeHost && attr.devicePointer) return attr.devicePointer;
+  return nullptr;
+}
+
 int bit_width(uint64_t v)
 {
   int b = 0;
@@ -167,6 +190,83 @@ void enable_pool_caching(int device)
 
 namespace {
 std::atomic<uint64_t> g_launches{0};
+
+struct WsDevice {
+  std::mutex mu;
+  void *ptr[kWsCount] = {};
+  size_t bytes[kWsCount] = {};
+  bool busy[kWsCount] = {};
+};
+
+WsDevice &ws_device(int dev)
+{
+  static WsDevice devices[64];
+  return devices[dev & 63];
+}
+}  // namespace
+
+void *WsLease::get(int slot, size_t n, cudaStream_t st)
+{
+  if (ptr && bytes >= n) return ptr;
+  if (ptr && slot_ >= 0) {
+    // grow a slot this lease holds (rare)
+    WsDevice &w = ws_device(device_);
+    std::lock_guard<std::mutex> lock(w.mu);
+    AMRX_CUDA(cudaDeviceSynchronize());
+    cudaFree(w.ptr[slot_]);
+    w.ptr[slot_] = nullptr;
+    w.bytes[slot_] = 0;
+    AMRX_CUDA(cudaMalloc(&w.ptr[slot_], n));
+    w.bytes[slot_] = n;
+    ptr = w.ptr[slot_];
+    bytes = n;
+    return ptr;
+  }
+  if (ptr) {
+    own_.reserve(n, st);
+    ptr = own_.ptr;
+    bytes = own_.bytes;
+    return ptr;
+  }
+  int dev = 0;
+  AMRX_CUDA(cudaGetDevice(&dev));
+  WsDevice &w = ws_device(dev);
+  {
+    std::lock_guard<std::mutex> lock(w.mu);
+    if (!w.busy[slot]) {
+      if (w.bytes[slot] < n) {
+        // grow (rare): the slot outlives every stream, so plain cudaMalloc
+        if (w.ptr[slot]) {
+          AMRX_CUDA(cudaDeviceSynchronize());
+          cudaFree(w.ptr[slot]);
+          w.ptr[slot] = nullptr;
+          w.bytes[slot] = 0;
+        }
+        const size_t want = std::max<size_t>(n, 256);
+        AMRX_CUDA(cudaMalloc(&w.ptr[slot], want));
+        w.bytes[slot] = want;
+      }
+      w.busy[slot] = true;
+      device_ = dev;
+      slot_ = slot;
+      ptr = w.ptr[slot];
+      bytes = w.bytes[slot];
+      return ptr;
+    }
+  }
+  own_.reserve(n, st);
+  ptr = own_.ptr;
+  bytes = own_.bytes;
+  return ptr;
+}
+
+WsLease::~WsLease()
+{
+  if (slot_ >= 0) {
+    WsDevice &w = ws_device(device_);
+    std::lock_guard<std::mutex> lock(w.mu);
+    w.busy[slot_] = false;
+  }
 }
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -195,7 +295,6 @@ struct amrx_index {
   KeyGeom g{};
   int64_t bounds_hi[3] = {0, 0, 0};
   DevBuf keys, scal, dir, lmap, scratch;
-  ExtractScratch xs;
   amrx_index_info info{};
   // last extraction kept on the device for the count-then-copy pattern
   struct Cached {
@@ -426,13 +525,47 @@ amrx_status amrx_index_create(const int32_t *cells4, const double *scalars,
     AMRX_CUDA(cudaEventCreate(&e1));
     AMRX_CUDA(cudaEventRecord(e0, st));
 
-    DevIn<int4> cells(reinterpret_cast<const int4 *>(cells4), n, st);
-    DevIn<double> sc(scalars, n, st);
+    // inputs: device pointers are used in place; host arrays are staged
+    // into workspace slots.  The scalar upload runs on a side stream so it
+    // overlaps the pack + radix sort (the scalars are first needed by the
+    // gather that follows the sort).
+    WsLease l_cells, l_scal, l_idx, l_kalt, l_ialt, l_sort;
+    const int4 *cells_d = reinterpret_cast<const int4 *>(device_view(cells4));
+    if (!cells_d) {
+      cells_d = static_cast<const int4 *>(l_cells.get(kWsCells, n * 16, st));
+      AMRX_CUDA(cudaMemcpyAsync(const_cast<int4 *>(cells_d), cells4, n * 16,
+                                cudaMemcpyHostToDevice, st));
+    }
+    const double *sc_d = static_cast<const double *>(device_view(scalars));
+    cudaStream_t aux = nullptr;
+    cudaEvent_t sc_ready = nullptr;
+    if (!sc_d) {
+      sc_d = static_cast<const double *>(l_scal.get(kWsScal, n * 8, st));
+      AMRX_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+      AMRX_CUDA(cudaEventCreateWithFlags(&sc_ready, cudaEventDisableTiming));
+      AMRX_CUDA(cudaEventRecord(sc_ready, st));  // slot free in st order
+      AMRX_CUDA(cudaStreamWaitEvent(aux, sc_ready, 0));
+      AMRX_CUDA(cudaMemcpyAsync(const_cast<double *>(sc_d), scalars, n * 8,
+                                cudaMemcpyHostToDevice, aux));
+      AMRX_CUDA(cudaEventRecord(sc_ready, aux));
+    }
+    struct AuxGuard {
+      cudaStream_t s;
+      cudaEvent_t e;
+      ~AuxGuard()
+      {
+        if (s) {
+          cudaStreamSynchronize(s);
+          cudaStreamDestroy(s);
+        }
+        if (e) cudaEventDestroy(e);
+      }
+    } aux_guard{aux, sc_ready};
 
-    const PrepassResult pre = ingest_prepass(cells.ptr, n, ix->scratch, st);
+    const PrepassResult pre = ingest_prepass(cells_d, n, ix->scratch, st);
     if (pre.first_bad != ~0ull) {
       int4 c;
-      AMRX_CUDA(cudaMemcpy(&c, cells.ptr + pre.first_bad, sizeof c,
+      AMRX_CUDA(cudaMemcpy(&c, cells_d + pre.first_bad, sizeof c,
                            cudaMemcpyDeviceToHost));
       const std::string rec = "record " + std::to_string(pre.first_bad);
       if (c.w < 0 || c.w > kMaxLevel)
@@ -449,30 +582,28 @@ amrx_status amrx_index_create(const int32_t *cells4, const double *scalars,
     for (int a = 0; a < 3; a++) ix->bounds_hi[a] = pre.hi[a];
 
     ix->keys.reserve((n + kKeyPad) * sizeof(uint64_t), st);
-    DevBuf idx, keys_alt, idx_alt;
-    idx.reserve(n * sizeof(uint32_t), st);
-    ingest_pack(cells.ptr, n, ix->g, ix->keys.as<uint64_t>(), idx.as<uint32_t>(), st);
-    cells.stage.release();
+    uint32_t *idx = static_cast<uint32_t *>(l_idx.get(kWsIdx, n * 4, st));
+    ingest_pack(cells_d, n, ix->g, ix->keys.as<uint64_t>(), idx, st);
 
     uint64_t desc = 0, eq = 0;
     ingest_order_check(ix->keys.as<uint64_t>(), n, ix->scratch, &desc, &eq, st);
     ix->scal.reserve(n * sizeof(double), st);
     if (desc == 0) {
       // already in (i,j,k,level) order; stable ties mean identity
-      AMRX_CUDA(cudaMemcpyAsync(ix->scal.ptr, sc.ptr, n * sizeof(double),
+      if (sc_ready) AMRX_CUDA(cudaStreamWaitEvent(st, sc_ready, 0));
+      AMRX_CUDA(cudaMemcpyAsync(ix->scal.ptr, sc_d, n * sizeof(double),
                                 cudaMemcpyDeviceToDevice, st));
     } else {
       if (opts && (opts->flags & AMRX_FLAG_PRESORTED))
         fail(AMRX_ERR_INVALID_ARG, "input flagged presorted is not sorted");
-      keys_alt.reserve(n * sizeof(uint64_t), st);
-      idx_alt.reserve(n * sizeof(uint32_t), st);
+      auto *keys_alt = static_cast<uint64_t *>(l_kalt.get(kWsKeysAlt, n * 8, st));
+      auto *idx_alt = static_cast<uint32_t *>(l_ialt.get(kWsIdxAlt, n * 4, st));
+      void *sort_scratch = l_sort.get(kWsSort, radix_sort_scratch_bytes(n), st);
       int passes = 0;
-      radix_sort_pairs(ix->keys.as<uint64_t>(), idx.as<uint32_t>(),
-                       keys_alt.as<uint64_t>(), idx_alt.as<uint32_t>(), n,
-                       ix->g.total, ix->scratch, st, &passes);
-      keys_alt.release();
-      idx_alt.release();
-      gather_f64(idx.as<uint32_t>(), sc.ptr, ix->scal.as<double>(), n, st);
+      radix_sort_pairs(ix->keys.as<uint64_t>(), idx, keys_alt, idx_alt, n,
+                       ix->g.total, sort_scratch, st, &passes);
+      if (sc_ready) AMRX_CUDA(cudaStreamWaitEvent(st, sc_ready, 0));
+      gather_f64(idx, sc_d, ix->scal.as<double>(), n, st);
       uint64_t d2 = 0;
       ingest_order_check(ix->keys.as<uint64_t>(), n, ix->scratch, &d2, &eq, st);
       if (d2 != 0) fail(AMRX_ERR_INTERNAL, "radix sort left keys out of order");
@@ -501,12 +632,6 @@ amrx_status amrx_index_destroy(amrx_index *index)
       index->dir.release();
       index->lmap.release();
       index->scratch.release();
-      index->xs.ctl.release();
-      index->xs.tiles.release();
-      index->xs.stage_a.release();
-      index->xs.stage_b.release();
-      index->xs.scan.release();
-      index->xs.bits.release();
       index->out_a.release();
       index->out_b.release();
       cudaStreamSynchronize(index->stream);
@@ -678,9 +803,10 @@ amrx_status amrx_extract_dual(amrx_index *index, const amrx_range *range,
     check_range(index, range, b, e);
     const uint64_t cells = e - b;
     auto &C = index->cache;
-    const bool dev_out = corners8 && is_device_ptr(corners8);
-    if (dev_out && task_ids && !is_device_ptr(task_ids))
-      fail(AMRX_ERR_INVALID_ARG, "corners8 and task_ids must both be device or host");
+    // device memory or pinned host memory: written in place by the kernels
+    uint32_t *corners_w = static_cast<uint32_t *>(device_writable(corners8));
+    uint64_t *tasks_w = static_cast<uint64_t *>(device_writable(task_ids));
+    const bool dev_out = corners_w && (!task_ids || tasks_w);
 
     ExtractRequest rq{};
     rq.s = index->ctx();
@@ -691,10 +817,11 @@ amrx_status amrx_extract_dual(amrx_index *index, const amrx_range *range,
     rq.cell_end = e;
     rq.emit_dual = true;
     if (dev_out) {
-      rq.corners = corners8;
-      rq.tasks = task_ids;
+      rq.final_host = !is_device_ptr(corners8);
+      rq.corners = rq.final_host ? corners8 : corners_w;
+      rq.tasks = rq.final_host ? task_ids : tasks_w;
       rq.dual_cap = cap;
-      const ExtractResult r = run_extract(rq, index->xs, st);
+      const ExtractResult r = run_extract(rq, st);
       check_result(r, cells, false);
       fill_stats(stats, r, cells);
       *count = r.duals;
@@ -714,7 +841,7 @@ amrx_status amrx_extract_dual(amrx_index *index, const amrx_range *range,
         rq.corners = index->out_a.as<uint32_t>();
         rq.tasks = index->out_b.as<uint64_t>();
         rq.dual_cap = arena;
-        const ExtractResult r = run_extract(rq, index->xs, st);
+        const ExtractResult r = run_extract(rq, st);
         check_result(r, cells, false);
         if (r.duals <= arena) {
           C.valid = true;
@@ -758,7 +885,9 @@ amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range,
     const uint64_t cells = e - b;
     const size_t tri_bytes = params->xyz_is_f32 ? 36 : 72;
     auto &C = index->cache;
-    const bool dev_out = xyz9 && is_device_ptr(xyz9);
+    // device memory or pinned host memory: written in place by the kernels
+    void *xyz_w = device_writable(xyz9);
+    const bool dev_out = xyz_w != nullptr;
 
     ExtractRequest rq{};
     rq.s = index->ctx();
@@ -776,9 +905,10 @@ amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range,
         fail(AMRX_ERR_LENGTH, "extract_isosurface: mesh too large for 32-bit indices");
     };
     if (dev_out) {
-      rq.xyz = xyz9;
+      rq.final_host = !is_device_ptr(xyz9);
+      rq.xyz = rq.final_host ? xyz9 : xyz_w;
       rq.tri_cap = cap;
-      const ExtractResult r = run_extract(rq, index->xs, st);
+      const ExtractResult r = run_extract(rq, st);
       check_result(r, cells, true);
       fill_stats(stats, r, cells);
       *count = r.tris_written;
@@ -797,7 +927,7 @@ amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range,
         index->out_a.reserve(arena * tri_bytes, st);
         rq.xyz = index->out_a.ptr;
         rq.tri_cap = arena;
-        const ExtractResult r = run_extract(rq, index->xs, st);
+        const ExtractResult r = run_extract(rq, st);
         check_result(r, cells, true);
         if (r.tris_written <= arena) {
           C.valid = true;

@@ -822,9 +822,9 @@ int occupancy_grid()
 
 }  // namespace
 
-ExtractResult run_extract(const ExtractRequest &r, ExtractScratch &x,
-                          cudaStream_t st)
+ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
 {
+  ExtractScratch x;
   ExtractResult res{};
   const uint64_t cells = r.cell_end > r.cell_begin ? r.cell_end - r.cell_begin : 0;
   const uint64_t tiles = (cells + 31) / 32;
@@ -950,24 +950,52 @@ ExtractResult run_extract(const ExtractRequest &r, ExtractScratch &x,
 
   // pass 2 of the reference's scheme: exclusive scan of the tile counts
   // gives every tile its final offset; blocks move into candidate order
+  // A pinned host destination is filled by one bulk copy from a device
+  // buffer (full host-link bandwidth) rather than by the reorder kernel's
+  // scattered stores across the link.
   const int rgrid = int(std::min<uint64_t>((tiles + 7) / 8, uint64_t(device_sm_count()) * 16));
+  WsBuf host_a(kWsOutA), host_b(kWsOutB);
   if (tiles && dual_stage && res.duals > 0) {
     res.launches += scan_exclusive_u32_u64(dual_cnt, final_off, tiles, x.scan, st);
+    const uint64_t keep = std::min(res.duals, r.dual_cap);
+    uint32_t *dc = r.corners;
+    uint64_t *dt = r.tasks;
+    if (r.final_host) {
+      host_a.reserve(keep * 32 + 16, st);
+      dc = host_a.as<uint32_t>();
+      if (r.tasks) {
+        host_b.reserve(keep * 8 + 16, st);
+        dt = host_b.as<uint64_t>();
+      }
+    }
     reorder_kernel<<<std::max(1, rgrid), 256, 0, st>>>(
       dual_cnt, dual_off, final_off, uint32_t(tiles), 8, x.stage_a.as<uint32_t>(),
-      r.corners, r.dual_cap, r.tasks ? 2 : 0, x.stage_b.as<uint32_t>(),
-      reinterpret_cast<uint32_t *>(r.tasks));
+      dc, r.dual_cap, r.tasks ? 2 : 0, x.stage_b.as<uint32_t>(),
+      reinterpret_cast<uint32_t *>(dt));
     AMRX_LAUNCH_CHECK();
     res.launches += 1;
+    if (r.final_host) {
+      AMRX_CUDA(cudaMemcpyAsync(r.corners, dc, keep * 32, cudaMemcpyDeviceToHost, st));
+      if (r.tasks)
+        AMRX_CUDA(cudaMemcpyAsync(r.tasks, dt, keep * 8, cudaMemcpyDeviceToHost, st));
+    }
   }
   if (tiles && tri_stage && res.tris_written > 0) {
     res.launches += scan_exclusive_u32_u64(tri_cnt, final_off, tiles, x.scan, st);
+    const uint64_t keep = std::min(res.tris_written, r.tri_cap);
+    uint32_t *dx = static_cast<uint32_t *>(r.xyz);
+    if (r.final_host) {
+      host_a.reserve(keep * tri_words * 4 + 16, st);
+      dx = host_a.as<uint32_t>();
+    }
     reorder_kernel<<<std::max(1, rgrid), 256, 0, st>>>(
       tri_cnt, tri_off, final_off, uint32_t(tiles), tri_words,
-      x.stage_a.as<uint32_t>(), static_cast<uint32_t *>(r.xyz), r.tri_cap, 0,
-      nullptr, nullptr);
+      x.stage_a.as<uint32_t>(), dx, r.tri_cap, 0, nullptr, nullptr);
     AMRX_LAUNCH_CHECK();
     res.launches += 1;
+    if (r.final_host)
+      AMRX_CUDA(cudaMemcpyAsync(r.xyz, dx, keep * tri_words * 4,
+                                cudaMemcpyDeviceToHost, st));
   }
   AMRX_CUDA(cudaEventRecord(e2, st));
   AMRX_CUDA(cudaStreamSynchronize(st));

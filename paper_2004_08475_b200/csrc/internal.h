@@ -53,9 +53,48 @@ struct DevBuf {
 /// keep pool memory cached across frees on this device (idempotent)
 void enable_pool_caching(int device);
 
-/// scratch an extraction keeps between calls
+/*! Per-device workspace: the large temporaries of ingest and extraction
+    (staged inputs, sort ping-pong buffers, output staging arenas) live in
+    process-wide slots that only grow, so a pipeline that builds and drops
+    an index per batch allocates nothing in steady state.  A lease holds a
+    slot exclusively until it is destroyed; if the slot is busy (another
+    thread) the lease falls back to a private allocation. */
+enum WsSlot {
+  kWsCells, kWsScal, kWsIdx, kWsKeysAlt, kWsIdxAlt, kWsSort, kWsStageA,
+  kWsStageB, kWsTiles, kWsBits, kWsCtl, kWsScratch, kWsOutA, kWsOutB, kWsCount
+};
+
+struct WsLease {
+  void *ptr = nullptr;
+  size_t bytes = 0;
+  WsLease() = default;
+  WsLease(const WsLease &) = delete;
+  WsLease &operator=(const WsLease &) = delete;
+  ~WsLease();
+  /// at least `bytes` from slot `slot` of the current device (contents not kept)
+  void *get(int slot, size_t bytes, cudaStream_t st);
+  template <typename T> T *as() const { return static_cast<T *>(ptr); }
+
+ private:
+  int device_ = -1, slot_ = -1;
+  DevBuf own_;  // fallback when the shared slot is busy
+};
+
+/// a workspace lease with DevBuf's reserve/as surface
+struct WsBuf {
+  WsLease lease;
+  int slot;
+  void *ptr = nullptr;
+  explicit WsBuf(int s) : slot(s) {}
+  void reserve(size_t n, cudaStream_t st) { ptr = lease.get(slot, n, st); }
+  template <typename T> T *as() const { return static_cast<T *>(ptr); }
+};
+
+/// the temporaries of one extraction, all from the device workspace
 struct ExtractScratch {
-  DevBuf ctl, tiles, stage_a, stage_b, scan, bits;
+  WsBuf ctl{kWsCtl}, tiles{kWsTiles}, stage_a{kWsStageA}, stage_b{kWsStageB},
+    bits{kWsBits};
+  DevBuf scan;  // unused by the pool-free scan; kept for its signature
 };
 
 // ------------------------------------------------------------ ingest.cu
@@ -110,7 +149,10 @@ int scan_exclusive_u32_u64(const uint32_t *in, uint64_t *out, uint64_t n,
 /// result ends in keys/vals (alt buffers are scratch of the same size)
 void radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
                       uint32_t *vals_alt, uint64_t n, int key_bits,
-                      DevBuf &scratch, cudaStream_t st, int *passes_run);
+                      void *scratch, cudaStream_t st, int *passes_run);
+
+/// bytes of scratch radix_sort_pairs needs for n keys
+size_t radix_sort_scratch_bytes(uint64_t n);
 
 // ----------------------------------------------------------- extract.cu
 struct ExtractRequest {
@@ -128,6 +170,7 @@ struct ExtractRequest {
   uint64_t dual_cap;
   void *xyz;            // [tri_cap][9] f64/f32 or null
   uint64_t tri_cap;
+  bool final_host;      // corners/tasks/xyz are pinned host memory
 };
 
 struct ExtractResult {
@@ -141,8 +184,7 @@ struct ExtractResult {
   uint64_t launches;
 };
 
-ExtractResult run_extract(const ExtractRequest &r, ExtractScratch &x,
-                          cudaStream_t st);
+ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st);
 
 void run_find_exact(const SearchCtx &s, const KeyGeom &g, const int4 *cells,
                     uint64_t n, int64_t *out, cudaStream_t st);

@@ -218,9 +218,15 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
 
 }  // namespace
 
+size_t radix_sort_scratch_bytes(uint64_t n)
+{
+  const uint64_t tiles = (n + kSortTile - 1) / kSortTile;
+  return size_t(kMaxPasses) * kDigits * 12 + 256 + size_t(tiles) * kDigits * 8;
+}
+
 void radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
                       uint32_t *vals_alt, uint64_t n, int key_bits,
-                      DevBuf &scratch, cudaStream_t st, int *passes_run)
+                      void *scratch, cudaStream_t st, int *passes_run)
 {
   if (passes_run) *passes_run = 0;
   if (n <= 1 || key_bits <= 0) return;
@@ -232,8 +238,7 @@ void radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
   const size_t hist_bytes = size_t(kMaxPasses) * kDigits * 4;
   const size_t offs_bytes = size_t(kMaxPasses) * kDigits * 8;
   const size_t state_bytes = size_t(tiles) * kDigits * 8;
-  scratch.reserve(hist_bytes + offs_bytes + 256 + state_bytes, st);
-  auto *base = scratch.as<unsigned char>();
+  auto *base = static_cast<unsigned char *>(scratch);
   auto *hist = reinterpret_cast<unsigned int *>(base);
   auto *offs = reinterpret_cast<unsigned long long *>(base + hist_bytes);
   auto *ticket = reinterpret_cast<unsigned int *>(base + hist_bytes + offs_bytes);
