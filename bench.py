@@ -140,7 +140,7 @@ def run_amrx(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or args.force_dist:
         dist.init_process_group("nccl", device_id=dev)
     iso = iso_of(args.config)
 
@@ -168,38 +168,20 @@ def run_amrx(args):
         ix.close()
         return r.stats, ingest, len(r.fat)
 
-    keys_buf = scal_buf = None
-    if world > 1:
-        keys_buf = torch.empty(n + 256, dtype=torch.int64, device=dev)
-        scal_buf = torch.empty(n, dtype=torch.float64, device=dev)
+    from paper_2004_08475_b200 import dist as D
 
     def step_multi():
         # rank 0 sorts; NCCL broadcast of the sorted keys + scalars; each
-        # rank adopts them and extracts its own contiguous cell range
-        ingest = 0.0
-        if rank == 0:
-            ix0 = P.build_index(cells, scal, device=local, stream=sh)
-            kp, sp = ix0.device_arrays()
-            ingest = ix0.info.seconds_ingest
-            P.library()  # noqa
-            torch.cuda.current_stream().wait_stream(stream)
-            _copy_dev(keys_buf, kp, n * 8)
-            _copy_dev(scal_buf, sp, n * 8)
-            ix0.close()
-        dist.broadcast(keys_buf, 0)
-        dist.broadcast(scal_buf, 0)
-        torch.cuda.synchronize()
-        ix = P.adopt_index(keys_buf.data_ptr(), scal_buf.data_ptr(), n, geometry, device=local,
-                           stream=sh)
-        lo, hi = n * rank // world, n * (rank + 1) // world
-        r = P.extract_isosurface(ix, P.IsoParams(iso=iso), cell_range=(lo, hi), out=out)
-        cnt = torch.tensor([len(r.fat)], dtype=torch.int64, device=dev)
-        counts = [torch.zeros_like(cnt) for _ in range(world)]
-        dist.all_gather(counts, cnt)
+        # rank adopts them and extracts its own contiguous cell range; an
+        # all-gather of per-rank counts gives the global offsets
+        ix = D.replicate_index(cells if rank == 0 else None, scal if rank == 0 else None,
+                               device=dev, stream=sh)
+        ingest = ix.info.seconds_ingest
+        res = D.extract_isosurface_partitioned(ix, P.IsoParams(iso=iso), out=out, device=dev)
         ix.close()
-        return r.stats, ingest, int(sum(c.item() for c in counts))
+        return res.stats, ingest, res.total
 
-    step = step_multi if world > 1 else step_single
+    step = step_multi if (world > 1 or args.force_dist) else step_single
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -323,12 +305,6 @@ def run_amrx(args):
         dist.destroy_process_group()
 
 
-def _copy_dev(dst_tensor, src_ptr, nbytes):
-    from paper_2004_08475_b200 import synth
-    if synth.lib().amrxs_memcpy(dst_tensor.data_ptr(), src_ptr, nbytes):
-        raise RuntimeError("device copy failed")
-
-
 # ------------------------------------------------------------ CPU baseline
 def cpu_sample(cells, scal, target):
     """a contiguous sub-box (x slabs) of the workload with ~target cells"""
@@ -428,6 +404,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=12_000_000)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the multi-GPU code path even at world size 1 (testing)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
