@@ -302,6 +302,7 @@ def run_amrx(args):
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 
