@@ -373,7 +373,10 @@ KeyGeom make_geometry(const int64_t mn[3], const int64_t mx[3],
   for (int l = 0; l <= kMaxLevel; l++)
     if ((level_mask >> l) & 1u) g.levels[g.nlevels++] = int8_t(l);
   // directory: about two buckets per cell, 2^10 .. 2^30 entries
-  const int want = std::min(30, std::max(10, bit_width(n) + 1));
+  // (AMRX_DIR_BITS overrides the size, for experiments)
+  static const char *dir_env = std::getenv("AMRX_DIR_BITS");
+  const int want = dir_env ? std::max(1, std::min(33, std::atoi(dir_env)))
+                           : std::min(30, std::max(10, bit_width(n) + 1));
   g.dir_bits = std::min(g.total, want);
   g.dir_shift = g.total - g.dir_bits;
   // block level map at the coarsest level's granularity, if it is small
@@ -385,8 +388,10 @@ KeyGeom make_geometry(const int64_t mn[3], const int64_t mx[3],
     blocks *= double(g.map_dim[a]);
   }
   const double budget = std::max(double(1 << 26), 4.0 * double(n));
-  static const bool disabled = std::getenv("AMRX_NO_LEVEL_MAP") != nullptr;
-  g.map_on = !disabled && g.nlevels <= 8 && blocks <= budget;
+  // measured net-negative on C4 with the per-lane lookups (the map load sits
+  // in every probe's dependency chain): opt-in via AMRX_LEVEL_MAP=1
+  static const bool enabled = std::getenv("AMRX_LEVEL_MAP") != nullptr;
+  g.map_on = enabled && g.nlevels <= 8 && blocks <= budget;
   return g;
 }
 
@@ -813,6 +818,7 @@ amrx_status amrx_extract_dual(amrx_index *index, const amrx_range *range,
     rq.g = index->g;
     rq.scal = index->scal.as<double>();
     rq.lmap = index->lmap.as<uint8_t>();
+    rq.unique = index->info.duplicate_keys == 0;
     rq.cell_begin = b;
     rq.cell_end = e;
     rq.emit_dual = true;
@@ -894,6 +900,7 @@ amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range,
     rq.g = index->g;
     rq.scal = index->scal.as<double>();
     rq.lmap = index->lmap.as<uint8_t>();
+    rq.unique = index->info.duplicate_keys == 0;
     rq.cell_begin = b;
     rq.cell_end = e;
     rq.emit_tri = true;

@@ -205,6 +205,11 @@ enum DbgEvent {
   kDbgCount
 };
 
+// lane_find: fetch small buckets whole with vector loads (A/B switch)
+#ifndef AMRX_SMALL_BUCKET
+#define AMRX_SMALL_BUCKET 0
+#endif
+
 // counters are compiled in only for a diagnostic build (make DBG=1): the
 // atomics otherwise bloat the hot loop past the instruction cache
 #ifndef AMRX_DBG
@@ -265,7 +270,24 @@ __device__ __forceinline__ void lane_find(const SearchCtx &s, const uint64_t (&q
     uint64_t lo = __ldg(s.dir + ((FINER ? anchor : q[t]) >> s.dir_shift));
     const uint64_t hi = __ldg(s.dir + (q[t] >> s.dir_shift) + 1);
     const uint64_t from = (t > 0 && prev_q <= q[t] && prev_p > lo) ? prev_p : lo;
-    const uint64_t p = global_lower_bound(s.keys, from, hi, q[t]);
+    uint64_t p;
+    if (AMRX_SMALL_BUCKET && hi - from <= 6) {
+      // small bucket (the common case): one round trip of three 16-byte
+      // loads covers it; lower_bound = from + #keys < q (the array is
+      // padded with sentinels, so the loads never leave it)
+      const uint64_t a0 = from & ~1ull;
+      uint32_t below = 0;
+#pragma unroll
+      for (int v = 0; v < 4; v++) {
+        const ulonglong2 kv = ldg_u64x2(s.keys + a0 + 2 * v);
+        const uint64_t i0 = a0 + 2 * v, i1 = i0 + 1;
+        below += (i0 >= from && i0 < hi && kv.x < q[t]);
+        below += (i1 >= from && i1 < hi && kv.y < q[t]);
+      }
+      p = from + below;
+    } else {
+      p = global_lower_bound(s.keys, from, hi, q[t]);
+    }
     prev_p = p;
     prev_q = q[t];
     int64_t res = -1;
@@ -283,6 +305,71 @@ __device__ __forceinline__ void lane_find(const SearchCtx &s, const uint64_t (&q
     }
     out[t] = res;
     lvl[t] = rl + s.shift;
+  }
+}
+
+/*! K independent lookups per lane advanced in lock-step: the directory
+    loads of all K go out together, then every binary-search step issues up
+    to K independent key loads, so the dependent-latency chain is that of
+    ONE search instead of K.  Same contract as lane_find / warp_find. */
+template <int K, bool FINER>
+__device__ __forceinline__ void batch_find(const SearchCtx &s, const uint64_t (&q)[K],
+                                           const bool (&valid)[K], int64_t (&out)[K],
+                                           int (&lvl)[K])
+{
+  uint32_t lo[K], n[K];
+#pragma unroll
+  for (int k = 0; k < K; k++) {
+    lo[k] = 0;
+    n[k] = 0;
+    if (valid[k]) {
+      const uint64_t b0 = (FINER ? (q[k] & ~s.lmask) : q[k]) >> s.dir_shift;
+      lo[k] = __ldg(s.dir + b0);
+      n[k] = __ldg(s.dir + (q[k] >> s.dir_shift) + 1) - lo[k];
+    }
+  }
+  uint32_t first[K];  // bucket start: the FINER scan-back floor
+#pragma unroll
+  for (int k = 0; k < K; k++) first[k] = lo[k];
+  bool more = true;
+  while (more) {
+    more = false;
+#pragma unroll
+    for (int k = 0; k < K; k++)
+      if (n[k] > 0) {
+        const uint32_t half = n[k] >> 1;
+        if (ldg_u64(s.keys + lo[k] + half) < q[k]) {
+          lo[k] += half + 1;
+          n[k] -= half + 1;
+        } else {
+          n[k] = half;
+        }
+        more |= n[k] > 0;
+      }
+  }
+  uint64_t at[K], before[K];
+#pragma unroll
+  for (int k = 0; k < K; k++) {
+    at[k] = valid[k] ? ldg_u64(s.keys + lo[k]) : 0;  // padded: lo <= n
+    before[k] = (valid[k] && FINER && lo[k] > first[k]) ? ldg_u64(s.keys + lo[k] - 1) : ~0ull;
+  }
+#pragma unroll
+  for (int k = 0; k < K; k++) {
+    if (!valid[k]) continue;
+    int64_t res = -1;
+    int rl = 0;
+    if (at[k] == q[k]) {
+      res = int64_t(lo[k]);
+      rl = int(q[k] & s.lmask);
+    } else if (FINER && (before[k] & ~s.lmask) == (q[k] & ~s.lmask)) {
+      // same anchor, lower level: walk to the first of the run (rarely >1)
+      uint32_t x = lo[k] - 1;
+      while (x > first[k] && (ldg_u64(s.keys + x - 1) & ~s.lmask) == (q[k] & ~s.lmask)) x--;
+      res = int64_t(x);
+      rl = int(ldg_u64(s.keys + x) & s.lmask);
+    }
+    out[k] = res;
+    lvl[k] = rl + s.shift;
   }
 }
 

@@ -38,6 +38,11 @@
 #ifndef AMRX_LANE_SEARCH
 #define AMRX_LANE_SEARCH 1
 #endif
+// >0: resolve stencil points K at a time with lock-step lookups (batch_find);
+// 0: column by column (resolve_column)
+#ifndef AMRX_BATCH
+#define AMRX_BATCH 2  // measured best on C4: K=2 234 ms, K=3 242, K=4 286, columns 326
+#endif
 
 namespace amrx {
 
@@ -162,6 +167,7 @@ struct KArgs {
   KeyGeom g;
   const uint8_t *lmap;  // block level map (g.map_on)
   const uint32_t *above;  // bit i: scalar i > iso (EMIT_TRI)
+  bool unique;            // no duplicate keys in the index
   const double *scal;
   uint64_t cell_begin, cell_end;
   uint32_t num_tiles;
@@ -335,7 +341,7 @@ __device__ __noinline__ void find3_coarse(const SearchCtx &s, const uint64_t (&q
 }
 
 /*! resolve the three stencil points of column COL (dx, dy fixed; dz =
-    -1,0,+1) for the lanes flagged 'mine', in snap's probe order
+    -1,0,+1) this lane wants (bit t of `want`: dz = t-1), in snap's probe order
     (locator.cpp:122-134), skipping levels the block level map rules out
     (exact: a cell containing p lies in p's coarsest-aligned block):
       1. the hint level and every finer level in ONE warp_find (finer cells
@@ -345,7 +351,7 @@ __device__ __noinline__ void find3_coarse(const SearchCtx &s, const uint64_t (&q
          candidate level (holes, outside the domain) cost no search. */
 __device__ __forceinline__ void resolve_column(const KArgs &a, Smem &sm,
                                             int warp, int lane, const Cell &c,
-                                            uint32_t self, int COL, bool mine,
+                                            uint32_t self, int COL, uint32_t want,
                                             uint32_t &resolved,
                                             uint64_t &status)
 {
@@ -358,7 +364,7 @@ __device__ __forceinline__ void resolve_column(const KArgs &a, Smem &sm,
   const uint32_t le_hint = (2u << hint_bit) - 1;
   // at the hint level the points are their own anchors: build the keys
   // from one shared x/y part, no masking
-  const bool xy = mine && px >= g.mn[0] && px <= g.mx[0] && py >= g.mn[1] &&
+  const bool xy = want != 0 && px >= g.mn[0] && px <= g.mx[0] && py >= g.mn[1] &&
                   py <= g.mx[1];
   uint64_t base = uint64_t(c.level - g.shift);
   if (g.bits[0]) base |= uint64_t((px - g.mn[0]) >> g.shift) << g.sh[0];
@@ -371,8 +377,15 @@ __device__ __forceinline__ void resolve_column(const KArgs &a, Smem &sm,
 #pragma unroll
   for (int t = 0; t < 3; t++) {
     const int64_t pz = c.k + (t - 1) * w;
-    cand[t] = mine ? block_levels(g, a.lmap, px, py, pz) : 0u;
+    cand[t] = ((want >> t) & 1u) ? block_levels(g, a.lmap, px, py, pz) : 0u;
     v[t] = xy && pz >= g.mn[2] && pz <= g.mx[2] && (cand[t] & le_hint);
+    if (COL == 4 && t == 1 && a.unique && ((want >> 1) & 1u)) {
+      // the cell's own anchor on its own level: with no duplicate keys the
+      // lookup can only return the cell itself (lower_bound of its key)
+      v[t] = false;
+      out[t] = int64_t(self);
+      cand[t] = 0;
+    }
     q[t] = base | (g.bits[2] ? uint64_t((pz - g.mn[2]) >> g.shift) << g.sh[2] : 0);
     cand[t] &= ~le_hint;  // what is left for step 2
   }
@@ -417,9 +430,10 @@ __device__ __forceinline__ void resolve_column(const KArgs &a, Smem &sm,
         }
       }
   }
-  if (mine) {
+  {
 #pragma unroll
     for (int t = 0; t < 3; t++) {
+      if (!((want >> t) & 1u)) continue;
       const int p = COL + 9 * t;
       uint32_t st;
       if (out[t] < 0)
@@ -438,6 +452,122 @@ __device__ __forceinline__ void resolve_column(const KArgs &a, Smem &sm,
   }
 }
 
+#if AMRX_BATCH > 0
+struct Hit {
+  int64_t id;
+  int level;
+};
+
+/*! coarser-level probe for one point the hint+finer lookup missed: the
+    candidate levels above the hint, ascending (the reference's finest-first
+    order restricted to them).  Per lane, no warp collectives; rare, so out of
+    line -- and scalar, so the caller's batch arrays stay in registers. */
+__device__ __noinline__ Hit probe_coarser(const KArgs &a, const Cell &c, int p,
+                                          uint32_t cand)
+{
+  const KeyGeom &g = a.g;
+  const int64_t w = int64_t(1) << c.level;
+  const int64_t px = c.i + (p % 3 - 1) * w, py = c.j + ((p / 3) % 3 - 1) * w,
+                pz = c.k + (p / 9 - 1) * w;
+  while (cand) {
+    const int b = __ffs(cand) - 1;
+    cand &= cand - 1;
+    const int L = g.levels[b];
+    uint64_t q[1];
+    bool v[1];
+    int64_t o[1] = {-1};
+    int l1[1];
+    v[0] = query_key(g, px, py, pz, L, q[0]);
+    if (!v[0]) continue;
+    batch_find<1, false>(a.s, q, v, o, l1);
+    if (o[0] >= 0) return Hit{o[0], L};
+  }
+  return Hit{-1, c.level};
+}
+
+/*! resolve the stencil points in `need`, AMRX_BATCH at a time per lane with
+    their lookups advanced in lock-step (batch_find), in snap's probe order
+    (locator.cpp:122-134) with the two exact shortcuts of resolve_column:
+    hint + finer levels in one lookup, block-level-map candidates for the
+    coarser probes. */
+__device__ __forceinline__ void resolve_points(const KArgs &a, Smem &sm, int warp,
+                                               int lane, const Cell &c, uint32_t self,
+                                               uint32_t need, uint32_t &resolved,
+                                               uint64_t &status)
+{
+  constexpr int K = AMRX_BATCH;
+  const KeyGeom &g = a.g;
+  const int64_t w = int64_t(1) << c.level;
+  const int hint_bit = __popc(g.level_mask & ((1u << c.level) - 1));
+  const uint32_t le_hint = (2u << hint_bit) - 1;
+  uint32_t todo = need;
+  if (a.unique && ((todo >> 13) & 1u)) {
+    // the cell's own anchor on its own level: with no duplicate keys the
+    // lookup can only return the cell itself (lower_bound of its key)
+    todo &= ~(1u << 13);
+    resolved |= 1u << 13;
+    sm.id[warp][13][lane] = self;
+    sm.lev[warp][13][lane] = uint8_t(c.level);
+  }
+  while (__any_sync(kFull, todo != 0)) {
+    uint64_t q[K];
+    bool v[K];
+    int64_t out[K];
+    int lvl[K], pk[K];
+    uint32_t cand[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+      pk[k] = -1;
+      v[k] = false;
+      out[k] = -1;
+      lvl[k] = c.level;
+      cand[k] = 0;
+      q[k] = 0;
+      if (todo) {
+        const int p = __ffs(todo) - 1;
+        todo &= todo - 1;
+        pk[k] = p;
+        const int64_t px = c.i + (p % 3 - 1) * w, py = c.j + ((p / 3) % 3 - 1) * w,
+                      pz = c.k + (p / 9 - 1) * w;
+        cand[k] = block_levels(g, a.lmap, px, py, pz);
+        // at the hint level the point is its own anchor
+        v[k] = px >= g.mn[0] && px <= g.mx[0] && py >= g.mn[1] && py <= g.mx[1] &&
+               pz >= g.mn[2] && pz <= g.mx[2] && (cand[k] & le_hint);
+        if (v[k]) q[k] = pack_unchecked(g, px, py, pz, c.level);
+        cand[k] &= ~le_hint;
+      }
+    }
+    batch_find<K, true>(a.s, q, v, out, lvl);
+#pragma unroll
+    for (int k = 0; k < K; k++)
+      if (pk[k] >= 0 && out[k] < 0 && cand[k] != 0) {
+        dbg_add(a.s, kDbgCoarser);
+        const Hit h = probe_coarser(a, c, pk[k], cand[k]);
+        out[k] = h.id;
+        lvl[k] = h.level;
+      }
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+      if (pk[k] < 0) continue;
+      const int p = pk[k];
+      uint32_t st;
+      if (out[k] < 0)
+        st = kMiss;
+      else if (lvl[k] < c.level)
+        st = kFiner;
+      else if (lvl[k] == c.level && uint32_t(out[k]) < self)
+        st = kLower;
+      else
+        st = kOk;
+      status |= uint64_t(st) << (2 * p);
+      resolved |= 1u << p;
+      sm.id[warp][p][lane] = uint32_t(out[k]);
+      sm.lev[warp][p][lane] = uint8_t(lvl[k]);
+    }
+  }
+}
+#endif  // AMRX_BATCH > 0
+
 __device__ __forceinline__ void resolve_needed(const KArgs &a, Smem &sm,
                                                int warp, int lane,
                                                const Cell &c, uint32_t self,
@@ -445,6 +575,10 @@ __device__ __forceinline__ void resolve_needed(const KArgs &a, Smem &sm,
                                                uint32_t &resolved,
                                                uint64_t &status)
 {
+#if AMRX_BATCH > 0
+  resolve_points(a, sm, warp, lane, c, self, need, resolved, status);
+  return;
+#endif
   uint32_t cols = 0;
 #pragma unroll
   for (int col = 0; col < 9; col++)
@@ -454,8 +588,10 @@ __device__ __forceinline__ void resolve_needed(const KArgs &a, Smem &sm,
     const int col = __ffs(wcols) - 1;
     wcols &= wcols - 1;
     dbg_add(a.s, kDbgColumns);
-    resolve_column(a, sm, warp, lane, c, self, col, (cols >> col) & 1,
-                   resolved, status);
+    // only the points this lane's live candidates need (bit t: dz = t-1)
+    const uint32_t want = ((need >> col) & 1u) | (((need >> (col + 9)) & 1u) << 1) |
+                          (((need >> (col + 18)) & 1u) << 2);
+    resolve_column(a, sm, warp, lane, c, self, col, want, resolved, status);
   }
 }
 
@@ -862,6 +998,7 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
   k.s = r.s;
   k.g = r.g;
   k.lmap = r.lmap;
+  k.unique = r.unique;
   k.above = nullptr;
   if (T) {
     const uint64_t words = (r.s.n + 31) / 32;

@@ -171,6 +171,7 @@ struct ExtractRequest {
   void *xyz;            // [tri_cap][9] f64/f32 or null
   uint64_t tri_cap;
   bool final_host;      // corners/tasks/xyz are pinned host memory
+  bool unique;          // the index holds no duplicate keys
 };
 
 struct ExtractResult {
