@@ -98,22 +98,32 @@ orc_index *orc_build_index(const int32_t *cells4, const double *scalars,
     }
   }
 
-  sort_rec *recs = (sort_rec *)malloc(n * sizeof(sort_rec));
-  for (uint64_t r = 0; r < n; r++) {
-    memcpy(recs[r].c, cells4 + 4 * r, 16);
-    recs[r].idx = (uint32_t)r;
-  }
-  qsort(recs, n, sizeof(sort_rec), cmp_rec);
-
   orc_index *idx = (orc_index *)calloc(1, sizeof(orc_index));
   idx->n = n;
   idx->cells = (int32_t *)malloc(n * 16);
   idx->scalars = (double *)malloc(n * 8);
-  for (uint64_t r = 0; r < n; r++) {
-    memcpy(idx->cells + 4 * r, recs[r].c, 16);
-    idx->scalars[r] = scalars[recs[r].idx];
+
+  /* already in (key, input position) order: the stable sort is the
+   * identity, skip it (lets tests hold 10^8..10^9-cell indices) */
+  int sorted = 1;
+  for (uint64_t r = 1; r < n && sorted; r++)
+    if (cmp_cell(cells4 + 4 * (r - 1), cells4 + 4 * r) > 0) sorted = 0;
+  if (sorted) {
+    memcpy(idx->cells, cells4, n * 16);
+    memcpy(idx->scalars, scalars, n * 8);
+  } else {
+    sort_rec *recs = (sort_rec *)malloc(n * sizeof(sort_rec));
+    for (uint64_t r = 0; r < n; r++) {
+      memcpy(recs[r].c, cells4 + 4 * r, 16);
+      recs[r].idx = (uint32_t)r;
+    }
+    qsort(recs, n, sizeof(sort_rec), cmp_rec);
+    for (uint64_t r = 0; r < n; r++) {
+      memcpy(idx->cells + 4 * r, recs[r].c, 16);
+      idx->scalars[r] = scalars[recs[r].idx];
+    }
+    free(recs);
   }
-  free(recs);
 
   /* bounds, max level, distinct levels finest first (locator.cpp:70-89) */
   int present[MAX_LEVEL + 1] = {0};
@@ -341,8 +351,17 @@ uint64_t orc_extract_dual(const orc_index *idx, uint32_t *corners8,
                           uint32_t *owner, int64_t *base3, int32_t *level,
                           uint64_t cap, uint64_t *counters4)
 {
+  return orc_extract_dual_range(idx, 0, idx->n, corners8, owner, base3, level,
+                                cap, counters4);
+}
+
+uint64_t orc_extract_dual_range(const orc_index *idx, uint64_t cell_begin,
+                                uint64_t cell_end, uint32_t *corners8,
+                                uint32_t *owner, int64_t *base3, int32_t *level,
+                                uint64_t cap, uint64_t *counters4)
+{
   uint64_t count = 0, cnt[4] = {0};
-  for (uint64_t cell = 0; cell < idx->n; cell++) {
+  for (uint64_t cell = cell_begin; cell < cell_end && cell < idx->n; cell++) {
     const int32_t *c = idx->cells + 4 * cell;
     for (int delta = 0; delta < 8; delta++) {
       int64_t base[3];

@@ -48,6 +48,12 @@ uint64_t orc_extract_dual(const orc_index *idx, uint32_t *corners8,
                           uint32_t *owner, int64_t *base3, int32_t *level,
                           uint64_t cap, uint64_t *counters4);
 
+/* the same over cells [cell_begin, cell_end) (sampled parity at scale) */
+uint64_t orc_extract_dual_range(const orc_index *idx, uint64_t cell_begin,
+                                uint64_t cell_end, uint32_t *corners8,
+                                uint32_t *owner, int64_t *base3, int32_t *level,
+                                uint64_t cap, uint64_t *counters4);
+
 /* extract_isosurface passes 1+2 (pipeline.cpp:67-146) without the weld,
  * serial: the fat triangle soup in emission order, 9 doubles/triangle.
  * Writes up to cap triangles; returns the total, -1 (as UINT64_MAX) on a

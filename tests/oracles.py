@@ -136,6 +136,7 @@ class Restatement(_Lib):
     def __init__(self, path=RESTATEMENT_SO):
         super().__init__(path)
         self._fn("orc_extract_dual", U64, [P, P, P, P, P, U64, P])
+        self._fn("orc_extract_dual_range", U64, [P, U64, U64, P, P, P, P, U64, P])
         self._fn("orc_extract_iso", U64, [P, F64, P, U64, P])
         self._fn("orc_extract_iso_range", U64, [P, F64, U64, U64, P, U64, P])
         self._fn("orc_weld", U64, [P, U64, P, P])
@@ -150,6 +151,16 @@ class Restatement(_Lib):
         self.lib.orc_extract_dual(h, _ptr(corners), _ptr(owner), _ptr(base), _ptr(level),
                                   total, _ptr(cnt))
         return dict(corners=corners, owner=owner, base=base, level=level, counters=cnt)
+
+    def extract_dual_range(self, h, cell_begin, cell_end):
+        cnt = np.zeros(4, np.uint64)
+        total = self.lib.orc_extract_dual_range(h, cell_begin, cell_end, None, None, None,
+                                                None, 0, _ptr(cnt))
+        corners = np.empty((total, 8), np.uint32)
+        owner = np.empty(total, np.uint32)
+        self.lib.orc_extract_dual_range(h, cell_begin, cell_end, _ptr(corners), _ptr(owner),
+                                        None, None, total, _ptr(cnt))
+        return dict(corners=corners, owner=owner, counters=cnt)
 
     def extract_iso(self, h, iso, cell_begin=None, cell_end=None):
         cnt = np.zeros(4, np.uint64)
