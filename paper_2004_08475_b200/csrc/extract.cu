@@ -43,6 +43,10 @@
 #ifndef AMRX_BATCH
 #define AMRX_BATCH 2  // measured best on C4: K=2 234 ms, K=3 242, K=4 286, columns 326
 #endif
+// 1: borrow z-neighbour lanes' lookups (resolve_points); 0: every lane alone
+#ifndef AMRX_SHARE
+#define AMRX_SHARE 1
+#endif
 
 namespace amrx {
 
@@ -50,6 +54,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+constexpr int kTileCells = AMRX_SHARE ? 30 : 32;  // cells one warp tile owns
 
 // point index p = (ox+1) + 3(oy+1) + 9(oz+1), o in {-1,0,1}^3; self = 13
 constexpr uint32_t kCorner0Points = (1u << 0) | (1u << 1) | (1u << 3) |
@@ -485,30 +490,53 @@ __device__ __noinline__ Hit probe_coarser(const KArgs &a, const Cell &c, int p,
   return Hit{-1, c.level};
 }
 
-/*! resolve the stencil points in `need`, AMRX_BATCH at a time per lane with
-    their lookups advanced in lock-step (batch_find), in snap's probe order
-    (locator.cpp:122-134) with the two exact shortcuts of resolve_column:
-    hint + finer levels in one lookup, block-level-map candidates for the
-    coarser probes. */
-__device__ __forceinline__ void resolve_points(const KArgs &a, Smem &sm, int warp,
-                                               int lane, const Cell &c, uint32_t self,
-                                               uint32_t need, uint32_t &resolved,
-                                               uint64_t &status)
+/// a CellId as kept in shared memory (u32, all ones = absent) back to int64
+__device__ __forceinline__ int64_t stored_id(uint32_t v)
+{
+  return v == 0xffffffffu ? int64_t(-1) : int64_t(v);
+}
+
+/// status of a resolved point relative to the owner (dual.cpp:60-67)
+__device__ __forceinline__ void record_point(Smem &sm, int warp, int lane, const Cell &c,
+                                             uint32_t self, int p, int64_t id, int lev,
+                                             uint32_t &resolved, uint64_t &status)
+{
+  uint32_t st;
+  if (id < 0)
+    st = kMiss;
+  else if (lev < c.level)
+    st = kFiner;
+  else if (lev == c.level && uint32_t(id) < self)
+    st = kLower;
+  else
+    st = kOk;
+  status |= uint64_t(st) << (2 * p);
+  resolved |= 1u << p;
+  sm.id[warp][p][lane] = uint32_t(id);
+  sm.lev[warp][p][lane] = uint8_t(lev);
+}
+
+/*! look up the stencil points in `todo`, AMRX_BATCH at a time per lane
+    with their lookups advanced in lock-step (batch_find), in snap's probe
+    order (locator.cpp:122-134): hint + finer levels in one lookup, then
+    the coarser candidate levels (probe_coarser). */
+#ifndef AMRX_LOOKUP_NOINLINE
+#define AMRX_LOOKUP_NOINLINE 0  // out of line measured 1.6x slower (spills + calls)
+#endif
+#if AMRX_LOOKUP_NOINLINE
+#define AMRX_LOOKUP_ATTR __noinline__
+#else
+#define AMRX_LOOKUP_ATTR __forceinline__
+#endif
+__device__ AMRX_LOOKUP_ATTR void lookup_points(const KArgs &a, Smem &sm, int warp, int lane,
+                                              const Cell &c, uint32_t self, uint32_t todo,
+                                              uint32_t &resolved, uint64_t &status)
 {
   constexpr int K = AMRX_BATCH;
   const KeyGeom &g = a.g;
   const int64_t w = int64_t(1) << c.level;
   const int hint_bit = __popc(g.level_mask & ((1u << c.level) - 1));
   const uint32_t le_hint = (2u << hint_bit) - 1;
-  uint32_t todo = need;
-  if (a.unique && ((todo >> 13) & 1u)) {
-    // the cell's own anchor on its own level: with no duplicate keys the
-    // lookup can only return the cell itself (lower_bound of its key)
-    todo &= ~(1u << 13);
-    resolved |= 1u << 13;
-    sm.id[warp][13][lane] = self;
-    sm.lev[warp][13][lane] = uint8_t(c.level);
-  }
   while (__any_sync(kFull, todo != 0)) {
     uint64_t q[K];
     bool v[K];
@@ -547,23 +575,97 @@ __device__ __forceinline__ void resolve_points(const KArgs &a, Smem &sm, int war
         lvl[k] = h.level;
       }
 #pragma unroll
-    for (int k = 0; k < K; k++) {
-      if (pk[k] < 0) continue;
-      const int p = pk[k];
-      uint32_t st;
-      if (out[k] < 0)
-        st = kMiss;
-      else if (lvl[k] < c.level)
-        st = kFiner;
-      else if (lvl[k] == c.level && uint32_t(out[k]) < self)
-        st = kLower;
-      else
-        st = kOk;
-      status |= uint64_t(st) << (2 * p);
-      resolved |= 1u << p;
-      sm.id[warp][p][lane] = uint32_t(out[k]);
-      sm.lev[warp][p][lane] = uint8_t(lvl[k]);
-    }
+    for (int k = 0; k < K; k++)
+      if (pk[k] >= 0) record_point(sm, warp, lane, c, self, pk[k], out[k], lvl[k], resolved, status);
+  }
+}
+
+/*! resolve the stencil points in `need`, sharing lookups between lanes.
+    Lanes hold consecutive cells, so lane L-1 is usually L's z-predecessor
+    on the same level: then L's point (dx,dy,-1) IS L-1's point (dx,dy,0)
+    with the same hint level -- the identical snap query (locator.cpp:
+    122-134), hence the identical answer -- and likewise (dx,dy,+1) with
+    lane L+1.  So each lane looks up the centre points (dx,dy,0) of the
+    columns it needs plus only those dz = +-1 points its neighbour will not
+    have, in ONE lock-step pass, then borrows the rest from the neighbours'
+    shared-memory results; with unique keys the z-neighbour cells themselves
+    need no lookup at all.  With AMRX_SHARE the tile is 30 cells and lanes 0
+    and 31 are halo lanes holding the cells just before and after it: they
+    evaluate no candidates, they only look up the centres their neighbour
+    borrows, so no working lane is left without a neighbour.  Exact by
+    construction: a borrowed answer is the answer to the very same query. */
+__device__ __forceinline__ void resolve_points(const KArgs &a, Smem &sm, int warp, int lane,
+                                               const Cell &c, uint32_t self, uint64_t kself,
+                                               bool valid, uint32_t need, uint32_t &resolved,
+                                               uint64_t &status)
+{
+  if (!AMRX_SHARE) {
+    uint32_t todo = need & ~resolved;
+    if (a.unique && ((todo >> 13) & 1u))
+      record_point(sm, warp, lane, c, self, 13, self, c.level, resolved, status);
+    lookup_points(a, sm, warp, lane, c, self, need & ~resolved, resolved, status);
+    return;
+  }
+  const KeyGeom &g = a.g;
+  const int64_t w = int64_t(1) << c.level;
+  // is lane L-1 (L+1) this cell's z-predecessor (successor) on the same level?
+  const uint64_t dz = g.bits[2] ? (uint64_t(w >> g.shift) << g.sh[2]) : 0;
+  const uint64_t kp = __shfl_up_sync(kFull, kself, 1);
+  const uint64_t ks = __shfl_down_sync(kFull, kself, 1);
+  const bool vp = __shfl_up_sync(kFull, valid, 1);
+  const bool vs = __shfl_down_sync(kFull, valid, 1);
+  const bool pred_ok = valid && lane > 0 && vp && dz && c.k - w >= g.mn[2] && kp == kself - dz;
+  const bool succ_ok = valid && lane < 31 && vs && dz && c.k + w <= g.mx[2] && ks == kself + dz;
+
+  // halo lanes: adopt what the neighbour will borrow (lane 0 serves lane 1's
+  // dz = -1 points, lane 31 serves lane 30's dz = +1 points)
+  const uint32_t need_next = __shfl_down_sync(kFull, need, 1);
+  const uint32_t need_prev = __shfl_up_sync(kFull, need, 1);
+  if (lane == 0) need = succ_ok ? ((need_next & 0x1ffu) << 9) : 0u;
+  if (lane == 31) need = pred_ok ? (((need_prev >> 18) & 0x1ffu) << 9) : 0u;
+
+  uint32_t todo = need & ~resolved;
+  if (a.unique) {
+    // with no duplicate keys a lookup of an existing cell's own key returns
+    // that cell: the cell itself, and its z-neighbours
+    if ((todo >> 13) & 1u) record_point(sm, warp, lane, c, self, 13, self, c.level, resolved, status);
+    if (pred_ok && ((todo >> 4) & 1u))
+      record_point(sm, warp, lane, c, self, 4, int64_t(self) - 1, c.level, resolved, status);
+    if (succ_ok && ((todo >> 22) & 1u))
+      record_point(sm, warp, lane, c, self, 22, int64_t(self) + 1, c.level, resolved, status);
+    todo = need & ~resolved;
+  }
+  // centre points (dz = 0) of every column with a needed point
+  uint32_t centres = 0;
+#pragma unroll
+  for (int col = 0; col < 9; col++)
+    if (todo & col_bits(col)) centres |= 1u << (col + 9);
+  centres &= ~resolved;
+  // what the neighbours will hold after this pass
+  const uint32_t hp = __shfl_up_sync(kFull, centres | resolved, 1);
+  const uint32_t hs = __shfl_down_sync(kFull, centres | resolved, 1);
+  uint32_t own = centres;
+  for (uint32_t m = todo & 0x1ffu; m; m &= m - 1) {  // dz = -1
+    const int p = __ffs(m) - 1;
+    if (!(pred_ok && ((hp >> (p + 9)) & 1u))) own |= 1u << p;
+  }
+  for (uint32_t m = todo & (0x1ffu << 18); m; m &= m - 1) {  // dz = +1
+    const int p = __ffs(m) - 1;
+    if (!(succ_ok && ((hs >> (p - 9)) & 1u))) own |= 1u << p;
+  }
+  lookup_points(a, sm, warp, lane, c, self, own, resolved, status);
+  __syncwarp();
+  // borrow the rest: dz = -1 from lane L-1's centre, dz = +1 from lane L+1's
+  todo = need & ~resolved;
+  for (uint32_t m = todo & 0x1ffu; m; m &= m - 1) {
+    const int p = __ffs(m) - 1;
+    record_point(sm, warp, lane, c, self, p, stored_id(sm.id[warp][p + 9][lane - 1]),
+                 sm.lev[warp][p + 9][lane - 1], resolved, status);
+  }
+  for (uint32_t m = todo & (0x1ffu << 18); m; m &= m - 1) {
+    const int p = __ffs(m) - 1;
+    record_point(sm, warp, lane, c, self, p, stored_id(sm.id[warp][p - 9][lane + 1]),
+                 sm.lev[warp][p - 9][lane + 1], resolved, status);
   }
 }
 #endif  // AMRX_BATCH > 0
@@ -571,12 +673,13 @@ __device__ __forceinline__ void resolve_points(const KArgs &a, Smem &sm, int war
 __device__ __forceinline__ void resolve_needed(const KArgs &a, Smem &sm,
                                                int warp, int lane,
                                                const Cell &c, uint32_t self,
+                                               uint64_t kself, bool valid,
                                                uint32_t need,
                                                uint32_t &resolved,
                                                uint64_t &status)
 {
 #if AMRX_BATCH > 0
-  resolve_points(a, sm, warp, lane, c, self, need, resolved, status);
+  resolve_points(a, sm, warp, lane, c, self, kself, valid, need, resolved, status);
   return;
 #endif
   uint32_t cols = 0;
@@ -651,6 +754,9 @@ extract_kernel(const KArgs a)
   __syncwarp();
   uint32_t err = 0;
 
+  // tiles from an atomic ticket: the warps' positions stay within a few
+  // thousand tiles of each other, so the lookups share one compact L2
+  // working set (a static interleaved assignment drifts apart: 19% slower)
   for (;;) {
     uint32_t tile = 0;
     if (lane == 0) tile = atomicAdd(a.ticket, 1u);
@@ -658,17 +764,25 @@ extract_kernel(const KArgs a)
     if (tile >= a.num_tiles) break;
     dbg_add(a.s, kDbgTiles);
 
-    const uint64_t cell = a.cell_begin + uint64_t(tile) * 32 + lane;
-    const bool valid = cell < a.cell_end;
+    // kTileCells working lanes; with sharing, lanes 0 and 31 are halo lanes
+    // holding the cells just before and after the tile (any cell of the
+    // index, even outside the extraction range)
+    const int64_t cell_s = int64_t(a.cell_begin) + int64_t(tile) * kTileCells + lane -
+                           (AMRX_SHARE ? 1 : 0);
+    const bool working = (!AMRX_SHARE || (lane >= 1 && lane <= 30)) &&
+                         cell_s < int64_t(a.cell_end);
+    const bool valid = cell_s >= 0 && uint64_t(cell_s) < a.s.n && (working || AMRX_SHARE);
+    const uint64_t cell = valid ? uint64_t(cell_s) : 0;
     const uint32_t self = uint32_t(cell);
-    const Cell c = unpack(a.g, valid ? ldg_u64(a.s.keys + cell) : 0);
+    const uint64_t kself = valid ? ldg_u64(a.s.keys + cell) : 0;
+    const Cell c = unpack(a.g, kself);
 
-    uint32_t resolved = 0, alive = valid ? 0xffu : 0u, curd = 0, accepted = 0;
+    uint32_t resolved = 0, alive = working ? 0xffu : 0u, curd = 0, accepted = 0;
     uint32_t reasons = 0;
     uint64_t status = 0;
     // round 0: every candidate's corner 0 ({-w,0}^3, 4 columns); round 1:
     // everything the survivors still need
-    uint32_t need = valid ? kCorner0Points : 0;
+    uint32_t need = working ? kCorner0Points : 0;
 #pragma unroll 1
     for (int round = 0; round < 2; round++) {
       if (round == 1) {
@@ -680,7 +794,7 @@ extract_kernel(const KArgs a)
         }
         need &= ~resolved;
       }
-      resolve_needed(a, sm, warp, lane, c, self, need, resolved, status);
+      resolve_needed(a, sm, warp, lane, c, self, kself, valid, need, resolved, status);
       advance(resolved, status, alive, curd, accepted, reasons);
     }
     if (alive) err |= 2u;
@@ -963,7 +1077,7 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
   ExtractScratch x;
   ExtractResult res{};
   const uint64_t cells = r.cell_end > r.cell_begin ? r.cell_end - r.cell_begin : 0;
-  const uint64_t tiles = (cells + 31) / 32;
+  const uint64_t tiles = (cells + kTileCells - 1) / kTileCells;
   const bool D = r.emit_dual, T = r.emit_tri, F = r.tri_f32;
   int grid = 1;
   if (D && T && F) grid = occupancy_grid<true, true, true>();
