@@ -388,8 +388,9 @@ KeyGeom make_geometry(const int64_t mn[3], const int64_t mx[3],
     blocks *= double(g.map_dim[a]);
   }
   const double budget = std::max(double(1 << 26), 4.0 * double(n));
-  // measured net-negative on C4 with the per-lane lookups (the map load sits
-  // in every probe's dependency chain): opt-in via AMRX_LEVEL_MAP=1
+  // consulted on the coarser-probe path only; measured net-negative on C4
+  // (236 vs 216 ms: most coarser probes hit, the map load only adds
+  // latency), so opt-in via AMRX_LEVEL_MAP=1 for hole-heavy data
   static const bool enabled = std::getenv("AMRX_LEVEL_MAP") != nullptr;
   g.map_on = enabled && g.nlevels <= 8 && blocks <= budget;
   return g;
@@ -911,6 +912,61 @@ amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range,
           tris > uint64_t(std::numeric_limits<uint32_t>::max()) / 3)
         fail(AMRX_ERR_LENGTH, "extract_isosurface: mesh too large for 32-bit indices");
     };
+    if (dev_out && !is_device_ptr(xyz9) && cells >= (uint64_t(1) << 24)) {
+      // pinned host output, large input: extract in cell-range chunks (their
+      // concatenation is the candidate order) so each chunk's download
+      // overlaps the next chunk's extraction
+      const int nch = int(std::min<uint64_t>(8, cells >> 23));
+      cudaStream_t cp;
+      cudaEvent_t done[2];
+      AMRX_CUDA(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
+      AMRX_CUDA(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
+      AMRX_CUDA(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+      struct Cleanup {
+        cudaStream_t s;
+        cudaEvent_t e0, e1;
+        ~Cleanup()
+        {
+          cudaStreamSynchronize(s);
+          cudaStreamDestroy(s);
+          cudaEventDestroy(e0);
+          cudaEventDestroy(e1);
+        }
+      } cleanup{cp, done[0], done[1]};
+      ExtractResult tot{};
+      uint64_t off = 0;
+      for (int ci = 0; ci < nch; ci++) {
+        rq.cell_begin = b + cells * uint64_t(ci) / uint64_t(nch);
+        rq.cell_end = b + cells * uint64_t(ci + 1) / uint64_t(nch);
+        rq.final_host = true;
+        rq.xyz = static_cast<char *>(xyz9) + off * tri_bytes;
+        rq.tri_cap = cap > off ? cap - off : 0;
+        rq.copy_stream = cp;
+        rq.out_slot = (ci & 1) ? kWsOutB : kWsOutA;
+        rq.slot_free = ci >= 2 ? done[ci & 1] : nullptr;
+        rq.copy_done = done[ci & 1];
+        rq.bits_ready = ci > 0;
+        const ExtractResult r = run_extract(rq, st);
+        check_result(r, rq.cell_end - rq.cell_begin, true);
+        for (int i = 0; i < 4; i++) tot.counters[i] += r.counters[i];
+        tot.duals += r.duals;
+        tot.tris_counted += r.tris_counted;
+        tot.tris_written += r.tris_written;
+        tot.ms += r.ms;
+        tot.ms2 += r.ms2;
+        tot.launches += r.launches;
+        off += r.tris_written;
+      }
+      AMRX_CUDA(cudaStreamSynchronize(cp));
+      fill_stats(stats, tot, cells);
+      *count = tot.tris_written;
+      C.valid = false;
+      length_check(tot.tris_written);
+      if (tot.tris_written > cap)
+        fail(AMRX_ERR_CAPACITY, "output capacity " + std::to_string(cap) + " < " +
+                                  std::to_string(tot.tris_written) + " triangles");
+      return;
+    }
     if (dev_out) {
       rq.final_host = !is_device_ptr(xyz9);
       rq.xyz = rq.final_host ? xyz9 : xyz_w;

@@ -474,6 +474,9 @@ __device__ __noinline__ Hit probe_coarser(const KArgs &a, const Cell &c, int p,
   const int64_t w = int64_t(1) << c.level;
   const int64_t px = c.i + (p % 3 - 1) * w, py = c.j + ((p / 3) % 3 - 1) * w,
                 pz = c.k + (p / 9 - 1) * w;
+  // only levels present in the point's coarsest-aligned block can hold it
+  // (exact); a point in a hole or outside the domain costs no lookup
+  cand &= block_levels(g, a.lmap, px, py, pz);
   while (cand) {
     const int b = __ffs(cand) - 1;
     cand &= cand - 1;
@@ -557,7 +560,9 @@ __device__ AMRX_LOOKUP_ATTR void lookup_points(const KArgs &a, Smem &sm, int war
         pk[k] = p;
         const int64_t px = c.i + (p % 3 - 1) * w, py = c.j + ((p / 3) % 3 - 1) * w,
                       pz = c.k + (p / 9 - 1) * w;
-        cand[k] = block_levels(g, a.lmap, px, py, pz);
+        // every present level is a candidate here; the block level map is
+        // consulted only on the rare coarser-probe path (probe_coarser)
+        cand[k] = (1u << g.nlevels) - 1;
         // at the hint level the point is its own anchor
         v[k] = px >= g.mn[0] && px <= g.mx[0] && py >= g.mn[1] && py <= g.mx[1] &&
                pz >= g.mn[2] && pz <= g.mx[2] && (cand[k] & le_hint);
@@ -1118,11 +1123,14 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
     const uint64_t words = (r.s.n + 31) / 32;
     x.bits.reserve(words * 4 + 64, st);
     k.above = x.bits.as<uint32_t>();
-    const int bgrid = int(std::min<uint64_t>((words + 7) / 8, uint64_t(device_sm_count()) * 16));
-    sign_bits_kernel<<<std::max(1, bgrid), 256, 0, st>>>(r.scal, r.s.n, r.iso,
-                                                         x.bits.as<uint32_t>());
-    AMRX_LAUNCH_CHECK();
-    res.launches += 1;
+    if (!r.bits_ready) {
+      const int bgrid =
+        int(std::min<uint64_t>((words + 7) / 8, uint64_t(device_sm_count()) * 16));
+      sign_bits_kernel<<<std::max(1, bgrid), 256, 0, st>>>(r.scal, r.s.n, r.iso,
+                                                           x.bits.as<uint32_t>());
+      AMRX_LAUNCH_CHECK();
+      res.launches += 1;
+    }
   }
   k.scal = r.scal;
   k.cell_begin = r.cell_begin;
@@ -1235,18 +1243,36 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
     res.launches += scan_exclusive_u32_u64(tri_cnt, final_off, tiles, x.scan, st);
     const uint64_t keep = std::min(res.tris_written, r.tri_cap);
     uint32_t *dx = static_cast<uint32_t *>(r.xyz);
+    WsBuf chunk_buf(r.out_slot >= 0 ? r.out_slot : kWsOutA);
     if (r.final_host) {
-      host_a.reserve(keep * tri_words * 4 + 16, st);
-      dx = host_a.as<uint32_t>();
+      WsBuf &hb = r.out_slot >= 0 ? chunk_buf : host_a;
+      hb.reserve(keep * tri_words * 4 + 16, st);
+      dx = hb.as<uint32_t>();
+      // the previous copy out of this buffer must have drained
+      if (r.slot_free) AMRX_CUDA(cudaStreamWaitEvent(st, r.slot_free, 0));
     }
     reorder_kernel<<<std::max(1, rgrid), 256, 0, st>>>(
       tri_cnt, tri_off, final_off, uint32_t(tiles), tri_words,
       x.stage_a.as<uint32_t>(), dx, r.tri_cap, 0, nullptr, nullptr);
     AMRX_LAUNCH_CHECK();
     res.launches += 1;
-    if (r.final_host)
-      AMRX_CUDA(cudaMemcpyAsync(r.xyz, dx, keep * tri_words * 4,
-                                cudaMemcpyDeviceToHost, st));
+    if (r.final_host) {
+      if (r.copy_stream) {
+        // overlapped: the copy drains on its own stream while the caller
+        // extracts the next chunk
+        cudaEvent_t ready;
+        AMRX_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+        AMRX_CUDA(cudaEventRecord(ready, st));
+        AMRX_CUDA(cudaStreamWaitEvent(r.copy_stream, ready, 0));
+        AMRX_CUDA(cudaMemcpyAsync(r.xyz, dx, keep * tri_words * 4,
+                                  cudaMemcpyDeviceToHost, r.copy_stream));
+        if (r.copy_done) AMRX_CUDA(cudaEventRecord(r.copy_done, r.copy_stream));
+        cudaEventDestroy(ready);
+      } else {
+        AMRX_CUDA(cudaMemcpyAsync(r.xyz, dx, keep * tri_words * 4,
+                                  cudaMemcpyDeviceToHost, st));
+      }
+    }
   }
   AMRX_CUDA(cudaEventRecord(e2, st));
   AMRX_CUDA(cudaStreamSynchronize(st));

@@ -172,6 +172,13 @@ struct ExtractRequest {
   uint64_t tri_cap;
   bool final_host;      // corners/tasks/xyz are pinned host memory
   bool unique;          // the index holds no duplicate keys
+  // chunked host output (iso): D2H on copy_stream from workspace slot
+  // out_slot, after slot_free (if set); copy_done recorded after the copy
+  cudaStream_t copy_stream = nullptr;
+  int out_slot = -1;
+  cudaEvent_t slot_free = nullptr;
+  cudaEvent_t copy_done = nullptr;
+  bool bits_ready = false;  // the sign bits in the workspace are for this iso
 };
 
 struct ExtractResult {

@@ -189,3 +189,13 @@ def test_c4_partitioned_equals_full(P):
         assert (torch.from_numpy(bits(part.fat)).cuda() == digest[acc: acc + k]).all()
         acc += k
     assert acc == total
+    # pinned host output takes the chunked, download-overlapped path
+    host = torch.empty((total + 16, 9), dtype=torch.float64, pin_memory=True)
+    h = P.extract_isosurface(idx, P.IsoParams(iso=synth.C4_ISO), out=host)
+    assert len(h.fat) == total
+    assert (torch.from_numpy(bits(h.fat.numpy())).cuda() == digest).all()
+    # and a too-small pinned buffer reports the needed count
+    small = torch.empty((total // 2, 9), dtype=torch.float64, pin_memory=True)
+    with pytest.raises(P.CapacityError) as e:
+        P.extract_isosurface(idx, P.IsoParams(iso=synth.C4_ISO), out=small)
+    assert e.value.count == total
