@@ -294,7 +294,7 @@ struct amrx_index {
   uint64_t n = 0;
   KeyGeom g{};
   int64_t bounds_hi[3] = {0, 0, 0};
-  DevBuf keys, scal, dir, lmap, scratch;
+  DevBuf keys, scal, dir, lmap, order, scratch;
   amrx_index_info info{};
   // last extraction kept on the device for the count-then-copy pattern
   struct Cached {
@@ -440,8 +440,9 @@ void finalize_index(amrx_index *ix)
 {
   pad_keys(ix->keys.as<uint64_t>(), ix->n, ix->stream);
   ix->dir.reserve(((uint64_t(1) << ix->g.dir_bits) + 1) * sizeof(uint32_t), ix->stream);
+  ix->order.reserve(16, ix->stream);
   build_directory(ix->keys.as<uint64_t>(), ix->n, ix->g, ix->dir.as<uint32_t>(),
-                  ix->scratch, ix->stream);
+                  ix->order.as<unsigned long long>(), ix->scratch, ix->stream);
   if (ix->g.map_on) {
     const uint64_t bytes =
       ((uint64_t(ix->g.map_dim[0]) * uint64_t(ix->g.map_dim[1]) *
@@ -450,6 +451,17 @@ void finalize_index(amrx_index *ix)
     build_level_map(ix->keys.as<uint64_t>(), ix->n, ix->g, ix->lmap.as<uint8_t>(),
                     bytes, ix->stream);
   }
+}
+
+/*! the order check fused into the directory build (after the stream has
+    synchronised): sorted keys may not descend; equal neighbours are
+    duplicate cells */
+uint64_t sorted_equal_pairs(amrx_index *ix)
+{
+  unsigned long long h[2];
+  AMRX_CUDA(cudaMemcpy(h, ix->order.ptr, sizeof h, cudaMemcpyDeviceToHost));
+  if (h[0] != 0) fail(AMRX_ERR_INTERNAL, "index keys are not in (i,j,k,level) order");
+  return h[1];
 }
 
 void check_range(const amrx_index *ix, const amrx_range *range, uint64_t &b,
@@ -610,9 +622,6 @@ amrx_status amrx_index_create(const int32_t *cells4, const double *scalars,
                        ix->g.total, sort_scratch, st, &passes);
       if (sc_ready) AMRX_CUDA(cudaStreamWaitEvent(st, sc_ready, 0));
       gather_f64(idx, sc_d, ix->scal.as<double>(), n, st);
-      uint64_t d2 = 0;
-      ingest_order_check(ix->keys.as<uint64_t>(), n, ix->scratch, &d2, &eq, st);
-      if (d2 != 0) fail(AMRX_ERR_INTERNAL, "radix sort left keys out of order");
     }
     finalize_index(ix.get());
     AMRX_CUDA(cudaEventRecord(e1, st));
@@ -621,7 +630,7 @@ amrx_status amrx_index_create(const int32_t *cells4, const double *scalars,
     AMRX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    finish_info(ix.get(), eq, ms);
+    finish_info(ix.get(), sorted_equal_pairs(ix.get()), ms);
     *out = ix.release();
   });
 }
@@ -637,6 +646,7 @@ amrx_status amrx_index_destroy(amrx_index *index)
       index->scal.release();
       index->dir.release();
       index->lmap.release();
+      index->order.release();
       index->scratch.release();
       index->out_a.release();
       index->out_b.release();
@@ -738,7 +748,7 @@ amrx_status amrx_index_adopt(const void *keys_dev, const double *scalars_dev,
     AMRX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    finish_info(ix.get(), uint64_t(g16[11]), ms);
+    finish_info(ix.get(), sorted_equal_pairs(ix.get()), ms);
     *out = ix.release();
   });
 }

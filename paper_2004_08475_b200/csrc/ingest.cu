@@ -125,10 +125,25 @@ __global__ void __launch_bounds__(kThreads)
 gather_kernel(const uint32_t *__restrict__ perm, const double *__restrict__ in,
               double *__restrict__ out, uint64_t n)
 {
+  // four independent random loads in flight per thread (the gather is
+  // bound by outstanding 32-byte sector reads, not by bandwidth)
+  constexpr int U = 4;
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
-       r += stride)
-    out[r] = __ldg(in + __ldg(perm + r));
+  for (uint64_t r0 = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r0 < n;
+       r0 += stride * U) {
+    uint32_t p[U];
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint64_t r = r0 + u * stride;
+      p[u] = r < n ? __ldg(perm + r) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) v[u] = r0 + u * stride < n ? __ldg(in + p[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (r0 + u * stride < n) out[r0 + u * stride] = v[u];
+  }
 }
 
 __global__ void pad_kernel(uint64_t *keys, uint64_t n)
@@ -140,18 +155,36 @@ __global__ void pad_kernel(uint64_t *keys, uint64_t n)
     warp issues one atomic per distinct bucket it holds */
 __global__ void __launch_bounds__(kThreads)
 bucket_count_kernel(const uint64_t *__restrict__ keys, uint64_t n, int shift,
-                    uint32_t *__restrict__ cnt)
+                    uint32_t *__restrict__ cnt, unsigned long long *order2)
 {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   const uint64_t start = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  unsigned long long desc = 0, eq = 0;
   // whole warps iterate together so the match below sees all lanes
   for (uint64_t base = start - (threadIdx.x & 31); base < n; base += stride) {
     const uint64_t r = base + (threadIdx.x & 31);
     const bool in = r < n;
-    const uint64_t b = in ? (ldg_u64(keys + r) >> shift) : ~0ull;
+    const uint64_t k = in ? ldg_u64(keys + r) : 0;
+    // fused order check of the sorted keys (descents must be 0; equal
+    // neighbours are duplicate cells)
+    if (in && r + 1 < n) {
+      const uint64_t k1 = ldg_u64(keys + r + 1);
+      desc += k > k1;
+      eq += k == k1;
+    }
+    const uint64_t b = in ? (k >> shift) : ~0ull;
     const uint32_t peers = __match_any_sync(kFull, b);
     if (in && (__ffs(peers) - 1) == int(threadIdx.x & 31))
       atomicAdd(cnt + b, __popc(peers));
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    desc += __shfl_xor_sync(kFull, desc, off);
+    eq += __shfl_xor_sync(kFull, eq, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (desc) atomicAdd(order2, desc);
+    if (eq) atomicAdd(order2 + 1, eq);
   }
 }
 
@@ -262,19 +295,53 @@ scan_downsweep_kernel(const T *in, A *out, uint64_t n,
                         uint64_t(threadIdx.x) * kScanItems;
   A v[kScanItems];
   A s = 0;
+  const bool full = base + kScanItems <= n;
+  if (full && (sizeof(T) * kScanItems) % 16 == 0 &&
+      (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+    // a thread's items are contiguous: 16-byte vector loads
+    constexpr int per = 16 / sizeof(T);
+    const uint4 *src = reinterpret_cast<const uint4 *>(in + base);
 #pragma unroll
-  for (int t = 0; t < kScanItems; t++) {
-    const uint64_t r = base + t;
-    v[t] = r < n ? A(in[r]) : A(0);
-    s += v[t];
+    for (int q = 0; q < kScanItems / per; q++) {
+      const uint4 w = src[q];
+      const T *e = reinterpret_cast<const T *>(&w);
+#pragma unroll
+      for (int t = 0; t < per; t++) v[q * per + t] = A(e[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < kScanItems; t++) s += v[t];
+  } else {
+#pragma unroll
+    for (int t = 0; t < kScanItems; t++) {
+      const uint64_t r = base + t;
+      v[t] = r < n ? A(in[r]) : A(0);
+      s += v[t];
+    }
   }
   A run = block_exclusive_sum<A>(s, sm, nullptr) +
           (block_offsets ? block_offsets[blockIdx.x] : A(0));
+  if (full && (sizeof(A) * kScanItems) % 16 == 0 &&
+      (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+    constexpr int per = 16 / sizeof(A);
+    uint4 *dst = reinterpret_cast<uint4 *>(out + base);
 #pragma unroll
-  for (int t = 0; t < kScanItems; t++) {
-    const uint64_t r = base + t;
-    if (r < n) out[r] = run;
-    run += v[t];
+    for (int q = 0; q < kScanItems / per; q++) {
+      uint4 w;
+      A *e = reinterpret_cast<A *>(&w);
+#pragma unroll
+      for (int t = 0; t < per; t++) {
+        e[t] = run;
+        run += v[q * per + t];
+      }
+      dst[q] = w;
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < kScanItems; t++) {
+      const uint64_t r = base + t;
+      if (r < n) out[r] = run;
+      run += v[t];
+    }
   }
 }
 
@@ -372,12 +439,14 @@ void pad_keys(uint64_t *keys, uint64_t n, cudaStream_t st)
 }
 
 void build_directory(const uint64_t *keys, uint64_t n, const KeyGeom &g,
-                     uint32_t *dir, DevBuf &scratch, cudaStream_t st)
+                     uint32_t *dir, unsigned long long *order2, DevBuf &scratch,
+                     cudaStream_t st)
 {
   const uint64_t entries = (uint64_t(1) << g.dir_bits) + 1;
   AMRX_CUDA(cudaMemsetAsync(dir, 0, entries * sizeof(uint32_t), st));
+  AMRX_CUDA(cudaMemsetAsync(order2, 0, 16, st));
   bucket_count_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(
-    keys, n, g.dir_shift, dir);
+    keys, n, g.dir_shift, dir, order2);
   AMRX_LAUNCH_CHECK();
   scan_exclusive_u32(dir, dir, entries, scratch, st);
 }

@@ -124,9 +124,11 @@ void gather_f64(const uint32_t *perm, const double *in, double *out,
 /// fill kKeyPad sentinels (all ones) after the n sorted keys
 void pad_keys(uint64_t *keys, uint64_t n, cudaStream_t st);
 
-/// dir[b] = first position whose key >> g.dir_shift >= b, b in [0, 2^D]
+/// dir[b] = first position whose key >> g.dir_shift >= b, b in [0, 2^D];
+/// order2 (device, 2 x u64) receives the keys' descents and equal pairs
 void build_directory(const uint64_t *keys, uint64_t n, const KeyGeom &g,
-                     uint32_t *dir, DevBuf &scratch, cudaStream_t st);
+                     uint32_t *dir, unsigned long long *order2, DevBuf &scratch,
+                     cudaStream_t st);
 
 /// block level map (KeyGeom::map_*): fill map (map bytes, zeroed here)
 void build_level_map(const uint64_t *keys, uint64_t n, const KeyGeom &g,

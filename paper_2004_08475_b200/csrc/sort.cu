@@ -19,7 +19,10 @@ constexpr int kRadixBits = 8;
 constexpr int kDigits = 1 << kRadixBits;
 constexpr int kSortThreads = 512;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortItems = 8;  // keys per thread
+#ifndef AMRX_SORT_ITEMS
+#define AMRX_SORT_ITEMS 8
+#endif
+constexpr int kSortItems = AMRX_SORT_ITEMS;  // keys per thread
 constexpr int kSortTile = kSortThreads * kSortItems;
 constexpr int kMaxPasses = 8;
 
