@@ -119,6 +119,54 @@ __host__ __device__ inline Cell unpack(const KeyGeom &g, uint64_t key)
   return c;
 }
 
+/*! the 27-point stencil {-w,0,w}^3 of one cell at its own level, in packed
+    key space: a stencil point p = (ox+1) + 3(oy+1) + 9(oz+1) is its own
+    anchor at the cell's level, so its key is the cell's key plus packed
+    per-axis steps -- valid exactly when the point lies in the stored
+    anchor range (bit p of `inrange`). */
+struct Stencil {
+  uint64_t k0;          // key of the cell itself
+  uint64_t sx, sy, sz;  // packed +w per axis (0 for a constant axis)
+  uint32_t inrange;     // bit p: point p's anchor is inside [mn, mx]^3
+};
+
+__host__ __device__ inline Stencil make_stencil(const KeyGeom &g, uint64_t key, int level)
+{
+  Stencil s;
+  s.k0 = key;
+  const uint64_t wu = uint64_t(1) << (level - g.shift);  // w in packed units
+  uint32_t out = 0;
+  // points with o_axis = -1 / +1, for axis x, y, z (p%3, p/3%3, p/9)
+  const uint32_t m_minus[3] = {0x1249249u, 0x1C0E07u, 0x1FFu};
+  const uint32_t m_plus[3] = {0x4924924u, 0x70381C0u, 0x7FC0000u};
+  uint64_t *step[3] = {&s.sx, &s.sy, &s.sz};
+  for (int a = 0; a < 3; a++) {
+    if (!g.bits[a]) {
+      *step[a] = 0;
+      out |= m_minus[a] | m_plus[a];  // a constant axis has no neighbours
+      continue;
+    }
+    const uint64_t u = (key >> g.sh[a]) & ((uint64_t(1) << g.bits[a]) - 1);
+    const uint64_t umax = uint64_t(g.mx[a] - g.mn[a]) >> g.shift;
+    *step[a] = wu << g.sh[a];
+    if (u < wu) out |= m_minus[a];
+    if (u + wu > umax) out |= m_plus[a];
+  }
+  s.inrange = ~out & 0x7FFFFFFu;
+  return s;
+}
+
+/// key of stencil point p (meaningful when bit p of inrange is set)
+__host__ __device__ inline uint64_t stencil_key(const Stencil &s, int p)
+{
+  const int ox = p % 3 - 1, oy = (p / 3) % 3 - 1, oz = p / 9 - 1;
+  uint64_t k = s.k0;
+  k += ox > 0 ? s.sx : (ox < 0 ? uint64_t(0) - s.sx : 0);
+  k += oy > 0 ? s.sy : (oy < 0 ? uint64_t(0) - s.sy : 0);
+  k += oz > 0 ? s.sz : (oz < 0 ? uint64_t(0) - s.sz : 0);
+  return k;
+}
+
 // ------------------------------------------------------------------------
 // device helpers
 

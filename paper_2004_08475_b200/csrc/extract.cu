@@ -532,12 +532,12 @@ __device__ __forceinline__ void record_point(Smem &sm, int warp, int lane, const
 #define AMRX_LOOKUP_ATTR __forceinline__
 #endif
 __device__ AMRX_LOOKUP_ATTR void lookup_points(const KArgs &a, Smem &sm, int warp, int lane,
-                                              const Cell &c, uint32_t self, uint32_t todo,
+                                              const Cell &c, const Stencil &st,
+                                              uint32_t self, uint32_t todo,
                                               uint32_t &resolved, uint64_t &status)
 {
   constexpr int K = AMRX_BATCH;
   const KeyGeom &g = a.g;
-  const int64_t w = int64_t(1) << c.level;
   const int hint_bit = __popc(g.level_mask & ((1u << c.level) - 1));
   const uint32_t le_hint = (2u << hint_bit) - 1;
   while (__any_sync(kFull, todo != 0)) {
@@ -558,16 +558,13 @@ __device__ AMRX_LOOKUP_ATTR void lookup_points(const KArgs &a, Smem &sm, int war
         const int p = __ffs(todo) - 1;
         todo &= todo - 1;
         pk[k] = p;
-        const int64_t px = c.i + (p % 3 - 1) * w, py = c.j + ((p / 3) % 3 - 1) * w,
-                      pz = c.k + (p / 9 - 1) * w;
         // every present level is a candidate here; the block level map is
         // consulted only on the rare coarser-probe path (probe_coarser)
-        cand[k] = (1u << g.nlevels) - 1;
-        // at the hint level the point is its own anchor
-        v[k] = px >= g.mn[0] && px <= g.mx[0] && py >= g.mn[1] && py <= g.mx[1] &&
-               pz >= g.mn[2] && pz <= g.mx[2] && (cand[k] & le_hint);
-        if (v[k]) q[k] = pack_unchecked(g, px, py, pz, c.level);
-        cand[k] &= ~le_hint;
+        cand[k] = ((1u << g.nlevels) - 1) & ~le_hint;
+        // at the hint level the point is its own anchor: key = cell key +
+        // packed steps, valid iff inside the stored range
+        v[k] = (st.inrange >> p) & 1u;
+        q[k] = stencil_key(st, p);
       }
     }
     batch_find<K, true>(a.s, q, v, out, lvl);
@@ -600,27 +597,26 @@ __device__ AMRX_LOOKUP_ATTR void lookup_points(const KArgs &a, Smem &sm, int war
     borrows, so no working lane is left without a neighbour.  Exact by
     construction: a borrowed answer is the answer to the very same query. */
 __device__ __forceinline__ void resolve_points(const KArgs &a, Smem &sm, int warp, int lane,
-                                               const Cell &c, uint32_t self, uint64_t kself,
-                                               bool valid, uint32_t need, uint32_t &resolved,
+                                               const Cell &c, const Stencil &st, uint32_t self,
+                                               uint64_t kself, bool valid, uint32_t need,
+                                               uint32_t &resolved,
                                                uint64_t &status)
 {
   if (!AMRX_SHARE) {
     uint32_t todo = need & ~resolved;
     if (a.unique && ((todo >> 13) & 1u))
       record_point(sm, warp, lane, c, self, 13, self, c.level, resolved, status);
-    lookup_points(a, sm, warp, lane, c, self, need & ~resolved, resolved, status);
+    lookup_points(a, sm, warp, lane, c, st, self, need & ~resolved, resolved, status);
     return;
   }
-  const KeyGeom &g = a.g;
-  const int64_t w = int64_t(1) << c.level;
   // is lane L-1 (L+1) this cell's z-predecessor (successor) on the same level?
-  const uint64_t dz = g.bits[2] ? (uint64_t(w >> g.shift) << g.sh[2]) : 0;
+  const uint64_t dz = st.sz;
   const uint64_t kp = __shfl_up_sync(kFull, kself, 1);
   const uint64_t ks = __shfl_down_sync(kFull, kself, 1);
   const bool vp = __shfl_up_sync(kFull, valid, 1);
   const bool vs = __shfl_down_sync(kFull, valid, 1);
-  const bool pred_ok = valid && lane > 0 && vp && dz && c.k - w >= g.mn[2] && kp == kself - dz;
-  const bool succ_ok = valid && lane < 31 && vs && dz && c.k + w <= g.mx[2] && ks == kself + dz;
+  const bool pred_ok = valid && lane > 0 && vp && ((st.inrange >> 4) & 1u) && kp == kself - dz;
+  const bool succ_ok = valid && lane < 31 && vs && ((st.inrange >> 22) & 1u) && ks == kself + dz;
 
   // halo lanes: adopt what the neighbour will borrow (lane 0 serves lane 1's
   // dz = -1 points, lane 31 serves lane 30's dz = +1 points)
@@ -658,7 +654,7 @@ __device__ __forceinline__ void resolve_points(const KArgs &a, Smem &sm, int war
     const int p = __ffs(m) - 1;
     if (!(succ_ok && ((hs >> (p - 9)) & 1u))) own |= 1u << p;
   }
-  lookup_points(a, sm, warp, lane, c, self, own, resolved, status);
+  lookup_points(a, sm, warp, lane, c, st, self, own, resolved, status);
   __syncwarp();
   // borrow the rest: dz = -1 from lane L-1's centre, dz = +1 from lane L+1's
   todo = need & ~resolved;
@@ -677,14 +673,14 @@ __device__ __forceinline__ void resolve_points(const KArgs &a, Smem &sm, int war
 
 __device__ __forceinline__ void resolve_needed(const KArgs &a, Smem &sm,
                                                int warp, int lane,
-                                               const Cell &c, uint32_t self,
-                                               uint64_t kself, bool valid,
+                                               const Cell &c, const Stencil &st,
+                                               uint32_t self, uint64_t kself, bool valid,
                                                uint32_t need,
                                                uint32_t &resolved,
                                                uint64_t &status)
 {
 #if AMRX_BATCH > 0
-  resolve_points(a, sm, warp, lane, c, self, kself, valid, need, resolved, status);
+  resolve_points(a, sm, warp, lane, c, st, self, kself, valid, need, resolved, status);
   return;
 #endif
   uint32_t cols = 0;
@@ -781,6 +777,7 @@ extract_kernel(const KArgs a)
     const uint32_t self = uint32_t(cell);
     const uint64_t kself = valid ? ldg_u64(a.s.keys + cell) : 0;
     const Cell c = unpack(a.g, kself);
+    const Stencil st = make_stencil(a.g, kself, c.level);
 
     uint32_t resolved = 0, alive = working ? 0xffu : 0u, curd = 0, accepted = 0;
     uint32_t reasons = 0;
@@ -799,7 +796,7 @@ extract_kernel(const KArgs a)
         }
         need &= ~resolved;
       }
-      resolve_needed(a, sm, warp, lane, c, self, kself, valid, need, resolved, status);
+      resolve_needed(a, sm, warp, lane, c, st, self, kself, valid, need, resolved, status);
       advance(resolved, status, alive, curd, accepted, reasons);
     }
     if (alive) err |= 2u;
