@@ -294,7 +294,7 @@ struct amrx_index {
   uint64_t n = 0;
   KeyGeom g{};
   int64_t bounds_hi[3] = {0, 0, 0};
-  DevBuf keys, scal, dir, lmap, order, scratch;
+  DevBuf keys, scal, dir, occ, lmap, order, scratch;
   amrx_index_info info{};
   // last extraction kept on the device for the count-then-copy pattern
   struct Cached {
@@ -319,6 +319,8 @@ struct amrx_index {
     s.shift = g.shift;
     s.lmask = (uint64_t(1) << g.lbits) - 1;
     s.dbg = nullptr;
+    // popcount positions hold only without duplicate keys
+    s.occ = g.occ && info.duplicate_keys == 0 ? occ.as<uint64_t>() : nullptr;
     return s;
   }
 };
@@ -378,6 +380,13 @@ KeyGeom make_geometry(const int64_t mn[3], const int64_t mx[3],
   const int want = dir_env ? std::max(1, std::min(33, std::atoi(dir_env)))
                            : std::min(30, std::max(10, bit_width(n) + 1));
   g.dir_bits = std::min(g.total, want);
+  // occupancy directory (AMRX_OCC=0 disables): 64 key values per bucket,
+  // when that many buckets cost at most ~4 per cell (12 B each)
+  static const char *occ_env = std::getenv("AMRX_OCC");
+  const int occ_bits = std::max(0, g.total - kOccShift);
+  g.occ = !(occ_env && occ_env[0] == '0') && !dir_env && occ_bits <= 31 &&
+          (uint64_t(1) << occ_bits) <= 4 * n + (uint64_t(1) << 20);
+  if (g.occ) g.dir_bits = occ_bits;
   g.dir_shift = g.total - g.dir_bits;
   // block level map at the coarsest level's granularity, if it is small
   g.map_shift = hi_level;
@@ -410,7 +419,8 @@ void finish_info(amrx_index *ix, uint64_t equal_pairs, double ms)
   in.key_bits = ix->g.total;
   in.directory_bits = ix->g.dir_bits;
   in.duplicate_keys = equal_pairs;
-  in.device_bytes = ix->keys.bytes + ix->scal.bytes + ix->dir.bytes;
+  in.device_bytes = ix->keys.bytes + ix->scal.bytes + ix->dir.bytes +
+                    (ix->g.occ ? ix->occ.bytes : 0);
   in.seconds_ingest = ms / 1000.0;
 }
 
@@ -441,7 +451,10 @@ void finalize_index(amrx_index *ix)
   pad_keys(ix->keys.as<uint64_t>(), ix->n, ix->stream);
   ix->dir.reserve(((uint64_t(1) << ix->g.dir_bits) + 1) * sizeof(uint32_t), ix->stream);
   ix->order.reserve(16, ix->stream);
+  if (ix->g.occ)
+    ix->occ.reserve(((uint64_t(1) << ix->g.dir_bits) + 1) * sizeof(uint64_t), ix->stream);
   build_directory(ix->keys.as<uint64_t>(), ix->n, ix->g, ix->dir.as<uint32_t>(),
+                  ix->g.occ ? ix->occ.as<uint64_t>() : nullptr,
                   ix->order.as<unsigned long long>(), ix->scratch, ix->stream);
   if (ix->g.map_on) {
     const uint64_t bytes =
@@ -645,6 +658,7 @@ amrx_status amrx_index_destroy(amrx_index *index)
       index->keys.release();
       index->scal.release();
       index->dir.release();
+      index->occ.release();
       index->lmap.release();
       index->order.release();
       index->scratch.release();

@@ -40,7 +40,13 @@ struct KeyGeom {
   int32_t map_shift;
   int64_t map_base[3];  // block index of the lowest anchor per axis
   int64_t map_dim[3];   // blocks per axis
+  // occupancy directory: buckets are 64 consecutive key values (dir_shift
+  // = 6, or one bucket when total <= 6) and occ[b] bit v is set iff key
+  // (b << 6) + v is stored, so a lookup is two loads and a popcount
+  int32_t occ;
 };
+
+constexpr int kOccShift = 6;  // key values per occupancy word = 2^6
 
 /// candidate-level bits (index into g.levels) for point p from the map
 __device__ __forceinline__ uint32_t block_levels(const KeyGeom &g,
@@ -244,7 +250,36 @@ struct SearchCtx {
   int32_t shift;         // finest level present (level field offset)
   uint64_t lmask;        // mask of the level field
   unsigned long long *dbg;  // optional event counters (AMRX_DEBUG_COUNTERS)
+  // occupancy words parallel to dir (KeyGeom::occ), or null: set only for
+  // an index without duplicate keys, where position = dir[b] + popcount
+  const uint64_t *occ;
 };
+
+/*! lookup through the occupancy directory (SearchCtx::occ): the exact key,
+    or under FINER the first stored key with q's anchor and a lower level
+    field -- the finest cell at that anchor, which sorts first -- exactly
+    what the bucket search returns for unique keys (the level field is the
+    key's low part and 64 is a multiple of 2^lbits, so an anchor's keys
+    share one word).  `word` and `start` are occ[b] and dir[b]. */
+template <bool FINER>
+__device__ __forceinline__ int64_t occ_resolve(uint64_t q, uint64_t word, uint32_t start,
+                                               uint64_t lmask, int &rl)
+{
+  const int bit = int(q & 63);
+  const uint64_t below = word & ((uint64_t(1) << bit) - 1);
+  rl = int(q & lmask);
+  if ((word >> bit) & 1u) return int64_t(start) + __popcll(below);
+  if (FINER) {
+    const int grp = bit & ~int(lmask);  // first value of q's anchor
+    const uint64_t m = below & ~((uint64_t(1) << grp) - 1);
+    if (m) {
+      const int f = __ffsll((long long)m) - 1;
+      rl = f & int(lmask);
+      return int64_t(start) + __popcll(word & ((uint64_t(1) << f) - 1));
+    }
+  }
+  return -1;
+}
 
 /// debug event counters, one atomic per warp-level event, lane 0 only
 enum DbgEvent {
@@ -314,6 +349,13 @@ __device__ __forceinline__ void lane_find(const SearchCtx &s, const uint64_t (&q
 #pragma unroll
   for (int t = 0; t < NQ; t++) {
     if (!valid[t]) continue;
+    if (s.occ) {
+      const uint64_t b = q[t] >> s.dir_shift;
+      int rl;
+      out[t] = occ_resolve<FINER>(q[t], ldg_u64(s.occ + b), __ldg(s.dir + b), s.lmask, rl);
+      lvl[t] = rl + s.shift;
+      continue;
+    }
     const uint64_t anchor = q[t] & ~s.lmask;
     uint64_t lo = __ldg(s.dir + ((FINER ? anchor : q[t]) >> s.dir_shift));
     const uint64_t hi = __ldg(s.dir + (q[t] >> s.dir_shift) + 1);
@@ -365,6 +407,28 @@ __device__ __forceinline__ void batch_find(const SearchCtx &s, const uint64_t (&
                                            const bool (&valid)[K], int64_t (&out)[K],
                                            int (&lvl)[K])
 {
+  if (s.occ) {  // occupancy directory: no search at all
+    uint64_t word[K];
+    uint32_t start[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+      word[k] = 0;
+      start[k] = 0;
+      if (valid[k]) {
+        const uint64_t b = q[k] >> s.dir_shift;
+        word[k] = ldg_u64(s.occ + b);
+        start[k] = __ldg(s.dir + b);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < K; k++)
+      if (valid[k]) {
+        int rl;
+        out[k] = occ_resolve<FINER>(q[k], word[k], start[k], s.lmask, rl);
+        lvl[k] = rl + s.shift;
+      }
+    return;
+  }
   uint32_t lo[K], n[K];
 #pragma unroll
   for (int k = 0; k < K; k++) {

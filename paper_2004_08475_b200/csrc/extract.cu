@@ -13,21 +13,20 @@
 //   sliver drop on exact equality                     proj/src/contour.cpp:80-84
 //   two-pass count -> prefix -> emit                  proj/src/pipeline.cpp:80-146
 //
-// B200 design: one warp owns 32 consecutive cells (a "tile",
-// handed out in order by an atomic ticket).  Instead of 8 independent
-// candidates x 8 corner snaps, the warp resolves the cell's 27-point stencil
-// {-w,0,w}^3 column by column: one column = the three points (dx,dy,{-1,0,1})
-// whose keys are adjacent in the (i,j,k,level) order, so the 32 lanes' 96
-// queries of a column land in one or two 1 KB key windows staged in shared
-// memory (warp_find).  Round 1 resolves the 4 columns holding every
-// candidate's corner 0 (82-86% of candidates die there); round 2 resolves the
-// remaining columns the survivors need.  The rules are then applied corner by
-// corner in the reference's order, so the reported reason is the reference's.
-// Counting and emitting happen in the same kernel: a warp-scan gives
-// per-lane offsets and a decoupled look-back over tile aggregates gives the
-// tile's global offset -- the reference's "pass 1 / prefix sum / pass 2"
-// with the prefix sum made single-pass, so candidate order is preserved
-// without running the search twice.
+// B200 design: one warp owns a tile of 30 consecutive cells
+// (lanes 1..30; lanes 0 and 31 are halo lanes holding the cells either side),
+// handed out by an atomic ticket.  Instead of 8 independent candidates x 8
+// corner snaps, each lane resolves its cell's 27-point stencil {-w,0,w}^3 --
+// a per-tile packed Stencil makes every point's key a few adds -- with
+// AMRX_BATCH lock-step directory-bucket searches (batch_find), and borrows
+// the dz = +-1 points from its z-neighbour lanes, whose centre points are the
+// identical queries.  Round 0 resolves every candidate's corner 0 (82-86% of
+// candidates die there); round 1 what the survivors still need.  The rules
+// are then applied corner by corner in the reference's order, so the
+// reported reason is the reference's.  Duals and triangles go to per-warp
+// staging chunks with per-tile (offset, count) records; a scan over the tile
+// counts and reorder_kernel restore candidate order -- the reference's
+// "pass 1 / prefix sum / pass 2" with the search run once.
 #include "internal.h"
 #include "mc_tables.inc"
 
@@ -124,9 +123,6 @@ __device__ __forceinline__ uint64_t reserve(uint64_t *cur_end, uint32_t agg,
   return cur;
 }
 
-/*! move each tile's block from its staging position to its place in
-    candidate order (final offset = exclusive scan of tile counts): one warp
-    per tile, `words` 32-bit words per item, coalesced both ways */
 /// bit i of the result: scalar i > iso (the strict case test of contour.cpp:22-28)
 __global__ void __launch_bounds__(256)
 sign_bits_kernel(const double *__restrict__ scal, uint64_t n, double iso,
@@ -141,6 +137,9 @@ sign_bits_kernel(const double *__restrict__ scal, uint64_t n, double iso,
   }
 }
 
+/*! move each tile's block from its staging position to its place in
+    candidate order (final offset = exclusive scan of tile counts): one warp
+    per tile, `words` 32-bit words per item, coalesced both ways */
 __global__ void __launch_bounds__(256)
 reorder_kernel(const uint32_t *__restrict__ cnt, const uint64_t *__restrict__ src_off,
                const uint64_t *__restrict__ dst_off, uint32_t tiles, int words,

@@ -155,7 +155,8 @@ __global__ void pad_kernel(uint64_t *keys, uint64_t n)
     warp issues one atomic per distinct bucket it holds */
 __global__ void __launch_bounds__(kThreads)
 bucket_count_kernel(const uint64_t *__restrict__ keys, uint64_t n, int shift,
-                    uint32_t *__restrict__ cnt, unsigned long long *order2)
+                    uint32_t *__restrict__ cnt, unsigned long long *order2,
+                    unsigned long long *__restrict__ occ)
 {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   const uint64_t start = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -174,8 +175,20 @@ bucket_count_kernel(const uint64_t *__restrict__ keys, uint64_t n, int shift,
     }
     const uint64_t b = in ? (k >> shift) : ~0ull;
     const uint32_t peers = __match_any_sync(kFull, b);
-    if (in && (__ffs(peers) - 1) == int(threadIdx.x & 31))
-      atomicAdd(cnt + b, __popc(peers));
+    const bool leader = in && (__ffs(peers) - 1) == int(threadIdx.x & 31);
+    if (leader) atomicAdd(cnt + b, __popc(peers));
+    if (occ) {
+      // occupancy word of the bucket: OR of its keys' low-6-bit values over
+      // the run of lanes holding it (sorted keys: runs are contiguous)
+      unsigned long long bits = in ? 1ull << (k & 63) : 0ull;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const unsigned long long y = __shfl_down_sync(kFull, bits, off);
+        const uint64_t bo = __shfl_down_sync(kFull, (unsigned long long)b, off);
+        if (int(threadIdx.x & 31) + off < 32 && bo == b) bits |= y;
+      }
+      if (leader) atomicOr(occ + b, bits);
+    }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -439,14 +452,15 @@ void pad_keys(uint64_t *keys, uint64_t n, cudaStream_t st)
 }
 
 void build_directory(const uint64_t *keys, uint64_t n, const KeyGeom &g,
-                     uint32_t *dir, unsigned long long *order2, DevBuf &scratch,
-                     cudaStream_t st)
+                     uint32_t *dir, uint64_t *occ, unsigned long long *order2,
+                     DevBuf &scratch, cudaStream_t st)
 {
   const uint64_t entries = (uint64_t(1) << g.dir_bits) + 1;
   AMRX_CUDA(cudaMemsetAsync(dir, 0, entries * sizeof(uint32_t), st));
+  if (occ) AMRX_CUDA(cudaMemsetAsync(occ, 0, entries * sizeof(uint64_t), st));
   AMRX_CUDA(cudaMemsetAsync(order2, 0, 16, st));
   bucket_count_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(
-    keys, n, g.dir_shift, dir, order2);
+    keys, n, g.dir_shift, dir, order2, reinterpret_cast<unsigned long long *>(occ));
   AMRX_LAUNCH_CHECK();
   scan_exclusive_u32(dir, dir, entries, scratch, st);
 }
