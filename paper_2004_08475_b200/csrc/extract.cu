@@ -43,8 +43,10 @@
 #define AMRX_BATCH 2  // measured best on C4: K=2 234 ms, K=3 242, K=4 286, columns 326
 #endif
 // 1: borrow z-neighbour lanes' lookups (resolve_points); 0: every lane alone
+// (with the occupancy directory a lookup costs less than the sharing's
+// shuffles: C4 iso 141 ms shared vs 125 ms alone, both at AMRX_MINB 4)
 #ifndef AMRX_SHARE
-#define AMRX_SHARE 1
+#define AMRX_SHARE 0
 #endif
 
 namespace amrx {
@@ -192,7 +194,9 @@ struct KArgs {
 };
 
 struct Smem {
-  uint64_t win[kWarps][kWin];
+#if !AMRX_LANE_SEARCH
+  uint64_t win[kWarps][kWin];  // warp_find's key windows
+#endif
   uint32_t id[kWarps][27][32];
   uint8_t lev[kWarps][27][32];
   uint64_t mc_rows[256];
@@ -421,7 +425,11 @@ __device__ __forceinline__ void resolve_column(const KArgs &a, Smem &sm,
         v2[t] = query_key(g, px, py, c.k + (t - 1) * w, L[t], q[t]);
       }
     }
+#if AMRX_LANE_SEARCH
+    find3_coarse(a.s, q, v2, o2, l2, nullptr);
+#else
     find3_coarse(a.s, q, v2, o2, l2, sm.win[warp]);
+#endif
 #pragma unroll
     for (int t = 0; t < 3; t++)
       if (pend[t]) {
@@ -463,9 +471,10 @@ struct Hit {
 };
 
 /*! coarser-level probe for one point the hint+finer lookup missed: the
-    candidate levels above the hint, ascending (the reference's finest-first
-    order restricted to them).  Per lane, no warp collectives; rare, so out of
-    line -- and scalar, so the caller's batch arrays stay in registers. */
+    present levels above the hint (bit L of `cand` = level L), ascending
+    (the reference's finest-first order restricted to them).  Per lane, no
+    warp collectives; rare, so out of line -- and scalar, so the caller's
+    batch arrays stay in registers. */
 __device__ __noinline__ Hit probe_coarser(const KArgs &a, const Cell &c, int p,
                                           uint32_t cand)
 {
@@ -473,13 +482,16 @@ __device__ __noinline__ Hit probe_coarser(const KArgs &a, const Cell &c, int p,
   const int64_t w = int64_t(1) << c.level;
   const int64_t px = c.i + (p % 3 - 1) * w, py = c.j + ((p / 3) % 3 - 1) * w,
                 pz = c.k + (p / 9 - 1) * w;
-  // only levels present in the point's coarsest-aligned block can hold it
-  // (exact); a point in a hole or outside the domain costs no lookup
-  cand &= block_levels(g, a.lmap, px, py, pz);
+  if (g.map_on) {
+    // only levels present in the point's coarsest-aligned block can hold
+    // it (exact); a point in a hole or outside the domain costs no lookup
+    uint32_t idx = block_levels(g, a.lmap, px, py, pz), lv = 0;
+    for (; idx; idx &= idx - 1) lv |= 1u << g.levels[__ffs(idx) - 1];
+    cand &= lv;
+  }
   while (cand) {
-    const int b = __ffs(cand) - 1;
+    const int L = __ffs(cand) - 1;
     cand &= cand - 1;
-    const int L = g.levels[b];
     uint64_t q[1];
     bool v[1];
     int64_t o[1] = {-1};
@@ -536,30 +548,25 @@ __device__ AMRX_LOOKUP_ATTR void lookup_points(const KArgs &a, Smem &sm, int war
                                               uint32_t &resolved, uint64_t &status)
 {
   constexpr int K = AMRX_BATCH;
-  const KeyGeom &g = a.g;
-  const int hint_bit = __popc(g.level_mask & ((1u << c.level) - 1));
-  const uint32_t le_hint = (2u << hint_bit) - 1;
+  // present levels coarser than the hint: what a miss probes next (the
+  // block level map is consulted only on that rare path, probe_coarser)
+  const uint32_t coarser = a.g.level_mask & ~((2u << c.level) - 1);
   while (__any_sync(kFull, todo != 0)) {
     uint64_t q[K];
     bool v[K];
     int64_t out[K];
     int lvl[K], pk[K];
-    uint32_t cand[K];
 #pragma unroll
     for (int k = 0; k < K; k++) {
       pk[k] = -1;
       v[k] = false;
       out[k] = -1;
       lvl[k] = c.level;
-      cand[k] = 0;
       q[k] = 0;
       if (todo) {
         const int p = __ffs(todo) - 1;
         todo &= todo - 1;
         pk[k] = p;
-        // every present level is a candidate here; the block level map is
-        // consulted only on the rare coarser-probe path (probe_coarser)
-        cand[k] = ((1u << g.nlevels) - 1) & ~le_hint;
         // at the hint level the point is its own anchor: key = cell key +
         // packed steps, valid iff inside the stored range
         v[k] = (st.inrange >> p) & 1u;
@@ -569,9 +576,9 @@ __device__ AMRX_LOOKUP_ATTR void lookup_points(const KArgs &a, Smem &sm, int war
     batch_find<K, true>(a.s, q, v, out, lvl);
 #pragma unroll
     for (int k = 0; k < K; k++)
-      if (pk[k] >= 0 && out[k] < 0 && cand[k] != 0) {
+      if (pk[k] >= 0 && out[k] < 0 && coarser != 0) {
         dbg_add(a.s, kDbgCoarser);
-        const Hit h = probe_coarser(a, c, pk[k], cand[k]);
+        const Hit h = probe_coarser(a, c, pk[k], coarser);
         out[k] = h.id;
         lvl[k] = h.level;
       }
@@ -729,10 +736,10 @@ __device__ __forceinline__ void advance(uint32_t resolved, uint64_t status,
 
 template <bool EMIT_DUAL, bool EMIT_TRI, bool F32>
 #ifndef AMRX_MINB
-#define AMRX_MINB 3  // CTAs per SM the register budget is sized for
+#define AMRX_MINB 4  // CTAs per SM the register budget is sized for (64 regs)
 #endif
 __global__ void __launch_bounds__(kThreads, AMRX_MINB)
-extract_kernel(const KArgs a)
+extract_kernel(const __grid_constant__ KArgs a)
 {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem &sm = *reinterpret_cast<Smem *>(smem_raw);
