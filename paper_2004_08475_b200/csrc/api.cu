@@ -402,6 +402,19 @@ KeyGeom make_geometry(const int64_t mn[3], const int64_t mx[3],
   // latency), so opt-in via AMRX_LEVEL_MAP=1 for hole-heavy data
   static const bool enabled = std::getenv("AMRX_LEVEL_MAP") != nullptr;
   g.map_on = enabled && g.nlevels <= 8 && blocks <= budget;
+  g.aligned = 1;
+  for (int a = 0; a < 3; a++)
+    if (mn[a] & ((int64_t(1) << hi_level) - 1)) g.aligned = 0;
+  const uint64_t lmask = (uint64_t(1) << g.lbits) - 1;
+  for (int L = 0; L < 32; L++) {
+    uint64_t clear = lmask;
+    if (L >= g.shift)
+      for (int a = 0; a < 3; a++) {
+        const int low = std::min(L - g.shift, g.bits[a]);
+        clear |= ((uint64_t(1) << low) - 1) << g.sh[a];
+      }
+    g.cmask[L] = ~clear;
+  }
   return g;
 }
 

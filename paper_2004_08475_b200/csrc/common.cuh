@@ -44,6 +44,12 @@ struct KeyGeom {
   // = 6, or one bucket when total <= 6) and occ[b] bit v is set iff key
   // (b << 6) + v is stored, so a lookup is two loads and a popcount
   int32_t occ;
+  // packed-space coarsening: when every min anchor is aligned to the
+  // coarsest level present (aligned = 1), anchor_mask(p, L) of an in-range
+  // point p is its packed key with the low L-shift bits of each coordinate
+  // field cleared: key_L = (key & cmask[L]) | (L - shift)
+  int32_t aligned;
+  uint64_t cmask[32];
 };
 
 constexpr int kOccShift = 6;  // key values per occupancy word = 2^6

@@ -475,10 +475,25 @@ struct Hit {
     (the reference's finest-first order restricted to them).  Per lane, no
     warp collectives; rare, so out of line -- and scalar, so the caller's
     batch arrays stay in registers. */
-__device__ __noinline__ Hit probe_coarser(const KArgs &a, const Cell &c, int p,
-                                          uint32_t cand)
+__device__ __noinline__ Hit probe_coarser(const KArgs &a, const Cell &c, const Stencil &st,
+                                          int p, uint32_t cand)
 {
   const KeyGeom &g = a.g;
+  if (g.aligned && !g.map_on && ((st.inrange >> p) & 1u)) {
+    // in-range point, aligned origin: coarsen in packed key space
+    const uint64_t q0 = stencil_key(st, p);
+    while (cand) {
+      const int L = __ffs(cand) - 1;
+      cand &= cand - 1;
+      uint64_t q[1] = {(q0 & g.cmask[L]) | uint64_t(L - g.shift)};
+      const bool v[1] = {true};
+      int64_t o[1] = {-1};
+      int l1[1];
+      batch_find<1, false>(a.s, q, v, o, l1);
+      if (o[0] >= 0) return Hit{o[0], L};
+    }
+    return Hit{-1, c.level};
+  }
   const int64_t w = int64_t(1) << c.level;
   const int64_t px = c.i + (p % 3 - 1) * w, py = c.j + ((p / 3) % 3 - 1) * w,
                 pz = c.k + (p / 9 - 1) * w;
@@ -578,7 +593,7 @@ __device__ AMRX_LOOKUP_ATTR void lookup_points(const KArgs &a, Smem &sm, int war
     for (int k = 0; k < K; k++)
       if (pk[k] >= 0 && out[k] < 0 && coarser != 0) {
         dbg_add(a.s, kDbgCoarser);
-        const Hit h = probe_coarser(a, c, pk[k], coarser);
+        const Hit h = probe_coarser(a, c, st, pk[k], coarser);
         out[k] = h.id;
         lvl[k] = h.level;
       }
