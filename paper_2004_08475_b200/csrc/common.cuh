@@ -339,6 +339,33 @@ static __device__ __noinline__ int64_t find_in_bucket(const SearchCtx &s, uint64
   return res;
 }
 
+/// batch_find through the occupancy directory only (s.occ must be set)
+template <int K, bool FINER>
+__device__ __forceinline__ void occ_find(const SearchCtx &s, const uint64_t (&q)[K],
+                                         const bool (&valid)[K], int64_t (&out)[K],
+                                         int (&lvl)[K])
+{
+  uint64_t word[K];
+  uint32_t start[K];
+#pragma unroll
+  for (int k = 0; k < K; k++) {
+    word[k] = 0;
+    start[k] = 0;
+    if (valid[k]) {
+      const uint64_t b = q[k] >> s.dir_shift;
+      word[k] = ldg_u64(s.occ + b);
+      start[k] = __ldg(s.dir + b);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < K; k++)
+    if (valid[k]) {
+      int rl;
+      out[k] = occ_resolve<FINER>(q[k], word[k], start[k], s.lmask, rl);
+      lvl[k] = rl + s.shift;
+    }
+}
+
 /*! Per-lane lookup of NQ ascending keys inside their own directory buckets
     (no warp cooperation): with ~2 directory entries per cell a bucket
     holds a handful of keys, so each query costs two directory loads and a
@@ -414,25 +441,7 @@ __device__ __forceinline__ void batch_find(const SearchCtx &s, const uint64_t (&
                                            int (&lvl)[K])
 {
   if (s.occ) {  // occupancy directory: no search at all
-    uint64_t word[K];
-    uint32_t start[K];
-#pragma unroll
-    for (int k = 0; k < K; k++) {
-      word[k] = 0;
-      start[k] = 0;
-      if (valid[k]) {
-        const uint64_t b = q[k] >> s.dir_shift;
-        word[k] = ldg_u64(s.occ + b);
-        start[k] = __ldg(s.dir + b);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < K; k++)
-      if (valid[k]) {
-        int rl;
-        out[k] = occ_resolve<FINER>(q[k], word[k], start[k], s.lmask, rl);
-        lvl[k] = rl + s.shift;
-      }
+    occ_find<K, FINER>(s, q, valid, out, lvl);
     return;
   }
   uint32_t lo[K], n[K];

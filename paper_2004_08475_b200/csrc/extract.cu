@@ -42,6 +42,11 @@
 #ifndef AMRX_BATCH
 #define AMRX_BATCH 2  // measured best on C4: K=2 234 ms, K=3 242, K=4 286, columns 326
 #endif
+// 1: point classification masks + mask-based rules (resolve_marks); 0: the
+// 2-bit status walk (lookup_points / resolve_points + advance)
+#ifndef AMRX_COLUMNS
+#define AMRX_COLUMNS 1
+#endif
 // 1: borrow z-neighbour lanes' lookups (resolve_points); 0: every lane alone
 // (with the occupancy directory a lookup costs less than the sharing's
 // shuffles: C4 iso 141 ms shared vs 125 ms alone, both at AMRX_MINB 4)
@@ -545,6 +550,91 @@ __device__ __forceinline__ void record_point(Smem &sm, int warp, int lane, const
   sm.lev[warp][p][lane] = uint8_t(lev);
 }
 
+// ---------------------------------------------------------------------------
+// Mask-based rules (AMRX_COLUMNS, the default): each resolved stencil point
+// is classified into four 27-bit masks, and a candidate's fate is a mask test
+// over its corner cube (no per-corner walk).
+
+/// per-lane point classification (bit p = stencil point p), dual.cpp:60-67
+struct Marks {
+  uint32_t ok, miss, fin, low;
+  __device__ __forceinline__ uint32_t resolved() const { return ok | miss | fin | low; }
+};
+
+/// a candidate's corners {0,1}^3 as stencil bits, shifted by its corner 0
+constexpr uint32_t kCube = 0x361Bu;  // points 0,1,3,4,9,10,12,13
+__host__ __device__ constexpr int base_of(int delta)
+{
+  return (delta & 1) + 3 * ((delta >> 1) & 1) + 9 * (delta >> 2);
+}
+
+/// classify one resolved point (record_point with the mask representation)
+__device__ __forceinline__ void mark_point(Smem &sm, int warp, int lane, const Cell &c,
+                                           uint32_t self, int p, int64_t id, int lev,
+                                           Marks &m)
+{
+  const uint32_t bit = 1u << p;
+  if (id < 0)
+    m.miss |= bit;
+  else if (lev < c.level)
+    m.fin |= bit;
+  else if (lev == c.level && uint32_t(id) < self)
+    m.low |= bit;
+  else
+    m.ok |= bit;
+  sm.id[warp][p][lane] = uint32_t(id);
+  sm.lev[warp][p][lane] = uint8_t(lev);
+}
+
+/*! resolve the stencil points in `todo` into the marks: AMRX_BATCH per lane
+    at a time with their lookups in lock-step (batch_find), in snap's probe
+    order (locator.cpp:122-134): hint level + finer in one lookup, then the
+    coarser candidate levels (probe_coarser).  A loop over runtime point
+    indices: unrolling it per point was measured slower for the iso kernel
+    (the hot code outgrows the instruction cache next to marching cubes). */
+__device__ __forceinline__ void resolve_marks(const KArgs &a, Smem &sm, int warp, int lane,
+                                              const Cell &c, const Stencil &st,
+                                              uint32_t self, uint32_t todo, Marks &m)
+{
+  constexpr int K = AMRX_BATCH;
+  // present levels coarser than the hint: what a miss probes next
+  const uint32_t coarser = a.g.level_mask & ~((2u << c.level) - 1);
+  while (__any_sync(kFull, todo != 0)) {
+    uint64_t q[K];
+    bool v[K];
+    int64_t out[K];
+    int lvl[K], pk[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+      pk[k] = -1;
+      v[k] = false;
+      out[k] = -1;
+      lvl[k] = c.level;
+      q[k] = 0;
+      if (todo) {
+        const int p = __ffs(todo) - 1;
+        todo &= todo - 1;
+        pk[k] = p;
+        // at the hint level the point is its own anchor: key = cell key +
+        // packed steps, valid iff inside the stored range
+        v[k] = (st.inrange >> p) & 1u;
+        q[k] = stencil_key(st, p);
+      }
+    }
+    batch_find<K, true>(a.s, q, v, out, lvl);
+#pragma unroll
+    for (int k = 0; k < K; k++)
+      if (pk[k] >= 0) {
+        if (out[k] < 0 && coarser) {
+          const Hit h = probe_coarser(a, c, st, pk[k], coarser);
+          out[k] = h.id;
+          lvl[k] = h.level;
+        }
+        mark_point(sm, warp, lane, c, self, pk[k], out[k], lvl[k], m);
+      }
+  }
+}
+
 /*! look up the stencil points in `todo`, AMRX_BATCH at a time per lane
     with their lookups advanced in lock-step (batch_find), in snap's probe
     order (locator.cpp:122-134): hint + finer levels in one lookup, then
@@ -800,8 +890,59 @@ extract_kernel(const __grid_constant__ KArgs a)
     const Cell c = unpack(a.g, kself);
     const Stencil st = make_stencil(a.g, kself, c.level);
 
-    uint32_t resolved = 0, alive = working ? 0xffu : 0u, curd = 0, accepted = 0;
-    uint32_t reasons = 0;
+    uint32_t accepted = 0, reasons = 0;
+#if AMRX_COLUMNS
+    {
+      Marks m{0, 0, 0, 0};
+      uint32_t need = working ? kCorner0Points : 0;
+      if (working && a.unique) {
+        // the cell's own key can only find the cell itself (no duplicates)
+        m.ok |= 1u << 13;
+        sm.id[warp][13][lane] = self;
+        sm.lev[warp][13][lane] = uint8_t(c.level);
+        need &= ~(1u << 13);
+      }
+      // round 0: every candidate's corner 0 ({-w,0}^3); round 1: the
+      // survivors' other corners (one inlined copy of the column code)
+      uint32_t alive = 0;
+#pragma unroll 1
+      for (int round = 0; round < 2; round++) {
+        if (round == 1) {
+          // candidate delta lives on iff its corner 0 (point base_of(delta))
+          // is acceptable; a dead one's reason is its corner 0's (corner
+          // order, dual.cpp:49-67); corner-0 points map one-to-one to
+          // candidates
+#pragma unroll
+          for (int delta = 0; delta < 8; delta++)
+            alive |= ((m.ok >> base_of(delta)) & 1u) << delta;
+          reasons = (uint32_t(__popc(m.miss & kCorner0Points)) << 8) |
+                    (uint32_t(__popc(m.fin & kCorner0Points)) << 16) |
+                    (uint32_t(__popc(m.low & kCorner0Points)) << 24);
+          need = 0;
+          for (uint32_t mm = alive; mm; mm &= mm - 1) need |= kCube << base_of(__ffs(mm) - 1);
+          need &= ~m.resolved();
+        }
+        resolve_marks(a, sm, warp, lane, c, st, self, need, m);
+      }
+      // corners in order d = 0..7 are ascending stencil points, so the
+      // first failing corner is the lowest failing bit
+      const uint32_t res = m.resolved();
+      for (uint32_t mm = alive; mm; mm &= mm - 1) {
+        const int delta = __ffs(mm) - 1;
+        const uint32_t cube = kCube << base_of(delta);
+        if (cube & ~res) err |= 2u;  // cannot happen: every corner resolved
+        const uint32_t bad = cube & ~m.ok;
+        if (!bad) {
+          accepted |= 1u << delta;
+          reasons += 1u;
+        } else {
+          const uint32_t b = bad & (0u - bad);
+          reasons += (m.miss & b) ? (1u << 8) : (m.fin & b) ? (1u << 16) : (1u << 24);
+        }
+      }
+    }
+#else
+    uint32_t resolved = 0, alive = working ? 0xffu : 0u, curd = 0;
     uint64_t status = 0;
     // round 0: every candidate's corner 0 ({-w,0}^3, 4 columns); round 1:
     // everything the survivors still need
@@ -821,6 +962,7 @@ extract_kernel(const __grid_constant__ KArgs a)
       advance(resolved, status, alive, curd, accepted, reasons);
     }
     if (alive) err |= 2u;
+#endif
 
     // ---- pass 1 + pass 2 fused.  No waiting on other tiles: the tile's
     // block goes to this warp's private chunk of the staging arena and
