@@ -294,7 +294,7 @@ struct amrx_index {
   uint64_t n = 0;
   KeyGeom g{};
   int64_t bounds_hi[3] = {0, 0, 0};
-  DevBuf keys, scal, dir, occ, lmap, order, scratch;
+  DevBuf keys, scal, dir, rec, lmap, order, scratch;
   amrx_index_info info{};
   // last extraction kept on the device for the count-then-copy pattern
   struct Cached {
@@ -313,14 +313,16 @@ struct amrx_index {
   {
     SearchCtx s;
     s.keys = keys.as<uint64_t>();
-    s.dir = dir.as<uint32_t>();
+    // occupancy records when the keys are unique (positions = popcounts),
+    // else the plain directory (built on demand, ensure_search_dir)
+    const bool use_rec = g.occ && info.duplicate_keys == 0;
+    s.dir = use_rec ? nullptr : dir.as<uint32_t>();
+    s.rec = use_rec ? rec.as<uint2>() : nullptr;
     s.n = n;
     s.dir_shift = g.dir_shift;
     s.shift = g.shift;
     s.lmask = (uint64_t(1) << g.lbits) - 1;
     s.dbg = nullptr;
-    // popcount positions hold only without duplicate keys
-    s.occ = g.occ && info.duplicate_keys == 0 ? occ.as<uint64_t>() : nullptr;
     return s;
   }
 };
@@ -380,11 +382,11 @@ KeyGeom make_geometry(const int64_t mn[3], const int64_t mx[3],
   const int want = dir_env ? std::max(1, std::min(33, std::atoi(dir_env)))
                            : std::min(30, std::max(10, bit_width(n) + 1));
   g.dir_bits = std::min(g.total, want);
-  // occupancy directory (AMRX_OCC=0 disables): 64 key values per bucket,
-  // when that many buckets cost at most ~4 per cell (12 B each)
+  // occupancy records (AMRX_OCC=0 disables): 32 key values per bucket,
+  // when that many buckets cost at most ~4 per cell (8 B each)
   static const char *occ_env = std::getenv("AMRX_OCC");
   const int occ_bits = std::max(0, g.total - kOccShift);
-  g.occ = !(occ_env && occ_env[0] == '0') && !dir_env && occ_bits <= 31 &&
+  g.occ = !(occ_env && occ_env[0] == '0') && !dir_env && occ_bits <= 32 &&
           (uint64_t(1) << occ_bits) <= 4 * n + (uint64_t(1) << 20);
   if (g.occ) g.dir_bits = occ_bits;
   g.dir_shift = g.total - g.dir_bits;
@@ -433,7 +435,7 @@ void finish_info(amrx_index *ix, uint64_t equal_pairs, double ms)
   in.directory_bits = ix->g.dir_bits;
   in.duplicate_keys = equal_pairs;
   in.device_bytes = ix->keys.bytes + ix->scal.bytes + ix->dir.bytes +
-                    (ix->g.occ ? ix->occ.bytes : 0);
+                    ix->rec.bytes;
   in.seconds_ingest = ms / 1000.0;
 }
 
@@ -462,13 +464,17 @@ void setup_stream(amrx_index *ix, const amrx_index_opts *opts)
 void finalize_index(amrx_index *ix)
 {
   pad_keys(ix->keys.as<uint64_t>(), ix->n, ix->stream);
-  ix->dir.reserve(((uint64_t(1) << ix->g.dir_bits) + 1) * sizeof(uint32_t), ix->stream);
+  const uint64_t entries = (uint64_t(1) << ix->g.dir_bits) + 1;
   ix->order.reserve(16, ix->stream);
-  if (ix->g.occ)
-    ix->occ.reserve(((uint64_t(1) << ix->g.dir_bits) + 1) * sizeof(uint64_t), ix->stream);
-  build_directory(ix->keys.as<uint64_t>(), ix->n, ix->g, ix->dir.as<uint32_t>(),
-                  ix->g.occ ? ix->occ.as<uint64_t>() : nullptr,
-                  ix->order.as<unsigned long long>(), ix->scratch, ix->stream);
+  if (ix->g.occ) {
+    ix->rec.reserve(entries * sizeof(uint2), ix->stream);
+    build_directory(ix->keys.as<uint64_t>(), ix->n, ix->g, nullptr, ix->rec.as<uint2>(),
+                    ix->order.as<unsigned long long>(), ix->scratch, ix->stream);
+  } else {
+    ix->dir.reserve(entries * sizeof(uint32_t), ix->stream);
+    build_directory(ix->keys.as<uint64_t>(), ix->n, ix->g, ix->dir.as<uint32_t>(), nullptr,
+                    ix->order.as<unsigned long long>(), ix->scratch, ix->stream);
+  }
   if (ix->g.map_on) {
     const uint64_t bytes =
       ((uint64_t(ix->g.map_dim[0]) * uint64_t(ix->g.map_dim[1]) *
@@ -488,6 +494,17 @@ uint64_t sorted_equal_pairs(amrx_index *ix)
   AMRX_CUDA(cudaMemcpy(h, ix->order.ptr, sizeof h, cudaMemcpyDeviceToHost));
   if (h[0] != 0) fail(AMRX_ERR_INTERNAL, "index keys are not in (i,j,k,level) order");
   return h[1];
+}
+
+/*! an index with duplicate keys cannot use the occupancy records
+    (positions are not popcounts): build the plain bucket directory too */
+void ensure_search_dir(amrx_index *ix, uint64_t equal_pairs)
+{
+  if (!ix->g.occ || equal_pairs == 0) return;
+  const uint64_t entries = (uint64_t(1) << ix->g.dir_bits) + 1;
+  ix->dir.reserve(entries * sizeof(uint32_t), ix->stream);
+  build_directory(ix->keys.as<uint64_t>(), ix->n, ix->g, ix->dir.as<uint32_t>(), nullptr,
+                  ix->order.as<unsigned long long>(), ix->scratch, ix->stream);
 }
 
 void check_range(const amrx_index *ix, const amrx_range *range, uint64_t &b,
@@ -656,7 +673,11 @@ amrx_status amrx_index_create(const int32_t *cells4, const double *scalars,
     AMRX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    finish_info(ix.get(), sorted_equal_pairs(ix.get()), ms);
+    {
+      const uint64_t eq = sorted_equal_pairs(ix.get());
+      ensure_search_dir(ix.get(), eq);
+      finish_info(ix.get(), eq, ms);
+    }
     *out = ix.release();
   });
 }
@@ -671,7 +692,7 @@ amrx_status amrx_index_destroy(amrx_index *index)
       index->keys.release();
       index->scal.release();
       index->dir.release();
-      index->occ.release();
+      index->rec.release();
       index->lmap.release();
       index->order.release();
       index->scratch.release();
@@ -775,7 +796,11 @@ amrx_status amrx_index_adopt(const void *keys_dev, const double *scalars_dev,
     AMRX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    finish_info(ix.get(), sorted_equal_pairs(ix.get()), ms);
+    {
+      const uint64_t eq = sorted_equal_pairs(ix.get());
+      ensure_search_dir(ix.get(), eq);
+      finish_info(ix.get(), eq, ms);
+    }
     *out = ix.release();
   });
 }

@@ -40,9 +40,10 @@ struct KeyGeom {
   int32_t map_shift;
   int64_t map_base[3];  // block index of the lowest anchor per axis
   int64_t map_dim[3];   // blocks per axis
-  // occupancy directory: buckets are 64 consecutive key values (dir_shift
-  // = 6, or one bucket when total <= 6) and occ[b] bit v is set iff key
-  // (b << 6) + v is stored, so a lookup is two loads and a popcount
+  // occupancy records: buckets are 32 consecutive key values (dir_shift
+  // = 5, or one bucket when total <= 5); record b = {first position of the
+  // bucket, bit v set iff key (b << 5) + v is stored}, so a lookup is one
+  // 8-byte load and a popcount
   int32_t occ;
   // packed-space coarsening: when every min anchor is aligned to the
   // coarsest level present (aligned = 1), anchor_mask(p, L) of an in-range
@@ -52,7 +53,7 @@ struct KeyGeom {
   uint64_t cmask[32];
 };
 
-constexpr int kOccShift = 6;  // key values per occupancy word = 2^6
+constexpr int kOccShift = 5;  // key values per occupancy record = 2^5
 
 /// candidate-level bits (index into g.levels) for point p from the map
 __device__ __forceinline__ uint32_t block_levels(const KeyGeom &g,
@@ -256,35 +257,40 @@ struct SearchCtx {
   int32_t shift;         // finest level present (level field offset)
   uint64_t lmask;        // mask of the level field
   unsigned long long *dbg;  // optional event counters (AMRX_DEBUG_COUNTERS)
-  // occupancy words parallel to dir (KeyGeom::occ), or null: set only for
-  // an index without duplicate keys, where position = dir[b] + popcount
-  const uint64_t *occ;
+  // occupancy records (KeyGeom::occ), or null: set only for an index
+  // without duplicate keys, where position = rec[b].x + popcount; then the
+  // plain directory `dir` is not built (null)
+  const uint2 *rec;
 };
 
-/*! lookup through the occupancy directory (SearchCtx::occ): the exact key,
-    or under FINER the first stored key with q's anchor and a lower level
+/*! lookup through an occupancy record r = rec[q >> 5]: the exact key, or
+    under FINER the first stored key with q's anchor and a lower level
     field -- the finest cell at that anchor, which sorts first -- exactly
     what the bucket search returns for unique keys (the level field is the
-    key's low part and 64 is a multiple of 2^lbits, so an anchor's keys
-    share one word).  `word` and `start` are occ[b] and dir[b]. */
+    key's low part and 32 is a multiple of 2^lbits, lbits <= 5, so an
+    anchor's keys share one record). */
 template <bool FINER>
-__device__ __forceinline__ int64_t occ_resolve(uint64_t q, uint64_t word, uint32_t start,
-                                               uint64_t lmask, int &rl)
+__device__ __forceinline__ int64_t occ_resolve(uint64_t q, uint2 r, uint32_t lmask, int &rl)
 {
-  const int bit = int(q & 63);
-  const uint64_t below = word & ((uint64_t(1) << bit) - 1);
-  rl = int(q & lmask);
-  if ((word >> bit) & 1u) return int64_t(start) + __popcll(below);
+  const uint32_t bit = uint32_t(q) & 31u;
+  const uint32_t below = r.y & ((1u << bit) - 1u);
+  rl = int(uint32_t(q) & lmask);
+  if ((r.y >> bit) & 1u) return int64_t(r.x + uint32_t(__popc(below)));
   if (FINER) {
-    const int grp = bit & ~int(lmask);  // first value of q's anchor
-    const uint64_t m = below & ~((uint64_t(1) << grp) - 1);
+    const uint32_t grp = bit & ~lmask;  // first value of q's anchor
+    const uint32_t m = below & ~((1u << grp) - 1u);
     if (m) {
-      const int f = __ffsll((long long)m) - 1;
-      rl = f & int(lmask);
-      return int64_t(start) + __popcll(word & ((uint64_t(1) << f) - 1));
+      const uint32_t f = uint32_t(__ffs(int(m))) - 1u;
+      rl = int(f & lmask);
+      return int64_t(r.x + uint32_t(__popc(r.y & ((1u << f) - 1u))));
     }
   }
   return -1;
+}
+
+__device__ __forceinline__ uint2 ldg_rec(const uint2 *rec, uint64_t q, int dir_shift)
+{
+  return __ldg(rec + (q >> dir_shift));
 }
 
 /// debug event counters, one atomic per warp-level event, lane 0 only
@@ -339,29 +345,20 @@ static __device__ __noinline__ int64_t find_in_bucket(const SearchCtx &s, uint64
   return res;
 }
 
-/// batch_find through the occupancy directory only (s.occ must be set)
+/// batch_find through the occupancy records only (s.rec must be set)
 template <int K, bool FINER>
 __device__ __forceinline__ void occ_find(const SearchCtx &s, const uint64_t (&q)[K],
                                          const bool (&valid)[K], int64_t (&out)[K],
                                          int (&lvl)[K])
 {
-  uint64_t word[K];
-  uint32_t start[K];
+  uint2 r[K];
 #pragma unroll
-  for (int k = 0; k < K; k++) {
-    word[k] = 0;
-    start[k] = 0;
-    if (valid[k]) {
-      const uint64_t b = q[k] >> s.dir_shift;
-      word[k] = ldg_u64(s.occ + b);
-      start[k] = __ldg(s.dir + b);
-    }
-  }
+  for (int k = 0; k < K; k++) r[k] = valid[k] ? ldg_rec(s.rec, q[k], s.dir_shift) : make_uint2(0, 0);
 #pragma unroll
   for (int k = 0; k < K; k++)
     if (valid[k]) {
       int rl;
-      out[k] = occ_resolve<FINER>(q[k], word[k], start[k], s.lmask, rl);
+      out[k] = occ_resolve<FINER>(q[k], r[k], uint32_t(s.lmask), rl);
       lvl[k] = rl + s.shift;
     }
 }
@@ -382,10 +379,9 @@ __device__ __forceinline__ void lane_find(const SearchCtx &s, const uint64_t (&q
 #pragma unroll
   for (int t = 0; t < NQ; t++) {
     if (!valid[t]) continue;
-    if (s.occ) {
-      const uint64_t b = q[t] >> s.dir_shift;
+    if (s.rec) {
       int rl;
-      out[t] = occ_resolve<FINER>(q[t], ldg_u64(s.occ + b), __ldg(s.dir + b), s.lmask, rl);
+      out[t] = occ_resolve<FINER>(q[t], ldg_rec(s.rec, q[t], s.dir_shift), uint32_t(s.lmask), rl);
       lvl[t] = rl + s.shift;
       continue;
     }
@@ -440,7 +436,7 @@ __device__ __forceinline__ void batch_find(const SearchCtx &s, const uint64_t (&
                                            const bool (&valid)[K], int64_t (&out)[K],
                                            int (&lvl)[K])
 {
-  if (s.occ) {  // occupancy directory: no search at all
+  if (s.rec) {  // occupancy records: no search at all
     occ_find<K, FINER>(s, q, valid, out, lvl);
     return;
   }
@@ -559,6 +555,10 @@ __device__ void warp_find(const SearchCtx &s, const uint64_t (&q)[NQ],
                           const bool (&valid)[NQ], int64_t (&out)[NQ],
                           int (&lvl)[NQ], uint64_t *win)
 {
+  if (s.rec) {  // occupancy records: per lane, no search (warp-uniform branch)
+    occ_find<NQ, FINER>(s, q, valid, out, lvl);
+    return;
+  }
   const uint32_t lane = lane_id();
   const uint64_t amask = FINER ? ~s.lmask : ~0ull;
   bool any = false;

@@ -586,6 +586,46 @@ __device__ __forceinline__ void mark_point(Smem &sm, int warp, int lane, const C
   sm.lev[warp][p][lane] = uint8_t(lev);
 }
 
+constexpr uint32_t kFast0 = kCorner0Points & ~(1u << 13);  // 0 1 3 4 9 10 12
+constexpr uint32_t kFast1 = kCube << 13 & ~(1u << 13);       // 14 16 17 22 23 25 26
+
+/*! stencil point P (compile-time) if this lane needs it: the common case --
+    its own anchor exists on the hint level -- resolved inline (one
+    occupancy word + one directory entry, the key from compile-time steps);
+    anything else (finer, coarser, absent) is left in `pend` */
+template <int P>
+__device__ __forceinline__ void fast_point(const KArgs &a, Smem &sm, int warp, int lane,
+                                           const Cell &c, const Stencil &st, uint32_t need,
+                                           Marks &m, uint32_t &pend)
+{
+  if (!((need >> P) & 1u)) return;
+  constexpr int ox = P % 3 - 1, oy = (P / 3) % 3 - 1, oz = P / 9 - 1;
+  uint64_t q = st.k0;
+  if (ox > 0) q += st.sx;
+  if (ox < 0) q -= st.sx;
+  if (oy > 0) q += st.sy;
+  if (oy < 0) q -= st.sy;
+  if (oz > 0) q += st.sz;
+  if (oz < 0) q -= st.sz;
+  if ((st.inrange >> P) & 1u) {
+    const uint2 r = ldg_rec(a.s.rec, q, a.s.dir_shift);
+    const uint32_t bit = uint32_t(q) & 31u;
+    if ((r.y >> bit) & 1u) {
+      // same level: lower CellId (dual.cpp:64-66) <=> lower key <=> the
+      // point precedes the cell in (i,j,k) order, known at compile time
+      constexpr bool lower = ox < 0 || (ox == 0 && (oy < 0 || (oy == 0 && oz < 0)));
+      if (lower)
+        m.low |= 1u << P;
+      else
+        m.ok |= 1u << P;
+      sm.id[warp][P][lane] = r.x + uint32_t(__popc(r.y & ((1u << bit) - 1u)));
+      sm.lev[warp][P][lane] = uint8_t(c.level);
+      return;
+    }
+  }
+  pend |= 1u << P;
+}
+
 /*! resolve the stencil points in `todo` into the marks: AMRX_BATCH per lane
     at a time with their lookups in lock-step (batch_find), in snap's probe
     order (locator.cpp:122-134): hint level + finer in one lookup, then the
@@ -921,6 +961,33 @@ extract_kernel(const __grid_constant__ KArgs a)
           need = 0;
           for (uint32_t mm = alive; mm; mm &= mm - 1) need |= kCube << base_of(__ffs(mm) - 1);
           need &= ~m.resolved();
+        }
+        if (a.s.rec) {
+          // the points every cell of a uniform region needs -- all
+          // candidates' corner 0 in round 0, candidate 7's cube in round 1 --
+          // with compile-time offsets; the rest and every miss go through
+          // the runtime loop
+          uint32_t pend = 0;
+          if (round == 0) {
+            fast_point<0>(a, sm, warp, lane, c, st, need, m, pend);
+            fast_point<1>(a, sm, warp, lane, c, st, need, m, pend);
+            fast_point<3>(a, sm, warp, lane, c, st, need, m, pend);
+            fast_point<4>(a, sm, warp, lane, c, st, need, m, pend);
+            fast_point<9>(a, sm, warp, lane, c, st, need, m, pend);
+            fast_point<10>(a, sm, warp, lane, c, st, need, m, pend);
+            fast_point<12>(a, sm, warp, lane, c, st, need, m, pend);
+            need &= ~kFast0;
+          } else if (__any_sync(kFull, (need & kFast1) != 0)) {
+            fast_point<14>(a, sm, warp, lane, c, st, need, m, pend);
+            fast_point<16>(a, sm, warp, lane, c, st, need, m, pend);
+            fast_point<17>(a, sm, warp, lane, c, st, need, m, pend);
+            fast_point<22>(a, sm, warp, lane, c, st, need, m, pend);
+            fast_point<23>(a, sm, warp, lane, c, st, need, m, pend);
+            fast_point<25>(a, sm, warp, lane, c, st, need, m, pend);
+            fast_point<26>(a, sm, warp, lane, c, st, need, m, pend);
+            need &= ~kFast1;
+          }
+          need |= pend;
         }
         resolve_marks(a, sm, warp, lane, c, st, self, need, m);
       }

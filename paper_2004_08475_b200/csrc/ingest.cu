@@ -156,7 +156,7 @@ __global__ void pad_kernel(uint64_t *keys, uint64_t n)
 __global__ void __launch_bounds__(kThreads)
 bucket_count_kernel(const uint64_t *__restrict__ keys, uint64_t n, int shift,
                     uint32_t *__restrict__ cnt, unsigned long long *order2,
-                    unsigned long long *__restrict__ occ)
+                    uint2 *__restrict__ rec)
 {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   const uint64_t start = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -176,18 +176,19 @@ bucket_count_kernel(const uint64_t *__restrict__ keys, uint64_t n, int shift,
     const uint64_t b = in ? (k >> shift) : ~0ull;
     const uint32_t peers = __match_any_sync(kFull, b);
     const bool leader = in && (__ffs(peers) - 1) == int(threadIdx.x & 31);
-    if (leader) atomicAdd(cnt + b, __popc(peers));
-    if (occ) {
-      // occupancy word of the bucket: OR of its keys' low-6-bit values over
-      // the run of lanes holding it (sorted keys: runs are contiguous)
-      unsigned long long bits = in ? 1ull << (k & 63) : 0ull;
+    if (rec) {
+      // occupancy record of the bucket: OR of its keys' low-5-bit values
+      // over the run of lanes holding it (sorted keys: runs are contiguous)
+      uint32_t bits = in ? 1u << (uint32_t(k) & 31u) : 0u;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
-        const unsigned long long y = __shfl_down_sync(kFull, bits, off);
+        const uint32_t y = __shfl_down_sync(kFull, bits, off);
         const uint64_t bo = __shfl_down_sync(kFull, (unsigned long long)b, off);
         if (int(threadIdx.x & 31) + off < 32 && bo == b) bits |= y;
       }
-      if (leader) atomicOr(occ + b, bits);
+      if (leader) atomicOr(&rec[b].y, bits);
+    } else if (leader) {
+      atomicAdd(cnt + b, __popc(peers));
     }
   }
 #pragma unroll
@@ -358,6 +359,45 @@ scan_downsweep_kernel(const T *in, A *out, uint64_t n,
   }
 }
 
+/// per tile: the number of keys its occupancy records hold
+__global__ void __launch_bounds__(kScanThreads)
+rec_reduce_kernel(const uint2 *__restrict__ rec, uint64_t n, uint32_t *__restrict__ sums)
+{
+  __shared__ uint32_t sm[32];
+  const uint64_t base = uint64_t(blockIdx.x) * kScanTile;
+  uint32_t s = 0;
+#pragma unroll
+  for (int t = 0; t < kScanItems; t++) {
+    const uint64_t r = base + uint64_t(t) * kScanThreads + threadIdx.x;
+    if (r < n) s += __popc(rec[r].y);
+  }
+  uint32_t total;
+  block_exclusive_sum<uint32_t>(s, sm, &total);
+  if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+/// rec[b].x = keys in records before b (exclusive scan of the popcounts)
+__global__ void __launch_bounds__(kScanThreads)
+rec_downsweep_kernel(uint2 *rec, uint64_t n, const uint32_t *__restrict__ block_offsets)
+{
+  __shared__ uint32_t sm[32];
+  const uint64_t base = uint64_t(blockIdx.x) * kScanTile + uint64_t(threadIdx.x) * kScanItems;
+  uint2 v[kScanItems];
+  uint32_t s = 0;
+#pragma unroll
+  for (int t = 0; t < kScanItems; t++) {
+    v[t] = base + t < n ? rec[base + t] : make_uint2(0, 0);
+    s += __popc(v[t].y);
+  }
+  uint32_t run = block_exclusive_sum<uint32_t>(s, sm, nullptr) +
+                 (block_offsets ? block_offsets[blockIdx.x] : 0u);
+#pragma unroll
+  for (int t = 0; t < kScanItems; t++) {
+    if (base + t < n) rec[base + t] = make_uint2(run, v[t].y);
+    run += __popc(v[t].y);
+  }
+}
+
 /// recursive reduce-then-scan; block sums of each level in a pool buffer
 template <typename T, typename A>
 int scan_exclusive(const T *in, A *out, uint64_t n, cudaStream_t st)
@@ -452,15 +492,30 @@ void pad_keys(uint64_t *keys, uint64_t n, cudaStream_t st)
 }
 
 void build_directory(const uint64_t *keys, uint64_t n, const KeyGeom &g,
-                     uint32_t *dir, uint64_t *occ, unsigned long long *order2,
+                     uint32_t *dir, uint2 *rec, unsigned long long *order2,
                      DevBuf &scratch, cudaStream_t st)
 {
   const uint64_t entries = (uint64_t(1) << g.dir_bits) + 1;
-  AMRX_CUDA(cudaMemsetAsync(dir, 0, entries * sizeof(uint32_t), st));
-  if (occ) AMRX_CUDA(cudaMemsetAsync(occ, 0, entries * sizeof(uint64_t), st));
   AMRX_CUDA(cudaMemsetAsync(order2, 0, 16, st));
+  if (rec) {
+    AMRX_CUDA(cudaMemsetAsync(rec, 0, entries * sizeof(uint2), st));
+    bucket_count_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(
+      keys, n, g.dir_shift, nullptr, order2, rec);
+    AMRX_LAUNCH_CHECK();
+    const uint64_t blocks = (entries + kScanTile - 1) / kScanTile;
+    DevBuf sums;
+    sums.reserve(size_t(blocks) * sizeof(uint32_t), st);
+    rec_reduce_kernel<<<unsigned(blocks), kScanThreads, 0, st>>>(rec, entries, sums.as<uint32_t>());
+    AMRX_LAUNCH_CHECK();
+    scan_exclusive<uint32_t, uint32_t>(sums.as<uint32_t>(), sums.as<uint32_t>(), blocks, st);
+    rec_downsweep_kernel<<<unsigned(blocks), kScanThreads, 0, st>>>(rec, entries,
+                                                                   sums.as<uint32_t>());
+    AMRX_LAUNCH_CHECK();
+    return;
+  }
+  AMRX_CUDA(cudaMemsetAsync(dir, 0, entries * sizeof(uint32_t), st));
   bucket_count_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(
-    keys, n, g.dir_shift, dir, order2, reinterpret_cast<unsigned long long *>(occ));
+    keys, n, g.dir_shift, dir, order2, nullptr);
   AMRX_LAUNCH_CHECK();
   scan_exclusive_u32(dir, dir, entries, scratch, st);
 }

@@ -125,10 +125,11 @@ void gather_f64(const uint32_t *perm, const double *in, double *out,
 void pad_keys(uint64_t *keys, uint64_t n, cudaStream_t st);
 
 /// dir[b] = first position whose key >> g.dir_shift >= b, b in [0, 2^D];
-/// occ (2^D + 1 words, or null; g.occ geometry) = occupancy words;
-/// order2 (device, 2 x u64) receives the keys' descents and equal pairs
+/// or, with rec (2^D + 1 records; g.occ geometry) instead, the occupancy
+/// records (dir unused); order2 (device, 2 x u64) receives the keys'
+/// descents and equal pairs
 void build_directory(const uint64_t *keys, uint64_t n, const KeyGeom &g,
-                     uint32_t *dir, uint64_t *occ, unsigned long long *order2,
+                     uint32_t *dir, uint2 *rec, unsigned long long *order2,
                      DevBuf &scratch, cudaStream_t st);
 
 /// block level map (KeyGeom::map_*): fill map (map bytes, zeroed here)
