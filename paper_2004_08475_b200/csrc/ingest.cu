@@ -155,8 +155,7 @@ __global__ void pad_kernel(uint64_t *keys, uint64_t n)
     warp issues one atomic per distinct bucket it holds */
 __global__ void __launch_bounds__(kThreads)
 bucket_count_kernel(const uint64_t *__restrict__ keys, uint64_t n, int shift,
-                    uint32_t *__restrict__ cnt, unsigned long long *order2,
-                    uint2 *__restrict__ rec)
+                    uint32_t *__restrict__ cnt, unsigned long long *order2)
 {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   const uint64_t start = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -176,20 +175,7 @@ bucket_count_kernel(const uint64_t *__restrict__ keys, uint64_t n, int shift,
     const uint64_t b = in ? (k >> shift) : ~0ull;
     const uint32_t peers = __match_any_sync(kFull, b);
     const bool leader = in && (__ffs(peers) - 1) == int(threadIdx.x & 31);
-    if (rec) {
-      // occupancy record of the bucket: OR of its keys' low-5-bit values
-      // over the run of lanes holding it (sorted keys: runs are contiguous)
-      uint32_t bits = in ? 1u << (uint32_t(k) & 31u) : 0u;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t y = __shfl_down_sync(kFull, bits, off);
-        const uint64_t bo = __shfl_down_sync(kFull, (unsigned long long)b, off);
-        if (int(threadIdx.x & 31) + off < 32 && bo == b) bits |= y;
-      }
-      if (leader) atomicOr(&rec[b].y, bits);
-    } else if (leader) {
-      atomicAdd(cnt + b, __popc(peers));
-    }
+    if (leader) atomicAdd(cnt + b, __popc(peers));
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -359,42 +345,114 @@ scan_downsweep_kernel(const T *in, A *out, uint64_t n,
   }
 }
 
-/// per tile: the number of keys its occupancy records hold
-__global__ void __launch_bounds__(kScanThreads)
-rec_reduce_kernel(const uint2 *__restrict__ rec, uint64_t n, uint32_t *__restrict__ sums)
+// ------------------------------------------- occupancy records, one pass
+// A block owns 4096 consecutive buckets; their keys are one contiguous run
+// of the sorted array, starting at tile_start[t].  The block ORs the keys'
+// bits and counts them per bucket in shared memory, scans the counts and
+// writes its records once: no memset, no device-wide scan, each key read
+// once.  The counts (not popcounts) make rec[b].x the exact lower bound of
+// bucket b even with duplicate keys, so the records double as the search
+// directory (bounds rec[b].x, rec[b+1].x).
+constexpr int kRecTileLog = 12;
+constexpr int kRecTile = 1 << kRecTileLog;
+constexpr int kRecThreads = 512;
+
+/// tile_start[t] = first position whose bucket >= t * kRecTile, t in [0, tiles]
+__global__ void __launch_bounds__(kThreads)
+rec_tile_start_kernel(const uint64_t *__restrict__ keys, uint64_t n, int shift,
+                      uint64_t tiles, uint32_t *__restrict__ tile_start)
 {
-  __shared__ uint32_t sm[32];
-  const uint64_t base = uint64_t(blockIdx.x) * kScanTile;
-  uint32_t s = 0;
-#pragma unroll
-  for (int t = 0; t < kScanItems; t++) {
-    const uint64_t r = base + uint64_t(t) * kScanThreads + threadIdx.x;
-    if (r < n) s += __popc(rec[r].y);
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i <= n; i += stride) {
+    const uint64_t cur = i < n ? std::min<uint64_t>(ldg_u64(keys + i) >> shift, tiles) : tiles;
+    const uint64_t from = i > 0 ? (ldg_u64(keys + i - 1) >> shift) + 1 : 0;
+    for (uint64_t t = from; t <= cur; t++) tile_start[t] = uint32_t(i);
   }
-  uint32_t total;
-  block_exclusive_sum<uint32_t>(s, sm, &total);
-  if (threadIdx.x == 0) sums[blockIdx.x] = total;
 }
 
-/// rec[b].x = keys in records before b (exclusive scan of the popcounts)
-__global__ void __launch_bounds__(kScanThreads)
-rec_downsweep_kernel(uint2 *rec, uint64_t n, const uint32_t *__restrict__ block_offsets)
+__global__ void __launch_bounds__(kRecThreads)
+rec_build_kernel(const uint64_t *__restrict__ keys, uint64_t n, int dir_shift,
+                 uint64_t entries, const uint32_t *__restrict__ tile_start,
+                 uint2 *__restrict__ rec, unsigned long long *order2)
 {
-  __shared__ uint32_t sm[32];
-  const uint64_t base = uint64_t(blockIdx.x) * kScanTile + uint64_t(threadIdx.x) * kScanItems;
-  uint2 v[kScanItems];
-  uint32_t s = 0;
-#pragma unroll
-  for (int t = 0; t < kScanItems; t++) {
-    v[t] = base + t < n ? rec[base + t] : make_uint2(0, 0);
-    s += __popc(v[t].y);
+  __shared__ uint32_t bits[kRecTile];
+  __shared__ uint32_t cnt[kRecTile];
+  __shared__ uint32_t wsum[32];
+  const uint64_t t = blockIdx.x;
+  for (int j = threadIdx.x; j < kRecTile; j += kRecThreads) {
+    bits[j] = 0;
+    cnt[j] = 0;
   }
-  uint32_t run = block_exclusive_sum<uint32_t>(s, sm, nullptr) +
-                 (block_offsets ? block_offsets[blockIdx.x] : 0u);
+  __syncthreads();
+  const uint64_t lo = tile_start[t], hi = tile_start[t + 1];
+  const int lane = threadIdx.x & 31;
+  unsigned long long desc = 0, eq = 0;
+  // whole warps step together so the match below sees all lanes
+  for (uint64_t base = lo + (threadIdx.x & ~31u); base < hi; base += kRecThreads) {
+    const uint64_t i = base + lane;
+    const bool in = i < hi;
+    const uint64_t k = in ? ldg_u64(keys + i) : 0;
+    if (in && i + 1 < n) {
+      const uint64_t k1 = ldg_u64(keys + i + 1);
+      desc += k > k1;
+      eq += k == k1;
+    }
+    const uint32_t b = in ? uint32_t(k >> dir_shift) & (kRecTile - 1) : 0xffffffffu;
+    const uint32_t peers = __match_any_sync(kFull, b);
+    uint32_t v = in ? 1u << (uint32_t(k) & 31u) : 0u;
 #pragma unroll
-  for (int t = 0; t < kScanItems; t++) {
-    if (base + t < n) rec[base + t] = make_uint2(run, v[t].y);
-    run += __popc(v[t].y);
+    for (int off = 1; off < 32; off <<= 1) {  // segmented OR over the run
+      const uint32_t y = __shfl_down_sync(kFull, v, off);
+      const uint32_t bo = __shfl_down_sync(kFull, b, off);
+      if (lane + off < 32 && bo == b) v |= y;
+    }
+    if (in && (__ffs(peers) - 1) == lane) {
+      atomicOr(&bits[b], v);
+      atomicAdd(&cnt[b], uint32_t(__popc(peers)));
+    }
+  }
+  __syncthreads();
+  // exclusive scan of the 4096 counts: 8 per thread
+  constexpr int per = kRecTile / kRecThreads;
+  uint32_t c[per], sum = 0;
+#pragma unroll
+  for (int j = 0; j < per; j++) {
+    c[j] = cnt[threadIdx.x * per + j];
+    sum += c[j];
+  }
+  uint32_t x = sum;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, off);
+    if (lane >= off) x += y;
+  }
+  if (lane == 31) wsum[threadIdx.x >> 5] = x;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t w = threadIdx.x < kRecThreads / 32 ? wsum[threadIdx.x] : 0u;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, w, off);
+      if (lane >= off) w += y;
+    }
+    wsum[threadIdx.x] = w;
+  }
+  __syncthreads();
+  uint32_t run = uint32_t(lo) + (x - sum) + ((threadIdx.x >> 5) ? wsum[(threadIdx.x >> 5) - 1] : 0u);
+  const uint64_t r0 = (t << kRecTileLog) + uint64_t(threadIdx.x) * per;
+#pragma unroll
+  for (int j = 0; j < per; j++) {
+    if (r0 + j < entries) rec[r0 + j] = make_uint2(run, bits[threadIdx.x * per + j]);
+    run += c[j];
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    desc += __shfl_xor_sync(kFull, desc, off);
+    eq += __shfl_xor_sync(kFull, eq, off);
+  }
+  if (lane == 0) {
+    if (desc) atomicAdd(order2, desc);
+    if (eq) atomicAdd(order2 + 1, eq);
   }
 }
 
@@ -498,24 +556,20 @@ void build_directory(const uint64_t *keys, uint64_t n, const KeyGeom &g,
   const uint64_t entries = (uint64_t(1) << g.dir_bits) + 1;
   AMRX_CUDA(cudaMemsetAsync(order2, 0, 16, st));
   if (rec) {
-    AMRX_CUDA(cudaMemsetAsync(rec, 0, entries * sizeof(uint2), st));
-    bucket_count_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(
-      keys, n, g.dir_shift, nullptr, order2, rec);
+    const uint64_t tiles = (entries + kRecTile - 1) / kRecTile;
+    DevBuf starts;
+    starts.reserve(size_t(tiles + 1) * sizeof(uint32_t), st);
+    rec_tile_start_kernel<<<grid_for(n + 1, kThreads, 4), kThreads, 0, st>>>(
+      keys, n, g.dir_shift + kRecTileLog, tiles, starts.as<uint32_t>());
     AMRX_LAUNCH_CHECK();
-    const uint64_t blocks = (entries + kScanTile - 1) / kScanTile;
-    DevBuf sums;
-    sums.reserve(size_t(blocks) * sizeof(uint32_t), st);
-    rec_reduce_kernel<<<unsigned(blocks), kScanThreads, 0, st>>>(rec, entries, sums.as<uint32_t>());
-    AMRX_LAUNCH_CHECK();
-    scan_exclusive<uint32_t, uint32_t>(sums.as<uint32_t>(), sums.as<uint32_t>(), blocks, st);
-    rec_downsweep_kernel<<<unsigned(blocks), kScanThreads, 0, st>>>(rec, entries,
-                                                                   sums.as<uint32_t>());
+    rec_build_kernel<<<unsigned(tiles), kRecThreads, 0, st>>>(
+      keys, n, g.dir_shift, entries, starts.as<uint32_t>(), rec, order2);
     AMRX_LAUNCH_CHECK();
     return;
   }
   AMRX_CUDA(cudaMemsetAsync(dir, 0, entries * sizeof(uint32_t), st));
   bucket_count_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(
-    keys, n, g.dir_shift, dir, order2, nullptr);
+    keys, n, g.dir_shift, dir, order2);
   AMRX_LAUNCH_CHECK();
   scan_exclusive_u32(dir, dir, entries, scratch, st);
 }
