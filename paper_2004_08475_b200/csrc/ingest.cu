@@ -439,12 +439,15 @@ rec_build_kernel(const uint64_t *__restrict__ keys, uint64_t n, int dir_shift,
   }
   __syncthreads();
   uint32_t run = uint32_t(lo) + (x - sum) + ((threadIdx.x >> 5) ? wsum[(threadIdx.x >> 5) - 1] : 0u);
-  const uint64_t r0 = (t << kRecTileLog) + uint64_t(threadIdx.x) * per;
 #pragma unroll
-  for (int j = 0; j < per; j++) {
-    if (r0 + j < entries) rec[r0 + j] = make_uint2(run, bits[threadIdx.x * per + j]);
+  for (int j = 0; j < per; j++) {  // counts -> bucket starts, in place
+    cnt[threadIdx.x * per + j] = run;
     run += c[j];
   }
+  __syncthreads();
+  const uint64_t r0 = t << kRecTileLog;
+  for (int j = threadIdx.x; j < kRecTile; j += kRecThreads)  // coalesced
+    if (r0 + j < entries) rec[r0 + j] = make_uint2(cnt[j], bits[j]);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     desc += __shfl_xor_sync(kFull, desc, off);
