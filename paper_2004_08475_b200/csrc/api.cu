@@ -590,7 +590,7 @@ amrx_status amrx_index_create(const int32_t *cells4, const double *scalars,
     // into workspace slots.  The scalar upload runs on a side stream so it
     // overlaps the pack + radix sort (the scalars are first needed by the
     // gather that follows the sort).
-    WsLease l_cells, l_scal, l_idx, l_kalt, l_ialt, l_sort;
+    WsLease l_cells, l_scal, l_idx, l_ialt, l_sort;
     const int4 *cells_d = reinterpret_cast<const int4 *>(device_view(cells4));
     if (!cells_d) {
       cells_d = static_cast<const int4 *>(l_cells.get(kWsCells, n * 16, st));
@@ -657,14 +657,23 @@ amrx_status amrx_index_create(const int32_t *cells4, const double *scalars,
     } else {
       if (opts && (opts->flags & AMRX_FLAG_PRESORTED))
         fail(AMRX_ERR_INVALID_ARG, "input flagged presorted is not sorted");
-      auto *keys_alt = static_cast<uint64_t *>(l_kalt.get(kWsKeysAlt, n * 8, st));
+      // the sort ping-pongs with a pool buffer the size of the key array;
+      // if the keys end there the two buffers trade places (no copy).  The
+      // last pass writes the scalars in key order (the gather, fused)
+      DevBuf keys_alt;
+      keys_alt.reserve((n + kKeyPad) * sizeof(uint64_t), st);
       auto *idx_alt = static_cast<uint32_t *>(l_ialt.get(kWsIdxAlt, n * 4, st));
       void *sort_scratch = l_sort.get(kWsSort, radix_sort_scratch_bytes(n), st);
       int passes = 0;
-      radix_sort_pairs(ix->keys.as<uint64_t>(), idx, keys_alt, idx_alt, n,
-                       ix->g.total, sort_scratch, st, &passes);
-      if (sc_ready) AMRX_CUDA(cudaStreamWaitEvent(st, sc_ready, 0));
-      gather_f64(idx, sc_d, ix->scal.as<double>(), n, st);
+      const bool in_alt =
+        radix_sort_pairs(ix->keys.as<uint64_t>(), idx, keys_alt.as<uint64_t>(), idx_alt, n,
+                         ix->g.total, sort_scratch, st, &passes, sc_d,
+                         ix->scal.as<double>(), sc_ready);
+      if (in_alt) {
+        std::swap(ix->keys.ptr, keys_alt.ptr);
+        std::swap(ix->keys.bytes, keys_alt.bytes);
+        std::swap(ix->keys.stream, keys_alt.stream);
+      }
     }
     finalize_index(ix.get());
     AMRX_CUDA(cudaEventRecord(e1, st));

@@ -149,11 +149,16 @@ int scan_exclusive_u32_u64(const uint32_t *in, uint64_t *out, uint64_t n,
                            DevBuf &scratch, cudaStream_t st);
 
 // -------------------------------------------------------------- sort.cu
-/// stable LSD radix sort of (keys, vals) over bits [0, key_bits); the
-/// result ends in keys/vals (alt buffers are scratch of the same size)
-void radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
+/// stable LSD radix sort of (keys, vals) over bits [0, key_bits), ping-
+/// ponging with the alt buffers; returns true when the sorted keys (and,
+/// without gsrc, values) ended in the alt buffers.  With gsrc, the last
+/// pass writes gdst[i] = gsrc[value of sorted item i] instead of the
+/// values (after gsrc_ready, if set)
+bool radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
                       uint32_t *vals_alt, uint64_t n, int key_bits,
-                      void *scratch, cudaStream_t st, int *passes_run);
+                      void *scratch, cudaStream_t st, int *passes_run,
+                      const double *gsrc = nullptr, double *gdst = nullptr,
+                      cudaEvent_t gsrc_ready = nullptr);
 
 /// bytes of scratch radix_sort_pairs needs for n keys
 size_t radix_sort_scratch_bytes(uint64_t n);

@@ -98,13 +98,20 @@ struct PassSmem {
   uint32_t tile;
 };
 
+/*! one LSD pass.  GATHER (the last pass): instead of the u32 values, write
+    gsrc[value] -- the payload the values index (the scalars in input
+    order) -- so the separate gather kernel and the value round trip
+    disappear; the random payload loads are issued together per thread in
+    the final scatter, after the look-back. */
+template <bool GATHER>
 __global__ void __launch_bounds__(kSortThreads)
 onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
                      const uint32_t *__restrict__ vals_in,
                      uint64_t *__restrict__ keys_out,
                      uint32_t *__restrict__ vals_out, uint64_t n, int shift,
                      const unsigned long long *__restrict__ digit_start,
-                     unsigned long long *state, unsigned int *ticket)
+                     unsigned long long *state, unsigned int *ticket,
+                     const double *__restrict__ gsrc, double *__restrict__ gdst)
 {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PassSmem &sm = *reinterpret_cast<PassSmem *>(smem_raw);
@@ -210,6 +217,29 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
     }
   __syncthreads();
   const uint64_t valid = n - base < uint64_t(kSortTile) ? n - base : kSortTile;
+  if (GATHER) {
+    constexpr int U = 4;  // payload loads in flight per thread
+    for (int p0 = threadIdx.x; p0 < int(valid); p0 += U * kSortThreads) {
+      double g[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int pos = p0 + u * kSortThreads;
+        g[u] = pos < int(valid) ? __ldg(gsrc + sm.vals[pos]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int pos = p0 + u * kSortThreads;
+        if (pos < int(valid)) {
+          const uint64_t kk = sm.keys[pos];
+          const uint32_t d = uint32_t((kk >> shift) & (kDigits - 1));
+          const uint64_t dst = sm.gofs[d] + (pos - sm.bexcl[d]);
+          keys_out[dst] = kk;
+          gdst[dst] = g[u];
+        }
+      }
+    }
+    return;
+  }
   for (int pos = threadIdx.x; pos < int(valid); pos += kSortThreads) {
     const uint64_t kk = sm.keys[pos];
     const uint32_t d = uint32_t((kk >> shift) & (kDigits - 1));
@@ -227,12 +257,13 @@ size_t radix_sort_scratch_bytes(uint64_t n)
   return size_t(kMaxPasses) * kDigits * 12 + 256 + size_t(tiles) * kDigits * 8;
 }
 
-void radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
+bool radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
                       uint32_t *vals_alt, uint64_t n, int key_bits,
-                      void *scratch, cudaStream_t st, int *passes_run)
+                      void *scratch, cudaStream_t st, int *passes_run,
+                      const double *gsrc, double *gdst, cudaEvent_t gsrc_ready)
 {
   if (passes_run) *passes_run = 0;
-  if (n <= 1 || key_bits <= 0) return;
+  if (n <= 1 || key_bits <= 0) return false;
   const int passes = (key_bits + kRadixBits - 1) / kRadixBits;
   const uint64_t tiles = (n + kSortTile - 1) / kSortTile;
 
@@ -265,34 +296,49 @@ void radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
   static bool attr_set = false;
   const size_t smem = sizeof(PassSmem);
   if (!attr_set) {
-    AMRX_CUDA(cudaFuncSetAttribute(onesweep_pass_kernel,
+    AMRX_CUDA(cudaFuncSetAttribute(onesweep_pass_kernel<false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(smem)));
+    AMRX_CUDA(cudaFuncSetAttribute(onesweep_pass_kernel<true>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(smem)));
     attr_set = true;
+  }
+  int last = -1;
+  bool trivial[kMaxPasses] = {};
+  for (int p = 0; p < passes; p++) {
+    for (int d = 0; d < kDigits; d++)
+      if (h[size_t(p) * kDigits + d] == n) trivial[p] = true;
+    if (!trivial[p]) last = p;
   }
   uint64_t *kin = keys, *kout = keys_alt;
   uint32_t *vin = vals, *vout = vals_alt;
   int run = 0;
   for (int p = 0; p < passes; p++) {
-    bool trivial = false;
-    for (int d = 0; d < kDigits; d++)
-      if (h[size_t(p) * kDigits + d] == n) trivial = true;
-    if (trivial) continue;
+    if (trivial[p]) continue;
     AMRX_CUDA(cudaMemsetAsync(state, 0, state_bytes, st));
     AMRX_CUDA(cudaMemsetAsync(ticket, 0, 4, st));
-    onesweep_pass_kernel<<<unsigned(tiles), kSortThreads, smem, st>>>(
-      kin, vin, kout, vout, n, p * kRadixBits, offs + size_t(p) * kDigits,
-      state, ticket);
+    if (gsrc && p == last) {
+      if (gsrc_ready) AMRX_CUDA(cudaStreamWaitEvent(st, gsrc_ready, 0));
+      onesweep_pass_kernel<true><<<unsigned(tiles), kSortThreads, smem, st>>>(
+        kin, vin, kout, vout, n, p * kRadixBits, offs + size_t(p) * kDigits,
+        state, ticket, gsrc, gdst);
+    } else {
+      onesweep_pass_kernel<false><<<unsigned(tiles), kSortThreads, smem, st>>>(
+        kin, vin, kout, vout, n, p * kRadixBits, offs + size_t(p) * kDigits,
+        state, ticket, nullptr, nullptr);
+    }
     AMRX_LAUNCH_CHECK();
     std::swap(kin, kout);
     std::swap(vin, vout);
     run++;
   }
-  if (kin != keys) {
-    AMRX_CUDA(cudaMemcpyAsync(keys, kin, n * 8, cudaMemcpyDeviceToDevice, st));
-    AMRX_CUDA(cudaMemcpyAsync(vals, vin, n * 4, cudaMemcpyDeviceToDevice, st));
-  }
   if (passes_run) *passes_run = run;
+  if (gsrc && last < 0) {  // nothing to permute: the payload in input order
+    if (gsrc_ready) AMRX_CUDA(cudaStreamWaitEvent(st, gsrc_ready, 0));
+    AMRX_CUDA(cudaMemcpyAsync(gdst, gsrc, n * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  return kin != keys;  // the sorted keys (and u32 values) are in the alt buffers
 }
 
 }  // namespace amrx
