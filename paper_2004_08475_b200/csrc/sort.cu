@@ -15,7 +15,10 @@ namespace amrx {
 
 namespace {
 
-constexpr int kRadixBits = 8;
+#ifndef AMRX_RADIX_BITS
+#define AMRX_RADIX_BITS 9  // C4: 4 passes of 9 bits 63.5 ms ingest vs 5 of 8 bits 64.7
+#endif
+constexpr int kRadixBits = AMRX_RADIX_BITS;  // digit width (<= 9: one thread per digit)
 constexpr int kDigits = 1 << kRadixBits;
 constexpr int kSortThreads = 512;
 constexpr int kSortWarps = kSortThreads / 32;
