@@ -597,31 +597,48 @@ amrx_status amrx_index_create(const int32_t *cells4, const double *scalars,
       AMRX_CUDA(cudaMemcpyAsync(const_cast<int4 *>(cells_d), cells4, n * 16,
                                 cudaMemcpyHostToDevice, st));
     }
+    // host scalars are uploaded after the cells, in chunks on a side stream:
+    // they are first needed once the keys are sorted, and each chunk is
+    // scattered into key order as soon as it lands (scalar_chunks below)
     const double *sc_d = static_cast<const double *>(device_view(scalars));
+    constexpr int kScalChunks = 8;
     cudaStream_t aux = nullptr;
-    cudaEvent_t sc_ready = nullptr;
+    cudaEvent_t sc_ev[kScalChunks] = {};
+    cudaEvent_t sc_ready = nullptr;  // all chunks landed
+    uint64_t sc_cut[kScalChunks + 1] = {};
     if (!sc_d) {
       sc_d = static_cast<const double *>(l_scal.get(kWsScal, n * 8, st));
       AMRX_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
-      AMRX_CUDA(cudaEventCreateWithFlags(&sc_ready, cudaEventDisableTiming));
-      AMRX_CUDA(cudaEventRecord(sc_ready, st));  // slot free in st order
-      AMRX_CUDA(cudaStreamWaitEvent(aux, sc_ready, 0));
-      AMRX_CUDA(cudaMemcpyAsync(const_cast<double *>(sc_d), scalars, n * 8,
-                                cudaMemcpyHostToDevice, aux));
-      AMRX_CUDA(cudaEventRecord(sc_ready, aux));
+      for (int c = 0; c < kScalChunks; c++)
+        AMRX_CUDA(cudaEventCreateWithFlags(&sc_ev[c], cudaEventDisableTiming));
+      // the slot is free and the cells copy queued in st order: the side
+      // stream starts after it, so the cells get the host link first
+      AMRX_CUDA(cudaEventRecord(sc_ev[0], st));
+      AMRX_CUDA(cudaStreamWaitEvent(aux, sc_ev[0], 0));
+      for (int c = 0; c <= kScalChunks; c++) sc_cut[c] = n * uint64_t(c) / kScalChunks;
+      for (int c = 0; c < kScalChunks; c++) {
+        if (sc_cut[c + 1] > sc_cut[c])
+          AMRX_CUDA(cudaMemcpyAsync(const_cast<double *>(sc_d) + sc_cut[c], scalars + sc_cut[c],
+                                    (sc_cut[c + 1] - sc_cut[c]) * 8, cudaMemcpyHostToDevice,
+                                    aux));
+        AMRX_CUDA(cudaEventRecord(sc_ev[c], aux));
+      }
+      sc_ready = sc_ev[kScalChunks - 1];
     }
     struct AuxGuard {
       cudaStream_t s;
-      cudaEvent_t e;
+      cudaEvent_t *e;
+      int ne;
       ~AuxGuard()
       {
         if (s) {
           cudaStreamSynchronize(s);
           cudaStreamDestroy(s);
         }
-        if (e) cudaEventDestroy(e);
+        for (int c = 0; c < ne; c++)
+          if (e[c]) cudaEventDestroy(e[c]);
       }
-    } aux_guard{aux, sc_ready};
+    } aux_guard{aux, sc_ev, kScalChunks};
 
     const PrepassResult pre = ingest_prepass(cells_d, n, ix->scratch, st);
     if (pre.first_bad != ~0ull) {
@@ -647,6 +664,8 @@ amrx_status amrx_index_create(const int32_t *cells4, const double *scalars,
     ingest_pack(cells_d, n, ix->g, ix->keys.as<uint64_t>(), idx, st);
 
     uint64_t desc = 0, eq = 0;
+    uint32_t *rank = nullptr;
+    bool scatter_pending = false;
     ingest_order_check(ix->keys.as<uint64_t>(), n, ix->scratch, &desc, &eq, st);
     ix->scal.reserve(n * sizeof(double), st);
     if (desc == 0) {
@@ -665,17 +684,32 @@ amrx_status amrx_index_create(const int32_t *cells4, const double *scalars,
       auto *idx_alt = static_cast<uint32_t *>(l_ialt.get(kWsIdxAlt, n * 4, st));
       void *sort_scratch = l_sort.get(kWsSort, radix_sort_scratch_bytes(n), st);
       int passes = 0;
+      // resident scalars: gathered by the last pass; arriving scalars: the
+      // last pass leaves the inverse permutation for the chunk scatters
       const bool in_alt =
         radix_sort_pairs(ix->keys.as<uint64_t>(), idx, keys_alt.as<uint64_t>(), idx_alt, n,
-                         ix->g.total, sort_scratch, st, &passes, sc_d,
-                         ix->scal.as<double>(), sc_ready);
+                         ix->g.total, sort_scratch, st, &passes, aux ? nullptr : sc_d,
+                         aux ? nullptr : ix->scal.as<double>(), nullptr,
+                         aux ? &rank : nullptr);
       if (in_alt) {
         std::swap(ix->keys.ptr, keys_alt.ptr);
         std::swap(ix->keys.bytes, keys_alt.bytes);
         std::swap(ix->keys.stream, keys_alt.stream);
       }
+      scatter_pending = aux != nullptr;
     }
     finalize_index(ix.get());
+    if (scatter_pending) {
+      for (int c = 0; c < kScalChunks; c++) {
+        AMRX_CUDA(cudaStreamWaitEvent(st, sc_ev[c], 0));
+        if (rank)
+          scatter_f64(rank + sc_cut[c], sc_d + sc_cut[c], ix->scal.as<double>(),
+                      sc_cut[c + 1] - sc_cut[c], st);
+      }
+      if (!rank)  // no pass permuted anything
+        AMRX_CUDA(cudaMemcpyAsync(ix->scal.ptr, sc_d, n * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, st));
+    }
     AMRX_CUDA(cudaEventRecord(e1, st));
     AMRX_CUDA(cudaStreamSynchronize(st));
     float ms = 0;

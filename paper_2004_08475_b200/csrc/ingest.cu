@@ -146,6 +146,22 @@ gather_kernel(const uint32_t *__restrict__ perm, const double *__restrict__ in,
   }
 }
 
+__global__ void __launch_bounds__(kThreads)
+scatter_kernel(const uint32_t *__restrict__ rank, const double *__restrict__ in,
+               double *__restrict__ out, uint64_t n)
+{
+  constexpr int U = 4;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t r0 = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r0 < n;
+       r0 += stride * U) {
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint64_t r = r0 + u * stride;
+      if (r < n) out[__ldg(rank + r)] = __ldg(in + r);
+    }
+  }
+}
+
 __global__ void pad_kernel(uint64_t *keys, uint64_t n)
 {
   keys[n + threadIdx.x] = ~0ull;
@@ -543,6 +559,14 @@ void gather_f64(const uint32_t *perm, const double *in, double *out,
 {
   gather_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(perm, in, out,
                                                               n);
+  AMRX_LAUNCH_CHECK();
+}
+
+void scatter_f64(const uint32_t *rank, const double *in, double *out, uint64_t n,
+                 cudaStream_t st)
+{
+  if (n == 0) return;
+  scatter_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(rank, in, out, n);
   AMRX_LAUNCH_CHECK();
 }
 

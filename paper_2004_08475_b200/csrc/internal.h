@@ -153,12 +153,18 @@ int scan_exclusive_u32_u64(const uint32_t *in, uint64_t *out, uint64_t n,
 /// ponging with the alt buffers; returns true when the sorted keys (and,
 /// without gsrc, values) ended in the alt buffers.  With gsrc, the last
 /// pass writes gdst[i] = gsrc[value of sorted item i] instead of the
-/// values (after gsrc_ready, if set)
+/// values (after gsrc_ready, if set).  With rank_out instead, the last
+/// pass writes the inverse permutation (rank[input position] = sorted
+/// position) and *rank_out points at it (null if no pass ran: identity)
 bool radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
                       uint32_t *vals_alt, uint64_t n, int key_bits,
                       void *scratch, cudaStream_t st, int *passes_run,
                       const double *gsrc = nullptr, double *gdst = nullptr,
-                      cudaEvent_t gsrc_ready = nullptr);
+                      cudaEvent_t gsrc_ready = nullptr, uint32_t **rank_out = nullptr);
+
+/// out[rank[i]] = in[i] for i in [0, n) (a payload chunk into key order)
+void scatter_f64(const uint32_t *rank, const double *in, double *out, uint64_t n,
+                 cudaStream_t st);
 
 /// bytes of scratch radix_sort_pairs needs for n keys
 size_t radix_sort_scratch_bytes(uint64_t n);

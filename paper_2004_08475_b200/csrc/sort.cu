@@ -101,12 +101,15 @@ struct PassSmem {
   uint32_t tile;
 };
 
-/*! one LSD pass.  GATHER (the last pass): instead of the u32 values, write
-    gsrc[value] -- the payload the values index (the scalars in input
-    order) -- so the separate gather kernel and the value round trip
-    disappear; the random payload loads are issued together per thread in
-    the final scatter, after the look-back. */
-template <bool GATHER>
+/*! one LSD pass.  MODE kPassGather (the last pass): instead of the u32
+    values, write gsrc[value] -- the payload the values index (the scalars
+    in input order) -- so the separate gather kernel and the value round
+    trip disappear; the random payload loads are issued together per thread
+    in the final scatter, after the look-back.  MODE kPassInverse (the last
+    pass): write vals_out[value] = sorted position (the inverse permutation,
+    for scattering a payload that is still arriving). */
+enum { kPassPlain = 0, kPassGather = 1, kPassInverse = 2 };
+template <int MODE>
 __global__ void __launch_bounds__(kSortThreads)
 onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
                      const uint32_t *__restrict__ vals_in,
@@ -220,7 +223,17 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
     }
   __syncthreads();
   const uint64_t valid = n - base < uint64_t(kSortTile) ? n - base : kSortTile;
-  if (GATHER) {
+  if (MODE == kPassInverse) {
+    for (int pos = threadIdx.x; pos < int(valid); pos += kSortThreads) {
+      const uint64_t kk = sm.keys[pos];
+      const uint32_t d = uint32_t((kk >> shift) & (kDigits - 1));
+      const uint64_t dst = sm.gofs[d] + (pos - sm.bexcl[d]);
+      keys_out[dst] = kk;
+      vals_out[sm.vals[pos]] = uint32_t(dst);
+    }
+    return;
+  }
+  if (MODE == kPassGather) {
     constexpr int U = 4;  // payload loads in flight per thread
     for (int p0 = threadIdx.x; p0 < int(valid); p0 += U * kSortThreads) {
       double g[U];
@@ -263,9 +276,11 @@ size_t radix_sort_scratch_bytes(uint64_t n)
 bool radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
                       uint32_t *vals_alt, uint64_t n, int key_bits,
                       void *scratch, cudaStream_t st, int *passes_run,
-                      const double *gsrc, double *gdst, cudaEvent_t gsrc_ready)
+                      const double *gsrc, double *gdst, cudaEvent_t gsrc_ready,
+                      uint32_t **rank_out)
 {
   if (passes_run) *passes_run = 0;
+  if (rank_out) *rank_out = nullptr;
   if (n <= 1 || key_bits <= 0) return false;
   const int passes = (key_bits + kRadixBits - 1) / kRadixBits;
   const uint64_t tiles = (n + kSortTile - 1) / kSortTile;
@@ -299,10 +314,13 @@ bool radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
   static bool attr_set = false;
   const size_t smem = sizeof(PassSmem);
   if (!attr_set) {
-    AMRX_CUDA(cudaFuncSetAttribute(onesweep_pass_kernel<false>,
+    AMRX_CUDA(cudaFuncSetAttribute(onesweep_pass_kernel<kPassPlain>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(smem)));
-    AMRX_CUDA(cudaFuncSetAttribute(onesweep_pass_kernel<true>,
+    AMRX_CUDA(cudaFuncSetAttribute(onesweep_pass_kernel<kPassGather>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(smem)));
+    AMRX_CUDA(cudaFuncSetAttribute(onesweep_pass_kernel<kPassInverse>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(smem)));
     attr_set = true;
@@ -321,13 +339,18 @@ bool radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
     if (trivial[p]) continue;
     AMRX_CUDA(cudaMemsetAsync(state, 0, state_bytes, st));
     AMRX_CUDA(cudaMemsetAsync(ticket, 0, 4, st));
-    if (gsrc && p == last) {
+    if (rank_out && p == last) {
+      onesweep_pass_kernel<kPassInverse><<<unsigned(tiles), kSortThreads, smem, st>>>(
+        kin, vin, kout, vout, n, p * kRadixBits, offs + size_t(p) * kDigits,
+        state, ticket, nullptr, nullptr);
+      *rank_out = vout;
+    } else if (gsrc && p == last) {
       if (gsrc_ready) AMRX_CUDA(cudaStreamWaitEvent(st, gsrc_ready, 0));
-      onesweep_pass_kernel<true><<<unsigned(tiles), kSortThreads, smem, st>>>(
+      onesweep_pass_kernel<kPassGather><<<unsigned(tiles), kSortThreads, smem, st>>>(
         kin, vin, kout, vout, n, p * kRadixBits, offs + size_t(p) * kDigits,
         state, ticket, gsrc, gdst);
     } else {
-      onesweep_pass_kernel<false><<<unsigned(tiles), kSortThreads, smem, st>>>(
+      onesweep_pass_kernel<kPassPlain><<<unsigned(tiles), kSortThreads, smem, st>>>(
         kin, vin, kout, vout, n, p * kRadixBits, offs + size_t(p) * kDigits,
         state, ticket, nullptr, nullptr);
     }
@@ -337,7 +360,7 @@ bool radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
     run++;
   }
   if (passes_run) *passes_run = run;
-  if (gsrc && last < 0) {  // nothing to permute: the payload in input order
+  if (gsrc && !rank_out && last < 0) {  // nothing to permute: the payload in input order
     if (gsrc_ready) AMRX_CUDA(cudaStreamWaitEvent(st, gsrc_ready, 0));
     AMRX_CUDA(cudaMemcpyAsync(gdst, gsrc, n * 8, cudaMemcpyDeviceToDevice, st));
   }
