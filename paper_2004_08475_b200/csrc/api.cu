@@ -1021,7 +1021,16 @@ amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range,
       // pinned host output, large input: extract in cell-range chunks (their
       // concatenation is the candidate order) so each chunk's download
       // overlaps the next chunk's extraction
-      const int nch = int(std::min<uint64_t>(8, cells >> 23));
+      // the downloads are the bottleneck (host link), so the only exposed
+      // extraction time is the first chunk's: start small, then grow --
+      // cut points at 1/64, 1/32 (cumulative 3/64), then equal eighths of
+      // the rest
+      uint64_t cut[12];
+      int nch = 0;
+      cut[0] = 0;
+      cut[++nch] = cells / 64;
+      cut[++nch] = cells * 3 / 64;
+      for (int k = 1; k <= 8; k++) cut[++nch] = cells * 3 / 64 + (cells - cells * 3 / 64) * k / 8;
       cudaStream_t cp;
       cudaEvent_t done[2];
       AMRX_CUDA(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
@@ -1041,8 +1050,8 @@ amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range,
       ExtractResult tot{};
       uint64_t off = 0;
       for (int ci = 0; ci < nch; ci++) {
-        rq.cell_begin = b + cells * uint64_t(ci) / uint64_t(nch);
-        rq.cell_end = b + cells * uint64_t(ci + 1) / uint64_t(nch);
+        rq.cell_begin = b + cut[ci];
+        rq.cell_end = b + cut[ci + 1];
         rq.final_host = true;
         rq.xyz = static_cast<char *>(xyz9) + off * tri_bytes;
         rq.tri_cap = cap > off ? cap - off : 0;
