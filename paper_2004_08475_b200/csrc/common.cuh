@@ -300,11 +300,6 @@ enum DbgEvent {
   kDbgCount
 };
 
-// lane_find: fetch small buckets whole with vector loads (A/B switch)
-#ifndef AMRX_SMALL_BUCKET
-#define AMRX_SMALL_BUCKET 0
-#endif
-
 // counters are compiled in only for a diagnostic build (make DBG=1): the
 // atomics otherwise bloat the hot loop past the instruction cache
 #ifndef AMRX_DBG
@@ -363,74 +358,10 @@ __device__ __forceinline__ void occ_find(const SearchCtx &s, const uint64_t (&q)
     }
 }
 
-/*! Per-lane lookup of NQ ascending keys inside their own directory buckets
-    (no warp cooperation): with ~2 directory entries per cell a bucket
-    holds a handful of keys, so each query costs two directory loads and a
-    short binary search through L1-cached key loads.  Same contract as
-    warp_find (exact hit, or under FINER the first same-anchor lower-level
-    key).  Consecutive queries resume from the previous lower_bound. */
-template <int NQ, bool FINER>
-__device__ __forceinline__ void lane_find(const SearchCtx &s, const uint64_t (&q)[NQ],
-                                          const bool (&valid)[NQ],
-                                          int64_t (&out)[NQ], int (&lvl)[NQ])
-{
-  uint64_t prev_p = 0;
-  uint64_t prev_q = 0;
-#pragma unroll
-  for (int t = 0; t < NQ; t++) {
-    if (!valid[t]) continue;
-    if (s.rec) {
-      int rl;
-      out[t] = occ_resolve<FINER>(q[t], ldg_rec(s.rec, q[t], s.dir_shift), uint32_t(s.lmask), rl);
-      lvl[t] = rl + s.shift;
-      continue;
-    }
-    const uint64_t anchor = q[t] & ~s.lmask;
-    uint64_t lo = __ldg(s.dir + ((FINER ? anchor : q[t]) >> s.dir_shift));
-    const uint64_t hi = __ldg(s.dir + (q[t] >> s.dir_shift) + 1);
-    const uint64_t from = (t > 0 && prev_q <= q[t] && prev_p > lo) ? prev_p : lo;
-    uint64_t p;
-    if (AMRX_SMALL_BUCKET && hi - from <= 6) {
-      // small bucket (the common case): one round trip of three 16-byte
-      // loads covers it; lower_bound = from + #keys < q (the array is
-      // padded with sentinels, so the loads never leave it)
-      const uint64_t a0 = from & ~1ull;
-      uint32_t below = 0;
-#pragma unroll
-      for (int v = 0; v < 4; v++) {
-        const ulonglong2 kv = ldg_u64x2(s.keys + a0 + 2 * v);
-        const uint64_t i0 = a0 + 2 * v, i1 = i0 + 1;
-        below += (i0 >= from && i0 < hi && kv.x < q[t]);
-        below += (i1 >= from && i1 < hi && kv.y < q[t]);
-      }
-      p = from + below;
-    } else {
-      p = global_lower_bound(s.keys, from, hi, q[t]);
-    }
-    prev_p = p;
-    prev_q = q[t];
-    int64_t res = -1;
-    int rl = 0;
-    if (p < hi && ldg_u64(s.keys + p) == q[t]) {
-      res = int64_t(p);
-      rl = int(q[t] & s.lmask);
-    } else if (FINER) {
-      uint64_t x = p;
-      while (x > lo && (ldg_u64(s.keys + x - 1) & ~s.lmask) == anchor) x--;
-      if (x < p) {
-        res = int64_t(x);
-        rl = int(ldg_u64(s.keys + x) & s.lmask);
-      }
-    }
-    out[t] = res;
-    lvl[t] = rl + s.shift;
-  }
-}
-
 /*! K independent lookups per lane advanced in lock-step: the directory
     loads of all K go out together, then every binary-search step issues up
     to K independent key loads, so the dependent-latency chain is that of
-    ONE search instead of K.  Same contract as lane_find / warp_find. */
+    ONE search instead of K.  Same contract as warp_find. */
 template <int K, bool FINER>
 __device__ __forceinline__ void batch_find(const SearchCtx &s, const uint64_t (&q)[K],
                                            const bool (&valid)[K], int64_t (&out)[K],

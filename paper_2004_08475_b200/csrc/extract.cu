@@ -13,16 +13,16 @@
 //   sliver drop on exact equality                     proj/src/contour.cpp:80-84
 //   two-pass count -> prefix -> emit                  proj/src/pipeline.cpp:80-146
 //
-// B200 design: one warp owns a tile of 30 consecutive cells
-// (lanes 1..30; lanes 0 and 31 are halo lanes holding the cells either side),
-// handed out by an atomic ticket.  Instead of 8 independent candidates x 8
-// corner snaps, each lane resolves its cell's 27-point stencil {-w,0,w}^3 --
-// a per-tile packed Stencil makes every point's key a few adds -- with
-// AMRX_BATCH lock-step directory-bucket searches (batch_find), and borrows
-// the dz = +-1 points from its z-neighbour lanes, whose centre points are the
-// identical queries.  Round 0 resolves every candidate's corner 0 (82-86% of
-// candidates die there); round 1 what the survivors still need.  The rules
-// are then applied corner by corner in the reference's order, so the
+// B200 design: one warp owns a tile of 32 consecutive cells,
+// one per lane, handed out by an atomic ticket.  Instead of 8 independent
+// candidates x 8 corner snaps, each lane resolves the points of its cell's
+// 27-point stencil {-w,0,w}^3 its live candidates need: a point's key is the
+// cell key plus packed steps (Stencil), a lookup is one occupancy record load
+// + popcount, and the 14 points of a uniform region have compile-time
+// offsets (fast_point).  Round 0 resolves every candidate's corner 0 (82-86%
+// of candidates die there); round 1 what the survivors still need.  Points
+// are classified into 27-bit masks and a candidate is a mask test over its
+// corner cube; the lowest failing bit is its first failing corner, so the
 // reported reason is the reference's.  Duals and triangles go to per-warp
 // staging chunks with per-tile (offset, count) records; a scan over the tile
 // counts and reorder_kernel restore candidate order -- the reference's
@@ -33,43 +33,18 @@
 #include <cstdio>
 #include <cstdlib>
 
-// 1: per-lane bucket search (lane_find); 0: warp-cooperative windows (warp_find)
-#ifndef AMRX_LANE_SEARCH
-#define AMRX_LANE_SEARCH 1
-#endif
-// >0: resolve stencil points K at a time with lock-step lookups (batch_find);
-// 0: column by column (resolve_column)
-#ifndef AMRX_BATCH
-#define AMRX_BATCH 2  // measured best on C4: K=2 234 ms, K=3 242, K=4 286, columns 326
-#endif
-// 1: point classification masks + mask-based rules (resolve_marks); 0: the
-// 2-bit status walk (lookup_points / resolve_points + advance)
-#ifndef AMRX_COLUMNS
-#define AMRX_COLUMNS 1
-#endif
-// 1: borrow z-neighbour lanes' lookups (resolve_points); 0: every lane alone
-// (with the occupancy directory a lookup costs less than the sharing's
-// shuffles: C4 iso 141 ms shared vs 125 ms alone, both at AMRX_MINB 4)
-#ifndef AMRX_SHARE
-#define AMRX_SHARE 0
-#endif
-
 namespace amrx {
 
 namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kTileCells = AMRX_SHARE ? 30 : 32;  // cells one warp tile owns
+constexpr int kTileCells = 32;  // cells one warp tile owns (one per lane)
 
 // point index p = (ox+1) + 3(oy+1) + 9(oz+1), o in {-1,0,1}^3; self = 13
 constexpr uint32_t kCorner0Points = (1u << 0) | (1u << 1) | (1u << 3) |
                                     (1u << 4) | (1u << 9) | (1u << 10) |
                                     (1u << 12) | (1u << 13);
-constexpr uint32_t col_bits(int col)
-{
-  return (1u << col) | (1u << (col + 9)) | (1u << (col + 18));
-}
 
 enum : uint32_t { kOk = 0, kMiss = 1, kFiner = 2, kLower = 3 };
 
@@ -83,13 +58,6 @@ __device__ __forceinline__ int point_of(int delta, int d)
          9 * (((d >> 2) & 1) + ((delta >> 2) & 1));
 }
 
-__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v)
-{
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1)
-    v += __shfl_xor_sync(kFull, (unsigned long long)v, off);
-  return v;
-}
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v)
 {
@@ -199,9 +167,6 @@ struct KArgs {
 };
 
 struct Smem {
-#if !AMRX_LANE_SEARCH
-  uint64_t win[kWarps][kWin];  // warp_find's key windows
-#endif
   uint32_t id[kWarps][27][32];
   uint8_t lev[kWarps][27][32];
   uint64_t mc_rows[256];
@@ -210,8 +175,6 @@ struct Smem {
   // cursors (cur, end) for duals and triangles
   unsigned long long acc[kWarps][8];
   uint64_t chunk[kWarps][4];
-  // remain[delta][d]: stencil points of candidate delta's corners d..7
-  uint32_t remain[8][9];
 };
 
 /// slot-numbered corner mask -> table row (mc::to_table_case, mc_tables.cpp:324-330)
@@ -341,135 +304,6 @@ __device__ __noinline__ int mc_dual(const KArgs &a, const Smem &sm, int warp, in
   return count;
 }
 
-/// warp_find for the coarser-level probes: rare, so out of line
-__device__ __noinline__ void find3_coarse(const SearchCtx &s, const uint64_t (&q)[3],
-                                          const bool (&v)[3], int64_t (&o)[3],
-                                          int (&l)[3], uint64_t *win)
-{
-#if AMRX_LANE_SEARCH
-  lane_find<3, false>(s, q, v, o, l);
-#else
-  warp_find<3, false>(s, q, v, o, l, win);
-#endif
-}
-
-/*! resolve the three stencil points of column COL (dx, dy fixed; dz =
-    -1,0,+1) this lane wants (bit t of `want`: dz = t-1), in snap's probe order
-    (locator.cpp:122-134), skipping levels the block level map rules out
-    (exact: a cell containing p lies in p's coarsest-aligned block):
-      1. the hint level and every finer level in ONE warp_find (finer cells
-         containing a stencil point share its anchor, see warp_find);
-      2. the candidate coarser levels ascending, one warp_find per round --
-         in valid data the first coarser probe hits, and points with no
-         candidate level (holes, outside the domain) cost no search. */
-__device__ __forceinline__ void resolve_column(const KArgs &a, Smem &sm,
-                                            int warp, int lane, const Cell &c,
-                                            uint32_t self, int COL, uint32_t want,
-                                            uint32_t &resolved,
-                                            uint64_t &status)
-{
-  const KeyGeom &g = a.g;
-  const int ox = COL % 3 - 1, oy = COL / 3 - 1;
-  const int64_t w = int64_t(1) << c.level;
-  const int64_t px = c.i + ox * w, py = c.j + oy * w;
-  // level bits: index of the hint level in g.levels
-  const int hint_bit = __popc(g.level_mask & ((1u << c.level) - 1));
-  const uint32_t le_hint = (2u << hint_bit) - 1;
-  // at the hint level the points are their own anchors: build the keys
-  // from one shared x/y part, no masking
-  const bool xy = want != 0 && px >= g.mn[0] && px <= g.mx[0] && py >= g.mn[1] &&
-                  py <= g.mx[1];
-  uint64_t base = uint64_t(c.level - g.shift);
-  if (g.bits[0]) base |= uint64_t((px - g.mn[0]) >> g.shift) << g.sh[0];
-  if (g.bits[1]) base |= uint64_t((py - g.mn[1]) >> g.shift) << g.sh[1];
-  uint64_t q[3];
-  bool v[3];
-  int64_t out[3] = {-1, -1, -1};
-  int lvl[3] = {c.level, c.level, c.level};
-  uint32_t cand[3];
-#pragma unroll
-  for (int t = 0; t < 3; t++) {
-    const int64_t pz = c.k + (t - 1) * w;
-    cand[t] = ((want >> t) & 1u) ? block_levels(g, a.lmap, px, py, pz) : 0u;
-    v[t] = xy && pz >= g.mn[2] && pz <= g.mx[2] && (cand[t] & le_hint);
-    if (COL == 4 && t == 1 && a.unique && ((want >> 1) & 1u)) {
-      // the cell's own anchor on its own level: with no duplicate keys the
-      // lookup can only return the cell itself (lower_bound of its key)
-      v[t] = false;
-      out[t] = int64_t(self);
-      cand[t] = 0;
-    }
-    q[t] = base | (g.bits[2] ? uint64_t((pz - g.mn[2]) >> g.shift) << g.sh[2] : 0);
-    cand[t] &= ~le_hint;  // what is left for step 2
-  }
-#if AMRX_LANE_SEARCH
-  lane_find<3, true>(a.s, q, v, out, lvl);
-#else
-  if (__any_sync(kFull, v[0] || v[1] || v[2]))
-    warp_find<3, true>(a.s, q, v, out, lvl, sm.win[warp]);
-#endif
-
-  // step 2: coarser candidate levels, ascending (= the reference's finest
-  // first order restricted to the levels above the hint)
-  bool pend[3];
-#pragma unroll
-  for (int t = 0; t < 3; t++) pend[t] = out[t] < 0 && cand[t] != 0;
-  while (__any_sync(kFull, pend[0] || pend[1] || pend[2])) {
-    dbg_add(a.s, kDbgCoarser);
-    bool v2[3];
-    int64_t o2[3] = {-1, -1, -1};
-    int l2[3], L[3];
-#pragma unroll
-    for (int t = 0; t < 3; t++) {
-      L[t] = 0;
-      v2[t] = false;
-      if (pend[t]) {
-        const int b = __ffs(cand[t]) - 1;
-        cand[t] &= cand[t] - 1;
-        L[t] = g.levels[b];
-        v2[t] = query_key(g, px, py, c.k + (t - 1) * w, L[t], q[t]);
-      }
-    }
-#if AMRX_LANE_SEARCH
-    find3_coarse(a.s, q, v2, o2, l2, nullptr);
-#else
-    find3_coarse(a.s, q, v2, o2, l2, sm.win[warp]);
-#endif
-#pragma unroll
-    for (int t = 0; t < 3; t++)
-      if (pend[t]) {
-        if (v2[t] && o2[t] >= 0) {
-          out[t] = o2[t];
-          lvl[t] = L[t];
-          pend[t] = false;
-        } else if (!cand[t]) {
-          pend[t] = false;
-        }
-      }
-  }
-  {
-#pragma unroll
-    for (int t = 0; t < 3; t++) {
-      if (!((want >> t) & 1u)) continue;
-      const int p = COL + 9 * t;
-      uint32_t st;
-      if (out[t] < 0)
-        st = kMiss;
-      else if (lvl[t] < c.level)
-        st = kFiner;
-      else if (lvl[t] == c.level && uint32_t(out[t]) < self)
-        st = kLower;
-      else
-        st = kOk;
-      status |= uint64_t(st) << (2 * p);
-      resolved |= 1u << p;
-      sm.id[warp][p][lane] = uint32_t(out[t]);
-      sm.lev[warp][p][lane] = uint8_t(lvl[t]);
-    }
-  }
-}
-
-#if AMRX_BATCH > 0
 struct Hit {
   int64_t id;
   int level;
@@ -524,34 +358,8 @@ __device__ __noinline__ Hit probe_coarser(const KArgs &a, const Cell &c, const S
   return Hit{-1, c.level};
 }
 
-/// a CellId as kept in shared memory (u32, all ones = absent) back to int64
-__device__ __forceinline__ int64_t stored_id(uint32_t v)
-{
-  return v == 0xffffffffu ? int64_t(-1) : int64_t(v);
-}
-
-/// status of a resolved point relative to the owner (dual.cpp:60-67)
-__device__ __forceinline__ void record_point(Smem &sm, int warp, int lane, const Cell &c,
-                                             uint32_t self, int p, int64_t id, int lev,
-                                             uint32_t &resolved, uint64_t &status)
-{
-  uint32_t st;
-  if (id < 0)
-    st = kMiss;
-  else if (lev < c.level)
-    st = kFiner;
-  else if (lev == c.level && uint32_t(id) < self)
-    st = kLower;
-  else
-    st = kOk;
-  status |= uint64_t(st) << (2 * p);
-  resolved |= 1u << p;
-  sm.id[warp][p][lane] = uint32_t(id);
-  sm.lev[warp][p][lane] = uint8_t(lev);
-}
-
 // ---------------------------------------------------------------------------
-// Mask-based rules (AMRX_COLUMNS, the default): each resolved stencil point
+// Mask-based rules: each resolved stencil point
 // is classified into four 27-bit masks, and a candidate's fate is a mask test
 // over its corner cube (no per-corner walk).
 
@@ -568,7 +376,7 @@ __host__ __device__ constexpr int base_of(int delta)
   return (delta & 1) + 3 * ((delta >> 1) & 1) + 9 * (delta >> 2);
 }
 
-/// classify one resolved point (record_point with the mask representation)
+/// classify one resolved point (dual.cpp:60-67: missing, finer, lower key, ok)
 __device__ __forceinline__ void mark_point(Smem &sm, int warp, int lane, const Cell &c,
                                            uint32_t self, int p, int64_t id, int lev,
                                            Marks &m)
@@ -626,7 +434,7 @@ __device__ __forceinline__ void fast_point(const KArgs &a, Smem &sm, int warp, i
   pend |= 1u << P;
 }
 
-/*! resolve the stencil points in `todo` into the marks: AMRX_BATCH per lane
+/*! resolve the stencil points in `todo` into the marks: two per lane
     at a time with their lookups in lock-step (batch_find), in snap's probe
     order (locator.cpp:122-134): hint level + finer in one lookup, then the
     coarser candidate levels (probe_coarser).  A loop over runtime point
@@ -636,7 +444,7 @@ __device__ __forceinline__ void resolve_marks(const KArgs &a, Smem &sm, int warp
                                               const Cell &c, const Stencil &st,
                                               uint32_t self, uint32_t todo, Marks &m)
 {
-  constexpr int K = AMRX_BATCH;
+  constexpr int K = 2;  // measured best: K = 1 +1%, K = 3 +13%
   // present levels coarser than the hint: what a miss probes next
   const uint32_t coarser = a.g.level_mask & ~((2u << c.level) - 1);
   while (__any_sync(kFull, todo != 0)) {
@@ -675,210 +483,6 @@ __device__ __forceinline__ void resolve_marks(const KArgs &a, Smem &sm, int warp
   }
 }
 
-/*! look up the stencil points in `todo`, AMRX_BATCH at a time per lane
-    with their lookups advanced in lock-step (batch_find), in snap's probe
-    order (locator.cpp:122-134): hint + finer levels in one lookup, then
-    the coarser candidate levels (probe_coarser). */
-#ifndef AMRX_LOOKUP_NOINLINE
-#define AMRX_LOOKUP_NOINLINE 0  // out of line measured 1.6x slower (spills + calls)
-#endif
-#if AMRX_LOOKUP_NOINLINE
-#define AMRX_LOOKUP_ATTR __noinline__
-#else
-#define AMRX_LOOKUP_ATTR __forceinline__
-#endif
-__device__ AMRX_LOOKUP_ATTR void lookup_points(const KArgs &a, Smem &sm, int warp, int lane,
-                                              const Cell &c, const Stencil &st,
-                                              uint32_t self, uint32_t todo,
-                                              uint32_t &resolved, uint64_t &status)
-{
-  constexpr int K = AMRX_BATCH;
-  // present levels coarser than the hint: what a miss probes next (the
-  // block level map is consulted only on that rare path, probe_coarser)
-  const uint32_t coarser = a.g.level_mask & ~((2u << c.level) - 1);
-  while (__any_sync(kFull, todo != 0)) {
-    uint64_t q[K];
-    bool v[K];
-    int64_t out[K];
-    int lvl[K], pk[K];
-#pragma unroll
-    for (int k = 0; k < K; k++) {
-      pk[k] = -1;
-      v[k] = false;
-      out[k] = -1;
-      lvl[k] = c.level;
-      q[k] = 0;
-      if (todo) {
-        const int p = __ffs(todo) - 1;
-        todo &= todo - 1;
-        pk[k] = p;
-        // at the hint level the point is its own anchor: key = cell key +
-        // packed steps, valid iff inside the stored range
-        v[k] = (st.inrange >> p) & 1u;
-        q[k] = stencil_key(st, p);
-      }
-    }
-    batch_find<K, true>(a.s, q, v, out, lvl);
-#pragma unroll
-    for (int k = 0; k < K; k++)
-      if (pk[k] >= 0 && out[k] < 0 && coarser != 0) {
-        dbg_add(a.s, kDbgCoarser);
-        const Hit h = probe_coarser(a, c, st, pk[k], coarser);
-        out[k] = h.id;
-        lvl[k] = h.level;
-      }
-#pragma unroll
-    for (int k = 0; k < K; k++)
-      if (pk[k] >= 0) record_point(sm, warp, lane, c, self, pk[k], out[k], lvl[k], resolved, status);
-  }
-}
-
-/*! resolve the stencil points in `need`, sharing lookups between lanes.
-    Lanes hold consecutive cells, so lane L-1 is usually L's z-predecessor
-    on the same level: then L's point (dx,dy,-1) IS L-1's point (dx,dy,0)
-    with the same hint level -- the identical snap query (locator.cpp:
-    122-134), hence the identical answer -- and likewise (dx,dy,+1) with
-    lane L+1.  So each lane looks up the centre points (dx,dy,0) of the
-    columns it needs plus only those dz = +-1 points its neighbour will not
-    have, in ONE lock-step pass, then borrows the rest from the neighbours'
-    shared-memory results; with unique keys the z-neighbour cells themselves
-    need no lookup at all.  With AMRX_SHARE the tile is 30 cells and lanes 0
-    and 31 are halo lanes holding the cells just before and after it: they
-    evaluate no candidates, they only look up the centres their neighbour
-    borrows, so no working lane is left without a neighbour.  Exact by
-    construction: a borrowed answer is the answer to the very same query. */
-__device__ __forceinline__ void resolve_points(const KArgs &a, Smem &sm, int warp, int lane,
-                                               const Cell &c, const Stencil &st, uint32_t self,
-                                               uint64_t kself, bool valid, uint32_t need,
-                                               uint32_t &resolved,
-                                               uint64_t &status)
-{
-  if (!AMRX_SHARE) {
-    uint32_t todo = need & ~resolved;
-    if (a.unique && ((todo >> 13) & 1u))
-      record_point(sm, warp, lane, c, self, 13, self, c.level, resolved, status);
-    lookup_points(a, sm, warp, lane, c, st, self, need & ~resolved, resolved, status);
-    return;
-  }
-  // is lane L-1 (L+1) this cell's z-predecessor (successor) on the same level?
-  const uint64_t dz = st.sz;
-  const uint64_t kp = __shfl_up_sync(kFull, kself, 1);
-  const uint64_t ks = __shfl_down_sync(kFull, kself, 1);
-  const bool vp = __shfl_up_sync(kFull, valid, 1);
-  const bool vs = __shfl_down_sync(kFull, valid, 1);
-  const bool pred_ok = valid && lane > 0 && vp && ((st.inrange >> 4) & 1u) && kp == kself - dz;
-  const bool succ_ok = valid && lane < 31 && vs && ((st.inrange >> 22) & 1u) && ks == kself + dz;
-
-  // halo lanes: adopt what the neighbour will borrow (lane 0 serves lane 1's
-  // dz = -1 points, lane 31 serves lane 30's dz = +1 points)
-  const uint32_t need_next = __shfl_down_sync(kFull, need, 1);
-  const uint32_t need_prev = __shfl_up_sync(kFull, need, 1);
-  if (lane == 0) need = succ_ok ? ((need_next & 0x1ffu) << 9) : 0u;
-  if (lane == 31) need = pred_ok ? (((need_prev >> 18) & 0x1ffu) << 9) : 0u;
-
-  uint32_t todo = need & ~resolved;
-  if (a.unique) {
-    // with no duplicate keys a lookup of an existing cell's own key returns
-    // that cell: the cell itself, and its z-neighbours
-    if ((todo >> 13) & 1u) record_point(sm, warp, lane, c, self, 13, self, c.level, resolved, status);
-    if (pred_ok && ((todo >> 4) & 1u))
-      record_point(sm, warp, lane, c, self, 4, int64_t(self) - 1, c.level, resolved, status);
-    if (succ_ok && ((todo >> 22) & 1u))
-      record_point(sm, warp, lane, c, self, 22, int64_t(self) + 1, c.level, resolved, status);
-    todo = need & ~resolved;
-  }
-  // centre points (dz = 0) of every column with a needed point
-  uint32_t centres = 0;
-#pragma unroll
-  for (int col = 0; col < 9; col++)
-    if (todo & col_bits(col)) centres |= 1u << (col + 9);
-  centres &= ~resolved;
-  // what the neighbours will hold after this pass
-  const uint32_t hp = __shfl_up_sync(kFull, centres | resolved, 1);
-  const uint32_t hs = __shfl_down_sync(kFull, centres | resolved, 1);
-  uint32_t own = centres;
-  for (uint32_t m = todo & 0x1ffu; m; m &= m - 1) {  // dz = -1
-    const int p = __ffs(m) - 1;
-    if (!(pred_ok && ((hp >> (p + 9)) & 1u))) own |= 1u << p;
-  }
-  for (uint32_t m = todo & (0x1ffu << 18); m; m &= m - 1) {  // dz = +1
-    const int p = __ffs(m) - 1;
-    if (!(succ_ok && ((hs >> (p - 9)) & 1u))) own |= 1u << p;
-  }
-  lookup_points(a, sm, warp, lane, c, st, self, own, resolved, status);
-  __syncwarp();
-  // borrow the rest: dz = -1 from lane L-1's centre, dz = +1 from lane L+1's
-  todo = need & ~resolved;
-  for (uint32_t m = todo & 0x1ffu; m; m &= m - 1) {
-    const int p = __ffs(m) - 1;
-    record_point(sm, warp, lane, c, self, p, stored_id(sm.id[warp][p + 9][lane - 1]),
-                 sm.lev[warp][p + 9][lane - 1], resolved, status);
-  }
-  for (uint32_t m = todo & (0x1ffu << 18); m; m &= m - 1) {
-    const int p = __ffs(m) - 1;
-    record_point(sm, warp, lane, c, self, p, stored_id(sm.id[warp][p - 9][lane + 1]),
-                 sm.lev[warp][p - 9][lane + 1], resolved, status);
-  }
-}
-#endif  // AMRX_BATCH > 0
-
-__device__ __forceinline__ void resolve_needed(const KArgs &a, Smem &sm,
-                                               int warp, int lane,
-                                               const Cell &c, const Stencil &st,
-                                               uint32_t self, uint64_t kself, bool valid,
-                                               uint32_t need,
-                                               uint32_t &resolved,
-                                               uint64_t &status)
-{
-#if AMRX_BATCH > 0
-  resolve_points(a, sm, warp, lane, c, st, self, kself, valid, need, resolved, status);
-  return;
-#endif
-  uint32_t cols = 0;
-#pragma unroll
-  for (int col = 0; col < 9; col++)
-    if (need & col_bits(col)) cols |= 1u << col;
-  uint32_t wcols = __reduce_or_sync(kFull, cols);
-  while (wcols) {
-    const int col = __ffs(wcols) - 1;
-    wcols &= wcols - 1;
-    dbg_add(a.s, kDbgColumns);
-    // only the points this lane's live candidates need (bit t: dz = t-1)
-    const uint32_t want = ((need >> col) & 1u) | (((need >> (col + 9)) & 1u) << 1) |
-                          (((need >> (col + 18)) & 1u) << 2);
-    resolve_column(a, sm, warp, lane, c, self, col, want, resolved, status);
-  }
-}
-
-/// walk each live candidate's corners in order while they are resolved
-__device__ __forceinline__ void advance(uint32_t resolved, uint64_t status,
-                                        uint32_t &alive, uint32_t &curd,
-                                        uint32_t &accepted, uint32_t &reasons)
-{
-#pragma unroll 1
-  for (int delta = 0; delta < 8; delta++) {
-    if (!((alive >> delta) & 1)) continue;
-    int d = int((curd >> (4 * delta)) & 15);
-    while (d < 8) {
-      const int p = point_of(delta, d);
-      if (!((resolved >> p) & 1)) break;
-      const uint32_t st = uint32_t(status >> (2 * p)) & 3;
-      if (st != kOk) {
-        alive &= ~(1u << delta);
-        reasons += 1u << (8 * st);  // one byte per outcome, <= 8 per cell
-        break;
-      }
-      d++;
-    }
-    if (d == 8) {
-      accepted |= 1u << delta;
-      alive &= ~(1u << delta);
-      reasons += 1u;
-    }
-    curd = (curd & ~(15u << (4 * delta))) | (uint32_t(d) << (4 * delta));
-  }
-}
-
 template <bool EMIT_DUAL, bool EMIT_TRI, bool F32>
 #ifndef AMRX_MINB
 #define AMRX_MINB 4  // CTAs per SM the register budget is sized for (64 regs)
@@ -894,13 +498,6 @@ extract_kernel(const __grid_constant__ KArgs a)
     __syncthreads();
   }
 
-  for (int i = threadIdx.x; i < 72; i += kThreads) {
-    const int delta = i / 9, d0 = i % 9;
-    uint32_t m = 0;
-    for (int d = d0; d < 8; d++) m |= 1u << point_of(delta, d);
-    sm.remain[delta][d0] = m;
-  }
-  __syncthreads();
   if (lane < 8) sm.acc[warp][lane] = 0;
   if (lane < 4) sm.chunk[warp][lane] = 0;
   __syncwarp();
@@ -916,22 +513,16 @@ extract_kernel(const __grid_constant__ KArgs a)
     if (tile >= a.num_tiles) break;
     dbg_add(a.s, kDbgTiles);
 
-    // kTileCells working lanes; with sharing, lanes 0 and 31 are halo lanes
-    // holding the cells just before and after the tile (any cell of the
-    // index, even outside the extraction range)
-    const int64_t cell_s = int64_t(a.cell_begin) + int64_t(tile) * kTileCells + lane -
-                           (AMRX_SHARE ? 1 : 0);
-    const bool working = (!AMRX_SHARE || (lane >= 1 && lane <= 30)) &&
-                         cell_s < int64_t(a.cell_end);
-    const bool valid = cell_s >= 0 && uint64_t(cell_s) < a.s.n && (working || AMRX_SHARE);
-    const uint64_t cell = valid ? uint64_t(cell_s) : 0;
+    const uint64_t cell_s = a.cell_begin + uint64_t(tile) * kTileCells + lane;
+    const bool working = cell_s < a.cell_end;
+    const bool valid = working && cell_s < a.s.n;
+    const uint64_t cell = valid ? cell_s : 0;
     const uint32_t self = uint32_t(cell);
     const uint64_t kself = valid ? ldg_u64(a.s.keys + cell) : 0;
     const Cell c = unpack(a.g, kself);
     const Stencil st = make_stencil(a.g, kself, c.level);
 
     uint32_t accepted = 0, reasons = 0;
-#if AMRX_COLUMNS
     {
       Marks m{0, 0, 0, 0};
       uint32_t need = working ? kCorner0Points : 0;
@@ -1008,28 +599,6 @@ extract_kernel(const __grid_constant__ KArgs a)
         }
       }
     }
-#else
-    uint32_t resolved = 0, alive = working ? 0xffu : 0u, curd = 0;
-    uint64_t status = 0;
-    // round 0: every candidate's corner 0 ({-w,0}^3, 4 columns); round 1:
-    // everything the survivors still need
-    uint32_t need = working ? kCorner0Points : 0;
-#pragma unroll 1
-    for (int round = 0; round < 2; round++) {
-      if (round == 1) {
-        need = 0;
-#pragma unroll 1
-        for (uint32_t m = alive; m; m &= m - 1) {
-          const int delta = __ffs(m) - 1;
-          need |= sm.remain[delta][(curd >> (4 * delta)) & 15];
-        }
-        need &= ~resolved;
-      }
-      resolve_needed(a, sm, warp, lane, c, st, self, kself, valid, need, resolved, status);
-      advance(resolved, status, alive, curd, accepted, reasons);
-    }
-    if (alive) err |= 2u;
-#endif
 
     // ---- pass 1 + pass 2 fused.  No waiting on other tiles: the tile's
     // block goes to this warp's private chunk of the staging arena and
