@@ -133,6 +133,33 @@ AMRX_API amrx_status amrx_index_adopt(const void *keys_dev, const double *scalar
                              uint64_t n_cells, const int64_t *geometry16,
                              const amrx_index_opts *opts, amrx_index **out);
 
+/* ---- distributed build (dist.py): every rank holds a slice of the cell
+ * list; the global geometry is agreed first, each rank sorts its slice, the
+ * sorted runs are exchanged by key range (plus a halo), and each rank
+ * indexes the key range it received.  No reference counterpart: the
+ * reference is single-process. */
+
+/* bounds of n records: mn[3] (min anchor), mx[3] (max anchor), hi[3]
+ * (max anchor + width), level mask -- to be reduced across ranks into the
+ * global geometry words 0-9 of amrx_index_geometry's layout */
+AMRX_API amrx_status amrx_bounds(const int32_t *cells4, uint64_t n_cells,
+                                 const amrx_index_opts *opts, int64_t *bounds10);
+
+/* sort a slice under the global geometry (words 0-10 of geometry16; word 10
+ * = global cell count): sorted packed keys + scalars only, no search
+ * structure (amrx_index_device_arrays reads them) */
+AMRX_API amrx_status amrx_index_sort_part(const int32_t *cells4, const double *scalars,
+                                          uint64_t n_cells, const int64_t *geometry16,
+                                          const amrx_index_opts *opts, amrx_index **out);
+
+/* index a partition: packed keys (any order; sorted here) + scalars on this
+ * device, all inside the key range [geometry16[13], geometry16[14]); word
+ * 12 = global CellId of the partition's first key.  Every id it reports is
+ * global.  Needs unique cells and the occupancy-record geometry. */
+AMRX_API amrx_status amrx_index_from_keys(const void *keys_dev, const double *scalars_dev,
+                                          uint64_t n_cells, const int64_t *geometry16,
+                                          const amrx_index_opts *opts, amrx_index **out);
+
 /* find_exact for n cells (4 x int32 each): out_ids = CellId or -1 */
 AMRX_API amrx_status amrx_find_exact(amrx_index *index, const int32_t *cells4,
                             uint64_t n, int64_t *out_ids);

@@ -10,8 +10,9 @@ from .amrx import (  # noqa: F401
     ACCEPTED, FINER_CORNER, LOWER_KEY_CORNER, MISSING_CORNER, MAX_LEVEL,
     CapacityError, CellIndex, CudaError, DualMesh, ExtractionResult,
     ExtractionStats, InternalError, IsoParams, LoadError, UnsupportedError,
-    adopt_index, build_index, dual_bases, extract_dual_mesh,
-    extract_isosurface, find_exact, kernel_launches, library, snap, try_build_duals,
+    adopt_index, build_index, cell_bounds, dual_bases, extract_dual_mesh,
+    extract_isosurface, find_exact, index_from_keys, kernel_launches, library, snap,
+    sort_part, try_build_duals,
 )
 
 __all__ = [
@@ -19,4 +20,5 @@ __all__ = [
     "extract_isosurface", "IsoParams", "ExtractionStats", "ExtractionResult",
     "CellIndex", "DualMesh", "LoadError", "InternalError", "CapacityError",
     "UnsupportedError", "CudaError", "adopt_index", "dual_bases", "library",
+    "cell_bounds", "sort_part", "index_from_keys",
 ]

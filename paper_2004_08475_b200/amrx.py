@@ -121,6 +121,9 @@ def library():
         "amrx_index_device_arrays": [P, P, P],
         "amrx_index_geometry": [P, P],
         "amrx_index_adopt": [P, P, U64, P, P, P],
+        "amrx_bounds": [P, U64, P, P],
+        "amrx_index_sort_part": [P, P, U64, P, P, P],
+        "amrx_index_from_keys": [P, P, U64, P, P, P],
         "amrx_find_exact": [P, P, U64, P],
         "amrx_snap": [P, P, P, I32, U64, P],
         "amrx_try_build_duals": [P, P, U64, P, P],
@@ -302,6 +305,54 @@ def adopt_index(keys_dev_ptr, scalars_dev_ptr, n_cells, geometry, device=-1, str
     h = C.c_void_p()
     _check(lib.amrx_index_adopt(C.c_void_p(keys_dev_ptr), C.c_void_p(scalars_dev_ptr),
                                 n_cells, _ptr(g), C.byref(opts), C.byref(h)))
+    return CellIndex(h.value, lib)
+
+
+def _cells_arg(cells):
+    if isinstance(cells, np.ndarray) or not hasattr(cells, "data_ptr"):
+        cells = np.ascontiguousarray(np.asarray(cells, dtype=np.int32).reshape(-1, 4))
+        return cells, len(cells)
+    return cells, (cells.shape[0] if cells.numel() else 0)
+
+
+def cell_bounds(cells, device=-1, stream=None):
+    """(10,) int64: min anchor[3], max anchor[3], max anchor + width[3],
+    level mask of a slice of the cell list -- reduced across ranks into the
+    global geometry of a distributed build (dist.build_distributed)"""
+    lib = library()
+    cells, n = _cells_arg(cells)
+    out = np.zeros(10, np.int64)
+    opts = _Opts(device, C.c_void_p(stream) if stream else None, 0)
+    _check(lib.amrx_bounds(_ptr(cells) if n else C.c_void_p(1), n, C.byref(opts), _ptr(out)))
+    return out
+
+
+def sort_part(cells, scalars, geometry, device=-1, stream=None):
+    """a slice sorted under the global geometry: sorted keys + scalars only
+    (device_arrays()), no search structure"""
+    lib = library()
+    cells, n = _cells_arg(cells)
+    if isinstance(scalars, np.ndarray) or not hasattr(scalars, "data_ptr"):
+        scalars = np.ascontiguousarray(np.asarray(scalars, dtype=np.float64).reshape(-1))
+    g = np.ascontiguousarray(geometry, np.int64)
+    opts = _Opts(device, C.c_void_p(stream) if stream else None, 0)
+    h = C.c_void_p()
+    _check(lib.amrx_index_sort_part(_ptr(cells) if n else C.c_void_p(1), _ptr(scalars), n,
+                                    _ptr(g), C.byref(opts), C.byref(h)))
+    return CellIndex(h.value, lib)
+
+
+def index_from_keys(keys_dev_ptr, scalars_dev_ptr, n_cells, geometry, device=-1, stream=None):
+    """index of one partition of a distributed index: packed keys (any
+    order) + scalars on this device inside the key range geometry[13:15];
+    geometry[12] = global CellId of its first key; every id it reports is
+    global"""
+    lib = library()
+    g = np.ascontiguousarray(geometry, np.int64)
+    opts = _Opts(device, C.c_void_p(stream) if stream else None, 0)
+    h = C.c_void_p()
+    _check(lib.amrx_index_from_keys(C.c_void_p(keys_dev_ptr), C.c_void_p(scalars_dev_ptr),
+                                    n_cells, _ptr(g), C.byref(opts), C.byref(h)))
     return CellIndex(h.value, lib)
 
 

@@ -295,6 +295,12 @@ struct amrx_index {
   KeyGeom g{};
   int64_t bounds_hi[3] = {0, 0, 0};
   DevBuf keys, scal, dir, rec, lmap, order, scratch;
+  // partitions of a distributed index (amrx_index_from_keys): records of
+  // buckets [rec_lo, rec_lo + rec_n) only, global id of local position 0
+  uint64_t rec_lo = 0, rec_n = 0;
+  int64_t id_base = 0;
+  uint64_t key_lo = 0, key_hi = 0;
+  bool searchable = true;  // false: sorted arrays only (amrx_index_sort_part)
   amrx_index_info info{};
   // last extraction kept on the device for the count-then-copy pattern
   struct Cached {
@@ -317,7 +323,8 @@ struct amrx_index {
     // else the plain directory (built on demand, ensure_search_dir)
     const bool use_rec = g.occ && info.duplicate_keys == 0;
     s.dir = use_rec ? nullptr : dir.as<uint32_t>();
-    s.rec = use_rec ? rec.as<uint2>() : nullptr;
+    s.rec = use_rec ? rec.as<uint2>() - rec_lo : nullptr;
+    s.id_base = id_base;
     s.n = n;
     s.dir_shift = g.dir_shift;
     s.shift = g.shift;
@@ -466,10 +473,15 @@ void finalize_index(amrx_index *ix)
   pad_keys(ix->keys.as<uint64_t>(), ix->n, ix->stream);
   const uint64_t entries = (uint64_t(1) << ix->g.dir_bits) + 1;
   ix->order.reserve(16, ix->stream);
+  if (!ix->searchable) {
+    AMRX_CUDA(cudaMemsetAsync(ix->order.ptr, 0, 16, ix->stream));
+    return;
+  }
   if (ix->g.occ) {
-    ix->rec.reserve(entries * sizeof(uint2), ix->stream);
+    ix->rec.reserve((ix->rec_n ? ix->rec_n + 1 : entries) * sizeof(uint2), ix->stream);
     build_directory(ix->keys.as<uint64_t>(), ix->n, ix->g, nullptr, ix->rec.as<uint2>(),
-                    ix->order.as<unsigned long long>(), ix->scratch, ix->stream);
+                    ix->order.as<unsigned long long>(), ix->scratch, ix->stream,
+                    ix->rec_lo, ix->rec_n);
   } else {
     ix->dir.reserve(entries * sizeof(uint32_t), ix->stream);
     build_directory(ix->keys.as<uint64_t>(), ix->n, ix->g, ix->dir.as<uint32_t>(), nullptr,
@@ -500,11 +512,20 @@ uint64_t sorted_equal_pairs(amrx_index *ix)
     (positions are not popcounts): build the plain bucket directory too */
 void ensure_search_dir(amrx_index *ix, uint64_t equal_pairs)
 {
-  if (!ix->g.occ || equal_pairs == 0) return;
+  if (!ix->g.occ || equal_pairs == 0 || !ix->searchable) return;
+  if (ix->rec_n)
+    fail(AMRX_ERR_UNSUPPORTED, "a partition of a distributed index needs unique cells (" +
+                                 std::to_string(equal_pairs) + " duplicate keys)");
   const uint64_t entries = (uint64_t(1) << ix->g.dir_bits) + 1;
   ix->dir.reserve(entries * sizeof(uint32_t), ix->stream);
   build_directory(ix->keys.as<uint64_t>(), ix->n, ix->g, ix->dir.as<uint32_t>(), nullptr,
                   ix->order.as<unsigned long long>(), ix->scratch, ix->stream);
+}
+
+void require_searchable(const amrx_index *ix)
+{
+  if (ix && !ix->searchable)
+    fail(AMRX_ERR_INVALID_ARG, "this index holds sorted arrays only (amrx_index_sort_part)");
 }
 
 void check_range(const amrx_index *ix, const amrx_range *range, uint64_t &b,
@@ -558,11 +579,17 @@ const char *amrx_version(void) { return "amrx 0.1 (sm_100a)"; }
 
 uint64_t amrx_kernel_launches(void) { return g_launches.load(); }
 
-amrx_status amrx_index_create(const int32_t *cells4, const double *scalars,
-                              uint64_t n_cells, uint64_t n_scalars,
-                              const amrx_index_opts *opts, amrx_index **out)
+namespace {
+
+/*! build_index over n_cells records.  g16 = NULL: the geometry comes from
+    the records' own bounds; else from the global geometry words of a
+    distributed build (every record must lie inside them).  search = false:
+    stop after the sort (sorted keys + scalars only, for the exchange). */
+void create_impl(const int32_t *cells4, const double *scalars, uint64_t n_cells,
+                 uint64_t n_scalars, const amrx_index_opts *opts, const int64_t *g16,
+                 bool search, amrx_index **out)
 {
-  return guarded([&] {
+  {
     if (!out) fail(AMRX_ERR_INVALID_ARG, "out is null");
     *out = nullptr;
     // locator.cpp:29-36, same order and wording
@@ -654,10 +681,23 @@ amrx_status amrx_index_create(const int32_t *cells4, const double *scalars,
                             ") is not a multiple of the level-" +
                             std::to_string(c.w) + " cell width");
     }
-    const int64_t mn[3] = {pre.mn[0], pre.mn[1], pre.mn[2]};
-    const int64_t mx[3] = {pre.mx[0], pre.mx[1], pre.mx[2]};
-    ix->g = make_geometry(mn, mx, pre.level_mask, n);
-    for (int a = 0; a < 3; a++) ix->bounds_hi[a] = pre.hi[a];
+    ix->searchable = search;
+    if (g16) {
+      for (int a = 0; a < 3; a++)
+        if (pre.mn[a] < g16[a] || pre.mx[a] > g16[3 + a])
+          fail(AMRX_ERR_INVALID_ARG, "records outside the given geometry");
+      if ((pre.level_mask & ~uint32_t(g16[9])) != 0)
+        fail(AMRX_ERR_INVALID_ARG, "records on levels outside the given geometry");
+      const int64_t mn[3] = {g16[0], g16[1], g16[2]};
+      const int64_t mx[3] = {g16[3], g16[4], g16[5]};
+      ix->g = make_geometry(mn, mx, uint32_t(g16[9]), uint64_t(g16[10]));
+      for (int a = 0; a < 3; a++) ix->bounds_hi[a] = g16[6 + a];
+    } else {
+      const int64_t mn[3] = {pre.mn[0], pre.mn[1], pre.mn[2]};
+      const int64_t mx[3] = {pre.mx[0], pre.mx[1], pre.mx[2]};
+      ix->g = make_geometry(mn, mx, pre.level_mask, n);
+      for (int a = 0; a < 3; a++) ix->bounds_hi[a] = pre.hi[a];
+    }
 
     ix->keys.reserve((n + kKeyPad) * sizeof(uint64_t), st);
     uint32_t *idx = static_cast<uint32_t *>(l_idx.get(kWsIdx, n * 4, st));
@@ -721,6 +761,132 @@ amrx_status amrx_index_create(const int32_t *cells4, const double *scalars,
       ensure_search_dir(ix.get(), eq);
       finish_info(ix.get(), eq, ms);
     }
+    *out = ix.release();
+  }
+}
+
+}  // namespace
+
+amrx_status amrx_index_create(const int32_t *cells4, const double *scalars,
+                              uint64_t n_cells, uint64_t n_scalars,
+                              const amrx_index_opts *opts, amrx_index **out)
+{
+  return guarded([&] { create_impl(cells4, scalars, n_cells, n_scalars, opts, nullptr, true, out); });
+}
+
+amrx_status amrx_index_sort_part(const int32_t *cells4, const double *scalars,
+                                 uint64_t n_cells, const int64_t *geometry16,
+                                 const amrx_index_opts *opts, amrx_index **out)
+{
+  return guarded([&] {
+    if (!geometry16) fail(AMRX_ERR_INVALID_ARG, "null geometry");
+    create_impl(cells4, scalars, n_cells, n_cells, opts, geometry16, false, out);
+  });
+}
+
+amrx_status amrx_bounds(const int32_t *cells4, uint64_t n_cells, const amrx_index_opts *opts,
+                        int64_t *bounds10)
+{
+  return guarded([&] {
+    if (!bounds10) fail(AMRX_ERR_INVALID_ARG, "null argument");
+    if (n_cells == 0) fail(AMRX_ERR_LOAD, "dataset is empty");
+    if (!cells4) fail(AMRX_ERR_INVALID_ARG, "null input array");
+    int dev = opts && opts->device >= 0 ? opts->device : -1;
+    if (dev < 0) AMRX_CUDA(cudaGetDevice(&dev));
+    DeviceGuard dg(dev);
+    cudaStream_t st = opts && opts->stream ? static_cast<cudaStream_t>(opts->stream) : nullptr;
+    DevIn<int4> cells(reinterpret_cast<const int4 *>(cells4), n_cells, st);
+    DevBuf scratch;
+    const PrepassResult pre = ingest_prepass(cells.ptr, n_cells, scratch, st);
+    if (pre.first_bad != ~0ull)
+      fail(AMRX_ERR_LOAD, "record " + std::to_string(pre.first_bad) +
+                            ": level out of range or anchor not a multiple of the cell width");
+    for (int a = 0; a < 3; a++) {
+      bounds10[a] = pre.mn[a];
+      bounds10[3 + a] = pre.mx[a];
+      bounds10[6 + a] = pre.hi[a];
+    }
+    bounds10[9] = pre.level_mask;
+  });
+}
+
+amrx_status amrx_index_from_keys(const void *keys_dev, const double *scalars_dev,
+                                 uint64_t n_cells, const int64_t *g16,
+                                 const amrx_index_opts *opts, amrx_index **out)
+{
+  return guarded([&] {
+    if (!out || !keys_dev || !scalars_dev || !g16)
+      fail(AMRX_ERR_INVALID_ARG, "null argument");
+    *out = nullptr;
+    if (n_cells == 0) fail(AMRX_ERR_LOAD, "dataset is empty");
+    if (n_cells > uint64_t(std::numeric_limits<uint32_t>::max()))
+      fail(AMRX_ERR_LOAD, "dataset too large for 32-bit cell ids");
+    if (uint64_t(g16[14]) <= uint64_t(g16[13]))
+      fail(AMRX_ERR_INVALID_ARG, "empty key range");
+    auto ix = std::make_unique<amrx_index>();
+    setup_stream(ix.get(), opts);
+    cudaStream_t st = ix->stream;
+    const uint64_t n = n_cells;
+    ix->n = n;
+    const int64_t mn[3] = {g16[0], g16[1], g16[2]};
+    const int64_t mx[3] = {g16[3], g16[4], g16[5]};
+    ix->g = make_geometry(mn, mx, uint32_t(g16[9]), uint64_t(g16[10]));
+    for (int a = 0; a < 3; a++) ix->bounds_hi[a] = g16[6 + a];
+    if (!ix->g.occ)
+      fail(AMRX_ERR_UNSUPPORTED, "this geometry has no occupancy records: a partition "
+                                 "index needs them");
+    ix->id_base = g16[12];
+    ix->key_lo = uint64_t(g16[13]);
+    ix->key_hi = uint64_t(g16[14]);
+    ix->rec_lo = ((ix->key_lo >> ix->g.dir_shift) >> 12) << 12;
+    ix->rec_n = ((ix->key_hi - 1) >> ix->g.dir_shift) - ix->rec_lo + 1;
+    cudaEvent_t e0, e1;
+    AMRX_CUDA(cudaEventCreate(&e0));
+    AMRX_CUDA(cudaEventCreate(&e1));
+    AMRX_CUDA(cudaEventRecord(e0, st));
+    ix->keys.reserve((n + kKeyPad) * sizeof(uint64_t), st);
+    ix->scal.reserve(n * sizeof(double), st);
+    AMRX_CUDA(cudaMemcpyAsync(ix->keys.ptr, keys_dev, n * 8, cudaMemcpyDefault, st));
+    uint64_t desc = 0, eq = 0;
+    ingest_order_check(ix->keys.as<uint64_t>(), n, ix->scratch, &desc, &eq, st);
+    if (desc == 0) {
+      AMRX_CUDA(cudaMemcpyAsync(ix->scal.ptr, scalars_dev, n * 8, cudaMemcpyDefault, st));
+    } else {
+      // e.g. the sorted runs an all-to-all exchange delivers: one radix
+      // sort, the last pass gathering the scalars
+      WsLease l_idx, l_ialt, l_sort;
+      auto *idx = static_cast<uint32_t *>(l_idx.get(kWsIdx, n * 4, st));
+      fill_iota(idx, n, st);
+      DevBuf keys_alt;
+      keys_alt.reserve((n + kKeyPad) * sizeof(uint64_t), st);
+      auto *idx_alt = static_cast<uint32_t *>(l_ialt.get(kWsIdxAlt, n * 4, st));
+      void *sort_scratch = l_sort.get(kWsSort, radix_sort_scratch_bytes(n), st);
+      int passes = 0;
+      if (radix_sort_pairs(ix->keys.as<uint64_t>(), idx, keys_alt.as<uint64_t>(), idx_alt, n,
+                           ix->g.total, sort_scratch, st, &passes, scalars_dev,
+                           ix->scal.as<double>())) {
+        std::swap(ix->keys.ptr, keys_alt.ptr);
+        std::swap(ix->keys.bytes, keys_alt.bytes);
+        std::swap(ix->keys.stream, keys_alt.stream);
+      }
+    }
+    uint64_t ends[2];
+    AMRX_CUDA(cudaMemcpyAsync(&ends[0], ix->keys.as<uint64_t>(), 8, cudaMemcpyDeviceToHost, st));
+    AMRX_CUDA(cudaMemcpyAsync(&ends[1], ix->keys.as<uint64_t>() + n - 1, 8,
+                              cudaMemcpyDeviceToHost, st));
+    AMRX_CUDA(cudaStreamSynchronize(st));
+    if (ends[0] < ix->key_lo || ends[1] >= ix->key_hi)
+      fail(AMRX_ERR_INVALID_ARG, "keys outside the partition's key range");
+    finalize_index(ix.get());
+    AMRX_CUDA(cudaEventRecord(e1, st));
+    AMRX_CUDA(cudaStreamSynchronize(st));
+    float ms = 0;
+    AMRX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const uint64_t eq2 = sorted_equal_pairs(ix.get());
+    ensure_search_dir(ix.get(), eq2);
+    finish_info(ix.get(), eq2, ms);
     *out = ix.release();
   });
 }
@@ -800,7 +966,17 @@ amrx_status amrx_index_geometry(const amrx_index *index, int64_t *g16)
     g16[9] = g.level_mask;
     g16[10] = int64_t(index->n);
     g16[11] = int64_t(index->info.duplicate_keys);
-    for (int i = 12; i < 16; i++) g16[i] = 0;
+    g16[12] = index->id_base;
+    g16[13] = int64_t(index->key_lo);
+    g16[14] = int64_t(index->key_hi);
+    // key layout for partitioning: shift of the most significant coordinate
+    // field present, finest level, coarsest level, key bits
+    int major = g.lbits;
+    for (int a = 2; a >= 0; a--)
+      if (g.bits[a]) major = g.sh[a];
+    const int coarsest = g.nlevels ? g.levels[g.nlevels - 1] : g.shift;
+    g16[15] = int64_t(major) | (int64_t(g.shift) << 8) | (int64_t(coarsest) << 16) |
+              (int64_t(g.total) << 24);
   });
 }
 
@@ -852,6 +1028,7 @@ amrx_status amrx_find_exact(amrx_index *index, const int32_t *cells4,
                             uint64_t n, int64_t *out_ids)
 {
   return guarded([&] {
+    require_searchable(index);
     if (!index) fail(AMRX_ERR_INVALID_ARG, "null index");
     if (n == 0) return;
     DeviceGuard dg(index->device);
@@ -869,6 +1046,7 @@ amrx_status amrx_snap(amrx_index *index, const int64_t *points3,
                       int64_t *out_ids)
 {
   return guarded([&] {
+    require_searchable(index);
     if (!index) fail(AMRX_ERR_INVALID_ARG, "null index");
     if (n == 0) return;
     DeviceGuard dg(index->device);
@@ -887,6 +1065,7 @@ amrx_status amrx_try_build_duals(amrx_index *index, const uint64_t *tasks,
                                  uint32_t *out_corners8)
 {
   return guarded([&] {
+    require_searchable(index);
     if (!index) fail(AMRX_ERR_INVALID_ARG, "null index");
     if (n == 0) return;
     DeviceGuard dg(index->device);
@@ -906,6 +1085,7 @@ amrx_status amrx_extract_dual(amrx_index *index, const amrx_range *range,
                               uint64_t cap, uint64_t *count, amrx_stats *stats)
 {
   return guarded([&] {
+    require_searchable(index);
     if (!index || !count) fail(AMRX_ERR_INVALID_ARG, "null argument");
     std::lock_guard<std::mutex> lock(index->mu);
     DeviceGuard dg(index->device);
@@ -988,6 +1168,7 @@ amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range,
                              uint64_t cap, uint64_t *count, amrx_stats *stats)
 {
   return guarded([&] {
+    require_searchable(index);
     if (!index || !count || !params) fail(AMRX_ERR_INVALID_ARG, "null argument");
     std::lock_guard<std::mutex> lock(index->mu);
     DeviceGuard dg(index->device);

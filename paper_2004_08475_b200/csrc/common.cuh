@@ -259,8 +259,13 @@ struct SearchCtx {
   unsigned long long *dbg;  // optional event counters (AMRX_DEBUG_COUNTERS)
   // occupancy records (KeyGeom::occ), or null: set only for an index
   // without duplicate keys, where position = rec[b].x + popcount; then the
-  // plain directory `dir` is not built (null)
+  // plain directory `dir` is not built (null).  A partition's index holds
+  // the records of its key range only: `rec` is offset so rec[b] is still
+  // indexed by the global bucket (only in-range buckets are ever read)
   const uint2 *rec;
+  // global CellId of local position 0 (a partition of a distributed index;
+  // 0 otherwise): added to every id a query or an extraction reports
+  int64_t id_base;
 };
 
 /*! lookup through an occupancy record r = rec[q >> 5]: the exact key, or

@@ -654,12 +654,13 @@ extract_kernel(const __grid_constant__ KArgs a)
         const uint64_t slot = base + k;
         if (slot >= a.dual_cap) continue;
         uint32_t ids[8];
+        const uint32_t ib = uint32_t(a.s.id_base);  // global ids (partition)
 #pragma unroll
-        for (int d = 0; d < 8; d++) ids[d] = sm.id[warp][point_of(delta, d)][lane];
+        for (int d = 0; d < 8; d++) ids[d] = sm.id[warp][point_of(delta, d)][lane] + ib;
         uint4 *dst = reinterpret_cast<uint4 *>(a.corners + slot * 8);
         dst[0] = make_uint4(ids[0], ids[1], ids[2], ids[3]);
         dst[1] = make_uint4(ids[4], ids[5], ids[6], ids[7]);
-        a.tasks[slot] = cell * 8 + uint64_t(delta);
+        a.tasks[slot] = uint64_t(int64_t(cell) + a.s.id_base) * 8 + uint64_t(delta);
       }
     }
     if (EMIT_TRI) {
@@ -755,7 +756,7 @@ find_exact_kernel(const SearchCtx s, const KeyGeom g,
            query_key(g, cc.x, cc.y, cc.z, cc.w, q[0]);
     int l1[1];
     warp_find<1, false>(s, q, v, o, l1, win[warp]);
-    if (in) out[r] = v[0] ? o[0] : -1;
+    if (in) out[r] = v[0] && o[0] >= 0 ? o[0] + s.id_base : -1;
   }
 }
 
@@ -775,7 +776,7 @@ snap_kernel(const SearchCtx s, const KeyGeom g,
                   pz = in ? points[3 * r + 2] : 0;
     const int32_t h = in ? (hints ? hints[r] : hint_all) : -1;
     const int64_t res = warp_snap(s, g, in, px, py, pz, h, win[warp]);
-    if (in) out[r] = res;
+    if (in) out[r] = res >= 0 ? res + s.id_base : -1;
   }
 }
 
@@ -793,7 +794,7 @@ try_build_kernel(const SearchCtx s, const KeyGeom g,
     const uint64_t r = base + (threadIdx.x & 31);
     bool live = r < n;
     const uint64_t task = live ? tasks[r] : 0;
-    const uint64_t cell = task >> 3;
+    const uint64_t cell = uint64_t(int64_t(task >> 3) - s.id_base);  // local position
     const int delta = int(task & 7);
     live = live && cell < s.n;
     const Cell c = unpack(g, live ? ldg_u64(s.keys + cell) : 0);
@@ -829,7 +830,8 @@ try_build_kernel(const SearchCtx s, const KeyGeom g,
     if (r < n) {
       reject[r] = uint8_t(code);
       if (corners)
-        for (int d = 0; d < 8; d++) corners[8 * r + d] = code == 0 ? ids[d] : 0;
+        for (int d = 0; d < 8; d++)
+          corners[8 * r + d] = code == 0 ? ids[d] + uint32_t(s.id_base) : 0;
     }
   }
 }

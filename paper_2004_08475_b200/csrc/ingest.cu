@@ -162,6 +162,14 @@ scatter_kernel(const uint32_t *__restrict__ rank, const double *__restrict__ in,
   }
 }
 
+__global__ void __launch_bounds__(kThreads)
+iota_kernel(uint32_t *__restrict__ p, uint64_t n)
+{
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n; r += stride)
+    p[r] = uint32_t(r);
+}
+
 __global__ void pad_kernel(uint64_t *keys, uint64_t n)
 {
   keys[n + threadIdx.x] = ~0ull;
@@ -373,15 +381,19 @@ constexpr int kRecTileLog = 12;
 constexpr int kRecTile = 1 << kRecTileLog;
 constexpr int kRecThreads = 512;
 
-/// tile_start[t] = first position whose bucket >= t * kRecTile, t in [0, tiles]
+/// tile_start[t] = first position whose bucket >= rec_lo + t * kRecTile,
+/// t in [0, tiles]; rec_lo is a multiple of kRecTile and no key lies below it
 __global__ void __launch_bounds__(kThreads)
-rec_tile_start_kernel(const uint64_t *__restrict__ keys, uint64_t n, int shift,
-                      uint64_t tiles, uint32_t *__restrict__ tile_start)
+rec_tile_start_kernel(const uint64_t *__restrict__ keys, uint64_t n, int dir_shift,
+                      uint64_t rec_lo, uint64_t tiles, uint32_t *__restrict__ tile_start)
 {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  const auto tile_of = [&](uint64_t i) {
+    return std::min<uint64_t>(((ldg_u64(keys + i) >> dir_shift) - rec_lo) >> kRecTileLog, tiles);
+  };
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i <= n; i += stride) {
-    const uint64_t cur = i < n ? std::min<uint64_t>(ldg_u64(keys + i) >> shift, tiles) : tiles;
-    const uint64_t from = i > 0 ? (ldg_u64(keys + i - 1) >> shift) + 1 : 0;
+    const uint64_t cur = i < n ? tile_of(i) : tiles;
+    const uint64_t from = i > 0 ? tile_of(i - 1) + 1 : 0;
     for (uint64_t t = from; t <= cur; t++) tile_start[t] = uint32_t(i);
   }
 }
@@ -461,7 +473,7 @@ rec_build_kernel(const uint64_t *__restrict__ keys, uint64_t n, int dir_shift,
     run += c[j];
   }
   __syncthreads();
-  const uint64_t r0 = t << kRecTileLog;
+  const uint64_t r0 = t << kRecTileLog;  // records are relative to rec_lo
   for (int j = threadIdx.x; j < kRecTile; j += kRecThreads)  // coalesced
     if (r0 + j < entries) rec[r0 + j] = make_uint2(cnt[j], bits[j]);
 #pragma unroll
@@ -570,6 +582,13 @@ void scatter_f64(const uint32_t *rank, const double *in, double *out, uint64_t n
   AMRX_LAUNCH_CHECK();
 }
 
+void fill_iota(uint32_t *p, uint64_t n, cudaStream_t st)
+{
+  if (n == 0) return;
+  iota_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(p, n);
+  AMRX_LAUNCH_CHECK();
+}
+
 void pad_keys(uint64_t *keys, uint64_t n, cudaStream_t st)
 {
   pad_kernel<<<1, kKeyPad, 0, st>>>(keys, n);
@@ -578,16 +597,17 @@ void pad_keys(uint64_t *keys, uint64_t n, cudaStream_t st)
 
 void build_directory(const uint64_t *keys, uint64_t n, const KeyGeom &g,
                      uint32_t *dir, uint2 *rec, unsigned long long *order2,
-                     DevBuf &scratch, cudaStream_t st)
+                     DevBuf &scratch, cudaStream_t st, uint64_t rec_lo, uint64_t rec_n)
 {
-  const uint64_t entries = (uint64_t(1) << g.dir_bits) + 1;
+  uint64_t entries = (uint64_t(1) << g.dir_bits) + 1;
   AMRX_CUDA(cudaMemsetAsync(order2, 0, 16, st));
   if (rec) {
+    if (rec_n) entries = rec_n + 1;
     const uint64_t tiles = (entries + kRecTile - 1) / kRecTile;
     DevBuf starts;
     starts.reserve(size_t(tiles + 1) * sizeof(uint32_t), st);
     rec_tile_start_kernel<<<grid_for(n + 1, kThreads, 4), kThreads, 0, st>>>(
-      keys, n, g.dir_shift + kRecTileLog, tiles, starts.as<uint32_t>());
+      keys, n, g.dir_shift, rec_lo, tiles, starts.as<uint32_t>());
     AMRX_LAUNCH_CHECK();
     rec_build_kernel<<<unsigned(tiles), kRecThreads, 0, st>>>(
       keys, n, g.dir_shift, entries, starts.as<uint32_t>(), rec, order2);

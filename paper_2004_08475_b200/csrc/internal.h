@@ -121,16 +121,21 @@ void ingest_order_check(const uint64_t *keys, uint64_t n, DevBuf &scratch,
 void gather_f64(const uint32_t *perm, const double *in, double *out,
                 uint64_t n, cudaStream_t st);
 
+/// p[i] = i for i in [0, n)
+void fill_iota(uint32_t *p, uint64_t n, cudaStream_t st);
+
 /// fill kKeyPad sentinels (all ones) after the n sorted keys
 void pad_keys(uint64_t *keys, uint64_t n, cudaStream_t st);
 
 /// dir[b] = first position whose key >> g.dir_shift >= b, b in [0, 2^D];
-/// or, with rec (2^D + 1 records; g.occ geometry) instead, the occupancy
-/// records (dir unused); order2 (device, 2 x u64) receives the keys'
-/// descents and equal pairs
+/// or, with rec (g.occ geometry) instead, the occupancy records (dir
+/// unused): rec[b - rec_lo] for buckets b in [rec_lo, rec_lo + rec_n] (all
+/// 2^D + 1 when rec_n = 0; rec_lo a multiple of 4096, no key below it);
+/// order2 (device, 2 x u64) receives the keys' descents and equal pairs
 void build_directory(const uint64_t *keys, uint64_t n, const KeyGeom &g,
                      uint32_t *dir, uint2 *rec, unsigned long long *order2,
-                     DevBuf &scratch, cudaStream_t st);
+                     DevBuf &scratch, cudaStream_t st, uint64_t rec_lo = 0,
+                     uint64_t rec_n = 0);
 
 /// block level map (KeyGeom::map_*): fill map (map bytes, zeroed here)
 void build_level_map(const uint64_t *keys, uint64_t n, const KeyGeom &g,

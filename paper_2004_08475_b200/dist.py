@@ -86,6 +86,226 @@ def partitioned(n, extract_range, group=None, device=None):
                              counters)
 
 
+# ---------------------------------------------------------------------------
+# Distributed build (every rank holds a slice of the cell list).  The plan is
+# pure integer arithmetic over packed keys, so tests run it over gloo on CPU.
+
+def geometry_layout(geometry):
+    """(major_shift, finest, coarsest, key_bits) from geometry word 15"""
+    w = int(geometry[15])
+    return w & 0xFF, (w >> 8) & 0xFF, (w >> 16) & 0xFF, (w >> 24) & 0xFF
+
+
+def choose_splitters(samples, world):
+    """world-1 strictly increasing key boundaries from the sorted union of
+    every rank's evenly spaced samples; rank q owns keys [s_q, s_q+1) with
+    s_0 = 0 and s_world = 2^63"""
+    import torch
+    smp = torch.sort(samples.reshape(-1)).values
+    cut = [smp[(len(smp) * q) // world] for q in range(1, world)]
+    out = [0]
+    for c in cut:
+        out.append(max(int(c), out[-1] + 1))
+    out.append(1 << 63)
+    return out
+
+
+def halo_ranges(bounds, geometry):
+    """key range each rank must hold to extract its owned range exactly:
+    its owned keys plus every key whose major coordinate (the most
+    significant field of the key, i unless that axis is constant) lies
+    within two coarsest cell widths -- a stencil point is within one owner
+    width of its cell, and a cell containing it within one coarsest width
+    of the point"""
+    msh, finest, coarsest, bits = geometry_layout(geometry)
+    hw = 2 << (coarsest - finest)  # two coarsest widths in packed units
+    top = 1 << bits
+    world = len(bounds) - 1
+    lo, hi = [], []
+    for q in range(world):
+        a, b = bounds[q], min(bounds[q + 1], top)
+        if b <= a:
+            lo.append(a)
+            hi.append(a)
+            continue
+        lo.append(max(0, (a >> msh) - hw) << msh)
+        hi.append(min(top, ((b - 1) >> msh) + hw + 1 << msh))
+    return lo, hi
+
+
+def send_plan(sorted_keys, lo, hi):
+    """(start, count) of the sorted local keys each rank needs"""
+    import torch
+    bl = torch.tensor(lo, dtype=sorted_keys.dtype, device=sorted_keys.device)
+    bh = torch.tensor(hi, dtype=sorted_keys.dtype, device=sorted_keys.device)
+    a = torch.searchsorted(sorted_keys, bl)
+    b = torch.searchsorted(sorted_keys, bh)
+    return a.tolist(), (b - a).tolist()
+
+
+def global_geometry(bounds10, counts):
+    """geometry words 0-10 from every rank's amrx_bounds output + count"""
+    b = np.asarray(bounds10, np.int64).reshape(-1, 10)
+    g = np.zeros(16, np.int64)
+    g[0:3] = b[:, 0:3].min(0)
+    g[3:9] = b[:, 3:9].max(0)
+    m = 0
+    for x in b[:, 9]:
+        m |= int(x)
+    g[9] = m
+    g[10] = int(np.sum(np.asarray(counts, np.int64)))
+    return g
+
+
+def owned_split(rkeys, bounds, rank):
+    """(keys below the owned range, keys in it) among a rank's received keys"""
+    s_r, s_r1 = bounds[rank], bounds[rank + 1]
+    below = int((rkeys < s_r).sum().item())
+    inside = rkeys >= s_r
+    if s_r1 < (1 << 63):
+        inside &= rkeys < s_r1
+    return below, int(inside.sum().item())
+
+
+def exchange_runs(keys, scal, lo, hi, group=None, device=None):
+    """send every rank the slice of my sorted (keys, scalars) inside its
+    [lo, hi) (halos overlap, so some keys go to two ranks); returns what I
+    received: `world` sorted runs, concatenated in rank order"""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    start, count = send_plan(keys, lo, hi)
+    send = torch.cat([torch.stack([keys[a:a + c], scal[a:a + c].view(torch.int64)], 1)
+                      for a, c in zip(start, count)])
+    rc = torch.empty(world, dtype=torch.int64, device=device)
+    dist.all_to_all_single(rc, torch.tensor(count, dtype=torch.int64, device=device),
+                           group=group)
+    rcount = rc.tolist()
+    recv = torch.empty((sum(rcount), 2), dtype=torch.int64, device=device)
+    dist.all_to_all_single(recv, send, output_split_sizes=rcount, input_split_sizes=count,
+                           group=group)
+    return recv[:, 0].contiguous(), recv[:, 1].contiguous().view(torch.float64)
+
+
+@dataclass
+class DistributedIndex:
+    index: object        # this rank's partition (CellIndex), global ids
+    owned: tuple         # local position range of the cells this rank owns
+    id_base: int         # global CellId of local position 0
+    total: int           # global cell count
+    seconds: dict        # host wall time per phase
+
+
+def sorted_arrays(index, device):
+    """torch copies of an index's sorted packed keys (int64) and scalars"""
+    import torch
+    n = len(index)
+    kp, sp = index.device_arrays()
+    keys = torch.empty(n, dtype=torch.int64, device=device)
+    scal = torch.empty(n, dtype=torch.float64, device=device)
+    rt = _cudart()
+    torch.cuda.synchronize(device)
+    if rt.cudaMemcpy(C.c_void_p(keys.data_ptr()), C.c_void_p(kp), n * 8, 3) or \
+            rt.cudaMemcpy(C.c_void_p(scal.data_ptr()), C.c_void_p(sp), n * 8, 3):
+        raise RuntimeError("device copy failed")
+    return keys, scal
+
+
+def build_distributed(cells, scalars, group=None, device=None, stream=None, samples=4096):
+    """Distributed build_index: rank r holds a slice (cells, scalars) of the
+    global cell list.  (1) bounds all-reduced into the global key geometry;
+    (2) each rank radix-sorts its slice (amrx_index_sort_part); (3) sampled
+    splitters give every rank a contiguous owned key range, widened by a
+    halo of two coarsest cell widths; (4) one all-to-all moves each sorted
+    run to the ranks whose ranges cover it; (5) each rank sorts what it
+    received and indexes it (amrx_index_from_keys) with the global id of its
+    first key.  Extracting the owned range then reproduces exactly the
+    single-GPU slice of the output (candidate order is owner-cell major)."""
+    import time
+    import torch
+    import torch.distributed as dist
+    from . import amrx as P
+    t0 = time.perf_counter()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    sh = stream.cuda_stream if stream is not None and hasattr(stream, "cuda_stream") else stream
+    n_loc = cells.shape[0]
+    b = torch.tensor(np.append(P.cell_bounds(cells, device=dev.index, stream=sh), n_loc),
+                     dtype=torch.int64, device=dev)
+    everyone = [torch.empty_like(b) for _ in range(world)]
+    dist.all_gather(everyone, b, group=group)
+    allb = torch.stack(everyone).cpu().numpy()
+    g = global_geometry(allb[:, :10], allb[:, 10])
+    n = int(g[10])
+    t1 = time.perf_counter()
+    part = P.sort_part(cells, scalars, g, device=dev.index, stream=sh)
+    g = part.geometry()
+    g[10] = n
+    if geometry_layout(g)[3] > 63:
+        raise P.UnsupportedError("distributed build needs keys of at most 63 bits")
+    keys, scal = sorted_arrays(part, dev)
+    part.close()
+    t2 = time.perf_counter()
+    # splitters from evenly spaced samples of every rank's sorted slice
+    pos = torch.linspace(0, max(n_loc - 1, 0), samples, device=dev).round().long()
+    smp = keys[pos] if n_loc else torch.zeros(samples, dtype=torch.int64, device=dev)
+    gathered = [torch.empty_like(smp) for _ in range(world)]
+    dist.all_gather(gathered, smp, group=group)
+    bounds = choose_splitters(torch.cat(gathered), world)
+    lo, hi = halo_ranges(bounds, g)
+    rkeys, rscal = exchange_runs(keys, scal, lo, hi, group, dev)
+    del keys, scal
+    t3 = time.perf_counter()
+    below, own = owned_split(rkeys, bounds, rank)
+    owns = allgather_counts(own, group, dev)
+    id_base = int(sum(owns[:rank])) - below
+    g[12], g[13], g[14] = id_base, lo[rank], hi[rank]
+    index = None
+    if len(rkeys) and own:
+        index = P.index_from_keys(rkeys.data_ptr(), rscal.data_ptr(), len(rkeys), g,
+                                  device=dev.index, stream=sh)
+    t4 = time.perf_counter()
+    return DistributedIndex(index, (below, below + own), id_base, n,
+                            {"geometry": t1 - t0, "sort": t2 - t1, "exchange": t3 - t2,
+                             "index": t4 - t3})
+
+
+def extract_isosurface_distributed(dindex, params, group=None, out=None, device=None):
+    """this rank's slice of extract_isosurface over a distributed index"""
+    from . import amrx as P
+
+    def run(lo, hi):
+        if dindex.index is None or hi <= lo:
+            return np.zeros((0, 9)), P.ExtractionStats()
+        r = P.extract_isosurface(dindex.index, params, cell_range=(lo, hi), out=out)
+        return r.fat, r.stats
+
+    return partitioned_range(dindex.owned, run, group, device)
+
+
+def extract_dual_mesh_distributed(dindex, group=None, device=None):
+    """this rank's slice of extract_dual_mesh (global CellIds)"""
+    from . import amrx as P
+
+    def run(lo, hi):
+        d = P.extract_dual_mesh(dindex.index, cell_range=(lo, hi))
+        return d, d.stats
+
+    return partitioned_range(dindex.owned, run, group, device)
+
+
+def partitioned_range(owned, extract_range, group=None, device=None):
+    """partitioned() for an explicit owned range of local positions"""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    items, stats = extract_range(*owned)
+    counts = allgather_counts(len(items), group, device)
+    off = exclusive_offsets(counts)
+    counters = allreduce_counters(stats, group, device)
+    return PartitionedResult(items, int(off[rank]), int(off[-1]), counts, owned, stats,
+                             counters)
+
+
 def _cudart():
     for name in ("libcudart.so.12", "libcudart.so"):
         try:
