@@ -170,15 +170,29 @@ def run_amrx(args):
 
     from paper_2004_08475_b200 import dist as D
 
+    # each rank holds a slice of the (shuffled) cell list
+    lo_c, hi_c = n * rank // max(world, 1), n * (rank + 1) // max(world, 1)
+    my_cells, my_scal = cells[lo_c:hi_c], scal[lo_c:hi_c]
+
     def step_multi():
-        # rank 0 sorts; NCCL broadcast of the sorted keys + scalars; each
-        # rank adopts them and extracts its own contiguous cell range; an
+        if args.dist_mode == "replicate":
+            # rank 0 sorts; NCCL broadcast of the sorted keys + scalars; each
+            # rank adopts them and extracts its own contiguous cell range
+            ix = D.replicate_index(cells if rank == 0 else None,
+                                   scal if rank == 0 else None, device=dev, stream=sh)
+            ingest = ix.info.seconds_ingest
+            res = D.extract_isosurface_partitioned(ix, P.IsoParams(iso=iso), out=out,
+                                                   device=dev)
+            ix.close()
+            return res.stats, ingest, res.total
+        # distributed build: slice sort, sampled splitters, all-to-all by
+        # key range (+ halo), partition index; owned-range extraction; an
         # all-gather of per-rank counts gives the global offsets
-        ix = D.replicate_index(cells if rank == 0 else None, scal if rank == 0 else None,
-                               device=dev, stream=sh)
-        ingest = ix.info.seconds_ingest
-        res = D.extract_isosurface_partitioned(ix, P.IsoParams(iso=iso), out=out, device=dev)
-        ix.close()
+        di = D.build_distributed(my_cells, my_scal, device=dev, stream=sh)
+        ingest = di.index.info.seconds_ingest if di.index is not None else 0.0
+        res = D.extract_isosurface_distributed(di, P.IsoParams(iso=iso), out=out, device=dev)
+        if di.index is not None:
+            di.index.close()
         return res.stats, ingest, res.total
 
     step = step_multi if (world > 1 or args.force_dist) else step_single
@@ -220,6 +234,43 @@ def run_amrx(args):
 
     # ---- e2e through the same public call with pinned host buffers
     e2e = None
+    if world > 1 and not args.no_e2e:
+        # every rank's slice from pinned host memory, its part of the soup
+        # into pinned host memory
+        hcells = torch.empty(my_cells.shape, dtype=torch.int32, pin_memory=True)
+        hscal = torch.empty(my_scal.shape, dtype=torch.float64, pin_memory=True)
+        hcells.copy_(my_cells)
+        hscal.copy_(my_scal)
+        hout = torch.empty((int(cap * 1.5 / world) + 4096, 9), dtype=torch.float64,
+                           pin_memory=True)
+
+        def step_e2e_multi():
+            di = D.build_distributed(hcells, hscal, device=dev, stream=sh)
+            res = D.extract_isosurface_distributed(di, P.IsoParams(iso=iso), out=hout,
+                                                   device=dev)
+            if di.index is not None:
+                di.index.close()
+            return res.total, len(res.fat)
+
+        step_e2e_multi()
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        k2 = max(1, min(args.steps, 3))
+        mine = 0
+        for _ in range(k2):
+            nt, mine = step_e2e_multi()
+        torch.cuda.synchronize()
+        dist.barrier()
+        ms_e2e = 1000 * (time.perf_counter() - t0) / k2
+        mt = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(mt, op=dist.ReduceOp.MAX)
+        ms_e2e = float(mt.item())
+        e2e = {"value": duals_full / (ms_e2e / 1000.0), "unit": "dual cells/s",
+               "ms_per_step": ms_e2e, "triangles_per_s": nt / (ms_e2e / 1000.0),
+               "h2d_bytes_per_step": int(n * 24), "d2h_bytes_per_step": int(nt * 72),
+               "note": "every rank uploads its slice and downloads its part; bytes are job totals"}
+        del hcells, hscal, hout
     if world == 1 and not args.no_e2e:
         hcells = torch.empty(cells.shape, dtype=torch.int32, pin_memory=True)
         hscal = torch.empty(scal.shape, dtype=torch.float64, pin_memory=True)
@@ -285,7 +336,7 @@ def run_amrx(args):
         "data": "synthetic (GPU generator: vortex-tube brick AMR, bijective-hash soup order)",
         "config": {"workload": f"{args.config}: {n} cells, levels 0-3, iso {iso}",
                    "cells": n, "triangles": tris, "duals": duals_full, "iso": iso,
-                   "parallelism": f"range-partition x{world}" if world > 1 else "single GPU",
+                   "parallelism": (f"distributed sort + range partition x{world}" if args.dist_mode == "partition" else f"rank-0 sort + broadcast x{world}") if world > 1 else "single GPU",
                    "l2": "inputs (24 B/cell) far larger than L2", **meta},
         "iso_triangles_per_s": tris / (ms / 1000.0),
         "paper_split_ms": {"X_extract_kernel": kern_ms, "ingest_sort": 1000 * statistics.mean(ingest_s),
@@ -405,6 +456,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=12_000_000)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-mode", default="partition", choices=["partition", "replicate"],
+                    help="multi-GPU build: distributed sort + exchange, or rank-0 sort + broadcast")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the multi-GPU code path even at world size 1 (testing)")
     args = ap.parse_args()
