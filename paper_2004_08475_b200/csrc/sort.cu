@@ -97,6 +97,8 @@ struct PassSmem {
   uint32_t vals[kSortTile];
   uint32_t whist[kSortWarps][kDigits];  // per-warp counts -> warp offsets
   uint32_t bexcl[kDigits];              // tile-local digit start
+  uint32_t hist[kDigits];               // tile digit counts (early publish)
+  uint32_t wsum[kSortWarps];            // block scan: per-warp totals
   unsigned long long gofs[kDigits];     // global start of this tile's run
   uint32_t tile;
 };
@@ -126,6 +128,7 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
   if (threadIdx.x == 0) sm.tile = atomicAdd(ticket, 1u);
   for (int i = threadIdx.x; i < kSortWarps * kDigits; i += kSortThreads)
     (&sm.whist[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < kDigits; i += kSortThreads) sm.hist[i] = 0;
   __syncthreads();
   const uint32_t tile = sm.tile;
   const uint64_t base = uint64_t(tile) * kSortTile;
@@ -144,6 +147,15 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
     v[t] = in ? __ldg(vals_in + r) : 0u;
     dig[t] = in ? uint32_t((k[t] >> shift) & (kDigits - 1)) : uint32_t(kDigits);
   }
+  // the tile's digit counts by shared atomics, published right away so the
+  // successors' look-back finds this tile's aggregate while it still ranks
+#pragma unroll
+  for (int t = 0; t < kSortItems; t++)
+    if (dig[t] < kDigits) atomicAdd(&sm.hist[dig[t]], 1u);
+  __syncthreads();
+  const bool digit_thread = threadIdx.x < kDigits;
+  unsigned long long *me = state + uint64_t(tile) * kDigits + threadIdx.x;
+  if (digit_thread) st_relaxed(me, (tile == 0 ? kFlagPre : kFlagAgg) | sm.hist[threadIdx.x]);
   // warp multisplit: rank within (warp, digit) in input order
   const uint32_t lt = lanemask_lt();
 #pragma unroll
@@ -169,34 +181,37 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
       total += c;
     }
   }
-  // tile-local digit starts (exclusive scan of totals over 256 digits)
-  if (threadIdx.x < kDigits) sm.bexcl[threadIdx.x] = total;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t run = 0;
-    for (int b = 0; b < kDigits; b += 32) {
-      const uint32_t c = sm.bexcl[b + lane];
-      uint32_t x = c;
+  // tile-local digit starts: block-wide exclusive scan of the totals, one
+  // digit per thread (warp scans + a scan of the warp sums)
+  {
+    uint32_t x = total;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, off);
+      if (lane >= off) x += y;
+    }
+    if (lane == 31) sm.wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t w = lane < kSortWarps ? sm.wsum[lane] : 0u;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, x, off);
-        if (lane >= off) x += y;
+        const uint32_t y = __shfl_up_sync(kFull, w, off);
+        if (lane >= off) w += y;
       }
-      sm.bexcl[b + lane] = run + x - c;
-      run += __shfl_sync(kFull, x, 31);
+      if (lane < kSortWarps) sm.wsum[lane] = w;
     }
+    __syncthreads();
+    if (digit_thread)
+      sm.bexcl[threadIdx.x] = x - total + (warp ? sm.wsum[warp - 1] : 0u);
   }
 
-  // decoupled look-back per digit: publish the aggregate, sum the
-  // predecessors' until an inclusive prefix appears, publish ours
-  if (threadIdx.x < kDigits) {
+  // decoupled look-back per digit (the aggregate went out before the
+  // ranking): sum the predecessors' until an inclusive prefix appears
+  if (digit_thread) {
     const int d = threadIdx.x;
-    unsigned long long *me = state + uint64_t(tile) * kDigits + d;
     unsigned long long excl = 0;
-    if (tile == 0) {
-      st_relaxed(me, kFlagPre | total);
-    } else {
-      st_relaxed(me, kFlagAgg | total);
+    if (tile != 0) {
       int64_t j = int64_t(tile) - 1;
       while (true) {
         unsigned long long s;
