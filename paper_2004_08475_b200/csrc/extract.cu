@@ -244,7 +244,7 @@ __device__ __noinline__ int mc_dual(const KArgs &a, const Smem &sm, int warp, in
     val[d] = __ldg(a.scal + ids[d]);
     if (val[d] > iso) mask |= 1 << d;
   }
-  const uint64_t word = sm.mc_rows[table_row(uint32_t(mask))];
+  const uint64_t word = sm.mc_rows[mask];  // rows pre-permuted by corner mask
   const int ntab = int(word & 15);
   if (ntab == 0) return 0;
 
@@ -494,7 +494,10 @@ extract_kernel(const __grid_constant__ KArgs a)
   Smem &sm = *reinterpret_cast<Smem *>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (EMIT_TRI) {
-    for (int i = threadIdx.x; i < 256; i += kThreads) sm.mc_rows[i] = c_mc_rows[i];
+    // indexed by the slot-numbered corner mask directly (table_row applied
+    // once here instead of per dual)
+    for (int i = threadIdx.x; i < 256; i += kThreads)
+      sm.mc_rows[i] = c_mc_rows[table_row(uint32_t(i))];
     __syncthreads();
   }
 
@@ -620,7 +623,7 @@ extract_kernel(const __grid_constant__ KArgs a)
         }
         if (mask != 0 && mask != 0xffu) {
           cross |= 1u << delta;
-          upper += uint32_t(sm.mc_rows[table_row(mask)] & 15);
+          upper += uint32_t(sm.mc_rows[mask] & 15);
         }
       }
     }
