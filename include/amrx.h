@@ -209,6 +209,17 @@ AMRX_API amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range
                              uint64_t cap, uint64_t *count,
                              amrx_stats *stats);
 
+/* weld (proj/src/weld.cpp:31-64, replaces amriso::weld): merge bitwise-
+ * identical corner positions of n_tris fat triangles (9 FP64 each, host or
+ * device) into shared vertices, position-sorted like the reference.
+ * verts3 gets 3 FP64 per vertex (capacity vcap vertices; vcap = 3 * n_tris
+ * always suffices), tris3 3 vertex ids per triangle; *n_verts the vertex
+ * count.  AMRX_ERR_LENGTH when n_tris > UINT32_MAX/3 (weld.cpp:36-37);
+ * AMRX_ERR_CAPACITY when vcap is too small (*n_verts = the need). */
+AMRX_API amrx_status amrx_weld(const double *xyz9, uint64_t n_tris, double *verts3,
+                               uint64_t vcap, uint32_t *tris3, uint64_t *n_verts,
+                               const amrx_index_opts *opts);
+
 /* kernels this process has launched through the library so far */
 AMRX_API uint64_t amrx_kernel_launches(void);
 

@@ -124,6 +124,7 @@ def library():
         "amrx_bounds": [P, U64, P, P],
         "amrx_index_sort_part": [P, P, U64, P, P, P],
         "amrx_index_from_keys": [P, P, U64, P, P, P],
+        "amrx_weld": [P, U64, P, U64, P, P, P],
         "amrx_find_exact": [P, P, U64, P],
         "amrx_snap": [P, P, P, I32, U64, P],
         "amrx_try_build_duals": [P, P, U64, P, P],
@@ -354,6 +355,33 @@ def index_from_keys(keys_dev_ptr, scalars_dev_ptr, n_cells, geometry, device=-1,
     _check(lib.amrx_index_from_keys(C.c_void_p(keys_dev_ptr), C.c_void_p(scalars_dev_ptr),
                                     n_cells, _ptr(g), C.byref(opts), C.byref(h)))
     return CellIndex(h.value, lib)
+
+
+@dataclass
+class IndexedMesh:
+    """IndexedMesh (weld.hpp:28-31): shared vertices + triangle indices"""
+    vertices: object   # (V, 3) float64, position-sorted
+    triangles: object  # (T, 3) uint32
+
+
+def weld(triangles, device=-1, stream=None):
+    """weld (weld.cpp:31-64) on the GPU: merge bitwise-identical corner
+    positions of a fat triangle soup ((T, 9) float64, numpy or torch host or
+    CUDA) into an IndexedMesh with the reference's vertex order."""
+    lib = library()
+    if isinstance(triangles, np.ndarray) or not hasattr(triangles, "data_ptr"):
+        tri = np.ascontiguousarray(np.asarray(triangles, np.float64).reshape(-1, 9))
+        n = len(tri)
+    else:
+        tri = triangles.contiguous()
+        n = tri.shape[0] if tri.numel() else 0
+    verts = np.empty((3 * n, 3), np.float64)
+    idx = np.empty((n, 3), np.uint32)
+    nv = C.c_uint64()
+    opts = _Opts(device, C.c_void_p(stream) if stream else None, 0)
+    _check(lib.amrx_weld(_ptr(tri) if n else None, n, _ptr(verts), 3 * n, _ptr(idx),
+                         C.byref(nv), C.byref(opts)))
+    return IndexedMesh(verts[: nv.value].copy(), idx)
 
 
 def find_exact(index: CellIndex, coords):

@@ -891,6 +891,38 @@ amrx_status amrx_index_from_keys(const void *keys_dev, const double *scalars_dev
   });
 }
 
+amrx_status amrx_weld(const double *xyz9, uint64_t n_tris, double *verts3, uint64_t vcap,
+                      uint32_t *tris3, uint64_t *n_verts, const amrx_index_opts *opts)
+{
+  return guarded([&] {
+    if (!n_verts) fail(AMRX_ERR_INVALID_ARG, "null argument");
+    *n_verts = 0;
+    if (n_tris == 0) return;
+    if (!xyz9) fail(AMRX_ERR_INVALID_ARG, "null input array");
+    if (n_tris > uint64_t(std::numeric_limits<uint32_t>::max()) / 3)
+      fail(AMRX_ERR_LENGTH, "weld: too many triangles for 32-bit indices");
+    int dev = opts && opts->device >= 0 ? opts->device : -1;
+    if (dev < 0) AMRX_CUDA(cudaGetDevice(&dev));
+    DeviceGuard dg(dev);
+    enable_pool_caching(dev);
+    cudaStream_t st = opts && opts->stream ? static_cast<cudaStream_t>(opts->stream) : nullptr;
+    DevIn<double> in(xyz9, n_tris * 9, st);
+    DevOut<uint32_t> tris(tris3, tris3 ? n_tris * 3 : 0, st);
+    // vertices: device output in place, else a device buffer of the bound
+    const uint64_t vbound = std::min<uint64_t>(vcap, 3 * n_tris);
+    DevOut<double> verts(verts3, verts3 ? vbound * 3 : 0, st);
+    const uint64_t nv = run_weld(in.ptr, n_tris, verts.ptr, verts3 ? vbound : 0, tris.ptr, st);
+    *n_verts = nv;
+    if (verts3 && nv > vcap)
+      fail(AMRX_ERR_CAPACITY, "vertex capacity " + std::to_string(vcap) + " < " +
+                                std::to_string(nv) + " vertices");
+    if (verts3 && verts.staged)
+      AMRX_CUDA(cudaMemcpyAsync(verts3, verts.ptr, nv * 24, cudaMemcpyDeviceToHost, st));
+    tris.finish(st);
+    AMRX_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
 amrx_status amrx_index_destroy(amrx_index *index)
 {
   return guarded([&] {

@@ -225,4 +225,10 @@ void run_try_build(const SearchCtx &s, const KeyGeom &g, const uint64_t *tasks,
 
 int device_sm_count();
 
+// ------------------------------------------------------------- weld.cu
+/// weld n_tris fat triangles (device xyz9); verts (vcap) / tris (3 per
+/// triangle) may be null; returns the vertex count
+uint64_t run_weld(const double *xyz9, uint64_t n_tris, double *verts, uint64_t vcap,
+                  uint32_t *tris, cudaStream_t st);
+
 }  // namespace amrx

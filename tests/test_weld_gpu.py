@@ -1,0 +1,87 @@
+"""GPU weld (amrx_weld, csrc/weld.cu) against the reference's weld
+(proj/src/weld.cpp:31-64): the restatement (oracle/amrx_oracle.c orc_weld)
+and, where it was built, the reference library itself.  Bit-exact vertex
+arrays (position-sorted) and identical triangle indices."""
+import os
+
+import numpy as np
+import pytest
+
+import oracles
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _cases():
+    z = np.load(os.path.join(HERE, "golden", "cases.npz"))
+    names = sorted({k.split("/")[0] for k in z.files})
+    return {n: {k.split("/")[1]: z[k] for k in z.files if k.startswith(n + "/")} for n in names}
+
+
+CASES = _cases()
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2004_08475_b200 as P
+    return P
+
+
+def same(a, b):
+    return a.shape == b.shape and (np.ascontiguousarray(a).view(np.uint64) ==
+                                   np.ascontiguousarray(b).view(np.uint64)).all()
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_weld_matches_restatement(P, name):
+    fat = CASES[name]["fat"]
+    m = P.weld(fat)
+    v, t = oracles.restatement().weld(fat)
+    assert same(m.vertices, v)
+    assert (m.triangles == t).all()
+    # expanding the indexed mesh gives the soup back (weld keeps triangle
+    # order and exact positions)
+    if len(fat):
+        assert same(m.vertices[m.triangles.astype(np.int64)].reshape(-1, 9), fat)
+
+
+def test_weld_matches_reference_library(P):
+    R = oracles.reference()
+    if R is None:
+        pytest.skip("oracle/_ref not built")
+    for name in ("octree_sphere", "slots_l4_s3", "blocks_jump2"):
+        fat = CASES[name]["fat"]
+        m = P.weld(fat)
+        v, t = R.weld(fat)
+        assert same(m.vertices, v) and (m.triangles == t).all()
+
+
+def test_weld_device_input_and_larger_soup(P):
+    """a ~1M-triangle soup of the brick generator, from a device tensor"""
+    import torch
+    from paper_2004_08475_b200 import synth
+    ds = synth.bricks([24, 16, 16], seed=5, shuffle=True)
+    idx = P.build_index(ds.cells, ds.scalars)
+    fat = P.extract_isosurface(idx, P.IsoParams(iso=synth.C4_ISO)).fat
+    idx.close()
+    m = P.weld(torch.from_numpy(fat).cuda())
+    v, t = oracles.restatement().weld(fat)
+    assert same(m.vertices, v) and (m.triangles == t).all()
+
+
+def test_weld_empty(P):
+    m = P.weld(np.zeros((0, 9)))
+    assert m.vertices.shape == (0, 3) and m.triangles.shape == (0, 3)
+
+
+def test_weld_signed_zero_is_one_vertex(P):
+    """-0.0 == +0.0 in the reference's comparison: one vertex"""
+    tri = np.array([[0.0, 1, 2, 3, 4, 5, 6, 7, 8], [-0.0, 1, 2, 9, 9, 9, 6, 7, 8]])
+    m = P.weld(tri)
+    v, t = oracles.restatement().weld(tri)
+    assert same(m.vertices, v) and (m.triangles == t).all()
