@@ -6,12 +6,14 @@
 //                                      proj/include/amriso/pipeline.hpp:65-66
 //   vector<DualCell> extract_dual_mesh(const CellIndex&, int)
 //                                      proj/include/amriso/pipeline.hpp:70-71
+//   IndexedMesh weld(span<const FatTriangle>)
+//                                      proj/include/amriso/weld.hpp:33-43
 //
 // Compiled against the reference's own headers and linked in place of
-// proj/src/pipeline.cpp and of build_index in proj/src/locator.cpp (see
-// INTEGRATION.md); everything else -- snap/find_exact/validate_dataset, the
-// dual rules used by tests, contour_hex, weld, I/O, generators, the CLI --
-// stays the reference's.  All computation goes through the C ABI
+// proj/src/pipeline.cpp, proj/src/weld.cpp and of build_index in
+// proj/src/locator.cpp; everything else --
+// snap/find_exact/validate_dataset, the dual rules used by tests,
+// contour_hex, I/O, generators, the CLI -- stays the reference's.  All computation goes through the C ABI
 // (include/amrx.h) to libamrx.so on the GPU; there is no CPU fallback.
 //
 // Error mapping (amrx_status -> the reference's exception types):
@@ -19,6 +21,7 @@
 //   AMRX_ERR_LENGTH -> length_error, AMRX_ERR_INTERNAL -> logic_error,
 //   anything else (CUDA, no device) -> runtime_error.
 #include "amriso/pipeline.hpp"
+#include "amriso/weld.hpp"
 
 #include "amrx.h"
 
@@ -156,7 +159,6 @@ ExtractionResult extract_isosurface(const CellIndex &index, const IsoParams &par
   stats.seconds_pass1 = st.seconds_pass1;
   stats.seconds_pass2 = st.seconds_pass2;
 
-  // the weld stays the reference's own (weld.cpp:31-64), see DESIGN.md
   const auto t_weld = Clock::now();
   result.mesh = weld(fat);
   stats.seconds_weld = seconds_since(t_weld);
@@ -165,6 +167,24 @@ ExtractionResult extract_isosurface(const CellIndex &index, const IsoParams &par
 
   if (params.emit_dual_mesh) result.duals = extract_dual_mesh(index, params.thread_count);
   return result;
+}
+
+IndexedMesh weld(std::span<const FatTriangle> triangles)
+{
+  IndexedMesh mesh;
+  if (triangles.empty()) return mesh;
+  const uint64_t n = triangles.size();
+  if (n > std::numeric_limits<uint32_t>::max() / 3)
+    throw std::length_error("weld: too many triangles for 32-bit indices");
+  std::vector<vec3d> verts(3 * n);
+  mesh.triangles.resize(n);
+  uint64_t nv = 0;
+  check(amrx_weld(reinterpret_cast<const double *>(triangles.data()), n,
+                  reinterpret_cast<double *>(verts.data()), 3 * n,
+                  reinterpret_cast<uint32_t *>(mesh.triangles.data()), &nv, nullptr));
+  verts.resize(nv);
+  mesh.vertices = std::move(verts);
+  return mesh;
 }
 
 }  // namespace amriso
