@@ -369,18 +369,26 @@ def weld(triangles, device=-1, stream=None):
     positions of a fat triangle soup ((T, 9) float64, numpy or torch host or
     CUDA) into an IndexedMesh with the reference's vertex order."""
     lib = library()
+    on_gpu = hasattr(triangles, "is_cuda") and triangles.is_cuda
     if isinstance(triangles, np.ndarray) or not hasattr(triangles, "data_ptr"):
         tri = np.ascontiguousarray(np.asarray(triangles, np.float64).reshape(-1, 9))
         n = len(tri)
     else:
         tri = triangles.contiguous()
         n = tri.shape[0] if tri.numel() else 0
-    verts = np.empty((3 * n, 3), np.float64)
-    idx = np.empty((n, 3), np.uint32)
+    if on_gpu:  # CUDA tensor in: the mesh stays on the device
+        import torch
+        verts = torch.empty((3 * n, 3), dtype=torch.float64, device=tri.device)
+        idx = torch.empty((n, 3), dtype=torch.int32, device=tri.device)
+    else:
+        verts = np.empty((3 * n, 3), np.float64)
+        idx = np.empty((n, 3), np.uint32)
     nv = C.c_uint64()
     opts = _Opts(device, C.c_void_p(stream) if stream else None, 0)
     _check(lib.amrx_weld(_ptr(tri) if n else None, n, _ptr(verts), 3 * n, _ptr(idx),
                          C.byref(nv), C.byref(opts)))
+    if on_gpu:
+        return IndexedMesh(verts[: nv.value], idx)  # ids as int32 (torch has no uint32 ops)
     return IndexedMesh(verts[: nv.value].copy(), idx)
 
 

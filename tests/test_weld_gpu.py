@@ -69,9 +69,11 @@ def test_weld_device_input_and_larger_soup(P):
     idx = P.build_index(ds.cells, ds.scalars)
     fat = P.extract_isosurface(idx, P.IsoParams(iso=synth.C4_ISO)).fat
     idx.close()
-    m = P.weld(torch.from_numpy(fat).cuda())
+    m = P.weld(torch.from_numpy(fat).cuda())  # the mesh stays on the device
     v, t = oracles.restatement().weld(fat)
-    assert same(m.vertices, v) and (m.triangles == t).all()
+    assert m.vertices.is_cuda and m.triangles.is_cuda
+    assert same(m.vertices.cpu().numpy(), v)
+    assert (m.triangles.cpu().numpy().view(np.uint32) == t).all()
 
 
 def test_weld_empty(P):
