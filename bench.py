@@ -108,6 +108,15 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- workload
+DATA_DESC = {
+    "c1": "synthetic (reference generator gen_octree, sphere field)",
+    "c2": "synthetic (reference generator random_slot_dataset, white noise)",
+    "c3": "synthetic (GPU generator: 6-level octree toward a turbulent-noise zero set, soup order)",
+    "c4": "synthetic (GPU generator: vortex-tube brick AMR, bijective-hash soup order)",
+    "c5": "synthetic (GPU generator: brick AMR, generator order)",
+}
+
+
 def make_workload(cfg_name, device):
     """device-resident synthetic input: (cells int32[n,4], scalars f64[n]) torch CUDA"""
     from paper_2004_08475_b200 import synth
@@ -119,6 +128,9 @@ def make_workload(cfg_name, device):
         return ds.cells, ds.scalars, dict(bricks=list(b3), level_cells=ds.level_cells)
     import torch
     gen = getattr(synth, cfg["kind"])
+    if cfg["kind"] == "octree_noise":  # GPU generator: device tensors already
+        cells, scal = gen(*cfg["args"], device=device)
+        return cells, scal, dict(level_cells=torch.bincount(cells[:, 3].long()).tolist())
     cells, scal = gen(*cfg["args"])
     return (torch.from_numpy(cells).to(device), torch.from_numpy(scal).to(device), {})
 
@@ -147,6 +159,7 @@ def run_amrx(args):
     # every rank generates the same input deterministically (the "batch")
     cells, scal, meta = make_workload(args.config, dev)
     n = cells.shape[0]
+    n_levels = int(torch.unique(cells[:, 3]).numel())
     stream = torch.cuda.Stream(device=dev)
     sh = stream.cuda_stream
 
@@ -348,8 +361,8 @@ def run_amrx(args):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "int64 keys / f64 scalars",
-        "data": "synthetic (GPU generator: vortex-tube brick AMR, bijective-hash soup order)",
-        "config": {"workload": f"{args.config}: {n} cells, levels 0-3, iso {iso}",
+        "data": DATA_DESC.get(args.config, "synthetic"),
+        "config": {"workload": f"{args.config}: {n} cells, {n_levels} levels, iso {iso}",
                    "cells": n, "triangles": tris, "duals": duals_full, "iso": iso,
                    "parallelism": (f"distributed sort + range partition x{world}" if args.dist_mode == "partition" else f"rank-0 sort + broadcast x{world}") if world > 1 else "single GPU",
                    "l2": "inputs (24 B/cell) far larger than L2", **meta},

@@ -390,11 +390,13 @@ KeyGeom make_geometry(const int64_t mn[3], const int64_t mx[3],
                            : std::min(30, std::max(10, bit_width(n) + 1));
   g.dir_bits = std::min(g.total, want);
   // occupancy records (AMRX_OCC=0 disables): 32 key values per bucket,
-  // when that many buckets cost at most ~4 per cell (8 B each)
+  // 8 B each, when they cost at most ~192 B per cell (or 1 GB): a sparse
+  // key space (C3: 105M cells, 36-bit keys -> 17 GB) still pays -- the
+  // bucket search is ~4x slower per lookup
   static const char *occ_env = std::getenv("AMRX_OCC");
   const int occ_bits = std::max(0, g.total - kOccShift);
   g.occ = !(occ_env && occ_env[0] == '0') && !dir_env && occ_bits <= 32 &&
-          (uint64_t(1) << occ_bits) <= 4 * n + (uint64_t(1) << 20);
+          (uint64_t(8) << occ_bits) <= std::max<uint64_t>(192 * n, uint64_t(1) << 30);
   if (g.occ) g.dir_bits = occ_bits;
   g.dir_shift = g.total - g.dir_bits;
   // block level map at the coarsest level's granularity, if it is small

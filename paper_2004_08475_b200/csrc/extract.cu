@@ -30,6 +30,7 @@
 #include "internal.h"
 #include "mc_tables.inc"
 
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 
@@ -911,7 +912,14 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
   // staging capacity: what the caller can take plus one chunk per warp of
   // slack for partially used chunks (so a fitting result never overflows)
   uint64_t dual_stage = D && r.corners ? r.dual_cap + warps * kDualChunk : 0;
-  uint64_t tri_stage = T && r.xyz ? r.tri_cap + warps * kTriChunk : 0;
+  // triangles are reserved at the case tables' upper bound (slivers drop
+  // some): size for the largest reserved/kept ratio seen so far (a rerun
+  // costs a whole extraction), at least 1/8 over the caller's capacity
+  static std::atomic<uint32_t> reserve_ratio_x1024{1024 + 128};
+  uint64_t tri_stage =
+    T && r.xyz ? r.tri_cap + r.tri_cap / 1024 * (reserve_ratio_x1024.load() - 1024) +
+                   warps * kTriChunk
+               : 0;
   const int tri_words = F ? 9 : 18;  // 32-bit words per triangle
 
   KArgs k;
@@ -988,7 +996,13 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
     const bool tri_short = tri_stage && h[9] > tri_stage && h[6] <= r.tri_cap;
     if (attempt || (!dual_short && !tri_short)) break;
     if (dual_short) dual_stage = h[8] + warps * kDualChunk;
-    if (tri_short) tri_stage = h[9] + warps * kTriChunk;
+    if (tri_short) {
+      tri_stage = h[9] + warps * kTriChunk;
+      const uint64_t ratio = h[6] ? h[9] * 1024 / h[6] + 32 : 2048;
+      uint32_t cur = reserve_ratio_x1024.load();
+      while (ratio > cur && !reserve_ratio_x1024.compare_exchange_weak(cur, uint32_t(ratio))) {
+      }
+    }
   }
   for (int i = 0; i < 4; i++) res.counters[i] = h[i];
   res.duals = h[4];
@@ -1015,7 +1029,10 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
   // scattered stores across the link.
   const int rgrid = int(std::min<uint64_t>((tiles + 7) / 8, uint64_t(device_sm_count()) * 16));
   WsBuf host_a(kWsOutA), host_b(kWsOutB);
-  if (tiles && dual_stage && res.duals > 0) {
+  // a result larger than the caller's capacity is not moved: the caller
+  // reports the count (capacity error) or retries with room for it, and
+  // tiles past the staging capacity were never written
+  if (tiles && dual_stage && res.duals > 0 && res.duals <= r.dual_cap) {
     res.launches += scan_exclusive_u32_u64(dual_cnt, final_off, tiles, x.scan, st);
     const uint64_t keep = std::min(res.duals, r.dual_cap);
     uint32_t *dc = r.corners;
@@ -1040,7 +1057,7 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
         AMRX_CUDA(cudaMemcpyAsync(r.tasks, dt, keep * 8, cudaMemcpyDeviceToHost, st));
     }
   }
-  if (tiles && tri_stage && res.tris_written > 0) {
+  if (tiles && tri_stage && res.tris_written > 0 && res.tris_written <= r.tri_cap) {
     res.launches += scan_exclusive_u32_u64(tri_cnt, final_off, tiles, x.scan, st);
     const uint64_t keep = std::min(res.tris_written, r.tri_cap);
     uint32_t *dx = static_cast<uint32_t *>(r.xyz);

@@ -132,11 +132,65 @@ def body_holes(bricks3):
     return [fus, wing]
 
 
+def octree_noise(root=(48, 48, 48), levels=6, seed=3, k=0.45, base=0.02, shuffle=True,
+                 device="cuda"):
+    """C3: a 6-level octree (levels 0..levels-1) over a root grid of
+    coarsest cells, refined toward the zero set of a turbulent-noise field
+    (four octaves of products of sines with random phases), the field at the
+    cell centre as the scalar; optionally shuffled into a soup.  Built with
+    torch on the GPU (no reference counterpart: the reference's own
+    generators are CPU, synth.cpp).  Returns (cells int32[n,4], scalars
+    f64[n]) on `device`."""
+    import math
+    import torch
+    g = torch.Generator().manual_seed(seed)
+    ph = (torch.rand((4, 3), generator=g, dtype=torch.float64) * 2 * math.pi).tolist()
+
+    def field(c):
+        x, y, z = c[:, 0], c[:, 1], c[:, 2]
+        f = torch.zeros_like(x)
+        for o in range(4):
+            w = base * (2 ** o)
+            f += (0.5 ** o) * torch.sin(w * x + ph[o][0]) * torch.sin(w * y + ph[o][1]) * \
+                torch.sin(w * z + ph[o][2])
+        return f
+
+    L = levels - 1
+    W = 1 << L
+    r = [torch.arange(n, device=device, dtype=torch.int64) * W for n in root]
+    cur = torch.stack(torch.meshgrid(*r, indexing="ij"), -1).reshape(-1, 3)
+    off = torch.tensor([[(d >> 0) & 1, (d >> 1) & 1, (d >> 2) & 1] for d in range(8)],
+                       device=device, dtype=torch.int64)
+    cells, scal = [], []
+    while True:
+        w = 1 << L
+        f = field(cur.to(torch.float64) + 0.5 * w)
+        refine = (f.abs() < k * w * base) if L > 0 else torch.zeros_like(f, dtype=torch.bool)
+        keep = ~refine
+        cells.append(torch.cat([cur[keep], torch.full((int(keep.sum()), 1), L, device=device,
+                                                      dtype=torch.int64)], 1))
+        scal.append(f[keep])
+        if L == 0 or not bool(refine.any()):
+            break
+        cur = (cur[refine][:, None, :] + off[None] * (w // 2)).reshape(-1, 3)
+        L -= 1
+    cells = torch.cat(cells).to(torch.int32)
+    scal = torch.cat(scal)
+    if shuffle:
+        gp = torch.Generator(device=device).manual_seed(seed)
+        perm = torch.randperm(len(cells), device=device, generator=gp)
+        cells, scal = cells[perm].contiguous(), scal[perm].contiguous()
+    return cells, scal
+
+
 CONFIGS = {
     # C1: SURVEY §8(d): gen_octree(6, sphere((25,27.5,30), 20), 3.2), iso 0
     "c1": dict(kind="octree_sphere", args=(6, (25.0, 27.5, 30.0), 20.0, 3.2), iso=0.0),
     # C2: random_slot_dataset(mt19937(seed), 23, 4, 0.15), iso 0.1
     "c2": dict(kind="slots", args=(2026, 23, 4, 0.15), iso=0.1),
+    # C3: 104.8M-cell 6-level octree refined toward a turbulent-noise zero
+    # set, the noise as scalar, iso 0 (GPU generator, soup order)
+    "c3": dict(kind="octree_noise", args=(), iso=0.0),
     # C4: 626M-cell 4-level soup (bricks 512 x 256 x 256 -> tuned knobs)
     "c4": dict(kind="bricks", bricks=(512, 256, 256), seed=1, shuffle=True, iso=None),
     # C5: ~250M-cell mixed-level AMR, dual mesh only

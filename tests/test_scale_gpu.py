@@ -3,7 +3,8 @@
 * C2 (~9.7M cells, block-structured, level jumps up to 4, holes, white
   noise, iso 0.1): FULL bit-exact comparison of the dual mesh, the reject
   counters and the FP64 soup against the reference library itself.
-* C4 (626M-cell soup) and C5 (250M, dual mesh only): the oracle cannot run
+* C3 (105M-cell 6-level noise octree), C4 (626M-cell soup) and C5 (250M,
+  dual mesh only): the oracle cannot run
   the whole path in a test's time, so (a) sampled cell ranges of the GPU
   output are compared bit-for-bit with the C restatement evaluated over the
   SAME full index (the sorted arrays downloaded from the GPU -- candidates
@@ -86,6 +87,12 @@ def _big(P, name):
     import torch
     from paper_2004_08475_b200 import synth
     cfg = synth.CONFIGS[name]
+    if cfg["kind"] == "octree_noise":
+        cells, scal = synth.octree_noise(*cfg["args"])
+        idx = P.build_index(cells, scal)
+        del cells, scal
+        torch.cuda.synchronize()
+        return idx
     b3 = cfg["bricks"]
     ds = synth.bricks(b3, seed=cfg["seed"], shuffle=cfg["shuffle"], knobs=synth.C4_KNOBS,
                       holes=synth.body_holes(b3))
@@ -125,16 +132,18 @@ def _exactly_once(P, corners):
     return int(same.sum().item())
 
 
-@pytest.mark.parametrize("name", ["c4", "c5"])
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
 def test_full_scale_properties_and_sampled_parity(P, name):
     import torch
     idx = _big(P, name)
     n = len(idx)
-    assert n > (600_000_000 if name == "c4" else 200_000_000)
+    assert n > {"c3": 100_000_000, "c4": 600_000_000, "c5": 200_000_000}[name]
     from paper_2004_08475_b200 import synth
-    iso = synth.C4_ISO
+    iso = synth.C4_ISO if synth.CONFIGS[name]["iso"] is None else synth.CONFIGS[name]["iso"]
+    if name == "c3":
+        assert idx.levels == [0, 1, 2, 3, 4, 5]
     # --- dual mesh on the device
-    cap = int(n * 1.2)
+    cap = int(n * (1.9 if name == "c3" else 1.2))  # octrees own ~1.7 duals per cell
     corners = torch.empty((cap, 8), dtype=torch.int32, device="cuda")
     tasks = torch.empty(cap, dtype=torch.int64, device="cuda")
     d = P.extract_dual_mesh(idx, out=(corners, tasks))
@@ -160,7 +169,7 @@ def test_full_scale_properties_and_sampled_parity(P, name):
         od = o.extract_dual_range(h, b, e)
         assert (gd.corners == od["corners"]).all(), (name, b)
         assert (gd.owner == od["owner"]).all()
-        if name == "c4":
+        if name != "c5":  # C5 is the dual-mesh-only configuration
             gi = P.extract_isosurface(idx, P.IsoParams(iso=iso), cell_range=(b, e))
             oi = o.extract_iso(h, iso, b, e)
             assert gi.fat.shape == oi["fat"].shape, (b, gi.fat.shape, oi["fat"].shape)
