@@ -209,6 +209,15 @@ AMRX_API amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range
                              uint64_t cap, uint64_t *count,
                              amrx_stats *stats);
 
+/* validate_dataset (proj/src/locator.cpp:136-161): duplicate pairs (n,
+ * n+1) of equal adjacent cells and overlap pairs (n, coarser cell holding
+ * cell n's anchor), 2 x uint32 CellIds each, in the reference's order.
+ * Either buffer may be NULL (count only); AMRX_ERR_CAPACITY when a cap is
+ * too small (the counts are still set). */
+AMRX_API amrx_status amrx_validate(amrx_index *index, uint32_t *dup_pairs, uint64_t dup_cap,
+                                   uint64_t *n_dup, uint32_t *overlap_pairs,
+                                   uint64_t overlap_cap, uint64_t *n_overlap);
+
 /* weld (proj/src/weld.cpp:31-64, replaces amriso::weld): merge bitwise-
  * identical corner positions of n_tris fat triangles (9 FP64 each, host or
  * device) into shared vertices, position-sorted like the reference.

@@ -331,6 +331,22 @@ int64_t ref_validate(void *h, uint64_t *dups, uint64_t *overlaps)
   return int64_t(r.duplicates.size() + r.overlaps.size());
 }
 
+/// validate_dataset pairs: dup2 / ovl2 (2 x u32 each, may be null) get the
+/// first `cap` pairs of each list
+void ref_validate_pairs(void *h, uint32_t *dup2, uint32_t *ovl2, uint64_t cap)
+{
+  const ValidationReport r =
+    validate_dataset(static_cast<RefIndex *>(h)->index);
+  for (size_t n = 0; dup2 && n < r.duplicates.size() && n < cap; n++) {
+    dup2[2 * n] = r.duplicates[n].first.index;
+    dup2[2 * n + 1] = r.duplicates[n].second.index;
+  }
+  for (size_t n = 0; ovl2 && n < r.overlaps.size() && n < cap; n++) {
+    ovl2[2 * n] = r.overlaps[n].first.index;
+    ovl2[2 * n + 1] = r.overlaps[n].second.index;
+  }
+}
+
 // ----------------------------------------------------------- dual mesh
 void *ref_extract_dual(void *h, int threads, double *seconds)
 {

@@ -125,6 +125,7 @@ def library():
         "amrx_index_sort_part": [P, P, U64, P, P, P],
         "amrx_index_from_keys": [P, P, U64, P, P, P],
         "amrx_weld": [P, U64, P, U64, P, P, P],
+        "amrx_validate": [P, P, U64, P, P, U64, P],
         "amrx_find_exact": [P, P, U64, P],
         "amrx_snap": [P, P, P, I32, U64, P],
         "amrx_try_build_duals": [P, P, U64, P, P],
@@ -355,6 +356,45 @@ def index_from_keys(keys_dev_ptr, scalars_dev_ptr, n_cells, geometry, device=-1,
     _check(lib.amrx_index_from_keys(C.c_void_p(keys_dev_ptr), C.c_void_p(scalars_dev_ptr),
                                     n_cells, _ptr(g), C.byref(opts), C.byref(h)))
     return CellIndex(h.value, lib)
+
+
+@dataclass
+class ValidationReport:
+    """ValidationReport (locator.hpp:70-78): (n, n+1) duplicate pairs and
+    (finer, coarser) overlap pairs of CellIds"""
+    duplicates: np.ndarray  # (D, 2) uint32
+    overlaps: np.ndarray    # (O, 2) uint32
+
+    def ok(self):
+        return len(self.duplicates) == 0 and len(self.overlaps) == 0
+
+    def describe(self, index):
+        """the reference's text (locator.cpp:163-185)"""
+        cells = index.cells
+
+        def cell(i):
+            c = cells[int(i)]
+            return f"({c[0]} {c[1]} {c[2]} level {c[3]})"
+
+        out = f"{len(self.duplicates)} duplicate pair(s), {len(self.overlaps)} overlap pair(s)"
+        for a, _ in self.duplicates[:8]:
+            out += "\n  duplicate cell " + cell(a)
+        for a, b in self.overlaps[:8]:
+            out += "\n  cell " + cell(a) + " lies inside " + cell(b)
+        return out
+
+
+def validate_dataset(index: CellIndex):
+    """validate_dataset (locator.cpp:136-161) on the GPU"""
+    lib = index._lib
+    nd, no = C.c_uint64(), C.c_uint64()
+    _check(lib.amrx_validate(index.handle, None, 0, C.byref(nd), None, 0, C.byref(no)))
+    dup = np.empty((nd.value, 2), np.uint32)
+    ovl = np.empty((no.value, 2), np.uint32)
+    _check(lib.amrx_validate(index.handle, _ptr(dup) if nd.value else None, nd.value,
+                             C.byref(nd), _ptr(ovl) if no.value else None, no.value,
+                             C.byref(no)))
+    return ValidationReport(dup, ovl)
 
 
 @dataclass

@@ -893,6 +893,33 @@ amrx_status amrx_index_from_keys(const void *keys_dev, const double *scalars_dev
   });
 }
 
+amrx_status amrx_validate(amrx_index *index, uint32_t *dup_pairs, uint64_t dup_cap,
+                          uint64_t *n_dup, uint32_t *overlap_pairs, uint64_t overlap_cap,
+                          uint64_t *n_overlap)
+{
+  return guarded([&] {
+    require_searchable(index);
+    if (!index || !n_dup || !n_overlap) fail(AMRX_ERR_INVALID_ARG, "null argument");
+    std::lock_guard<std::mutex> lock(index->mu);
+    DeviceGuard dg(index->device);
+    cudaStream_t st = index->stream;
+    DevOut<uint32_t> dp(dup_pairs, dup_pairs ? 2 * dup_cap : 0, st);
+    DevOut<uint32_t> op(overlap_pairs, overlap_pairs ? 2 * overlap_cap : 0, st);
+    run_validate(index->ctx(), index->g, op.ptr, overlap_cap, n_overlap, dp.ptr, dup_cap, n_dup,
+                 st);
+    if (dup_pairs && dp.staged && *n_dup)
+      AMRX_CUDA(cudaMemcpyAsync(dup_pairs, dp.ptr, std::min(*n_dup, dup_cap) * 8,
+                                cudaMemcpyDeviceToHost, st));
+    if (overlap_pairs && op.staged && *n_overlap)
+      AMRX_CUDA(cudaMemcpyAsync(overlap_pairs, op.ptr, std::min(*n_overlap, overlap_cap) * 8,
+                                cudaMemcpyDeviceToHost, st));
+    AMRX_CUDA(cudaStreamSynchronize(st));
+    if ((dup_pairs && *n_dup > dup_cap) || (overlap_pairs && *n_overlap > overlap_cap))
+      fail(AMRX_ERR_CAPACITY, "validate: " + std::to_string(*n_dup) + " duplicate and " +
+                                std::to_string(*n_overlap) + " overlap pairs exceed the buffers");
+  });
+}
+
 amrx_status amrx_weld(const double *xyz9, uint64_t n_tris, double *verts3, uint64_t vcap,
                       uint32_t *tris3, uint64_t *n_verts, const amrx_index_opts *opts)
 {

@@ -225,6 +225,14 @@ void run_try_build(const SearchCtx &s, const KeyGeom &g, const uint64_t *tasks,
 
 int device_sm_count();
 
+// --------------------------------------------------------- validate.cu
+/// validate_dataset: overlap / duplicate pairs (2 x u32 each, global ids)
+/// into the buffers (device, may be null) up to their capacities; the
+/// counts are returned either way
+void run_validate(const SearchCtx &s, const KeyGeom &g, uint32_t *ovl_pairs, uint64_t ovl_cap,
+                  uint64_t *n_ovl, uint32_t *dup_pairs, uint64_t dup_cap, uint64_t *n_dup,
+                  cudaStream_t st);
+
 // ------------------------------------------------------------- weld.cu
 /// weld n_tris fat triangles (device xyz9); verts (vcap) / tris (3 per
 /// triangle) may be null; returns the vertex count

@@ -8,11 +8,13 @@
 //                                      proj/include/amriso/pipeline.hpp:70-71
 //   IndexedMesh weld(span<const FatTriangle>)
 //                                      proj/include/amriso/weld.hpp:33-43
+//   ValidationReport validate_dataset(const CellIndex&)
+//                                      proj/include/amriso/locator.hpp:80
 //
 // Compiled against the reference's own headers and linked in place of
-// proj/src/pipeline.cpp, proj/src/weld.cpp and of build_index in
-// proj/src/locator.cpp; everything else --
-// snap/find_exact/validate_dataset, the dual rules used by tests,
+// proj/src/pipeline.cpp, proj/src/weld.cpp and of build_index and
+// validate_dataset in proj/src/locator.cpp; everything
+// else -- snap/find_exact, the dual rules used by tests,
 // contour_hex, I/O, generators, the CLI -- stays the reference's.  All computation goes through the C ABI
 // (include/amrx.h) to libamrx.so on the GPU; there is no CPU fallback.
 //
@@ -167,6 +169,24 @@ ExtractionResult extract_isosurface(const CellIndex &index, const IsoParams &par
 
   if (params.emit_dual_mesh) result.duals = extract_dual_mesh(index, params.thread_count);
   return result;
+}
+
+ValidationReport validate_dataset(const CellIndex &index)
+{
+  ValidationReport report;
+  if (index.size() == 0) return report;
+  IndexHandle h;
+  upload(index, h);
+  uint64_t nd = 0, no = 0;
+  check(amrx_validate(h.p, nullptr, 0, &nd, nullptr, 0, &no));
+  std::vector<uint32_t> dup(2 * nd), ovl(2 * no);
+  check(amrx_validate(h.p, nd ? dup.data() : nullptr, nd, &nd, no ? ovl.data() : nullptr, no,
+                      &no));
+  for (uint64_t n = 0; n < nd; n++)
+    report.duplicates.push_back({CellId{dup[2 * n]}, CellId{dup[2 * n + 1]}});
+  for (uint64_t n = 0; n < no; n++)
+    report.overlaps.push_back({CellId{ovl[2 * n]}, CellId{ovl[2 * n + 1]}});
+  return report;
 }
 
 IndexedMesh weld(std::span<const FatTriangle> triangles)

@@ -195,6 +195,7 @@ class Reference(_Lib):
         self._fn("ref_gen_slots", P, [U32, C.c_int, C.c_int, F64])
         self._fn("ref_acceptance_fixture", P, [C.c_int, P])
         self._fn("ref_validate", I64, [P, P, P])
+        self._fn("ref_validate_pairs", None, [P, P, P, U64])
         self._fn("ref_extract_dual", P, [P, C.c_int, P])
         self._fn("ref_duals_count", U64, [P])
         self._fn("ref_duals_get", None, [P, P, P, P, P])
@@ -252,6 +253,13 @@ class Reference(_Lib):
         d, o = C.c_uint64(0), C.c_uint64(0)
         self.lib.ref_validate(h, C.byref(d), C.byref(o))
         return d.value, o.value
+
+    def validate_pairs(self, h):
+        nd, no = self.validate(h)
+        dup = np.empty((nd, 2), np.uint32)
+        ovl = np.empty((no, 2), np.uint32)
+        self.lib.ref_validate_pairs(h, _ptr(dup), _ptr(ovl), max(nd, no))
+        return dup, ovl
 
     def extract_dual(self, h, threads=0):
         secs = C.c_double(0)
