@@ -233,33 +233,38 @@ __device__ __noinline__ int mc_dual(const KArgs &a, const Smem &sm, int warp, in
                        uint64_t at, uint64_t cap, uint32_t &err)
 {
   const int64_t w = int64_t(1) << c.level;
-  uint32_t ids[8];
-  double val[8];
-  int lv[8];
   int mask = 0;
 #pragma unroll
-  for (int d = 0; d < 8; d++) {
-    const int p = point_of(delta, d);
-    ids[d] = sm.id[warp][p][lane];
-    lv[d] = sm.lev[warp][p][lane];
-    val[d] = __ldg(a.scal + ids[d]);
-    if (val[d] > iso) mask |= 1 << d;
-  }
+  for (int d = 0; d < 8; d++)
+    if (__ldg(a.scal + sm.id[warp][point_of(delta, d)][lane]) > iso) mask |= 1 << d;
   const uint64_t word = sm.mc_rows[mask];  // rows pre-permuted by corner mask
   const int ntab = int(word & 15);
   if (ntab == 0) return 0;
 
+  // an edge's endpoints are runtime corner numbers: their ids, levels and
+  // scalars are re-read from shared memory / L1 rather than kept in
+  // dynamically indexed arrays (which live in local memory)
   const auto edge_point = [&](int e, double (&pt)[3]) {
     const uint32_t ends = e < 8 ? uint32_t(AMRX_MC_EDGE_LO >> (8 * e))
                                 : uint32_t(AMRX_MC_EDGE_HI >> (8 * (e - 8)));
     int u = int(ends & 15), v = int((ends >> 4) & 15);
-    if (ids[u] == ids[v]) err |= 1u;  // collapsed edge selected (contour.cpp:67-70)
-    if (ids[v] < ids[u]) {            // lower CellId first (contour.cpp:42-44)
+    const int pu = point_of(delta, u), pv = point_of(delta, v);
+    uint32_t idu = sm.id[warp][pu][lane], idv = sm.id[warp][pv][lane];
+    int lu = sm.lev[warp][pu][lane], lvv = sm.lev[warp][pv][lane];
+    if (idu == idv) err |= 1u;  // collapsed edge selected (contour.cpp:67-70)
+    if (idv < idu) {            // lower CellId first (contour.cpp:42-44)
       const int t = u;
       u = v;
       v = t;
+      const uint32_t ti = idu;
+      idu = idv;
+      idv = ti;
+      const int tl = lu;
+      lu = lvv;
+      lvv = tl;
     }
-    const double t = __ddiv_rn(__dsub_rn(iso, val[u]), __dsub_rn(val[v], val[u]));
+    const double vu = __ldg(a.scal + idu), vv = __ldg(a.scal + idv);
+    const double t = __ddiv_rn(__dsub_rn(iso, vu), __dsub_rn(vv, vu));
     const int ou[3] = {((u & 1) + (delta & 1)) - 1, (((u >> 1) & 1) + ((delta >> 1) & 1)) - 1,
                        (((u >> 2) & 1) + ((delta >> 2) & 1)) - 1};
     const int ov[3] = {((v & 1) + (delta & 1)) - 1, (((v >> 1) & 1) + ((delta >> 1) & 1)) - 1,
@@ -267,8 +272,8 @@ __device__ __noinline__ int mc_dual(const KArgs &a, const Smem &sm, int warp, in
     const int64_t self[3] = {c.i, c.j, c.k};
 #pragma unroll
     for (int ax = 0; ax < 3; ax++) {
-      const double pa = centre(anchor_mask(self[ax] + ou[ax] * w, lv[u]), lv[u]);
-      const double pb = centre(anchor_mask(self[ax] + ov[ax] * w, lv[v]), lv[v]);
+      const double pa = centre(anchor_mask(self[ax] + ou[ax] * w, lu), lu);
+      const double pb = centre(anchor_mask(self[ax] + ov[ax] * w, lvv), lvv);
       pt[ax] = __dadd_rn(pa, __dmul_rn(t, __dsub_rn(pb, pa)));
     }
   };
