@@ -319,7 +319,7 @@ def run_amrx(args):
     weld_ms = None
     if world == 1:
         wsoup = out[:tris]
-        P.weld(wsoup[:1024])  # warm-up (allocations)
+        P.weld(wsoup)  # warm-up (the pool grows to the weld's buffers once)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         mesh = P.weld(wsoup)
