@@ -158,13 +158,25 @@ struct DevOut {
 
 DevBuf::~DevBuf() { release(); }
 
+namespace {
+void release_idle_memory(int device);
+}
+
 void DevBuf::reserve(size_t n, cudaStream_t st)
 {
   if (n <= bytes && ptr) return;
   release();
   if (n == 0) n = 16;
   stream = st;
-  AMRX_CUDA(cudaMallocAsync(&ptr, n, st));
+  if (cudaMallocAsync(&ptr, n, st) != cudaSuccess) {
+    // out of memory: give back idle workspace slots and the pool's cached
+    // blocks, then try once more
+    cudaGetLastError();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    release_idle_memory(dev);
+    AMRX_CUDA(cudaMallocAsync(&ptr, n, st));
+  }
   bytes = n;
 }
 
@@ -203,6 +215,51 @@ WsDevice &ws_device(int dev)
   static WsDevice devices[64];
   return devices[dev & 63];
 }
+
+/// free the idle workspace slots (caller holds no lock on w) and trim the
+/// stream-ordered pool: the memory-pressure fallback of every allocation
+void release_idle_slots(WsDevice &w)
+{
+  cudaDeviceSynchronize();
+  for (int i = 0; i < kWsCount; i++)
+    if (!w.busy[i] && w.ptr[i]) {
+      cudaFree(w.ptr[i]);
+      w.ptr[i] = nullptr;
+      w.bytes[i] = 0;
+    }
+}
+
+void release_idle_memory(int device)
+{
+  WsDevice &w = ws_device(device);
+  {
+    std::lock_guard<std::mutex> lock(w.mu);
+    release_idle_slots(w);
+  }
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  cudaGetLastError();
+}
+
+/// cudaMalloc with the memory-pressure fallback (w.mu held by the caller)
+void slot_malloc(WsDevice &w, int device, void **p, size_t n, int slot)
+{
+  if (cudaMalloc(p, n) == cudaSuccess) return;
+  cudaGetLastError();
+  release_idle_slots(w);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  cudaGetLastError();
+  if (cudaMalloc(p, n) != cudaSuccess) {
+    cudaGetLastError();
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    throw ApiError(AMRX_ERR_CUDA, "out of device memory for a " + std::to_string(n >> 20) +
+                                    " MiB workspace buffer (slot " + std::to_string(slot) + ", " +
+                                    std::to_string(fr >> 20) +
+                                    " of " + std::to_string(tot >> 20) + " MiB free)");
+  }
+}
 }  // namespace
 
 void *WsLease::get(int slot, size_t n, cudaStream_t st)
@@ -216,7 +273,7 @@ void *WsLease::get(int slot, size_t n, cudaStream_t st)
     cudaFree(w.ptr[slot_]);
     w.ptr[slot_] = nullptr;
     w.bytes[slot_] = 0;
-    AMRX_CUDA(cudaMalloc(&w.ptr[slot_], n));
+    slot_malloc(w, device_, &w.ptr[slot_], n, slot_);
     w.bytes[slot_] = n;
     ptr = w.ptr[slot_];
     bytes = n;
@@ -243,7 +300,7 @@ void *WsLease::get(int slot, size_t n, cudaStream_t st)
           w.bytes[slot] = 0;
         }
         const size_t want = std::max<size_t>(n, 256);
-        AMRX_CUDA(cudaMalloc(&w.ptr[slot], want));
+        slot_malloc(w, dev, &w.ptr[slot], want, slot);
         w.bytes[slot] = want;
       }
       w.busy[slot] = true;
@@ -301,6 +358,7 @@ struct amrx_index {
   int64_t id_base = 0;
   uint64_t key_lo = 0, key_hi = 0;
   bool searchable = true;  // false: sorted arrays only (amrx_index_sort_part)
+  uint32_t jobs_per_kcell = 0;  // marching-cubes jobs per 1024 cells, last extraction
   amrx_index_info info{};
   // last extraction kept on the device for the count-then-copy pattern
   struct Cached {
@@ -1253,6 +1311,7 @@ amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range,
     rq.cell_end = e;
     rq.emit_tri = true;
     rq.tri_f32 = params->xyz_is_f32 != 0;
+    rq.jobs_per_kcell = &index->jobs_per_kcell;
     rq.iso = params->iso;
     const auto length_check = [&](uint64_t tris) {
       if (params->check_length &&

@@ -99,6 +99,27 @@ __device__ __forceinline__ uint64_t reserve(uint64_t *cur_end, uint32_t agg,
   return cur;
 }
 
+/*! A crossing dual handed from extract_kernel to mc_jobs_kernel: its corner
+    ids and levels, owner key, candidate and triangle count bound, reserved
+    staging slot and tile.  64 bytes. */
+struct McJob {
+  uint32_t id[8];
+  uint64_t key;
+  uint64_t out;
+  uint8_t lev[8];
+  uint32_t tile;
+  uint16_t meta;  // delta | ntab << 8
+  uint16_t pad;
+};
+static_assert(sizeof(McJob) == 64, "McJob is 64 bytes");
+
+/*! Marching cubes writes each dual's triangles at the case table's upper
+    bound; the slots a dual leaves unused (sliver triangles are dropped,
+    contour.cpp:80-84) get this signalling-NaN marker as their first word --
+    arithmetic never produces a signalling NaN -- and reorder_tri_kernel
+    skips them. */
+constexpr uint32_t kGapMark = 0xFFB4C0DEu;
+
 /// bit i of the result: scalar i > iso (the strict case test of contour.cpp:22-28)
 __global__ void __launch_bounds__(256)
 sign_bits_kernel(const double *__restrict__ scal, uint64_t n, double iso,
@@ -110,6 +131,43 @@ sign_bits_kernel(const double *__restrict__ scal, uint64_t n, double iso,
     const uint64_t r = base + (threadIdx.x & 31);
     const uint32_t word = __ballot_sync(kFull, r < n && __ldg(scal + r) > iso);
     if ((threadIdx.x & 31) == 0) bits[base >> 5] = word;
+  }
+}
+
+/*! the triangle variant of reorder_kernel: a tile's staging block holds
+    up[t] reserved slots of which cnt[t] are triangles; when slivers left
+    gaps (rare: cnt < up) the warp compacts the block while moving it */
+__global__ void __launch_bounds__(256)
+reorder_tri_kernel(const uint32_t *__restrict__ cnt, const uint32_t *__restrict__ up,
+                   const uint64_t *__restrict__ src_off, const uint64_t *__restrict__ dst_off,
+                   uint32_t tiles, int words, const uint32_t *__restrict__ src,
+                   uint32_t *__restrict__ dst, uint64_t dst_cap)
+{
+  const int lane = threadIdx.x & 31;
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < tiles; t += warps) {
+    const uint32_t n = cnt[t], u = up[t];
+    if (!n) continue;
+    const uint64_t so = src_off[t], d0 = dst_off[t];
+    if (n == u) {
+      const uint64_t keep = d0 >= dst_cap ? 0 : (d0 + n > dst_cap ? dst_cap - d0 : n);
+      const uint64_t nw = keep * uint64_t(words);
+      for (uint64_t w = lane; w < nw; w += 32) dst[d0 * words + w] = __ldg(src + so * words + w);
+      continue;
+    }
+    uint64_t done = 0;
+    for (uint32_t i0 = 0; i0 < u; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      const bool ok = i < u && __ldg(src + (so + i) * words) != kGapMark;
+      uint32_t bal = __ballot_sync(kFull, ok);
+      while (bal) {  // the kept slots of this chunk, in order
+        const int l = __ffs(bal) - 1;
+        bal &= bal - 1;
+        const uint64_t d = d0 + done++;
+        if (d < dst_cap && lane < words)
+          dst[d * words + lane] = __ldg(src + (so + i0 + l) * words + lane);
+      }
+    }
   }
 }
 
@@ -159,8 +217,11 @@ struct KArgs {
   uint64_t tri_cap;
   uint32_t *tile_dual_cnt;
   uint64_t *tile_dual_off;
-  uint32_t *tile_tri_cnt;
+  uint32_t *tile_tri_cnt;  // triangles kept (upper bound minus slivers)
+  uint32_t *tile_tri_up;   // slots reserved (the case tables' upper bound)
   uint64_t *tile_tri_off;
+  struct McJob *jobs;      // crossing duals for mc_jobs_kernel (EMIT_TRI)
+  uint64_t job_cap;
   unsigned int *ticket;
   unsigned long long *out;  // [0..3] counters, [4] duals, [5] tris counted,
                             // [6] tris written, [7] error flags,
@@ -188,88 +249,56 @@ __device__ __forceinline__ int table_row(uint32_t mask)
   return row;
 }
 
-/*! a tile wrote each lane's triangles at its upper-bound offset `from`;
-    slivers left gaps, so move every lane's run to its exact offset `to`
-    (to <= from), lanes in order so a left shift never overwrites unread
-    data.  Whole warp; rare. */
-template <bool F32>
-__device__ __noinline__ void compact_tile(void *xyz, uint64_t cap, uint64_t from,
-                                          uint64_t to, uint32_t count)
-{
-  const int lane = int(lane_id());
-  const int words = F32 ? 9 : 18;  // 32-bit words per triangle
-  uint32_t *base = static_cast<uint32_t *>(xyz);
-  for (int src = 0; src < 32; src++) {
-    const uint64_t f = __shfl_sync(kFull, (unsigned long long)from, src);
-    const uint64_t t = __shfl_sync(kFull, (unsigned long long)to, src);
-    const uint32_t n = __shfl_sync(kFull, count, src);
-    if (f == t || n == 0) continue;
-    const uint64_t keep = f + n <= cap ? n : (f < cap ? cap - f : 0);
-    const uint64_t nw = keep * uint64_t(words);
-    for (uint64_t w0 = 0; w0 < nw; w0 += 32) {
-      const uint64_t w = w0 + uint64_t(lane);
-      uint32_t v = 0;
-      if (w < nw) v = base[f * words + w];
-      __syncwarp();
-      if (w < nw) base[t * words + w] = v;
-      __syncwarp();
-    }
-  }
-}
-
 /// centre of the corner cell: anchor + half width, in double (core.hpp:113-118)
 __device__ __forceinline__ double centre(int64_t anchor, int level)
 {
   return __dadd_rn(double(anchor), __dmul_rn(0.5, double(int64_t(1) << level)));
 }
 
-/*! marching cubes over one accepted dual (contour.cpp:52-87): count (and,
-    when out != null, write) its non-sliver triangles.  FP64 with explicit
-    round-to-nearest intrinsics: no FMA contraction, matching the
-    reference's -ffp-contract=off build. */
-template <bool F32>
-__device__ __noinline__ int mc_dual(const KArgs &a, const Smem &sm, int warp, int lane,
-                       const Cell &c, int delta, double iso, bool write, void *out,
-                       uint64_t at, uint64_t cap, uint32_t &err)
+/*! marching cubes over one accepted dual (contour.cpp:52-87): write its
+    non-sliver triangles from slot `at` (staging capacity `cap`) and return
+    how many.  FP64 with explicit round-to-nearest intrinsics: no FMA
+    contraction, matching the reference's -ffp-contract=off build.
+    corner(d) gives the id and level of the dual's corner d (an edge's
+    endpoints are runtime corner numbers: they are re-read through it from
+    shared memory rather than kept in dynamically indexed arrays, which
+    would live in local memory). */
+template <bool F32, typename Corner>
+__device__ __forceinline__ int mc_core(const double *scal, const uint64_t *rows, const Cell &c,
+                                       int delta, double iso, void *out, uint64_t at,
+                                       uint64_t cap, uint32_t &err, Corner corner)
 {
   const int64_t w = int64_t(1) << c.level;
   int mask = 0;
 #pragma unroll
   for (int d = 0; d < 8; d++)
-    if (__ldg(a.scal + sm.id[warp][point_of(delta, d)][lane]) > iso) mask |= 1 << d;
-  const uint64_t word = sm.mc_rows[mask];  // rows pre-permuted by corner mask
+    if (__ldg(scal + corner(d).x) > iso) mask |= 1 << d;
+  const uint64_t word = rows[mask];  // rows pre-permuted by corner mask
   const int ntab = int(word & 15);
   if (ntab == 0) return 0;
 
-  // an edge's endpoints are runtime corner numbers: their ids, levels and
-  // scalars are re-read from shared memory / L1 rather than kept in
-  // dynamically indexed arrays (which live in local memory)
   const auto edge_point = [&](int e, double (&pt)[3]) {
     const uint32_t ends = e < 8 ? uint32_t(AMRX_MC_EDGE_LO >> (8 * e))
                                 : uint32_t(AMRX_MC_EDGE_HI >> (8 * (e - 8)));
     int u = int(ends & 15), v = int((ends >> 4) & 15);
-    const int pu = point_of(delta, u), pv = point_of(delta, v);
-    uint32_t idu = sm.id[warp][pu][lane], idv = sm.id[warp][pv][lane];
-    int lu = sm.lev[warp][pu][lane], lvv = sm.lev[warp][pv][lane];
-    if (idu == idv) err |= 1u;  // collapsed edge selected (contour.cpp:67-70)
-    if (idv < idu) {            // lower CellId first (contour.cpp:42-44)
+    uint2 cu = corner(u), cv = corner(v);  // (id, level)
+    if (cu.x == cv.x) err |= 1u;  // collapsed edge selected (contour.cpp:67-70)
+    if (cv.x < cu.x) {            // lower CellId first (contour.cpp:42-44)
       const int t = u;
       u = v;
       v = t;
-      const uint32_t ti = idu;
-      idu = idv;
-      idv = ti;
-      const int tl = lu;
-      lu = lvv;
-      lvv = tl;
+      const uint2 tc = cu;
+      cu = cv;
+      cv = tc;
     }
-    const double vu = __ldg(a.scal + idu), vv = __ldg(a.scal + idv);
+    const double vu = __ldg(scal + cu.x), vv = __ldg(scal + cv.x);
     const double t = __ddiv_rn(__dsub_rn(iso, vu), __dsub_rn(vv, vu));
     const int ou[3] = {((u & 1) + (delta & 1)) - 1, (((u >> 1) & 1) + ((delta >> 1) & 1)) - 1,
                        (((u >> 2) & 1) + ((delta >> 2) & 1)) - 1};
     const int ov[3] = {((v & 1) + (delta & 1)) - 1, (((v >> 1) & 1) + ((delta >> 1) & 1)) - 1,
                        (((v >> 2) & 1) + ((delta >> 2) & 1)) - 1};
     const int64_t self[3] = {c.i, c.j, c.k};
+    const int lu = int(cu.y), lvv = int(cv.y);
 #pragma unroll
     for (int ax = 0; ax < 3; ax++) {
       const double pa = centre(anchor_mask(self[ax] + ou[ax] * w, lu), lu);
@@ -289,25 +318,86 @@ __device__ __noinline__ int mc_dual(const KArgs &a, const Smem &sm, int warp, in
     const bool e12 = p1[0] == p2[0] && p1[1] == p2[1] && p1[2] == p2[2];
     const bool e02 = p0[0] == p2[0] && p0[1] == p2[1] && p0[2] == p2[2];
     if (e01 || e12 || e02) continue;
-    if (write) {
-      const uint64_t slot = at + uint64_t(count);
-      if (slot < cap) {
-        if (F32) {
-          float *o = static_cast<float *>(out) + slot * 9;
-          o[0] = float(p0[0]); o[1] = float(p0[1]); o[2] = float(p0[2]);
-          o[3] = float(p1[0]); o[4] = float(p1[1]); o[5] = float(p1[2]);
-          o[6] = float(p2[0]); o[7] = float(p2[1]); o[8] = float(p2[2]);
-        } else {
-          double *o = static_cast<double *>(out) + slot * 9;
-          o[0] = p0[0]; o[1] = p0[1]; o[2] = p0[2];
-          o[3] = p1[0]; o[4] = p1[1]; o[5] = p1[2];
-          o[6] = p2[0]; o[7] = p2[1]; o[8] = p2[2];
-        }
+    const uint64_t slot = at + uint64_t(count);
+    if (slot < cap) {
+      if (F32) {
+        float *o = static_cast<float *>(out) + slot * 9;
+        o[0] = float(p0[0]); o[1] = float(p0[1]); o[2] = float(p0[2]);
+        o[3] = float(p1[0]); o[4] = float(p1[1]); o[5] = float(p1[2]);
+        o[6] = float(p2[0]); o[7] = float(p2[1]); o[8] = float(p2[2]);
+      } else {
+        double *o = static_cast<double *>(out) + slot * 9;
+        o[0] = p0[0]; o[1] = p0[1]; o[2] = p0[2];
+        o[3] = p1[0]; o[4] = p1[1]; o[5] = p1[2];
+        o[6] = p2[0]; o[7] = p2[1]; o[8] = p2[2];
       }
     }
     count++;
   }
+  for (int g = count; g < ntab; g++) {  // mark the slots slivers left unused
+    const uint64_t slot = at + uint64_t(g);
+    if (slot < cap) static_cast<uint32_t *>(out)[slot * (F32 ? 9 : 18)] = kGapMark;
+  }
   return count;
+}
+
+struct McArgs {
+  KeyGeom g;
+  const double *scal;
+  double iso;
+  const McJob *jobs;
+  uint64_t job_cap;
+  void *xyz;
+  uint64_t tri_cap;
+  uint32_t *tile_tri_cnt;
+  unsigned long long *out;  // [5] tris counted, [6] written, [7] errors, [10] jobs
+};
+
+constexpr int kMcThreads = 256;
+
+/*! marching cubes over the crossing duals extract_kernel queued, one per
+    thread: every lane busy (inside extract_kernel only the few lanes of a
+    tile that own a crossing dual were), and its own register budget.  A
+    job's corner ids and levels sit in this thread's shared-memory column. */
+template <bool F32>
+__global__ void __launch_bounds__(kMcThreads)
+mc_jobs_kernel(const __grid_constant__ McArgs a)
+{
+  __shared__ uint64_t rows[256];
+  __shared__ uint32_t jid[8][kMcThreads];
+  __shared__ uint8_t jlev[8][kMcThreads];
+  for (int i = threadIdx.x; i < 256; i += kMcThreads) rows[i] = c_mc_rows[table_row(uint32_t(i))];
+  __syncthreads();
+  const uint64_t n = std::min<uint64_t>(*(volatile unsigned long long *)(a.out + 10), a.job_cap);
+  const int t = threadIdx.x;
+  uint32_t err = 0;
+  unsigned long long wrote_sum = 0;
+  for (uint64_t j = uint64_t(blockIdx.x) * kMcThreads + t; j < n;
+       j += uint64_t(gridDim.x) * kMcThreads) {
+    const McJob &job = a.jobs[j];
+#pragma unroll
+    for (int d = 0; d < 8; d++) {
+      jid[d][t] = job.id[d];
+      jlev[d][t] = job.lev[d];
+    }
+    const Cell c = unpack(a.g, job.key);
+    const uint32_t meta = job.meta;
+    const int wrote = mc_core<F32>(a.scal, rows, c, int(meta & 7), a.iso, a.xyz, job.out,
+                                   a.tri_cap, err,
+                                   [&](int d) { return make_uint2(jid[d][t], jlev[d][t]); });
+    const uint32_t deficit = (meta >> 8) - uint32_t(wrote);
+    if (deficit) atomicSub(a.tile_tri_cnt + job.tile, deficit);
+    wrote_sum += uint64_t(wrote);
+  }
+  wrote_sum = __reduce_add_sync(kFull, uint32_t(wrote_sum));
+  err = __reduce_or_sync(kFull, err);
+  if ((t & 31) == 0) {
+    if (wrote_sum) {
+      atomicAdd(a.out + 5, wrote_sum);
+      atomicAdd(a.out + 6, wrote_sum);
+    }
+    if (err) atomicOr(a.out + 7, (unsigned long long)err);
+  }
 }
 
 struct Hit {
@@ -614,7 +704,7 @@ extract_kernel(const __grid_constant__ KArgs a)
     // (offset, count) to the tile table; reorder_kernel later moves blocks
     // into candidate order (the reference's prefix sum, pipeline.cpp:109-114).
     const uint32_t nd = __popc(accepted);
-    uint32_t upper = 0, cross = 0;
+    uint32_t upper = 0, cross = 0, ntabs = 0;
     if (EMIT_TRI) {
       // duals whose 8 corners all classify alike carry no triangle: decide
       // from the sign bits (value > iso, contour.cpp:22-28) before touching
@@ -628,8 +718,10 @@ extract_kernel(const __grid_constant__ KArgs a)
           mask |= ((__ldg(a.above + (id >> 5)) >> (id & 31)) & 1u) << d;
         }
         if (mask != 0 && mask != 0xffu) {
+          const uint32_t nt = uint32_t(sm.mc_rows[mask] & 15);
           cross |= 1u << delta;
-          upper += uint32_t(sm.mc_rows[mask] & 15);
+          ntabs |= nt << (4 * delta);
+          upper += nt;
         }
       }
     }
@@ -673,26 +765,50 @@ extract_kernel(const __grid_constant__ KArgs a)
       }
     }
     if (EMIT_TRI) {
-      // reserve the table's upper bound, emit each crossing dual once, then
-      // close the gaps slivers left (contour.cpp:80-84 drops them; rare)
+      // reserve the table's upper bound for the tile, then queue its
+      // crossing duals (candidate order: lane, then delta) with their slots
+      // for mc_jobs_kernel, which subtracts what slivers drop
       const uint32_t incl = warp_incl_scan(upper);
       const uint32_t agg_up = __shfl_sync(kFull, incl, 31);
       const uint64_t block =
         reserve(&sm.chunk[warp][2], agg_up, kTriChunk, a.out + 9);
-      const uint64_t start = block + (incl - upper);
-      uint32_t wrote = 0;
-      for (uint32_t m = cross; m; m &= m - 1)
-        wrote += mc_dual<F32>(a, sm, warp, lane, c, __ffs(m) - 1, a.iso, true,
-                              a.xyz, start + wrote, a.tri_cap, err);
-      const uint32_t incl_w = warp_incl_scan(wrote);
-      const uint32_t agg = __shfl_sync(kFull, incl_w, 31);
-      if (agg != agg_up)
-        compact_tile<F32>(a.xyz, a.tri_cap, start, block + (incl_w - wrote), wrote);
+      const uint32_t nc = __popc(cross);
+      const uint32_t incl_c = warp_incl_scan(nc);
+      const uint32_t total = __shfl_sync(kFull, incl_c, 31);
+      unsigned long long jb = 0;
       if (lane == 0) {
-        a.tile_tri_cnt[tile] = agg;
+        a.tile_tri_cnt[tile] = agg_up;
+        a.tile_tri_up[tile] = agg_up;
+        sm.acc[warp][7] += agg_up;  // slots reserved (sizes the next staging)
         a.tile_tri_off[tile] = block;
-        sm.acc[warp][5] += agg;
-        sm.acc[warp][6] += agg;
+        if (total) jb = atomicAdd(a.out + 10, (unsigned long long)total);
+      }
+      jb = __shfl_sync(kFull, jb, 0);
+      uint64_t at = block + (incl - upper), j = jb + (incl_c - nc);
+      for (uint32_t mm = cross; mm; mm &= mm - 1, j++) {
+        const int delta = __ffs(mm) - 1;
+        const uint32_t nt = (ntabs >> (4 * delta)) & 15u;
+        if (j < a.job_cap) {
+          McJob &job = a.jobs[j];
+          uint32_t ids[8];
+          uint8_t lvs[8];
+#pragma unroll
+          for (int d = 0; d < 8; d++) {
+            ids[d] = sm.id[warp][point_of(delta, d)][lane];
+            lvs[d] = sm.lev[warp][point_of(delta, d)][lane];
+          }
+          uint4 *q = reinterpret_cast<uint4 *>(&job);
+          q[0] = make_uint4(ids[0], ids[1], ids[2], ids[3]);
+          q[1] = make_uint4(ids[4], ids[5], ids[6], ids[7]);
+          q[2] = make_uint4(uint32_t(kself), uint32_t(kself >> 32), uint32_t(at),
+                            uint32_t(at >> 32));
+          q[3] = make_uint4(uint32_t(lvs[0]) | uint32_t(lvs[1]) << 8 | uint32_t(lvs[2]) << 16 |
+                              uint32_t(lvs[3]) << 24,
+                            uint32_t(lvs[4]) | uint32_t(lvs[5]) << 8 | uint32_t(lvs[6]) << 16 |
+                              uint32_t(lvs[7]) << 24,
+                            tile, uint32_t(delta) | nt << 8);
+        }
+        at += nt;
       }
     }
     __syncwarp();
@@ -704,6 +820,7 @@ extract_kernel(const __grid_constant__ KArgs a)
 #pragma unroll
     for (int i = 0; i < 7; i++)
       if (sm.acc[warp][i]) atomicAdd(a.out + i, sm.acc[warp][i]);
+    if (sm.acc[warp][7]) atomicAdd(a.out + 11, sm.acc[warp][7]);
     if (err) atomicOr(a.out + 7, (unsigned long long)err);
   }
 }
@@ -903,16 +1020,17 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
   // control block | tile tables (count u32 + staging offset u64 + final
   // offset u64, per output kind)
   x.ctl.reserve(256, st);
-  x.tiles.reserve(size_t(tiles + 1) * 40 + 64, st);
+  x.tiles.reserve(size_t(tiles + 1) * 48 + 64, st);
   auto *ctl = x.ctl.as<unsigned long long>();
   auto *tb = x.tiles.as<unsigned char>();
   uint32_t *dual_cnt = reinterpret_cast<uint32_t *>(tb);
   uint32_t *tri_cnt = dual_cnt + (tiles + 1);
-  uint64_t *dual_off = reinterpret_cast<uint64_t *>(tb + ((2 * (tiles + 1) * 4 + 15) & ~size_t(15)));
+  uint32_t *tri_up = tri_cnt + (tiles + 1);
+  uint64_t *dual_off = reinterpret_cast<uint64_t *>(tb + ((3 * (tiles + 1) * 4 + 15) & ~size_t(15)));
   uint64_t *tri_off = dual_off + (tiles + 1);
   uint64_t *final_off = tri_off + (tiles + 1);
   AMRX_CUDA(cudaMemsetAsync(ctl, 0, 256, st));
-  if (tiles) AMRX_CUDA(cudaMemsetAsync(tb, 0, size_t(tiles + 1) * 8, st));
+  if (tiles) AMRX_CUDA(cudaMemsetAsync(tb, 0, size_t(tiles + 1) * 12, st));
 
   // staging capacity: what the caller can take plus one chunk per warp of
   // slack for partially used chunks (so a fitting result never overflows)
@@ -959,6 +1077,13 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
   k.tile_dual_cnt = dual_cnt;
   k.tile_dual_off = dual_off;
   k.tile_tri_cnt = tri_cnt;
+  k.tile_tri_up = tri_up;
+  // marching-cubes jobs: sized by the largest jobs/cell ratio seen so far
+  // (an overflow reruns the extraction once, like the staging arenas)
+  const uint32_t jratio = r.jobs_per_kcell && *r.jobs_per_kcell ? *r.jobs_per_kcell : 160;
+  uint64_t job_cap = T ? cells / 1024 * jratio + 4096 : 0;
+  k.job_cap = job_cap;
+  k.jobs = nullptr;
   k.tile_tri_off = tri_off;
   k.out = ctl;
   k.ticket = reinterpret_cast<unsigned int *>(ctl + 16);
@@ -969,13 +1094,18 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
   AMRX_CUDA(cudaEventCreate(&e0));
   AMRX_CUDA(cudaEventCreate(&e1));
   AMRX_CUDA(cudaEventCreate(&e2));
-  unsigned long long h[10];
+  unsigned long long h[12];
   for (int attempt = 0;; attempt++) {
     if (dual_stage) {
       x.stage_a.reserve(dual_stage * 32, st);
       x.stage_b.reserve(dual_stage * 8, st);
     }
     if (tri_stage) x.stage_a.reserve(tri_stage * tri_words * 4, st);
+    if (T) {
+      x.jobs.reserve(job_cap * sizeof(McJob), st);
+      k.jobs = x.jobs.as<McJob>();
+      k.job_cap = job_cap;
+    }
     k.corners = dual_stage ? x.stage_a.as<uint32_t>() : nullptr;
     k.tasks = dual_stage ? x.stage_b.as<uint64_t>() : nullptr;
     k.dual_cap = dual_stage;
@@ -991,6 +1121,25 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
       else if (T) launch_extract<false, true, false>(k, grid, st);
       else launch_extract<false, false, false>(k, grid, st);
       res.launches += 1;
+      if (T && tri_stage) {
+        McArgs m;
+        m.g = k.g;
+        m.scal = k.scal;
+        m.iso = k.iso;
+        m.jobs = k.jobs;
+        m.job_cap = k.job_cap;
+        m.xyz = k.xyz;
+        m.tri_cap = k.tri_cap;
+        m.tile_tri_cnt = k.tile_tri_cnt;
+        m.out = ctl;
+        const int mgrid = device_sm_count() * 8;
+        if (F)
+          mc_jobs_kernel<true><<<mgrid, kMcThreads, 0, st>>>(m);
+        else
+          mc_jobs_kernel<false><<<mgrid, kMcThreads, 0, st>>>(m);
+        AMRX_LAUNCH_CHECK();
+        res.launches += 1;
+      }
     }
     AMRX_CUDA(cudaEventRecord(e1, st));
     AMRX_CUDA(cudaMemcpyAsync(h, ctl, sizeof h, cudaMemcpyDeviceToHost, st));
@@ -999,11 +1148,18 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
     // buffer (upper-bound reservations): grow it and run again
     const bool dual_short = dual_stage && h[8] > dual_stage && h[4] <= r.dual_cap;
     const bool tri_short = tri_stage && h[9] > tri_stage && h[6] <= r.tri_cap;
-    if (attempt || (!dual_short && !tri_short)) break;
+    const bool job_short = T && tri_stage && h[10] > job_cap;
+    if (job_short) job_cap = h[10] + 4096;
+    if (T && tri_stage && r.jobs_per_kcell && cells)
+      *r.jobs_per_kcell = uint32_t(std::min<uint64_t>(h[10] * 1024 / cells + 16, 8192));
+    if (attempt || (!dual_short && !tri_short && !job_short)) break;
     if (dual_short) dual_stage = h[8] + warps * kDualChunk;
     if (tri_short) {
       tri_stage = h[9] + warps * kTriChunk;
-      const uint64_t ratio = h[6] ? h[9] * 1024 / h[6] + 32 : 2048;
+      // reserved slots per kept triangle (the chunk cursor h[9] also counts
+      // each warp's partly used chunks, which the slack term covers)
+      const uint64_t ratio =
+        std::min<uint64_t>(h[6] ? h[11] * 1024 / h[6] + 32 : 1024 + 128, 4096);
       uint32_t cur = reserve_ratio_x1024.load();
       while (ratio > cur && !reserve_ratio_x1024.compare_exchange_weak(cur, uint32_t(ratio))) {
       }
@@ -1074,9 +1230,9 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
       // the previous copy out of this buffer must have drained
       if (r.slot_free) AMRX_CUDA(cudaStreamWaitEvent(st, r.slot_free, 0));
     }
-    reorder_kernel<<<std::max(1, rgrid), 256, 0, st>>>(
-      tri_cnt, tri_off, final_off, uint32_t(tiles), tri_words,
-      x.stage_a.as<uint32_t>(), dx, r.tri_cap, 0, nullptr, nullptr);
+    reorder_tri_kernel<<<std::max(1, rgrid), 256, 0, st>>>(
+      tri_cnt, tri_up, tri_off, final_off, uint32_t(tiles), tri_words,
+      x.stage_a.as<uint32_t>(), dx, r.tri_cap);
     AMRX_LAUNCH_CHECK();
     res.launches += 1;
     if (r.final_host) {

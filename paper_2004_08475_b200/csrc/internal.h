@@ -61,7 +61,7 @@ void enable_pool_caching(int device);
     thread) the lease falls back to a private allocation. */
 enum WsSlot {
   kWsCells, kWsScal, kWsIdx, kWsKeysAlt, kWsIdxAlt, kWsSort, kWsStageA,
-  kWsStageB, kWsTiles, kWsBits, kWsCtl, kWsScratch, kWsOutA, kWsOutB, kWsCount
+  kWsStageB, kWsTiles, kWsBits, kWsCtl, kWsScratch, kWsOutA, kWsOutB, kWsJobs, kWsCount
 };
 
 struct WsLease {
@@ -93,7 +93,7 @@ struct WsBuf {
 /// the temporaries of one extraction, all from the device workspace
 struct ExtractScratch {
   WsBuf ctl{kWsCtl}, tiles{kWsTiles}, stage_a{kWsStageA}, stage_b{kWsStageB},
-    bits{kWsBits};
+    bits{kWsBits}, jobs{kWsJobs};
   DevBuf scan;  // unused by the pool-free scan; kept for its signature
 };
 
@@ -199,6 +199,9 @@ struct ExtractRequest {
   cudaEvent_t slot_free = nullptr;
   cudaEvent_t copy_done = nullptr;
   bool bits_ready = false;  // the sign bits in the workspace are for this iso
+  // marching-cubes jobs per 1024 cells seen by this index's last extraction
+  // (sizes the job buffer; an overflow reruns once and updates it)
+  uint32_t *jobs_per_kcell = nullptr;
 };
 
 struct ExtractResult {

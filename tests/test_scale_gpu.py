@@ -84,8 +84,13 @@ def test_synth_generators_match_reference(ref):
 
 
 def _big(P, name):
+    import gc
     import torch
     from paper_2004_08475_b200 import synth
+    # the previous big test's tensors sit in torch's cache and its index may
+    # not be collected yet: give the memory back before the next 100+ GB
+    gc.collect()
+    torch.cuda.empty_cache()
     cfg = synth.CONFIGS[name]
     if cfg["kind"] == "octree_noise":
         cells, scal = synth.octree_noise(*cfg["args"])
@@ -114,13 +119,13 @@ def _exactly_once(P, corners):
     symmetric 64-bit hashes (a duplicate dual collides in both)"""
     import torch
     c = torch.as_tensor(corners).cuda() if not hasattr(corners, "cuda") else corners
-    c = c.to(torch.int64) & 0xFFFFFFFF
     n = c.shape[0]
     hs = []
     for mult, add in ((0x9E3779B97F4A7C15, 0x632BE59BD9B4E019), (0xC2B2AE3D27D4EB4F, 0x165667B19E3779F9)):
         h = torch.zeros(n, dtype=torch.int64, device=c.device)
-        for k in range(8):
-            x = c[:, k] * (mult - (1 << 64) if mult >= 1 << 63 else mult) + add
+        for k in range(8):  # one widened column at a time (memory)
+            x = (c[:, k].to(torch.int64) & 0xFFFFFFFF) * \
+                (mult - (1 << 64) if mult >= 1 << 63 else mult) + add
             x = x ^ (x >> 29)
             x = x * 0x5851F42D4C957F2D
             x = x ^ (x >> 32)
