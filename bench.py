@@ -371,7 +371,8 @@ def run_amrx(args):
                            "Y_step": ms},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic,
-                     "kernel": "extract_kernel<iso, f64>", "peak_kind": kind,
+                     "kernel": "iso extraction: extract_kernel<iso, f64> + mc_jobs_kernel<f64> "
+                               "(CUDA events around both launches)", "peak_kind": kind,
                      "alg_bytes_per_launch": alg_bytes},
         "weld": weld_info if weld_ms is not None else None,
         "cpu_baseline": cpu,
