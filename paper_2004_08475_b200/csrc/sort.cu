@@ -20,7 +20,10 @@ namespace {
 #endif
 constexpr int kRadixBits = AMRX_RADIX_BITS;  // digit width (<= 9: one thread per digit)
 constexpr int kDigits = 1 << kRadixBits;
-constexpr int kSortThreads = 512;
+#ifndef AMRX_SORT_THREADS
+#define AMRX_SORT_THREADS 512
+#endif
+constexpr int kSortThreads = AMRX_SORT_THREADS;
 constexpr int kSortWarps = kSortThreads / 32;
 #ifndef AMRX_SORT_ITEMS
 #define AMRX_SORT_ITEMS 8
