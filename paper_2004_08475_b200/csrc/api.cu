@@ -760,7 +760,9 @@ void create_impl(const int32_t *cells4, const double *scalars, uint64_t n_cells,
     }
 
     ix->keys.reserve((n + kKeyPad) * sizeof(uint64_t), st);
-    uint32_t *idx = static_cast<uint32_t *>(l_idx.get(kWsIdx, n * 4, st));
+    // resident scalars travel through the sort as the payload (read in
+    // input order by the first pass); arriving scalars need the positions
+    uint32_t *idx = aux ? static_cast<uint32_t *>(l_idx.get(kWsIdx, n * 4, st)) : nullptr;
     ingest_pack(cells_d, n, ix->g, ix->keys.as<uint64_t>(), idx, st);
 
     uint64_t desc = 0, eq = 0;
@@ -781,16 +783,32 @@ void create_impl(const int32_t *cells4, const double *scalars, uint64_t n_cells,
       // last pass writes the scalars in key order (the gather, fused)
       DevBuf keys_alt;
       keys_alt.reserve((n + kKeyPad) * sizeof(uint64_t), st);
-      auto *idx_alt = static_cast<uint32_t *>(l_ialt.get(kWsIdxAlt, n * 4, st));
       void *sort_scratch = l_sort.get(kWsSort, radix_sort_scratch_bytes(n), st);
       int passes = 0;
-      // resident scalars: gathered by the last pass; arriving scalars: the
-      // last pass leaves the inverse permutation for the chunk scatters
-      const bool in_alt =
-        radix_sort_pairs(ix->keys.as<uint64_t>(), idx, keys_alt.as<uint64_t>(), idx_alt, n,
-                         ix->g.total, sort_scratch, st, &passes, aux ? nullptr : sc_d,
-                         aux ? nullptr : ix->scal.as<double>(), nullptr,
-                         aux ? &rank : nullptr);
+      bool in_alt = false;
+      if (aux) {
+        // arriving scalars: the last pass leaves the inverse permutation
+        // for the chunk scatters
+        auto *idx_alt = static_cast<uint32_t *>(l_ialt.get(kWsIdxAlt, n * 4, st));
+        in_alt = radix_sort_pairs(ix->keys.as<uint64_t>(), idx, keys_alt.as<uint64_t>(),
+                                  idx_alt, n, ix->g.total, sort_scratch, st, &passes, nullptr,
+                                  nullptr, nullptr, &rank);
+      } else {
+        // resident scalars: the sort's 64-bit payload from the first pass
+        // on (coalesced reads in input order; no gather, no positions)
+        DevBuf scal_alt;
+        scal_alt.reserve(n * sizeof(double), st);
+        in_alt = radix_sort_pairs_u64(ix->keys.as<uint64_t>(),
+                                      reinterpret_cast<const uint64_t *>(sc_d),
+                                      ix->scal.as<uint64_t>(), keys_alt.as<uint64_t>(),
+                                      scal_alt.as<uint64_t>(), n, ix->g.total, sort_scratch, st,
+                                      &passes);
+        if (in_alt) {
+          std::swap(ix->scal.ptr, scal_alt.ptr);
+          std::swap(ix->scal.bytes, scal_alt.bytes);
+          std::swap(ix->scal.stream, scal_alt.stream);
+        }
+      }
       if (in_alt) {
         std::swap(ix->keys.ptr, keys_alt.ptr);
         std::swap(ix->keys.bytes, keys_alt.bytes);

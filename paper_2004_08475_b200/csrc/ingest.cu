@@ -94,7 +94,7 @@ pack_kernel(const int4 *__restrict__ cells, uint64_t n, const KeyGeom g,
        r += stride) {
     const int4 c = __ldg(cells + r);
     keys[r] = pack_unchecked(g, c.x, c.y, c.z, c.w);
-    idx[r] = uint32_t(r);
+    if (idx) idx[r] = uint32_t(r);
   }
 }
 

@@ -167,6 +167,14 @@ bool radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
                       const double *gsrc = nullptr, double *gdst = nullptr,
                       cudaEvent_t gsrc_ready = nullptr, uint32_t **rank_out = nullptr);
 
+/// radix_sort_pairs with a 64-bit payload that enters from vals_src (read
+/// by the first pass only: e.g. the caller's scalars in input order) and
+/// ping-pongs between vals and vals_alt; true when keys and values ended in
+/// the alt buffers
+bool radix_sort_pairs_u64(uint64_t *keys, const uint64_t *vals_src, uint64_t *vals,
+                          uint64_t *keys_alt, uint64_t *vals_alt, uint64_t n, int key_bits,
+                          void *scratch, cudaStream_t st, int *passes_run);
+
 /// out[rank[i]] = in[i] for i in [0, n) (a payload chunk into key order)
 void scatter_f64(const uint32_t *rank, const double *in, double *out, uint64_t n,
                  cudaStream_t st);

@@ -95,9 +95,10 @@ __global__ void digit_offsets_kernel(const unsigned int *hist, int passes,
   }
 }
 
+template <typename V>
 struct PassSmem {
   uint64_t keys[kSortTile];
-  uint32_t vals[kSortTile];
+  V vals[kSortTile];
   uint32_t whist[kSortWarps][kDigits];  // per-warp counts -> warp offsets
   uint32_t bexcl[kDigits];              // tile-local digit start
   uint32_t hist[kDigits];               // tile digit counts (early publish)
@@ -114,18 +115,19 @@ struct PassSmem {
     pass): write vals_out[value] = sorted position (the inverse permutation,
     for scattering a payload that is still arriving). */
 enum { kPassPlain = 0, kPassGather = 1, kPassInverse = 2 };
-template <int MODE>
+template <int MODE, typename V>
 __global__ void __launch_bounds__(kSortThreads)
 onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
-                     const uint32_t *__restrict__ vals_in,
+                     const V *__restrict__ vals_in,
                      uint64_t *__restrict__ keys_out,
-                     uint32_t *__restrict__ vals_out, uint64_t n, int shift,
+                     V *__restrict__ vals_out, uint64_t n, int shift,
                      const unsigned long long *__restrict__ digit_start,
                      unsigned long long *state, unsigned int *ticket,
                      const double *__restrict__ gsrc, double *__restrict__ gdst)
 {
+  static_assert(MODE == kPassPlain || sizeof(V) == 4, "gather/inverse carry u32 values");
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  PassSmem &sm = *reinterpret_cast<PassSmem *>(smem_raw);
+  PassSmem<V> &sm = *reinterpret_cast<PassSmem<V> *>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
   if (threadIdx.x == 0) sm.tile = atomicAdd(ticket, 1u);
@@ -139,7 +141,7 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
   // warp-striped load: item t of lane l in warp w is tile position
   // w*256 + t*32 + l, so (w, t, l) order is input order
   uint64_t k[kSortItems];
-  uint32_t v[kSortItems];
+  V v[kSortItems];
   uint32_t dig[kSortItems];
   uint32_t rank[kSortItems];
 #pragma unroll
@@ -147,7 +149,7 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
     const uint64_t r = base + uint64_t(warp) * (32 * kSortItems) + t * 32 + lane;
     const bool in = r < n;
     k[t] = in ? ldg_u64(keys_in + r) : ~0ull;
-    v[t] = in ? __ldg(vals_in + r) : 0u;
+    v[t] = in ? __ldg(vals_in + r) : V(0);
     dig[t] = in ? uint32_t((k[t] >> shift) & (kDigits - 1)) : uint32_t(kDigits);
   }
   // the tile's digit counts by shared atomics, published right away so the
@@ -247,7 +249,7 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
       const uint32_t d = uint32_t((kk >> shift) & (kDigits - 1));
       const uint64_t dst = sm.gofs[d] + (pos - sm.bexcl[d]);
       keys_out[dst] = kk;
-      vals_out[sm.vals[pos]] = uint32_t(dst);
+      vals_out[sm.vals[pos]] = V(dst);
     }
     return;
   }
@@ -291,11 +293,15 @@ size_t radix_sort_scratch_bytes(uint64_t n)
   return size_t(kMaxPasses) * kDigits * 12 + 256 + size_t(tiles) * kDigits * 8;
 }
 
-bool radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
-                      uint32_t *vals_alt, uint64_t n, int key_bits,
-                      void *scratch, cudaStream_t st, int *passes_run,
-                      const double *gsrc, double *gdst, cudaEvent_t gsrc_ready,
-                      uint32_t **rank_out)
+namespace {
+
+/*! the pass driver for u32 or u64 values; vals_src (may differ from vals)
+    is what the first executed pass reads, so a payload can enter the sort
+    straight from the caller's read-only input */
+template <typename V>
+bool sort_impl(uint64_t *keys, const V *vals_src, V *vals, uint64_t *keys_alt, V *vals_alt,
+               uint64_t n, int key_bits, void *scratch, cudaStream_t st, int *passes_run,
+               const double *gsrc, double *gdst, cudaEvent_t gsrc_ready, uint32_t **rank_out)
 {
   if (passes_run) *passes_run = 0;
   if (rank_out) *rank_out = nullptr;
@@ -330,17 +336,19 @@ bool radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
   AMRX_CUDA(cudaStreamSynchronize(st));
 
   static bool attr_set = false;
-  const size_t smem = sizeof(PassSmem);
+  const size_t smem = sizeof(PassSmem<V>);
   if (!attr_set) {
-    AMRX_CUDA(cudaFuncSetAttribute(onesweep_pass_kernel<kPassPlain>,
+    AMRX_CUDA(cudaFuncSetAttribute(onesweep_pass_kernel<kPassPlain, V>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(smem)));
-    AMRX_CUDA(cudaFuncSetAttribute(onesweep_pass_kernel<kPassGather>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(smem)));
-    AMRX_CUDA(cudaFuncSetAttribute(onesweep_pass_kernel<kPassInverse>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(smem)));
+    if (sizeof(V) == 4) {
+      AMRX_CUDA(cudaFuncSetAttribute(onesweep_pass_kernel<kPassGather, uint32_t>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(sizeof(PassSmem<uint32_t>))));
+      AMRX_CUDA(cudaFuncSetAttribute(onesweep_pass_kernel<kPassInverse, uint32_t>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(sizeof(PassSmem<uint32_t>))));
+    }
     attr_set = true;
   }
   int last = -1;
@@ -351,25 +359,32 @@ bool radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
     if (!trivial[p]) last = p;
   }
   uint64_t *kin = keys, *kout = keys_alt;
-  uint32_t *vin = vals, *vout = vals_alt;
+  V *vin = vals, *vout = vals_alt;
   int run = 0;
   for (int p = 0; p < passes; p++) {
     if (trivial[p]) continue;
     AMRX_CUDA(cudaMemsetAsync(state, 0, state_bytes, st));
     AMRX_CUDA(cudaMemsetAsync(ticket, 0, 4, st));
-    if (rank_out && p == last) {
-      onesweep_pass_kernel<kPassInverse><<<unsigned(tiles), kSortThreads, smem, st>>>(
-        kin, vin, kout, vout, n, p * kRadixBits, offs + size_t(p) * kDigits,
-        state, ticket, nullptr, nullptr);
-      *rank_out = vout;
-    } else if (gsrc && p == last) {
-      if (gsrc_ready) AMRX_CUDA(cudaStreamWaitEvent(st, gsrc_ready, 0));
-      onesweep_pass_kernel<kPassGather><<<unsigned(tiles), kSortThreads, smem, st>>>(
-        kin, vin, kout, vout, n, p * kRadixBits, offs + size_t(p) * kDigits,
-        state, ticket, gsrc, gdst);
+    const V *src = run == 0 ? vals_src : vin;
+    if constexpr (sizeof(V) == 4) {
+      if (rank_out && p == last) {
+        onesweep_pass_kernel<kPassInverse, uint32_t><<<unsigned(tiles), kSortThreads, smem, st>>>(
+          kin, src, kout, vout, n, p * kRadixBits, offs + size_t(p) * kDigits,
+          state, ticket, nullptr, nullptr);
+        *rank_out = vout;
+      } else if (gsrc && p == last) {
+        if (gsrc_ready) AMRX_CUDA(cudaStreamWaitEvent(st, gsrc_ready, 0));
+        onesweep_pass_kernel<kPassGather, uint32_t><<<unsigned(tiles), kSortThreads, smem, st>>>(
+          kin, src, kout, vout, n, p * kRadixBits, offs + size_t(p) * kDigits,
+          state, ticket, gsrc, gdst);
+      } else {
+        onesweep_pass_kernel<kPassPlain, V><<<unsigned(tiles), kSortThreads, smem, st>>>(
+          kin, src, kout, vout, n, p * kRadixBits, offs + size_t(p) * kDigits,
+          state, ticket, nullptr, nullptr);
+      }
     } else {
-      onesweep_pass_kernel<kPassPlain><<<unsigned(tiles), kSortThreads, smem, st>>>(
-        kin, vin, kout, vout, n, p * kRadixBits, offs + size_t(p) * kDigits,
+      onesweep_pass_kernel<kPassPlain, V><<<unsigned(tiles), kSortThreads, smem, st>>>(
+        kin, src, kout, vout, n, p * kRadixBits, offs + size_t(p) * kDigits,
         state, ticket, nullptr, nullptr);
     }
     AMRX_LAUNCH_CHECK();
@@ -382,7 +397,29 @@ bool radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
     if (gsrc_ready) AMRX_CUDA(cudaStreamWaitEvent(st, gsrc_ready, 0));
     AMRX_CUDA(cudaMemcpyAsync(gdst, gsrc, n * 8, cudaMemcpyDeviceToDevice, st));
   }
-  return kin != keys;  // the sorted keys (and u32 values) are in the alt buffers
+  if (run == 0 && vals_src != vals)  // nothing permuted: the payload as given
+    AMRX_CUDA(cudaMemcpyAsync(vals, vals_src, n * sizeof(V), cudaMemcpyDeviceToDevice, st));
+  return kin != keys;  // the sorted keys (and values) are in the alt buffers
+}
+
+}  // namespace
+
+bool radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
+                      uint32_t *vals_alt, uint64_t n, int key_bits,
+                      void *scratch, cudaStream_t st, int *passes_run,
+                      const double *gsrc, double *gdst, cudaEvent_t gsrc_ready,
+                      uint32_t **rank_out)
+{
+  return sort_impl<uint32_t>(keys, vals, vals, keys_alt, vals_alt, n, key_bits, scratch, st,
+                             passes_run, gsrc, gdst, gsrc_ready, rank_out);
+}
+
+bool radix_sort_pairs_u64(uint64_t *keys, const uint64_t *vals_src, uint64_t *vals,
+                          uint64_t *keys_alt, uint64_t *vals_alt, uint64_t n, int key_bits,
+                          void *scratch, cudaStream_t st, int *passes_run)
+{
+  return sort_impl<uint64_t>(keys, vals_src, vals, keys_alt, vals_alt, n, key_bits, scratch,
+                             st, passes_run, nullptr, nullptr, nullptr, nullptr);
 }
 
 }  // namespace amrx
