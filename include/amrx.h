@@ -229,6 +229,11 @@ AMRX_API amrx_status amrx_weld(const double *xyz9, uint64_t n_tris, double *vert
                                uint64_t vcap, uint32_t *tris3, uint64_t *n_verts,
                                const amrx_index_opts *opts);
 
+/* give back the device memory the library keeps cached between calls (idle
+ * workspace buffers, the stream-ordered pool's free blocks) on `device`
+ * (-1 = current); indexes stay valid */
+AMRX_API amrx_status amrx_release_cached_memory(int device);
+
 /* kernels this process has launched through the library so far */
 AMRX_API uint64_t amrx_kernel_launches(void);
 

@@ -126,6 +126,7 @@ def library():
         "amrx_index_from_keys": [P, P, U64, P, P, P],
         "amrx_weld": [P, U64, P, U64, P, P, P],
         "amrx_validate": [P, P, U64, P, P, U64, P],
+        "amrx_release_cached_memory": [I32],
         "amrx_find_exact": [P, P, U64, P],
         "amrx_snap": [P, P, P, I32, U64, P],
         "amrx_try_build_duals": [P, P, U64, P, P],
@@ -268,6 +269,13 @@ class CellIndex:
             self.close()
         except Exception:
             pass
+
+
+def release_cached_memory(device=-1):
+    """return the device memory the library caches between calls (idle
+    workspace buffers, pool free blocks) -- e.g. before a large torch
+    allocation in the same process"""
+    _check(library().amrx_release_cached_memory(device))
 
 
 def kernel_launches():

@@ -996,6 +996,16 @@ amrx_status amrx_validate(amrx_index *index, uint32_t *dup_pairs, uint64_t dup_c
   });
 }
 
+amrx_status amrx_release_cached_memory(int device)
+{
+  return guarded([&] {
+    int dev = device;
+    if (dev < 0) AMRX_CUDA(cudaGetDevice(&dev));
+    DeviceGuard dg(dev);
+    release_idle_memory(dev);
+  });
+}
+
 amrx_status amrx_weld(const double *xyz9, uint64_t n_tris, double *verts3, uint64_t vcap,
                       uint32_t *tris3, uint64_t *n_verts, const amrx_index_opts *opts)
 {

@@ -91,6 +91,7 @@ def _big(P, name):
     # not be collected yet: give the memory back before the next 100+ GB
     gc.collect()
     torch.cuda.empty_cache()
+    P.release_cached_memory()
     cfg = synth.CONFIGS[name]
     if cfg["kind"] == "octree_noise":
         cells, scal = synth.octree_noise(*cfg["args"])
