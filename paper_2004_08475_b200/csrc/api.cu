@@ -763,12 +763,25 @@ void create_impl(const int32_t *cells4, const double *scalars, uint64_t n_cells,
     // resident scalars travel through the sort as the payload (read in
     // input order by the first pass); arriving scalars need the positions
     uint32_t *idx = aux ? static_cast<uint32_t *>(l_idx.get(kWsIdx, n * 4, st)) : nullptr;
-    ingest_pack(cells_d, n, ix->g, ix->keys.as<uint64_t>(), idx, st);
+    // one pass over the cells: keys, the sort's digit histograms (into the
+    // sort's scratch) and the order check
+    void *sort_scratch = l_sort.get(kWsSort, radix_sort_scratch_bytes(n), st);
+    auto *digit_hist = static_cast<unsigned int *>(sort_scratch);
+    ix->scratch.reserve(16, st);
+    auto *order2 = ix->scratch.as<unsigned long long>();
+    ingest_pack(cells_d, n, ix->g, ix->keys.as<uint64_t>(), idx, st, digit_hist,
+                (ix->g.total + kSortRadixBits - 1) / kSortRadixBits, order2);
 
     uint64_t desc = 0, eq = 0;
     uint32_t *rank = nullptr;
     bool scatter_pending = false;
-    ingest_order_check(ix->keys.as<uint64_t>(), n, ix->scratch, &desc, &eq, st);
+    {
+      unsigned long long h2[2];
+      AMRX_CUDA(cudaMemcpyAsync(h2, order2, 16, cudaMemcpyDeviceToHost, st));
+      AMRX_CUDA(cudaStreamSynchronize(st));
+      desc = h2[0];
+      eq = h2[1];
+    }
     ix->scal.reserve(n * sizeof(double), st);
     if (desc == 0) {
       // already in (i,j,k,level) order; stable ties mean identity
@@ -783,7 +796,6 @@ void create_impl(const int32_t *cells4, const double *scalars, uint64_t n_cells,
       // last pass writes the scalars in key order (the gather, fused)
       DevBuf keys_alt;
       keys_alt.reserve((n + kKeyPad) * sizeof(uint64_t), st);
-      void *sort_scratch = l_sort.get(kWsSort, radix_sort_scratch_bytes(n), st);
       int passes = 0;
       bool in_alt = false;
       if (aux) {
@@ -792,7 +804,7 @@ void create_impl(const int32_t *cells4, const double *scalars, uint64_t n_cells,
         auto *idx_alt = static_cast<uint32_t *>(l_ialt.get(kWsIdxAlt, n * 4, st));
         in_alt = radix_sort_pairs(ix->keys.as<uint64_t>(), idx, keys_alt.as<uint64_t>(),
                                   idx_alt, n, ix->g.total, sort_scratch, st, &passes, nullptr,
-                                  nullptr, nullptr, &rank);
+                                  nullptr, nullptr, &rank, digit_hist);
       } else {
         // resident scalars: the sort's 64-bit payload from the first pass
         // on (coalesced reads in input order; no gather, no positions)
@@ -802,7 +814,7 @@ void create_impl(const int32_t *cells4, const double *scalars, uint64_t n_cells,
                                       reinterpret_cast<const uint64_t *>(sc_d),
                                       ix->scal.as<uint64_t>(), keys_alt.as<uint64_t>(),
                                       scal_alt.as<uint64_t>(), n, ix->g.total, sort_scratch, st,
-                                      &passes);
+                                      &passes, digit_hist);
         if (in_alt) {
           std::swap(ix->scal.ptr, scal_alt.ptr);
           std::swap(ix->scal.bytes, scal_alt.bytes);

@@ -98,6 +98,62 @@ pack_kernel(const int4 *__restrict__ cells, uint64_t n, const KeyGeom g,
   }
 }
 
+/*! pack + the sort's digit histograms + the order check in one read of the
+    cells: per-block shared histograms flushed once; a key's successor
+    comes from the next lane (whole warps step together), or is packed again
+    at a warp's last lane */
+__global__ void __launch_bounds__(kThreads)
+pack_hist_kernel(const int4 *__restrict__ cells, uint64_t n, const KeyGeom g,
+                 uint64_t *__restrict__ keys, uint32_t *__restrict__ idx,
+                 unsigned int *__restrict__ hist, int passes,
+                 unsigned long long *__restrict__ order2)
+{
+  __shared__ unsigned int h[kSortMaxPasses][kSortDigits];
+  for (int i = threadIdx.x; i < passes * kSortDigits; i += blockDim.x) (&h[0][0])[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  unsigned long long desc = 0, eq = 0;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); base < n;
+       base += stride) {
+    const uint64_t r = base + lane;
+    const bool in = r < n;
+    uint64_t k = 0;
+    if (in) {
+      const int4 c = __ldg(cells + r);
+      k = pack_unchecked(g, c.x, c.y, c.z, c.w);
+      keys[r] = k;
+      if (idx) idx[r] = uint32_t(r);
+#pragma unroll 1
+      for (int p = 0; p < passes; p++)
+        atomicAdd(&h[p][(k >> (p * kSortRadixBits)) & (kSortDigits - 1)], 1u);
+    }
+    uint64_t nxt = __shfl_down_sync(kFull, (unsigned long long)k, 1);
+    if (lane == 31 && r + 1 < n) {
+      const int4 c = __ldg(cells + r + 1);
+      nxt = pack_unchecked(g, c.x, c.y, c.z, c.w);
+    }
+    if (in && r + 1 < n) {
+      desc += k > nxt;
+      eq += k == nxt;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    desc += __shfl_xor_sync(kFull, desc, off);
+    eq += __shfl_xor_sync(kFull, eq, off);
+  }
+  if (lane == 0) {
+    if (desc) atomicAdd(order2, desc);
+    if (eq) atomicAdd(order2 + 1, eq);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * kSortDigits; i += blockDim.x) {
+    const unsigned int v = (&h[0][0])[i];
+    if (v) atomicAdd(hist + i, v);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads)
 order_check_kernel(const uint64_t *__restrict__ keys, uint64_t n,
                    unsigned long long *out2)
@@ -542,8 +598,17 @@ PrepassResult ingest_prepass(const int4 *cells, uint64_t n, DevBuf &scratch,
 }
 
 void ingest_pack(const int4 *cells, uint64_t n, const KeyGeom &g,
-                 uint64_t *keys, uint32_t *idx, cudaStream_t st)
+                 uint64_t *keys, uint32_t *idx, cudaStream_t st,
+                 unsigned int *hist, int passes, unsigned long long *order2)
 {
+  if (hist) {
+    AMRX_CUDA(cudaMemsetAsync(hist, 0, size_t(kSortMaxPasses) * kSortDigits * 4, st));
+    AMRX_CUDA(cudaMemsetAsync(order2, 0, 16, st));
+    pack_hist_kernel<<<grid_for(n, kThreads, 8), kThreads, 0, st>>>(cells, n, g, keys, idx,
+                                                                   hist, passes, order2);
+    AMRX_LAUNCH_CHECK();
+    return;
+  }
   pack_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(cells, n, g, keys,
                                                             idx);
   AMRX_LAUNCH_CHECK();

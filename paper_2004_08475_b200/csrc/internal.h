@@ -109,9 +109,20 @@ struct PrepassResult {
 PrepassResult ingest_prepass(const int4 *cells, uint64_t n, DevBuf &scratch,
                              cudaStream_t st);
 
-/// key = pack(cell), idx = position
+/// radix digits of the sort (sort.cu) -- also the layout of the digit
+/// histograms ingest_pack can produce for it
+constexpr int kSortRadixBits = 9;
+constexpr int kSortDigits = 1 << kSortRadixBits;
+constexpr int kSortMaxPasses = 8;
+
+/// key = pack(cell), idx = position (idx may be null).  With hist (device,
+/// kSortMaxPasses x kSortDigits u32, zeroed here) the same pass counts the
+/// sort's digits of the first `passes` digits, and order2 (device, 2 u64,
+/// zeroed here) receives the keys' descents and equal neighbours
 void ingest_pack(const int4 *cells, uint64_t n, const KeyGeom &g,
-                 uint64_t *keys, uint32_t *idx, cudaStream_t st);
+                 uint64_t *keys, uint32_t *idx, cudaStream_t st,
+                 unsigned int *hist = nullptr, int passes = 0,
+                 unsigned long long *order2 = nullptr);
 
 /// number of i with key[i] > key[i+1] (0 = already sorted), and equal pairs
 void ingest_order_check(const uint64_t *keys, uint64_t n, DevBuf &scratch,
@@ -165,7 +176,8 @@ bool radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
                       uint32_t *vals_alt, uint64_t n, int key_bits,
                       void *scratch, cudaStream_t st, int *passes_run,
                       const double *gsrc = nullptr, double *gdst = nullptr,
-                      cudaEvent_t gsrc_ready = nullptr, uint32_t **rank_out = nullptr);
+                      cudaEvent_t gsrc_ready = nullptr, uint32_t **rank_out = nullptr,
+                      const unsigned int *hist_in = nullptr);
 
 /// radix_sort_pairs with a 64-bit payload that enters from vals_src (read
 /// by the first pass only: e.g. the caller's scalars in input order) and
@@ -173,7 +185,8 @@ bool radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
 /// the alt buffers
 bool radix_sort_pairs_u64(uint64_t *keys, const uint64_t *vals_src, uint64_t *vals,
                           uint64_t *keys_alt, uint64_t *vals_alt, uint64_t n, int key_bits,
-                          void *scratch, cudaStream_t st, int *passes_run);
+                          void *scratch, cudaStream_t st, int *passes_run,
+                          const unsigned int *hist_in = nullptr);
 
 /// out[rank[i]] = in[i] for i in [0, n) (a payload chunk into key order)
 void scatter_f64(const uint32_t *rank, const double *in, double *out, uint64_t n,

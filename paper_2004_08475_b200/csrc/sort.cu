@@ -15,10 +15,9 @@ namespace amrx {
 
 namespace {
 
-#ifndef AMRX_RADIX_BITS
-#define AMRX_RADIX_BITS 9  // C4: 4 passes of 9 bits 63.5 ms ingest vs 5 of 8 bits 64.7
-#endif
-constexpr int kRadixBits = AMRX_RADIX_BITS;  // digit width (<= 9: one thread per digit)
+// digit width (<= 9: one thread per digit); C4: 4 passes of 9 bits 63.5 ms
+// ingest vs 5 of 8 bits 64.7
+constexpr int kRadixBits = kSortRadixBits;
 constexpr int kDigits = 1 << kRadixBits;
 #ifndef AMRX_SORT_THREADS
 #define AMRX_SORT_THREADS 512
@@ -30,7 +29,7 @@ constexpr int kSortWarps = kSortThreads / 32;
 #endif
 constexpr int kSortItems = AMRX_SORT_ITEMS;  // keys per thread
 constexpr int kSortTile = kSortThreads * kSortItems;
-constexpr int kMaxPasses = 8;
+constexpr int kMaxPasses = kSortMaxPasses;
 
 constexpr unsigned long long kFlagAgg = 1ull << 62;
 constexpr unsigned long long kFlagPre = 2ull << 62;
@@ -301,7 +300,8 @@ namespace {
 template <typename V>
 bool sort_impl(uint64_t *keys, const V *vals_src, V *vals, uint64_t *keys_alt, V *vals_alt,
                uint64_t n, int key_bits, void *scratch, cudaStream_t st, int *passes_run,
-               const double *gsrc, double *gdst, cudaEvent_t gsrc_ready, uint32_t **rank_out)
+               const double *gsrc, double *gdst, cudaEvent_t gsrc_ready, uint32_t **rank_out,
+               const unsigned int *hist_in)
 {
   if (passes_run) *passes_run = 0;
   if (rank_out) *rank_out = nullptr;
@@ -321,11 +321,15 @@ bool sort_impl(uint64_t *keys, const V *vals_src, V *vals, uint64_t *keys_alt, V
   auto *state = reinterpret_cast<unsigned long long *>(base + hist_bytes +
                                                        offs_bytes + 256);
 
-  AMRX_CUDA(cudaMemsetAsync(hist, 0, hist_bytes, st));
-  const int hgrid = int(std::min<uint64_t>((n + 1023) / 1024,
-                                           uint64_t(device_sm_count()) * 8));
-  histogram_kernel<<<std::max(1, hgrid), 256, 0, st>>>(keys, n, passes, hist);
-  AMRX_LAUNCH_CHECK();
+  if (hist_in) {
+    hist = const_cast<unsigned int *>(hist_in);  // counted while packing
+  } else {
+    AMRX_CUDA(cudaMemsetAsync(hist, 0, hist_bytes, st));
+    const int hgrid = int(std::min<uint64_t>((n + 1023) / 1024,
+                                             uint64_t(device_sm_count()) * 8));
+    histogram_kernel<<<std::max(1, hgrid), 256, 0, st>>>(keys, n, passes, hist);
+    AMRX_LAUNCH_CHECK();
+  }
   digit_offsets_kernel<<<1, 32 * kMaxPasses, 0, st>>>(hist, passes, offs);
   AMRX_LAUNCH_CHECK();
 
@@ -408,18 +412,19 @@ bool radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
                       uint32_t *vals_alt, uint64_t n, int key_bits,
                       void *scratch, cudaStream_t st, int *passes_run,
                       const double *gsrc, double *gdst, cudaEvent_t gsrc_ready,
-                      uint32_t **rank_out)
+                      uint32_t **rank_out, const unsigned int *hist_in)
 {
   return sort_impl<uint32_t>(keys, vals, vals, keys_alt, vals_alt, n, key_bits, scratch, st,
-                             passes_run, gsrc, gdst, gsrc_ready, rank_out);
+                             passes_run, gsrc, gdst, gsrc_ready, rank_out, hist_in);
 }
 
 bool radix_sort_pairs_u64(uint64_t *keys, const uint64_t *vals_src, uint64_t *vals,
                           uint64_t *keys_alt, uint64_t *vals_alt, uint64_t n, int key_bits,
-                          void *scratch, cudaStream_t st, int *passes_run)
+                          void *scratch, cudaStream_t st, int *passes_run,
+                          const unsigned int *hist_in)
 {
   return sort_impl<uint64_t>(keys, vals_src, vals, keys_alt, vals_alt, n, key_bits, scratch,
-                             st, passes_run, nullptr, nullptr, nullptr, nullptr);
+                             st, passes_run, nullptr, nullptr, nullptr, nullptr, hist_in);
 }
 
 }  // namespace amrx
