@@ -165,17 +165,34 @@ def run_amrx(args):
 
     # output buffer sized from a first (untimed) run
     idx = P.build_index(cells, scal, device=local, stream=sh)
-    probe = P.extract_isosurface(idx, P.IsoParams(iso=iso))
-    ntri_full = len(probe.fat)
-    duals_full = probe.stats.duals_accepted
+    from paper_2004_08475_b200 import synth as S
+    dual_only = bool(S.CONFIGS[args.config].get("dual_only"))
+    if dual_only:  # C5: the dual mesh only (8 x u32 corners + u64 task id per dual)
+        dprobe = P.extract_dual_mesh(idx)
+        duals_full, ntri_full = len(dprobe.corners), 0
+        del dprobe
+        dcap = int(duals_full * 1.02) + 1024
+        out_c = torch.empty((dcap, 8), dtype=torch.int32, device=dev)
+        out_t = torch.empty(dcap, dtype=torch.int64, device=dev)
+        out = torch.empty((1, 9), dtype=torch.float64, device=dev)
+        cap = 1
+    else:
+        probe = P.extract_isosurface(idx, P.IsoParams(iso=iso))
+        ntri_full = len(probe.fat)
+        duals_full = probe.stats.duals_accepted
+        del probe
+        cap = int(ntri_full * 1.05) + 1024
+        out = torch.empty((cap, 9), dtype=torch.float64, device=dev)
     geometry = idx.geometry()
     idx.close()
-    del probe
-    cap = int(ntri_full * 1.05) + 1024
-    out = torch.empty((cap, 9), dtype=torch.float64, device=dev)
 
     def step_single():
         ix = P.build_index(cells, scal, device=local, stream=sh)
+        if dual_only:
+            d = P.extract_dual_mesh(ix, out=(out_c, out_t))
+            ingest = ix.info.seconds_ingest
+            ix.close()
+            return d.stats, ingest, 0
         r = P.extract_isosurface(ix, P.IsoParams(iso=iso), out=out)
         ingest = ix.info.seconds_ingest
         ix.close()
@@ -284,7 +301,7 @@ def run_amrx(args):
                "h2d_bytes_per_step": int(n * 24), "d2h_bytes_per_step": int(nt * 72),
                "note": "every rank uploads its slice and downloads its part; bytes are job totals"}
         del hcells, hscal, hout
-    if world == 1 and not args.no_e2e:
+    if world == 1 and not args.no_e2e and not dual_only:
         hcells = torch.empty(cells.shape, dtype=torch.int32, pin_memory=True)
         hscal = torch.empty(scal.shape, dtype=torch.float64, pin_memory=True)
         hcells.copy_(cells)
@@ -317,7 +334,7 @@ def run_amrx(args):
     # the weld (not part of the step: the reference arm excludes it too),
     # once on the device-resident soup of the last step
     weld_ms = None
-    if world == 1:
+    if world == 1 and not dual_only:
         wsoup = out[:tris]
         P.weld(wsoup)  # warm-up (the pool grows to the weld's buffers once)
         torch.cuda.synchronize()
@@ -337,7 +354,10 @@ def run_amrx(args):
 
     hbm, kind = peaks()
     kern_ms = 1000.0 * statistics.mean(kernel_s)
-    alg_bytes = n * 16 / world + tris * 72 / world
+    # algorithmic bytes: iso 16 B/cell + 72 B/triangle; dual
+    # mesh 8 B/cell + 40 B/dual (corners + task id)
+    alg_bytes = (n * 8 + duals_full * 40) / world if dual_only else \
+        n * 16 / world + tris * 72 / world
     achieved = alg_bytes / (kern_ms / 1000.0) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
@@ -371,8 +391,9 @@ def run_amrx(args):
                            "Y_step": ms},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic,
-                     "kernel": "iso extraction: extract_kernel<iso, f64> + mc_jobs_kernel<f64> "
-                               "(CUDA events around both launches)", "peak_kind": kind,
+                     "kernel": ("dual mesh: extract_kernel<dual>" if dual_only else
+                                "iso extraction: extract_kernel<iso, f64> + mc_jobs_kernel<f64> "
+                                "(CUDA events around both launches)"), "peak_kind": kind,
                      "alg_bytes_per_launch": alg_bytes},
         "weld": weld_info if weld_ms is not None else None,
         "cpu_baseline": cpu,
@@ -417,7 +438,18 @@ def cpu_baseline(cells, scal, iso, args, impl_line=False):
     t0 = time.perf_counter()
     h = R.build(hc, hs)
     t_build = time.perf_counter() - t0
-    if kind == "reference":
+    from paper_2004_08475_b200 import synth as S
+    dual_only = bool(S.CONFIGS[args.config].get("dual_only"))
+    if kind == "reference" and dual_only:
+        R.extract_dual(h, threads)  # warm-up
+        t1 = time.perf_counter()
+        res = R.extract_dual(h, threads)
+        t_ext = time.perf_counter() - t1
+        duals = len(res["corners"])
+        tris = 0
+        weld = None
+        cores = threads
+    elif kind == "reference":
         # warm-up (first run per process is 2-7x slower)
         R.extract_iso(h, iso, threads)
         res = R.extract_iso(h, iso, threads)

@@ -31,6 +31,8 @@
 #include "mc_tables.inc"
 
 #include <atomic>
+#include <mutex>
+#include <unordered_map>
 #include <cstdio>
 #include <cstdlib>
 
@@ -1080,7 +1082,17 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
   k.tile_tri_up = tri_up;
   // marching-cubes jobs: sized by the largest jobs/cell ratio seen so far
   // (an overflow reruns the extraction once, like the staging arenas)
-  const uint32_t jratio = r.jobs_per_kcell && *r.jobs_per_kcell ? *r.jobs_per_kcell : 160;
+  // jobs per 1024 cells: this index's last extraction, else the last one of
+  // an index of the same size (a pipeline rebuilding the same dataset)
+  static std::mutex ratio_mu;
+  static std::unordered_map<uint64_t, uint32_t> ratio_by_size;
+  const uint64_t size_key = r.s.n * 1315423911ull ^ cells;
+  uint32_t jratio = r.jobs_per_kcell ? *r.jobs_per_kcell : 0;
+  if (!jratio) {
+    std::lock_guard<std::mutex> lock(ratio_mu);
+    const auto it = ratio_by_size.find(size_key);
+    jratio = it != ratio_by_size.end() ? it->second : 160;
+  }
   uint64_t job_cap = T ? cells / 1024 * jratio + 4096 : 0;
   k.job_cap = job_cap;
   k.jobs = nullptr;
@@ -1150,8 +1162,13 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
     const bool tri_short = tri_stage && h[9] > tri_stage && h[6] <= r.tri_cap;
     const bool job_short = T && tri_stage && h[10] > job_cap;
     if (job_short) job_cap = h[10] + 4096;
-    if (T && tri_stage && r.jobs_per_kcell && cells)
-      *r.jobs_per_kcell = uint32_t(std::min<uint64_t>(h[10] * 1024 / cells + 16, 8192));
+    if (T && tri_stage && cells) {
+      const uint32_t learned = uint32_t(std::min<uint64_t>(h[10] * 1024 / cells + 16, 8192));
+      if (r.jobs_per_kcell) *r.jobs_per_kcell = learned;
+      std::lock_guard<std::mutex> lock(ratio_mu);
+      if (ratio_by_size.size() > 4096) ratio_by_size.clear();
+      ratio_by_size[size_key] = learned;
+    }
     if (attempt || (!dual_short && !tri_short && !job_short)) break;
     if (dual_short) dual_stage = h[8] + warps * kDualChunk;
     if (tri_short) {

@@ -194,5 +194,6 @@ CONFIGS = {
     # C4: 626M-cell 4-level soup (bricks 512 x 256 x 256 -> tuned knobs)
     "c4": dict(kind="bricks", bricks=(512, 256, 256), seed=1, shuffle=True, iso=None),
     # C5: ~250M-cell mixed-level AMR, dual mesh only
-    "c5": dict(kind="bricks", bricks=(384, 192, 192), seed=5, shuffle=False, iso=None),
+    "c5": dict(kind="bricks", bricks=(384, 192, 192), seed=5, shuffle=False, iso=None,
+               dual_only=True),
 }
