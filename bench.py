@@ -382,7 +382,8 @@ def run_amrx(args):
         "vs_baseline": None,
         "dtype": "int64 keys / f64 scalars",
         "data": DATA_DESC.get(args.config, "synthetic"),
-        "config": {"workload": f"{args.config}: {n} cells, {n_levels} levels, iso {iso}",
+        "config": {"workload": f"{args.config}: {n} cells, {n_levels} levels, " +
+                               ("dual mesh only" if dual_only else f"iso {iso}"),
                    "cells": n, "triangles": tris, "duals": duals_full, "iso": iso,
                    "parallelism": (f"distributed sort + range partition x{world}" if args.dist_mode == "partition" else f"rank-0 sort + broadcast x{world}") if world > 1 else "single GPU",
                    "l2": "inputs (24 B/cell) far larger than L2", **meta},
