@@ -31,6 +31,7 @@
 #include "mc_tables.inc"
 
 #include <atomic>
+#include <utility>
 #include <mutex>
 #include <unordered_map>
 #include <cstdio>
@@ -495,16 +496,16 @@ __device__ __forceinline__ void mark_point(Smem &sm, int warp, int lane, const C
 constexpr uint32_t kFast0 = kCorner0Points & ~(1u << 13);  // 0 1 3 4 9 10 12
 constexpr uint32_t kFast1 = kCube << 13 & ~(1u << 13);       // 14 16 17 22 23 25 26
 
-/*! stencil point P (compile-time) if this lane needs it: the common case --
-    its own anchor exists on the hint level -- resolved inline (one
-    occupancy word + one directory entry, the key from compile-time steps);
-    anything else (finer, coarser, absent) is left in `pend` */
+/*! stencil points Ps (compile-time) for the lanes that need them, from one
+    occupancy record each (the key from compile-time steps): every record
+    load of the list is issued before any is used, so they are in flight
+    together.  The common case -- the point's own anchor exists on the hint
+    level -- is resolved here; anything else (finer, coarser, absent) is
+    left in `pend` for the runtime loop. */
 template <int P>
-__device__ __forceinline__ void fast_point(const KArgs &a, Smem &sm, int warp, int lane,
-                                           const Cell &c, const Stencil &st, uint32_t need,
-                                           Marks &m, uint32_t &pend)
+__device__ __forceinline__ void fast_issue(const KArgs &a, const Stencil &st, uint32_t need,
+                                           uint2 &r, uint32_t &bit)
 {
-  if (!((need >> P) & 1u)) return;
   constexpr int ox = P % 3 - 1, oy = (P / 3) % 3 - 1, oz = P / 9 - 1;
   uint64_t q = st.k0;
   if (ox > 0) q += st.sx;
@@ -513,23 +514,50 @@ __device__ __forceinline__ void fast_point(const KArgs &a, Smem &sm, int warp, i
   if (oy < 0) q -= st.sy;
   if (oz > 0) q += st.sz;
   if (oz < 0) q -= st.sz;
-  if ((st.inrange >> P) & 1u) {
-    const uint2 r = ldg_rec(a.s.rec, q, a.s.dir_shift);
-    const uint32_t bit = uint32_t(q) & 31u;
-    if ((r.y >> bit) & 1u) {
-      // same level: lower CellId (dual.cpp:64-66) <=> lower key <=> the
-      // point precedes the cell in (i,j,k) order, known at compile time
-      constexpr bool lower = ox < 0 || (ox == 0 && (oy < 0 || (oy == 0 && oz < 0)));
-      if (lower)
-        m.low |= 1u << P;
-      else
-        m.ok |= 1u << P;
-      sm.id[warp][P][lane] = r.x + uint32_t(__popc(r.y & ((1u << bit) - 1u)));
-      sm.lev[warp][P][lane] = uint8_t(c.level);
-      return;
-    }
+  bit = uint32_t(q) & 31u;
+  r = make_uint2(0, 0);
+  if (((need & st.inrange) >> P) & 1u) r = ldg_rec(a.s.rec, q, a.s.dir_shift);
+}
+
+template <int P>
+__device__ __forceinline__ void fast_finish(Smem &sm, int warp, int lane, const Cell &c,
+                                            uint32_t need, uint2 r, uint32_t bit, Marks &m,
+                                            uint32_t &pend)
+{
+  if (!((need >> P) & 1u)) return;
+  if ((r.y >> bit) & 1u) {  // (an out-of-range point has r = 0: a miss)
+    constexpr int ox = P % 3 - 1, oy = (P / 3) % 3 - 1, oz = P / 9 - 1;
+    constexpr bool lower = ox < 0 || (ox == 0 && (oy < 0 || (oy == 0 && oz < 0)));
+    if (lower)
+      m.low |= 1u << P;
+    else
+      m.ok |= 1u << P;
+    sm.id[warp][P][lane] = r.x + uint32_t(__popc(r.y & ((1u << bit) - 1u)));
+    sm.lev[warp][P][lane] = uint8_t(c.level);
+    return;
   }
   pend |= 1u << P;
+}
+
+template <int... Ps, size_t... I>
+__device__ __forceinline__ void fast_batch_impl(std::index_sequence<I...>, const KArgs &a,
+                                                Smem &sm, int warp, int lane, const Cell &c,
+                                                const Stencil &st, uint32_t need, Marks &m,
+                                                uint32_t &pend)
+{
+  uint2 r[sizeof...(Ps)];
+  uint32_t bit[sizeof...(Ps)];
+  (fast_issue<Ps>(a, st, need, r[I], bit[I]), ...);
+  (fast_finish<Ps>(sm, warp, lane, c, need, r[I], bit[I], m, pend), ...);
+}
+
+template <int... Ps>
+__device__ __forceinline__ void fast_batch(const KArgs &a, Smem &sm, int warp, int lane,
+                                           const Cell &c, const Stencil &st, uint32_t need,
+                                           Marks &m, uint32_t &pend)
+{
+  fast_batch_impl<Ps...>(std::make_index_sequence<sizeof...(Ps)>{}, a, sm, warp, lane, c, st,
+                         need, m, pend);
 }
 
 /*! resolve the stencil points in `todo` into the marks: two per lane
@@ -661,22 +689,10 @@ extract_kernel(const __grid_constant__ KArgs a)
           // the runtime loop
           uint32_t pend = 0;
           if (round == 0) {
-            fast_point<0>(a, sm, warp, lane, c, st, need, m, pend);
-            fast_point<1>(a, sm, warp, lane, c, st, need, m, pend);
-            fast_point<3>(a, sm, warp, lane, c, st, need, m, pend);
-            fast_point<4>(a, sm, warp, lane, c, st, need, m, pend);
-            fast_point<9>(a, sm, warp, lane, c, st, need, m, pend);
-            fast_point<10>(a, sm, warp, lane, c, st, need, m, pend);
-            fast_point<12>(a, sm, warp, lane, c, st, need, m, pend);
+            fast_batch<0, 1, 3, 4, 9, 10, 12>(a, sm, warp, lane, c, st, need, m, pend);
             need &= ~kFast0;
           } else if (__any_sync(kFull, (need & kFast1) != 0)) {
-            fast_point<14>(a, sm, warp, lane, c, st, need, m, pend);
-            fast_point<16>(a, sm, warp, lane, c, st, need, m, pend);
-            fast_point<17>(a, sm, warp, lane, c, st, need, m, pend);
-            fast_point<22>(a, sm, warp, lane, c, st, need, m, pend);
-            fast_point<23>(a, sm, warp, lane, c, st, need, m, pend);
-            fast_point<25>(a, sm, warp, lane, c, st, need, m, pend);
-            fast_point<26>(a, sm, warp, lane, c, st, need, m, pend);
+            fast_batch<14, 16, 17, 22, 23, 25, 26>(a, sm, warp, lane, c, st, need, m, pend);
             need &= ~kFast1;
           }
           need |= pend;
