@@ -19,7 +19,7 @@
 // 27-point stencil {-w,0,w}^3 its live candidates need: a point's key is the
 // cell key plus packed steps (Stencil), a lookup is one occupancy record load
 // + popcount, and the 14 points of a uniform region have compile-time
-// offsets (fast_point).  Round 0 resolves every candidate's corner 0 (82-86%
+// offsets (fast_batch).  Round 0 resolves every candidate's corner 0 (82-86%
 // of candidates die there); round 1 what the survivors still need.  Points
 // are classified into 27-bit masks and a candidate is a mask test over its
 // corner cube; the lowest failing bit is its first failing corner, so the
@@ -363,7 +363,10 @@ constexpr int kMcThreads = 256;
     tile that own a crossing dual were), and its own register budget.  A
     job's corner ids and levels sit in this thread's shared-memory column. */
 template <bool F32>
-__global__ void __launch_bounds__(kMcThreads)
+#ifndef AMRX_MC_MINB
+#define AMRX_MC_MINB 4
+#endif
+__global__ void __launch_bounds__(kMcThreads, AMRX_MC_MINB)
 mc_jobs_kernel(const __grid_constant__ McArgs a)
 {
   __shared__ uint64_t rows[256];
