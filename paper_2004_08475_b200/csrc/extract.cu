@@ -573,7 +573,10 @@ __device__ __forceinline__ void resolve_marks(const KArgs &a, Smem &sm, int warp
                                               const Cell &c, const Stencil &st,
                                               uint32_t self, uint32_t todo, Marks &m)
 {
-  constexpr int K = 2;  // measured best: K = 1 +1%, K = 3 +13%
+#ifndef AMRX_SLOW_K
+#define AMRX_SLOW_K 2  // measured best: K = 1 +1%, K = 3 +13% (before the fast batches)
+#endif
+  constexpr int K = AMRX_SLOW_K;
   // present levels coarser than the hint: what a miss probes next
   const uint32_t coarser = a.g.level_mask & ~((2u << c.level) - 1);
   while (__any_sync(kFull, todo != 0)) {
