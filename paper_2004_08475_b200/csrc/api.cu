@@ -928,7 +928,7 @@ amrx_status amrx_index_from_keys(const void *keys_dev, const double *scalars_dev
     ix->id_base = g16[12];
     ix->key_lo = uint64_t(g16[13]);
     ix->key_hi = uint64_t(g16[14]);
-    ix->rec_lo = ((ix->key_lo >> ix->g.dir_shift) >> 12) << 12;
+    ix->rec_lo = ((ix->key_lo >> ix->g.dir_shift) >> kRecTileLog) << kRecTileLog;
     ix->rec_n = ((ix->key_hi - 1) >> ix->g.dir_shift) - ix->rec_lo + 1;
     cudaEvent_t e0, e1;
     AMRX_CUDA(cudaEventCreate(&e0));

@@ -433,9 +433,12 @@ scan_downsweep_kernel(const T *in, A *out, uint64_t n,
 // once.  The counts (not popcounts) make rec[b].x the exact lower bound of
 // bucket b even with duplicate keys, so the records double as the search
 // directory (bounds rec[b].x, rec[b+1].x).
-constexpr int kRecTileLog = 12;
+
 constexpr int kRecTile = 1 << kRecTileLog;
-constexpr int kRecThreads = 512;
+#ifndef AMRX_REC_THREADS
+#define AMRX_REC_THREADS 256  // C4 ingest: 256 49.8 ms, 512 50.4, 1024 52.2
+#endif
+constexpr int kRecThreads = AMRX_REC_THREADS;
 
 /// tile_start[t] = first position whose bucket >= rec_lo + t * kRecTile,
 /// t in [0, tiles]; rec_lo is a multiple of kRecTile and no key lies below it

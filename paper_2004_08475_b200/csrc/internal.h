@@ -115,6 +115,10 @@ constexpr int kSortRadixBits = 9;
 constexpr int kSortDigits = 1 << kSortRadixBits;
 constexpr int kSortMaxPasses = 8;
 
+/// occupancy records are built per tile of 2^kRecTileLog buckets; a
+/// partition's first bucket is a multiple of the tile
+constexpr int kRecTileLog = 12;
+
 /// key = pack(cell), idx = position (idx may be null).  With hist (device,
 /// kSortMaxPasses x kSortDigits u32, zeroed here) the same pass counts the
 /// sort's digits of the first `passes` digits, and order2 (device, 2 u64,
