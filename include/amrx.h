@@ -112,6 +112,15 @@ AMRX_API amrx_status amrx_index_create(const int32_t *cells4, const double *scal
                               uint64_t n_cells, uint64_t n_scalars,
                               const amrx_index_opts *opts, amrx_index **out);
 
+/* read_amr (proj/src/io.cpp:178-181, io.hpp:43): an AMRCELL1 file (binary,
+ * 24-byte header + 24-byte records, io.cpp:76-126) or, for a ".txt" path,
+ * the text form (io.cpp:128-176) -> a device index.  Binary records stream
+ * through pinned chunks into device memory (no host copy of the dataset).
+ * Errors are AMRX_ERR_LOAD with the reference's messages, prefixed with the
+ * path ("<path>: record 1: scalar is not finite", "<path>: truncated: ..."). */
+AMRX_API amrx_status amrx_read_amr(const char *path, const amrx_index_opts *opts,
+                                   amrx_index **out);
+
 AMRX_API amrx_status amrx_index_destroy(amrx_index *index);
 
 AMRX_API amrx_status amrx_index_get_info(const amrx_index *index, amrx_index_info *out);

@@ -13,7 +13,7 @@ from .amrx import (  # noqa: F401
     adopt_index, build_index, cell_bounds, dual_bases, extract_dual_mesh,
     extract_isosurface, find_exact, index_from_keys, kernel_launches, library, snap,
     sort_part, try_build_duals, weld, IndexedMesh, validate_dataset, ValidationReport,
-    release_cached_memory,
+    release_cached_memory, read_amr, write_amr,
 )
 
 __all__ = [
@@ -23,4 +23,5 @@ __all__ = [
     "UnsupportedError", "CudaError", "adopt_index", "dual_bases", "library",
     "cell_bounds", "sort_part", "index_from_keys", "weld", "IndexedMesh",
     "validate_dataset", "ValidationReport", "release_cached_memory",
+    "read_amr", "write_amr",
 ]

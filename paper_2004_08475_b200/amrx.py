@@ -115,6 +115,7 @@ def library():
     P, U64, I64, I32 = C.c_void_p, C.c_uint64, C.c_int64, C.c_int32
     sig = {
         "amrx_index_create": [P, P, U64, U64, P, P],
+        "amrx_read_amr": [C.c_char_p, P, P],
         "amrx_index_destroy": [P],
         "amrx_index_get_info": [P, P],
         "amrx_index_download": [P, P, P],
@@ -304,6 +305,34 @@ def build_index(cells, scalars, device=-1, presorted=False, stream=None):
                                  _ptr(scalars) if n_s else C.c_void_p(1),
                                  n_cells, n_s, C.byref(opts), C.byref(h)))
     return CellIndex(h.value, lib)
+
+
+def read_amr(path, device=-1, stream=None):
+    """Read an AMRCELL1 cell file (binary, or text for a ``.txt`` path) into
+    a device CellIndex (read_amr, io.cpp:76-181).  Binary records stream
+    through pinned chunks straight to the GPU; errors raise LoadError with
+    the reference's messages, prefixed with the path."""
+    lib = library()
+    opts = _Opts(device, C.c_void_p(stream) if stream else None, 0)
+    h = C.c_void_p()
+    _check(lib.amrx_read_amr(os.fsencode(os.fspath(path)), C.byref(opts), C.byref(h)))
+    return CellIndex(h.value, lib)
+
+
+def write_amr(path, cells, scalars):
+    """Write cells + scalars as an AMRCELL1 binary file (write_amr's binary
+    branch, io.cpp:194-208; host-side, for producing inputs)."""
+    cells = np.ascontiguousarray(np.asarray(cells, np.int32).reshape(-1, 4))
+    scalars = np.ascontiguousarray(np.asarray(scalars, np.float64).reshape(-1))
+    rec = np.empty(len(cells), dtype=[("c", "<i4", 4), ("s", "<f8")])
+    rec["c"] = cells
+    rec["s"] = scalars
+    with open(path, "wb") as f:
+        f.write(b"AMRCELL1")
+        f.write(np.array([1], "<u4").tobytes())
+        f.write(np.array([len(cells)], "<u8").tobytes())
+        f.write(np.array([1], "<u4").tobytes())
+        f.write(rec.tobytes())
 
 
 def adopt_index(keys_dev_ptr, scalars_dev_ptr, n_cells, geometry, device=-1, stream=None):

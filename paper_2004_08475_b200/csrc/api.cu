@@ -7,6 +7,15 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cmath>
+#include <filesystem>
+#include <fstream>
+#include <sstream>
+#include <thread>
+
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -862,6 +871,243 @@ amrx_status amrx_index_create(const int32_t *cells4, const double *scalars,
                               const amrx_index_opts *opts, amrx_index **out)
 {
   return guarded([&] { create_impl(cells4, scalars, n_cells, n_scalars, opts, nullptr, true, out); });
+}
+
+}  // extern "C"
+
+namespace {
+
+constexpr char kAmrMagic[8] = {'A', 'M', 'R', 'C', 'E', 'L', 'L', '1'};
+constexpr uint64_t kAmrHeader = 24, kAmrRecord = 24;  // io.cpp:35-37
+
+/// build_index errors re-raised with the path in front (io.cpp:122-125)
+template <typename Fn>
+void with_path(const std::string &path, Fn &&fn)
+{
+  try {
+    fn();
+  } catch (const ApiError &e) {
+    if (e.code != AMRX_ERR_LOAD) throw;
+    fail(AMRX_ERR_LOAD, path + ": " + e.what());
+  }
+}
+
+struct Fd {
+  int fd = -1;
+  ~Fd()
+  {
+    if (fd >= 0) ::close(fd);
+  }
+};
+
+constexpr int kReadThreads = 8;
+constexpr uint64_t kReadChunk = uint64_t(1) << 19;  // records per chunk (12 MiB)
+
+/// pinned chunks + their "upload done" events, kept for the process
+/// (cudaHostAlloc of the ring costs more than reading a small file)
+struct PinnedRing {
+  int device = -1;
+  std::vector<void *> host;
+  std::vector<cudaEvent_t> done;
+};
+std::mutex g_read_ring_mu;
+
+PinnedRing &read_ring(int dev)
+{
+  static PinnedRing r;
+  if (r.device != dev) {
+    for (void *p : r.host) cudaFreeHost(p);
+    for (cudaEvent_t e : r.done) cudaEventDestroy(e);
+    r.host.clear();
+    r.done.clear();
+    for (int b = 0; b < 2 * kReadThreads; b++) {
+      void *h = nullptr;
+      AMRX_CUDA(cudaHostAlloc(&h, kReadChunk * kAmrRecord, cudaHostAllocDefault));
+      r.host.push_back(h);
+      cudaEvent_t e;
+      AMRX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      r.done.push_back(e);
+    }
+    r.device = dev;
+  }
+  return r;
+}
+
+/*! read_amr_binary (io.cpp:76-126) feeding the GPU: the header checks in
+    the reference's order and wording, then the records stream through a
+    ring of pinned chunks (pread on the host overlaps the upload and the
+    device-side split of the previous chunk) straight into device arrays,
+    which build_index then takes as device input.  No host copy of the
+    dataset is ever materialised. */
+void read_amr_binary(const std::string &path, const amrx_index_opts *opts, amrx_index **out)
+{
+  Fd f;
+  f.fd = ::open(path.c_str(), O_RDONLY);
+  struct stat sb;
+  if (f.fd < 0 || ::fstat(f.fd, &sb) != 0 || !S_ISREG(sb.st_mode))
+    fail(AMRX_ERR_LOAD, path + ": cannot open file");
+  const uint64_t size = uint64_t(sb.st_size);
+  auto read_at = [&](void *dst, uint64_t bytes, uint64_t off) {
+    auto *p = static_cast<char *>(dst);
+    while (bytes) {
+      const ssize_t got = ::pread(f.fd, p, bytes, off_t(off));
+      if (got <= 0) fail(AMRX_ERR_LOAD, path + ": read error");
+      p += got;
+      off += uint64_t(got);
+      bytes -= uint64_t(got);
+    }
+  };
+  if (size < kAmrHeader) fail(AMRX_ERR_LOAD, path + ": file shorter than the 24-byte header");
+  unsigned char hdr[kAmrHeader];
+  read_at(hdr, kAmrHeader, 0);
+  uint32_t version, fields;
+  uint64_t n;
+  std::memcpy(&version, hdr + 8, 4);
+  std::memcpy(&n, hdr + 12, 8);
+  std::memcpy(&fields, hdr + 20, 4);
+  if (std::memcmp(hdr, kAmrMagic, 8) != 0)
+    fail(AMRX_ERR_LOAD, path + ": bad magic, not a cell data file");
+  if (version != 1) fail(AMRX_ERR_LOAD, path + ": unsupported version " + std::to_string(version));
+  if (fields != 1)
+    fail(AMRX_ERR_LOAD,
+         path + ": expected exactly 1 field, file declares " + std::to_string(fields));
+  if (n == 0) fail(AMRX_ERR_LOAD, path + ": file declares zero cells");
+  const uint64_t expected = kAmrHeader + n * kAmrRecord;
+  if (size < expected)
+    fail(AMRX_ERR_LOAD, path + ": truncated: header declares " + std::to_string(n) +
+                          " cells but only " + std::to_string((size - kAmrHeader) / kAmrRecord) +
+                          " fit in the file");
+  if (size > expected)
+    fail(AMRX_ERR_LOAD, path + ": " + std::to_string(size - expected) +
+                          " trailing bytes after the last record");
+
+  int dev = opts && opts->device >= 0 ? opts->device : -1;
+  if (dev < 0) AMRX_CUDA(cudaGetDevice(&dev));
+  DeviceGuard dg(dev);
+  enable_pool_caching(dev);
+  cudaStream_t st = nullptr;
+  AMRX_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct StreamOwner {
+    cudaStream_t s;
+    ~StreamOwner() { cudaStreamDestroy(s); }
+  } so{st};
+  DevBuf cells, scal, bad, stage;
+  cells.reserve(n * 16, st);
+  scal.reserve(n * 8, st);
+  bad.reserve(8, st);
+  AMRX_CUDA(cudaMemsetAsync(bad.ptr, 0xff, 8, st));
+  // two sets of T pinned chunks: the host threads pread set g % 2 while
+  // the GPU uploads and splits the other one
+  const int T = kReadThreads;
+  const uint64_t chunks = (n + kReadChunk - 1) / kReadChunk;
+  std::unique_lock<std::mutex> lock(g_read_ring_mu);
+  PinnedRing &pr = read_ring(dev);
+  stage.reserve(size_t(2 * T) * kReadChunk * kAmrRecord, st);
+  std::vector<std::thread> pool;
+  for (uint64_t g0 = 0, gi = 0; g0 < chunks; g0 += uint64_t(T), gi++) {
+    const int set = int(gi & 1);
+    const int m = int(std::min<uint64_t>(uint64_t(T), chunks - g0));
+    for (int t = 0; t < m; t++) AMRX_CUDA(cudaEventSynchronize(pr.done[set * T + t]));
+    std::atomic<bool> bad_read{false};
+    pool.clear();
+    for (int t = 0; t < m; t++)
+      pool.emplace_back([&, t] {
+        const uint64_t first = (g0 + uint64_t(t)) * kReadChunk;
+        const uint64_t cnt = std::min(kReadChunk, n - first);
+        auto *p = static_cast<char *>(pr.host[set * T + t]);
+        uint64_t bytes = cnt * kAmrRecord, off = kAmrHeader + first * kAmrRecord;
+        while (bytes) {
+          const ssize_t got = ::pread(f.fd, p, bytes, off_t(off));
+          if (got <= 0) {
+            bad_read = true;
+            return;
+          }
+          p += got;
+          off += uint64_t(got);
+          bytes -= uint64_t(got);
+        }
+      });
+    for (auto &th : pool) th.join();
+    if (bad_read) fail(AMRX_ERR_LOAD, path + ": read error");
+    for (int t = 0; t < m; t++) {
+      const int b = set * T + t;
+      const uint64_t first = (g0 + uint64_t(t)) * kReadChunk;
+      const uint64_t cnt = std::min(kReadChunk, n - first);
+      void *dst = stage.as<char>() + size_t(b) * kReadChunk * kAmrRecord;
+      AMRX_CUDA(cudaMemcpyAsync(dst, pr.host[b], cnt * kAmrRecord, cudaMemcpyHostToDevice, st));
+      split_records(dst, cnt, first, cells.as<int4>(), scal.as<double>(),
+                    bad.as<unsigned long long>(), st);
+      AMRX_CUDA(cudaEventRecord(pr.done[b], st));
+    }
+  }
+  unsigned long long first_bad = 0;
+  AMRX_CUDA(cudaMemcpyAsync(&first_bad, bad.ptr, 8, cudaMemcpyDeviceToHost, st));
+  AMRX_CUDA(cudaStreamSynchronize(st));
+  stage.release();
+  lock.unlock();
+  if (first_bad != ~0ull)
+    fail(AMRX_ERR_LOAD, path + ": record " + std::to_string(first_bad) + ": scalar is not finite");
+  with_path(path, [&] {
+    create_impl(cells.as<int32_t>(), scal.as<double>(), n, n, opts, nullptr, true, out);
+  });
+}
+
+/// read_amr_text (io.cpp:128-176): one "i j k level scalar" per line, '#'
+/// comments and blank lines skipped, parsed with the same stream
+/// extraction so the accepted spellings are the reference's
+void read_amr_text(const std::string &path, const amrx_index_opts *opts, amrx_index **out)
+{
+  std::ifstream in(path, std::ios::binary);
+  if (!in) fail(AMRX_ERR_LOAD, path + ": cannot open file");
+  std::ostringstream buf;
+  buf << in.rdbuf();
+  if (!in && !in.eof()) fail(AMRX_ERR_LOAD, path + ": read error");
+  std::istringstream lines(std::move(buf).str());
+  std::vector<int32_t> cells;
+  std::vector<double> scalars;
+  std::string line;
+  for (uint64_t no = 1; std::getline(lines, line); no++) {
+    const auto hash = line.find('#');
+    if (hash != std::string::npos) line.resize(hash);
+    if (line.find_first_not_of(" \t\r\v\f") == std::string::npos) continue;
+    const std::string at = path + ": line " + std::to_string(no) + ": ";
+    std::istringstream fields(line);
+    long long v[4];
+    double x;
+    if (!(fields >> v[0] >> v[1] >> v[2] >> v[3] >> x))
+      fail(AMRX_ERR_LOAD, at + "expected 'i j k level scalar'");
+    std::string extra;
+    if (fields >> extra) fail(AMRX_ERR_LOAD, at + "trailing characters '" + extra + "'");
+    for (int a = 0; a < 3; a++)
+      if (v[a] < std::numeric_limits<int32_t>::min() || v[a] > std::numeric_limits<int32_t>::max())
+        fail(AMRX_ERR_LOAD, at + "anchor out of 32-bit range");
+    if (v[3] < 0 || v[3] > 30)
+      fail(AMRX_ERR_LOAD, at + "level " + std::to_string(v[3]) + " out of range");
+    if (!std::isfinite(x)) fail(AMRX_ERR_LOAD, at + "scalar is not finite");
+    for (int a = 0; a < 4; a++) cells.push_back(int32_t(v[a]));
+    scalars.push_back(x);
+  }
+  with_path(path, [&] {
+    create_impl(cells.data(), scalars.data(), scalars.size(), scalars.size(), opts, nullptr,
+                true, out);
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+amrx_status amrx_read_amr(const char *path, const amrx_index_opts *opts, amrx_index **out)
+{
+  return guarded([&] {
+    if (!path || !out) fail(AMRX_ERR_INVALID_ARG, "null argument");
+    *out = nullptr;
+    const std::string p(path);
+    if (std::filesystem::path(p).extension() == ".txt")
+      read_amr_text(p, opts, out);
+    else
+      read_amr_binary(p, opts, out);
+  });
 }
 
 amrx_status amrx_index_sort_part(const int32_t *cells4, const double *scalars,

@@ -657,6 +657,39 @@ void fill_iota(uint32_t *p, uint64_t n, cudaStream_t st)
   AMRX_LAUNCH_CHECK();
 }
 
+namespace {
+
+/// AMRCELL1 records (io.cpp:35-37: i, j, k, level as int32 then the f64
+/// scalar, 24 bytes, little-endian) into the index's input arrays; the
+/// lowest record number with a non-finite scalar goes to *bad
+/// (io.cpp:115-116 checks them in record order)
+__global__ void __launch_bounds__(kThreads)
+split_records_kernel(const uint64_t *__restrict__ rec, uint64_t n, uint64_t first,
+                     int4 *__restrict__ cells, double *__restrict__ scal,
+                     unsigned long long *__restrict__ bad)
+{
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n; r += stride) {
+    const uint64_t a = __ldg(rec + 3 * r), b = __ldg(rec + 3 * r + 1), c = __ldg(rec + 3 * r + 2);
+    cells[first + r] = make_int4(int(uint32_t(a)), int(uint32_t(a >> 32)), int(uint32_t(b)),
+                                 int(uint32_t(b >> 32)));
+    const double v = __longlong_as_double((long long)c);
+    scal[first + r] = v;
+    if (!isfinite(v)) atomicMin(bad, (unsigned long long)(first + r));
+  }
+}
+
+}  // namespace
+
+void split_records(const void *rec, uint64_t n, uint64_t first, int4 *cells, double *scal,
+                   unsigned long long *bad, cudaStream_t st)
+{
+  if (n == 0) return;
+  split_records_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(
+    static_cast<const uint64_t *>(rec), n, first, cells, scal, bad);
+  AMRX_LAUNCH_CHECK();
+}
+
 void pad_keys(uint64_t *keys, uint64_t n, cudaStream_t st)
 {
   pad_kernel<<<1, kKeyPad, 0, st>>>(keys, n);

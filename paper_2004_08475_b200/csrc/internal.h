@@ -138,6 +138,10 @@ void gather_f64(const uint32_t *perm, const double *in, double *out,
 
 /// p[i] = i for i in [0, n)
 void fill_iota(uint32_t *p, uint64_t n, cudaStream_t st);
+/// n AMRCELL1 records (24 B each, 8-byte aligned) -> cells[first..] and
+/// scal[first..]; atomicMin(*bad) with the first non-finite scalar's record
+void split_records(const void *rec, uint64_t n, uint64_t first, int4 *cells, double *scal,
+                   unsigned long long *bad, cudaStream_t st);
 
 /// fill kKeyPad sentinels (all ones) after the n sorted keys
 void pad_keys(uint64_t *keys, uint64_t n, cudaStream_t st);

@@ -10,18 +10,22 @@
 //                                      proj/include/amriso/weld.hpp:33-43
 //   ValidationReport validate_dataset(const CellIndex&)
 //                                      proj/include/amriso/locator.hpp:80
+//   CellIndex read_amr(const std::filesystem::path&)
+//                                      proj/include/amriso/io.hpp:43
 //
 // Compiled against the reference's own headers and linked in place of
-// proj/src/pipeline.cpp, proj/src/weld.cpp and of build_index and
-// validate_dataset in proj/src/locator.cpp; everything
-// else -- snap/find_exact, the dual rules used by tests,
-// contour_hex, I/O, generators, the CLI -- stays the reference's.  All computation goes through the C ABI
+// proj/src/pipeline.cpp, proj/src/weld.cpp, of build_index and
+// validate_dataset in proj/src/locator.cpp and of read_amr in proj/src/io.cpp
+// (see INTEGRATION.md); everything else -- snap/find_exact, the dual rules
+// used by tests, contour_hex, the writers, generators, the CLI -- stays the
+// reference's.  All computation goes through the C ABI
 // (include/amrx.h) to libamrx.so on the GPU; there is no CPU fallback.
 //
 // Error mapping (amrx_status -> the reference's exception types):
 //   AMRX_ERR_LOAD -> LoadError, AMRX_ERR_INVALID_ARG -> invalid_argument,
 //   AMRX_ERR_LENGTH -> length_error, AMRX_ERR_INTERNAL -> logic_error,
 //   anything else (CUDA, no device) -> runtime_error.
+#include "amriso/io.hpp"
 #include "amriso/pipeline.hpp"
 #include "amriso/weld.hpp"
 
@@ -84,12 +88,11 @@ double seconds_since(Clock::time_point t)
 
 }  // namespace
 
-CellIndex build_index(std::vector<CellCoord> cells, std::vector<double> scalars)
+namespace {
+
+/// the host CellIndex of a device index (tests read index.data directly)
+CellIndex host_index(IndexHandle &h)
 {
-  IndexHandle h;
-  check(amrx_index_create(reinterpret_cast<const int32_t *>(cells.data()),
-                          scalars.data(), cells.size(), scalars.size(), nullptr,
-                          &h.p));
   amrx_index_info info;
   check(amrx_index_get_info(h.p, &info));
   CellIndex index;
@@ -102,6 +105,24 @@ CellIndex build_index(std::vector<CellCoord> cells, std::vector<double> scalars)
                        {info.bounds_hi[0], info.bounds_hi[1], info.bounds_hi[2]}};
   index.levels.assign(info.levels, info.levels + info.level_count);
   return index;
+}
+
+}  // namespace
+
+CellIndex build_index(std::vector<CellCoord> cells, std::vector<double> scalars)
+{
+  IndexHandle h;
+  check(amrx_index_create(reinterpret_cast<const int32_t *>(cells.data()),
+                          scalars.data(), cells.size(), scalars.size(), nullptr,
+                          &h.p));
+  return host_index(h);
+}
+
+CellIndex read_amr(const std::filesystem::path &path)
+{
+  IndexHandle h;
+  check(amrx_read_amr(path.c_str(), nullptr, &h.p));
+  return host_index(h);
 }
 
 std::vector<DualCell> extract_dual_mesh(const CellIndex &index, int)
