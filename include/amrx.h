@@ -58,7 +58,8 @@ typedef enum amrx_status {
   AMRX_ERR_CUDA = 5,          /* CUDA runtime failure (message names the call) */
   AMRX_ERR_CAPACITY = 6,      /* caller buffer too small; *count holds the need */
   AMRX_ERR_UNSUPPORTED = 7,   /* dataset outside this build's limits */
-  AMRX_ERR_NO_DEVICE = 8      /* no CUDA device / kernel image for this GPU */
+  AMRX_ERR_NO_DEVICE = 8,     /* no CUDA device / kernel image for this GPU */
+  AMRX_ERR_IO = 9             /* file could not be written -> runtime_error */
 } amrx_status;
 
 typedef struct amrx_index amrx_index;
@@ -242,6 +243,24 @@ AMRX_API amrx_status amrx_weld(const double *xyz9, uint64_t n_tris, double *vert
  * workspace buffers, the stream-ordered pool's free blocks) on `device`
  * (-1 = current); indexes stay valid */
 AMRX_API amrx_status amrx_release_cached_memory(int device);
+
+/* Writers (proj/src/io.cpp:212-305): write_obj (obj_string, shortest
+ * round-trip decimals, 1-based faces), write_ply (binary little-endian,
+ * float32 positions, uchar 3 + uint32 x3 faces) and write_dual_mesh
+ * (dual_mesh_string: 8 corner cell centres then 8 scalars per line) with
+ * byte-identical output, formatted by `threads` host threads (0 = all
+ * cores) and written through "<path>.tmp" + rename like write_file_atomic
+ * (io.cpp:307-333).  Host pointers; vertices are (x,y,z) f64 triples,
+ * triangles u32 triples, corners8 the 8 CellIds of each dual, cells4 /
+ * scalars the sorted arrays of the index (amrx_index_download). */
+AMRX_API amrx_status amrx_write_obj(const char *path, const double *verts3, uint64_t n_verts,
+                                    const uint32_t *tris3, uint64_t n_tris, int threads);
+AMRX_API amrx_status amrx_write_ply(const char *path, const double *verts3, uint64_t n_verts,
+                                    const uint32_t *tris3, uint64_t n_tris, int threads);
+AMRX_API amrx_status amrx_write_dual_mesh(const char *path, const uint32_t *corners8,
+                                          uint64_t n_duals, const int32_t *cells4,
+                                          const double *scalars, uint64_t n_cells,
+                                          int threads);
 
 /* kernels this process has launched through the library so far */
 AMRX_API uint64_t amrx_kernel_launches(void);

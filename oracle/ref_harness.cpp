@@ -573,4 +573,48 @@ void ref_mc_tables(int8_t *tri256x16, uint16_t *edge256, uint8_t *corner8,
   std::memcpy(edge_corner24, mc::edge_corner, sizeof(mc::edge_corner));
 }
 
+// ---------------------------------------------------------------- writers
+// the reference's write_obj / write_ply / write_dual_mesh (io.cpp:235-305)
+// on caller arrays; 0 = ok, else ref_last_error()
+int ref_write_mesh(const char *path, int ply, const double *verts3, uint64_t nv,
+                   const uint32_t *tris3, uint64_t nt)
+{
+  return guarded([&]() -> void * {
+           IndexedMesh m;
+           m.vertices.resize(nv);
+           for (uint64_t v = 0; v < nv; v++)
+             m.vertices[v] = {verts3[3 * v], verts3[3 * v + 1], verts3[3 * v + 2]};
+           m.triangles.resize(nt);
+           for (uint64_t t = 0; t < nt; t++)
+             m.triangles[t] = {tris3[3 * t], tris3[3 * t + 1], tris3[3 * t + 2]};
+           if (ply)
+             write_ply(m, path);
+           else
+             write_obj(m, path);
+           return reinterpret_cast<void *>(1);
+         })
+           ? 0
+           : 1;
+}
+
+int ref_write_dual_mesh(const char *path, const uint32_t *corners8, uint64_t nd,
+                        const int32_t *cells4, const double *scalars, uint64_t nc)
+{
+  return guarded([&]() -> void * {
+           CellIndex index;
+           index.data.cells.resize(nc);
+           for (uint64_t c = 0; c < nc; c++)
+             index.data.cells[c] = {cells4[4 * c], cells4[4 * c + 1], cells4[4 * c + 2],
+                                    cells4[4 * c + 3]};
+           index.data.scalars.assign(scalars, scalars + nc);
+           std::vector<DualCell> duals(nd);
+           for (uint64_t d = 0; d < nd; d++)
+             for (int k = 0; k < 8; k++) duals[d].corners[k] = CellId{corners8[8 * d + k]};
+           write_dual_mesh(duals, index, path);
+           return reinterpret_cast<void *>(1);
+         })
+           ? 0
+           : 1;
+}
+
 } // extern "C"

@@ -14,6 +14,7 @@ from .amrx import (  # noqa: F401
     extract_isosurface, find_exact, index_from_keys, kernel_launches, library, snap,
     sort_part, try_build_duals, weld, IndexedMesh, validate_dataset, ValidationReport,
     release_cached_memory, read_amr, write_amr,
+    write_obj, write_ply, write_dual_mesh,
 )
 
 __all__ = [
@@ -23,5 +24,5 @@ __all__ = [
     "UnsupportedError", "CudaError", "adopt_index", "dual_bases", "library",
     "cell_bounds", "sort_part", "index_from_keys", "weld", "IndexedMesh",
     "validate_dataset", "ValidationReport", "release_cached_memory",
-    "read_amr", "write_amr",
+    "read_amr", "write_amr", "write_obj", "write_ply", "write_dual_mesh",
 ]

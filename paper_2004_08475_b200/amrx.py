@@ -40,6 +40,7 @@ AMRX_ERR_CUDA = 5
 AMRX_ERR_CAPACITY = 6
 AMRX_ERR_UNSUPPORTED = 7
 AMRX_ERR_NO_DEVICE = 8
+AMRX_ERR_IO = 9
 
 MAX_LEVEL = 30
 
@@ -116,6 +117,9 @@ def library():
     sig = {
         "amrx_index_create": [P, P, U64, U64, P, P],
         "amrx_read_amr": [C.c_char_p, P, P],
+        "amrx_write_obj": [C.c_char_p, P, U64, P, U64, I32],
+        "amrx_write_ply": [C.c_char_p, P, U64, P, U64, I32],
+        "amrx_write_dual_mesh": [C.c_char_p, P, U64, P, P, U64, I32],
         "amrx_index_destroy": [P],
         "amrx_index_get_info": [P, P],
         "amrx_index_download": [P, P, P],
@@ -163,6 +167,8 @@ def _check(status, count=None):
         raise CapacityError(msg, count)
     if status == AMRX_ERR_UNSUPPORTED:
         raise UnsupportedError(msg)
+    if status == AMRX_ERR_IO:
+        raise OSError(msg)
     raise CudaError(msg)
 
 
@@ -629,3 +635,48 @@ def dual_bases(index: CellIndex, tasks):
     w = np.left_shift(np.int64(1), c[:, 3])
     base = np.stack([c[:, a] - np.where((delta >> a) & 1, 0, w) for a in range(3)], axis=1)
     return base, c[:, 3].astype(np.int32)
+
+
+def _host(a, dtype, cols):
+    """host, contiguous, ``dtype`` (int32 CellIds/indices are viewed as u32)"""
+    if hasattr(a, "is_cuda"):
+        a = a.cpu().numpy()
+    a = np.asarray(a)
+    if a.dtype != dtype and a.dtype.kind in "iu" and a.dtype.itemsize == np.dtype(dtype).itemsize:
+        a = a.view(dtype)
+    return np.ascontiguousarray(a, dtype).reshape(-1, cols)
+
+
+def _mesh_arrays(mesh):
+    v = _host(mesh.vertices, np.float64, 3)
+    t = _host(mesh.triangles, np.uint32, 3)
+    return v, t
+
+
+def write_obj(path, mesh, threads=0):
+    """write_obj (io.cpp:219-239): Wavefront OBJ, shortest round-trip decimals,
+    byte-identical to the reference; formatted by host threads."""
+    v, t = _mesh_arrays(mesh)
+    _check(library().amrx_write_obj(os.fsencode(os.fspath(path)), _ptr(v), len(v), _ptr(t),
+                                    len(t), threads))
+
+
+def write_ply(path, mesh, threads=0):
+    """write_ply (io.cpp:241-272): binary little-endian PLY, float32 positions."""
+    v, t = _mesh_arrays(mesh)
+    _check(library().amrx_write_ply(os.fsencode(os.fspath(path)), _ptr(v), len(v), _ptr(t),
+                                    len(t), threads))
+
+
+def write_dual_mesh(path, duals, index, threads=0):
+    """write_dual_mesh (io.cpp:274-305): per dual, the 8 corner cell centres
+    then the 8 scalars.  ``duals`` is a DualMesh (or (n, 8) corner CellIds),
+    ``index`` the CellIndex they came from."""
+    corners = duals.corners if hasattr(duals, "corners") else duals
+    corners = _host(corners, np.uint32, 8)
+    cells = np.ascontiguousarray(index.cells)
+    scal = np.ascontiguousarray(index.scalars)
+    _check(library().amrx_write_dual_mesh(os.fsencode(os.fspath(path)), _ptr(corners),
+                                          len(corners), _ptr(cells), _ptr(scal), len(cells),
+                                          threads))
+

@@ -1721,3 +1721,14 @@ amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range,
 }
 
 }  // extern "C"
+
+namespace amrx {
+/// the writers (writers.cpp) report through the same thread-local message
+void set_last_error(const std::string &msg, bool clear)
+{
+  if (clear)
+    g_last_error.clear();
+  else
+    g_last_error = msg;
+}
+}  // namespace amrx

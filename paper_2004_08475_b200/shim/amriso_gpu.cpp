@@ -12,19 +12,21 @@
 //                                      proj/include/amriso/locator.hpp:80
 //   CellIndex read_amr(const std::filesystem::path&)
 //                                      proj/include/amriso/io.hpp:43
+//   write_obj / write_ply / write_dual_mesh  proj/include/amriso/io.hpp:51-64
 //
 // Compiled against the reference's own headers and linked in place of
 // proj/src/pipeline.cpp, proj/src/weld.cpp, of build_index and
-// validate_dataset in proj/src/locator.cpp and of read_amr in proj/src/io.cpp
-// (see INTEGRATION.md); everything else -- snap/find_exact, the dual rules
-// used by tests, contour_hex, the writers, generators, the CLI -- stays the
-// reference's.  All computation goes through the C ABI
+// validate_dataset in proj/src/locator.cpp and of read_amr and the three
+// file writers in proj/src/io.cpp; everything else --
+// snap/find_exact, the dual rules used by tests, contour_hex, the string
+// formatters, generators, the CLI -- stays the reference's.  All computation goes through the C ABI
 // (include/amrx.h) to libamrx.so on the GPU; there is no CPU fallback.
 //
 // Error mapping (amrx_status -> the reference's exception types):
 //   AMRX_ERR_LOAD -> LoadError, AMRX_ERR_INVALID_ARG -> invalid_argument,
 //   AMRX_ERR_LENGTH -> length_error, AMRX_ERR_INTERNAL -> logic_error,
-//   anything else (CUDA, no device) -> runtime_error.
+//   AMRX_ERR_IO -> runtime_error (the message as is), anything else (CUDA,
+//   no device) -> runtime_error.
 #include "amriso/io.hpp"
 #include "amriso/pipeline.hpp"
 #include "amriso/weld.hpp"
@@ -53,6 +55,7 @@ static_assert(sizeof(FatTriangle) == 72, "FatTriangle must be 9 x f64");
   case AMRX_ERR_INVALID_ARG: throw std::invalid_argument(msg);
   case AMRX_ERR_LENGTH: throw std::length_error(msg);
   case AMRX_ERR_INTERNAL: throw std::logic_error(msg);
+  case AMRX_ERR_IO: throw std::runtime_error(msg);  // write_file_atomic's wording
   default: throw std::runtime_error("amrx: " + msg);
   }
 }
@@ -123,6 +126,35 @@ CellIndex read_amr(const std::filesystem::path &path)
   IndexHandle h;
   check(amrx_read_amr(path.c_str(), nullptr, &h.p));
   return host_index(h);
+}
+
+static_assert(sizeof(vec3d) == 24, "vec3d must be 3 x f64");
+
+void write_obj(const IndexedMesh &mesh, const std::filesystem::path &path)
+{
+  check(amrx_write_obj(path.c_str(), mesh.vertices.empty() ? nullptr : &mesh.vertices[0].x,
+                       mesh.vertices.size(),
+                       mesh.triangles.empty() ? nullptr : mesh.triangles.data()->data(),
+                       mesh.triangles.size(), 0));
+}
+
+void write_ply(const IndexedMesh &mesh, const std::filesystem::path &path)
+{
+  check(amrx_write_ply(path.c_str(), mesh.vertices.empty() ? nullptr : &mesh.vertices[0].x,
+                       mesh.vertices.size(),
+                       mesh.triangles.empty() ? nullptr : mesh.triangles.data()->data(),
+                       mesh.triangles.size(), 0));
+}
+
+void write_dual_mesh(const std::vector<DualCell> &duals, const CellIndex &index,
+                     const std::filesystem::path &path)
+{
+  std::vector<uint32_t> corners(duals.size() * 8);
+  for (size_t d = 0; d < duals.size(); d++)
+    for (int k = 0; k < 8; k++) corners[8 * d + k] = duals[d].corners[k].index;
+  check(amrx_write_dual_mesh(path.c_str(), corners.data(), duals.size(),
+                             reinterpret_cast<const int32_t *>(index.data.cells.data()),
+                             index.data.scalars.data(), index.size(), 0));
 }
 
 std::vector<DualCell> extract_dual_mesh(const CellIndex &index, int)

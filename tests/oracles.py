@@ -213,6 +213,8 @@ class Reference(_Lib):
         self._fn("ref_weld", P, [P, U64])
         self._fn("ref_mesh_sizes", U64, [P, P])
         self._fn("ref_degenerate_hexes", None, [U32, C.c_int, P, P, P, P])
+        self._fn("ref_write_mesh", C.c_int, [C.c_char_p, C.c_int, P, U64, P, U64])
+        self._fn("ref_write_dual_mesh", C.c_int, [C.c_char_p, P, U64, P, P, U64])
         self._libc = C.CDLL(None)
         self._libc.free.argtypes = [P]
         del L
