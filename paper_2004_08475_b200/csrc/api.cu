@@ -337,6 +337,20 @@ WsLease::~WsLease()
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+void ensure_smem_attr(const void *kernel, size_t bytes)
+{
+  int dev = 0;
+  AMRX_CUDA(cudaGetDevice(&dev));
+  static std::mutex mu;
+  static std::vector<std::pair<const void *, int>> done;
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto &d : done)
+    if (d.first == kernel && d.second == dev) return;
+  AMRX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(bytes)));
+  done.emplace_back(kernel, dev);
+}
+
 int device_sm_count()
 {
   int dev = 0;

@@ -996,13 +996,7 @@ int grid_query(uint64_t n)
 template <bool D, bool T, bool F>
 void launch_extract(const KArgs &k, int grid, cudaStream_t st)
 {
-  static bool attr = false;
-  if (!attr) {
-    AMRX_CUDA(cudaFuncSetAttribute(extract_kernel<D, T, F>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(sizeof(Smem))));
-    attr = true;
-  }
+  ensure_smem_attr(reinterpret_cast<const void *>(extract_kernel<D, T, F>), sizeof(Smem));
   extract_kernel<D, T, F><<<grid, kThreads, sizeof(Smem), st>>>(k);
   AMRX_LAUNCH_CHECK();
 }
@@ -1010,17 +1004,17 @@ void launch_extract(const KArgs &k, int grid, cudaStream_t st)
 template <bool D, bool T, bool F>
 int occupancy_grid()
 {
-  static int grid = 0;
-  if (!grid) {
-    AMRX_CUDA(cudaFuncSetAttribute(extract_kernel<D, T, F>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(sizeof(Smem))));
-    int per_sm = 0;
+  static int per_sm[64] = {0};  // per device
+  int dev = 0;
+  AMRX_CUDA(cudaGetDevice(&dev));
+  int &ps = per_sm[dev & 63];
+  if (!ps) {
+    ensure_smem_attr(reinterpret_cast<const void *>(extract_kernel<D, T, F>), sizeof(Smem));
     AMRX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &per_sm, extract_kernel<D, T, F>, kThreads, sizeof(Smem)));
-    grid = std::max(1, per_sm) * device_sm_count();
+      &ps, extract_kernel<D, T, F>, kThreads, sizeof(Smem)));
+    ps = std::max(1, ps);
   }
-  return grid;
+  return ps * device_sm_count();
 }
 
 }  // namespace

@@ -27,6 +27,9 @@ struct Error {
 
 void note_launch();
 
+/// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
+void ensure_smem_attr(const void *kernel, size_t bytes);
+
 #define AMRX_LAUNCH_CHECK()                                              \
   do {                                                                   \
     ::amrx::note_launch();                                               \

@@ -339,21 +339,13 @@ bool sort_impl(uint64_t *keys, const V *vals_src, V *vals, uint64_t *keys_alt, V
                             cudaMemcpyDeviceToHost, st));
   AMRX_CUDA(cudaStreamSynchronize(st));
 
-  static bool attr_set = false;
   const size_t smem = sizeof(PassSmem<V>);
-  if (!attr_set) {
-    AMRX_CUDA(cudaFuncSetAttribute(onesweep_pass_kernel<kPassPlain, V>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(smem)));
-    if (sizeof(V) == 4) {
-      AMRX_CUDA(cudaFuncSetAttribute(onesweep_pass_kernel<kPassGather, uint32_t>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(sizeof(PassSmem<uint32_t>))));
-      AMRX_CUDA(cudaFuncSetAttribute(onesweep_pass_kernel<kPassInverse, uint32_t>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(sizeof(PassSmem<uint32_t>))));
-    }
-    attr_set = true;
+  ensure_smem_attr(reinterpret_cast<const void *>(onesweep_pass_kernel<kPassPlain, V>), smem);
+  if (sizeof(V) == 4) {
+    ensure_smem_attr(reinterpret_cast<const void *>(onesweep_pass_kernel<kPassGather, uint32_t>),
+                     sizeof(PassSmem<uint32_t>));
+    ensure_smem_attr(reinterpret_cast<const void *>(onesweep_pass_kernel<kPassInverse, uint32_t>),
+                     sizeof(PassSmem<uint32_t>));
   }
   int last = -1;
   bool trivial[kMaxPasses] = {};
