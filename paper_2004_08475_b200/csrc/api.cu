@@ -995,6 +995,10 @@ void read_amr_binary(const std::string &path, const amrx_index_opts *opts, amrx_
     fail(AMRX_ERR_LOAD, path + ": " + std::to_string(size - expected) +
                           " trailing bytes after the last record");
 
+  // build_index's 32-bit CellId limit before staging 24 B per record on the
+  // device (the reference would first scan the scalars of such a file)
+  if (n > uint64_t(std::numeric_limits<uint32_t>::max()))
+    fail(AMRX_ERR_LOAD, path + ": dataset too large for 32-bit cell ids");
   int dev = opts && opts->device >= 0 ? opts->device : -1;
   if (dev < 0) AMRX_CUDA(cudaGetDevice(&dev));
   DeviceGuard dg(dev);
