@@ -2,6 +2,7 @@
 chunks to the GPU.  The index read from a file must equal build_index over
 the same arrays; malformed files raise LoadError with the reference's
 messages (test_io.cpp:135-236 pins the same wording through the drop-in)."""
+import os
 import struct
 
 import numpy as np
@@ -115,3 +116,14 @@ def test_text_errors(P, tmp_path):
     ]:
         path.write_text(text)
         assert needle in load_error(P, path)
+
+
+def test_too_many_cells_refused_before_staging(P, tmp_path):
+    # a sparse file whose size matches a 2^32-record header: refused by the
+    # 32-bit CellId limit without reading or staging ~100 GB
+    n = 1 << 32
+    path = tmp_path / "huge.amr"
+    with open(path, "wb") as f:
+        f.write(b"AMRCELL1" + struct.pack("<IQI", 1, n, 1))
+    os.truncate(path, 24 + 24 * n)
+    assert "dataset too large for 32-bit cell ids" in load_error(P, path)
