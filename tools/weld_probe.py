@@ -39,7 +39,11 @@ def main():
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         assert st == 0, lib.amrx_last_error()
-        print(f"weld {n} triangles -> {nv.value} vertices: {1000 * dt:.1f} ms", flush=True)
+        v = verts[:nv.value].contiguous().view(torch.int64)
+        chk = (int(v.sum()), int((v * torch.arange(1, nv.value + 1, device="cuda")[:, None]).sum()),
+               int((tris.to(torch.int64) * torch.arange(1, n + 1, device="cuda")[:, None]).sum()))
+        print(f"weld {n} triangles -> {nv.value} vertices: {1000 * dt:.1f} ms  checksum {chk}",
+              flush=True)
 
 
 if __name__ == "__main__":
