@@ -141,32 +141,36 @@ slot_flags_kernel(const uint32_t *__restrict__ rep, uint64_t cap, uint32_t *__re
     flags[h] = __ldg(rep + h) != kEmpty;
 }
 
-/// occupied slot h -> its group number u: slot[h] = u, urep[u] = rep[h]
+/// occupied slot h -> its group number u: slot[h] = u, gpos[u] = the
+/// position (bits) of the group's lowest corner rep[h]
 __global__ void __launch_bounds__(kThreads)
-slot_compact_kernel(const uint32_t *__restrict__ rep, const uint32_t *__restrict__ excl,
-                    uint64_t cap, uint32_t *__restrict__ slot, uint32_t *__restrict__ urep)
+slot_compact_kernel(const double *__restrict__ xyz9, const uint32_t *__restrict__ rep,
+                    const uint32_t *__restrict__ excl, uint64_t cap, uint32_t *__restrict__ slot,
+                    double *__restrict__ gpos)
 {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   for (uint64_t h = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; h < cap; h += stride) {
     const uint32_t r = __ldg(rep + h);
     if (r != kEmpty) {
-      const uint32_t u = __ldg(excl + h);
-      slot[h] = u;
-      urep[u] = r;
+      const uint64_t u = __ldg(excl + h);
+      slot[h] = uint32_t(u);
+      gpos[3 * u] = __ldg(xyz9 + 3 * uint64_t(r));
+      gpos[3 * u + 1] = __ldg(xyz9 + 3 * uint64_t(r) + 1);
+      gpos[3 * u + 2] = __ldg(xyz9 + 3 * uint64_t(r) + 2);
     }
   }
 }
 
-/// keys[i] = image of coordinate `axis` of group perm[i]'s representative
+/// keys[i] = image of coordinate `axis` of group perm[i] (perm null: i)
 __global__ void __launch_bounds__(kThreads)
-group_keys_kernel(const double *__restrict__ xyz9, const uint32_t *__restrict__ urep, uint64_t n,
-                  int axis, const uint32_t *__restrict__ perm, uint64_t *__restrict__ keys,
+group_keys_kernel(const double *__restrict__ gpos, uint64_t n, int axis,
+                  const uint32_t *__restrict__ perm, uint64_t *__restrict__ keys,
                   uint32_t *__restrict__ vals)
 {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint32_t u = perm ? __ldg(perm + i) : uint32_t(i);
-    keys[i] = order_image(__ldg(xyz9 + 3 * uint64_t(__ldg(urep + u)) + axis));
+    const uint64_t u = perm ? __ldg(perm + i) : i;
+    keys[i] = order_image(__ldg(gpos + 3 * u + axis));
     if (!perm) vals[i] = uint32_t(i);
   }
 }
@@ -174,19 +178,17 @@ group_keys_kernel(const double *__restrict__ xyz9, const uint32_t *__restrict__ 
 /// vertex v = the v-th group in position order: its coordinates, and the
 /// group -> vertex map
 __global__ void __launch_bounds__(kThreads)
-group_emit_kernel(const double *__restrict__ xyz9, const uint32_t *__restrict__ urep,
-                  const uint32_t *__restrict__ perm, uint64_t nv, double *__restrict__ verts,
-                  uint64_t vcap, uint32_t *__restrict__ vid)
+group_emit_kernel(const double *__restrict__ gpos, const uint32_t *__restrict__ perm, uint64_t nv,
+                  double *__restrict__ verts, uint64_t vcap, uint32_t *__restrict__ vid)
 {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   for (uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < nv; v += stride) {
-    const uint32_t u = __ldg(perm + v);
+    const uint64_t u = __ldg(perm + v);
     vid[u] = uint32_t(v);
     if (verts && v < vcap) {
-      const uint64_t r = __ldg(urep + u);
-      verts[3 * v] = __ldg(xyz9 + 3 * r);
-      verts[3 * v + 1] = __ldg(xyz9 + 3 * r + 1);
-      verts[3 * v + 2] = __ldg(xyz9 + 3 * r + 2);
+      verts[3 * v] = __ldg(gpos + 3 * u);
+      verts[3 * v + 1] = __ldg(gpos + 3 * u + 1);
+      verts[3 * v + 2] = __ldg(gpos + 3 * u + 2);
     }
   }
 }
@@ -281,11 +283,11 @@ uint64_t run_weld_hash(const double *xyz9, uint64_t n_tris, double *verts, uint6
   AMRX_CUDA(cudaStreamSynchronize(st));
   const uint64_t nv = uint64_t(tail[0]) + tail[1];
   flags.release();
-  DevBuf urep;
-  urep.reserve(nv * 4, st);
-  slot_compact_kernel<<<grid_of(cap), kThreads, 0, st>>>(rep.as<uint32_t>(), excl.as<uint32_t>(),
-                                                         cap, slot.as<uint32_t>(),
-                                                         urep.as<uint32_t>());
+  DevBuf gpos;
+  gpos.reserve(nv * 24, st);
+  slot_compact_kernel<<<grid_of(cap), kThreads, 0, st>>>(xyz9, rep.as<uint32_t>(),
+                                                         excl.as<uint32_t>(), cap,
+                                                         slot.as<uint32_t>(), gpos.as<double>());
   AMRX_LAUNCH_CHECK();
   excl.release();
   rep.release();
@@ -299,7 +301,7 @@ uint64_t run_weld_hash(const double *xyz9, uint64_t n_tris, double *verts, uint6
   for (int pass = 0; pass < 3; pass++) {
     const int axis = 2 - pass;  // z, y, x: LSD over the fields
     group_keys_kernel<<<grid_of(nv), kThreads, 0, st>>>(
-      xyz9, urep.as<uint32_t>(), nv, axis, pass ? vb[cur].as<uint32_t>() : nullptr,
+      gpos.as<double>(), nv, axis, pass ? vb[cur].as<uint32_t>() : nullptr,
       kb[cur].as<uint64_t>(), vb[cur].as<uint32_t>());
     AMRX_LAUNCH_CHECK();
     int passes = 0;
@@ -310,9 +312,8 @@ uint64_t run_weld_hash(const double *xyz9, uint64_t n_tris, double *verts, uint6
   }
   DevBuf vid;
   vid.reserve(nv * 4, st);
-  group_emit_kernel<<<grid_of(nv), kThreads, 0, st>>>(xyz9, urep.as<uint32_t>(),
-                                                      vb[cur].as<uint32_t>(), nv, verts, vcap,
-                                                      vid.as<uint32_t>());
+  group_emit_kernel<<<grid_of(nv), kThreads, 0, st>>>(gpos.as<double>(), vb[cur].as<uint32_t>(),
+                                                      nv, verts, vcap, vid.as<uint32_t>());
   AMRX_LAUNCH_CHECK();
   if (tris) {
     corner_vid_kernel<<<grid_of(n), kThreads, 0, st>>>(cslot.as<uint32_t>(), slot.as<uint32_t>(),
