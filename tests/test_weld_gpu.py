@@ -87,3 +87,49 @@ def test_weld_signed_zero_is_one_vertex(P):
     m = P.weld(tri)
     v, t = oracles.restatement().weld(tri)
     assert same(m.vertices, v) and (m.triangles == t).all()
+
+
+def test_weld_signed_zero_lowest_tag_keeps_its_bits(P):
+    """the vertex carries the bits of the group's lowest-tag corner (-0.0 here)"""
+    tri = np.array([[-0.0, 1, 2, 3, 4, 5, 6, 7, 8], [0.0, 1, 2, 9, 9, 9, 6, 7, 8],
+                    [0.0, 1, -0.0, 3, 4, 5, 0, 0, 0]])
+    m = P.weld(tri)
+    v, t = oracles.restatement().weld(tri)
+    assert same(m.vertices, v) and (m.triangles == t).all()
+    assert np.signbit(m.vertices[m.triangles[0, 0], 0])  # (-0, 1, 2): tag 0 wins over tag 3
+
+
+def test_weld_heavy_sharing(P):
+    """200k triangles over 64 distinct positions (long groups, hash pressure),
+    with signed zeros mixed in"""
+    rng = np.random.default_rng(11)
+    pts = rng.integers(-2, 3, size=(64, 3)).astype(np.float64)
+    pick = rng.integers(0, 64, size=(200_000, 3))
+    tri = pts[pick].reshape(-1, 9).copy()
+    flip = (tri == 0) & (rng.random(tri.shape) < 0.5)
+    tri[flip] = -0.0
+    m = P.weld(tri)
+    v, t = oracles.restatement().weld(tri)
+    assert same(m.vertices, v) and (m.triangles == t).all()
+
+
+def test_weld_sort_path_matches(P, tmp_path):
+    """the sort-based GPU weld (AMRX_WELD=sort, read once per process) gives
+    the same mesh as the hash weld"""
+    import subprocess
+    import sys
+    from paper_2004_08475_b200 import synth
+    ds = synth.bricks([16, 12, 12], seed=7, shuffle=True)
+    idx = P.build_index(ds.cells, ds.scalars)
+    fat = P.extract_isosurface(idx, P.IsoParams(iso=synth.C4_ISO)).fat
+    idx.close()
+    np.save(tmp_path / "fat.npy", fat)
+    m = P.weld(fat)
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); import paper_2004_08475_b200 as P; "
+            "m = P.weld(np.load(%r)); np.save(%r, m.vertices); np.save(%r, m.triangles)"
+            % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+               str(tmp_path / "fat.npy"), str(tmp_path / "v.npy"), str(tmp_path / "t.npy")))
+    subprocess.run([sys.executable, "-c", code], check=True, timeout=600,
+                   env=dict(os.environ, AMRX_WELD="sort"))
+    assert same(m.vertices, np.load(tmp_path / "v.npy"))
+    assert (m.triangles == np.load(tmp_path / "t.npy")).all()
