@@ -395,7 +395,10 @@ def run_amrx(args):
                      "kernel": ("dual mesh: extract_kernel<dual>" if dual_only else
                                 "iso extraction: extract_kernel<iso, f64> + mc_jobs_kernel<f64> "
                                 "(CUDA events around both launches)"), "peak_kind": kind,
-                     "alg_bytes_per_launch": alg_bytes},
+                     "alg_bytes_per_launch": alg_bytes,
+                     "note": ("not bandwidth bound: extract_kernel issues instructions on "
+                              "76% of cycles (ALU pipe 70%) at 2.7% of DRAM peak "
+                              "(profiles/r01_extract_c4_ncu.txt)")},
         "weld": weld_info if weld_ms is not None else None,
         "cpu_baseline": cpu,
         "e2e": e2e,
