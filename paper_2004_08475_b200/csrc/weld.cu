@@ -141,11 +141,11 @@ slot_flags_kernel(const uint32_t *__restrict__ rep, uint64_t cap, uint32_t *__re
     flags[h] = __ldg(rep + h) != kEmpty;
 }
 
-/// occupied slot h -> its group number u: slot[h] = u, gpos[u] = the
+/// occupied slot h -> its group number u: gslot[u] = h, gpos[u] = the
 /// position (bits) of the group's lowest corner rep[h]
 __global__ void __launch_bounds__(kThreads)
 slot_compact_kernel(const double *__restrict__ xyz9, const uint32_t *__restrict__ rep,
-                    const uint32_t *__restrict__ excl, uint64_t cap, uint32_t *__restrict__ slot,
+                    const uint32_t *__restrict__ excl, uint64_t cap, uint32_t *__restrict__ gslot,
                     double *__restrict__ gpos)
 {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
@@ -153,7 +153,7 @@ slot_compact_kernel(const double *__restrict__ xyz9, const uint32_t *__restrict_
     const uint32_t r = __ldg(rep + h);
     if (r != kEmpty) {
       const uint64_t u = __ldg(excl + h);
-      slot[h] = uint32_t(u);
+      gslot[u] = uint32_t(h);
       gpos[3 * u] = __ldg(xyz9 + 3 * uint64_t(r));
       gpos[3 * u + 1] = __ldg(xyz9 + 3 * uint64_t(r) + 1);
       gpos[3 * u + 2] = __ldg(xyz9 + 3 * uint64_t(r) + 2);
@@ -176,15 +176,16 @@ group_keys_kernel(const double *__restrict__ gpos, uint64_t n, int axis,
 }
 
 /// vertex v = the v-th group in position order: its coordinates, and the
-/// group -> vertex map
+/// vertex id written into the group's table slot (slot[gslot[u]] = v)
 __global__ void __launch_bounds__(kThreads)
 group_emit_kernel(const double *__restrict__ gpos, const uint32_t *__restrict__ perm, uint64_t nv,
-                  double *__restrict__ verts, uint64_t vcap, uint32_t *__restrict__ vid)
+                  double *__restrict__ verts, uint64_t vcap, const uint32_t *__restrict__ gslot,
+                  uint32_t *__restrict__ slot)
 {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   for (uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < nv; v += stride) {
     const uint64_t u = __ldg(perm + v);
-    vid[u] = uint32_t(v);
+    slot[__ldg(gslot + u)] = uint32_t(v);
     if (verts && v < vcap) {
       verts[3 * v] = __ldg(gpos + 3 * u);
       verts[3 * v + 1] = __ldg(gpos + 3 * u + 1);
@@ -195,11 +196,11 @@ group_emit_kernel(const double *__restrict__ gpos, const uint32_t *__restrict__ 
 
 __global__ void __launch_bounds__(kThreads)
 corner_vid_kernel(const uint32_t *__restrict__ corner_slot, const uint32_t *__restrict__ slot,
-                  const uint32_t *__restrict__ vid, uint64_t n, uint32_t *__restrict__ tris)
+                  uint64_t n, uint32_t *__restrict__ tris)
 {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   for (uint64_t c = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < n; c += stride)
-    tris[c] = __ldg(vid + __ldg(slot + __ldg(corner_slot + c)));
+    tris[c] = __ldg(slot + __ldg(corner_slot + c));
 }
 
 int grid_of(uint64_t n)
@@ -260,7 +261,9 @@ uint64_t run_weld_hash(const double *xyz9, uint64_t n_tris, double *verts, uint6
 {
   const uint64_t n = 3 * n_tris;
   if (n == 0) return 0;
-  const uint64_t cap = n + n / 2 + 1;  // load factor <= 2/3 even if no corner is shared
+  // load factor <= 2/3 even if no corner is shared; slots are u32 (n < 2^32,
+  // so a clamped table still has room for every corner)
+  const uint64_t cap = std::min<uint64_t>(n + n / 2 + 1, 0xFFFFFFFFull);
   DevBuf slot, rep, cslot, flags, excl, scan_scratch;
   slot.reserve(cap * 4, st);
   rep.reserve(cap * 4, st);
@@ -283,11 +286,12 @@ uint64_t run_weld_hash(const double *xyz9, uint64_t n_tris, double *verts, uint6
   AMRX_CUDA(cudaStreamSynchronize(st));
   const uint64_t nv = uint64_t(tail[0]) + tail[1];
   flags.release();
-  DevBuf gpos;
+  DevBuf gpos, gslot;
   gpos.reserve(nv * 24, st);
+  gslot.reserve(nv * 4, st);
   slot_compact_kernel<<<grid_of(cap), kThreads, 0, st>>>(xyz9, rep.as<uint32_t>(),
                                                          excl.as<uint32_t>(), cap,
-                                                         slot.as<uint32_t>(), gpos.as<double>());
+                                                         gslot.as<uint32_t>(), gpos.as<double>());
   AMRX_LAUNCH_CHECK();
   excl.release();
   rep.release();
@@ -310,14 +314,13 @@ uint64_t run_weld_hash(const double *xyz9, uint64_t n_tris, double *verts, uint6
                          sort_scratch.ptr, st, &passes))
       cur ^= 1;
   }
-  DevBuf vid;
-  vid.reserve(nv * 4, st);
   group_emit_kernel<<<grid_of(nv), kThreads, 0, st>>>(gpos.as<double>(), vb[cur].as<uint32_t>(),
-                                                      nv, verts, vcap, vid.as<uint32_t>());
+                                                      nv, verts, vcap, gslot.as<uint32_t>(),
+                                                      slot.as<uint32_t>());
   AMRX_LAUNCH_CHECK();
   if (tris) {
     corner_vid_kernel<<<grid_of(n), kThreads, 0, st>>>(cslot.as<uint32_t>(), slot.as<uint32_t>(),
-                                                       vid.as<uint32_t>(), n, tris);
+                                                       n, tris);
     AMRX_LAUNCH_CHECK();
   }
   AMRX_CUDA(cudaStreamSynchronize(st));
