@@ -78,3 +78,31 @@ def test_empty_range_and_no_crossing(P):
     assert len(r.fat) == 0 and r.stats.duals_accepted == 27
     d = P.extract_dual_mesh(idx, cell_range=(10, 10))
     assert len(d.corners) == 0
+
+
+def test_level30_cells_span_the_int32_range(P):
+    """Coarsest legal level (locator.cpp:38-41: level <= 30): a 4x4x4 block of
+    level-30 cells whose anchors cover [-2^31, 2^31), one of them refined into
+    eight level-29 cells.  Stencil points and dual bases leave the int32 range
+    here, which snap rejects by its range guard (locator.cpp:107-115)."""
+    W = 1 << 30
+    c = [[i * W, j * W, k * W, 30] for k in range(-2, 2) for j in range(-2, 2)
+         for i in range(-2, 2) if (i, j, k) != (0, 0, 0)]
+    H = 1 << 29
+    c += [[i * H, j * H, k * H, 29] for k in range(2) for j in range(2) for i in range(2)]
+    c = np.array(c, np.int64)
+    rng = np.random.default_rng(30)
+    scal = rng.normal(size=len(c))
+    idx, r = same(P, c[rng.permutation(len(c))], scal, 0.0)
+    assert r.stats.duals_accepted > 0
+
+
+def test_key_wider_than_64_bits_is_refused(P):
+    """Fine cells spread across the whole int32 range need more than the
+    64-bit packed key holds: the build refuses with AMRX_ERR_UNSUPPORTED and
+    a message instead of producing a wrong index."""
+    lim = (1 << 31) - 2
+    c = np.array([[-lim - 1, -lim - 1, -lim - 1, 0], [lim, lim, lim, 0], [0, 0, 0, 5]],
+                 np.int32)
+    with pytest.raises(P.UnsupportedError):
+        P.build_index(c, np.zeros(len(c)))
