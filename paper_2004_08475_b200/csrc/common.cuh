@@ -172,12 +172,12 @@ __host__ __device__ inline Stencil make_stencil(const KeyGeom &g, uint64_t key, 
 /// key of stencil point p (meaningful when bit p of inrange is set)
 __host__ __device__ inline uint64_t stencil_key(const Stencil &s, int p)
 {
-  const int ox = p % 3 - 1, oy = (p / 3) % 3 - 1, oz = p / 9 - 1;
-  uint64_t k = s.k0;
-  k += ox > 0 ? s.sx : (ox < 0 ? uint64_t(0) - s.sx : 0);
-  k += oy > 0 ? s.sy : (oy < 0 ? uint64_t(0) - s.sy : 0);
-  k += oz > 0 ? s.sz : (oz < 0 ? uint64_t(0) - s.sz : 0);
-  return k;
+  // p < 27: p / 3 == (p * 11) >> 5 (exact for p < 32), then signed offsets
+  // times the packed steps (mod 2^64: the point's key when it is in range)
+  const uint32_t up = uint32_t(p), q1 = (up * 11u) >> 5, q2 = (q1 * 11u) >> 5;
+  return s.k0 + uint64_t(int64_t(int32_t(up - 3u * q1) - 1)) * s.sx +
+         uint64_t(int64_t(int32_t(q1 - 3u * q2) - 1)) * s.sy +
+         uint64_t(int64_t(int32_t(q2) - 1)) * s.sz;
 }
 
 // ------------------------------------------------------------------------
