@@ -170,11 +170,15 @@ __host__ __device__ inline Stencil make_stencil(const KeyGeom &g, uint64_t key, 
 }
 
 /// key of stencil point p (meaningful when bit p of inrange is set)
+template <bool DIGITS = false>
 __host__ __device__ inline uint64_t stencil_key(const Stencil &s, int p)
 {
   // p < 27: p / 3 == (p * 11) >> 5 (exact for p < 32), then signed offsets
   // times the packed steps (mod 2^64: the point's key when it is in range)
   const uint32_t up = uint32_t(p), q1 = (up * 11u) >> 5, q2 = (q1 * 11u) >> 5;
+  if (DIGITS)  // unsigned digits 0..2: per axis one 32x64 wide multiply-add
+    return (s.k0 - s.sx - s.sy - s.sz) + uint64_t(up - 3u * q1) * s.sx +
+           uint64_t(q1 - 3u * q2) * s.sy + uint64_t(q2) * s.sz;
   return s.k0 + uint64_t(int64_t(int32_t(up - 3u * q1) - 1)) * s.sx +
          uint64_t(int64_t(int32_t(q1 - 3u * q2) - 1)) * s.sy +
          uint64_t(int64_t(int32_t(q2) - 1)) * s.sz;

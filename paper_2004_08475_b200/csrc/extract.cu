@@ -569,6 +569,7 @@ __device__ __forceinline__ void fast_batch(const KArgs &a, Smem &sm, int warp, i
     coarser candidate levels (probe_coarser).  A loop over runtime point
     indices: unrolling it per point was measured slower for the iso kernel
     (the hot code outgrows the instruction cache next to marching cubes). */
+template <bool DIGITS>
 __device__ __forceinline__ void resolve_marks(const KArgs &a, Smem &sm, int warp, int lane,
                                               const Cell &c, const Stencil &st,
                                               uint32_t self, uint32_t todo, Marks &m)
@@ -598,7 +599,7 @@ __device__ __forceinline__ void resolve_marks(const KArgs &a, Smem &sm, int warp
         // at the hint level the point is its own anchor: key = cell key +
         // packed steps, valid iff inside the stored range
         v[k] = (st.inrange >> p) & 1u;
-        q[k] = stencil_key(st, p);
+        q[k] = stencil_key<DIGITS>(st, p);
       }
     }
     batch_find<K, true>(a.s, q, v, out, lvl);
@@ -703,7 +704,7 @@ extract_kernel(const __grid_constant__ KArgs a)
           }
           need |= pend;
         }
-        resolve_marks(a, sm, warp, lane, c, st, self, need, m);
+        resolve_marks<EMIT_TRI>(a, sm, warp, lane, c, st, self, need, m);
       }
       // corners in order d = 0..7 are ascending stencil points, so the
       // first failing corner is the lowest failing bit
