@@ -397,7 +397,7 @@ def run_amrx(args):
                                 "(CUDA events around both launches)"), "peak_kind": kind,
                      "alg_bytes_per_launch": alg_bytes,
                      "note": ("not bandwidth bound: extract_kernel issues instructions on "
-                              "78% of cycles (ALU pipe 66%) at 2.9% of DRAM peak "
+                              "78% of cycles (ALU pipe 67%) at 3.0% of DRAM peak "
                               "(profiles/r01_extract_c4_ncu.txt)")},
         "weld": weld_info if weld_ms is not None else None,
         "cpu_baseline": cpu,
