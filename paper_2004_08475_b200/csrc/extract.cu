@@ -416,10 +416,13 @@ struct Hit {
     (the reference's finest-first order restricted to them).  Per lane, no
     warp collectives; rare, so out of line -- and scalar, so the caller's
     batch arrays stay in registers. */
-__device__ __noinline__ Hit probe_coarser(const KArgs &a, const Cell &c, const Stencil &st,
+__device__ __noinline__ Hit probe_coarser(const KArgs &a, int level, const Stencil &st,
                                           int p, uint32_t cand)
 {
   const KeyGeom &g = a.g;
+  struct {
+    int level;
+  } c{level};
   if (g.aligned && !g.map_on && ((st.inrange >> p) & 1u)) {
     // in-range point, aligned origin: coarsen in packed key space
     const uint64_t q0 = stencil_key(st, p);
@@ -435,9 +438,12 @@ __device__ __noinline__ Hit probe_coarser(const KArgs &a, const Cell &c, const S
     }
     return Hit{-1, c.level};
   }
+  // the cell's coordinates only on this (unaligned / level-map) path:
+  // decoded from its key here, so the hot loop carries just the level
+  const Cell cc = unpack(g, st.k0);
   const int64_t w = int64_t(1) << c.level;
-  const int64_t px = c.i + (p % 3 - 1) * w, py = c.j + ((p / 3) % 3 - 1) * w,
-                pz = c.k + (p / 9 - 1) * w;
+  const int64_t px = cc.i + (p % 3 - 1) * w, py = cc.j + ((p / 3) % 3 - 1) * w,
+                pz = cc.k + (p / 9 - 1) * w;
   if (g.map_on) {
     // only levels present in the point's coarsest-aligned block can hold
     // it (exact); a point in a hole or outside the domain costs no lookup
@@ -607,7 +613,7 @@ __device__ __forceinline__ void resolve_marks(const KArgs &a, Smem &sm, int warp
     for (int k = 0; k < K; k++)
       if (pk[k] >= 0) {
         if (out[k] < 0 && coarser) {
-          const Hit h = probe_coarser(a, c, st, pk[k], coarser);
+          const Hit h = probe_coarser(a, c.level, st, pk[k], coarser);
           out[k] = h.id;
           lvl[k] = h.level;
         }
