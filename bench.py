@@ -114,6 +114,7 @@ DATA_DESC = {
     "c3": "synthetic (GPU generator: 6-level octree toward a turbulent-noise zero set, soup order)",
     "c4": "synthetic (GPU generator: vortex-tube brick AMR, bijective-hash soup order)",
     "c5": "synthetic (GPU generator: brick AMR, generator order)",
+    "deep": "synthetic (GPU generator: 13-level octree toward a landing-gear surface, soup order)",
 }
 
 
@@ -128,7 +129,7 @@ def make_workload(cfg_name, device):
         return ds.cells, ds.scalars, dict(bricks=list(b3), level_cells=ds.level_cells)
     import torch
     gen = getattr(synth, cfg["kind"])
-    if cfg["kind"] == "octree_noise":  # GPU generator: device tensors already
+    if cfg["kind"] in ("octree_noise", "octree_sdf"):  # GPU generators: device tensors
         cells, scal = gen(*cfg["args"], device=device)
         return cells, scal, dict(level_cells=torch.bincount(cells[:, 3].long()).tolist())
     cells, scal = gen(*cfg["args"])

@@ -76,6 +76,25 @@ typedef struct amrx_index_opts {
  * skips the radix sort */
 #define AMRX_FLAG_PRESORTED 0x1u
 
+/* lookup structure of the index (default: chosen from the key space).  The
+ * reference's find_exact/snap are a binary search over the sorted cells
+ * (locator.cpp:94-134); the device index answers the same queries through
+ *   RECORDS    a 32-value occupancy record per bucket of the key space:
+ *              one 8-byte load + popcount per lookup (dense key spaces)
+ *   HASH       records of the occupied buckets only, open-addressed
+ *              (sparse or deep key spaces, any key width)
+ *   DIRECTORY  a bucket directory + binary search of the bucket
+ * An index with duplicate cells always uses the directory (a record's
+ * popcount cannot count equal keys).  The results are identical. */
+#define AMRX_FLAG_LOOKUP_RECORDS 0x2u
+#define AMRX_FLAG_LOOKUP_HASH 0x4u
+#define AMRX_FLAG_LOOKUP_DIRECTORY 0x8u
+
+/* amrx_index_info.lookup */
+#define AMRX_LOOKUP_DIRECTORY 0
+#define AMRX_LOOKUP_RECORDS 1
+#define AMRX_LOOKUP_HASH 2
+
 typedef struct amrx_index_info {
   uint64_t cell_count;
   int32_t max_level;
@@ -83,11 +102,14 @@ typedef struct amrx_index_info {
   int32_t levels[31];       /* distinct levels present, finest first */
   int64_t bounds_lo[3];     /* hull of all cell boxes (locator.cpp:70-83) */
   int64_t bounds_hi[3];
-  int32_t key_bits;         /* bits of the packed 64-bit sort key in use */
-  int32_t directory_bits;   /* log2 of the search directory size */
+  int32_t key_bits;         /* bits of the packed sort key in use */
+  int32_t directory_bits;   /* log2 of the lookup structure's entry count */
   uint64_t duplicate_keys;  /* adjacent equal keys after the sort */
   uint64_t device_bytes;    /* HBM held by the index */
   double seconds_ingest;    /* device time of pack + sort + gather + directory */
+  int32_t lookup;           /* AMRX_LOOKUP_* in use */
+  uint32_t max_probe;       /* HASH: longest displacement from a home slot */
+  uint64_t lookup_entries;  /* records / hash slots / directory entries */
 } amrx_index_info;
 
 typedef struct amrx_stats {
@@ -261,6 +283,11 @@ AMRX_API amrx_status amrx_write_dual_mesh(const char *path, const uint32_t *corn
                                           uint64_t n_duals, const int32_t *cells4,
                                           const double *scalars, uint64_t n_cells,
                                           int threads);
+
+/* testing hook: cap every extraction round's staging at `items` outputs
+ * (0 = the default), so small inputs exercise the multi-round path; the
+ * results are identical for every value */
+AMRX_API void amrx_debug_round_limit(uint64_t items);
 
 /* kernels this process has launched through the library so far */
 AMRX_API uint64_t amrx_kernel_launches(void);

@@ -76,7 +76,19 @@ class _IndexInfo(C.Structure):
                 ("bounds_lo", C.c_int64 * 3), ("bounds_hi", C.c_int64 * 3),
                 ("key_bits", C.c_int32), ("directory_bits", C.c_int32),
                 ("duplicate_keys", C.c_uint64), ("device_bytes", C.c_uint64),
-                ("seconds_ingest", C.c_double)]
+                ("seconds_ingest", C.c_double), ("lookup", C.c_int32),
+                ("max_probe", C.c_uint32), ("lookup_entries", C.c_uint64)]
+
+
+# index lookup structures (amrx.h AMRX_FLAG_LOOKUP_* / AMRX_LOOKUP_*)
+_LOOKUP_FLAGS = {None: 0, "auto": 0, "records": 0x2, "hash": 0x4, "directory": 0x8}
+_LOOKUP_NAMES = {0: "directory", 1: "records", 2: "hash"}
+
+
+def _flags(presorted=False, lookup=None):
+    if lookup not in _LOOKUP_FLAGS:
+        raise ValueError(f"lookup must be one of {sorted(k for k in _LOOKUP_FLAGS if k)}")
+    return (1 if presorted else 0) | _LOOKUP_FLAGS[lookup]
 
 
 class _Opts(C.Structure):
@@ -145,6 +157,8 @@ def library():
     lib.amrx_last_error.restype = C.c_char_p
     lib.amrx_last_error.argtypes = []
     lib.amrx_version.restype = C.c_char_p
+    lib.amrx_debug_round_limit.restype = None
+    lib.amrx_debug_round_limit.argtypes = [C.c_uint64]
     lib.amrx_kernel_launches.restype = C.c_uint64
     lib.amrx_kernel_launches.argtypes = []
     _lib = lib
@@ -193,6 +207,9 @@ class IndexInfo:
     duplicate_keys: int
     device_bytes: int
     seconds_ingest: float
+    lookup: str = "records"
+    max_probe: int = 0
+    lookup_entries: int = 0
 
 
 class CellIndex:
@@ -212,7 +229,8 @@ class CellIndex:
             info.cell_count, info.max_level, list(info.levels[: info.level_count]),
             tuple(info.bounds_lo), tuple(info.bounds_hi), info.key_bits,
             info.directory_bits, info.duplicate_keys, info.device_bytes,
-            info.seconds_ingest)
+            info.seconds_ingest, _LOOKUP_NAMES.get(info.lookup, str(info.lookup)),
+            info.max_probe, info.lookup_entries)
 
     # -- CellIndex surface
     def size(self):
@@ -285,15 +303,23 @@ def release_cached_memory(device=-1):
     _check(library().amrx_release_cached_memory(device))
 
 
+def debug_round_limit(items=0):
+    """testing hook: cap every extraction round's staging at ``items``
+    outputs (0 = default) -- results are identical for every value"""
+    library().amrx_debug_round_limit(int(items))
+
+
 def kernel_launches():
     """kernels launched through libamrx.so by this process so far"""
     return int(library().amrx_kernel_launches())
 
 
-def build_index(cells, scalars, device=-1, presorted=False, stream=None):
+def build_index(cells, scalars, device=-1, presorted=False, stream=None, lookup=None):
     """Sort cells (with their scalars) into a device CellIndex
     (build_index, locator.cpp:26-92).  ``cells`` is (n,4) int32 (i,j,k,level),
-    numpy or torch (host or CUDA)."""
+    numpy or torch (host or CUDA).  ``lookup`` forces the index's lookup
+    structure ("records", "hash" or "directory"; default: chosen from the
+    key space) -- every choice gives identical results."""
     lib = library()
     if isinstance(cells, np.ndarray) or not hasattr(cells, "data_ptr"):
         cells = np.ascontiguousarray(np.asarray(cells, dtype=np.int32).reshape(-1, 4))
@@ -305,7 +331,7 @@ def build_index(cells, scalars, device=-1, presorted=False, stream=None):
         n_s = len(scalars)
     else:
         n_s = scalars.numel()
-    opts = _Opts(device, C.c_void_p(stream) if stream else None, 1 if presorted else 0)
+    opts = _Opts(device, C.c_void_p(stream) if stream else None, _flags(presorted, lookup))
     h = C.c_void_p()
     _check(lib.amrx_index_create(_ptr(cells) if n_cells else C.c_void_p(1),
                                  _ptr(scalars) if n_s else C.c_void_p(1),
@@ -313,13 +339,13 @@ def build_index(cells, scalars, device=-1, presorted=False, stream=None):
     return CellIndex(h.value, lib)
 
 
-def read_amr(path, device=-1, stream=None):
+def read_amr(path, device=-1, stream=None, lookup=None):
     """Read an AMRCELL1 cell file (binary, or text for a ``.txt`` path) into
     a device CellIndex (read_amr, io.cpp:76-181).  Binary records stream
     through pinned chunks straight to the GPU; errors raise LoadError with
     the reference's messages, prefixed with the path."""
     lib = library()
-    opts = _Opts(device, C.c_void_p(stream) if stream else None, 0)
+    opts = _Opts(device, C.c_void_p(stream) if stream else None, _flags(False, lookup))
     h = C.c_void_p()
     _check(lib.amrx_read_amr(os.fsencode(os.fspath(path)), C.byref(opts), C.byref(h)))
     return CellIndex(h.value, lib)
@@ -341,12 +367,13 @@ def write_amr(path, cells, scalars):
         f.write(rec.tobytes())
 
 
-def adopt_index(keys_dev_ptr, scalars_dev_ptr, n_cells, geometry, device=-1, stream=None):
+def adopt_index(keys_dev_ptr, scalars_dev_ptr, n_cells, geometry, device=-1, stream=None,
+                lookup=None):
     """Index over already-sorted packed keys + scalars on this device (the
     multi-GPU replica path: no sort, directory only)."""
     lib = library()
     g = np.ascontiguousarray(geometry, np.int64)
-    opts = _Opts(device, C.c_void_p(stream) if stream else None, 0)
+    opts = _Opts(device, C.c_void_p(stream) if stream else None, _flags(False, lookup))
     h = C.c_void_p()
     _check(lib.amrx_index_adopt(C.c_void_p(keys_dev_ptr), C.c_void_p(scalars_dev_ptr),
                                 n_cells, _ptr(g), C.byref(opts), C.byref(h)))
@@ -387,14 +414,15 @@ def sort_part(cells, scalars, geometry, device=-1, stream=None):
     return CellIndex(h.value, lib)
 
 
-def index_from_keys(keys_dev_ptr, scalars_dev_ptr, n_cells, geometry, device=-1, stream=None):
+def index_from_keys(keys_dev_ptr, scalars_dev_ptr, n_cells, geometry, device=-1, stream=None,
+                    lookup=None):
     """index of one partition of a distributed index: packed keys (any
     order) + scalars on this device inside the key range geometry[13:15];
     geometry[12] = global CellId of its first key; every id it reports is
     global"""
     lib = library()
     g = np.ascontiguousarray(geometry, np.int64)
-    opts = _Opts(device, C.c_void_p(stream) if stream else None, 0)
+    opts = _Opts(device, C.c_void_p(stream) if stream else None, _flags(False, lookup))
     h = C.c_void_p()
     _check(lib.amrx_index_from_keys(C.c_void_p(keys_dev_ptr), C.c_void_p(scalars_dev_ptr),
                                     n_cells, _ptr(g), C.byref(opts), C.byref(h)))

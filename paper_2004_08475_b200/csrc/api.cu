@@ -374,12 +374,17 @@ struct amrx_index {
   uint64_t n = 0;
   KeyGeom g{};
   int64_t bounds_hi[3] = {0, 0, 0};
-  DevBuf keys, scal, dir, rec, lmap, order, scratch;
+  DevBuf keys, scal, dir, rec, order, scratch;
   // partitions of a distributed index (amrx_index_from_keys): records of
   // buckets [rec_lo, rec_lo + rec_n) only, global id of local position 0
   uint64_t rec_lo = 0, rec_n = 0;
   int64_t id_base = 0;
   uint64_t key_lo = 0, key_hi = 0;
+  bool partition = false;  // amrx_index_from_keys: a key range of a distributed index
+  // a partition's interior: the local positions whose every lookup stays in
+  // [key_lo, key_hi) (extraction ranges must lie inside it)
+  uint64_t safe_lo = 0, safe_hi = ~0ull;
+  uint64_t hmask = 0;      // hashed records: slots - 1
   bool searchable = true;  // false: sorted arrays only (amrx_index_sort_part)
   uint32_t jobs_per_kcell = 0;  // marching-cubes jobs per 1024 cells, last extraction
   amrx_index_info info{};
@@ -400,11 +405,13 @@ struct amrx_index {
   {
     SearchCtx s;
     s.keys = keys.as<uint64_t>();
-    // occupancy records when the keys are unique (positions = popcounts),
-    // else the plain directory (built on demand, ensure_search_dir)
-    const bool use_rec = g.occ && info.duplicate_keys == 0;
-    s.dir = use_rec ? nullptr : dir.as<uint32_t>();
-    s.rec = use_rec ? rec.as<uint2>() - rec_lo : nullptr;
+    // dense or hashed occupancy records (unique keys: positions are
+    // popcounts), else the bucket directory (ensure_search_dir switches an
+    // index with duplicate keys to it)
+    s.rec = g.occ == kOccDense ? rec.as<uint2>() - rec_lo : nullptr;
+    s.htab = g.occ == kOccHash ? rec.as<uint4>() : nullptr;
+    s.hmask = hmask;
+    s.dir = g.occ == kOccNone ? dir.as<uint32_t>() : nullptr;
     s.id_base = id_base;
     s.n = n;
     s.dir_shift = g.dir_shift;
@@ -430,8 +437,18 @@ struct DeviceGuard {
   }
 };
 
+/// directory size for the binary-search lookup: about two buckets per cell
+int directory_bits(const KeyGeom &g, uint64_t n)
+{
+  return std::min(g.total, std::min(30, std::max(10, bit_width(n) + 1)));
+}
+
+/*! the key geometry of a dataset (field widths from its extent) and its
+    lookup structure: AMRX_FLAG_LOOKUP_* in `flags` forces one; by default
+    dense occupancy records while they cost at most ~192 B per cell (or
+    1 GB), else hashed records */
 KeyGeom make_geometry(const int64_t mn[3], const int64_t mx[3],
-                      uint32_t level_mask, uint64_t n)
+                      uint32_t level_mask, uint64_t n, uint32_t flags)
 {
   KeyGeom g{};
   int lo_level = 0, hi_level = 0;
@@ -464,36 +481,27 @@ KeyGeom make_geometry(const int64_t mn[3], const int64_t mx[3],
   g.nlevels = 0;
   for (int l = 0; l <= kMaxLevel; l++)
     if ((level_mask >> l) & 1u) g.levels[g.nlevels++] = int8_t(l);
-  // directory: about two buckets per cell, 2^10 .. 2^30 entries
-  // (AMRX_DIR_BITS overrides the size, for experiments)
-  static const char *dir_env = std::getenv("AMRX_DIR_BITS");
-  const int want = dir_env ? std::max(1, std::min(33, std::atoi(dir_env)))
-                           : std::min(30, std::max(10, bit_width(n) + 1));
-  g.dir_bits = std::min(g.total, want);
-  // occupancy records (AMRX_OCC=0 disables): 32 key values per bucket,
-  // 8 B each, when they cost at most ~192 B per cell (or 1 GB): a sparse
-  // key space (C3: 105M cells, 36-bit keys -> 17 GB) still pays -- the
-  // bucket search is ~4x slower per lookup
-  static const char *occ_env = std::getenv("AMRX_OCC");
+  const uint32_t force = flags & (AMRX_FLAG_LOOKUP_RECORDS | AMRX_FLAG_LOOKUP_HASH |
+                                  AMRX_FLAG_LOOKUP_DIRECTORY);
+  if (force & (force - 1))
+    fail(AMRX_ERR_INVALID_ARG, "more than one AMRX_FLAG_LOOKUP_* flag");
   const int occ_bits = std::max(0, g.total - kOccShift);
-  g.occ = !(occ_env && occ_env[0] == '0') && !dir_env && occ_bits <= 32 &&
-          (uint64_t(8) << occ_bits) <= std::max<uint64_t>(192 * n, uint64_t(1) << 30);
-  if (g.occ) g.dir_bits = occ_bits;
-  g.dir_shift = g.total - g.dir_bits;
-  // block level map at the coarsest level's granularity, if it is small
-  g.map_shift = hi_level;
-  double blocks = 1;
-  for (int a = 0; a < 3; a++) {
-    g.map_base[a] = mn[a] >> hi_level;  // arithmetic shift: floor
-    g.map_dim[a] = (mx[a] >> hi_level) - g.map_base[a] + 1;
-    blocks *= double(g.map_dim[a]);
+  const uint64_t dense_bytes = occ_bits <= 32 ? uint64_t(8) << occ_bits : ~0ull;
+  if (force == AMRX_FLAG_LOOKUP_DIRECTORY) {
+    g.occ = kOccNone;
+  } else if (force == AMRX_FLAG_LOOKUP_HASH) {
+    g.occ = kOccHash;
+  } else if (force == AMRX_FLAG_LOOKUP_RECORDS) {
+    if (dense_bytes > (uint64_t(64) << 30))
+      fail(AMRX_ERR_UNSUPPORTED, "dense occupancy records for a " + std::to_string(g.total) +
+                                   "-bit key space would exceed 64 GB (use the hash lookup)");
+    g.occ = kOccDense;
+  } else {
+    g.occ = dense_bytes <= std::max<uint64_t>(192 * n, uint64_t(1) << 30) ? kOccDense
+                                                                          : kOccHash;
   }
-  const double budget = std::max(double(1 << 26), 4.0 * double(n));
-  // consulted on the coarser-probe path only; measured net-negative on C4
-  // (236 vs 216 ms: most coarser probes hit, the map load only adds
-  // latency), so opt-in via AMRX_LEVEL_MAP=1 for hole-heavy data
-  static const bool enabled = std::getenv("AMRX_LEVEL_MAP") != nullptr;
-  g.map_on = enabled && g.nlevels <= 8 && blocks <= budget;
+  g.dir_bits = g.occ == kOccNone ? directory_bits(g, n) : occ_bits;
+  g.dir_shift = g.total - g.dir_bits;
   g.aligned = 1;
   for (int a = 0; a < 3; a++)
     if (mn[a] & ((int64_t(1) << hi_level) - 1)) g.aligned = 0;
@@ -522,7 +530,10 @@ void finish_info(amrx_index *ix, uint64_t equal_pairs, double ms)
     in.bounds_hi[a] = ix->bounds_hi[a];
   }
   in.key_bits = ix->g.total;
-  in.directory_bits = ix->g.dir_bits;
+  in.lookup = ix->g.occ == kOccDense  ? AMRX_LOOKUP_RECORDS
+              : ix->g.occ == kOccHash ? AMRX_LOOKUP_HASH
+                                      : AMRX_LOOKUP_DIRECTORY;
+  in.directory_bits = ix->g.occ == kOccHash ? bit_width(ix->hmask) : ix->g.dir_bits;
   in.duplicate_keys = equal_pairs;
   in.device_bytes = ix->keys.bytes + ix->scal.bytes + ix->dir.bytes +
                     ix->rec.bytes;
@@ -550,56 +561,67 @@ void setup_stream(amrx_index *ix, const amrx_index_opts *opts)
   }
 }
 
-/// bring the device-side directory + padding up for sorted keys
+/// bring the device-side lookup structure + padding up for sorted keys;
+/// ix->order receives {descents, equal pairs, longest hash probe}
 void finalize_index(amrx_index *ix)
 {
-  pad_keys(ix->keys.as<uint64_t>(), ix->n, ix->stream);
+  cudaStream_t st = ix->stream;
+  pad_keys(ix->keys.as<uint64_t>(), ix->n, st);
   const uint64_t entries = (uint64_t(1) << ix->g.dir_bits) + 1;
-  ix->order.reserve(16, ix->stream);
-  if (!ix->searchable) {
-    AMRX_CUDA(cudaMemsetAsync(ix->order.ptr, 0, 16, ix->stream));
-    return;
-  }
-  if (ix->g.occ) {
-    ix->rec.reserve((ix->rec_n ? ix->rec_n + 1 : entries) * sizeof(uint2), ix->stream);
-    build_directory(ix->keys.as<uint64_t>(), ix->n, ix->g, nullptr, ix->rec.as<uint2>(),
-                    ix->order.as<unsigned long long>(), ix->scratch, ix->stream,
-                    ix->rec_lo, ix->rec_n);
+  ix->order.reserve(32, st);
+  AMRX_CUDA(cudaMemsetAsync(ix->order.ptr, 0, 32, st));
+  auto *order = ix->order.as<unsigned long long>();
+  if (!ix->searchable) return;
+  if (ix->g.occ == kOccDense) {
+    ix->rec.reserve((ix->rec_n ? ix->rec_n + 1 : entries) * sizeof(uint2), st);
+    build_directory(ix->keys.as<uint64_t>(), ix->n, ix->g, nullptr, ix->rec.as<uint2>(), order,
+                    ix->scratch, st, ix->rec_lo, ix->rec_n);
+    ix->info.lookup_entries = ix->rec_n ? ix->rec_n + 1 : entries;
+  } else if (ix->g.occ == kOccHash) {
+    const uint64_t buckets = hash_count(ix->keys.as<uint64_t>(), ix->n, ix->g, order,
+                                        ix->scratch, st);
+    uint64_t slots = 64;
+    while (slots < 2 * buckets) slots <<= 1;
+    ix->rec.reserve(slots * sizeof(uint4), st);
+    ix->hmask = slots - 1;
+    build_hash(ix->keys.as<uint64_t>(), ix->n, ix->g, ix->rec.as<uint4>(), slots,
+               reinterpret_cast<unsigned int *>(order + 2), st);
+    ix->info.lookup_entries = slots;
   } else {
-    ix->dir.reserve(entries * sizeof(uint32_t), ix->stream);
+    ix->dir.reserve(entries * sizeof(uint32_t), st);
     build_directory(ix->keys.as<uint64_t>(), ix->n, ix->g, ix->dir.as<uint32_t>(), nullptr,
-                    ix->order.as<unsigned long long>(), ix->scratch, ix->stream);
-  }
-  if (ix->g.map_on) {
-    const uint64_t bytes =
-      ((uint64_t(ix->g.map_dim[0]) * uint64_t(ix->g.map_dim[1]) *
-          uint64_t(ix->g.map_dim[2]) + 3) & ~uint64_t(3));
-    ix->lmap.reserve(bytes, ix->stream);
-    build_level_map(ix->keys.as<uint64_t>(), ix->n, ix->g, ix->lmap.as<uint8_t>(),
-                    bytes, ix->stream);
+                    order, ix->scratch, st);
+    ix->info.lookup_entries = entries;
   }
 }
 
-/*! the order check fused into the directory build (after the stream has
+/*! the order check fused into the lookup build (after the stream has
     synchronised): sorted keys may not descend; equal neighbours are
     duplicate cells */
 uint64_t sorted_equal_pairs(amrx_index *ix)
 {
-  unsigned long long h[2];
+  unsigned long long h[3];
   AMRX_CUDA(cudaMemcpy(h, ix->order.ptr, sizeof h, cudaMemcpyDeviceToHost));
   if (h[0] != 0) fail(AMRX_ERR_INTERNAL, "index keys are not in (i,j,k,level) order");
+  ix->info.max_probe = uint32_t(h[2]);
   return h[1];
 }
 
-/*! an index with duplicate keys cannot use the occupancy records
-    (positions are not popcounts): build the plain bucket directory too */
+/*! an index with duplicate keys cannot use occupancy records (positions
+    are not popcounts): it switches to the bucket directory */
 void ensure_search_dir(amrx_index *ix, uint64_t equal_pairs)
 {
-  if (!ix->g.occ || equal_pairs == 0 || !ix->searchable) return;
-  if (ix->rec_n)
+  if (ix->g.occ == kOccNone || equal_pairs == 0 || !ix->searchable) return;
+  if (ix->partition)
     fail(AMRX_ERR_UNSUPPORTED, "a partition of a distributed index needs unique cells (" +
                                  std::to_string(equal_pairs) + " duplicate keys)");
+  ix->rec.release();
+  ix->g.occ = kOccNone;
+  ix->g.dir_bits = directory_bits(ix->g, ix->n);
+  ix->g.dir_shift = ix->g.total - ix->g.dir_bits;
+  ix->info.max_probe = 0;
   const uint64_t entries = (uint64_t(1) << ix->g.dir_bits) + 1;
+  ix->info.lookup_entries = entries;
   ix->dir.reserve(entries * sizeof(uint32_t), ix->stream);
   build_directory(ix->keys.as<uint64_t>(), ix->n, ix->g, ix->dir.as<uint32_t>(), nullptr,
                   ix->order.as<unsigned long long>(), ix->scratch, ix->stream);
@@ -611,12 +633,28 @@ void require_searchable(const amrx_index *ix)
     fail(AMRX_ERR_INVALID_ARG, "this index holds sorted arrays only (amrx_index_sort_part)");
 }
 
+/// point queries (find_exact, snap, try_build_dual, validate) need every
+/// cell: a partition holds one key range plus its halo
+void require_full(const amrx_index *ix)
+{
+  require_searchable(ix);
+  if (ix && ix->partition)
+    fail(AMRX_ERR_INVALID_ARG, "point queries need a full index; this is one partition of a "
+                               "distributed index (extract its owned cell range instead)");
+}
+
 void check_range(const amrx_index *ix, const amrx_range *range, uint64_t &b,
                  uint64_t &e)
 {
-  b = range ? range->cell_begin : 0;
-  e = range ? std::min<uint64_t>(range->cell_end, ix->n) : ix->n;
+  const uint64_t lo = std::min(ix->safe_lo, ix->n), hi = std::min(ix->safe_hi, ix->n);
+  b = range ? range->cell_begin : lo;
+  e = range ? std::min<uint64_t>(range->cell_end, ix->n) : hi;
   if (b > e) fail(AMRX_ERR_INVALID_ARG, "cell range begins after it ends");
+  if (b < e && (b < lo || e > hi))
+    fail(AMRX_ERR_INVALID_ARG, "cell range [" + std::to_string(b) + ", " + std::to_string(e) +
+                                 ") leaves the partition's interior [" + std::to_string(lo) +
+                                 ", " + std::to_string(hi) + "): its halo cells' neighbours "
+                                 "live on other ranks");
 }
 
 void fill_stats(amrx_stats *st, const ExtractResult &r, uint64_t cells)
@@ -661,6 +699,8 @@ const char *amrx_last_error(void) { return g_last_error.c_str(); }
 const char *amrx_version(void) { return "amrx 0.1 (sm_100a)"; }
 
 uint64_t amrx_kernel_launches(void) { return g_launches.load(); }
+
+void amrx_debug_round_limit(uint64_t items) { amrx::g_round_limit.store(items); }
 
 namespace {
 
@@ -773,12 +813,12 @@ void create_impl(const int32_t *cells4, const double *scalars, uint64_t n_cells,
         fail(AMRX_ERR_INVALID_ARG, "records on levels outside the given geometry");
       const int64_t mn[3] = {g16[0], g16[1], g16[2]};
       const int64_t mx[3] = {g16[3], g16[4], g16[5]};
-      ix->g = make_geometry(mn, mx, uint32_t(g16[9]), uint64_t(g16[10]));
+      ix->g = make_geometry(mn, mx, uint32_t(g16[9]), uint64_t(g16[10]), opts ? opts->flags : 0);
       for (int a = 0; a < 3; a++) ix->bounds_hi[a] = g16[6 + a];
     } else {
       const int64_t mn[3] = {pre.mn[0], pre.mn[1], pre.mn[2]};
       const int64_t mx[3] = {pre.mx[0], pre.mx[1], pre.mx[2]};
-      ix->g = make_geometry(mn, mx, pre.level_mask, n);
+      ix->g = make_geometry(mn, mx, pre.level_mask, n, opts ? opts->flags : 0);
       for (int a = 0; a < 3; a++) ix->bounds_hi[a] = pre.hi[a];
     }
 
@@ -1184,16 +1224,19 @@ amrx_status amrx_index_from_keys(const void *keys_dev, const double *scalars_dev
     ix->n = n;
     const int64_t mn[3] = {g16[0], g16[1], g16[2]};
     const int64_t mx[3] = {g16[3], g16[4], g16[5]};
-    ix->g = make_geometry(mn, mx, uint32_t(g16[9]), uint64_t(g16[10]));
+    ix->g = make_geometry(mn, mx, uint32_t(g16[9]), uint64_t(g16[10]), opts ? opts->flags : 0);
     for (int a = 0; a < 3; a++) ix->bounds_hi[a] = g16[6 + a];
-    if (!ix->g.occ)
-      fail(AMRX_ERR_UNSUPPORTED, "this geometry has no occupancy records: a partition "
-                                 "index needs them");
+    if (ix->g.occ == kOccNone)
+      fail(AMRX_ERR_UNSUPPORTED, "a partition index needs occupancy records (dense or "
+                                 "hashed), not the directory");
+    ix->partition = true;
     ix->id_base = g16[12];
     ix->key_lo = uint64_t(g16[13]);
     ix->key_hi = uint64_t(g16[14]);
-    ix->rec_lo = ((ix->key_lo >> ix->g.dir_shift) >> kRecTileLog) << kRecTileLog;
-    ix->rec_n = ((ix->key_hi - 1) >> ix->g.dir_shift) - ix->rec_lo + 1;
+    if (ix->g.occ == kOccDense) {
+      ix->rec_lo = ((ix->key_lo >> ix->g.dir_shift) >> kRecTileLog) << kRecTileLog;
+      ix->rec_n = ((ix->key_hi - 1) >> ix->g.dir_shift) - ix->rec_lo + 1;
+    }
     cudaEvent_t e0, e1;
     AMRX_CUDA(cudaEventCreate(&e0));
     AMRX_CUDA(cudaEventCreate(&e1));
@@ -1231,6 +1274,27 @@ amrx_status amrx_index_from_keys(const void *keys_dev, const double *scalars_dev
     AMRX_CUDA(cudaStreamSynchronize(st));
     if (ends[0] < ix->key_lo || ends[1] >= ix->key_hi)
       fail(AMRX_ERR_INVALID_ARG, "keys outside the partition's key range");
+    {
+      // interior: a lookup of cell c has its major coordinate in
+      // (m - 2 cw, m + cw] (m = c's, cw = the coarsest width: a stencil
+      // point is one owner width away, then masked to a coarser level), so
+      // cells two coarsest widths inside each end of the range only look
+      // up keys in it (dist.halo_ranges builds ranges with that halo)
+      const KeyGeom &g = ix->g;
+      int msh = g.lbits;
+      for (int a = 2; a >= 0; a--)
+        if (g.bits[a]) msh = g.sh[a];
+      const int coarsest = g.nlevels ? g.levels[g.nlevels - 1] : g.shift;
+      const uint64_t hw = uint64_t(2) << (coarsest - g.shift);
+      const uint64_t top = g.total >= 64 ? ~0ull : (uint64_t(1) << g.total);
+      const uint64_t mlo = ix->key_lo >> msh, mhi = ix->key_hi >> msh;
+      uint64_t q[2] = {ix->key_lo == 0 ? 0 : (mlo + hw) << msh,
+                       ix->key_hi >= top ? ~0ull : (mhi > hw ? (mhi - hw) << msh : 0)};
+      uint64_t pos[2];
+      lower_bounds(ix->keys.as<uint64_t>(), n, q, 2, pos, st);
+      ix->safe_lo = pos[0];
+      ix->safe_hi = pos[1];
+    }
     finalize_index(ix.get());
     AMRX_CUDA(cudaEventRecord(e1, st));
     AMRX_CUDA(cudaStreamSynchronize(st));
@@ -1250,7 +1314,7 @@ amrx_status amrx_validate(amrx_index *index, uint32_t *dup_pairs, uint64_t dup_c
                           uint64_t *n_overlap)
 {
   return guarded([&] {
-    require_searchable(index);
+    require_full(index);
     if (!index || !n_dup || !n_overlap) fail(AMRX_ERR_INVALID_ARG, "null argument");
     std::lock_guard<std::mutex> lock(index->mu);
     DeviceGuard dg(index->device);
@@ -1325,7 +1389,6 @@ amrx_status amrx_index_destroy(amrx_index *index)
       index->scal.release();
       index->dir.release();
       index->rec.release();
-      index->lmap.release();
       index->order.release();
       index->scratch.release();
       index->out_a.release();
@@ -1419,7 +1482,7 @@ amrx_status amrx_index_adopt(const void *keys_dev, const double *scalars_dev,
     ix->n = n_cells;
     const int64_t mn[3] = {g16[0], g16[1], g16[2]};
     const int64_t mx[3] = {g16[3], g16[4], g16[5]};
-    ix->g = make_geometry(mn, mx, uint32_t(g16[9]), n_cells);
+    ix->g = make_geometry(mn, mx, uint32_t(g16[9]), n_cells, opts ? opts->flags : 0);
     for (int a = 0; a < 3; a++) ix->bounds_hi[a] = g16[6 + a];
     cudaEvent_t e0, e1;
     AMRX_CUDA(cudaEventCreate(&e0));
@@ -1451,7 +1514,7 @@ amrx_status amrx_find_exact(amrx_index *index, const int32_t *cells4,
                             uint64_t n, int64_t *out_ids)
 {
   return guarded([&] {
-    require_searchable(index);
+    require_full(index);
     if (!index) fail(AMRX_ERR_INVALID_ARG, "null index");
     if (n == 0) return;
     DeviceGuard dg(index->device);
@@ -1469,7 +1532,7 @@ amrx_status amrx_snap(amrx_index *index, const int64_t *points3,
                       int64_t *out_ids)
 {
   return guarded([&] {
-    require_searchable(index);
+    require_full(index);
     if (!index) fail(AMRX_ERR_INVALID_ARG, "null index");
     if (n == 0) return;
     DeviceGuard dg(index->device);
@@ -1488,7 +1551,7 @@ amrx_status amrx_try_build_duals(amrx_index *index, const uint64_t *tasks,
                                  uint32_t *out_corners8)
 {
   return guarded([&] {
-    require_searchable(index);
+    require_full(index);
     if (!index) fail(AMRX_ERR_INVALID_ARG, "null index");
     if (n == 0) return;
     DeviceGuard dg(index->device);
@@ -1517,7 +1580,7 @@ amrx_status amrx_extract_dual(amrx_index *index, const amrx_range *range,
     check_range(index, range, b, e);
     const uint64_t cells = e - b;
     auto &C = index->cache;
-    // device memory or pinned host memory: written in place by the kernels
+    // device memory or pinned host memory: written by the rounds directly
     uint32_t *corners_w = static_cast<uint32_t *>(device_writable(corners8));
     uint64_t *tasks_w = static_cast<uint64_t *>(device_writable(task_ids));
     const bool dev_out = corners_w && (!task_ids || tasks_w);
@@ -1526,7 +1589,6 @@ amrx_status amrx_extract_dual(amrx_index *index, const amrx_range *range,
     rq.s = index->ctx();
     rq.g = index->g;
     rq.scal = index->scal.as<double>();
-    rq.lmap = index->lmap.as<uint8_t>();
     rq.unique = index->info.duplicate_keys == 0;
     rq.cell_begin = b;
     rq.cell_end = e;
@@ -1546,29 +1608,21 @@ amrx_status amrx_extract_dual(amrx_index *index, const amrx_range *range,
                                   " < " + std::to_string(r.duals) + " duals");
       return;
     }
-    // host (or absent) output: run into the device arena, keep it cached
+    // pageable host (or absent) output: extract into the index's device
+    // arena, which grows to fit, and keep it for the count-then-copy pattern
     const bool hit = C.valid && C.kind == 1 && C.begin == b && C.end == e;
     if (!hit) {
-      uint64_t arena = std::max<uint64_t>(1024, cells + cells / 4);
-      for (int attempt = 0; attempt < 2; attempt++) {
-        index->out_a.reserve(arena * 32, st);
-        index->out_b.reserve(arena * 8, st);
-        rq.corners = index->out_a.as<uint32_t>();
-        rq.tasks = index->out_b.as<uint64_t>();
-        rq.dual_cap = arena;
-        const ExtractResult r = run_extract(rq, st);
-        check_result(r, cells, false);
-        if (r.duals <= arena) {
-          C.valid = true;
-          C.kind = 1;
-          C.begin = b;
-          C.end = e;
-          C.count = r.duals;
-          fill_stats(&C.stats, r, cells);
-          break;
-        }
-        arena = r.duals;
-      }
+      C.valid = false;
+      rq.grow_a = &index->out_a;
+      rq.grow_b = &index->out_b;
+      const ExtractResult r = run_extract(rq, st);
+      check_result(r, cells, false);
+      C.valid = true;
+      C.kind = 1;
+      C.begin = b;
+      C.end = e;
+      C.count = r.duals;
+      fill_stats(&C.stats, r, cells);
     }
     *count = C.count;
     if (stats) *stats = C.stats;
@@ -1576,10 +1630,10 @@ amrx_status amrx_extract_dual(amrx_index *index, const amrx_range *range,
     if (C.count > cap)
       fail(AMRX_ERR_CAPACITY, "output capacity " + std::to_string(cap) + " < " +
                                 std::to_string(C.count) + " duals");
-    if (corners8)
+    if (corners8 && C.count)
       AMRX_CUDA(cudaMemcpyAsync(corners8, index->out_a.ptr, C.count * 32,
                                 cudaMemcpyDefault, st));
-    if (task_ids)
+    if (task_ids && C.count)
       AMRX_CUDA(cudaMemcpyAsync(task_ids, index->out_b.ptr, C.count * 8,
                                 cudaMemcpyDefault, st));
     AMRX_CUDA(cudaStreamSynchronize(st));
@@ -1601,7 +1655,7 @@ amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range,
     const uint64_t cells = e - b;
     const size_t tri_bytes = params->xyz_is_f32 ? 36 : 72;
     auto &C = index->cache;
-    // device memory or pinned host memory: written in place by the kernels
+    // device memory or pinned host memory: written by the rounds directly
     void *xyz_w = device_writable(xyz9);
     const bool dev_out = xyz_w != nullptr;
 
@@ -1609,87 +1663,24 @@ amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range,
     rq.s = index->ctx();
     rq.g = index->g;
     rq.scal = index->scal.as<double>();
-    rq.lmap = index->lmap.as<uint8_t>();
     rq.unique = index->info.duplicate_keys == 0;
     rq.cell_begin = b;
     rq.cell_end = e;
     rq.emit_tri = true;
     rq.tri_f32 = params->xyz_is_f32 != 0;
-    rq.jobs_per_kcell = &index->jobs_per_kcell;
     rq.iso = params->iso;
     const auto length_check = [&](uint64_t tris) {
       if (params->check_length &&
           tris > uint64_t(std::numeric_limits<uint32_t>::max()) / 3)
         fail(AMRX_ERR_LENGTH, "extract_isosurface: mesh too large for 32-bit indices");
     };
-    if (dev_out && !is_device_ptr(xyz9) && cells >= (uint64_t(1) << 24)) {
-      // pinned host output, large input: extract in cell-range chunks (their
-      // concatenation is the candidate order) so each chunk's download
-      // overlaps the next chunk's extraction
-      // the downloads are the bottleneck (host link), so the only exposed
-      // extraction time is the first chunk's: start small, then grow --
-      // cut points at 1/64, 1/32 (cumulative 3/64), then equal eighths of
-      // the rest
-      uint64_t cut[12];
-      int nch = 0;
-      cut[0] = 0;
-      cut[++nch] = cells / 64;
-      cut[++nch] = cells * 3 / 64;
-      for (int k = 1; k <= 8; k++) cut[++nch] = cells * 3 / 64 + (cells - cells * 3 / 64) * k / 8;
-      cudaStream_t cp;
-      cudaEvent_t done[2];
-      AMRX_CUDA(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
-      AMRX_CUDA(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
-      AMRX_CUDA(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
-      struct Cleanup {
-        cudaStream_t s;
-        cudaEvent_t e0, e1;
-        ~Cleanup()
-        {
-          cudaStreamSynchronize(s);
-          cudaStreamDestroy(s);
-          cudaEventDestroy(e0);
-          cudaEventDestroy(e1);
-        }
-      } cleanup{cp, done[0], done[1]};
-      ExtractResult tot{};
-      uint64_t off = 0;
-      for (int ci = 0; ci < nch; ci++) {
-        rq.cell_begin = b + cut[ci];
-        rq.cell_end = b + cut[ci + 1];
-        rq.final_host = true;
-        rq.xyz = static_cast<char *>(xyz9) + off * tri_bytes;
-        rq.tri_cap = cap > off ? cap - off : 0;
-        rq.copy_stream = cp;
-        rq.out_slot = (ci & 1) ? kWsOutB : kWsOutA;
-        rq.slot_free = ci >= 2 ? done[ci & 1] : nullptr;
-        rq.copy_done = done[ci & 1];
-        rq.bits_ready = ci > 0;
-        const ExtractResult r = run_extract(rq, st);
-        check_result(r, rq.cell_end - rq.cell_begin, true);
-        for (int i = 0; i < 4; i++) tot.counters[i] += r.counters[i];
-        tot.duals += r.duals;
-        tot.tris_counted += r.tris_counted;
-        tot.tris_written += r.tris_written;
-        tot.ms += r.ms;
-        tot.ms2 += r.ms2;
-        tot.launches += r.launches;
-        off += r.tris_written;
-      }
-      AMRX_CUDA(cudaStreamSynchronize(cp));
-      fill_stats(stats, tot, cells);
-      *count = tot.tris_written;
-      C.valid = false;
-      length_check(tot.tris_written);
-      if (tot.tris_written > cap)
-        fail(AMRX_ERR_CAPACITY, "output capacity " + std::to_string(cap) + " < " +
-                                  std::to_string(tot.tris_written) + " triangles");
-      return;
-    }
     if (dev_out) {
       rq.final_host = !is_device_ptr(xyz9);
       rq.xyz = rq.final_host ? xyz9 : xyz_w;
       rq.tri_cap = cap;
+      // pinned host output of a large input: small first rounds, each
+      // round's download overlapping the next round's extraction
+      rq.stream_rounds = rq.final_host && cells >= (uint64_t(1) << 24);
       const ExtractResult r = run_extract(rq, st);
       check_result(r, cells, true);
       fill_stats(stats, r, cells);
@@ -1704,26 +1695,18 @@ amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range,
     const bool hit = C.valid && C.kind == 2 && C.begin == b && C.end == e &&
                      C.iso == params->iso && C.f32 == params->xyz_is_f32;
     if (!hit) {
-      uint64_t arena = std::max<uint64_t>(4096, cells / 2);
-      for (int attempt = 0; attempt < 2; attempt++) {
-        index->out_a.reserve(arena * tri_bytes, st);
-        rq.xyz = index->out_a.ptr;
-        rq.tri_cap = arena;
-        const ExtractResult r = run_extract(rq, st);
-        check_result(r, cells, true);
-        if (r.tris_written <= arena) {
-          C.valid = true;
-          C.kind = 2;
-          C.begin = b;
-          C.end = e;
-          C.iso = params->iso;
-          C.f32 = params->xyz_is_f32;
-          C.count = r.tris_written;
-          fill_stats(&C.stats, r, cells);
-          break;
-        }
-        arena = r.tris_written;
-      }
+      C.valid = false;
+      rq.grow_a = &index->out_a;
+      const ExtractResult r = run_extract(rq, st);
+      check_result(r, cells, true);
+      C.valid = true;
+      C.kind = 2;
+      C.begin = b;
+      C.end = e;
+      C.iso = params->iso;
+      C.f32 = params->xyz_is_f32;
+      C.count = r.tris_written;
+      fill_stats(&C.stats, r, cells);
     }
     *count = C.count;
     if (stats) *stats = C.stats;
@@ -1732,8 +1715,9 @@ amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range,
     if (C.count > cap)
       fail(AMRX_ERR_CAPACITY, "output capacity " + std::to_string(cap) + " < " +
                                 std::to_string(C.count) + " triangles");
-    AMRX_CUDA(cudaMemcpyAsync(xyz9, index->out_a.ptr, C.count * tri_bytes,
-                              cudaMemcpyDefault, st));
+    if (C.count)
+      AMRX_CUDA(cudaMemcpyAsync(xyz9, index->out_a.ptr, C.count * tri_bytes,
+                                cudaMemcpyDefault, st));
     AMRX_CUDA(cudaStreamSynchronize(st));
   });
 }

@@ -32,18 +32,13 @@ struct KeyGeom {
   uint32_t level_mask;  // bit l set iff level l present
   int32_t nlevels;
   int8_t levels[32];    // present levels, finest first (locator.cpp:85-89)
-  // block level map: one byte per 2^map_shift-aligned block (map_shift =
-  // coarsest level present), bit b set iff some cell of level levels[b]
-  // lies in the block.  A cell containing point p lies in p's block, so
-  // only those levels can hit.  map_on = 0 when > 8 levels or too large.
-  int32_t map_on;
-  int32_t map_shift;
-  int64_t map_base[3];  // block index of the lowest anchor per axis
-  int64_t map_dim[3];   // blocks per axis
   // occupancy records: buckets are 32 consecutive key values (dir_shift
   // = 5, or one bucket when total <= 5); record b = {first position of the
   // bucket, bit v set iff key (b << 5) + v is stored}, so a lookup is one
-  // 8-byte load and a popcount
+  // 8-byte load and a popcount.  occ = kOccDense: a record for every
+  // bucket of the key space; kOccHash: records of the occupied buckets only,
+  // in an open-addressed table (sparse or deep key spaces); kOccNone: the
+  // bucket directory + binary search (duplicate keys, or forced)
   int32_t occ;
   // packed-space coarsening: when every min anchor is aligned to the
   // coarsest level present (aligned = 1), anchor_mask(p, L) of an in-range
@@ -54,22 +49,28 @@ struct KeyGeom {
 };
 
 constexpr int kOccShift = 5;  // key values per occupancy record = 2^5
+enum : int32_t { kOccNone = 0, kOccDense = 1, kOccHash = 2 };
 
-/// candidate-level bits (index into g.levels) for point p from the map
-__device__ __forceinline__ uint32_t block_levels(const KeyGeom &g,
-                                                 const uint8_t *map,
-                                                 int64_t px, int64_t py,
-                                                 int64_t pz)
+/*! Hashed occupancy records: slot = {u64 tag = bucket + 1 (0 = empty), u32
+    start, u32 bits} (16 bytes, one vector load).  Linear probing from
+    hash_home(bucket); the four buckets of an aligned 128-value superbucket
+    share one hashed home group (mix of bucket >> 2, low two bits kept), so
+    neighbouring records of a dense region sit in one 64-byte run like the
+    dense array's.  The table has at least twice as many slots as occupied
+    buckets; the build reports the longest probe. */
+__host__ __device__ inline uint64_t mix64(uint64_t x)
 {
-  if (!g.map_on) return (1u << g.nlevels) - 1;
-  const int64_t bx = (px >> g.map_shift) - g.map_base[0];
-  const int64_t by = (py >> g.map_shift) - g.map_base[1];
-  const int64_t bz = (pz >> g.map_shift) - g.map_base[2];
-  if (bx < 0 || by < 0 || bz < 0 || bx >= g.map_dim[0] || by >= g.map_dim[1] ||
-      bz >= g.map_dim[2])
-    return 0;
-  return __ldg(map + (uint64_t(bz) * uint64_t(g.map_dim[1]) + uint64_t(by)) *
-                       uint64_t(g.map_dim[0]) + uint64_t(bx));
+  x ^= x >> 31;
+  x *= 0x7fb5d329728ea185ull;
+  x ^= x >> 27;
+  x *= 0x81dadef4bc2dd44dull;
+  x ^= x >> 33;
+  return x;
+}
+
+__host__ __device__ inline uint64_t hash_home(uint64_t bucket, uint64_t mask)
+{
+  return ((mix64(bucket >> 2) << 2) | (bucket & 3)) & mask;
 }
 
 __host__ __device__ inline int64_t anchor_mask(int64_t x, int32_t level)
@@ -267,6 +268,10 @@ struct SearchCtx {
   // the records of its key range only: `rec` is offset so rec[b] is still
   // indexed by the global bucket (only in-range buckets are ever read)
   const uint2 *rec;
+  // hashed occupancy records (KeyGeom::occ == kOccHash), or null: 2^k
+  // 16-byte slots, hmask = 2^k - 1
+  const uint4 *htab;
+  uint64_t hmask;
   // global CellId of local position 0 (a partition of a distributed index;
   // 0 otherwise): added to every id a query or an extraction reports
   int64_t id_base;
@@ -300,6 +305,48 @@ __device__ __forceinline__ int64_t occ_resolve(uint64_t q, uint2 r, uint32_t lma
 __device__ __forceinline__ uint2 ldg_rec(const uint2 *rec, uint64_t q, int dir_shift)
 {
   return __ldg(rec + (q >> dir_shift));
+}
+
+__device__ __forceinline__ uint64_t slot_tag(uint4 e)
+{
+  return uint64_t(e.x) | (uint64_t(e.y) << 32);
+}
+
+/// the hashed record of bucket b, continuing a probe at slot h whose entry
+/// e was already loaded; {0, 0} (no bits) when the bucket is empty
+__device__ __forceinline__ uint2 hash_probe(const SearchCtx &s, uint64_t b, uint64_t h, uint4 e)
+{
+  for (;;) {
+    const uint64_t t = slot_tag(e);
+    if (t == b + 1) return make_uint2(e.z, e.w);
+    if (t == 0) return make_uint2(0, 0);
+    h = (h + 1) & s.hmask;
+    e = __ldg(s.htab + h);
+  }
+}
+
+/// batch_find through the hashed records: the K home slots are loaded
+/// together, the (rare) displaced entries probed afterwards
+template <int K, bool FINER>
+__device__ __forceinline__ void hash_find(const SearchCtx &s, const uint64_t (&q)[K],
+                                          const bool (&valid)[K], int64_t (&out)[K],
+                                          int (&lvl)[K])
+{
+  uint4 e[K];
+  uint64_t h[K];
+#pragma unroll
+  for (int k = 0; k < K; k++) {
+    h[k] = hash_home(q[k] >> s.dir_shift, s.hmask);
+    e[k] = valid[k] ? __ldg(s.htab + h[k]) : make_uint4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int k = 0; k < K; k++)
+    if (valid[k]) {
+      const uint2 r = hash_probe(s, q[k] >> s.dir_shift, h[k], e[k]);
+      int rl;
+      out[k] = occ_resolve<FINER>(q[k], r, uint32_t(s.lmask), rl);
+      lvl[k] = rl + s.shift;
+    }
 }
 
 /// debug event counters, one atomic per warp-level event, lane 0 only
@@ -378,6 +425,10 @@ __device__ __forceinline__ void batch_find(const SearchCtx &s, const uint64_t (&
 {
   if (s.rec) {  // occupancy records: no search at all
     occ_find<K, FINER>(s, q, valid, out, lvl);
+    return;
+  }
+  if (s.htab) {
+    hash_find<K, FINER>(s, q, valid, out, lvl);
     return;
   }
   uint32_t lo[K], n[K];
@@ -497,6 +548,10 @@ __device__ void warp_find(const SearchCtx &s, const uint64_t (&q)[NQ],
 {
   if (s.rec) {  // occupancy records: per lane, no search (warp-uniform branch)
     occ_find<NQ, FINER>(s, q, valid, out, lvl);
+    return;
+  }
+  if (s.htab) {
+    hash_find<NQ, FINER>(s, q, valid, out, lvl);
     return;
   }
   const uint32_t lane = lane_id();

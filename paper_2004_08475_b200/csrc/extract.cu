@@ -30,7 +30,11 @@
 #include "internal.h"
 #include "mc_tables.inc"
 
+#include <algorithm>
 #include <atomic>
+#include <initializer_list>
+#include <stdexcept>
+#include <string>
 #include <utility>
 #include <mutex>
 #include <unordered_map>
@@ -77,18 +81,40 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v)
 constexpr uint32_t kDualChunk = 1024;  // >= 8 * 32, the most one tile emits
 constexpr uint32_t kTriChunk = 2048;   // >= 40 * 32 (5 triangles x 8 duals)
 
+/*! Rounds (run_extract): a launch processes tiles in ticket order until
+    every tile is done, the round's tile limit is reached, or a staging
+    buffer's cursor passes its guard (capacity minus the headroom the tiles
+    already in flight may still claim: one chunk per warp per tile, with a
+    2x margin).  The warp that passes a guard adds kStopTicket to the ticket
+    counter -- every later ticket is out of range -- and records the counter
+    it saw, so the round's tiles are exactly [first ticket, stop).  No
+    allocation can exceed its buffer, and no tile is ever half done. */
+constexpr unsigned long long kStopTicket = 1ull << 40;
+
+__device__ __forceinline__ void stop_round(unsigned long long *ticket,
+                                           unsigned long long *stop_at)
+{
+  const unsigned long long old = atomicAdd(ticket, kStopTicket);
+  if (old < kStopTicket) atomicMin(stop_at, old);
+}
+
 /*! staging space for `agg` items of this tile from the warp's private
     chunk (cur_end[0], cur_end[1] in shared memory); a new chunk comes from
-    one atomicAdd on the arena cursor.  Warp-uniform. */
+    one atomicAdd on the arena cursor (and may end the round).  Warp-uniform. */
 __device__ __forceinline__ uint64_t reserve(uint64_t *cur_end, uint32_t agg,
                                             uint32_t chunk,
-                                            unsigned long long *cursor)
+                                            unsigned long long *cursor, uint64_t guard,
+                                            unsigned long long *ticket,
+                                            unsigned long long *stop_at)
 {
   if (agg == 0) return 0;
   uint64_t cur = cur_end[0], end = cur_end[1];
   if (cur + agg > end) {
     unsigned long long b = 0;
-    if (lane_id() == 0) b = atomicAdd(cursor, (unsigned long long)chunk);
+    if (lane_id() == 0) {
+      b = atomicAdd(cursor, (unsigned long long)chunk);
+      if (b + chunk > guard) stop_round(ticket, stop_at);
+    }
     b = __shfl_sync(kFull, b, 0);
     cur = b;
     end = b + chunk;
@@ -118,10 +144,18 @@ static_assert(sizeof(McJob) == 64, "McJob is 64 bytes");
 
 /*! Marching cubes writes each dual's triangles at the case table's upper
     bound; the slots a dual leaves unused (sliver triangles are dropped,
-    contour.cpp:80-84) get this signalling-NaN marker as their first word --
-    arithmetic never produces a signalling NaN -- and reorder_tri_kernel
-    skips them. */
-constexpr uint32_t kGapMark = 0xFFB4C0DEu;
+    contour.cpp:80-84) get a signalling-NaN marker in the word holding the
+    sign and exponent of x0 -- word 0 of an f32 slot, word 1 (the high half)
+    of an f64 slot -- and reorder_tri_kernel skips them.  Arithmetic never
+    produces a signalling NaN (a NaN result is quiet), so no real vertex
+    matches: all-ones exponent with the quiet bit clear. */
+constexpr uint32_t kGapMark32 = 0xFFB4C0DEu;  // f32: exponent 0xFF, quiet bit 0
+constexpr uint32_t kGapMark64 = 0xFFF4C0DEu;  // f64 high word: exponent 0x7FF, quiet bit 0
+__host__ __device__ constexpr int gap_word(int words) { return words == 9 ? 0 : 1; }
+__host__ __device__ constexpr uint32_t gap_mark(int words)
+{
+  return words == 9 ? kGapMark32 : kGapMark64;
+}
 
 /// bit i of the result: scalar i > iso (the strict case test of contour.cpp:22-28)
 __global__ void __launch_bounds__(256)
@@ -144,14 +178,14 @@ __global__ void __launch_bounds__(256)
 reorder_tri_kernel(const uint32_t *__restrict__ cnt, const uint32_t *__restrict__ up,
                    const uint64_t *__restrict__ src_off, const uint64_t *__restrict__ dst_off,
                    uint32_t tiles, int words, const uint32_t *__restrict__ src,
-                   uint32_t *__restrict__ dst, uint64_t dst_cap)
+                   uint32_t *__restrict__ dst, uint64_t dst_base, uint64_t dst_cap)
 {
   const int lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
   for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < tiles; t += warps) {
     const uint32_t n = cnt[t], u = up[t];
     if (!n) continue;
-    const uint64_t so = src_off[t], d0 = dst_off[t];
+    const uint64_t so = src_off[t], d0 = dst_base + dst_off[t];
     if (n == u) {
       const uint64_t keep = d0 >= dst_cap ? 0 : (d0 + n > dst_cap ? dst_cap - d0 : n);
       const uint64_t nw = keep * uint64_t(words);
@@ -159,9 +193,11 @@ reorder_tri_kernel(const uint32_t *__restrict__ cnt, const uint32_t *__restrict_
       continue;
     }
     uint64_t done = 0;
+    const int gw = gap_word(words);
+    const uint32_t gm = gap_mark(words);
     for (uint32_t i0 = 0; i0 < u; i0 += 32) {
       const uint32_t i = i0 + lane;
-      const bool ok = i < u && __ldg(src + (so + i) * words) != kGapMark;
+      const bool ok = i < u && __ldg(src + (so + i) * words + gw) != gm;
       uint32_t bal = __ballot_sync(kFull, ok);
       while (bal) {  // the kept slots of this chunk, in order
         const int l = __ffs(bal) - 1;
@@ -181,8 +217,8 @@ __global__ void __launch_bounds__(256)
 reorder_kernel(const uint32_t *__restrict__ cnt, const uint64_t *__restrict__ src_off,
                const uint64_t *__restrict__ dst_off, uint32_t tiles, int words,
                const uint32_t *__restrict__ src, uint32_t *__restrict__ dst,
-               uint64_t dst_cap, int words2, const uint32_t *__restrict__ src2,
-               uint32_t *__restrict__ dst2)
+               uint64_t dst_base, uint64_t dst_cap, int words2,
+               const uint32_t *__restrict__ src2, uint32_t *__restrict__ dst2)
 {
   const int lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
@@ -190,7 +226,7 @@ reorder_kernel(const uint32_t *__restrict__ cnt, const uint64_t *__restrict__ sr
        t += warps) {
     const uint32_t n = cnt[t];
     if (!n) continue;
-    const uint64_t so = src_off[t], d0 = dst_off[t];
+    const uint64_t so = src_off[t], d0 = dst_base + dst_off[t];
     const uint64_t keep = d0 >= dst_cap ? 0 : (d0 + n > dst_cap ? dst_cap - d0 : n);
     const uint64_t nw = keep * uint64_t(words);
     for (uint64_t w = lane; w < nw; w += 32)
@@ -206,7 +242,6 @@ reorder_kernel(const uint32_t *__restrict__ cnt, const uint64_t *__restrict__ sr
 struct KArgs {
   SearchCtx s;
   KeyGeom g;
-  const uint8_t *lmap;  // block level map (g.map_on)
   const uint32_t *above;  // bit i: scalar i > iso (EMIT_TRI)
   bool unique;            // no duplicate keys in the index
   const double *scal;
@@ -225,10 +260,16 @@ struct KArgs {
   uint64_t *tile_tri_off;
   struct McJob *jobs;      // crossing duals for mc_jobs_kernel (EMIT_TRI)
   uint64_t job_cap;
-  unsigned int *ticket;
+  // round control: tiles [ticket, tile_limit); a cursor past its guard ends
+  // the round (stop_round)
+  uint64_t tile_limit;
+  uint64_t dual_guard, tri_guard, job_guard;
+  unsigned long long *ticket;
+  unsigned long long *stop_at;
   unsigned long long *out;  // [0..3] counters, [4] duals, [5] tris counted,
                             // [6] tris written, [7] error flags,
-                            // [8] dual arena cursor, [9] tri arena cursor
+                            // [8] dual arena cursor, [9] tri arena cursor,
+                            // [10] job cursor
 };
 
 struct Smem {
@@ -339,7 +380,9 @@ __device__ __forceinline__ int mc_core(const double *scal, const uint64_t *rows,
   }
   for (int g = count; g < ntab; g++) {  // mark the slots slivers left unused
     const uint64_t slot = at + uint64_t(g);
-    if (slot < cap) static_cast<uint32_t *>(out)[slot * (F32 ? 9 : 18)] = kGapMark;
+    if (slot < cap)
+      static_cast<uint32_t *>(out)[slot * (F32 ? 9 : 18) + gap_word(F32 ? 9 : 18)] =
+        gap_mark(F32 ? 9 : 18);
   }
   return count;
 }
@@ -423,7 +466,7 @@ __device__ __noinline__ Hit probe_coarser(const KArgs &a, int level, const Stenc
   struct {
     int level;
   } c{level};
-  if (g.aligned && !g.map_on && ((st.inrange >> p) & 1u)) {
+  if (g.aligned && ((st.inrange >> p) & 1u)) {
     // in-range point, aligned origin: coarsen in packed key space
     const uint64_t q0 = stencil_key(st, p);
     while (cand) {
@@ -438,19 +481,13 @@ __device__ __noinline__ Hit probe_coarser(const KArgs &a, int level, const Stenc
     }
     return Hit{-1, c.level};
   }
-  // the cell's coordinates only on this (unaligned / level-map) path:
-  // decoded from its key here, so the hot loop carries just the level
+  // the cell's coordinates only on this (unaligned-origin or out-of-range
+  // point) path: decoded from its key here, so the hot loop carries just
+  // the level
   const Cell cc = unpack(g, st.k0);
   const int64_t w = int64_t(1) << c.level;
   const int64_t px = cc.i + (p % 3 - 1) * w, py = cc.j + ((p / 3) % 3 - 1) * w,
                 pz = cc.k + (p / 9 - 1) * w;
-  if (g.map_on) {
-    // only levels present in the point's coarsest-aligned block can hold
-    // it (exact); a point in a hole or outside the domain costs no lookup
-    uint32_t idx = block_levels(g, a.lmap, px, py, pz), lv = 0;
-    for (; idx; idx &= idx - 1) lv |= 1u << g.levels[__ffs(idx) - 1];
-    cand &= lv;
-  }
   while (cand) {
     const int L = __ffs(cand) - 1;
     cand &= cand - 1;
@@ -649,10 +686,11 @@ extract_kernel(const __grid_constant__ KArgs a)
   // thousand tiles of each other, so the lookups share one compact L2
   // working set (a static interleaved assignment drifts apart: 19% slower)
   for (;;) {
-    uint32_t tile = 0;
-    if (lane == 0) tile = atomicAdd(a.ticket, 1u);
-    tile = __shfl_sync(kFull, tile, 0);
-    if (tile >= a.num_tiles) break;
+    unsigned long long tk = 0;
+    if (lane == 0) tk = atomicAdd(a.ticket, 1ull);
+    tk = __shfl_sync(kFull, tk, 0);
+    if (tk >= a.tile_limit) break;
+    const uint32_t tile = uint32_t(tk);
     dbg_add(a.s, kDbgTiles);
 
     const uint64_t cell_s = a.cell_begin + uint64_t(tile) * kTileCells + lane;
@@ -774,8 +812,9 @@ extract_kernel(const __grid_constant__ KArgs a)
     if (EMIT_DUAL) {
       const uint32_t incl = warp_incl_scan(nd);
       const uint32_t agg = __shfl_sync(kFull, incl, 31);
-      const uint64_t base =
-        reserve(&sm.chunk[warp][0], agg, kDualChunk, a.out + 8) + (incl - nd);
+      const uint64_t base = reserve(&sm.chunk[warp][0], agg, kDualChunk, a.out + 8,
+                                    a.dual_guard, a.ticket, a.stop_at) +
+                            (incl - nd);
       if (lane == 0) {
         a.tile_dual_cnt[tile] = agg;
         a.tile_dual_off[tile] = base;
@@ -801,8 +840,8 @@ extract_kernel(const __grid_constant__ KArgs a)
       // for mc_jobs_kernel, which subtracts what slivers drop
       const uint32_t incl = warp_incl_scan(upper);
       const uint32_t agg_up = __shfl_sync(kFull, incl, 31);
-      const uint64_t block =
-        reserve(&sm.chunk[warp][2], agg_up, kTriChunk, a.out + 9);
+      const uint64_t block = reserve(&sm.chunk[warp][2], agg_up, kTriChunk, a.out + 9,
+                                     a.tri_guard, a.ticket, a.stop_at);
       const uint32_t nc = __popc(cross);
       const uint32_t incl_c = warp_incl_scan(nc);
       const uint32_t total = __shfl_sync(kFull, incl_c, 31);
@@ -810,9 +849,11 @@ extract_kernel(const __grid_constant__ KArgs a)
       if (lane == 0) {
         a.tile_tri_cnt[tile] = agg_up;
         a.tile_tri_up[tile] = agg_up;
-        sm.acc[warp][7] += agg_up;  // slots reserved (sizes the next staging)
-        a.tile_tri_off[tile] = block;
-        if (total) jb = atomicAdd(a.out + 10, (unsigned long long)total);
+            a.tile_tri_off[tile] = block;
+        if (total) {
+          jb = atomicAdd(a.out + 10, (unsigned long long)total);
+          if (jb + total > a.job_guard) stop_round(a.ticket, a.stop_at);
+        }
       }
       jb = __shfl_sync(kFull, jb, 0);
       uint64_t at = block + (incl - upper), j = jb + (incl_c - nc);
@@ -851,7 +892,6 @@ extract_kernel(const __grid_constant__ KArgs a)
 #pragma unroll
     for (int i = 0; i < 7; i++)
       if (sm.acc[warp][i]) atomicAdd(a.out + i, sm.acc[warp][i]);
-    if (sm.acc[warp][7]) atomicAdd(a.out + 11, sm.acc[warp][7]);
     if (err) atomicOr(a.out + 7, (unsigned long long)err);
   }
 }
@@ -1026,6 +1066,36 @@ int occupancy_grid()
 
 }  // namespace
 
+namespace {
+
+/// grow a device buffer to `need` bytes keeping its first `keep` bytes
+void grow_keep(DevBuf &b, size_t need, size_t keep, cudaStream_t st)
+{
+  if (b.ptr && b.bytes >= need) return;
+  DevBuf n;
+  n.reserve(std::max(need, b.bytes + b.bytes / 2), st);
+  if (keep && b.ptr) AMRX_CUDA(cudaMemcpyAsync(n.ptr, b.ptr, keep, cudaMemcpyDeviceToDevice, st));
+  std::swap(b.ptr, n.ptr);
+  std::swap(b.bytes, n.bytes);
+  std::swap(b.stream, n.stream);
+}
+
+// staging caps per round (rounds make any size correct; these bound memory)
+constexpr uint64_t kStageBytes = uint64_t(16) << 30;
+constexpr uint64_t kJobCap = uint64_t(64) << 20;  // 4 GB of McJob
+
+}  // namespace
+
+std::atomic<uint64_t> g_round_limit{0};  // amrx_debug_round_limit
+
+/*! The extraction in rounds.  Every round runs the search
+    kernel over the next tiles in ticket order until a staging buffer is
+    nearly full (stop_round), marching cubes over the round's crossing
+    duals, then the exclusive scan of the round's tile counts and the
+    reorder of its tiles into candidate order after everything earlier --
+    the reference's pass 1 / prefix sum / pass 2 (pipeline.cpp:80-146) with
+    the search run once.  The staging sizes only decide how many rounds a
+    call takes, never the result, and nothing is ever run twice. */
 ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
 {
   ExtractScratch x;
@@ -1040,6 +1110,8 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
   else if (T && F) grid = occupancy_grid<false, true, true>();
   else if (T) grid = occupancy_grid<false, true, false>();
   else grid = occupancy_grid<false, false, false>();
+  grid = int(std::max<uint64_t>(1, std::min<uint64_t>(grid, (tiles + kWarps - 1) / kWarps)));
+  if (g_round_limit.load()) grid = 1;  // testing hook: few tiles in flight, many rounds
   const uint64_t warps = uint64_t(grid) * kWarps;
 
   // control block | tile tables (count u32 + staging offset u64 + final
@@ -1055,39 +1127,50 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
   uint64_t *tri_off = dual_off + (tiles + 1);
   uint64_t *final_off = tri_off + (tiles + 1);
   AMRX_CUDA(cudaMemsetAsync(ctl, 0, 256, st));
+  AMRX_CUDA(cudaMemsetAsync(ctl + 17, 0xff, 8, st));  // stop_at: none
   if (tiles) AMRX_CUDA(cudaMemsetAsync(tb, 0, size_t(tiles + 1) * 12, st));
 
-  // staging capacity: what the caller can take plus one chunk per warp of
-  // slack for partially used chunks (so a fitting result never overflows)
-  uint64_t dual_stage = D && r.corners ? r.dual_cap + warps * kDualChunk : 0;
-  // triangles are reserved at the case tables' upper bound (slivers drop
-  // some): size for the largest reserved/kept ratio seen so far (a rerun
-  // costs a whole extraction), at least 1/8 over the caller's capacity
-  static std::atomic<uint32_t> reserve_ratio_x1024{1024 + 128};
-  uint64_t tri_stage =
-    T && r.xyz ? r.tri_cap + r.tri_cap / 1024 * (reserve_ratio_x1024.load() - 1024) +
-                   warps * kTriChunk
-               : 0;
+  const bool grow = r.grow_a != nullptr;
+  const bool want_d = D && (r.corners || grow);
+  const bool want_t = T && (r.xyz || grow);
+  const uint64_t out_d_cap = grow ? ~0ull : r.dual_cap;
+  const uint64_t out_t_cap = grow ? ~0ull : r.tri_cap;
   const int tri_words = F ? 9 : 18;  // 32-bit words per triangle
+  // guard headroom (stop_round): the tiles in flight claim at most one
+  // chunk each; 3 chunks per warp
+  const uint64_t hd = 3 * warps * kDualChunk, ht = 3 * warps * kTriChunk, hj = 3 * warps * 256;
+  const uint64_t lim = g_round_limit.load() ? g_round_limit.load() : ~0ull;
+  const uint64_t dual_stage =
+    want_d ? hd + std::min<uint64_t>({out_d_cap, cells + cells / 4 + 1024, kStageBytes / 40, lim})
+           : 0;
+  const uint64_t tri_stage =
+    want_t ? ht + std::min<uint64_t>({out_t_cap / 8 * 9 + 1024, 3 * cells + 1024,
+                                      kStageBytes / uint64_t(tri_words * 4), lim})
+           : 0;
+  const uint64_t job_cap =
+    want_t ? hj + std::min<uint64_t>({cells / 4 + 1024, kJobCap, lim}) : 0;
+  if (dual_stage) {
+    x.stage_a.reserve(dual_stage * 32, st);
+    x.stage_b.reserve(dual_stage * 8, st);
+  }
+  if (tri_stage) x.stage_a.reserve(tri_stage * tri_words * 4, st);
+  if (job_cap) x.jobs.reserve(job_cap * sizeof(McJob), st);
 
   KArgs k;
   k.s = r.s;
   k.g = r.g;
-  k.lmap = r.lmap;
   k.unique = r.unique;
   k.above = nullptr;
   if (T) {
     const uint64_t words = (r.s.n + 31) / 32;
     x.bits.reserve(words * 4 + 64, st);
     k.above = x.bits.as<uint32_t>();
-    if (!r.bits_ready) {
-      const int bgrid =
-        int(std::min<uint64_t>((words + 7) / 8, uint64_t(device_sm_count()) * 16));
-      sign_bits_kernel<<<std::max(1, bgrid), 256, 0, st>>>(r.scal, r.s.n, r.iso,
-                                                           x.bits.as<uint32_t>());
-      AMRX_LAUNCH_CHECK();
-      res.launches += 1;
-    }
+    const int bgrid =
+      int(std::min<uint64_t>((words + 7) / 8, uint64_t(device_sm_count()) * 16));
+    sign_bits_kernel<<<std::max(1, bgrid), 256, 0, st>>>(r.scal, r.s.n, r.iso,
+                                                         x.bits.as<uint32_t>());
+    AMRX_LAUNCH_CHECK();
+    res.launches += 1;
   }
   k.scal = r.scal;
   k.cell_begin = r.cell_begin;
@@ -1103,108 +1186,193 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
   k.tile_dual_off = dual_off;
   k.tile_tri_cnt = tri_cnt;
   k.tile_tri_up = tri_up;
-  // marching-cubes jobs: sized by the largest jobs/cell ratio seen so far
-  // (an overflow reruns the extraction once, like the staging arenas)
-  // jobs per 1024 cells: this index's last extraction, else the last one of
-  // an index of the same size (a pipeline rebuilding the same dataset)
-  static std::mutex ratio_mu;
-  static std::unordered_map<uint64_t, uint32_t> ratio_by_size;
-  const uint64_t size_key = r.s.n * 1315423911ull ^ cells;
-  uint32_t jratio = r.jobs_per_kcell ? *r.jobs_per_kcell : 0;
-  if (!jratio) {
-    std::lock_guard<std::mutex> lock(ratio_mu);
-    const auto it = ratio_by_size.find(size_key);
-    jratio = it != ratio_by_size.end() ? it->second : 160;
-  }
-  uint64_t job_cap = T ? cells / 1024 * jratio + 4096 : 0;
-  k.job_cap = job_cap;
-  k.jobs = nullptr;
   k.tile_tri_off = tri_off;
+  k.jobs = job_cap ? x.jobs.as<McJob>() : nullptr;
+  k.job_cap = job_cap;
+  k.dual_guard = dual_stage - std::min(dual_stage, hd);
+  k.tri_guard = tri_stage - std::min(tri_stage, ht);
+  k.job_guard = job_cap - std::min(job_cap, hj);
   k.out = ctl;
-  k.ticket = reinterpret_cast<unsigned int *>(ctl + 16);
+  k.ticket = ctl + 16;
+  k.stop_at = ctl + 17;
   static const bool debug = std::getenv("AMRX_DEBUG_COUNTERS") != nullptr;
   k.s.dbg = debug ? ctl + 18 : nullptr;  // ctl holds 32 u64
+
+  McArgs m;
+  m.g = k.g;
+  m.scal = k.scal;
+  m.iso = k.iso;
+  m.jobs = k.jobs;
+  m.job_cap = k.job_cap;
+  m.xyz = k.xyz;
+  m.tri_cap = k.tri_cap;
+  m.tile_tri_cnt = k.tile_tri_cnt;
+  m.out = ctl;
+
+  // host output: each round is reordered into a device buffer and copied
+  // down on a side stream while the next round runs (two buffers)
+  cudaStream_t cp = nullptr;
+  cudaEvent_t copied[2] = {nullptr, nullptr};
+  WsBuf out_a(kWsOutA), out_b(kWsOutB), out_c(kWsScratch);
+  struct Cleanup {
+    cudaStream_t s;
+    cudaEvent_t *e;
+    ~Cleanup()
+    {
+      if (s) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+      }
+      for (int i = 0; i < 2; i++)
+        if (e[i]) cudaEventDestroy(e[i]);
+    }
+  } cleanup{nullptr, copied};
+  if (r.final_host && (want_d || want_t)) {
+    AMRX_CUDA(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
+    cleanup.s = cp;
+    for (int i = 0; i < 2; i++)
+      AMRX_CUDA(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
+  }
 
   cudaEvent_t e0, e1, e2;
   AMRX_CUDA(cudaEventCreate(&e0));
   AMRX_CUDA(cudaEventCreate(&e1));
   AMRX_CUDA(cudaEventCreate(&e2));
-  unsigned long long h[12];
-  for (int attempt = 0;; attempt++) {
-    if (dual_stage) {
-      x.stage_a.reserve(dual_stage * 32, st);
-      x.stage_b.reserve(dual_stage * 8, st);
+  unsigned long long h[18] = {}, prev[8] = {};
+  uint64_t t0 = 0, base_d = 0, base_t = 0;
+  const int rgrid_cap = device_sm_count() * 16;
+  for (int round = 0; t0 < tiles; round++) {
+    // the round's tile limit: host output starts with small rounds (1/64,
+    // then 1/32 of the tiles) so the first download starts early
+    uint64_t limit = tiles;
+    if (r.stream_rounds) {
+      const uint64_t first = tiles / 64, second = tiles * 3 / 64;
+      if (round == 0 && first > 0) limit = first;
+      else if (t0 < second) limit = second;
+      else limit = std::min(tiles, t0 + (tiles - second + 7) / 8);
+      limit = std::max(limit, t0 + 1);
     }
-    if (tri_stage) x.stage_a.reserve(tri_stage * tri_words * 4, st);
-    if (T) {
-      x.jobs.reserve(job_cap * sizeof(McJob), st);
-      k.jobs = x.jobs.as<McJob>();
-      k.job_cap = job_cap;
+    if (round) {  // fresh cursors, the ticket at the first open tile
+      const unsigned long long reset[10] = {0, 0, 0, 0, 0, 0, 0, 0, t0, ~0ull};
+      AMRX_CUDA(cudaMemcpyAsync(ctl + 8, reset, sizeof reset, cudaMemcpyHostToDevice, st));
     }
-    k.corners = dual_stage ? x.stage_a.as<uint32_t>() : nullptr;
-    k.tasks = dual_stage ? x.stage_b.as<uint64_t>() : nullptr;
-    k.dual_cap = dual_stage;
-    k.xyz = tri_stage ? x.stage_a.ptr : nullptr;
-    k.tri_cap = tri_stage;
-    if (attempt) AMRX_CUDA(cudaMemsetAsync(ctl, 0, 256, st));
+    k.tile_limit = limit;
     AMRX_CUDA(cudaEventRecord(e0, st));
-    if (tiles) {
-      if (D && T && F) launch_extract<true, true, true>(k, grid, st);
-      else if (D && T) launch_extract<true, true, false>(k, grid, st);
-      else if (D) launch_extract<true, false, false>(k, grid, st);
-      else if (T && F) launch_extract<false, true, true>(k, grid, st);
-      else if (T) launch_extract<false, true, false>(k, grid, st);
-      else launch_extract<false, false, false>(k, grid, st);
+    if (D && T && F) launch_extract<true, true, true>(k, grid, st);
+    else if (D && T) launch_extract<true, true, false>(k, grid, st);
+    else if (D) launch_extract<true, false, false>(k, grid, st);
+    else if (T && F) launch_extract<false, true, true>(k, grid, st);
+    else if (T) launch_extract<false, true, false>(k, grid, st);
+    else launch_extract<false, false, false>(k, grid, st);
+    res.launches += 1;
+    if (T && tri_stage) {
+      const int mgrid = device_sm_count() * 8;
+      if (F)
+        mc_jobs_kernel<true><<<mgrid, kMcThreads, 0, st>>>(m);
+      else
+        mc_jobs_kernel<false><<<mgrid, kMcThreads, 0, st>>>(m);
+      AMRX_LAUNCH_CHECK();
       res.launches += 1;
-      if (T && tri_stage) {
-        McArgs m;
-        m.g = k.g;
-        m.scal = k.scal;
-        m.iso = k.iso;
-        m.jobs = k.jobs;
-        m.job_cap = k.job_cap;
-        m.xyz = k.xyz;
-        m.tri_cap = k.tri_cap;
-        m.tile_tri_cnt = k.tile_tri_cnt;
-        m.out = ctl;
-        const int mgrid = device_sm_count() * 8;
-        if (F)
-          mc_jobs_kernel<true><<<mgrid, kMcThreads, 0, st>>>(m);
-        else
-          mc_jobs_kernel<false><<<mgrid, kMcThreads, 0, st>>>(m);
-        AMRX_LAUNCH_CHECK();
-        res.launches += 1;
-      }
     }
     AMRX_CUDA(cudaEventRecord(e1, st));
     AMRX_CUDA(cudaMemcpyAsync(h, ctl, sizeof h, cudaMemcpyDeviceToHost, st));
     AMRX_CUDA(cudaStreamSynchronize(st));
-    // the staging arena ran out although the result fits the caller's
-    // buffer (upper-bound reservations): grow it and run again
-    const bool dual_short = dual_stage && h[8] > dual_stage && h[4] <= r.dual_cap;
-    const bool tri_short = tri_stage && h[9] > tri_stage && h[6] <= r.tri_cap;
-    const bool job_short = T && tri_stage && h[10] > job_cap;
-    if (job_short) job_cap = h[10] + 4096;
-    if (T && tri_stage && cells) {
-      const uint32_t learned = uint32_t(std::min<uint64_t>(h[10] * 1024 / cells + 16, 8192));
-      if (r.jobs_per_kcell) *r.jobs_per_kcell = learned;
-      std::lock_guard<std::mutex> lock(ratio_mu);
-      if (ratio_by_size.size() > 4096) ratio_by_size.clear();
-      ratio_by_size[size_key] = learned;
-    }
-    if (attempt || (!dual_short && !tri_short && !job_short)) break;
-    if (dual_short) dual_stage = h[8] + warps * kDualChunk;
-    if (tri_short) {
-      tri_stage = h[9] + warps * kTriChunk;
-      // reserved slots per kept triangle (the chunk cursor h[9] also counts
-      // each warp's partly used chunks, which the slack term covers)
-      const uint64_t ratio =
-        std::min<uint64_t>(h[6] ? h[11] * 1024 / h[6] + 32 : 1024 + 128, 4096);
-      uint32_t cur = reserve_ratio_x1024.load();
-      while (ratio > cur && !reserve_ratio_x1024.compare_exchange_weak(cur, uint32_t(ratio))) {
+    float ms = 0;
+    AMRX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    res.ms += ms;
+    const uint64_t stop = h[16] >= kStopTicket ? h[17] : h[16];
+    const uint64_t t1 = std::min({limit, tiles, uint64_t(stop)});
+    if (t1 <= t0 || h[8] > dual_stage || h[9] > tri_stage || h[10] > job_cap)
+      throw std::runtime_error("extract: round " + std::to_string(round) +
+                               " overran its staging or made no progress");
+    const uint32_t nt = uint32_t(t1 - t0);
+    const int rgrid = int(std::min<uint64_t>((nt + 7) / 8, uint64_t(rgrid_cap)));
+    const uint64_t round_d = h[4] - prev[4], round_t = h[6] - prev[6];
+    const int slot = round & 1;
+    AMRX_CUDA(cudaEventRecord(e1, st));
+    if (want_d && round_d) {
+      res.launches += scan_exclusive_u32_u64(dual_cnt + t0, final_off + t0, nt, x.scan, st);
+      uint32_t *dc = r.corners;
+      uint64_t *dt = r.tasks;
+      uint64_t dbase = base_d, dcap = r.dual_cap;
+      if (grow) {
+        grow_keep(*r.grow_a, (base_d + round_d) * 32, base_d * 32, st);
+        grow_keep(*r.grow_b, (base_d + round_d) * 8, base_d * 8, st);
+        dc = r.grow_a->as<uint32_t>();
+        dt = r.grow_b->as<uint64_t>();
+        dcap = ~0ull;
+      } else if (r.final_host) {
+        // this round's part into a device buffer (the copy that last used
+        // it has drained), then down to host memory at its offset
+        if (round >= 2) AMRX_CUDA(cudaStreamWaitEvent(st, copied[slot], 0));
+        WsBuf &bc = slot ? out_b : out_a;
+        bc.reserve(round_d * 32 + 16, st);
+        dc = bc.as<uint32_t>();
+        dt = nullptr;
+        if (r.tasks) {
+          out_c.reserve(round_d * 8 + 16, st);
+          dt = out_c.as<uint64_t>();
+        }
+        dbase = 0;
+        dcap = base_d < r.dual_cap ? std::min(round_d, r.dual_cap - base_d) : 0;
+      }
+      reorder_kernel<<<std::max(1, rgrid), 256, 0, st>>>(
+        dual_cnt + t0, dual_off + t0, final_off + t0, nt, 8, x.stage_a.as<uint32_t>(), dc,
+        dbase, dcap, dt ? 2 : 0, x.stage_b.as<uint32_t>(), reinterpret_cast<uint32_t *>(dt));
+      AMRX_LAUNCH_CHECK();
+      res.launches += 1;
+      if (r.final_host && !grow && dcap) {
+        AMRX_CUDA(cudaMemcpyAsync(r.corners + base_d * 8, dc, dcap * 32, cudaMemcpyDeviceToHost,
+                                  st));
+        if (r.tasks)  // (the tasks buffer is not double-buffered: copied in order)
+          AMRX_CUDA(cudaMemcpyAsync(r.tasks + base_d, dt, dcap * 8, cudaMemcpyDeviceToHost, st));
       }
     }
+    if (want_t && round_t) {
+      res.launches += scan_exclusive_u32_u64(tri_cnt + t0, final_off + t0, nt, x.scan, st);
+      uint32_t *dx = static_cast<uint32_t *>(r.xyz);
+      uint64_t tbase = base_t, tcap = r.tri_cap;
+      if (grow) {
+        grow_keep(*r.grow_a, (base_t + round_t) * tri_words * 4, base_t * tri_words * 4, st);
+        dx = r.grow_a->as<uint32_t>();
+        tcap = ~0ull;
+      } else if (r.final_host) {
+        if (round >= 2) AMRX_CUDA(cudaStreamWaitEvent(st, copied[slot], 0));
+        WsBuf &bx = slot ? out_b : out_a;
+        bx.reserve(round_t * tri_words * 4 + 16, st);
+        dx = bx.as<uint32_t>();
+        tbase = 0;
+        tcap = base_t < r.tri_cap ? std::min(round_t, r.tri_cap - base_t) : 0;
+      }
+      reorder_tri_kernel<<<std::max(1, rgrid), 256, 0, st>>>(
+        tri_cnt + t0, tri_up + t0, tri_off + t0, final_off + t0, nt, tri_words,
+        x.stage_a.as<uint32_t>(), dx, tbase, tcap);
+      AMRX_LAUNCH_CHECK();
+      res.launches += 1;
+      if (r.final_host && !grow && tcap) {
+        // overlapped: the copy drains on its own stream during the next round
+        cudaEvent_t ready;
+        AMRX_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+        AMRX_CUDA(cudaEventRecord(ready, st));
+        AMRX_CUDA(cudaStreamWaitEvent(cp, ready, 0));
+        AMRX_CUDA(cudaMemcpyAsync(static_cast<char *>(r.xyz) + base_t * tri_words * 4, dx,
+                                  tcap * tri_words * 4, cudaMemcpyDeviceToHost, cp));
+        AMRX_CUDA(cudaEventRecord(copied[slot], cp));
+        cudaEventDestroy(ready);
+      }
+    }
+    AMRX_CUDA(cudaEventRecord(e2, st));
+    AMRX_CUDA(cudaEventSynchronize(e2));
+    AMRX_CUDA(cudaEventElapsedTime(&ms, e1, e2));
+    res.ms2 += ms;
+    base_d += round_d;
+    base_t += round_t;
+    for (int i = 0; i < 8; i++) prev[i] = h[i];
+    t0 = t1;
+    res.rounds += 1;
   }
+  if (cp) AMRX_CUDA(cudaStreamSynchronize(cp));
+  AMRX_CUDA(cudaStreamSynchronize(st));
   for (int i = 0; i < 4; i++) res.counters[i] = h[i];
   res.duals = h[4];
   res.tris_counted = h[5];
@@ -1222,81 +1390,6 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
                    d[0] ? double(d[i]) / double(d[0]) : 0.0);
     std::fprintf(stderr, "\n");
   }
-
-  // pass 2 of the reference's scheme: exclusive scan of the tile counts
-  // gives every tile its final offset; blocks move into candidate order
-  // A pinned host destination is filled by one bulk copy from a device
-  // buffer (full host-link bandwidth) rather than by the reorder kernel's
-  // scattered stores across the link.
-  const int rgrid = int(std::min<uint64_t>((tiles + 7) / 8, uint64_t(device_sm_count()) * 16));
-  WsBuf host_a(kWsOutA), host_b(kWsOutB);
-  // a result larger than the caller's capacity is not moved: the caller
-  // reports the count (capacity error) or retries with room for it, and
-  // tiles past the staging capacity were never written
-  if (tiles && dual_stage && res.duals > 0 && res.duals <= r.dual_cap) {
-    res.launches += scan_exclusive_u32_u64(dual_cnt, final_off, tiles, x.scan, st);
-    const uint64_t keep = std::min(res.duals, r.dual_cap);
-    uint32_t *dc = r.corners;
-    uint64_t *dt = r.tasks;
-    if (r.final_host) {
-      host_a.reserve(keep * 32 + 16, st);
-      dc = host_a.as<uint32_t>();
-      if (r.tasks) {
-        host_b.reserve(keep * 8 + 16, st);
-        dt = host_b.as<uint64_t>();
-      }
-    }
-    reorder_kernel<<<std::max(1, rgrid), 256, 0, st>>>(
-      dual_cnt, dual_off, final_off, uint32_t(tiles), 8, x.stage_a.as<uint32_t>(),
-      dc, r.dual_cap, r.tasks ? 2 : 0, x.stage_b.as<uint32_t>(),
-      reinterpret_cast<uint32_t *>(dt));
-    AMRX_LAUNCH_CHECK();
-    res.launches += 1;
-    if (r.final_host) {
-      AMRX_CUDA(cudaMemcpyAsync(r.corners, dc, keep * 32, cudaMemcpyDeviceToHost, st));
-      if (r.tasks)
-        AMRX_CUDA(cudaMemcpyAsync(r.tasks, dt, keep * 8, cudaMemcpyDeviceToHost, st));
-    }
-  }
-  if (tiles && tri_stage && res.tris_written > 0 && res.tris_written <= r.tri_cap) {
-    res.launches += scan_exclusive_u32_u64(tri_cnt, final_off, tiles, x.scan, st);
-    const uint64_t keep = std::min(res.tris_written, r.tri_cap);
-    uint32_t *dx = static_cast<uint32_t *>(r.xyz);
-    WsBuf chunk_buf(r.out_slot >= 0 ? r.out_slot : kWsOutA);
-    if (r.final_host) {
-      WsBuf &hb = r.out_slot >= 0 ? chunk_buf : host_a;
-      hb.reserve(keep * tri_words * 4 + 16, st);
-      dx = hb.as<uint32_t>();
-      // the previous copy out of this buffer must have drained
-      if (r.slot_free) AMRX_CUDA(cudaStreamWaitEvent(st, r.slot_free, 0));
-    }
-    reorder_tri_kernel<<<std::max(1, rgrid), 256, 0, st>>>(
-      tri_cnt, tri_up, tri_off, final_off, uint32_t(tiles), tri_words,
-      x.stage_a.as<uint32_t>(), dx, r.tri_cap);
-    AMRX_LAUNCH_CHECK();
-    res.launches += 1;
-    if (r.final_host) {
-      if (r.copy_stream) {
-        // overlapped: the copy drains on its own stream while the caller
-        // extracts the next chunk
-        cudaEvent_t ready;
-        AMRX_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-        AMRX_CUDA(cudaEventRecord(ready, st));
-        AMRX_CUDA(cudaStreamWaitEvent(r.copy_stream, ready, 0));
-        AMRX_CUDA(cudaMemcpyAsync(r.xyz, dx, keep * tri_words * 4,
-                                  cudaMemcpyDeviceToHost, r.copy_stream));
-        if (r.copy_done) AMRX_CUDA(cudaEventRecord(r.copy_done, r.copy_stream));
-        cudaEventDestroy(ready);
-      } else {
-        AMRX_CUDA(cudaMemcpyAsync(r.xyz, dx, keep * tri_words * 4,
-                                  cudaMemcpyDeviceToHost, st));
-      }
-    }
-  }
-  AMRX_CUDA(cudaEventRecord(e2, st));
-  AMRX_CUDA(cudaStreamSynchronize(st));
-  AMRX_CUDA(cudaEventElapsedTime(&res.ms, e0, e1));
-  AMRX_CUDA(cudaEventElapsedTime(&res.ms2, e1, e2));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaEventDestroy(e2);

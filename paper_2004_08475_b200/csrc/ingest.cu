@@ -268,40 +268,6 @@ bucket_count_kernel(const uint64_t *__restrict__ keys, uint64_t n, int shift,
   }
 }
 
-/*! block level map: OR the cell's level bit into the byte of its
-    coarsest-aligned block; sorted neighbours share blocks, so a warp issues
-    one atomic per distinct (word, bits) it holds */
-__global__ void __launch_bounds__(kThreads)
-level_map_kernel(const uint64_t *__restrict__ keys, uint64_t n, const KeyGeom g,
-                 uint32_t *__restrict__ words)
-{
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  const uint64_t start = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  for (uint64_t base = start - (threadIdx.x & 31); base < n; base += stride) {
-    const uint64_t r = base + (threadIdx.x & 31);
-    const bool in = r < n;
-    uint64_t idx = ~0ull;
-    uint32_t bits = 0;
-    if (in) {
-      const Cell c = unpack(g, ldg_u64(keys + r));
-      const int b = __popc(g.level_mask & ((1u << c.level) - 1));
-      const uint64_t bx = uint64_t((c.i >> g.map_shift) - g.map_base[0]);
-      const uint64_t by = uint64_t((c.j >> g.map_shift) - g.map_base[1]);
-      const uint64_t bz = uint64_t((c.k >> g.map_shift) - g.map_base[2]);
-      idx = (bz * uint64_t(g.map_dim[1]) + by) * uint64_t(g.map_dim[0]) + bx;
-      bits = (1u << b) << (8 * (idx & 3));
-    }
-    const uint64_t word = idx >> 2;
-    const uint32_t peers = __match_any_sync(kFull, word);
-    // OR of the peers' bits, then one atomic by the first peer
-    uint32_t acc = 0;
-    for (uint32_t m = peers; m; m &= m - 1)
-      acc |= __shfl_sync(peers, bits, __ffs(m) - 1);
-    if (in && (__ffs(peers) - 1) == int(threadIdx.x & 31))
-      atomicOr(words + word, acc);
-  }
-}
-
 __global__ void __launch_bounds__(kThreads)
 unpack_kernel(const uint64_t *__restrict__ keys, uint64_t n, const KeyGeom g,
               int4 *__restrict__ cells)
@@ -546,6 +512,97 @@ rec_build_kernel(const uint64_t *__restrict__ keys, uint64_t n, int dir_shift,
   }
 }
 
+// ------------------------------------------- hashed occupancy records
+// For key spaces too sparse for a record per bucket (deep hierarchies, wide
+// extents): one 16-byte slot per OCCUPIED bucket in an open-addressed table
+// (common.cuh, hash_home).  Two passes over the sorted keys: count the
+// distinct buckets (fused with the order check), then insert one slot per
+// bucket, its bits ORed by the lanes holding the bucket's keys.
+
+/// acc[0] += distinct buckets, acc[1] += descents, acc[2] += equal pairs
+__global__ void __launch_bounds__(kThreads)
+hash_count_kernel(const uint64_t *__restrict__ keys, uint64_t n, int dir_shift,
+                  unsigned long long *acc)
+{
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  unsigned long long nb = 0, desc = 0, eq = 0;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t k = ldg_u64(keys + i);
+    nb += i == 0 || (ldg_u64(keys + i - 1) >> dir_shift) != (k >> dir_shift);
+    if (i + 1 < n) {
+      const uint64_t k1 = ldg_u64(keys + i + 1);
+      desc += k > k1;
+      eq += k == k1;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    nb += __shfl_xor_sync(kFull, nb, off);
+    desc += __shfl_xor_sync(kFull, desc, off);
+    eq += __shfl_xor_sync(kFull, eq, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (nb) atomicAdd(acc, nb);
+    if (desc) atomicAdd(acc + 1, desc);
+    if (eq) atomicAdd(acc + 2, eq);
+  }
+}
+
+/// one slot per distinct bucket (unique keys: a bucket holds <= 32 keys);
+/// the first key of a bucket inserts it with the OR of its keys' bits
+__global__ void __launch_bounds__(kThreads)
+hash_build_kernel(const uint64_t *__restrict__ keys, uint64_t n, int dir_shift,
+                  uint4 *__restrict__ tab, uint64_t mask, unsigned int *max_probe)
+{
+  const int lane = threadIdx.x & 31;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  unsigned int longest = 0;
+  for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); base < n;
+       base += stride) {
+    const uint64_t i = base + lane;
+    const bool in = i < n;
+    const uint64_t k = in ? ldg_u64(keys + i) : 0;
+    const uint64_t b = in ? k >> dir_shift : ~0ull;
+    uint64_t pb = __shfl_up_sync(kFull, b, 1);
+    if (lane == 0) pb = (in && i > 0) ? ldg_u64(keys + i - 1) >> dir_shift : ~0ull;
+    uint32_t v = in ? 1u << (uint32_t(k) & 31u) : 0u;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {  // segmented OR toward the run's first lane
+      const uint32_t y = __shfl_down_sync(kFull, v, off);
+      const uint64_t bo = __shfl_down_sync(kFull, b, off);
+      if (lane + off < 32 && bo == b) v |= y;
+    }
+    const uint64_t b31 = __shfl_sync(kFull, b, 31);
+    if (in && (i == 0 || pb != b)) {
+      if (b31 == b)  // the bucket continues past this warp's 32 keys
+        for (uint64_t j = base + 32; j < n; j++) {
+          const uint64_t kj = ldg_u64(keys + j);
+          if ((kj >> dir_shift) != b) break;
+          v |= 1u << (uint32_t(kj) & 31u);
+        }
+      uint64_t h = hash_home(b, mask);
+      unsigned int probe = 0;
+      while (atomicCAS(reinterpret_cast<unsigned long long *>(tab + h), 0ull,
+                       (unsigned long long)(b + 1)) != 0ull) {
+        h = (h + 1) & mask;
+        probe++;
+      }
+      reinterpret_cast<uint2 *>(tab + h)[1] = make_uint2(uint32_t(i), v);
+      longest = probe > longest ? probe : longest;
+    }
+  }
+  longest = __reduce_max_sync(kFull, longest);
+  if (lane == 0 && longest) atomicMax(max_probe, longest);
+}
+
+/// out[t] = lower_bound of q[t] in the sorted keys (one thread per query)
+__global__ void lower_bound_kernel(const uint64_t *__restrict__ keys, uint64_t n,
+                                   const uint64_t *__restrict__ q, int nq, uint64_t *out)
+{
+  const int t = threadIdx.x;
+  if (t < nq) out[t] = global_lower_bound(keys, 0, n, q[t]);
+}
+
 /// recursive reduce-then-scan; block sums of each level in a pool buffer
 template <typename T, typename A>
 int scan_exclusive(const T *in, A *out, uint64_t n, cudaStream_t st)
@@ -722,13 +779,44 @@ void build_directory(const uint64_t *keys, uint64_t n, const KeyGeom &g,
   scan_exclusive_u32(dir, dir, entries, scratch, st);
 }
 
-void build_level_map(const uint64_t *keys, uint64_t n, const KeyGeom &g,
-                     uint8_t *map, uint64_t map_bytes, cudaStream_t st)
+uint64_t hash_count(const uint64_t *keys, uint64_t n, const KeyGeom &g,
+                    unsigned long long *order2, DevBuf &scratch, cudaStream_t st)
 {
-  AMRX_CUDA(cudaMemsetAsync(map, 0, map_bytes, st));
-  level_map_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(
-    keys, n, g, reinterpret_cast<uint32_t *>(map));
+  scratch.reserve(32, st);
+  auto *acc = scratch.as<unsigned long long>();
+  AMRX_CUDA(cudaMemsetAsync(acc, 0, 24, st));
+  hash_count_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(keys, n, g.dir_shift, acc);
   AMRX_LAUNCH_CHECK();
+  unsigned long long h[3];
+  AMRX_CUDA(cudaMemcpyAsync(h, acc, sizeof h, cudaMemcpyDeviceToHost, st));
+  AMRX_CUDA(cudaStreamSynchronize(st));
+  const unsigned long long o2[2] = {h[1], h[2]};
+  AMRX_CUDA(cudaMemcpyAsync(order2, o2, 16, cudaMemcpyHostToDevice, st));
+  AMRX_CUDA(cudaStreamSynchronize(st));
+  return h[0];
+}
+
+void build_hash(const uint64_t *keys, uint64_t n, const KeyGeom &g, uint4 *tab, uint64_t slots,
+                unsigned int *max_probe, cudaStream_t st)
+{
+  AMRX_CUDA(cudaMemsetAsync(tab, 0, slots * sizeof(uint4), st));
+  AMRX_CUDA(cudaMemsetAsync(max_probe, 0, sizeof(unsigned int), st));
+  hash_build_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(keys, n, g.dir_shift, tab,
+                                                                   slots - 1, max_probe);
+  AMRX_LAUNCH_CHECK();
+}
+
+void lower_bounds(const uint64_t *keys, uint64_t n, const uint64_t *q, int nq, uint64_t *out,
+                  cudaStream_t st)
+{
+  DevBuf buf;
+  buf.reserve(size_t(2 * nq) * 8, st);
+  AMRX_CUDA(cudaMemcpyAsync(buf.ptr, q, size_t(nq) * 8, cudaMemcpyHostToDevice, st));
+  lower_bound_kernel<<<1, 32, 0, st>>>(keys, n, buf.as<uint64_t>(), nq, buf.as<uint64_t>() + nq);
+  AMRX_LAUNCH_CHECK();
+  AMRX_CUDA(cudaMemcpyAsync(out, buf.as<uint64_t>() + nq, size_t(nq) * 8, cudaMemcpyDeviceToHost,
+                            st));
+  AMRX_CUDA(cudaStreamSynchronize(st));
 }
 
 void unpack_cells(const uint64_t *keys, uint64_t n, const KeyGeom &g,

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <atomic>
 #include <string>
 #include <cuda_runtime.h>
 
@@ -159,9 +160,18 @@ void build_directory(const uint64_t *keys, uint64_t n, const KeyGeom &g,
                      DevBuf &scratch, cudaStream_t st, uint64_t rec_lo = 0,
                      uint64_t rec_n = 0);
 
-/// block level map (KeyGeom::map_*): fill map (map bytes, zeroed here)
-void build_level_map(const uint64_t *keys, uint64_t n, const KeyGeom &g,
-                     uint8_t *map, uint64_t map_bytes, cudaStream_t st);
+/// hashed records: distinct buckets of the sorted keys (synchronises);
+/// order2 (device, 2 x u64) receives the keys' descents and equal pairs
+uint64_t hash_count(const uint64_t *keys, uint64_t n, const KeyGeom &g,
+                    unsigned long long *order2, DevBuf &scratch, cudaStream_t st);
+/// fill the table of `slots` (a power of two >= 2 x buckets) 16-byte
+/// slots; *max_probe (device) = the longest displacement from a home slot
+void build_hash(const uint64_t *keys, uint64_t n, const KeyGeom &g, uint4 *tab, uint64_t slots,
+                unsigned int *max_probe, cudaStream_t st);
+
+/// lower_bound of nq host keys q in the sorted device keys -> host out (synchronises)
+void lower_bounds(const uint64_t *keys, uint64_t n, const uint64_t *q, int nq, uint64_t *out,
+                  cudaStream_t st);
 
 /// unpack sorted keys into 4 x int32 cells
 void unpack_cells(const uint64_t *keys, uint64_t n, const KeyGeom &g,
@@ -210,30 +220,28 @@ size_t radix_sort_scratch_bytes(uint64_t n);
 struct ExtractRequest {
   SearchCtx s;
   KeyGeom g;
-  const uint8_t *lmap;
   const double *scal;
   uint64_t cell_begin, cell_end;
   bool emit_dual;
   bool emit_tri;
   bool tri_f32;
   double iso;
+  // outputs: device memory, or pinned host memory (final_host) filled by
+  // one bulk copy per round; at most dual_cap / tri_cap items are written
   uint32_t *corners;    // [dual_cap][8] or null
   uint64_t *tasks;      // [dual_cap] or null
   uint64_t dual_cap;
   void *xyz;            // [tri_cap][9] f64/f32 or null
   uint64_t tri_cap;
-  bool final_host;      // corners/tasks/xyz are pinned host memory
+  bool final_host;
   bool unique;          // the index holds no duplicate keys
-  // chunked host output (iso): D2H on copy_stream from workspace slot
-  // out_slot, after slot_free (if set); copy_done recorded after the copy
-  cudaStream_t copy_stream = nullptr;
-  int out_slot = -1;
-  cudaEvent_t slot_free = nullptr;
-  cudaEvent_t copy_done = nullptr;
-  bool bits_ready = false;  // the sign bits in the workspace are for this iso
-  // marching-cubes jobs per 1024 cells seen by this index's last extraction
-  // (sizes the job buffer; an overflow reruns once and updates it)
-  uint32_t *jobs_per_kcell = nullptr;
+  // growable device outputs (an index's cached arena): when set, the
+  // pointers above are ignored and these grow to hold the whole result
+  DevBuf *grow_a = nullptr;  // corners (dual) or xyz (iso)
+  DevBuf *grow_b = nullptr;  // tasks (dual)
+  // host output: small first rounds (1/64, 1/32 of the tiles) so the
+  // first download overlaps the rest of the extraction
+  bool stream_rounds = false;
 };
 
 struct ExtractResult {
@@ -242,12 +250,16 @@ struct ExtractResult {
   uint64_t tris_counted; // count phase
   uint64_t tris_written; // emit phase
   uint32_t error_flags;  // bit0 collapsed edge, bit1 undecided candidate
-  float ms;              // device time of the extraction kernel
+  float ms;              // device time of the extraction kernels (all rounds)
   float ms2;             // device time of scan + reorder into final order
   uint64_t launches;
+  uint32_t rounds;       // staging rounds the call took
 };
 
 ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st);
+
+/// amrx_debug_round_limit: cap on every round's staging items (0 = default)
+extern std::atomic<uint64_t> g_round_limit;
 
 void run_find_exact(const SearchCtx &s, const KeyGeom &g, const int4 *cells,
                     uint64_t n, int64_t *out, cudaStream_t st);

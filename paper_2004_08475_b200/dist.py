@@ -99,9 +99,13 @@ def geometry_layout(geometry):
 def choose_splitters(samples, world):
     """world-1 strictly increasing key boundaries from the sorted union of
     every rank's evenly spaced samples; rank q owns keys [s_q, s_q+1) with
-    s_0 = 0 and s_world = 2^63"""
+    s_0 = 0 and s_world = 2^63.  Negative samples (an empty slice's
+    placeholders) are ignored, so empty slices do not pull splitters down."""
     import torch
-    smp = torch.sort(samples.reshape(-1)).values
+    smp = samples.reshape(-1)
+    smp = torch.sort(smp[smp >= 0]).values
+    if len(smp) == 0:
+        smp = torch.zeros(1, dtype=samples.dtype, device=samples.device)
     cut = [smp[(len(smp) * q) // world] for q in range(1, world)]
     out = [0]
     for c in cut:
@@ -248,7 +252,7 @@ def build_distributed(cells, scalars, group=None, device=None, stream=None, samp
     t2 = time.perf_counter()
     # splitters from evenly spaced samples of every rank's sorted slice
     pos = torch.linspace(0, max(n_loc - 1, 0), samples, device=dev).round().long()
-    smp = keys[pos] if n_loc else torch.zeros(samples, dtype=torch.int64, device=dev)
+    smp = keys[pos] if n_loc else torch.full((samples,), -1, dtype=torch.int64, device=dev)
     gathered = [torch.empty_like(smp) for _ in range(world)]
     dist.all_gather(gathered, smp, group=group)
     bounds = choose_splitters(torch.cat(gathered), world)
@@ -288,6 +292,9 @@ def extract_dual_mesh_distributed(dindex, group=None, device=None):
     from . import amrx as P
 
     def run(lo, hi):
+        if dindex.index is None or hi <= lo:
+            e = np.zeros((0, 8), np.uint32)
+            return P.DualMesh(e, np.zeros(0, np.uint64), P.ExtractionStats()), P.ExtractionStats()
         d = P.extract_dual_mesh(dindex.index, cell_range=(lo, hi))
         return d, d.stats
 

@@ -183,6 +183,80 @@ def octree_noise(root=(48, 48, 48), levels=6, seed=3, k=0.45, base=0.02, shuffle
     return cells, scal
 
 
+def landing_gear_sdf(c, scale):
+    """signed distance (finest units, FP64) to a landing-gear-like body: a
+    main strut, a side brace, an axle and two wheels (tori) -- the shape
+    class of the paper's 13-level NASA landing gear.
+    ``scale`` = the domain's finest-unit extent along y."""
+    import torch
+    S = float(scale)
+    x, y, z = c[:, 0], c[:, 1], c[:, 2]
+
+    def capsule(ax, ay, az, bx, by, bz, r):
+        px, py, pz = x - ax, y - ay, z - az
+        dx, dy, dz = bx - ax, by - ay, bz - az
+        h = ((px * dx + py * dy + pz * dz) / (dx * dx + dy * dy + dz * dz)).clamp(0.0, 1.0)
+        return torch.sqrt((px - h * dx) ** 2 + (py - h * dy) ** 2 + (pz - h * dz) ** 2) - r
+
+    def torus_y(cx, cy, cz, R, r):  # axis along y
+        q = torch.sqrt((x - cx) ** 2 + (z - cz) ** 2) - R
+        return torch.sqrt(q * q + (y - cy) ** 2) - r
+
+    cx, cy = 0.5 * S, 0.5 * S
+    d = capsule(cx, cy, 0.62 * S, cx, cy, 0.30 * S, 0.035 * S)           # strut
+    d = torch.minimum(d, capsule(cx, cy, 0.55 * S, cx + 0.16 * S, cy, 0.78 * S, 0.018 * S))
+    d = torch.minimum(d, capsule(cx, cy - 0.17 * S, 0.30 * S, cx, cy + 0.17 * S, 0.30 * S,
+                                 0.022 * S))                             # axle
+    for sy in (-0.15, 0.15):                                             # wheels
+        d = torch.minimum(d, torus_y(cx, cy + sy * S, 0.30 * S, 0.10 * S, 0.045 * S))
+    return d
+
+
+def octree_sdf(root=(3, 2, 2), levels=13, k=0.9, seed=13, shuffle=True, device="cuda",
+               noise=0.0):
+    """DEEP config: an octree of `levels` levels (0..levels-1) over a root
+    grid of coarsest cells, refined toward a landing-gear surface
+    (landing_gear_sdf) -- a cell is split while its centre lies within k
+    cell widths of the surface -- with the signed distance (plus optional
+    value noise) at the cell centre as the scalar, iso 0.  Built with torch
+    on the GPU; optionally shuffled into a soup.  Returns (cells int32[n,4],
+    scalars f64[n]) on `device`."""
+    import torch
+    L = levels - 1
+    W = 1 << L
+    scale = root[1] * W
+    r = [torch.arange(n, device=device, dtype=torch.int64) * W for n in root]
+    cur = torch.stack(torch.meshgrid(*r, indexing="ij"), -1).reshape(-1, 3)
+    off = torch.tensor([[(d >> 0) & 1, (d >> 1) & 1, (d >> 2) & 1] for d in range(8)],
+                       device=device, dtype=torch.int64)
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    ph = (torch.rand(3, generator=g, dtype=torch.float64) * 6.283185307179586).tolist()
+    cells, scal = [], []
+    while True:
+        w = 1 << L
+        ctr = cur.to(torch.float64) + 0.5 * w
+        f = landing_gear_sdf(ctr, scale)
+        if noise:
+            f = f + noise * torch.sin(ctr[:, 0] * 0.013 + ph[0]) * \
+                torch.sin(ctr[:, 1] * 0.011 + ph[1]) * torch.sin(ctr[:, 2] * 0.017 + ph[2])
+        refine = (f.abs() < k * w) if L > 0 else torch.zeros_like(f, dtype=torch.bool)
+        keep = ~refine
+        cells.append(torch.cat([cur[keep], torch.full((int(keep.sum()), 1), L, device=device,
+                                                      dtype=torch.int64)], 1).to(torch.int32))
+        scal.append(f[keep])
+        if L == 0 or not bool(refine.any()):
+            break
+        cur = (cur[refine][:, None, :] + off[None] * (w // 2)).reshape(-1, 3)
+        L -= 1
+    cells = torch.cat(cells)
+    scal = torch.cat(scal)
+    if shuffle:
+        gp = torch.Generator(device=device).manual_seed(seed)
+        perm = torch.randperm(len(cells), device=device, generator=gp)
+        cells, scal = cells[perm].contiguous(), scal[perm].contiguous()
+    return cells, scal
+
+
 CONFIGS = {
     # C1: SURVEY §8(d): gen_octree(6, sphere((25,27.5,30), 20), 3.2), iso 0
     "c1": dict(kind="octree_sphere", args=(6, (25.0, 27.5, 30.0), 20.0, 3.2), iso=0.0),
@@ -196,4 +270,8 @@ CONFIGS = {
     # C5: ~250M-cell mixed-level AMR, dual mesh only
     "c5": dict(kind="bricks", bricks=(384, 192, 192), seed=5, shuffle=False, iso=None,
                dual_only=True),
+    # DEEP: a 13-level octree (levels 0..12) refined toward a landing-gear
+    # surface (the paper's 13-level NASA landing gear shape class), soup
+    # order, iso 0 on the signed distance -- a sparse 47-bit key space
+    "deep": dict(kind="octree_sdf", args=((3, 2, 2), 13, 0.9), iso=0.0),
 }

@@ -15,7 +15,7 @@ LIB = os.path.join(ROOT, "paper_2004_08475_b200", "libamrx.so")
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*AMRX_API\s+(?:amrx_status|const char \*|uint64_t)\s*(amrx_\w+)\(", text,
+    return sorted(set(re.findall(r"^\s*AMRX_API\s+(?:amrx_status|const char \*|uint64_t|void)\s*(amrx_\w+)\(", text,
                                  re.MULTILINE)))
 
 

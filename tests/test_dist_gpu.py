@@ -25,7 +25,7 @@ def env():
     return P, D, torch
 
 
-def emulate(P, D, torch, cells, scal, world, samples=64):
+def emulate(P, D, torch, cells, scal, world, samples=64, lookup=None):
     dev = torch.device("cuda", 0)
     n = len(cells)
     cut = [n * r // world for r in range(world + 1)]
@@ -59,16 +59,19 @@ def emulate(P, D, torch, cells, scal, world, samples=64):
         below, own = split[r]
         g2 = gg.copy()
         g2[12], g2[13], g2[14] = sum(owns[:r]) - below, lo[r], hi[r]
-        idx = P.index_from_keys(rk.data_ptr(), rs.data_ptr(), len(rk), g2) if own else None
+        idx = P.index_from_keys(rk.data_ptr(), rs.data_ptr(), len(rk), g2,
+                                lookup=lookup) if own else None
+        if idx is not None and lookup:
+            assert idx.info.lookup == lookup
         parts.append((idx, (below, below + own)))
     return parts
 
 
-def check(P, D, torch, cells, scal, iso, world):
+def check(P, D, torch, cells, scal, iso, world, lookup=None):
     ref = P.build_index(cells, scal)
     d_ref = P.extract_dual_mesh(ref)
     r_ref = P.extract_isosurface(ref, P.IsoParams(iso=iso))
-    parts = emulate(P, D, torch, cells, scal, world)
+    parts = emulate(P, D, torch, cells, scal, world, lookup=lookup)
     corners, tasks, fats, counters = [], [], [], np.zeros(4, np.int64)
     for idx, (lo, hi) in parts:
         if idx is None:
@@ -101,12 +104,42 @@ def _cases():
 CASES = _cases()
 
 
+@pytest.mark.parametrize("lookup", [None, "hash"])
 @pytest.mark.parametrize("world", [2, 3, 5])
 @pytest.mark.parametrize("name", ["slots_l4_s3", "octree_sphere", "blocks_jump2", "acceptance_1"])
-def test_partitions_reproduce_single_gpu(env, name, world):
+def test_partitions_reproduce_single_gpu(env, name, world, lookup):
     P, D, torch = env
     c = CASES[name]
-    check(P, D, torch, c["in_cells"], c["in_scalars"], float(c["iso"]), world)
+    check(P, D, torch, c["in_cells"], c["in_scalars"], float(c["iso"]), world, lookup)
+
+
+def test_partition_refuses_queries_and_halo_ranges(env):
+    """a partition holds one key range plus its halo: point queries and
+    extraction ranges reaching into the halo are refused (their answers
+    would need other ranks' cells), the owned range is accepted"""
+    P, D, torch = env
+    from paper_2004_08475_b200 import synth
+    ds = synth.bricks([16, 8, 8], seed=3, shuffle=True, holes=synth.body_holes([16, 8, 8]))
+    cells, scal = ds.cells.cpu().numpy(), ds.scalars.cpu().numpy()
+    c = {"cells": cells}
+    parts = emulate(P, D, torch, cells, scal, 4)
+    checked = 0
+    for idx, (lo, hi) in parts:
+        if idx is None:
+            continue
+        with pytest.raises(ValueError, match="partition"):
+            P.find_exact(idx, c["cells"][:4])
+        with pytest.raises(ValueError, match="partition"):
+            P.snap(idx, c["cells"][:4, :3].astype(np.int64))
+        with pytest.raises(ValueError, match="partition"):
+            P.validate_dataset(idx)
+        P.extract_dual_mesh(idx, cell_range=(lo, hi))
+        if idx.geometry()[13] > 0:  # the key range (owned + halo) starts above key 0
+            with pytest.raises(ValueError, match="interior"):
+                P.extract_dual_mesh(idx, cell_range=(0, hi))
+            checked += 1
+        idx.close()
+    assert checked >= 1
 
 
 @pytest.mark.parametrize("world", [2, 8])

@@ -4,18 +4,21 @@ iso value no scalar crosses."""
 import numpy as np
 import pytest
 
+from conftest import LOOKUPS, LookupProxy
+
 import oracles
 
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def P():
+@pytest.fixture(scope="module", params=LOOKUPS)
+def P(request):
+    """the package, once per lookup structure (conftest.LookupProxy)"""
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import paper_2004_08475_b200 as P
-    return P
+    return LookupProxy(P, request.param)
 
 
 def same(P, cells, scal, iso):

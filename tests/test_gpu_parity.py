@@ -15,6 +15,7 @@ import numpy as np
 import pytest
 
 import oracles
+from conftest import LOOKUPS, LookupProxy
 
 pytestmark = pytest.mark.gpu
 
@@ -32,13 +33,14 @@ CASES = _cases()
 KNOWN = json.load(open(os.path.join(GOLD, "known_answers.json")))
 
 
-@pytest.fixture(scope="module")
-def P():
+@pytest.fixture(scope="module", params=LOOKUPS)
+def P(request):
+    """the package, once per lookup structure (conftest.LookupProxy)"""
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import paper_2004_08475_b200 as P
-    return P
+    return LookupProxy(P, request.param)
 
 
 def bits(a):

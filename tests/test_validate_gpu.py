@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 import oracles
+from conftest import LOOKUPS, LookupProxy
 
 pytestmark = pytest.mark.gpu
 
@@ -23,8 +24,9 @@ def _cases():
 CASES = _cases()
 
 
-@pytest.fixture(scope="module")
-def env():
+@pytest.fixture(scope="module", params=LOOKUPS)
+def env(request):
+    """(package once per lookup structure, reference library)"""
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -32,7 +34,7 @@ def env():
     if R is None:
         pytest.skip("oracle/_ref not built")
     import paper_2004_08475_b200 as P
-    return P, R
+    return LookupProxy(P, request.param), R
 
 
 def broken(cells, scal, seed, n_dup=7, n_ovl=11):
