@@ -165,7 +165,7 @@ def run_amrx(args):
     sh = stream.cuda_stream
 
     # output buffer sized from a first (untimed) run
-    idx = P.build_index(cells, scal, device=local, stream=sh)
+    idx = P.build_index(cells, scal, device=local, stream=sh, lookup=args.lookup)
     from paper_2004_08475_b200 import synth as S
     dual_only = bool(S.CONFIGS[args.config].get("dual_only"))
     if dual_only:  # C5: the dual mesh only (8 x u32 corners + u64 task id per dual)
@@ -185,10 +185,13 @@ def run_amrx(args):
         cap = int(ntri_full * 1.05) + 1024
         out = torch.empty((cap, 9), dtype=torch.float64, device=dev)
     geometry = idx.geometry()
+    index_info = {"lookup": idx.info.lookup, "key_bits": idx.info.key_bits,
+                  "lookup_entries": idx.info.lookup_entries, "max_probe": idx.info.max_probe,
+                  "index_device_bytes": idx.info.device_bytes}
     idx.close()
 
     def step_single():
-        ix = P.build_index(cells, scal, device=local, stream=sh)
+        ix = P.build_index(cells, scal, device=local, stream=sh, lookup=args.lookup)
         if dual_only:
             d = P.extract_dual_mesh(ix, out=(out_c, out_t))
             ingest = ix.info.seconds_ingest
@@ -310,7 +313,7 @@ def run_amrx(args):
         hout = torch.empty((cap, 9), dtype=torch.float64, pin_memory=True)
 
         def step_e2e():
-            ix = P.build_index(hcells, hscal, device=local, stream=sh)
+            ix = P.build_index(hcells, hscal, device=local, stream=sh, lookup=args.lookup)
             r = P.extract_isosurface(ix, P.IsoParams(iso=iso), out=hout)
             ix.close()
             return len(r.fat)
@@ -387,7 +390,7 @@ def run_amrx(args):
                                ("dual mesh only" if dual_only else f"iso {iso}"),
                    "cells": n, "triangles": tris, "duals": duals_full, "iso": iso,
                    "parallelism": (f"distributed sort + range partition x{world}" if args.dist_mode == "partition" else f"rank-0 sort + broadcast x{world}") if world > 1 else "single GPU",
-                   "l2": "inputs (24 B/cell) far larger than L2", **meta},
+                   "l2": "inputs (24 B/cell) far larger than L2", "index": index_info, **meta},
         "iso_triangles_per_s": tris / (ms / 1000.0),
         "paper_split_ms": {"X_extract_kernel": kern_ms, "ingest_sort": 1000 * statistics.mean(ingest_s),
                            "Y_step": ms},
@@ -513,6 +516,45 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def free_port():
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(n, argv):
+    """--gpus N without a launcher: re-run this script under torchrun with N
+    ranks on this node (one per GPU), NCCL_DEBUG=INFO so the communicator
+    lines show the rank count; returns the launcher's exit code"""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd, env=env)
+
+
+def selftest(args):
+    """--selftest: the multi-rank plumbing only (gloo on CPU): every rank
+    joins, an all-reduce of the ranks and a max-over-ranks timing, rank 0
+    prints one line -- what tests/test_bench_spawn.py runs"""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist.init_process_group("gloo")
+    t = torch.tensor([float(rank + 1)])
+    dist.all_reduce(t)
+    ms = torch.tensor([1.0 + rank])
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"selftest": "ok", "n_gpus": world, "rank_sum": float(t.item()),
+                          "ms_max": float(ms.item()),
+                          "nccl_debug": os.environ.get("NCCL_DEBUG")}), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -525,9 +567,20 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-mode", default="partition", choices=["partition", "replicate"],
                     help="multi-GPU build: distributed sort + exchange, or rank-0 sort + broadcast")
+    ap.add_argument("--lookup", default=None, choices=["records", "hash", "directory"],
+                    help="force the index lookup structure (default: chosen from the key space)")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the multi-GPU code path even at world size 1 (testing)")
+    ap.add_argument("--selftest", action="store_true",
+                    help="multi-rank plumbing check over gloo (no GPU work)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus, sys.argv[1:]))
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+    if args.selftest:
+        selftest(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

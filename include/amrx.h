@@ -59,7 +59,8 @@ typedef enum amrx_status {
   AMRX_ERR_CAPACITY = 6,      /* caller buffer too small; *count holds the need */
   AMRX_ERR_UNSUPPORTED = 7,   /* dataset outside this build's limits */
   AMRX_ERR_NO_DEVICE = 8,     /* no CUDA device / kernel image for this GPU */
-  AMRX_ERR_IO = 9             /* file could not be written -> runtime_error */
+  AMRX_ERR_IO = 9,            /* file could not be written -> runtime_error */
+  AMRX_ERR_NCCL = 10          /* NCCL missing or a collective failed (amrx_comm_*) */
 } amrx_status;
 
 typedef struct amrx_index amrx_index;
@@ -283,6 +284,43 @@ AMRX_API amrx_status amrx_write_dual_mesh(const char *path, const uint32_t *corn
                                           uint64_t n_duals, const int32_t *cells4,
                                           const double *scalars, uint64_t n_cells,
                                           int threads);
+
+/* ---- single-process multi-GPU (one host thread per device, NCCL over
+ * NVLink / NVSwitch).  The reference's parallelism is a thread pool over
+ * candidate chunks (proj/include/amriso/parallel.hpp:49-85); its output is
+ * candidate order (proj/src/pipeline.cpp:40-57), so device d extracting the
+ * sorted cells [n d / N, n (d+1) / N) and the parts concatenated in device
+ * order give exactly the single-GPU output. */
+typedef struct amrx_comm amrx_comm;
+typedef struct amrx_comm_index amrx_comm_index;
+
+/* one NCCL communicator over `ndev` devices (ncclCommInitAll); devices =
+ * NULL means 0..ndev-1, ndev <= 0 every visible device.  NCCL is loaded on
+ * first use (AMRX_ERR_NCCL if it is missing). */
+AMRX_API amrx_status amrx_comm_init(int ndev, const int *devices, amrx_comm **out);
+AMRX_API amrx_status amrx_comm_destroy(amrx_comm *comm);
+AMRX_API amrx_status amrx_comm_size(const amrx_comm *comm, int *ndev);
+
+/* build_index on the first device, the sorted keys + scalars broadcast to
+ * the others (ncclBroadcast), each of which builds its own lookup
+ * structure: a replicated index.  flags: AMRX_FLAG_* as in
+ * amrx_index_opts.  The comm must outlive the index. */
+AMRX_API amrx_status amrx_comm_index_create(amrx_comm *comm, const int32_t *cells4,
+                                            const double *scalars, uint64_t n_cells,
+                                            uint64_t n_scalars, uint32_t flags,
+                                            amrx_comm_index **out);
+AMRX_API amrx_status amrx_comm_index_destroy(amrx_comm_index *index);
+
+/* amrx_extract_iso / amrx_extract_dual over every device: each extracts
+ * its share, the parts land in the caller's buffer (host or device memory)
+ * at their candidate-order offsets; xyz9 / corners8 NULL = count only.
+ * Stats are summed (device times: the slowest device). */
+AMRX_API amrx_status amrx_comm_extract_iso(amrx_comm_index *index,
+                                           const amrx_iso_params *params, void *xyz9,
+                                           uint64_t cap, uint64_t *count, amrx_stats *stats);
+AMRX_API amrx_status amrx_comm_extract_dual(amrx_comm_index *index, uint32_t *corners8,
+                                            uint64_t *task_ids, uint64_t cap, uint64_t *count,
+                                            amrx_stats *stats);
 
 /* testing hook: cap every extraction round's staging at `items` outputs
  * (0 = the default), so small inputs exercise the multi-round path; the

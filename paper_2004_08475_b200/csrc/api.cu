@@ -30,15 +30,6 @@ namespace amrx {
 namespace {
 thread_local std::string g_last_error;
 
-struct ApiError : std::runtime_error {
-  int code;
-  ApiError(int c, const std::string &m) : std::runtime_error(m), code(c) {}
-};
-
-[[noreturn]] void fail(int code, const std::string &msg)
-{
-  throw ApiError(code, msg);
-}
 
 template <typename Fn>
 amrx_status guarded(Fn &&fn)
@@ -367,60 +358,7 @@ int device_sm_count()
 
 using namespace amrx;
 
-struct amrx_index {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  bool own_stream = false;
-  uint64_t n = 0;
-  KeyGeom g{};
-  int64_t bounds_hi[3] = {0, 0, 0};
-  DevBuf keys, scal, dir, rec, order, scratch;
-  // partitions of a distributed index (amrx_index_from_keys): records of
-  // buckets [rec_lo, rec_lo + rec_n) only, global id of local position 0
-  uint64_t rec_lo = 0, rec_n = 0;
-  int64_t id_base = 0;
-  uint64_t key_lo = 0, key_hi = 0;
-  bool partition = false;  // amrx_index_from_keys: a key range of a distributed index
-  // a partition's interior: the local positions whose every lookup stays in
-  // [key_lo, key_hi) (extraction ranges must lie inside it)
-  uint64_t safe_lo = 0, safe_hi = ~0ull;
-  uint64_t hmask = 0;      // hashed records: slots - 1
-  bool searchable = true;  // false: sorted arrays only (amrx_index_sort_part)
-  uint32_t jobs_per_kcell = 0;  // marching-cubes jobs per 1024 cells, last extraction
-  amrx_index_info info{};
-  // last extraction kept on the device for the count-then-copy pattern
-  struct Cached {
-    bool valid = false;
-    int kind = 0;  // 1 dual, 2 iso
-    uint64_t begin = 0, end = 0;
-    double iso = 0;
-    int f32 = 0;
-    uint64_t count = 0;
-    amrx_stats stats{};
-  } cache;
-  DevBuf out_a, out_b;  // arena: corners/xyz, tasks
-  std::mutex mu;
-
-  SearchCtx ctx() const
-  {
-    SearchCtx s;
-    s.keys = keys.as<uint64_t>();
-    // dense or hashed occupancy records (unique keys: positions are
-    // popcounts), else the bucket directory (ensure_search_dir switches an
-    // index with duplicate keys to it)
-    s.rec = g.occ == kOccDense ? rec.as<uint2>() - rec_lo : nullptr;
-    s.htab = g.occ == kOccHash ? rec.as<uint4>() : nullptr;
-    s.hmask = hmask;
-    s.dir = g.occ == kOccNone ? dir.as<uint32_t>() : nullptr;
-    s.id_base = id_base;
-    s.n = n;
-    s.dir_shift = g.dir_shift;
-    s.shift = g.shift;
-    s.lmask = (uint64_t(1) << g.lbits) - 1;
-    s.dbg = nullptr;
-    return s;
-  }
-};
+#include "index.h"
 
 namespace {
 
@@ -580,13 +518,15 @@ void finalize_index(amrx_index *ix)
   } else if (ix->g.occ == kOccHash) {
     const uint64_t buckets = hash_count(ix->keys.as<uint64_t>(), ix->n, ix->g, order,
                                         ix->scratch, st);
-    uint64_t slots = 64;
-    while (slots < 2 * buckets) slots <<= 1;
-    ix->rec.reserve(slots * sizeof(uint4), st);
-    ix->hmask = slots - 1;
-    build_hash(ix->keys.as<uint64_t>(), ix->n, ix->g, ix->rec.as<uint4>(), slots,
+    // >= 3 entries per record bucket (load <= 1/3): most probes end in
+    // their home table bucket
+    uint64_t tb = 32;
+    while (2 * tb < 3 * buckets) tb <<= 1;
+    ix->rec.reserve(tb * sizeof(ulonglong4), st);
+    ix->hmask = tb - 1;
+    build_hash(ix->keys.as<uint64_t>(), ix->n, ix->g, ix->rec.as<ulonglong4>(), tb,
                reinterpret_cast<unsigned int *>(order + 2), st);
-    ix->info.lookup_entries = slots;
+    ix->info.lookup_entries = 2 * tb;
   } else {
     ix->dir.reserve(entries * sizeof(uint32_t), st);
     build_directory(ix->keys.as<uint64_t>(), ix->n, ix->g, ix->dir.as<uint32_t>(), nullptr,
@@ -691,6 +631,162 @@ void check_result(const ExtractResult &r, uint64_t cells, bool tri)
 }
 
 }  // namespace
+
+namespace amrx {
+
+void extract_dual_impl(amrx_index *index, const amrx_range *range, uint32_t *corners8,
+                     uint64_t *task_ids, uint64_t cap, uint64_t *count, amrx_stats *stats,
+                     bool cached)
+{
+  require_searchable(index);
+  if (!index || !count) fail(AMRX_ERR_INVALID_ARG, "null argument");
+  std::lock_guard<std::mutex> lock(index->mu);
+  DeviceGuard dg(index->device);
+  cudaStream_t st = index->stream;
+  uint64_t b, e;
+  check_range(index, range, b, e);
+  const uint64_t cells = e - b;
+  auto &C = index->cache;
+  // device memory or pinned host memory: written by the rounds directly
+  uint32_t *corners_w = static_cast<uint32_t *>(device_writable(corners8));
+  uint64_t *tasks_w = static_cast<uint64_t *>(device_writable(task_ids));
+  const bool dev_out = !cached && corners_w && (!task_ids || tasks_w);
+
+  ExtractRequest rq{};
+  rq.s = index->ctx();
+  rq.g = index->g;
+  rq.scal = index->scal.as<double>();
+  rq.unique = index->info.duplicate_keys == 0;
+  rq.cell_begin = b;
+  rq.cell_end = e;
+  rq.emit_dual = true;
+  if (dev_out) {
+    rq.final_host = !is_device_ptr(corners8);
+    rq.corners = rq.final_host ? corners8 : corners_w;
+    rq.tasks = rq.final_host ? task_ids : tasks_w;
+    rq.dual_cap = cap;
+    const ExtractResult r = run_extract(rq, st);
+    check_result(r, cells, false);
+    fill_stats(stats, r, cells);
+    *count = r.duals;
+    C.valid = false;
+    if (r.duals > cap)
+      fail(AMRX_ERR_CAPACITY, "output capacity " + std::to_string(cap) +
+                                " < " + std::to_string(r.duals) + " duals");
+    return;
+  }
+  // pageable host (or absent) output: extract into the index's device
+  // arena, which grows to fit, and keep it for the count-then-copy pattern
+  const bool hit = C.valid && C.kind == 1 && C.begin == b && C.end == e;
+  if (!hit) {
+    C.valid = false;
+    rq.grow_a = &index->out_a;
+    rq.grow_b = &index->out_b;
+    const ExtractResult r = run_extract(rq, st);
+    check_result(r, cells, false);
+    C.valid = true;
+    C.kind = 1;
+    C.begin = b;
+    C.end = e;
+    C.count = r.duals;
+    fill_stats(&C.stats, r, cells);
+  }
+  *count = C.count;
+  if (stats) *stats = C.stats;
+  if (!corners8 && !task_ids) return;  // count query
+  if (C.count > cap)
+    fail(AMRX_ERR_CAPACITY, "output capacity " + std::to_string(cap) + " < " +
+                              std::to_string(C.count) + " duals");
+  if (corners8 && C.count)
+    AMRX_CUDA(cudaMemcpyAsync(corners8, index->out_a.ptr, C.count * 32,
+                              cudaMemcpyDefault, st));
+  if (task_ids && C.count)
+    AMRX_CUDA(cudaMemcpyAsync(task_ids, index->out_b.ptr, C.count * 8,
+                              cudaMemcpyDefault, st));
+  AMRX_CUDA(cudaStreamSynchronize(st));
+}
+
+void extract_iso_impl(amrx_index *index, const amrx_range *range,
+                    const amrx_iso_params *params, void *xyz9, uint64_t cap,
+                    uint64_t *count, amrx_stats *stats, bool cached)
+{
+  require_searchable(index);
+  if (!index || !count || !params) fail(AMRX_ERR_INVALID_ARG, "null argument");
+  std::lock_guard<std::mutex> lock(index->mu);
+  DeviceGuard dg(index->device);
+  cudaStream_t st = index->stream;
+  uint64_t b, e;
+  check_range(index, range, b, e);
+  const uint64_t cells = e - b;
+  const size_t tri_bytes = params->xyz_is_f32 ? 36 : 72;
+  auto &C = index->cache;
+  // device memory or pinned host memory: written by the rounds directly
+  void *xyz_w = device_writable(xyz9);
+  const bool dev_out = !cached && xyz_w != nullptr;
+
+  ExtractRequest rq{};
+  rq.s = index->ctx();
+  rq.g = index->g;
+  rq.scal = index->scal.as<double>();
+  rq.unique = index->info.duplicate_keys == 0;
+  rq.cell_begin = b;
+  rq.cell_end = e;
+  rq.emit_tri = true;
+  rq.tri_f32 = params->xyz_is_f32 != 0;
+  rq.iso = params->iso;
+  const auto length_check = [&](uint64_t tris) {
+    if (params->check_length &&
+        tris > uint64_t(std::numeric_limits<uint32_t>::max()) / 3)
+      fail(AMRX_ERR_LENGTH, "extract_isosurface: mesh too large for 32-bit indices");
+  };
+  if (dev_out) {
+    rq.final_host = !is_device_ptr(xyz9);
+    rq.xyz = rq.final_host ? xyz9 : xyz_w;
+    rq.tri_cap = cap;
+    // pinned host output of a large input: small first rounds, each
+    // round's download overlapping the next round's extraction
+    rq.stream_rounds = rq.final_host && cells >= (uint64_t(1) << 24);
+    const ExtractResult r = run_extract(rq, st);
+    check_result(r, cells, true);
+    fill_stats(stats, r, cells);
+    *count = r.tris_written;
+    C.valid = false;
+    length_check(r.tris_written);
+    if (r.tris_written > cap)
+      fail(AMRX_ERR_CAPACITY, "output capacity " + std::to_string(cap) +
+                                " < " + std::to_string(r.tris_written) + " triangles");
+    return;
+  }
+  const bool hit = C.valid && C.kind == 2 && C.begin == b && C.end == e &&
+                   C.iso == params->iso && C.f32 == params->xyz_is_f32;
+  if (!hit) {
+    C.valid = false;
+    rq.grow_a = &index->out_a;
+    const ExtractResult r = run_extract(rq, st);
+    check_result(r, cells, true);
+    C.valid = true;
+    C.kind = 2;
+    C.begin = b;
+    C.end = e;
+    C.iso = params->iso;
+    C.f32 = params->xyz_is_f32;
+    C.count = r.tris_written;
+    fill_stats(&C.stats, r, cells);
+  }
+  *count = C.count;
+  if (stats) *stats = C.stats;
+  length_check(C.count);
+  if (!xyz9) return;  // count query
+  if (C.count > cap)
+    fail(AMRX_ERR_CAPACITY, "output capacity " + std::to_string(cap) + " < " +
+                              std::to_string(C.count) + " triangles");
+  if (C.count)
+    AMRX_CUDA(cudaMemcpyAsync(xyz9, index->out_a.ptr, C.count * tri_bytes,
+                              cudaMemcpyDefault, st));
+  AMRX_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace amrx
 
 extern "C" {
 
@@ -1571,72 +1667,7 @@ amrx_status amrx_extract_dual(amrx_index *index, const amrx_range *range,
                               uint64_t cap, uint64_t *count, amrx_stats *stats)
 {
   return guarded([&] {
-    require_searchable(index);
-    if (!index || !count) fail(AMRX_ERR_INVALID_ARG, "null argument");
-    std::lock_guard<std::mutex> lock(index->mu);
-    DeviceGuard dg(index->device);
-    cudaStream_t st = index->stream;
-    uint64_t b, e;
-    check_range(index, range, b, e);
-    const uint64_t cells = e - b;
-    auto &C = index->cache;
-    // device memory or pinned host memory: written by the rounds directly
-    uint32_t *corners_w = static_cast<uint32_t *>(device_writable(corners8));
-    uint64_t *tasks_w = static_cast<uint64_t *>(device_writable(task_ids));
-    const bool dev_out = corners_w && (!task_ids || tasks_w);
-
-    ExtractRequest rq{};
-    rq.s = index->ctx();
-    rq.g = index->g;
-    rq.scal = index->scal.as<double>();
-    rq.unique = index->info.duplicate_keys == 0;
-    rq.cell_begin = b;
-    rq.cell_end = e;
-    rq.emit_dual = true;
-    if (dev_out) {
-      rq.final_host = !is_device_ptr(corners8);
-      rq.corners = rq.final_host ? corners8 : corners_w;
-      rq.tasks = rq.final_host ? task_ids : tasks_w;
-      rq.dual_cap = cap;
-      const ExtractResult r = run_extract(rq, st);
-      check_result(r, cells, false);
-      fill_stats(stats, r, cells);
-      *count = r.duals;
-      C.valid = false;
-      if (r.duals > cap)
-        fail(AMRX_ERR_CAPACITY, "output capacity " + std::to_string(cap) +
-                                  " < " + std::to_string(r.duals) + " duals");
-      return;
-    }
-    // pageable host (or absent) output: extract into the index's device
-    // arena, which grows to fit, and keep it for the count-then-copy pattern
-    const bool hit = C.valid && C.kind == 1 && C.begin == b && C.end == e;
-    if (!hit) {
-      C.valid = false;
-      rq.grow_a = &index->out_a;
-      rq.grow_b = &index->out_b;
-      const ExtractResult r = run_extract(rq, st);
-      check_result(r, cells, false);
-      C.valid = true;
-      C.kind = 1;
-      C.begin = b;
-      C.end = e;
-      C.count = r.duals;
-      fill_stats(&C.stats, r, cells);
-    }
-    *count = C.count;
-    if (stats) *stats = C.stats;
-    if (!corners8 && !task_ids) return;  // count query
-    if (C.count > cap)
-      fail(AMRX_ERR_CAPACITY, "output capacity " + std::to_string(cap) + " < " +
-                                std::to_string(C.count) + " duals");
-    if (corners8 && C.count)
-      AMRX_CUDA(cudaMemcpyAsync(corners8, index->out_a.ptr, C.count * 32,
-                                cudaMemcpyDefault, st));
-    if (task_ids && C.count)
-      AMRX_CUDA(cudaMemcpyAsync(task_ids, index->out_b.ptr, C.count * 8,
-                                cudaMemcpyDefault, st));
-    AMRX_CUDA(cudaStreamSynchronize(st));
+    extract_dual_impl(index, range, corners8, task_ids, cap, count, stats, false);
   });
 }
 
@@ -1644,82 +1675,7 @@ amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range,
                              const amrx_iso_params *params, void *xyz9,
                              uint64_t cap, uint64_t *count, amrx_stats *stats)
 {
-  return guarded([&] {
-    require_searchable(index);
-    if (!index || !count || !params) fail(AMRX_ERR_INVALID_ARG, "null argument");
-    std::lock_guard<std::mutex> lock(index->mu);
-    DeviceGuard dg(index->device);
-    cudaStream_t st = index->stream;
-    uint64_t b, e;
-    check_range(index, range, b, e);
-    const uint64_t cells = e - b;
-    const size_t tri_bytes = params->xyz_is_f32 ? 36 : 72;
-    auto &C = index->cache;
-    // device memory or pinned host memory: written by the rounds directly
-    void *xyz_w = device_writable(xyz9);
-    const bool dev_out = xyz_w != nullptr;
-
-    ExtractRequest rq{};
-    rq.s = index->ctx();
-    rq.g = index->g;
-    rq.scal = index->scal.as<double>();
-    rq.unique = index->info.duplicate_keys == 0;
-    rq.cell_begin = b;
-    rq.cell_end = e;
-    rq.emit_tri = true;
-    rq.tri_f32 = params->xyz_is_f32 != 0;
-    rq.iso = params->iso;
-    const auto length_check = [&](uint64_t tris) {
-      if (params->check_length &&
-          tris > uint64_t(std::numeric_limits<uint32_t>::max()) / 3)
-        fail(AMRX_ERR_LENGTH, "extract_isosurface: mesh too large for 32-bit indices");
-    };
-    if (dev_out) {
-      rq.final_host = !is_device_ptr(xyz9);
-      rq.xyz = rq.final_host ? xyz9 : xyz_w;
-      rq.tri_cap = cap;
-      // pinned host output of a large input: small first rounds, each
-      // round's download overlapping the next round's extraction
-      rq.stream_rounds = rq.final_host && cells >= (uint64_t(1) << 24);
-      const ExtractResult r = run_extract(rq, st);
-      check_result(r, cells, true);
-      fill_stats(stats, r, cells);
-      *count = r.tris_written;
-      C.valid = false;
-      length_check(r.tris_written);
-      if (r.tris_written > cap)
-        fail(AMRX_ERR_CAPACITY, "output capacity " + std::to_string(cap) +
-                                  " < " + std::to_string(r.tris_written) + " triangles");
-      return;
-    }
-    const bool hit = C.valid && C.kind == 2 && C.begin == b && C.end == e &&
-                     C.iso == params->iso && C.f32 == params->xyz_is_f32;
-    if (!hit) {
-      C.valid = false;
-      rq.grow_a = &index->out_a;
-      const ExtractResult r = run_extract(rq, st);
-      check_result(r, cells, true);
-      C.valid = true;
-      C.kind = 2;
-      C.begin = b;
-      C.end = e;
-      C.iso = params->iso;
-      C.f32 = params->xyz_is_f32;
-      C.count = r.tris_written;
-      fill_stats(&C.stats, r, cells);
-    }
-    *count = C.count;
-    if (stats) *stats = C.stats;
-    length_check(C.count);
-    if (!xyz9) return;  // count query
-    if (C.count > cap)
-      fail(AMRX_ERR_CAPACITY, "output capacity " + std::to_string(cap) + " < " +
-                                std::to_string(C.count) + " triangles");
-    if (C.count)
-      AMRX_CUDA(cudaMemcpyAsync(xyz9, index->out_a.ptr, C.count * tri_bytes,
-                                cudaMemcpyDefault, st));
-    AMRX_CUDA(cudaStreamSynchronize(st));
-  });
+  return guarded([&] { extract_iso_impl(index, range, params, xyz9, cap, count, stats, false); });
 }
 
 }  // extern "C"

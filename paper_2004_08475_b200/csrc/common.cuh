@@ -51,13 +51,16 @@ struct KeyGeom {
 constexpr int kOccShift = 5;  // key values per occupancy record = 2^5
 enum : int32_t { kOccNone = 0, kOccDense = 1, kOccHash = 2 };
 
-/*! Hashed occupancy records: slot = {u64 tag = bucket + 1 (0 = empty), u32
-    start, u32 bits} (16 bytes, one vector load).  Linear probing from
-    hash_home(bucket); the four buckets of an aligned 128-value superbucket
-    share one hashed home group (mix of bucket >> 2, low two bits kept), so
-    neighbouring records of a dense region sit in one 64-byte run like the
-    dense array's.  The table has at least twice as many slots as occupied
-    buckets; the build reports the longest probe. */
+/*! Hashed occupancy records: entry = {u64 tag = bucket + 1 (0 = empty),
+    u32 start, u32 bits}; two entries per 32-byte table bucket, which a
+    lookup reads with ONE 256-bit load (ld.global.nc.v4.u64).  Linear
+    probing over table buckets from hash_home; a table bucket with a free
+    entry ends a probe (buckets only ever fill up).  Record buckets b and
+    b^1 (the two halves of an aligned 64-value range) share a home, b
+    preferring entry b & 1, so neighbouring records of a dense region come
+    in one load and the extraction's fast path reads 16 bytes.  The table has at least
+    three entries per occupied record bucket; the build reports the longest
+    probe (in table buckets). */
 __host__ __device__ inline uint64_t mix64(uint64_t x)
 {
   x ^= x >> 31;
@@ -68,9 +71,10 @@ __host__ __device__ inline uint64_t mix64(uint64_t x)
   return x;
 }
 
+/// home table bucket of record bucket b (mask = table buckets - 1)
 __host__ __device__ inline uint64_t hash_home(uint64_t bucket, uint64_t mask)
 {
-  return ((mix64(bucket >> 2) << 2) | (bucket & 3)) & mask;
+  return mix64(bucket >> 1) & mask;
 }
 
 __host__ __device__ inline int64_t anchor_mask(int64_t x, int32_t level)
@@ -269,8 +273,8 @@ struct SearchCtx {
   // indexed by the global bucket (only in-range buckets are ever read)
   const uint2 *rec;
   // hashed occupancy records (KeyGeom::occ == kOccHash), or null: 2^k
-  // 16-byte slots, hmask = 2^k - 1
-  const uint4 *htab;
+  // 32-byte table buckets (two entries each), hmask = 2^k - 1
+  const ulonglong4 *htab;
   uint64_t hmask;
   // global CellId of local position 0 (a partition of a distributed index;
   // 0 otherwise): added to every id a query or an extraction reports
@@ -307,21 +311,38 @@ __device__ __forceinline__ uint2 ldg_rec(const uint2 *rec, uint64_t q, int dir_s
   return __ldg(rec + (q >> dir_shift));
 }
 
-__device__ __forceinline__ uint64_t slot_tag(uint4 e)
+/// one table bucket (two entries) in a single 256-bit read-only load
+__device__ __forceinline__ ulonglong4 ldg_bucket(const ulonglong4 *p)
 {
-  return uint64_t(e.x) | (uint64_t(e.y) << 32);
+  ulonglong4 v;
+  asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+      : "=l"(v.x), "=l"(v.y), "=l"(v.z), "=l"(v.w)
+      : "l"(p));
+  return v;
 }
 
-/// the hashed record of bucket b, continuing a probe at slot h whose entry
-/// e was already loaded; {0, 0} (no bits) when the bucket is empty
-__device__ __forceinline__ uint2 hash_probe(const SearchCtx &s, uint64_t b, uint64_t h, uint4 e)
+/// the record of bucket b in table bucket e (loaded from slot h); found =
+/// false with more = true when the probe must go on
+__device__ __forceinline__ uint2 bucket_match(ulonglong4 e, uint64_t b, bool &more)
+{
+  more = false;
+  if (e.x == b + 1) return make_uint2(uint32_t(e.y), uint32_t(e.y >> 32));
+  if (e.z == b + 1) return make_uint2(uint32_t(e.w), uint32_t(e.w >> 32));
+  more = e.x != 0 && e.z != 0;
+  return make_uint2(0, 0);
+}
+
+/// the hashed record of bucket b, continuing a probe at table bucket h
+/// whose content e was already loaded; {0, 0} (no bits) when b is empty
+__device__ __forceinline__ uint2 hash_probe(const SearchCtx &s, uint64_t b, uint64_t h,
+                                            ulonglong4 e)
 {
   for (;;) {
-    const uint64_t t = slot_tag(e);
-    if (t == b + 1) return make_uint2(e.z, e.w);
-    if (t == 0) return make_uint2(0, 0);
+    bool more;
+    const uint2 r = bucket_match(e, b, more);
+    if (!more) return r;
     h = (h + 1) & s.hmask;
-    e = __ldg(s.htab + h);
+    e = ldg_bucket(s.htab + h);
   }
 }
 
@@ -332,12 +353,12 @@ __device__ __forceinline__ void hash_find(const SearchCtx &s, const uint64_t (&q
                                           const bool (&valid)[K], int64_t (&out)[K],
                                           int (&lvl)[K])
 {
-  uint4 e[K];
+  ulonglong4 e[K];
   uint64_t h[K];
 #pragma unroll
   for (int k = 0; k < K; k++) {
     h[k] = hash_home(q[k] >> s.dir_shift, s.hmask);
-    e[k] = valid[k] ? __ldg(s.htab + h[k]) : make_uint4(0, 0, 0, 0);
+    e[k] = valid[k] ? ldg_bucket(s.htab + h[k]) : make_ulonglong4(0, 0, 0, 0);
   }
 #pragma unroll
   for (int k = 0; k < K; k++)

@@ -35,6 +35,7 @@
 #include <initializer_list>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <mutex>
 #include <unordered_map>
@@ -547,10 +548,12 @@ constexpr uint32_t kFast1 = kCube << 13 & ~(1u << 13);       // 14 16 17 22 23 2
     load of the list is issued before any is used, so they are in flight
     together.  The common case -- the point's own anchor exists on the hint
     level -- is resolved here; anything else (finer, coarser, absent) is
-    left in `pend` for the runtime loop. */
+    left in `pend` for the runtime loop.  L = kOccDense reads the dense
+    record (8 bytes); L = kOccHash the preferred entry of the record's home
+    table bucket (16 bytes: tag + record) -- an entry holding another bucket
+    leaves the point to the runtime loop's full probe. */
 template <int P>
-__device__ __forceinline__ void fast_issue(const KArgs &a, const Stencil &st, uint32_t need,
-                                           uint2 &r, uint32_t &bit)
+__device__ __forceinline__ uint64_t fast_key(const Stencil &st)
 {
   constexpr int ox = P % 3 - 1, oy = (P / 3) % 3 - 1, oz = P / 9 - 1;
   uint64_t q = st.k0;
@@ -560,17 +563,56 @@ __device__ __forceinline__ void fast_issue(const KArgs &a, const Stencil &st, ui
   if (oy < 0) q -= st.sy;
   if (oz > 0) q += st.sz;
   if (oz < 0) q -= st.sz;
-  bit = uint32_t(q) & 31u;
-  r = make_uint2(0, 0);
-  if (((need & st.inrange) >> P) & 1u) r = ldg_rec(a.s.rec, q, a.s.dir_shift);
+  return q;
 }
 
-template <int P>
-__device__ __forceinline__ void fast_finish(Smem &sm, int warp, int lane, const Cell &c,
-                                            uint32_t need, uint2 r, uint32_t bit, Marks &m,
-                                            uint32_t &pend)
+template <int L>
+struct FastRec;
+template <>
+struct FastRec<kOccDense> {
+  using T = uint2;
+};
+template <>
+struct FastRec<kOccHash> {
+  using T = uint4;  // {tag lo, tag hi, start, bits}
+};
+
+template <int P, int L>
+__device__ __forceinline__ void fast_issue(const KArgs &a, const Stencil &st, uint32_t need,
+                                           typename FastRec<L>::T &r)
+{
+  const uint64_t q = fast_key<P>(st);
+  const bool go = ((need & st.inrange) >> P) & 1u;
+  if (L == kOccDense) {
+    uint2 v = make_uint2(0, 0);
+    if (go) v = ldg_rec(a.s.rec, q, a.s.dir_shift);
+    reinterpret_cast<uint2 &>(r) = v;
+  } else {
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (go) {
+      const uint64_t b = q >> a.s.dir_shift;
+      v = __ldg(reinterpret_cast<const uint4 *>(a.s.htab + hash_home(b, a.s.hmask)) + (b & 1));
+    }
+    reinterpret_cast<uint4 &>(r) = v;
+  }
+}
+
+template <int P, int L>
+__device__ __forceinline__ void fast_finish(const KArgs &a, Smem &sm, int warp, int lane,
+                                            const Cell &c, const Stencil &st, uint32_t need,
+                                            typename FastRec<L>::T rr, Marks &m, uint32_t &pend)
 {
   if (!((need >> P) & 1u)) return;
+  const uint64_t q = fast_key<P>(st);
+  const uint32_t bit = uint32_t(q) & 31u;
+  uint2 r;
+  if (L == kOccDense) {
+    r = reinterpret_cast<const uint2 &>(rr);
+  } else {
+    const uint4 e = reinterpret_cast<const uint4 &>(rr);
+    const bool mine = (uint64_t(e.x) | (uint64_t(e.y) << 32)) == (q >> a.s.dir_shift) + 1;
+    r = mine ? make_uint2(e.z, e.w) : make_uint2(0, 0);
+  }
   if ((r.y >> bit) & 1u) {  // (an out-of-range point has r = 0: a miss)
     constexpr int ox = P % 3 - 1, oy = (P / 3) % 3 - 1, oz = P / 9 - 1;
     constexpr bool lower = ox < 0 || (ox == 0 && (oy < 0 || (oy == 0 && oz < 0)));
@@ -585,25 +627,24 @@ __device__ __forceinline__ void fast_finish(Smem &sm, int warp, int lane, const 
   pend |= 1u << P;
 }
 
-template <int... Ps, size_t... I>
+template <int L, int... Ps, size_t... I>
 __device__ __forceinline__ void fast_batch_impl(std::index_sequence<I...>, const KArgs &a,
                                                 Smem &sm, int warp, int lane, const Cell &c,
                                                 const Stencil &st, uint32_t need, Marks &m,
                                                 uint32_t &pend)
 {
-  uint2 r[sizeof...(Ps)];
-  uint32_t bit[sizeof...(Ps)];
-  (fast_issue<Ps>(a, st, need, r[I], bit[I]), ...);
-  (fast_finish<Ps>(sm, warp, lane, c, need, r[I], bit[I], m, pend), ...);
+  typename FastRec<L>::T r[sizeof...(Ps)];
+  (fast_issue<Ps, L>(a, st, need, r[I]), ...);
+  (fast_finish<Ps, L>(a, sm, warp, lane, c, st, need, r[I], m, pend), ...);
 }
 
-template <int... Ps>
+template <int L, int... Ps>
 __device__ __forceinline__ void fast_batch(const KArgs &a, Smem &sm, int warp, int lane,
                                            const Cell &c, const Stencil &st, uint32_t need,
                                            Marks &m, uint32_t &pend)
 {
-  fast_batch_impl<Ps...>(std::make_index_sequence<sizeof...(Ps)>{}, a, sm, warp, lane, c, st,
-                         need, m, pend);
+  fast_batch_impl<L, Ps...>(std::make_index_sequence<sizeof...(Ps)>{}, a, sm, warp, lane, c, st,
+                            need, m, pend);
 }
 
 /*! resolve the stencil points in `todo` into the marks: two per lane
@@ -659,7 +700,7 @@ __device__ __forceinline__ void resolve_marks(const KArgs &a, Smem &sm, int warp
   }
 }
 
-template <bool EMIT_DUAL, bool EMIT_TRI, bool F32>
+template <bool EMIT_DUAL, bool EMIT_TRI, bool F32, int LOOKUP>
 #ifndef AMRX_MINB
 #define AMRX_MINB 4  // CTAs per SM the register budget is sized for (64 regs)
 #endif
@@ -733,17 +774,18 @@ extract_kernel(const __grid_constant__ KArgs a)
           for (uint32_t mm = alive; mm; mm &= mm - 1) need |= kCube << base_of(__ffs(mm) - 1);
           need &= ~m.resolved();
         }
-        if (a.s.rec) {
+        if (LOOKUP != kOccNone) {
           // the points every cell of a uniform region needs -- all
           // candidates' corner 0 in round 0, candidate 7's cube in round 1 --
           // with compile-time offsets; the rest and every miss go through
           // the runtime loop
+          constexpr int L = LOOKUP == kOccHash ? kOccHash : kOccDense;
           uint32_t pend = 0;
           if (round == 0) {
-            fast_batch<0, 1, 3, 4, 9, 10, 12>(a, sm, warp, lane, c, st, need, m, pend);
+            fast_batch<L, 0, 1, 3, 4, 9, 10, 12>(a, sm, warp, lane, c, st, need, m, pend);
             need &= ~kFast0;
           } else if (__any_sync(kFull, (need & kFast1) != 0)) {
-            fast_batch<14, 16, 17, 22, 23, 25, 26>(a, sm, warp, lane, c, st, need, m, pend);
+            fast_batch<L, 14, 16, 17, 22, 23, 25, 26>(a, sm, warp, lane, c, st, need, m, pend);
             need &= ~kFast1;
           }
           need |= pend;
@@ -1040,15 +1082,15 @@ int grid_query(uint64_t n)
                                                        uint64_t(device_sm_count()) * 8)));
 }
 
-template <bool D, bool T, bool F>
+template <bool D, bool T, bool F, int L>
 void launch_extract(const KArgs &k, int grid, cudaStream_t st)
 {
-  ensure_smem_attr(reinterpret_cast<const void *>(extract_kernel<D, T, F>), sizeof(Smem));
-  extract_kernel<D, T, F><<<grid, kThreads, sizeof(Smem), st>>>(k);
+  ensure_smem_attr(reinterpret_cast<const void *>(extract_kernel<D, T, F, L>), sizeof(Smem));
+  extract_kernel<D, T, F, L><<<grid, kThreads, sizeof(Smem), st>>>(k);
   AMRX_LAUNCH_CHECK();
 }
 
-template <bool D, bool T, bool F>
+template <bool D, bool T, bool F, int L>
 int occupancy_grid()
 {
   static int per_sm[64] = {0};  // per device
@@ -1056,12 +1098,37 @@ int occupancy_grid()
   AMRX_CUDA(cudaGetDevice(&dev));
   int &ps = per_sm[dev & 63];
   if (!ps) {
-    ensure_smem_attr(reinterpret_cast<const void *>(extract_kernel<D, T, F>), sizeof(Smem));
+    ensure_smem_attr(reinterpret_cast<const void *>(extract_kernel<D, T, F, L>), sizeof(Smem));
     AMRX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &ps, extract_kernel<D, T, F>, kThreads, sizeof(Smem)));
+      &ps, extract_kernel<D, T, F, L>, kThreads, sizeof(Smem)));
     ps = std::max(1, ps);
   }
   return ps * device_sm_count();
+}
+
+/*! the extraction kernel variant for a request: dual mesh, or the soup in
+    f64 / f32, times the lookup structure's fast path (none, dense records,
+    hashed records) -- fn(kernel tag) with the template arguments bound */
+template <typename Fn>
+void with_variant(bool D, bool F, int occ, Fn &&fn)
+{
+  const auto by_lookup = [&](auto d, auto f) {
+    constexpr bool Dv = decltype(d)::value, Fv = decltype(f)::value;
+    if (occ == kOccDense)
+      fn(std::integral_constant<int, kOccDense>{}, d, f);
+    else if (occ == kOccHash)
+      fn(std::integral_constant<int, kOccHash>{}, d, f);
+    else
+      fn(std::integral_constant<int, kOccNone>{}, d, f);
+    (void)Dv;
+    (void)Fv;
+  };
+  if (D)
+    by_lookup(std::true_type{}, std::false_type{});
+  else if (F)
+    by_lookup(std::false_type{}, std::true_type{});
+  else
+    by_lookup(std::false_type{}, std::false_type{});
 }
 
 }  // namespace
@@ -1103,13 +1170,13 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
   const uint64_t cells = r.cell_end > r.cell_begin ? r.cell_end - r.cell_begin : 0;
   const uint64_t tiles = (cells + kTileCells - 1) / kTileCells;
   const bool D = r.emit_dual, T = r.emit_tri, F = r.tri_f32;
+  if (D == T) throw std::invalid_argument("extract: exactly one of dual mesh / soup per call");
+  const int occ = r.s.rec ? kOccDense : r.s.htab ? kOccHash : kOccNone;
   int grid = 1;
-  if (D && T && F) grid = occupancy_grid<true, true, true>();
-  else if (D && T) grid = occupancy_grid<true, true, false>();
-  else if (D) grid = occupancy_grid<true, false, false>();
-  else if (T && F) grid = occupancy_grid<false, true, true>();
-  else if (T) grid = occupancy_grid<false, true, false>();
-  else grid = occupancy_grid<false, false, false>();
+  with_variant(D, F, occ, [&](auto l, auto d, auto f) {
+    grid = occupancy_grid<decltype(d)::value, !decltype(d)::value, decltype(f)::value,
+                          decltype(l)::value>();
+  });
   grid = int(std::max<uint64_t>(1, std::min<uint64_t>(grid, (tiles + kWarps - 1) / kWarps)));
   if (g_round_limit.load()) grid = 1;  // testing hook: few tiles in flight, many rounds
   const uint64_t warps = uint64_t(grid) * kWarps;
@@ -1258,12 +1325,10 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
     }
     k.tile_limit = limit;
     AMRX_CUDA(cudaEventRecord(e0, st));
-    if (D && T && F) launch_extract<true, true, true>(k, grid, st);
-    else if (D && T) launch_extract<true, true, false>(k, grid, st);
-    else if (D) launch_extract<true, false, false>(k, grid, st);
-    else if (T && F) launch_extract<false, true, true>(k, grid, st);
-    else if (T) launch_extract<false, true, false>(k, grid, st);
-    else launch_extract<false, false, false>(k, grid, st);
+    with_variant(D, F, occ, [&](auto l, auto d, auto f) {
+      launch_extract<decltype(d)::value, !decltype(d)::value, decltype(f)::value,
+                     decltype(l)::value>(k, grid, st);
+    });
     res.launches += 1;
     if (T && tri_stage) {
       const int mgrid = device_sm_count() * 8;

@@ -548,11 +548,14 @@ hash_count_kernel(const uint64_t *__restrict__ keys, uint64_t n, int dir_shift,
   }
 }
 
-/// one slot per distinct bucket (unique keys: a bucket holds <= 32 keys);
-/// the first key of a bucket inserts it with the OR of its keys' bits
+/// one entry per distinct record bucket (unique keys: a bucket holds <= 32
+/// keys); the first key of a bucket inserts it with the OR of its keys' bits
+/// into the first free entry of its probe sequence, the entry b & 1 of a
+/// table bucket before the other (a full table bucket never empties, so a
+/// probe may stop at the first table bucket with a free entry)
 __global__ void __launch_bounds__(kThreads)
 hash_build_kernel(const uint64_t *__restrict__ keys, uint64_t n, int dir_shift,
-                  uint4 *__restrict__ tab, uint64_t mask, unsigned int *max_probe)
+                  ulonglong4 *__restrict__ tab, uint64_t mask, unsigned int *max_probe)
 {
   const int lane = threadIdx.x & 31;
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
@@ -582,12 +585,22 @@ hash_build_kernel(const uint64_t *__restrict__ keys, uint64_t n, int dir_shift,
         }
       uint64_t h = hash_home(b, mask);
       unsigned int probe = 0;
-      while (atomicCAS(reinterpret_cast<unsigned long long *>(tab + h), 0ull,
-                       (unsigned long long)(b + 1)) != 0ull) {
+      unsigned long long *slot = nullptr;
+      const int pref = int(b & 1);  // the preferred entry (lookups read it first)
+      for (;;) {
+        unsigned long long *e = reinterpret_cast<unsigned long long *>(tab + h);
+        if (atomicCAS(e + 2 * pref, 0ull, (unsigned long long)(b + 1)) == 0ull) {
+          slot = e + 2 * pref;
+          break;
+        }
+        if (atomicCAS(e + 2 * (pref ^ 1), 0ull, (unsigned long long)(b + 1)) == 0ull) {
+          slot = e + 2 * (pref ^ 1);
+          break;
+        }
         h = (h + 1) & mask;
         probe++;
       }
-      reinterpret_cast<uint2 *>(tab + h)[1] = make_uint2(uint32_t(i), v);
+      slot[1] = uint64_t(uint32_t(i)) | (uint64_t(v) << 32);
       longest = probe > longest ? probe : longest;
     }
   }
@@ -796,13 +809,13 @@ uint64_t hash_count(const uint64_t *keys, uint64_t n, const KeyGeom &g,
   return h[0];
 }
 
-void build_hash(const uint64_t *keys, uint64_t n, const KeyGeom &g, uint4 *tab, uint64_t slots,
-                unsigned int *max_probe, cudaStream_t st)
+void build_hash(const uint64_t *keys, uint64_t n, const KeyGeom &g, ulonglong4 *tab,
+                uint64_t buckets, unsigned int *max_probe, cudaStream_t st)
 {
-  AMRX_CUDA(cudaMemsetAsync(tab, 0, slots * sizeof(uint4), st));
+  AMRX_CUDA(cudaMemsetAsync(tab, 0, buckets * sizeof(ulonglong4), st));
   AMRX_CUDA(cudaMemsetAsync(max_probe, 0, sizeof(unsigned int), st));
   hash_build_kernel<<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(keys, n, g.dir_shift, tab,
-                                                                   slots - 1, max_probe);
+                                                                   buckets - 1, max_probe);
   AMRX_LAUNCH_CHECK();
 }
 

@@ -3,6 +3,7 @@
 
 #include <cstdint>
 #include <atomic>
+#include <stdexcept>
 #include <string>
 #include <cuda_runtime.h>
 
@@ -10,11 +11,17 @@
 
 namespace amrx {
 
-/// status + message carried out of the implementation to the C ABI
-struct Error {
-  int code;  // amrx_status
-  std::string message;
+/// a failure with its amrx_status code, turned into the return value (and
+/// the thread's amrx_last_error text) at the C ABI
+struct ApiError : std::runtime_error {
+  int code;
+  ApiError(int c, const std::string &m) : std::runtime_error(m), code(c) {}
 };
+
+[[noreturn]] inline void fail(int code, const std::string &msg) { throw ApiError(code, msg); }
+
+/// the thread-local amrx_last_error text (api.cu)
+void set_last_error(const std::string &msg, bool clear);
 
 [[noreturn]] void throw_cuda(cudaError_t e, const char *what, const char *file,
                              int line);
@@ -164,10 +171,10 @@ void build_directory(const uint64_t *keys, uint64_t n, const KeyGeom &g,
 /// order2 (device, 2 x u64) receives the keys' descents and equal pairs
 uint64_t hash_count(const uint64_t *keys, uint64_t n, const KeyGeom &g,
                     unsigned long long *order2, DevBuf &scratch, cudaStream_t st);
-/// fill the table of `slots` (a power of two >= 2 x buckets) 16-byte
-/// slots; *max_probe (device) = the longest displacement from a home slot
-void build_hash(const uint64_t *keys, uint64_t n, const KeyGeom &g, uint4 *tab, uint64_t slots,
-                unsigned int *max_probe, cudaStream_t st);
+/// fill the table of `buckets` (a power of two) 32-byte table buckets, two
+/// entries each; *max_probe (device) = the longest displacement (buckets)
+void build_hash(const uint64_t *keys, uint64_t n, const KeyGeom &g, ulonglong4 *tab,
+                uint64_t buckets, unsigned int *max_probe, cudaStream_t st);
 
 /// lower_bound of nq host keys q in the sorted device keys -> host out (synchronises)
 void lower_bounds(const uint64_t *keys, uint64_t n, const uint64_t *q, int nq, uint64_t *out,
