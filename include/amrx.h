@@ -298,6 +298,8 @@ typedef struct amrx_comm_index amrx_comm_index;
  * NULL means 0..ndev-1, ndev <= 0 every visible device.  NCCL is loaded on
  * first use (AMRX_ERR_NCCL if it is missing). */
 AMRX_API amrx_status amrx_comm_init(int ndev, const int *devices, amrx_comm **out);
+/* CUDA devices visible to this process */
+AMRX_API amrx_status amrx_device_count(int *n);
 AMRX_API amrx_status amrx_comm_destroy(amrx_comm *comm);
 AMRX_API amrx_status amrx_comm_size(const amrx_comm *comm, int *ndev);
 

@@ -41,6 +41,7 @@ AMRX_ERR_CAPACITY = 6
 AMRX_ERR_UNSUPPORTED = 7
 AMRX_ERR_NO_DEVICE = 8
 AMRX_ERR_IO = 9
+AMRX_ERR_NCCL = 10
 
 MAX_LEVEL = 30
 
@@ -149,6 +150,14 @@ def library():
         "amrx_try_build_duals": [P, P, U64, P, P],
         "amrx_extract_dual": [P, P, P, P, U64, P, P],
         "amrx_extract_iso": [P, P, P, P, U64, P, P],
+        "amrx_device_count": [P],
+        "amrx_comm_init": [C.c_int, P, P],
+        "amrx_comm_destroy": [P],
+        "amrx_comm_size": [P, P],
+        "amrx_comm_index_create": [P, P, P, U64, U64, C.c_uint32, P],
+        "amrx_comm_index_destroy": [P],
+        "amrx_comm_extract_iso": [P, P, P, U64, P, P],
+        "amrx_comm_extract_dual": [P, P, P, U64, P, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -708,3 +717,107 @@ def write_dual_mesh(path, duals, index, threads=0):
                                           len(corners), _ptr(cells), _ptr(scal), len(cells),
                                           threads))
 
+
+
+# ---------------------------------------------------------------------------
+# single-process multi-GPU (amrx_comm_*: NCCL over NVLink, one host thread
+# per device)
+
+def device_count():
+    n = C.c_int(0)
+    _check(library().amrx_device_count(C.byref(n)))
+    return n.value
+
+
+class Comm:
+    """one NCCL communicator over several GPUs of this process
+    (amrx_comm_init); ``devices`` = list of ordinals, None = all visible"""
+
+    def __init__(self, devices=None):
+        lib = library()
+        self._lib = lib
+        self._h = C.c_void_p()
+        if devices is None:
+            _check(lib.amrx_comm_init(0, None, C.byref(self._h)))
+        else:
+            d = (C.c_int * len(devices))(*devices)
+            _check(lib.amrx_comm_init(len(devices), d, C.byref(self._h)))
+
+    def size(self):
+        n = C.c_int(0)
+        _check(self._lib.amrx_comm_size(self._h, C.byref(n)))
+        return n.value
+
+    def build_index(self, cells, scalars, presorted=False, lookup=None):
+        """build_index on the first device, broadcast to the others"""
+        cells = np.ascontiguousarray(np.asarray(cells, np.int32).reshape(-1, 4)) \
+            if not hasattr(cells, "data_ptr") else cells
+        scalars = np.ascontiguousarray(np.asarray(scalars, np.float64).reshape(-1)) \
+            if not hasattr(scalars, "data_ptr") else scalars
+        n = cells.shape[0]
+        ns = scalars.shape[0]
+        h = C.c_void_p()
+        _check(self._lib.amrx_comm_index_create(self._h, _ptr(cells), _ptr(scalars), n, ns,
+                                                _flags(presorted, lookup), C.byref(h)))
+        return CommIndex(h.value, self)
+
+    def close(self):
+        if self._h:
+            self._lib.amrx_comm_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class CommIndex:
+    """a replicated index over a Comm's devices; extraction splits the
+    cells across them and concatenates in candidate order"""
+
+    def __init__(self, handle, comm):
+        self._h = C.c_void_p(handle)
+        self._comm = comm
+
+    def extract_isosurface(self, params=None, out=None):
+        if params is None:
+            params = IsoParams()
+        elif isinstance(params, (int, float)):
+            params = IsoParams(iso=float(params))
+        lib = self._comm._lib
+        p = _IsoParams(float(params.iso), 1 if params.f32 else 0, 1)
+        st = _Stats()
+        cnt = C.c_uint64(0)
+        if out is None:
+            _check(lib.amrx_comm_extract_iso(self._h, C.byref(p), None, 0, C.byref(cnt),
+                                             C.byref(st)))
+            out = np.empty((cnt.value, 9), np.float32 if params.f32 else np.float64)
+        rc = lib.amrx_comm_extract_iso(self._h, C.byref(p), _ptr(out), out.shape[0],
+                                       C.byref(cnt), C.byref(st))
+        _check(rc, cnt.value)
+        return ExtractionResult(out[: cnt.value], ExtractionStats._from(st))
+
+    def extract_dual_mesh(self):
+        lib = self._comm._lib
+        st = _Stats()
+        cnt = C.c_uint64(0)
+        _check(lib.amrx_comm_extract_dual(self._h, None, None, 0, C.byref(cnt), C.byref(st)))
+        corners = np.empty((cnt.value, 8), np.uint32)
+        tasks = np.empty(cnt.value, np.uint64)
+        if cnt.value:
+            _check(lib.amrx_comm_extract_dual(self._h, _ptr(corners), _ptr(tasks), cnt.value,
+                                              C.byref(cnt), C.byref(st)))
+        return DualMesh(corners, tasks, ExtractionStats._from(st))
+
+    def close(self):
+        if self._h:
+            self._comm._lib.amrx_comm_index_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -522,6 +522,8 @@ void finalize_index(amrx_index *ix)
     // their home table bucket
     uint64_t tb = 32;
     while (2 * tb < 3 * buckets) tb <<= 1;
+    if (tb > (uint64_t(1) << 32))
+      fail(AMRX_ERR_UNSUPPORTED, "hashed records: more than 2^32 table buckets");
     ix->rec.reserve(tb * sizeof(ulonglong4), st);
     ix->hmask = tb - 1;
     build_hash(ix->keys.as<uint64_t>(), ix->n, ix->g, ix->rec.as<ulonglong4>(), tb,

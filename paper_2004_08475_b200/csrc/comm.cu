@@ -199,6 +199,18 @@ amrx_status amrx_comm_init(int ndev, const int *devices, amrx_comm **out)
   });
 }
 
+amrx_status amrx_device_count(int *n)
+{
+  return guarded_comm([&] {
+    if (!n) fail(AMRX_ERR_INVALID_ARG, "null argument");
+    *n = 0;
+    if (cudaGetDeviceCount(n) != cudaSuccess) {
+      cudaGetLastError();
+      *n = 0;
+    }
+  });
+}
+
 amrx_status amrx_comm_destroy(amrx_comm *comm)
 {
   return guarded_comm([&] {

@@ -61,20 +61,17 @@ enum : int32_t { kOccNone = 0, kOccDense = 1, kOccHash = 2 };
     in one load and the extraction's fast path reads 16 bytes.  The table has at least
     three entries per occupied record bucket; the build reports the longest
     probe (in table buckets). */
-__host__ __device__ inline uint64_t mix64(uint64_t x)
-{
-  x ^= x >> 31;
-  x *= 0x7fb5d329728ea185ull;
-  x ^= x >> 27;
-  x *= 0x81dadef4bc2dd44dull;
-  x ^= x >> 33;
-  return x;
-}
-
-/// home table bucket of record bucket b (mask = table buckets - 1)
+/// home table bucket of record bucket b (mask = table buckets - 1, at most
+/// 2^32 buckets): a 32-bit multiply-xorshift hash of the pair id, cheap in
+/// the lookup loops (a 64-bit multiply is four IMADs)
 __host__ __device__ inline uint64_t hash_home(uint64_t bucket, uint64_t mask)
 {
-  return mix64(bucket >> 1) & mask;
+  const uint64_t p = bucket >> 1;
+  uint32_t x = uint32_t(p) * 0x9E3779B1u ^ uint32_t(p >> 32) * 0x85EBCA77u;
+  x ^= x >> 15;
+  x *= 0x2C1B3C6Du;
+  x ^= x >> 12;
+  return uint64_t(x) & mask;
 }
 
 __host__ __device__ inline int64_t anchor_mask(int64_t x, int32_t level)

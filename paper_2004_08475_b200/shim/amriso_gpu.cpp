@@ -34,9 +34,11 @@
 #include "amrx.h"
 
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -82,6 +84,140 @@ void upload(const CellIndex &index, IndexHandle &h)
                           index.data.scalars.size(), &opts, &h.p));
 }
 
+/*! Device indexes kept alive between calls, so the reference's CLI flow
+    build_index -> validate_dataset -> extract_isosurface -> extract_dual_mesh
+    (proj/src/cli.cpp:76-118) ingests once.  A CellIndex is immutable after
+    build_index, so an entry is keyed on its arrays' addresses
+    and size plus a fingerprint of 4096 evenly spaced records and scalars;
+    the two most recent datasets are kept. */
+struct IndexCache {
+  struct Entry {
+    const void *cells = nullptr, *scalars = nullptr;
+    size_t n = 0;
+    uint64_t fp = 0;
+    std::shared_ptr<IndexHandle> h;
+  };
+  std::mutex mu;
+  Entry e[2];
+
+  static uint64_t fingerprint(const CellIndex &ix)
+  {
+    const size_t n = ix.data.cells.size();
+    uint64_t f = 0x9e3779b97f4a7c15ull ^ n;
+    const auto mix = [&](uint64_t v) {
+      f ^= v + 0x9e3779b97f4a7c15ull + (f << 6) + (f >> 2);
+    };
+    const size_t step = n > 4096 ? n / 4096 : 1;
+    for (size_t i = 0; i < n; i += step) {
+      const CellCoord &c = ix.data.cells[i];
+      uint64_t s;
+      std::memcpy(&s, &ix.data.scalars[i], 8);
+      mix(uint64_t(uint32_t(c.i)) | uint64_t(uint32_t(c.j)) << 32);
+      mix(uint64_t(uint32_t(c.k)) | uint64_t(uint32_t(c.level)) << 32);
+      mix(s);
+    }
+    if (n) {
+      uint64_t s;
+      std::memcpy(&s, &ix.data.scalars[n - 1], 8);
+      mix(s ^ uint64_t(uint32_t(ix.data.cells[n - 1].k)));
+    }
+    return f;
+  }
+
+  /// the device index of `ix`, from the cache or uploaded (presorted)
+  std::shared_ptr<IndexHandle> get(const CellIndex &ix)
+  {
+    const uint64_t fp = fingerprint(ix);
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      for (Entry &x : e)
+        if (x.h && x.cells == ix.data.cells.data() && x.scalars == ix.data.scalars.data() &&
+            x.n == ix.data.cells.size() && x.fp == fp)
+          return x.h;
+    }
+    auto h = std::make_shared<IndexHandle>();
+    upload(ix, *h);
+    put(ix, fp, h);
+    return h;
+  }
+
+  void put(const CellIndex &ix, uint64_t fp, std::shared_ptr<IndexHandle> h)
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    e[1] = std::move(e[0]);
+    e[0] = Entry{ix.data.cells.data(), ix.data.scalars.data(), ix.data.cells.size(), fp,
+                 std::move(h)};
+  }
+};
+
+IndexCache &index_cache()
+{
+  static IndexCache c;
+  return c;
+}
+
+/*! every GPU of the box (or AMRISO_GPUS of them, like the reference's
+    AMRISO_THREADS): with more than one, extract_isosurface and
+    extract_dual_mesh run through one amrx_comm (NCCL broadcast of the
+    sorted index, each GPU its share of the cells, parts concatenated in
+    candidate order) */
+struct MultiGpu {
+  std::mutex mu;
+  amrx_comm *comm = nullptr;
+  int gpus = -1;
+  // the last dataset's replicated index (same key as IndexCache)
+  const void *cells = nullptr, *scalars = nullptr;
+  size_t n = 0;
+  uint64_t fp = 0;
+  amrx_comm_index *index = nullptr;
+
+  ~MultiGpu()
+  {
+    if (index) amrx_comm_index_destroy(index);
+    if (comm) amrx_comm_destroy(comm);
+  }
+
+  int count()
+  {
+    if (gpus < 0) {
+      int n = 1;
+      if (amrx_device_count(&n) != AMRX_OK) n = 1;
+      if (const char *e = std::getenv("AMRISO_GPUS")) {
+        const int want = std::atoi(e);
+        if (want > 0 && want < n) n = want;
+      }
+      gpus = n;
+    }
+    return gpus;
+  }
+
+  /// the replicated index of `ix` over all GPUs (mu held)
+  amrx_comm_index *get(const CellIndex &ix)
+  {
+    if (!comm) check(amrx_comm_init(count(), nullptr, &comm));
+    const uint64_t f = IndexCache::fingerprint(ix);
+    if (index && cells == ix.data.cells.data() && scalars == ix.data.scalars.data() &&
+        n == ix.data.cells.size() && fp == f)
+      return index;
+    if (index) amrx_comm_index_destroy(index);
+    index = nullptr;
+    check(amrx_comm_index_create(comm, reinterpret_cast<const int32_t *>(ix.data.cells.data()),
+                                 ix.data.scalars.data(), ix.data.cells.size(),
+                                 ix.data.scalars.size(), AMRX_FLAG_PRESORTED, &index));
+    cells = ix.data.cells.data();
+    scalars = ix.data.scalars.data();
+    n = ix.data.cells.size();
+    fp = f;
+    return index;
+  }
+};
+
+MultiGpu &multi_gpu()
+{
+  static MultiGpu m;
+  return m;
+}
+
 using Clock = std::chrono::steady_clock;
 
 double seconds_since(Clock::time_point t)
@@ -114,18 +250,23 @@ CellIndex host_index(IndexHandle &h)
 
 CellIndex build_index(std::vector<CellCoord> cells, std::vector<double> scalars)
 {
-  IndexHandle h;
+  auto h = std::make_shared<IndexHandle>();
   check(amrx_index_create(reinterpret_cast<const int32_t *>(cells.data()),
                           scalars.data(), cells.size(), scalars.size(), nullptr,
-                          &h.p));
-  return host_index(h);
+                          &h->p));
+  CellIndex index = host_index(*h);
+  // the returned CellIndex keeps these arrays (moved out, same addresses)
+  index_cache().put(index, IndexCache::fingerprint(index), std::move(h));
+  return index;
 }
 
 CellIndex read_amr(const std::filesystem::path &path)
 {
-  IndexHandle h;
-  check(amrx_read_amr(path.c_str(), nullptr, &h.p));
-  return host_index(h);
+  auto h = std::make_shared<IndexHandle>();
+  check(amrx_read_amr(path.c_str(), nullptr, &h->p));
+  CellIndex index = host_index(*h);
+  index_cache().put(index, IndexCache::fingerprint(index), std::move(h));
+  return index;
 }
 
 static_assert(sizeof(vec3d) == 24, "vec3d must be 3 x f64");
@@ -161,16 +302,29 @@ std::vector<DualCell> extract_dual_mesh(const CellIndex &index, int)
 {
   if (index.size() == 0)
     throw std::invalid_argument("extract_dual_mesh: empty dataset");
-  IndexHandle h;
-  upload(index, h);
   uint64_t count = 0;
   amrx_stats st;
-  check(amrx_extract_dual(h.p, nullptr, nullptr, nullptr, 0, &count, &st));
-  std::vector<uint32_t> corners(count * 8);
-  std::vector<uint64_t> tasks(count);
-  if (count)
-    check(amrx_extract_dual(h.p, nullptr, corners.data(), tasks.data(), count,
-                            &count, &st));
+  std::vector<uint32_t> corners;
+  std::vector<uint64_t> tasks;
+  MultiGpu &mg = multi_gpu();
+  if (mg.count() > 1) {
+    std::lock_guard<std::mutex> lock(mg.mu);
+    amrx_comm_index *m = mg.get(index);
+    check(amrx_comm_extract_dual(m, nullptr, nullptr, 0, &count, &st));
+    corners.resize(count * 8);
+    tasks.resize(count);
+    if (count)
+      check(amrx_comm_extract_dual(m, corners.data(), tasks.data(), count, &count, &st));
+  } else {
+    const auto hp = index_cache().get(index);
+    IndexHandle &h = *hp;
+    check(amrx_extract_dual(h.p, nullptr, nullptr, nullptr, 0, &count, &st));
+    corners.resize(count * 8);
+    tasks.resize(count);
+    if (count)
+      check(amrx_extract_dual(h.p, nullptr, corners.data(), tasks.data(), count,
+                              &count, &st));
+  }
   std::vector<DualCell> duals(count);
   for (uint64_t n = 0; n < count; n++) {
     DualCell &d = duals[n];
@@ -189,20 +343,29 @@ ExtractionResult extract_isosurface(const CellIndex &index, const IsoParams &par
 {
   if (index.size() == 0)
     throw std::invalid_argument("extract_isosurface: empty dataset");
-  IndexHandle h;
-  upload(index, h);
-
   ExtractionResult result;
   ExtractionStats &stats = result.stats;
   amrx_iso_params p{params.iso, 0, 1};
   uint64_t count = 0;
   amrx_stats st;
+  std::vector<FatTriangle> fat;
   // count, then emit into the caller-side soup (kept on the device between
   // the two calls, so the kernels run once)
-  check(amrx_extract_iso(h.p, nullptr, &p, nullptr, 0, &count, &st));
-  std::vector<FatTriangle> fat(count);
-  if (count)
-    check(amrx_extract_iso(h.p, nullptr, &p, fat.data(), count, &count, &st));
+  MultiGpu &mg = multi_gpu();
+  if (mg.count() > 1) {
+    std::lock_guard<std::mutex> lock(mg.mu);
+    amrx_comm_index *m = mg.get(index);
+    check(amrx_comm_extract_iso(m, &p, nullptr, 0, &count, &st));
+    fat.resize(count);
+    if (count) check(amrx_comm_extract_iso(m, &p, fat.data(), count, &count, &st));
+  } else {
+    const auto hp = index_cache().get(index);
+    IndexHandle &h = *hp;
+    check(amrx_extract_iso(h.p, nullptr, &p, nullptr, 0, &count, &st));
+    fat.resize(count);
+    if (count)
+      check(amrx_extract_iso(h.p, nullptr, &p, fat.data(), count, &count, &st));
+  }
 
   stats.cell_count = st.cell_count;
   stats.duals_accepted = st.duals_accepted;
@@ -228,8 +391,8 @@ ValidationReport validate_dataset(const CellIndex &index)
 {
   ValidationReport report;
   if (index.size() == 0) return report;
-  IndexHandle h;
-  upload(index, h);
+  const auto hp = index_cache().get(index);
+  IndexHandle &h = *hp;
   uint64_t nd = 0, no = 0;
   check(amrx_validate(h.p, nullptr, 0, &nd, nullptr, 0, &no));
   std::vector<uint32_t> dup(2 * nd), ovl(2 * no);
