@@ -95,6 +95,7 @@ typedef struct amrx_index_opts {
 #define AMRX_LOOKUP_DIRECTORY 0
 #define AMRX_LOOKUP_RECORDS 1
 #define AMRX_LOOKUP_HASH 2
+#define AMRX_LOOKUP_WIDE 3  /* > 64-bit keys: exact-key table, per-level probes */
 
 typedef struct amrx_index_info {
   uint64_t cell_count;
@@ -103,7 +104,7 @@ typedef struct amrx_index_info {
   int32_t levels[31];       /* distinct levels present, finest first */
   int64_t bounds_lo[3];     /* hull of all cell boxes (locator.cpp:70-83) */
   int64_t bounds_hi[3];
-  int32_t key_bits;         /* bits of the packed sort key in use */
+  int32_t key_bits;         /* bits of the packed sort key in use (> 64: two-word keys) */
   int32_t directory_bits;   /* log2 of the lookup structure's entry count */
   uint64_t duplicate_keys;  /* adjacent equal keys after the sort */
   uint64_t device_bytes;    /* HBM held by the index */

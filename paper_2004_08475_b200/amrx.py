@@ -83,7 +83,7 @@ class _IndexInfo(C.Structure):
 
 # index lookup structures (amrx.h AMRX_FLAG_LOOKUP_* / AMRX_LOOKUP_*)
 _LOOKUP_FLAGS = {None: 0, "auto": 0, "records": 0x2, "hash": 0x4, "directory": 0x8}
-_LOOKUP_NAMES = {0: "directory", 1: "records", 2: "hash"}
+_LOOKUP_NAMES = {0: "directory", 1: "records", 2: "hash", 3: "wide"}
 
 
 def _flags(presorted=False, lookup=None):

@@ -408,10 +408,6 @@ KeyGeom make_geometry(const int64_t mn[3], const int64_t mx[3],
   }
   g.lbits = bit_width(uint64_t(hi_level - lo_level));
   g.total = g.bits[0] + g.bits[1] + g.bits[2] + g.lbits;
-  if (g.total > 64)
-    fail(AMRX_ERR_UNSUPPORTED,
-         "dataset extent needs a " + std::to_string(g.total) +
-           "-bit cell key; this build packs keys into 64 bits");
   g.sh[2] = g.lbits;
   g.sh[1] = g.sh[2] + g.bits[2];
   g.sh[0] = g.sh[1] + g.bits[1];
@@ -419,6 +415,12 @@ KeyGeom make_geometry(const int64_t mn[3], const int64_t mx[3],
   g.nlevels = 0;
   for (int l = 0; l <= kMaxLevel; l++)
     if ((level_mask >> l) & 1u) g.levels[g.nlevels++] = int8_t(l);
+  if (g.total > 64) {
+    // two-word keys (wide.cuh): an exact-key table, per-level probes
+    g.wide = 1;
+    g.occ = kOccNone;
+    return g;
+  }
   const uint32_t force = flags & (AMRX_FLAG_LOOKUP_RECORDS | AMRX_FLAG_LOOKUP_HASH |
                                   AMRX_FLAG_LOOKUP_DIRECTORY);
   if (force & (force - 1))
@@ -468,10 +470,12 @@ void finish_info(amrx_index *ix, uint64_t equal_pairs, double ms)
     in.bounds_hi[a] = ix->bounds_hi[a];
   }
   in.key_bits = ix->g.total;
-  in.lookup = ix->g.occ == kOccDense  ? AMRX_LOOKUP_RECORDS
+  in.lookup = ix->g.wide ? AMRX_LOOKUP_WIDE
+              : ix->g.occ == kOccDense  ? AMRX_LOOKUP_RECORDS
               : ix->g.occ == kOccHash ? AMRX_LOOKUP_HASH
                                       : AMRX_LOOKUP_DIRECTORY;
-  in.directory_bits = ix->g.occ == kOccHash ? bit_width(ix->hmask) : ix->g.dir_bits;
+  in.directory_bits =
+    (ix->g.occ == kOccHash || ix->g.wide) ? bit_width(ix->hmask) : ix->g.dir_bits;
   in.duplicate_keys = equal_pairs;
   in.device_bytes = ix->keys.bytes + ix->scal.bytes + ix->dir.bytes +
                     ix->rec.bytes;
@@ -636,6 +640,12 @@ void check_result(const ExtractResult &r, uint64_t cells, bool tri)
 
 namespace amrx {
 
+/// the extraction over whichever key width the index has
+ExtractResult run_any(amrx_index *index, const ExtractRequest &rq, cudaStream_t st)
+{
+  return index->g.wide ? run_extract_wide(rq, index->wctx(), st) : run_extract(rq, st);
+}
+
 void extract_dual_impl(amrx_index *index, const amrx_range *range, uint32_t *corners8,
                      uint64_t *task_ids, uint64_t cap, uint64_t *count, amrx_stats *stats,
                      bool cached)
@@ -667,7 +677,7 @@ void extract_dual_impl(amrx_index *index, const amrx_range *range, uint32_t *cor
     rq.corners = rq.final_host ? corners8 : corners_w;
     rq.tasks = rq.final_host ? task_ids : tasks_w;
     rq.dual_cap = cap;
-    const ExtractResult r = run_extract(rq, st);
+    const ExtractResult r = run_any(index, rq, st);
     check_result(r, cells, false);
     fill_stats(stats, r, cells);
     *count = r.duals;
@@ -684,7 +694,7 @@ void extract_dual_impl(amrx_index *index, const amrx_range *range, uint32_t *cor
     C.valid = false;
     rq.grow_a = &index->out_a;
     rq.grow_b = &index->out_b;
-    const ExtractResult r = run_extract(rq, st);
+    const ExtractResult r = run_any(index, rq, st);
     check_result(r, cells, false);
     C.valid = true;
     C.kind = 1;
@@ -748,7 +758,7 @@ void extract_iso_impl(amrx_index *index, const amrx_range *range,
     // pinned host output of a large input: small first rounds, each
     // round's download overlapping the next round's extraction
     rq.stream_rounds = rq.final_host && cells >= (uint64_t(1) << 24);
-    const ExtractResult r = run_extract(rq, st);
+    const ExtractResult r = run_any(index, rq, st);
     check_result(r, cells, true);
     fill_stats(stats, r, cells);
     *count = r.tris_written;
@@ -764,7 +774,7 @@ void extract_iso_impl(amrx_index *index, const amrx_range *range,
   if (!hit) {
     C.valid = false;
     rq.grow_a = &index->out_a;
-    const ExtractResult r = run_extract(rq, st);
+    const ExtractResult r = run_any(index, rq, st);
     check_result(r, cells, true);
     C.valid = true;
     C.kind = 2;
@@ -920,6 +930,28 @@ void create_impl(const int32_t *cells4, const double *scalars, uint64_t n_cells,
       for (int a = 0; a < 3; a++) ix->bounds_hi[a] = pre.hi[a];
     }
 
+    if (ix->g.wide) {
+      if (g16 || !search)
+        fail(AMRX_ERR_UNSUPPORTED, "distributed builds need keys of at most 64 bits (this "
+                                   "dataset's extent needs " + std::to_string(ix->g.total) + ")");
+      if (sc_ready) AMRX_CUDA(cudaStreamWaitEvent(st, sc_ready, 0));
+      ix->keys.reserve(n * 16 + 256, st);
+      ix->scal.reserve(n * sizeof(double), st);
+      const WideBuild wb = wide_build(cells_d, sc_d, n, ix->g, ix->keys.as<ulonglong2>(),
+                                      ix->scal.as<double>(), ix->rec, st);
+      ix->hmask = wb.entries - 1;
+      ix->info.lookup_entries = wb.entries;
+      ix->info.max_probe = wb.max_probe;
+      AMRX_CUDA(cudaEventRecord(e1, st));
+      AMRX_CUDA(cudaStreamSynchronize(st));
+      float ms = 0;
+      AMRX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      finish_info(ix.get(), wb.equal_pairs, ms);
+      *out = ix.release();
+      return;
+    }
     ix->keys.reserve((n + kKeyPad) * sizeof(uint64_t), st);
     // resident scalars travel through the sort as the payload (read in
     // input order by the first pass); arriving scalars need the positions
@@ -1324,6 +1356,8 @@ amrx_status amrx_index_from_keys(const void *keys_dev, const double *scalars_dev
     const int64_t mx[3] = {g16[3], g16[4], g16[5]};
     ix->g = make_geometry(mn, mx, uint32_t(g16[9]), uint64_t(g16[10]), opts ? opts->flags : 0);
     for (int a = 0; a < 3; a++) ix->bounds_hi[a] = g16[6 + a];
+    if (ix->g.wide)
+      fail(AMRX_ERR_UNSUPPORTED, "distributed indexes need keys of at most 64 bits");
     if (ix->g.occ == kOccNone)
       fail(AMRX_ERR_UNSUPPORTED, "a partition index needs occupancy records (dense or "
                                  "hashed), not the directory");
@@ -1419,8 +1453,12 @@ amrx_status amrx_validate(amrx_index *index, uint32_t *dup_pairs, uint64_t dup_c
     cudaStream_t st = index->stream;
     DevOut<uint32_t> dp(dup_pairs, dup_pairs ? 2 * dup_cap : 0, st);
     DevOut<uint32_t> op(overlap_pairs, overlap_pairs ? 2 * overlap_cap : 0, st);
-    run_validate(index->ctx(), index->g, op.ptr, overlap_cap, n_overlap, dp.ptr, dup_cap, n_dup,
-                 st);
+    if (index->g.wide)
+      wide_validate(index->wctx(), index->g, op.ptr, overlap_cap, n_overlap, dp.ptr, dup_cap,
+                    n_dup, st);
+    else
+      run_validate(index->ctx(), index->g, op.ptr, overlap_cap, n_overlap, dp.ptr, dup_cap,
+                   n_dup, st);
     if (dup_pairs && dp.staged && *n_dup)
       AMRX_CUDA(cudaMemcpyAsync(dup_pairs, dp.ptr, std::min(*n_dup, dup_cap) * 8,
                                 cudaMemcpyDeviceToHost, st));
@@ -1516,7 +1554,10 @@ amrx_status amrx_index_download(const amrx_index *cindex, int32_t *cells4,
     cudaStream_t st = index->stream;
     if (cells4) {
       DevOut<int4> o(reinterpret_cast<int4 *>(cells4), index->n, st);
-      unpack_cells(index->keys.as<uint64_t>(), index->n, index->g, o.ptr, st);
+      if (index->g.wide)
+        wide_unpack(index->keys.as<ulonglong2>(), index->n, index->g, o.ptr, st);
+      else
+        unpack_cells(index->keys.as<uint64_t>(), index->n, index->g, o.ptr, st);
       o.finish(st);
       AMRX_CUDA(cudaStreamSynchronize(st));
     }
@@ -1532,6 +1573,8 @@ amrx_status amrx_index_device_arrays(const amrx_index *index, void **keys,
 {
   return guarded([&] {
     if (!index) fail(AMRX_ERR_INVALID_ARG, "null index");
+    if (index->g.wide)
+      fail(AMRX_ERR_UNSUPPORTED, "a two-word-key index has no packed 64-bit key array");
     if (keys) *keys = index->keys.ptr;
     if (scalars) *scalars = index->scal.ptr;
   });
@@ -1541,6 +1584,8 @@ amrx_status amrx_index_geometry(const amrx_index *index, int64_t *g16)
 {
   return guarded([&] {
     if (!index || !g16) fail(AMRX_ERR_INVALID_ARG, "null argument");
+    if (index->g.wide)
+      fail(AMRX_ERR_UNSUPPORTED, "replicated / distributed indexes need keys of at most 64 bits");
     const KeyGeom &g = index->g;
     for (int a = 0; a < 3; a++) {
       g16[a] = g.mn[a];
@@ -1581,6 +1626,8 @@ amrx_status amrx_index_adopt(const void *keys_dev, const double *scalars_dev,
     const int64_t mn[3] = {g16[0], g16[1], g16[2]};
     const int64_t mx[3] = {g16[3], g16[4], g16[5]};
     ix->g = make_geometry(mn, mx, uint32_t(g16[9]), n_cells, opts ? opts->flags : 0);
+    if (ix->g.wide)
+      fail(AMRX_ERR_UNSUPPORTED, "replicated indexes need keys of at most 64 bits");
     for (int a = 0; a < 3; a++) ix->bounds_hi[a] = g16[6 + a];
     cudaEvent_t e0, e1;
     AMRX_CUDA(cudaEventCreate(&e0));
@@ -1619,7 +1666,10 @@ amrx_status amrx_find_exact(amrx_index *index, const int32_t *cells4,
     cudaStream_t st = index->stream;
     DevIn<int4> in(reinterpret_cast<const int4 *>(cells4), n, st);
     DevOut<int64_t> o(out_ids, n, st);
-    run_find_exact(index->ctx(), index->g, in.ptr, n, o.ptr, st);
+    if (index->g.wide)
+      wide_find_exact(index->wctx(), index->g, in.ptr, n, o.ptr, st);
+    else
+      run_find_exact(index->ctx(), index->g, in.ptr, n, o.ptr, st);
     o.finish(st);
     AMRX_CUDA(cudaStreamSynchronize(st));
   });
@@ -1638,7 +1688,10 @@ amrx_status amrx_snap(amrx_index *index, const int64_t *points3,
     DevIn<int64_t> p(points3, 3 * n, st);
     DevIn<int32_t> h(hints, hints ? n : 0, st);
     DevOut<int64_t> o(out_ids, n, st);
-    run_snap(index->ctx(), index->g, p.ptr, h.ptr, hint_all, n, o.ptr, st);
+    if (index->g.wide)
+      wide_snap(index->wctx(), index->g, p.ptr, h.ptr, hint_all, n, o.ptr, st);
+    else
+      run_snap(index->ctx(), index->g, p.ptr, h.ptr, hint_all, n, o.ptr, st);
     o.finish(st);
     AMRX_CUDA(cudaStreamSynchronize(st));
   });
@@ -1657,7 +1710,10 @@ amrx_status amrx_try_build_duals(amrx_index *index, const uint64_t *tasks,
     DevIn<uint64_t> t(tasks, n, st);
     DevOut<uint8_t> r(out_reject, n, st);
     DevOut<uint32_t> c(out_corners8, out_corners8 ? 8 * n : 0, st);
-    run_try_build(index->ctx(), index->g, t.ptr, n, r.ptr, c.ptr, st);
+    if (index->g.wide)
+      wide_try_build(index->wctx(), index->g, t.ptr, n, r.ptr, c.ptr, st);
+    else
+      run_try_build(index->ctx(), index->g, t.ptr, n, r.ptr, c.ptr, st);
     r.finish(st);
     c.finish(st);
     AMRX_CUDA(cudaStreamSynchronize(st));

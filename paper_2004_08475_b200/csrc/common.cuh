@@ -40,6 +40,10 @@ struct KeyGeom {
   // in an open-addressed table (sparse or deep key spaces); kOccNone: the
   // bucket directory + binary search (duplicate keys, or forced)
   int32_t occ;
+  // wide = 1: the key needs more than 64 bits (extents spanning most of the
+  // int32 range at a fine level): two-word keys through the wide path
+  // (wide.cu) -- exact-key hashing, per-level probes
+  int32_t wide;
   // packed-space coarsening: when every min anchor is aligned to the
   // coarsest level present (aligned = 1), anchor_mask(p, L) of an in-range
   // point p is its packed key with the low L-shift bits of each coordinate
@@ -118,6 +122,37 @@ struct Cell {
   int64_t i, j, k;
   int32_t level;
 };
+
+// ---------------------------------------------------------------- wide keys
+// A two-word key (lo, hi) = the 128-bit integer with the same field layout
+// as the 64-bit key (KeyGeom::sh, bits, lbits), so its order is again the
+// reference's (i,j,k,level) order (core.hpp:82-88).
+typedef unsigned __int128 u128;
+
+__host__ __device__ inline u128 pack128(const KeyGeom &g, int64_t i, int64_t j, int64_t k,
+                                        int32_t level)
+{
+  u128 key = u128(uint64_t(level - g.shift));
+  if (g.bits[0]) key |= u128(uint64_t((i - g.mn[0]) >> g.shift)) << g.sh[0];
+  if (g.bits[1]) key |= u128(uint64_t((j - g.mn[1]) >> g.shift)) << g.sh[1];
+  if (g.bits[2]) key |= u128(uint64_t((k - g.mn[2]) >> g.shift)) << g.sh[2];
+  return key;
+}
+
+__host__ __device__ inline Cell unpack128(const KeyGeom &g, u128 key)
+{
+  Cell c;
+  c.level = int32_t(uint64_t(key) & ((uint64_t(1) << g.lbits) - 1)) + g.shift;
+  const auto field = [&](int a) -> int64_t {
+    if (!g.bits[a]) return g.mn[a];
+    const uint64_t u = uint64_t(key >> g.sh[a]) & ((uint64_t(1) << g.bits[a]) - 1);
+    return g.mn[a] + int64_t(u << g.shift);
+  };
+  c.i = field(0);
+  c.j = field(1);
+  c.k = field(2);
+  return c;
+}
 
 __host__ __device__ inline Cell unpack(const KeyGeom &g, uint64_t key)
 {

@@ -29,6 +29,7 @@
 // "pass 1 / prefix sum / pass 2" with the search run once.
 #include "internal.h"
 #include "mc_tables.inc"
+#include "wide.cuh"
 
 #include <algorithm>
 #include <atomic>
@@ -308,7 +309,7 @@ __device__ __forceinline__ double centre(int64_t anchor, int level)
     endpoints are runtime corner numbers: they are re-read through it from
     shared memory rather than kept in dynamically indexed arrays, which
     would live in local memory). */
-template <bool F32, typename Corner>
+template <bool F32, bool GAPS = true, typename Corner>
 __device__ __forceinline__ int mc_core(const double *scal, const uint64_t *rows, const Cell &c,
                                        int delta, double iso, void *out, uint64_t at,
                                        uint64_t cap, uint32_t &err, Corner corner)
@@ -379,7 +380,7 @@ __device__ __forceinline__ int mc_core(const double *scal, const uint64_t *rows,
     }
     count++;
   }
-  for (int g = count; g < ntab; g++) {  // mark the slots slivers left unused
+  for (int g = count; GAPS && g < ntab; g++) {  // mark the slots slivers left unused
     const uint64_t slot = at + uint64_t(g);
     if (slot < cap)
       static_cast<uint32_t *>(out)[slot * (F32 ? 9 : 18) + gap_word(F32 ? 9 : 18)] =
@@ -1458,6 +1459,208 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaEventDestroy(e2);
+  return res;
+}
+
+// ------------------------------------------------------- wide-key extraction
+
+namespace {
+
+struct WArgs {
+  WideCtx w;
+  KeyGeom g;
+  const double *scal;
+  uint64_t cell_begin, cell_end;
+  double iso;
+  uint32_t *dual_cnt, *tri_cnt;            // pass 1: per-cell counts
+  const uint64_t *dual_off, *tri_off;      // pass 2: exclusive scans of them
+  uint32_t *corners;
+  uint64_t *tasks;
+  uint64_t dual_cap;
+  void *xyz;
+  uint64_t tri_cap;
+  unsigned long long *out;  // [0..3] counters, [4] duals, [5] tris, [7] errors
+};
+
+/*! the reference's two passes (pipeline.cpp:80-146) for the wide path: one
+    thread per cell runs try_build_dual on its 8 candidates
+    (pipeline.cpp:40-57) and contour_hex on the accepted ones; pass 1
+    (WRITE = false) counts duals and triangles per cell, pass 2 writes them
+    at the scanned offsets -- candidate order by construction */
+template <bool DUAL, bool F32, bool WRITE>
+__global__ void __launch_bounds__(256)
+wide_extract_kernel(const __grid_constant__ WArgs a)
+{
+  __shared__ uint64_t rows[256];
+  if (!DUAL) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) rows[i] = c_mc_rows[table_row(uint32_t(i))];
+    __syncthreads();
+  }
+  unsigned long long cnt[4] = {0, 0, 0, 0}, nd_sum = 0, nt_sum = 0;
+  uint32_t err = 0;
+  const uint64_t cells = a.cell_end - a.cell_begin;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < cells; r += stride) {
+    const uint64_t cell = a.cell_begin + r;
+    const Cell c = unpack128(a.g, wide_key(a.w.keys, cell));
+    uint32_t nd = 0, nt = 0;
+    for (int delta = 0; delta < 8; delta++) {
+      uint32_t ids[8];
+      uint8_t lev[8];
+      const uint32_t code = wide_try(a.w, a.g, c, cell, delta, ids, lev);
+      cnt[code]++;
+      if (code) continue;
+      if (DUAL) {
+        if (WRITE) {
+          const uint64_t slot = a.dual_off[r] + nd;
+          if (slot < a.dual_cap) {
+            for (int d = 0; d < 8; d++) a.corners[slot * 8 + d] = ids[d];
+            if (a.tasks) a.tasks[slot] = cell * 8 + uint64_t(delta);
+          }
+        }
+        nd++;
+      } else {
+        const uint64_t at = WRITE ? a.tri_off[r] + nt : 0;
+        nt += uint32_t(mc_core<F32, false>(a.scal, rows, c, delta, a.iso,
+                                           WRITE ? a.xyz : nullptr, at, WRITE ? a.tri_cap : 0,
+                                           err, [&](int d) { return make_uint2(ids[d], lev[d]); }));
+      }
+    }
+    if (!WRITE) {
+      if (DUAL)
+        a.dual_cnt[r] = nd;
+      else
+        a.tri_cnt[r] = nt;
+    }
+    nd_sum += nd;
+    nt_sum += nt;
+  }
+  if (WRITE) return;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    for (int i = 0; i < 4; i++) cnt[i] += __shfl_xor_sync(kFull, cnt[i], off);
+    nd_sum += __shfl_xor_sync(kFull, nd_sum, off);
+    nt_sum += __shfl_xor_sync(kFull, nt_sum, off);
+  }
+  err = __reduce_or_sync(kFull, err);
+  if ((threadIdx.x & 31) == 0) {
+    for (int i = 0; i < 4; i++)
+      if (cnt[i]) atomicAdd(a.out + i, cnt[i]);
+    if (nd_sum) atomicAdd(a.out + 4, nd_sum);
+    if (nt_sum) {
+      atomicAdd(a.out + 5, nt_sum);
+      atomicAdd(a.out + 6, nt_sum);
+    }
+    if (err) atomicOr(a.out + 7, (unsigned long long)err);
+  }
+}
+
+template <bool DUAL, bool F32, bool WRITE>
+void launch_wide(const WArgs &a, cudaStream_t st)
+{
+  const uint64_t cells = a.cell_end - a.cell_begin;
+  const int grid = int(std::max<uint64_t>(
+    1, std::min<uint64_t>((cells + 255) / 256, uint64_t(device_sm_count()) * 8)));
+  wide_extract_kernel<DUAL, F32, WRITE><<<grid, 256, 0, st>>>(a);
+  AMRX_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+ExtractResult run_extract_wide(const ExtractRequest &r, const WideCtx &w, cudaStream_t st)
+{
+  ExtractResult res{};
+  const uint64_t cells = r.cell_end > r.cell_begin ? r.cell_end - r.cell_begin : 0;
+  const bool D = r.emit_dual, F = r.tri_f32;
+  DevBuf ctl, cnt, off, scratch, tmp_a, tmp_b;
+  ctl.reserve(256, st);
+  AMRX_CUDA(cudaMemsetAsync(ctl.ptr, 0, 256, st));
+  cnt.reserve(cells * 4 + 16, st);
+  off.reserve(cells * 8 + 16, st);
+  WArgs a{};
+  a.w = w;
+  a.g = r.g;
+  a.scal = r.scal;
+  a.cell_begin = r.cell_begin;
+  a.cell_end = r.cell_begin + cells;
+  a.iso = r.iso;
+  a.dual_cnt = a.tri_cnt = cnt.as<uint32_t>();
+  a.dual_off = a.tri_off = off.as<uint64_t>();
+  a.out = ctl.as<unsigned long long>();
+  cudaEvent_t e0, e1, e2;
+  AMRX_CUDA(cudaEventCreate(&e0));
+  AMRX_CUDA(cudaEventCreate(&e1));
+  AMRX_CUDA(cudaEventCreate(&e2));
+  AMRX_CUDA(cudaEventRecord(e0, st));
+  if (cells) {
+    if (D) launch_wide<true, false, false>(a, st);
+    else if (F) launch_wide<false, true, false>(a, st);
+    else launch_wide<false, false, false>(a, st);
+    res.launches += 1;
+  }
+  unsigned long long h[8];
+  AMRX_CUDA(cudaMemcpyAsync(h, ctl.ptr, sizeof h, cudaMemcpyDeviceToHost, st));
+  AMRX_CUDA(cudaStreamSynchronize(st));
+  AMRX_CUDA(cudaEventRecord(e1, st));
+  const uint64_t total = D ? h[4] : h[6];
+  const size_t item = D ? 32 : (F ? 36 : 72);
+  if (cells && total) {
+    res.launches += scan_exclusive_u32_u64(cnt.as<uint32_t>(), off.as<uint64_t>(), cells, scratch,
+                                           st);
+    // destination: the growable arena, a device buffer for host output, or
+    // the caller's device buffer (writes past its capacity are skipped)
+    void *dst = D ? static_cast<void *>(r.corners) : r.xyz;
+    uint64_t *dst_tasks = r.tasks;
+    uint64_t cap = D ? r.dual_cap : r.tri_cap;
+    if (r.grow_a) {
+      r.grow_a->reserve(total * item, st);
+      dst = r.grow_a->ptr;
+      if (D) {
+        r.grow_b->reserve(total * 8, st);
+        dst_tasks = r.grow_b->as<uint64_t>();
+      }
+      cap = total;
+    } else if (r.final_host) {
+      cap = std::min(cap, total);
+      tmp_a.reserve(cap * item + 16, st);
+      dst = tmp_a.ptr;
+      if (D && r.tasks) {
+        tmp_b.reserve(cap * 8 + 16, st);
+        dst_tasks = tmp_b.as<uint64_t>();
+      }
+    }
+    if (D) {
+      a.corners = static_cast<uint32_t *>(dst);
+      a.tasks = dst_tasks;
+      a.dual_cap = cap;
+      launch_wide<true, false, true>(a, st);
+    } else {
+      a.xyz = dst;
+      a.tri_cap = cap;
+      if (F) launch_wide<false, true, true>(a, st);
+      else launch_wide<false, false, true>(a, st);
+    }
+    res.launches += 1;
+    if (r.final_host && !r.grow_a && cap) {
+      AMRX_CUDA(cudaMemcpyAsync(D ? static_cast<void *>(r.corners) : r.xyz, dst, cap * item,
+                                cudaMemcpyDeviceToHost, st));
+      if (D && r.tasks)
+        AMRX_CUDA(cudaMemcpyAsync(r.tasks, dst_tasks, cap * 8, cudaMemcpyDeviceToHost, st));
+    }
+  }
+  AMRX_CUDA(cudaEventRecord(e2, st));
+  AMRX_CUDA(cudaStreamSynchronize(st));
+  AMRX_CUDA(cudaEventElapsedTime(&res.ms, e0, e1));
+  AMRX_CUDA(cudaEventElapsedTime(&res.ms2, e1, e2));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  for (int i = 0; i < 4; i++) res.counters[i] = h[i];
+  res.duals = h[4];
+  res.tris_counted = h[5];
+  res.tris_written = h[6];
+  res.error_flags = uint32_t(h[7]);
+  res.rounds = 1;
   return res;
 }
 

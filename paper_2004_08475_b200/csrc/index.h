@@ -8,6 +8,7 @@
 
 #include "amrx.h"
 #include "internal.h"
+#include "wide.cuh"
 
 using namespace amrx;
 
@@ -44,6 +45,18 @@ struct amrx_index {
   } cache;
   DevBuf out_a, out_b;  // arena: corners/xyz, tasks
   std::mutex mu;
+
+  /// the wide-key lookup context (g.wide)
+  WideCtx wctx() const
+  {
+    WideCtx w;
+    w.keys = keys.as<ulonglong2>();
+    w.tab = rec.as<ulonglong4>();
+    w.mask = hmask;
+    w.n = n;
+    w.id_base = 0;
+    return w;
+  }
 
   SearchCtx ctx() const
   {

@@ -265,6 +265,33 @@ struct ExtractResult {
 
 ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st);
 
+// ------------------------------------------------------------- wide.cu
+struct WideCtx;
+/// the extraction for wide (> 64-bit) keys: two counted passes (extract.cu)
+ExtractResult run_extract_wide(const ExtractRequest &r, const WideCtx &w, cudaStream_t st);
+
+struct WideBuild {
+  uint64_t equal_pairs;  // adjacent equal keys
+  uint64_t entries;      // exact-key table entries
+  uint32_t max_probe;
+  int passes;            // radix passes run
+};
+/// build_index for wide keys: pack, two stable radix sorts (lo, then hi
+/// word), keys + scalars in sorted order, the exact-key table (synchronises)
+WideBuild wide_build(const int4 *cells, const double *scal, uint64_t n, const KeyGeom &g,
+                     ulonglong2 *keys, double *scal_out, DevBuf &table, cudaStream_t st);
+void wide_unpack(const ulonglong2 *keys, uint64_t n, const KeyGeom &g, int4 *cells,
+                 cudaStream_t st);
+void wide_find_exact(const WideCtx &w, const KeyGeom &g, const int4 *cells, uint64_t n,
+                     int64_t *out, cudaStream_t st);
+void wide_snap(const WideCtx &w, const KeyGeom &g, const int64_t *points, const int32_t *hints,
+               int32_t hint_all, uint64_t n, int64_t *out, cudaStream_t st);
+void wide_try_build(const WideCtx &w, const KeyGeom &g, const uint64_t *tasks, uint64_t n,
+                    uint8_t *reject, uint32_t *corners, cudaStream_t st);
+void wide_validate(const WideCtx &w, const KeyGeom &g, uint32_t *ovl_pairs, uint64_t ovl_cap,
+                   uint64_t *n_ovl, uint32_t *dup_pairs, uint64_t dup_cap, uint64_t *n_dup,
+                   cudaStream_t st);
+
 /// amrx_debug_round_limit: cap on every round's staging items (0 = default)
 extern std::atomic<uint64_t> g_round_limit;
 

@@ -21,7 +21,6 @@ oracle standing in for the GPU extractor (tests/test_dist.py).
 """
 from __future__ import annotations
 
-import ctypes as C
 from dataclasses import dataclass
 
 import numpy as np
@@ -45,9 +44,9 @@ def allgather_counts(local: int, group=None, device=None):
     import torch.distributed as dist
     world = dist.get_world_size(group)
     t = torch.tensor([int(local)], dtype=torch.int64, device=device)
-    out = [torch.zeros_like(t) for _ in range(world)]
-    dist.all_gather(out, t, group=group)
-    return [int(x.item()) for x in out]
+    out = torch.empty(world, dtype=torch.int64, device=device)
+    dist.all_gather_into_tensor(out, t, group=group)
+    return out.tolist()  # one host sync
 
 
 @dataclass
@@ -102,10 +101,8 @@ def choose_splitters(samples, world):
     s_0 = 0 and s_world = 2^63.  Negative samples (an empty slice's
     placeholders) are ignored, so empty slices do not pull splitters down."""
     import torch
-    smp = samples.reshape(-1)
-    smp = torch.sort(smp[smp >= 0]).values
-    if len(smp) == 0:
-        smp = torch.zeros(1, dtype=samples.dtype, device=samples.device)
+    smp = torch.sort(samples.reshape(-1)).values.tolist()  # one host sync
+    smp = [x for x in smp if x >= 0] or [0]
     cut = [smp[(len(smp) * q) // world] for q in range(1, world)]
     out = [0]
     for c in cut:
@@ -144,7 +141,8 @@ def send_plan(sorted_keys, lo, hi):
     bh = torch.tensor(hi, dtype=sorted_keys.dtype, device=sorted_keys.device)
     a = torch.searchsorted(sorted_keys, bl)
     b = torch.searchsorted(sorted_keys, bh)
-    return a.tolist(), (b - a).tolist()
+    start, count = torch.stack([a, b - a]).tolist()  # one host sync
+    return start, count
 
 
 def global_geometry(bounds10, counts):
@@ -163,12 +161,13 @@ def global_geometry(bounds10, counts):
 
 def owned_split(rkeys, bounds, rank):
     """(keys below the owned range, keys in it) among a rank's received keys"""
+    import torch
     s_r, s_r1 = bounds[rank], bounds[rank + 1]
-    below = int((rkeys < s_r).sum().item())
     inside = rkeys >= s_r
     if s_r1 < (1 << 63):
         inside &= rkeys < s_r1
-    return below, int(inside.sum().item())
+    below, own = torch.stack([(rkeys < s_r).sum(), inside.sum()]).tolist()  # one host sync
+    return below, own
 
 
 def exchange_runs(keys, scal, lo, hi, group=None, device=None):
@@ -200,18 +199,25 @@ class DistributedIndex:
     seconds: dict        # host wall time per phase
 
 
+class _DeviceArray:
+    """a zero-copy view of library-owned device memory for torch
+    (__cuda_array_interface__); `owner` keeps the memory alive"""
+
+    def __init__(self, ptr, n, typestr, owner):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+        self.owner = owner
+
+
 def sorted_arrays(index, device):
-    """torch copies of an index's sorted packed keys (int64) and scalars"""
+    """torch views (no copy) of an index's sorted packed keys (int64) and
+    scalars; valid while `index` is open"""
     import torch
     n = len(index)
     kp, sp = index.device_arrays()
-    keys = torch.empty(n, dtype=torch.int64, device=device)
-    scal = torch.empty(n, dtype=torch.float64, device=device)
-    rt = _cudart()
-    torch.cuda.synchronize(device)
-    if rt.cudaMemcpy(C.c_void_p(keys.data_ptr()), C.c_void_p(kp), n * 8, 3) or \
-            rt.cudaMemcpy(C.c_void_p(scal.data_ptr()), C.c_void_p(sp), n * 8, 3):
-        raise RuntimeError("device copy failed")
+    keys = torch.as_tensor(_DeviceArray(kp, n, "<i8", index), device=device)
+    scal = torch.as_tensor(_DeviceArray(sp, n, "<f8", index), device=device)
     return keys, scal
 
 
@@ -236,9 +242,9 @@ def build_distributed(cells, scalars, group=None, device=None, stream=None, samp
     n_loc = cells.shape[0]
     b = torch.tensor(np.append(P.cell_bounds(cells, device=dev.index, stream=sh), n_loc),
                      dtype=torch.int64, device=dev)
-    everyone = [torch.empty_like(b) for _ in range(world)]
-    dist.all_gather(everyone, b, group=group)
-    allb = torch.stack(everyone).cpu().numpy()
+    allb = torch.empty((world, 11), dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(allb, b, group=group)
+    allb = allb.cpu().numpy()  # the geometry is host input to the sort
     g = global_geometry(allb[:, :10], allb[:, 10])
     n = int(g[10])
     t1 = time.perf_counter()
@@ -247,18 +253,18 @@ def build_distributed(cells, scalars, group=None, device=None, stream=None, samp
     g[10] = n
     if geometry_layout(g)[3] > 63:
         raise P.UnsupportedError("distributed build needs keys of at most 63 bits")
-    keys, scal = sorted_arrays(part, dev)
-    part.close()
+    keys, scal = sorted_arrays(part, dev)  # views: `part` stays open until the exchange
     t2 = time.perf_counter()
     # splitters from evenly spaced samples of every rank's sorted slice
     pos = torch.linspace(0, max(n_loc - 1, 0), samples, device=dev).round().long()
     smp = keys[pos] if n_loc else torch.full((samples,), -1, dtype=torch.int64, device=dev)
-    gathered = [torch.empty_like(smp) for _ in range(world)]
-    dist.all_gather(gathered, smp, group=group)
-    bounds = choose_splitters(torch.cat(gathered), world)
+    gathered = torch.empty(world * samples, dtype=smp.dtype, device=dev)
+    dist.all_gather_into_tensor(gathered, smp.contiguous(), group=group)
+    bounds = choose_splitters(gathered, world)
     lo, hi = halo_ranges(bounds, g)
     rkeys, rscal = exchange_runs(keys, scal, lo, hi, group, dev)
     del keys, scal
+    part.close()
     t3 = time.perf_counter()
     below, own = owned_split(rkeys, bounds, rank)
     owns = allgather_counts(own, group, dev)
@@ -313,18 +319,6 @@ def partitioned_range(owned, extract_range, group=None, device=None):
                              counters)
 
 
-def _cudart():
-    for name in ("libcudart.so.12", "libcudart.so"):
-        try:
-            lib = C.CDLL(name)
-            lib.cudaMemcpy.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]
-            lib.cudaMemcpy.restype = C.c_int
-            return lib
-        except OSError:
-            continue
-    raise OSError("libcudart not found")
-
-
 def replicate_index(cells=None, scalars=None, device=None, group=None, src=0, stream=None):
     """Rank `src` builds the index (pack + radix sort); its sorted keys and
     scalars (16 B/cell) are broadcast over NCCL; the other ranks adopt them
@@ -341,17 +335,15 @@ def replicate_index(cells=None, scalars=None, device=None, group=None, src=0, st
         meta[0] = len(idx)
         meta[1:] = torch.from_numpy(idx.geometry()).to(dev)
     dist.broadcast(meta, src, group=group)
-    n = int(meta[0].item())
-    geometry = meta[1:].cpu().numpy()
-    keys = torch.empty(n, dtype=torch.int64, device=dev)
-    scal = torch.empty(n, dtype=torch.float64, device=dev)
-    if rank == src:
-        kp, sp = idx.device_arrays()
-        rt = _cudart()
-        torch.cuda.synchronize(dev)
-        if rt.cudaMemcpy(keys.data_ptr(), kp, n * 8, 3) or \
-                rt.cudaMemcpy(scal.data_ptr(), sp, n * 8, 3):
-            raise RuntimeError("device copy failed")
+    meta = meta.cpu().numpy()  # one host sync
+    n = int(meta[0])
+    geometry = meta[1:]
+    if rank == src:  # broadcast straight from the index's own arrays (views)
+        keys, scal = sorted_arrays(idx, dev)
+        torch.cuda.synchronize(dev)  # the build ran on the library's stream
+    else:
+        keys = torch.empty(n, dtype=torch.int64, device=dev)
+        scal = torch.empty(n, dtype=torch.float64, device=dev)
     dist.broadcast(keys, src, group=group)
     dist.broadcast(scal, src, group=group)
     torch.cuda.synchronize(dev)

@@ -47,7 +47,7 @@ class LookupProxy:
     def build_index(self, *a, **k):
         k.setdefault("lookup", self.lookup_mode)
         idx = self._P.build_index(*a, **k)
-        if self.lookup_mode and idx.info.duplicate_keys == 0:
+        if self.lookup_mode and idx.info.duplicate_keys == 0 and idx.info.key_bits <= 64:
             assert idx.info.lookup == self.lookup_mode, (idx.info.lookup, self.lookup_mode)
         return idx
 

@@ -100,12 +100,16 @@ def test_level30_cells_span_the_int32_range(P):
     assert r.stats.duals_accepted > 0
 
 
-def test_key_wider_than_64_bits_is_refused(P):
-    """Fine cells spread across the whole int32 range need more than the
-    64-bit packed key holds: the build refuses with AMRX_ERR_UNSUPPORTED and
-    a message instead of producing a wrong index."""
+def test_key_wider_than_64_bits(P):
+    """Fine cells spread across the whole int32 range need a packed key of
+    more than 64 bits (3 x 32 coordinate bits + the level field): the index
+    takes two-word keys (csrc/wide.cuh) and every output equals the
+    restatement bit for bit (locator.cpp:26-50 accepts these inputs)."""
     lim = (1 << 31) - 2
-    c = np.array([[-lim - 1, -lim - 1, -lim - 1, 0], [lim, lim, lim, 0], [0, 0, 0, 5]],
-                 np.int32)
-    with pytest.raises(P.UnsupportedError):
-        P.build_index(c, np.zeros(len(c)))
+    c = np.array([[-lim - 1, -lim - 1, -lim - 1, 0], [lim, lim, lim, 0], [0, 0, 0, 5],
+                  [32, 0, 0, 5], [0, 32, 0, 5], [32, 32, 0, 5], [0, 0, 32, 5], [32, 0, 32, 5],
+                  [0, 32, 32, 5], [32, 32, 32, 5], [lim - 1, lim, lim, 0]], np.int32)
+    rng = np.random.default_rng(64)
+    idx, r = same(P, c[rng.permutation(len(c))], rng.normal(size=len(c)), 0.0)
+    assert idx.info.key_bits > 64 and idx.info.lookup == "wide"
+    assert r.stats.duals_accepted >= 1

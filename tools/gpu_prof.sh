@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT
-for cfg in ${CONFIGS:-c4}; do
-AMRX_LIB=$PWD/paper_2004_08475_b200/libamrx_dbg.so AMRX_DEBUG_COUNTERS=1 python tools/profile_extract.py --config $cfg 2>&1 | tail -3
-done
+CFG=${CFG:-c4}
+python tools/profile_extract.py --config $CFG > gpurun_out/prof_plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"extract_kernel|mc_jobs" -c 2 -o gpurun_out/prof_$CFG python tools/profile_extract.py --config $CFG > gpurun_out/ncu_$CFG.log 2>&1; echo ncu rc=$?
