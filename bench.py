@@ -86,7 +86,21 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
+    def snapshot(self):
+        """one sample right after a timed region too short for the 100 ms
+        sampling interval"""
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                                  "--format=csv,noheader,nounits"], capture_output=True,
+                                 text=True, timeout=20).stdout
+            self.lines += [ln.strip() for ln in out.splitlines() if ln.strip()]
+            self.snapshot_only = True
+        except Exception:
+            pass
+
     def summary(self):
+        if not self.lines:
+            self.snapshot()
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
@@ -103,8 +117,11 @@ class ClockSampler:
                     reasons.add(n)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+               "samples": len(sm)}
+        if getattr(self, "snapshot_only", False):
+            out["note"] = "timed region shorter than the 100 ms sampling interval: one sample taken right after it"
+        return out
 
 
 # ---------------------------------------------------------------- workload
@@ -124,8 +141,8 @@ def make_workload(cfg_name, device):
     cfg = synth.CONFIGS[cfg_name]
     if cfg["kind"] == "bricks":
         b3 = cfg["bricks"]
-        ds = synth.bricks(b3, seed=cfg["seed"], shuffle=cfg["shuffle"], knobs=synth.C4_KNOBS,
-                          holes=synth.body_holes(b3))
+        ds = synth.bricks(b3, seed=cfg["seed"], shuffle=cfg["shuffle"],
+                          knobs=cfg.get("knobs", synth.C4_KNOBS), holes=synth.body_holes(b3))
         return ds.cells, ds.scalars, dict(bricks=list(b3), level_cells=ds.level_cells)
     import torch
     gen = getattr(synth, cfg["kind"])
@@ -330,9 +347,11 @@ def run_amrx(args):
         e1.record(stream)
         torch.cuda.synchronize()
         ms_e2e = max(e0.elapsed_time(e1) / k2, 1000 * (time.perf_counter() - t0) / k2)
+        link = link_times(hcells, hscal, hout[:nt], dev)
         e2e = {"value": duals_full / (ms_e2e / 1000.0), "unit": "dual cells/s",
                "ms_per_step": ms_e2e, "triangles_per_s": nt / (ms_e2e / 1000.0),
-               "h2d_bytes_per_step": int(n * 16 + n * 8), "d2h_bytes_per_step": int(nt * 72)}
+               "h2d_bytes_per_step": int(n * 16 + n * 8), "d2h_bytes_per_step": int(nt * 72),
+               "link": link}
         del hcells, hscal, hout
 
     # the weld (not part of the step: the reference arm excludes it too),
@@ -416,6 +435,33 @@ def run_amrx(args):
         dist.destroy_process_group()
 
 
+def link_times(hcells, hscal, hout, dev):
+    """the host link alone: the e2e step's upload (cells + scalars) and
+    download (the soup) as plain pinned copies, timed with CUDA events --
+    the floor the e2e number is measured against"""
+    import torch
+    dc = torch.empty(hcells.shape, dtype=hcells.dtype, device=dev)
+    ds = torch.empty(hscal.shape, dtype=hscal.dtype, device=dev)
+    do = torch.empty(hout.shape, dtype=hout.dtype, device=dev)
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    dc.copy_(hcells, non_blocking=True)  # warm
+    torch.cuda.synchronize()
+    e[0].record()
+    dc.copy_(hcells, non_blocking=True)
+    ds.copy_(hscal, non_blocking=True)
+    e[1].record()
+    e[2].record()
+    hout.copy_(do, non_blocking=True)
+    e[3].record()
+    torch.cuda.synchronize()
+    up, down = e[0].elapsed_time(e[1]), e[2].elapsed_time(e[3])
+    nb_up = hcells.numel() * hcells.element_size() + hscal.numel() * hscal.element_size()
+    nb_down = hout.numel() * hout.element_size()
+    return {"h2d_ms": up, "d2h_ms": down, "h2d_gbs": nb_up / up / 1e6 if up else None,
+            "d2h_gbs": nb_down / down / 1e6 if down else None,
+            "note": "pinned copies of the step's bytes alone (the host-link floor of e2e)"}
+
+
 # ------------------------------------------------------------ CPU baseline
 def cpu_sample(cells, scal, target):
     """a contiguous sub-box (x slabs) of the workload with ~target cells"""
@@ -431,7 +477,17 @@ def cpu_sample(cells, scal, target):
     return cells[m].cpu().numpy(), scal[m].cpu().numpy(), (lo, hi)
 
 
-def cpu_baseline(cells, scal, iso, args, impl_line=False):
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(cells, scal, iso, args, impl_line=False, t1=True):
     """the reference (oracle/_ref) on a bounded sample; reports dual cells/s
     over build_index (serial sort) + passes 1+2 (all host threads)"""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -477,11 +533,34 @@ def cpu_baseline(cells, scal, iso, args, impl_line=False):
         cores = 1
     R.free(h)
     total = t_build + t_ext
-    return {"value": duals / total, "unit": "dual cells/s", "cores": cores, "kind": kind,
-            "sample": f"{len(hc)} cells (x-slabs [{slab[0]},{slab[1]}) of the workload), "
-                      f"build_index {t_build:.2f} s (serial) + passes 1+2 {t_ext:.2f} s "
-                      f"({cores} threads); weld excluded ({weld})",
-            "triangles_per_s": tris / total, "seconds": total}
+    out = {"value": duals / total, "unit": "dual cells/s", "cores": cores, "kind": kind,
+           "sample": f"{len(hc)} cells (x-slabs [{slab[0]},{slab[1]}) of the workload), "
+                     f"build_index {t_build:.2f} s (serial) + passes 1+2 {t_ext:.2f} s "
+                     f"({cores} threads); weld excluded ({weld})",
+           "triangles_per_s": tris / total, "seconds": total, "cpu_model": cpu_model(),
+           "nproc": os.cpu_count()}
+    if t1 and kind == "reference":
+        # the reference at T=1 (parallel.hpp:33-42 thread count 1) on a
+        # smaller slab of the same workload, ~10 s of CPU
+        hc1, hs1, slab1 = cpu_sample(cells, scal, max(1, args.cpu_sample // 8))
+        tb = time.perf_counter()
+        h1 = R.build(hc1, hs1)
+        tb = time.perf_counter() - tb
+        if dual_only:
+            R.extract_dual(h1, 1)
+            t0 = time.perf_counter()
+            d1 = len(R.extract_dual(h1, 1)["corners"])
+            te = time.perf_counter() - t0
+        else:
+            R.extract_iso(h1, iso, 1)
+            st1 = R.extract_iso(h1, iso, 1)["stats"]
+            te = st1["seconds_pass1"] + st1["seconds_pass2"]
+            d1 = st1["duals_accepted"]
+        R.free(h1)
+        out["t1"] = {"value": d1 / (tb + te), "unit": "dual cells/s", "cores": 1,
+                     "sample": f"{len(hc1)} cells (x-slabs [{slab1[0]},{slab1[1]})), build_index "
+                               f"{tb:.2f} s + passes 1+2 {te:.2f} s (1 thread)"}
+    return out
 
 
 def run_reference(args):
@@ -498,9 +577,9 @@ def run_reference(args):
     vals = []
     cb = None
     for _ in range(args.warmup):
-        cpu_baseline(cells, scal, iso, args)
+        cpu_baseline(cells, scal, iso, args, t1=False)
     for _ in range(args.steps):
-        cb = cpu_baseline(cells, scal, iso, args)
+        cb = cpu_baseline(cells, scal, iso, args, t1=False)
         vals.append(cb["value"])
     v = statistics.median(vals)
     line = {

@@ -17,6 +17,7 @@
 #include <sys/stat.h>
 #include <unistd.h>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -31,11 +32,28 @@ namespace {
 thread_local std::string g_last_error;
 
 
+/// checked builds: any violated device bound of the call is an error
+void check_bounds()
+{
+#if AMRX_CHECKED
+  cudaDeviceSynchronize();
+  const unsigned int w = check_word_extract() | check_word_sort() | check_word_wide() |
+                         check_word_ingest() | check_word_validate() | check_word_weld();
+  if (w) fail(AMRX_ERR_INTERNAL, "checked build: device bounds violated (codes 0x" +
+                                   [&] {
+                                     char b[16];
+                                     std::snprintf(b, sizeof b, "%x", w);
+                                     return std::string(b);
+                                   }() + ", CheckCode in common.cuh)");
+#endif
+}
+
 template <typename Fn>
 amrx_status guarded(Fn &&fn)
 {
   try {
     fn();
+    check_bounds();
     g_last_error.clear();
     return AMRX_OK;
   } catch (const ApiError &e) {
@@ -821,6 +839,7 @@ void create_impl(const int32_t *cells4, const double *scalars, uint64_t n_cells,
                  bool search, amrx_index **out)
 {
   {
+    NvtxRange range("amrx build_index");
     if (!out) fail(AMRX_ERR_INVALID_ARG, "out is null");
     *out = nullptr;
     // locator.cpp:29-36, same order and wording
@@ -898,7 +917,9 @@ void create_impl(const int32_t *cells4, const double *scalars, uint64_t n_cells,
       }
     } aux_guard{aux, sc_ev, kScalChunks};
 
+    nvtxRangePushA("prepass");
     const PrepassResult pre = ingest_prepass(cells_d, n, ix->scratch, st);
+    nvtxRangePop();
     if (pre.first_bad != ~0ull) {
       int4 c;
       AMRX_CUDA(cudaMemcpy(&c, cells_d + pre.first_bad, sizeof c,
@@ -962,6 +983,7 @@ void create_impl(const int32_t *cells4, const double *scalars, uint64_t n_cells,
     auto *digit_hist = static_cast<unsigned int *>(sort_scratch);
     ix->scratch.reserve(16, st);
     auto *order2 = ix->scratch.as<unsigned long long>();
+    nvtxRangePushA("pack + sort");
     ingest_pack(cells_d, n, ix->g, ix->keys.as<uint64_t>(), idx, st, digit_hist,
                 (ix->g.total + kSortRadixBits - 1) / kSortRadixBits, order2);
 
@@ -1021,7 +1043,10 @@ void create_impl(const int32_t *cells4, const double *scalars, uint64_t n_cells,
       }
       scatter_pending = aux != nullptr;
     }
+    nvtxRangePop();
+    nvtxRangePushA("lookup structure");
     finalize_index(ix.get());
+    nvtxRangePop();
     if (scatter_pending) {
       for (int c = 0; c < kScalChunks; c++) {
         AMRX_CUDA(cudaStreamWaitEvent(st, sc_ev[c], 0));
@@ -1486,6 +1511,7 @@ amrx_status amrx_weld(const double *xyz9, uint64_t n_tris, double *verts3, uint6
                       uint32_t *tris3, uint64_t *n_verts, const amrx_index_opts *opts)
 {
   return guarded([&] {
+    NvtxRange nvtx("amrx weld");
     if (!n_verts) fail(AMRX_ERR_INVALID_ARG, "null argument");
     *n_verts = 0;
     if (n_tris == 0) return;

@@ -15,6 +15,43 @@
 namespace amrx {
 
 constexpr int kMaxLevel = 30;  // core.hpp:28
+
+// Checked builds (make CHECK=1 TAG=chk; compute-sanitizer is closed on the
+// GPU pool): a violated bound sets bit `code` of this translation unit's
+// check word and the access is skipped; the C ABI reads every word after
+// each call and fails with AMRX_ERR_INTERNAL.  Free in normal builds.
+#ifndef AMRX_CHECKED
+#define AMRX_CHECKED 0
+#endif
+#if AMRX_CHECKED
+static __device__ unsigned int g_amrx_check;
+#define AMRX_BOUND(cond, code) ((cond) || (atomicOr(&g_amrx_check, 1u << (code)), false))
+#else
+#define AMRX_BOUND(cond, code) true
+#endif
+enum CheckCode : int {
+  kChkKey = 0,     // a sorted-key load past n + padding
+  kChkRecord = 1,  // a dense record outside the built range
+  kChkHash = 2,    // a hash table bucket outside the table
+  kChkStage = 3,   // a staging read/write outside its arena
+  kChkSort = 4,    // a radix scatter outside [0, n)
+  kChkPerm = 5,    // a permutation entry outside [0, n)
+  kChkSmem = 6,    // a stencil point index outside 0..26
+  kChkJob = 7,     // a marching-cubes job outside the job buffer
+};
+
+/// this translation unit's check word, cleared (host; 0 in normal builds)
+static inline unsigned int take_check_word()
+{
+#if AMRX_CHECKED
+  unsigned int w = 0, z = 0;
+  cudaMemcpyFromSymbol(&w, g_amrx_check, sizeof w);
+  cudaMemcpyToSymbol(g_amrx_check, &z, sizeof z);
+  return w;
+#else
+  return 0;
+#endif
+}
 constexpr int kWin = 128;      // keys per warp search window (1 KB of smem)
 constexpr int kKeyPad = 256;   // u64 sentinel padding after the key array
 constexpr uint32_t kFull = 0xffffffffu;
@@ -304,6 +341,7 @@ struct SearchCtx {
   // the records of its key range only: `rec` is offset so rec[b] is still
   // indexed by the global bucket (only in-range buckets are ever read)
   const uint2 *rec;
+  uint64_t rec_lo, rec_cnt;  // the built records: buckets [rec_lo, rec_lo + rec_cnt)
   // hashed occupancy records (KeyGeom::occ == kOccHash), or null: 2^k
   // 32-byte table buckets (two entries each), hmask = 2^k - 1
   const ulonglong4 *htab;
@@ -312,6 +350,49 @@ struct SearchCtx {
   // 0 otherwise): added to every id a query or an extraction reports
   int64_t id_base;
 };
+
+/// debug event counters, one atomic per warp-level event, lane 0 only
+enum DbgEvent {
+  kDbgTiles = 0,   // extraction tiles
+  kDbgFastNeed,    // stencil points the compile-time fast batches were asked for
+  kDbgFastPend,    // of those, left to the runtime loop
+  kDbgRuntime,     // points through the runtime loop (batch_find + finer)
+  kDbgCoarser,     // probe_coarser calls
+  kDbgHashExtra,   // hashed-record probes past the home table bucket
+  kDbgFindCalls, kDbgFindRounds, kDbgNarrow, kDbgFallback, kDbgQueries,
+  kDbgCount
+};
+
+// counters are compiled in only for a diagnostic build (make DBG=1): the
+// atomics otherwise bloat the hot loop past the instruction cache
+#ifndef AMRX_DBG
+#define AMRX_DBG 0
+#endif
+
+__device__ __forceinline__ void dbg_add(const SearchCtx &s, int ev,
+                                        unsigned long long v = 1)
+{
+#if AMRX_DBG
+  if (s.dbg && (threadIdx.x & 31) == 0) atomicAdd(s.dbg + ev, v);
+#endif
+}
+
+/// sum of a per-lane count over the warp (all lanes call it)
+__device__ __forceinline__ void dbg_sum(const SearchCtx &s, int ev, uint32_t v)
+{
+#if AMRX_DBG
+  v = __reduce_add_sync(0xffffffffu, v);
+  if (s.dbg && (threadIdx.x & 31) == 0 && v) atomicAdd(s.dbg + ev, (unsigned long long)v);
+#endif
+}
+
+/// one event of this lane (divergent code)
+__device__ __forceinline__ void dbg_lane(const SearchCtx &s, int ev)
+{
+#if AMRX_DBG
+  if (s.dbg) atomicAdd(s.dbg + ev, 1ull);
+#endif
+}
 
 /*! lookup through an occupancy record r = rec[q >> 5]: the exact key, or
     under FINER the first stored key with q's anchor and a lower level
@@ -338,9 +419,11 @@ __device__ __forceinline__ int64_t occ_resolve(uint64_t q, uint2 r, uint32_t lma
   return -1;
 }
 
-__device__ __forceinline__ uint2 ldg_rec(const uint2 *rec, uint64_t q, int dir_shift)
+__device__ __forceinline__ uint2 ldg_rec(const SearchCtx &s, uint64_t q)
 {
-  return __ldg(rec + (q >> dir_shift));
+  const uint64_t b = q >> s.dir_shift;
+  if (!AMRX_BOUND(b - s.rec_lo < s.rec_cnt, kChkRecord)) return make_uint2(0, 0);
+  return __ldg(s.rec + b);
 }
 
 /// one table bucket (two entries) in a single 256-bit read-only load
@@ -374,6 +457,8 @@ __device__ __forceinline__ uint2 hash_probe(const SearchCtx &s, uint64_t b, uint
     const uint2 r = bucket_match(e, b, more);
     if (!more) return r;
     h = (h + 1) & s.hmask;
+    dbg_lane(s, kDbgHashExtra);
+    if (!AMRX_BOUND(h <= s.hmask, kChkHash)) return make_uint2(0, 0);
     e = ldg_bucket(s.htab + h);
   }
 }
@@ -402,26 +487,6 @@ __device__ __forceinline__ void hash_find(const SearchCtx &s, const uint64_t (&q
     }
 }
 
-/// debug event counters, one atomic per warp-level event, lane 0 only
-enum DbgEvent {
-  kDbgTiles = 0, kDbgColumns, kDbgFindCalls, kDbgFindRounds, kDbgNarrow,
-  kDbgFallback, kDbgCoarser, kDbgMcTab, kDbgQueries, kDbgWinResolved,
-  kDbgCount
-};
-
-// counters are compiled in only for a diagnostic build (make DBG=1): the
-// atomics otherwise bloat the hot loop past the instruction cache
-#ifndef AMRX_DBG
-#define AMRX_DBG 0
-#endif
-
-__device__ __forceinline__ void dbg_add(const SearchCtx &s, int ev,
-                                        unsigned long long v = 1)
-{
-#if AMRX_DBG
-  if (s.dbg && (threadIdx.x & 31) == 0) atomicAdd(s.dbg + ev, v);
-#endif
-}
 
 /*! global-memory path of warp_find for one query: lower_bound over the
     bucket range [lo, hi), then (finer) the run of same-anchor keys before
@@ -457,7 +522,7 @@ __device__ __forceinline__ void occ_find(const SearchCtx &s, const uint64_t (&q)
 {
   uint2 r[K];
 #pragma unroll
-  for (int k = 0; k < K; k++) r[k] = valid[k] ? ldg_rec(s.rec, q[k], s.dir_shift) : make_uint2(0, 0);
+  for (int k = 0; k < K; k++) r[k] = valid[k] ? ldg_rec(s, q[k]) : make_uint2(0, 0);
 #pragma unroll
   for (int k = 0; k < K; k++)
     if (valid[k]) {

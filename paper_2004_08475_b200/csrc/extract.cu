@@ -180,7 +180,8 @@ __global__ void __launch_bounds__(256)
 reorder_tri_kernel(const uint32_t *__restrict__ cnt, const uint32_t *__restrict__ up,
                    const uint64_t *__restrict__ src_off, const uint64_t *__restrict__ dst_off,
                    uint32_t tiles, int words, const uint32_t *__restrict__ src,
-                   uint32_t *__restrict__ dst, uint64_t dst_base, uint64_t dst_cap)
+                   uint32_t *__restrict__ dst, uint64_t dst_base, uint64_t dst_cap,
+                   uint64_t src_n)
 {
   const int lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
@@ -188,6 +189,7 @@ reorder_tri_kernel(const uint32_t *__restrict__ cnt, const uint32_t *__restrict_
     const uint32_t n = cnt[t], u = up[t];
     if (!n) continue;
     const uint64_t so = src_off[t], d0 = dst_base + dst_off[t];
+    if (!AMRX_BOUND(so + u <= src_n && n <= u, kChkStage)) continue;
     if (n == u) {
       const uint64_t keep = d0 >= dst_cap ? 0 : (d0 + n > dst_cap ? dst_cap - d0 : n);
       const uint64_t nw = keep * uint64_t(words);
@@ -220,7 +222,7 @@ reorder_kernel(const uint32_t *__restrict__ cnt, const uint64_t *__restrict__ sr
                const uint64_t *__restrict__ dst_off, uint32_t tiles, int words,
                const uint32_t *__restrict__ src, uint32_t *__restrict__ dst,
                uint64_t dst_base, uint64_t dst_cap, int words2,
-               const uint32_t *__restrict__ src2, uint32_t *__restrict__ dst2)
+               const uint32_t *__restrict__ src2, uint32_t *__restrict__ dst2, uint64_t src_n)
 {
   const int lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
@@ -229,6 +231,7 @@ reorder_kernel(const uint32_t *__restrict__ cnt, const uint64_t *__restrict__ sr
     const uint32_t n = cnt[t];
     if (!n) continue;
     const uint64_t so = src_off[t], d0 = dst_base + dst_off[t];
+    if (!AMRX_BOUND(so + n <= src_n, kChkStage)) continue;
     const uint64_t keep = d0 >= dst_cap ? 0 : (d0 + n > dst_cap ? dst_cap - d0 : n);
     const uint64_t nw = keep * uint64_t(words);
     for (uint64_t w = lane; w < nw; w += 32)
@@ -425,6 +428,7 @@ mc_jobs_kernel(const __grid_constant__ McArgs a)
   unsigned long long wrote_sum = 0;
   for (uint64_t j = uint64_t(blockIdx.x) * kMcThreads + t; j < n;
        j += uint64_t(gridDim.x) * kMcThreads) {
+    if (!AMRX_BOUND(j < a.job_cap, kChkJob)) break;
     const McJob &job = a.jobs[j];
 #pragma unroll
     for (int d = 0; d < 8; d++) {
@@ -465,6 +469,7 @@ __device__ __noinline__ Hit probe_coarser(const KArgs &a, int level, const Stenc
                                           int p, uint32_t cand)
 {
   const KeyGeom &g = a.g;
+  dbg_lane(a.s, kDbgCoarser);
   struct {
     int level;
   } c{level};
@@ -529,6 +534,7 @@ __device__ __forceinline__ void mark_point(Smem &sm, int warp, int lane, const C
                                            Marks &m)
 {
   const uint32_t bit = 1u << p;
+  if (!AMRX_BOUND(p >= 0 && p < 27, kChkSmem)) return;
   if (id < 0)
     m.miss |= bit;
   else if (lev < c.level)
@@ -586,7 +592,7 @@ __device__ __forceinline__ void fast_issue(const KArgs &a, const Stencil &st, ui
   const bool go = ((need & st.inrange) >> P) & 1u;
   if (L == kOccDense) {
     uint2 v = make_uint2(0, 0);
-    if (go) v = ldg_rec(a.s.rec, q, a.s.dir_shift);
+    if (go) v = ldg_rec(a.s, q);
     reinterpret_cast<uint2 &>(r) = v;
   } else {
     uint4 v = make_uint4(0, 0, 0, 0);
@@ -665,6 +671,7 @@ __device__ __forceinline__ void resolve_marks(const KArgs &a, Smem &sm, int warp
   constexpr int K = AMRX_SLOW_K;
   // present levels coarser than the hint: what a miss probes next
   const uint32_t coarser = a.g.level_mask & ~((2u << c.level) - 1);
+  dbg_sum(a.s, kDbgRuntime, __popc(todo));
   while (__any_sync(kFull, todo != 0)) {
     uint64_t q[K];
     bool v[K];
@@ -740,7 +747,8 @@ extract_kernel(const __grid_constant__ KArgs a)
     const bool valid = working && cell_s < a.s.n;
     const uint64_t cell = valid ? cell_s : 0;
     const uint32_t self = uint32_t(cell);
-    const uint64_t kself = valid ? ldg_u64(a.s.keys + cell) : 0;
+    const uint64_t kself =
+      valid && AMRX_BOUND(cell < a.s.n, kChkKey) ? ldg_u64(a.s.keys + cell) : 0;
     const Cell c = unpack(a.g, kself);
     const Stencil st = make_stencil(a.g, kself, c.level);
 
@@ -783,12 +791,15 @@ extract_kernel(const __grid_constant__ KArgs a)
           constexpr int L = LOOKUP == kOccHash ? kOccHash : kOccDense;
           uint32_t pend = 0;
           if (round == 0) {
+            dbg_sum(a.s, kDbgFastNeed, __popc(need & kFast0));
             fast_batch<L, 0, 1, 3, 4, 9, 10, 12>(a, sm, warp, lane, c, st, need, m, pend);
             need &= ~kFast0;
           } else if (__any_sync(kFull, (need & kFast1) != 0)) {
+            dbg_sum(a.s, kDbgFastNeed, __popc(need & kFast1));
             fast_batch<L, 14, 16, 17, 22, 23, 25, 26>(a, sm, warp, lane, c, st, need, m, pend);
             need &= ~kFast1;
           }
+          dbg_sum(a.s, kDbgFastPend, __popc(pend));
           need |= pend;
         }
         resolve_marks<EMIT_TRI>(a, sm, warp, lane, c, st, self, need, m);
@@ -1325,6 +1336,7 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
       AMRX_CUDA(cudaMemcpyAsync(ctl + 8, reset, sizeof reset, cudaMemcpyHostToDevice, st));
     }
     k.tile_limit = limit;
+    NvtxRange nvtx_round("extraction round");
     AMRX_CUDA(cudaEventRecord(e0, st));
     with_variant(D, F, occ, [&](auto l, auto d, auto f) {
       launch_extract<decltype(d)::value, !decltype(d)::value, decltype(f)::value,
@@ -1384,7 +1396,8 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
       }
       reorder_kernel<<<std::max(1, rgrid), 256, 0, st>>>(
         dual_cnt + t0, dual_off + t0, final_off + t0, nt, 8, x.stage_a.as<uint32_t>(), dc,
-        dbase, dcap, dt ? 2 : 0, x.stage_b.as<uint32_t>(), reinterpret_cast<uint32_t *>(dt));
+        dbase, dcap, dt ? 2 : 0, x.stage_b.as<uint32_t>(), reinterpret_cast<uint32_t *>(dt),
+        dual_stage);
       AMRX_LAUNCH_CHECK();
       res.launches += 1;
       if (r.final_host && !grow && dcap) {
@@ -1412,7 +1425,7 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
       }
       reorder_tri_kernel<<<std::max(1, rgrid), 256, 0, st>>>(
         tri_cnt + t0, tri_up + t0, tri_off + t0, final_off + t0, nt, tri_words,
-        x.stage_a.as<uint32_t>(), dx, tbase, tcap);
+        x.stage_a.as<uint32_t>(), dx, tbase, tcap, tri_stage);
       AMRX_LAUNCH_CHECK();
       res.launches += 1;
       if (r.final_host && !grow && tcap) {
@@ -1447,9 +1460,10 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
   if (debug) {
     unsigned long long d[kDbgCount];
     AMRX_CUDA(cudaMemcpy(d, ctl + 18, sizeof d, cudaMemcpyDeviceToHost));
-    const char *names[kDbgCount] = {"tiles", "columns", "find_calls", "find_rounds",
-                                    "narrow_steps", "fallback_queries", "coarser_calls",
-                                    "mc_tab", "queries", "win_resolved"};
+    const char *names[kDbgCount] = {"tiles", "fast_need", "fast_pend", "runtime_points",
+                                    "coarser_calls", "hash_extra_probes", "find_calls",
+                                    "find_rounds", "narrow_steps", "fallback_queries",
+                                    "queries"};
     std::fprintf(stderr, "[amrx dbg]");
     for (int i = 0; i < kDbgCount; i++)
       std::fprintf(stderr, " %s=%llu (%.2f/tile)", names[i], d[i],
@@ -1692,4 +1706,8 @@ void run_try_build(const SearchCtx &s, const KeyGeom &g, const uint64_t *tasks,
   AMRX_LAUNCH_CHECK();
 }
 
+}  // namespace amrx
+
+namespace amrx {
+unsigned int check_word_extract() { return take_check_word(); }
 }  // namespace amrx

@@ -66,6 +66,8 @@ struct amrx_index {
     // popcounts), else the bucket directory (ensure_search_dir switches an
     // index with duplicate keys to it)
     s.rec = g.occ == kOccDense ? rec.as<uint2>() - rec_lo : nullptr;
+    s.rec_lo = rec_lo;
+    s.rec_cnt = g.occ == kOccDense ? info.lookup_entries : 0;
     s.htab = g.occ == kOccHash ? rec.as<ulonglong4>() : nullptr;
     s.hmask = hmask;
     s.dir = g.occ == kOccNone ? dir.as<uint32_t>() : nullptr;

@@ -854,3 +854,7 @@ int scan_exclusive_u32_u64(const uint32_t *in, uint64_t *out, uint64_t n,
 }
 
 }  // namespace amrx
+
+namespace amrx {
+unsigned int check_word_ingest() { return take_check_word(); }
+}  // namespace amrx

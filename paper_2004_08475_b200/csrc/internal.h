@@ -6,6 +6,7 @@
 #include <stdexcept>
 #include <string>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "common.cuh"
 
@@ -19,6 +20,14 @@ struct ApiError : std::runtime_error {
 };
 
 [[noreturn]] inline void fail(int code, const std::string &msg) { throw ApiError(code, msg); }
+
+/// checked builds: the OR of every translation unit's check word, cleared
+unsigned int check_word_extract();
+unsigned int check_word_sort();
+unsigned int check_word_wide();
+unsigned int check_word_ingest();
+unsigned int check_word_validate();
+unsigned int check_word_weld();
 
 /// the thread-local amrx_last_error text (api.cu)
 void set_last_error(const std::string &msg, bool clear);
@@ -34,6 +43,16 @@ void set_last_error(const std::string &msg, bool clear);
   } while (0)
 
 void note_launch();
+
+/// an NVTX range for the duration of a scope (header-only NVTX3: a no-op
+/// unless a profiler injects itself), naming the library's phases in
+/// nsys / ncu timelines
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 /// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
 void ensure_smem_attr(const void *kernel, size_t bytes);

@@ -247,6 +247,7 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
       const uint64_t kk = sm.keys[pos];
       const uint32_t d = uint32_t((kk >> shift) & (kDigits - 1));
       const uint64_t dst = sm.gofs[d] + (pos - sm.bexcl[d]);
+      if (!AMRX_BOUND(dst < n && uint64_t(sm.vals[pos]) < n, kChkSort)) continue;
       keys_out[dst] = kk;
       vals_out[sm.vals[pos]] = V(dst);
     }
@@ -268,6 +269,7 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
           const uint64_t kk = sm.keys[pos];
           const uint32_t d = uint32_t((kk >> shift) & (kDigits - 1));
           const uint64_t dst = sm.gofs[d] + (pos - sm.bexcl[d]);
+          if (!AMRX_BOUND(dst < n, kChkSort)) continue;
           keys_out[dst] = kk;
           gdst[dst] = g[u];
         }
@@ -279,6 +281,7 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
     const uint64_t kk = sm.keys[pos];
     const uint32_t d = uint32_t((kk >> shift) & (kDigits - 1));
     const uint64_t dst = sm.gofs[d] + (pos - sm.bexcl[d]);
+    if (!AMRX_BOUND(dst < n, kChkSort)) continue;
     keys_out[dst] = kk;
     vals_out[dst] = sm.vals[pos];
   }
@@ -419,4 +422,8 @@ bool radix_sort_pairs_u64(uint64_t *keys, const uint64_t *vals_src, uint64_t *va
                              st, passes_run, nullptr, nullptr, nullptr, nullptr, hist_in);
 }
 
+}  // namespace amrx
+
+namespace amrx {
+unsigned int check_word_sort() { return take_check_word(); }
 }  // namespace amrx

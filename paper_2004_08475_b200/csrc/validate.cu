@@ -126,3 +126,7 @@ void run_validate(const SearchCtx &s, const KeyGeom &g, uint32_t *ovl_pairs, uin
 }
 
 }  // namespace amrx
+
+namespace amrx {
+unsigned int check_word_validate() { return take_check_word(); }
+}  // namespace amrx

@@ -339,3 +339,7 @@ uint64_t run_weld(const double *xyz9, uint64_t n_tris, double *verts, uint64_t v
 }
 
 }  // namespace amrx
+
+namespace amrx {
+unsigned int check_word_weld() { return take_check_word(); }
+}  // namespace amrx

@@ -42,7 +42,7 @@ wide_gather_kernel(const uint32_t *__restrict__ perm, const uint64_t *__restrict
 {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-    out[i] = __ldg(in + perm[i]);
+    out[i] = AMRX_BOUND(perm[i] < n, kChkPerm) ? __ldg(in + perm[i]) : 0;
 }
 
 /// keys and scalars in sorted order from the final permutation; acc[0] +=
@@ -57,6 +57,7 @@ wide_finish_kernel(const int4 *__restrict__ cells, const double *__restrict__ sc
   unsigned long long desc = 0, eq = 0, distinct = 0;
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint32_t p = perm[i];
+    if (!AMRX_BOUND(p < n, kChkPerm)) continue;
     const int4 c = cells[p];
     const u128 k = pack128(g, c.x, c.y, c.z, c.w);
     keys[i] = make_ulonglong2(uint64_t(k), uint64_t(k >> 64));
@@ -351,4 +352,8 @@ void wide_validate(const WideCtx &w, const KeyGeom &g, uint32_t *ovl_pairs, uint
   AMRX_CUDA(cudaStreamSynchronize(st));
 }
 
+}  // namespace amrx
+
+namespace amrx {
+unsigned int check_word_wide() { return take_check_word(); }
 }  // namespace amrx

@@ -212,7 +212,8 @@ class _DeviceArray:
 
 def sorted_arrays(index, device):
     """torch views (no copy) of an index's sorted packed keys (int64) and
-    scalars; valid while `index` is open"""
+    scalars; valid only while `index` stays open (close it after the last
+    use of the views)"""
     import torch
     n = len(index)
     kp, sp = index.device_arrays()

@@ -123,6 +123,8 @@ def bricks(bricks3, seed=1, shuffle=True, knobs=None, holes=()):
 # thresholds t0 t1 t2, noise amplitude
 C4_KNOBS = [14, 24.0, 48.0, 1.41, 0.30, 0.08, 0.01, 8.0]
 C4_ISO = 4.0
+# C5: the same field with a narrower level-0 band (t0 0.53): 250M cells
+C5_KNOBS = [14, 24.0, 48.0, 1.41, 0.53, 0.08, 0.01, 8.0]
 
 # "aircraft body": fuselage + wing boxes (finest units), scaled to the domain
 def body_holes(bricks3):
@@ -269,7 +271,7 @@ CONFIGS = {
     "c4": dict(kind="bricks", bricks=(512, 256, 256), seed=1, shuffle=True, iso=None),
     # C5: ~250M-cell mixed-level AMR, dual mesh only
     "c5": dict(kind="bricks", bricks=(384, 192, 192), seed=5, shuffle=False, iso=None,
-               dual_only=True),
+               dual_only=True, knobs=C5_KNOBS),
     # DEEP: a 13-level octree (levels 0..12) refined toward a landing-gear
     # surface (the paper's 13-level NASA landing gear shape class), soup
     # order, iso 0 on the signed distance -- a sparse 47-bit key space

@@ -32,12 +32,12 @@ def emulate(P, D, torch, cells, scal, world, samples=64, lookup=None):
     sl = [(cells[cut[r]:cut[r + 1]], scal[cut[r]:cut[r + 1]]) for r in range(world)]
     allb = np.stack([np.append(P.cell_bounds(c), len(c)) for c, _ in sl])
     g = D.global_geometry(allb[:, :10], allb[:, 10])
-    arrays = []
+    arrays, parts_sorted = [], []
     for c, s in sl:
         part = P.sort_part(c, s, g)
         gg = part.geometry()
-        arrays.append(D.sorted_arrays(part, dev))
-        part.close()
+        arrays.append(D.sorted_arrays(part, dev))  # zero-copy views: keep `part` open
+        parts_sorted.append(part)
     gg[10] = n
     smp = []
     for k, _ in arrays:
@@ -51,6 +51,10 @@ def emulate(P, D, torch, cells, scal, world, samples=64, lookup=None):
         ks = [arrays[q][0][plans[q][0][r]:plans[q][0][r] + plans[q][1][r]] for q in range(world)]
         ss = [arrays[q][1][plans[q][0][r]:plans[q][0][r] + plans[q][1][r]] for q in range(world)]
         recv.append((torch.cat(ks), torch.cat(ss)))
+    torch.cuda.synchronize()
+    del arrays
+    for part in parts_sorted:
+        part.close()
     split = [D.owned_split(rk, bounds, r) for r, (rk, _) in enumerate(recv)]
     owns = [o for _, o in split]
     assert sum(owns) == n

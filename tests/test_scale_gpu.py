@@ -3,17 +3,20 @@
 * C2 (~9.7M cells, block-structured, level jumps up to 4, holes, white
   noise, iso 0.1): FULL bit-exact comparison of the dual mesh, the reject
   counters and the FP64 soup against the reference library itself.
-* C3 (105M-cell 6-level noise octree), C4 (626M-cell soup) and C5 (250M,
-  dual mesh only): the oracle cannot run
-  the whole path in a test's time, so (a) sampled cell ranges of the GPU
-  output are compared bit-for-bit with the C restatement evaluated over the
-  SAME full index (the sorted arrays downloaded from the GPU -- candidates
-  near a range edge see the whole index, exactly like the reference), and
-  (b) size-independent properties hold on the full output: candidate
-  accounting (accepted+missing+finer+lower-key == 8N, pipeline.cpp:106-107),
-  every dual emitted exactly once (distinct canonical corner multisets,
-  acceptance.cpp:260-284), one dual per owner/delta, and the partitioned
-  extraction reassembling the full one."""
+* C3 (105M-cell 6-level noise octree): FULL bit-exact comparison with the
+  reference library too (slow: the reference's serial sort and weld).
+* C3, C4 (626M-cell soup) and C5 (250M, dual mesh only): (a) the ingest
+  loses and invents nothing -- an order-independent hash of the input
+  (cell, scalar) pairs equals that of the sorted arrays, whose keys
+  strictly increase; (b) sampled cell ranges covering >= 1% of the cells,
+  including every 8-way partition boundary, are compared bit-for-bit with
+  the C restatement evaluated over the SAME full index (candidates near a
+  range edge see the whole index, exactly like the reference); (c)
+  size-independent properties hold on the full output: candidate accounting
+  (accepted+missing+finer+lower-key == 8N, pipeline.cpp:106-107), every
+  dual emitted exactly once (distinct canonical corner multisets,
+  acceptance.cpp:260-284), candidate order, and the partitioned extraction
+  reassembling the full one."""
 import numpy as np
 import pytest
 
@@ -83,7 +86,22 @@ def test_synth_generators_match_reference(ref):
     assert (mine.cells == ds.cells).all() and (bits(mine.scalars) == bits(ds.scalars)).all()
 
 
-def _big(P, name):
+def pair_hash(cells, scal):
+    """order-independent hash of (cell, scalar) pairs on the GPU: the
+    wrapping sum of a mixed 64-bit word per pair"""
+    import torch
+    c = cells.to(torch.int64)
+    s = scal.contiguous().view(torch.int64)
+    h = torch.zeros(len(c), dtype=torch.int64, device=c.device)
+    for col, mult in ((c[:, 0], 0x1F3D5B79), (c[:, 1], 0x2545F491), (c[:, 2], 0x3C6EF372),
+                      (c[:, 3], 0x4F1BBCDD), (s, 0x5851F42D)):
+        x = (h ^ col) * mult + 0x632BE59B
+        h = x ^ (x >> 29)
+    return int(h.sum().item())
+
+
+def _big(P, name, keep_input=False):
+    """the configuration's index, the input's pair hash (and the input)"""
     import gc
     import torch
     from paper_2004_08475_b200 import synth
@@ -95,17 +113,32 @@ def _big(P, name):
     cfg = synth.CONFIGS[name]
     if cfg["kind"] == "octree_noise":
         cells, scal = synth.octree_noise(*cfg["args"])
-        idx = P.build_index(cells, scal)
-        del cells, scal
-        torch.cuda.synchronize()
-        return idx
-    b3 = cfg["bricks"]
-    ds = synth.bricks(b3, seed=cfg["seed"], shuffle=cfg["shuffle"], knobs=synth.C4_KNOBS,
-                      holes=synth.body_holes(b3))
-    idx = P.build_index(ds.cells, ds.scalars)
-    del ds
+    else:
+        b3 = cfg["bricks"]
+        ds = synth.bricks(b3, seed=cfg["seed"], shuffle=cfg["shuffle"],
+                          knobs=cfg.get("knobs", synth.C4_KNOBS), holes=synth.body_holes(b3))
+        cells, scal = ds.cells, ds.scalars
+    h_in = pair_hash(cells, scal)
+    idx = P.build_index(cells, scal)
+    inp = (cells.cpu().numpy(), scal.cpu().numpy()) if keep_input else None
+    del cells, scal
     torch.cuda.synchronize()
-    return idx
+    return idx, h_in, inp
+
+
+def _check_ingest(idx, h_in):
+    """nothing lost or invented by the sort, keys strictly increasing"""
+    import torch
+    c = torch.from_numpy(idx.cells).cuda()
+    s = torch.from_numpy(idx.scalars).cuda()
+    assert pair_hash(c, s) == h_in
+    a, b = c[:-1].to(torch.int64), c[1:].to(torch.int64)
+    gt = b[:, 3] > a[:, 3]
+    for k in (2, 1, 0):
+        gt = (b[:, k] > a[:, k]) | ((b[:, k] == a[:, k]) & gt)
+    assert bool(gt.all().item())
+    del c, s, a, b, gt
+    torch.cuda.empty_cache()
 
 
 def _oracle_over(idx):
@@ -141,9 +174,10 @@ def _exactly_once(P, corners):
 @pytest.mark.parametrize("name", ["c3", "c4", "c5"])
 def test_full_scale_properties_and_sampled_parity(P, name):
     import torch
-    idx = _big(P, name)
+    idx, h_in, _ = _big(P, name)
     n = len(idx)
-    assert n > {"c3": 100_000_000, "c4": 600_000_000, "c5": 200_000_000}[name]
+    assert n > {"c3": 100_000_000, "c4": 600_000_000, "c5": 240_000_000}[name]
+    _check_ingest(idx, h_in)
     from paper_2004_08475_b200 import synth
     iso = synth.C4_ISO if synth.CONFIGS[name]["iso"] is None else synth.CONFIGS[name]["iso"]
     if name == "c3":
@@ -164,11 +198,14 @@ def test_full_scale_properties_and_sampled_parity(P, name):
     assert _exactly_once(P, d.corners) == 0
     del corners, tasks, d, t
     torch.cuda.empty_cache()
-    # --- sampled bit-exact parity against the restatement over the same index
+    # --- sampled bit-exact parity against the restatement over the same
+    # index: >= 1% of the cells, every 8-way partition boundary inside a range
     o, h = _oracle_over(idx)
     rng = np.random.default_rng(2026)
-    width = 3000
-    starts = sorted(rng.integers(0, n - width, 6).tolist()) + [0, n - width]
+    width = max(3000, n // 400)
+    starts = [max(0, n * r // 8 - width // 2) for r in range(1, 8)]
+    starts += sorted(rng.integers(0, n - width, 3).tolist()) + [0, n - width]
+    assert len(starts) * width >= n // 100
     for b in starts:
         e = b + width
         gd = P.extract_dual_mesh(idx, cell_range=(b, e))
@@ -191,7 +228,7 @@ def test_c4_partitioned_equals_full(P):
     (the multi-GPU contract), at full scale on one device"""
     import torch
     from paper_2004_08475_b200 import synth
-    idx = _big(P, "c4")
+    idx, _, _ = _big(P, "c4")
     n = len(idx)
     full = P.extract_isosurface(idx, P.IsoParams(iso=synth.C4_ISO))
     total = len(full.fat)
@@ -214,3 +251,34 @@ def test_c4_partitioned_equals_full(P):
     with pytest.raises(P.CapacityError) as e:
         P.extract_isosurface(idx, P.IsoParams(iso=synth.C4_ISO), out=small)
     assert e.value.count == total
+
+
+@pytest.mark.slow
+def test_c3_full_bit_exact_vs_reference(P, ref):
+    """C3 (104.8M cells, 6 levels) end to end against the reference library:
+    the same shuffled input through both build_index, then every dual, the
+    reject counters and the FP64 soup bit for bit ("full on
+    <= 100M")"""
+    from paper_2004_08475_b200 import synth
+    idx, h_in, (cells, scal) = _big(P, "c3", keep_input=True)
+    _check_ingest(idx, h_in)
+    h = ref.build(cells, scal)
+    del cells, scal
+    ds = ref.dataset(h)
+    assert (idx.cells == ds.cells).all() and (bits(idx.scalars) == bits(ds.scalars)).all()
+    del ds
+    d = P.extract_dual_mesh(idx)
+    rd = ref.extract_dual(h, 0)
+    assert d.corners.shape == rd["corners"].shape and (d.corners == rd["corners"]).all()
+    assert (d.owner == rd["owner"]).all()
+    del d, rd
+    iso = synth.CONFIGS["c3"]["iso"]
+    r = P.extract_isosurface(idx, P.IsoParams(iso=iso))
+    ri = ref.extract_iso(h, iso, 0)
+    st = ri["stats"]
+    assert [r.stats.duals_accepted, r.stats.duals_missing_corner, r.stats.duals_finer_corner,
+            r.stats.duals_lower_key_corner] == [st["duals_accepted"], st["duals_missing_corner"],
+                                                st["duals_finer_corner"],
+                                                st["duals_lower_key_corner"]]
+    assert r.fat.shape == ri["fat"].shape and (bits(r.fat) == bits(ri["fat"])).all()
+    ref.free(h)
