@@ -134,29 +134,50 @@ def body_holes(bricks3):
     return [fus, wing]
 
 
-def octree_noise(root=(48, 48, 48), levels=6, seed=3, k=0.45, base=0.02, shuffle=True,
-                 device="cuda"):
-    """C3: a 6-level octree (levels 0..levels-1) over a root grid of
-    coarsest cells, refined toward the zero set of a turbulent-noise field
-    (four octaves of products of sines with random phases), the field at the
-    cell centre as the scalar; optionally shuffled into a soup.  Built with
-    torch on the GPU (no reference counterpart: the reference's own
-    generators are CPU, synth.cpp).  Returns (cells int32[n,4], scalars
-    f64[n]) on `device`."""
-    import math
+def value_noise(p, seed, octaves=5, base=0.02):
+    """fixed-seed fractal value noise at FP64 positions p (n, 3): per octave
+    a lattice of pseudo-random values in [-1, 1) from an integer hash of the
+    lattice point, blended trilinearly with smoothstep weights; octave o has
+    frequency base * 2^o and amplitude 2^-o (hashed-lattice
+    value noise, >= 5 octaves, FP64 evaluation)"""
     import torch
-    g = torch.Generator().manual_seed(seed)
-    ph = (torch.rand((4, 3), generator=g, dtype=torch.float64) * 2 * math.pi).tolist()
+    f = torch.zeros(len(p), dtype=torch.float64, device=p.device)
+    amp, freq = 1.0, base
+    for o in range(octaves):
+        q = p * freq
+        i0 = torch.floor(q)
+        t = q - i0
+        s = t * t * (3.0 - 2.0 * t)
+        i0 = i0.to(torch.int64)
+        v = torch.zeros_like(f)
+        for d in range(8):
+            dx, dy, dz = d & 1, (d >> 1) & 1, (d >> 2) & 1
+            h = ((i0[:, 0] + dx) * 73856093) ^ ((i0[:, 1] + dy) * 19349663) ^ \
+                ((i0[:, 2] + dz) * 83492791) ^ ((seed * 131 + o) * 2654435761)
+            h = h ^ (h >> 13)
+            h = h * 0x5BD1E995
+            h = h ^ (h >> 15)
+            lat = (h & 0xFFFFFF).to(torch.float64) / float(1 << 23) - 1.0
+            w = (s[:, 0] if dx else 1.0 - s[:, 0]) * (s[:, 1] if dy else 1.0 - s[:, 1]) * \
+                (s[:, 2] if dz else 1.0 - s[:, 2])
+            v += w * lat
+        f += amp * v
+        amp *= 0.5
+        freq *= 2.0
+    return f
 
-    def field(c):
-        x, y, z = c[:, 0], c[:, 1], c[:, 2]
-        f = torch.zeros_like(x)
-        for o in range(4):
-            w = base * (2 ** o)
-            f += (0.5 ** o) * torch.sin(w * x + ph[o][0]) * torch.sin(w * y + ph[o][1]) * \
-                torch.sin(w * z + ph[o][2])
-        return f
 
+def octree_noise(root=(48, 48, 48), levels=6, seed=3, k=0.45, base=0.02, shuffle=True,
+                 device="cuda", octaves=5):
+    """C3: a 6-level octree (levels 0..levels-1) over a root grid of
+    coarsest cells, refined toward the zero set of a turbulent field --
+    fixed-seed hashed-lattice value noise, `octaves` octaves (value_noise) --
+    a cell being split while |f(centre)| < k w base; the field at the cell
+    centre is the scalar (iso 0 = its median by symmetry); optionally
+    shuffled into a soup.  Built with torch on the GPU (no reference
+    counterpart: the reference's own generators are CPU, synth.cpp).
+    Returns (cells int32[n,4], scalars f64[n]) on `device`."""
+    import torch
     L = levels - 1
     W = 1 << L
     r = [torch.arange(n, device=device, dtype=torch.int64) * W for n in root]
@@ -166,17 +187,17 @@ def octree_noise(root=(48, 48, 48), levels=6, seed=3, k=0.45, base=0.02, shuffle
     cells, scal = [], []
     while True:
         w = 1 << L
-        f = field(cur.to(torch.float64) + 0.5 * w)
+        f = value_noise(cur.to(torch.float64) + 0.5 * w, seed, octaves, base)
         refine = (f.abs() < k * w * base) if L > 0 else torch.zeros_like(f, dtype=torch.bool)
         keep = ~refine
         cells.append(torch.cat([cur[keep], torch.full((int(keep.sum()), 1), L, device=device,
-                                                      dtype=torch.int64)], 1))
+                                                      dtype=torch.int64)], 1).to(torch.int32))
         scal.append(f[keep])
         if L == 0 or not bool(refine.any()):
             break
         cur = (cur[refine][:, None, :] + off[None] * (w // 2)).reshape(-1, 3)
         L -= 1
-    cells = torch.cat(cells).to(torch.int32)
+    cells = torch.cat(cells)
     scal = torch.cat(scal)
     if shuffle:
         gp = torch.Generator(device=device).manual_seed(seed)
@@ -264,9 +285,10 @@ CONFIGS = {
     "c1": dict(kind="octree_sphere", args=(6, (25.0, 27.5, 30.0), 20.0, 3.2), iso=0.0),
     # C2: random_slot_dataset(mt19937(seed), 23, 4, 0.15), iso 0.1
     "c2": dict(kind="slots", args=(2026, 23, 4, 0.15), iso=0.1),
-    # C3: 104.8M-cell 6-level octree refined toward a turbulent-noise zero
-    # set, the noise as scalar, iso 0 (GPU generator, soup order)
-    "c3": dict(kind="octree_noise", args=(), iso=0.0),
+    # C3: ~100M-cell 6-level octree refined toward the zero set of 5-octave
+    # hashed-lattice value noise, the noise as scalar, iso 0 (its median by
+    # symmetry) (GPU generator, soup order)
+    "c3": dict(kind="octree_noise", args=((48, 48, 48), 6, 3, 0.7), iso=0.0),
     # C4: 626M-cell 4-level soup (bricks 512 x 256 x 256 -> tuned knobs)
     "c4": dict(kind="bricks", bricks=(512, 256, 256), seed=1, shuffle=True, iso=None),
     # C5: ~250M-cell mixed-level AMR, dual mesh only
