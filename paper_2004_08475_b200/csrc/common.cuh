@@ -100,7 +100,7 @@ enum : int32_t { kOccNone = 0, kOccDense = 1, kOccHash = 2 };
     b^1 (the two halves of an aligned 64-value range) share a home, b
     preferring entry b & 1, so neighbouring records of a dense region come
     in one load and the extraction's fast path reads 16 bytes.  The table has at least
-    three entries per occupied record bucket; the build reports the longest
+    twelve entries per occupied record bucket (api.cu); the build reports the longest
     probe (in table buckets). */
 /// home table bucket of record bucket b (mask = table buckets - 1, at most
 /// 2^32 buckets): a 32-bit multiply-xorshift hash of the pair id, cheap in

@@ -712,7 +712,10 @@ template <bool EMIT_DUAL, bool EMIT_TRI, bool F32, int LOOKUP>
 #ifndef AMRX_MINB
 #define AMRX_MINB 4  // CTAs per SM the register budget is sized for (64 regs)
 #endif
-__global__ void __launch_bounds__(kThreads, AMRX_MINB)
+#ifndef AMRX_MINB_HASH
+#define AMRX_MINB_HASH 4
+#endif
+__global__ void __launch_bounds__(kThreads, LOOKUP == kOccHash ? AMRX_MINB_HASH : AMRX_MINB)
 extract_kernel(const __grid_constant__ KArgs a)
 {
   extern __shared__ __align__(16) unsigned char smem_raw[];

@@ -9,6 +9,7 @@
 #include "internal.h"
 
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 namespace amrx {
@@ -94,11 +95,17 @@ __global__ void digit_offsets_kernel(const unsigned int *hist, int passes,
   }
 }
 
+#ifndef AMRX_SORT_WHIST16
+#define AMRX_SORT_WHIST16 1  // C4 ingest 49.9 -> 48.8 ms (u32 counts: more shared-memory traffic)
+#endif
+// per-warp digit counts (<= 32 x items) and their tile prefixes (< tile) fit u16
+using WhistT = std::conditional_t<AMRX_SORT_WHIST16 != 0, uint16_t, uint32_t>;
+
 template <typename V>
 struct PassSmem {
   uint64_t keys[kSortTile];
   V vals[kSortTile];
-  uint32_t whist[kSortWarps][kDigits];  // per-warp counts -> warp offsets
+  WhistT whist[kSortWarps][kDigits];  // per-warp counts -> warp offsets
   uint32_t bexcl[kDigits];              // tile-local digit start
   uint32_t hist[kDigits];               // tile digit counts (early publish)
   uint32_t wsum[kSortWarps];            // block scan: per-warp totals
@@ -170,7 +177,7 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
     if (dig[t] < kDigits) before = sm.whist[warp][dig[t]];
     rank[t] = before + __popc(peers & lt);
     __syncwarp();
-    if (leader && dig[t] < kDigits) sm.whist[warp][dig[t]] = before + __popc(peers);
+    if (leader && dig[t] < kDigits) sm.whist[warp][dig[t]] = WhistT(before + __popc(peers));
     __syncwarp();
   }
   __syncthreads();
@@ -181,7 +188,7 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
     const int d = threadIdx.x;
     for (int w = 0; w < kSortWarps; w++) {
       const uint32_t c = sm.whist[w][d];
-      sm.whist[w][d] = total;
+      sm.whist[w][d] = WhistT(total);
       total += c;
     }
   }
