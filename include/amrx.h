@@ -243,6 +243,27 @@ AMRX_API amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range
                              uint64_t cap, uint64_t *count,
                              amrx_stats *stats);
 
+/* extract_dual_mesh as the reference returns it (pipeline.cpp:160-194):
+ * 64-byte DualCell records (dual.hpp:30-35: 8 corner CellIds, the query base
+ * dual_base_of(owner, delta) as 3 x int64, the owner's level, the owner) in
+ * candidate order, built on the device.  cells64 NULL = count query (the
+ * duals stay on the device for the copy call). */
+AMRX_API amrx_status amrx_extract_dual_cells(amrx_index *index, const amrx_range *range,
+                                             void *cells64, uint64_t cap, uint64_t *count,
+                                             amrx_stats *stats);
+
+/* extract_isosurface as the reference returns it (pipeline.cpp:67-158):
+ * passes 1+2 and the weld (weld.cpp:31-64) on the device, only the indexed
+ * mesh crosses to the caller -- verts3 (3 f64 per vertex, position-sorted
+ * like the reference) and tris3 (3 u32 per triangle, candidate order).  Both
+ * NULL = count query (*n_verts, *n_tris; the mesh stays on the device for
+ * the copy call).  *seconds_weld = host time of the weld.  FP64 only. */
+AMRX_API amrx_status amrx_extract_iso_mesh(amrx_index *index, const amrx_range *range,
+                                           const amrx_iso_params *params, double *verts3,
+                                           uint64_t vcap, uint32_t *tris3, uint64_t tcap,
+                                           uint64_t *n_verts, uint64_t *n_tris,
+                                           double *seconds_weld, amrx_stats *stats);
+
 /* validate_dataset (proj/src/locator.cpp:136-161): duplicate pairs (n,
  * n+1) of equal adjacent cells and overlap pairs (n, coarser cell holding
  * cell n's anchor), 2 x uint32 CellIds each, in the reference's order.

@@ -12,7 +12,7 @@ from .amrx import (  # noqa: F401
     ExtractionStats, InternalError, IsoParams, LoadError, UnsupportedError,
     adopt_index, build_index, cell_bounds, dual_bases, extract_dual_mesh,
     extract_isosurface, find_exact, index_from_keys, kernel_launches, library, snap,
-    debug_round_limit, Comm, CommIndex, device_count,
+    debug_round_limit, Comm, CommIndex, device_count, extract_isosurface_mesh, extract_dual_cells,
     sort_part, try_build_duals, weld, IndexedMesh, validate_dataset, ValidationReport,
     release_cached_memory, read_amr, write_amr,
     write_obj, write_ply, write_dual_mesh,

@@ -151,6 +151,8 @@ def library():
         "amrx_extract_dual": [P, P, P, P, U64, P, P],
         "amrx_extract_iso": [P, P, P, P, U64, P, P],
         "amrx_device_count": [P],
+        "amrx_extract_iso_mesh": [P, P, P, P, U64, P, U64, P, P, P, P],
+        "amrx_extract_dual_cells": [P, P, P, U64, P, P],
         "amrx_comm_init": [C.c_int, P, P],
         "amrx_comm_destroy": [P],
         "amrx_comm_size": [P, P],
@@ -661,6 +663,49 @@ def extract_isosurface(index: CellIndex, params: IsoParams = None, cell_range=No
     if params.emit_dual_mesh:
         res.duals = extract_dual_mesh(index, cell_range=cell_range)
     return res
+
+
+DUAL_CELL = np.dtype([("corners", "<u4", 8), ("base", "<i8", 3), ("level", "<i4"),
+                      ("owner", "<u4")])  # DualCell, dual.hpp:30-35 (64 bytes)
+
+
+def extract_dual_cells(index: CellIndex, cell_range=None):
+    """extract_dual_mesh as the reference returns it (pipeline.cpp:160-194):
+    DualCell records (corners, base, level, owner) built on the device"""
+    lib = index._lib
+    st = _Stats()
+    cnt = C.c_uint64(0)
+    _check(lib.amrx_extract_dual_cells(index.handle, _range(cell_range), None, 0, C.byref(cnt),
+                                       C.byref(st)))
+    out = np.empty(cnt.value, DUAL_CELL)
+    if cnt.value:
+        _check(lib.amrx_extract_dual_cells(index.handle, _range(cell_range), _ptr(out), cnt.value,
+                                           C.byref(cnt), C.byref(st)))
+    return out
+
+
+def extract_isosurface_mesh(index: CellIndex, params: IsoParams = None, cell_range=None):
+    """extract_isosurface as the reference returns it (pipeline.cpp:67-158):
+    passes 1+2 and the weld on the device, only the IndexedMesh crosses to the
+    host (vertices position-sorted, triangles in candidate order); returns
+    (IndexedMesh, ExtractionStats, seconds_weld)"""
+    if params is None:
+        params = IsoParams()
+    elif isinstance(params, (int, float)):
+        params = IsoParams(iso=float(params))
+    lib = index._lib
+    p = _IsoParams(float(params.iso), 0, 1)
+    st = _Stats()
+    nv, nt, tw = C.c_uint64(0), C.c_uint64(0), C.c_double(0)
+    _check(lib.amrx_extract_iso_mesh(index.handle, _range(cell_range), C.byref(p), None, 0, None,
+                                     0, C.byref(nv), C.byref(nt), C.byref(tw), C.byref(st)))
+    verts = np.empty((nv.value, 3), np.float64)
+    tris = np.empty((nt.value, 3), np.uint32)
+    if nv.value or nt.value:
+        _check(lib.amrx_extract_iso_mesh(index.handle, _range(cell_range), C.byref(p),
+                                         _ptr(verts), nv.value, _ptr(tris), nt.value,
+                                         C.byref(nv), C.byref(nt), C.byref(tw), C.byref(st)))
+    return IndexedMesh(verts, tris), ExtractionStats._from(st), tw.value
 
 
 def dual_bases(index: CellIndex, tasks):

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <filesystem>
 #include <fstream>
@@ -677,7 +678,7 @@ void extract_dual_impl(amrx_index *index, const amrx_range *range, uint32_t *cor
 {
   require_searchable(index);
   if (!index || !count) fail(AMRX_ERR_INVALID_ARG, "null argument");
-  std::lock_guard<std::mutex> lock(index->mu);
+  std::lock_guard<std::recursive_mutex> lock(index->mu);
   DeviceGuard dg(index->device);
   cudaStream_t st = index->stream;
   uint64_t b, e;
@@ -749,7 +750,7 @@ void extract_iso_impl(amrx_index *index, const amrx_range *range,
 {
   require_searchable(index);
   if (!index || !count || !params) fail(AMRX_ERR_INVALID_ARG, "null argument");
-  std::lock_guard<std::mutex> lock(index->mu);
+  std::lock_guard<std::recursive_mutex> lock(index->mu);
   DeviceGuard dg(index->device);
   cudaStream_t st = index->stream;
   uint64_t b, e;
@@ -1480,7 +1481,7 @@ amrx_status amrx_validate(amrx_index *index, uint32_t *dup_pairs, uint64_t dup_c
   return guarded([&] {
     require_full(index);
     if (!index || !n_dup || !n_overlap) fail(AMRX_ERR_INVALID_ARG, "null argument");
-    std::lock_guard<std::mutex> lock(index->mu);
+    std::lock_guard<std::recursive_mutex> lock(index->mu);
     DeviceGuard dg(index->device);
     cudaStream_t st = index->stream;
     DevOut<uint32_t> dp(dup_pairs, dup_pairs ? 2 * dup_cap : 0, st);
@@ -1562,6 +1563,8 @@ amrx_status amrx_index_destroy(amrx_index *index)
       index->scratch.release();
       index->out_a.release();
       index->out_b.release();
+      index->mesh_v.release();
+      index->mesh_t.release();
       cudaStreamSynchronize(index->stream);
       if (index->own_stream) cudaStreamDestroy(index->stream);
     }
@@ -1767,6 +1770,85 @@ amrx_status amrx_extract_iso(amrx_index *index, const amrx_range *range,
                              uint64_t cap, uint64_t *count, amrx_stats *stats)
 {
   return guarded([&] { extract_iso_impl(index, range, params, xyz9, cap, count, stats, false); });
+}
+
+amrx_status amrx_extract_dual_cells(amrx_index *index, const amrx_range *range, void *cells64,
+                                    uint64_t cap, uint64_t *count, amrx_stats *stats)
+{
+  return guarded([&] {
+    if (!index || !count) fail(AMRX_ERR_INVALID_ARG, "null argument");
+    std::lock_guard<std::recursive_mutex> lock(index->mu);
+    // the duals (corners + task ids) into the index's device arena
+    extract_dual_impl(index, range, nullptr, nullptr, 0, count, stats, true);
+    if (!cells64) return;  // count query
+    if (*count > cap)
+      fail(AMRX_ERR_CAPACITY, "output capacity " + std::to_string(cap) + " < " +
+                                std::to_string(*count) + " duals");
+    DeviceGuard dg(index->device);
+    cudaStream_t st = index->stream;
+    // converted and copied out in 1 GB chunks (two buffers, the copy of one
+    // overlapping the conversion of the next)
+    constexpr uint64_t kChunk = uint64_t(1) << 24;  // duals per chunk
+    const uint64_t n = *count;
+    DevBuf buf[2];
+    for (uint64_t d0 = 0, k = 0; d0 < n; d0 += kChunk, k++) {
+      const uint64_t m = std::min(kChunk, n - d0);
+      DevBuf &b = buf[k & 1];
+      b.reserve(m * 64, st);
+      dual_cells(index->out_a.as<uint32_t>() + 8 * d0, index->out_b.as<uint64_t>() + d0, m,
+                 index->keys.ptr, index->g, b.ptr, st);
+      AMRX_CUDA(cudaMemcpyAsync(static_cast<char *>(cells64) + d0 * 64, b.ptr, m * 64,
+                                cudaMemcpyDefault, st));
+    }
+    AMRX_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+amrx_status amrx_extract_iso_mesh(amrx_index *index, const amrx_range *range,
+                                  const amrx_iso_params *params, double *verts3, uint64_t vcap,
+                                  uint32_t *tris3, uint64_t tcap, uint64_t *n_verts,
+                                  uint64_t *n_tris, double *seconds_weld, amrx_stats *stats)
+{
+  return guarded([&] {
+    if (!index || !params || !n_verts || !n_tris) fail(AMRX_ERR_INVALID_ARG, "null argument");
+    if (params->xyz_is_f32)
+      fail(AMRX_ERR_INVALID_ARG, "the welded mesh is built from the FP64 soup (xyz_is_f32 = 0)");
+    std::lock_guard<std::recursive_mutex> lock(index->mu);
+    // the soup into the index's device arena (or the cached one)
+    uint64_t count = 0;
+    extract_iso_impl(index, range, params, nullptr, 0, &count, stats, true);
+    DeviceGuard dg(index->device);
+    cudaStream_t st = index->stream;
+    if (!index->mesh_valid) {
+      NvtxRange nvtx("amrx weld (extract_isosurface)");
+      const auto t0 = std::chrono::steady_clock::now();
+      index->mesh_t.reserve(count * 12 + 16, st);
+      index->mesh_v.reserve(count * 72 + 16, st);  // at most 3 vertices per triangle
+      index->mesh_nv = count ? run_weld(index->out_a.as<double>(), count,
+                                        index->mesh_v.as<double>(), 3 * count,
+                                        index->mesh_t.as<uint32_t>(), st)
+                             : 0;
+      AMRX_CUDA(cudaStreamSynchronize(st));
+      index->mesh_weld_s =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      index->mesh_valid = true;
+    }
+    *n_verts = index->mesh_nv;
+    *n_tris = count;
+    if (seconds_weld) *seconds_weld = index->mesh_weld_s;
+    if (!verts3 && !tris3) return;  // count query
+    if ((verts3 && vcap < index->mesh_nv) || (tris3 && tcap < count))
+      fail(AMRX_ERR_CAPACITY, "mesh capacity (" + std::to_string(vcap) + " vertices, " +
+                                std::to_string(tcap) + " triangles) < " +
+                                std::to_string(index->mesh_nv) + " vertices, " +
+                                std::to_string(count) + " triangles");
+    if (verts3 && index->mesh_nv)
+      AMRX_CUDA(cudaMemcpyAsync(verts3, index->mesh_v.ptr, index->mesh_nv * 24,
+                                cudaMemcpyDefault, st));
+    if (tris3 && count)
+      AMRX_CUDA(cudaMemcpyAsync(tris3, index->mesh_t.ptr, count * 12, cudaMemcpyDefault, st));
+    AMRX_CUDA(cudaStreamSynchronize(st));
+  });
 }
 
 }  // extern "C"

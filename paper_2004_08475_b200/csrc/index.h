@@ -44,7 +44,12 @@ struct amrx_index {
     amrx_stats stats{};
   } cache;
   DevBuf out_a, out_b;  // arena: corners/xyz, tasks
-  std::mutex mu;
+  // the welded mesh of the cached soup (amrx_extract_iso_mesh)
+  DevBuf mesh_v, mesh_t;
+  bool mesh_valid = false;
+  uint64_t mesh_nv = 0;
+  double mesh_weld_s = 0;
+  std::recursive_mutex mu;  // extract_iso_mesh holds it across extraction + weld
 
   /// the wide-key lookup context (g.wide)
   WideCtx wctx() const

@@ -616,6 +616,41 @@ __global__ void lower_bound_kernel(const uint64_t *__restrict__ keys, uint64_t n
   if (t < nq) out[t] = global_lower_bound(keys, 0, n, q[t]);
 }
 
+/*! DualCell records (dual.hpp:30-35, 64 bytes: 8 corner CellIds, the
+    query base dual_base_of(owner, delta) (dual.hpp:61-67) as 3 x int64, the
+    owner's level, the owner) from the extraction's corners and task ids */
+template <bool WIDE>
+__global__ void __launch_bounds__(kThreads)
+dual_cells_kernel(const uint32_t *__restrict__ corners, const uint64_t *__restrict__ tasks,
+                  uint64_t n, const void *__restrict__ keys, const KeyGeom g,
+                  uint4 *__restrict__ out)
+{
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t d = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; d < n; d += stride) {
+    const uint64_t t = tasks[d];
+    const uint64_t owner = t >> 3;
+    const int delta = int(t & 7);
+    Cell c;
+    if (WIDE) {
+      const ulonglong2 k = __ldg(static_cast<const ulonglong2 *>(keys) + owner);
+      c = unpack128(g, u128(k.x) | (u128(k.y) << 64));
+    } else {
+      c = unpack(g, ldg_u64(static_cast<const uint64_t *>(keys) + owner));
+    }
+    const int64_t w = int64_t(1) << c.level;
+    const int64_t bx = c.i - ((delta & 1) ? 0 : w), by = c.j - ((delta & 2) ? 0 : w),
+                  bz = c.k - ((delta & 4) ? 0 : w);
+    const uint4 *src = reinterpret_cast<const uint4 *>(corners + 8 * d);
+    uint4 *dst = out + 4 * d;
+    dst[0] = src[0];
+    dst[1] = src[1];
+    dst[2] = make_uint4(uint32_t(bx), uint32_t(uint64_t(bx) >> 32), uint32_t(by),
+                        uint32_t(uint64_t(by) >> 32));
+    dst[3] = make_uint4(uint32_t(bz), uint32_t(uint64_t(bz) >> 32), uint32_t(c.level),
+                        uint32_t(owner));
+  }
+}
+
 /// recursive reduce-then-scan; block sums of each level in a pool buffer
 template <typename T, typename A>
 int scan_exclusive(const T *in, A *out, uint64_t n, cudaStream_t st)
@@ -830,6 +865,19 @@ void lower_bounds(const uint64_t *keys, uint64_t n, const uint64_t *q, int nq, u
   AMRX_CUDA(cudaMemcpyAsync(out, buf.as<uint64_t>() + nq, size_t(nq) * 8, cudaMemcpyDeviceToHost,
                             st));
   AMRX_CUDA(cudaStreamSynchronize(st));
+}
+
+void dual_cells(const uint32_t *corners, const uint64_t *tasks, uint64_t n, const void *keys,
+                const KeyGeom &g, void *out, cudaStream_t st)
+{
+  if (!n) return;
+  if (g.wide)
+    dual_cells_kernel<true><<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(
+      corners, tasks, n, keys, g, static_cast<uint4 *>(out));
+  else
+    dual_cells_kernel<false><<<grid_for(n, kThreads, 4), kThreads, 0, st>>>(
+      corners, tasks, n, keys, g, static_cast<uint4 *>(out));
+  AMRX_LAUNCH_CHECK();
 }
 
 void unpack_cells(const uint64_t *keys, uint64_t n, const KeyGeom &g,

@@ -199,6 +199,10 @@ void build_hash(const uint64_t *keys, uint64_t n, const KeyGeom &g, ulonglong4 *
 void lower_bounds(const uint64_t *keys, uint64_t n, const uint64_t *q, int nq, uint64_t *out,
                   cudaStream_t st);
 
+/// 64-byte DualCell records (dual.hpp:30-35) of n duals into out (device)
+void dual_cells(const uint32_t *corners, const uint64_t *tasks, uint64_t n, const void *keys,
+                const KeyGeom &g, void *out, cudaStream_t st);
+
 /// unpack sorted keys into 4 x int32 cells
 void unpack_cells(const uint64_t *keys, uint64_t n, const KeyGeom &g,
                   int4 *cells, cudaStream_t st);

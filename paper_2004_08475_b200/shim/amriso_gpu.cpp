@@ -33,7 +33,9 @@
 
 #include "amrx.h"
 
+#include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -41,6 +43,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 
 namespace amriso {
 
@@ -302,12 +305,23 @@ std::vector<DualCell> extract_dual_mesh(const CellIndex &index, int)
 {
   if (index.size() == 0)
     throw std::invalid_argument("extract_dual_mesh: empty dataset");
+  static_assert(sizeof(DualCell) == 64, "DualCell must be 8 x u32 + 3 x i64 + i32 + u32");
   uint64_t count = 0;
   amrx_stats st;
+  MultiGpu &mg = multi_gpu();
+  if (mg.count() <= 1) {
+    // the DualCell records are built on the device and land in the vector
+    // with one copy (pipeline.cpp:160-194)
+    const auto hp = index_cache().get(index);
+    IndexHandle &h = *hp;
+    check(amrx_extract_dual_cells(h.p, nullptr, nullptr, 0, &count, &st));
+    std::vector<DualCell> duals(count);
+    if (count) check(amrx_extract_dual_cells(h.p, nullptr, duals.data(), count, &count, &st));
+    return duals;
+  }
   std::vector<uint32_t> corners;
   std::vector<uint64_t> tasks;
-  MultiGpu &mg = multi_gpu();
-  if (mg.count() > 1) {
+  {
     std::lock_guard<std::mutex> lock(mg.mu);
     amrx_comm_index *m = mg.get(index);
     check(amrx_comm_extract_dual(m, nullptr, nullptr, 0, &count, &st));
@@ -315,27 +329,27 @@ std::vector<DualCell> extract_dual_mesh(const CellIndex &index, int)
     tasks.resize(count);
     if (count)
       check(amrx_comm_extract_dual(m, corners.data(), tasks.data(), count, &count, &st));
-  } else {
-    const auto hp = index_cache().get(index);
-    IndexHandle &h = *hp;
-    check(amrx_extract_dual(h.p, nullptr, nullptr, nullptr, 0, &count, &st));
-    corners.resize(count * 8);
-    tasks.resize(count);
-    if (count)
-      check(amrx_extract_dual(h.p, nullptr, corners.data(), tasks.data(), count,
-                              &count, &st));
   }
   std::vector<DualCell> duals(count);
-  for (uint64_t n = 0; n < count; n++) {
-    DualCell &d = duals[n];
-    const uint32_t owner = uint32_t(tasks[n] >> 3);
-    const int delta = int(tasks[n] & 7);
-    const CellCoord &c = index.data.cells[owner];
-    for (int k = 0; k < 8; k++) d.corners[k] = CellId{corners[8 * n + k]};
-    d.base = dual_base_of(c, delta);
-    d.level = c.level;
-    d.owner = CellId{owner};
-  }
+  // DualCell{corners, base, level, owner} from the corner ids and the task
+  // id owner*8+delta (dual_base_of, dual.hpp:61-67), on every host core
+  const auto fill = [&](uint64_t lo, uint64_t hi) {
+    for (uint64_t n = lo; n < hi; n++) {
+      DualCell &d = duals[n];
+      const uint32_t owner = uint32_t(tasks[n] >> 3);
+      const int delta = int(tasks[n] & 7);
+      const CellCoord &c = index.data.cells[owner];
+      for (int k = 0; k < 8; k++) d.corners[k] = CellId{corners[8 * n + k]};
+      d.base = dual_base_of(c, delta);
+      d.level = c.level;
+      d.owner = CellId{owner};
+    }
+  };
+  const unsigned nt = count > (1u << 20) ? std::max(1u, std::thread::hardware_concurrency()) : 1u;
+  std::vector<std::thread> th;
+  for (unsigned t = 1; t < nt; t++) th.emplace_back(fill, count * t / nt, count * (t + 1) / nt);
+  fill(0, count / nt);
+  for (auto &x : th) x.join();
   return duals;
 }
 
@@ -343,28 +357,44 @@ ExtractionResult extract_isosurface(const CellIndex &index, const IsoParams &par
 {
   if (index.size() == 0)
     throw std::invalid_argument("extract_isosurface: empty dataset");
+
   ExtractionResult result;
   ExtractionStats &stats = result.stats;
   amrx_iso_params p{params.iso, 0, 1};
   uint64_t count = 0;
   amrx_stats st;
-  std::vector<FatTriangle> fat;
-  // count, then emit into the caller-side soup (kept on the device between
-  // the two calls, so the kernels run once)
   MultiGpu &mg = multi_gpu();
   if (mg.count() > 1) {
-    std::lock_guard<std::mutex> lock(mg.mu);
-    amrx_comm_index *m = mg.get(index);
-    check(amrx_comm_extract_iso(m, &p, nullptr, 0, &count, &st));
-    fat.resize(count);
-    if (count) check(amrx_comm_extract_iso(m, &p, fat.data(), count, &count, &st));
+    // every GPU extracts its share; the soup meets on the host and is
+    // welded on the first GPU
+    std::vector<FatTriangle> fat;
+    {
+      std::lock_guard<std::mutex> lock(mg.mu);
+      amrx_comm_index *m = mg.get(index);
+      check(amrx_comm_extract_iso(m, &p, nullptr, 0, &count, &st));
+      fat.resize(count);
+      if (count) check(amrx_comm_extract_iso(m, &p, fat.data(), count, &count, &st));
+    }
+    const auto t_weld = Clock::now();
+    result.mesh = weld(fat);
+    stats.seconds_weld = seconds_since(t_weld);
   } else {
+    // passes 1+2 and the weld on the device (pipeline.cpp:67-158): only the
+    // indexed mesh crosses to the host; the soup stays in the index's arena
     const auto hp = index_cache().get(index);
     IndexHandle &h = *hp;
-    check(amrx_extract_iso(h.p, nullptr, &p, nullptr, 0, &count, &st));
-    fat.resize(count);
-    if (count)
-      check(amrx_extract_iso(h.p, nullptr, &p, fat.data(), count, &count, &st));
+    uint64_t nv = 0;
+    double t_weld = 0;
+    check(amrx_extract_iso_mesh(h.p, nullptr, &p, nullptr, 0, nullptr, 0, &nv, &count, &t_weld,
+                                &st));
+    result.mesh.vertices.resize(nv);
+    result.mesh.triangles.resize(count);
+    if (nv || count)
+      check(amrx_extract_iso_mesh(
+        h.p, nullptr, &p, nv ? &result.mesh.vertices[0].x : nullptr, nv,
+        count ? result.mesh.triangles.data()->data() : nullptr, count, &nv, &count, &t_weld,
+        &st));
+    stats.seconds_weld = t_weld;
   }
 
   stats.cell_count = st.cell_count;
@@ -376,10 +406,6 @@ ExtractionResult extract_isosurface(const CellIndex &index, const IsoParams &par
   stats.fat_triangle_count = st.fat_triangle_count;
   stats.seconds_pass1 = st.seconds_pass1;
   stats.seconds_pass2 = st.seconds_pass2;
-
-  const auto t_weld = Clock::now();
-  result.mesh = weld(fat);
-  stats.seconds_weld = seconds_since(t_weld);
   stats.welded_vertex_count = result.mesh.vertices.size();
   stats.welded_triangle_count = result.mesh.triangles.size();
 

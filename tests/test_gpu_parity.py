@@ -272,3 +272,19 @@ def test_larger_known_answers(P, ref, which):
     k = KNOWN[which]
     assert st["fat_triangle_count"] == k["fat_triangle_count"]
     ref.free(h)
+
+
+def test_dual_cells_records(P, ref):
+    """amrx_extract_dual_cells: the reference's DualCell records (corners,
+    base = dual_base_of(owner, delta), level, owner) built on the device"""
+    c = CASES["slots_l4_s3"]
+    idx = P.build_index(c["in_cells"], c["in_scalars"])
+    recs = P.extract_dual_cells(idx)
+    h = ref.build(c["in_cells"], c["in_scalars"])
+    rd = ref.extract_dual(h, 0)
+    assert (recs["corners"] == rd["corners"]).all()
+    assert (recs["owner"] == rd["owner"]).all()
+    d = P.extract_dual_mesh(idx)
+    base, lev = P.dual_bases(idx, d.tasks)
+    assert (recs["base"] == base).all() and (recs["level"] == lev).all()
+    ref.free(h)

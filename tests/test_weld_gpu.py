@@ -133,3 +133,25 @@ def test_weld_sort_path_matches(P, tmp_path):
                    env=dict(os.environ, AMRX_WELD="sort"))
     assert same(m.vertices, np.load(tmp_path / "v.npy"))
     assert (m.triangles == np.load(tmp_path / "t.npy")).all()
+
+
+@pytest.mark.parametrize("name", ["slots_l4_s3", "octree_sphere", "acceptance_1"])
+def test_extract_isosurface_mesh_equals_reference(P, ref, name):
+    """extract + weld on the device (amrx_extract_iso_mesh, what the drop-in's
+    extract_isosurface returns) == the reference's welded mesh, bit for bit"""
+    import os
+    here = os.path.dirname(os.path.abspath(__file__))
+    z = np.load(os.path.join(here, "golden", "cases.npz"))
+    cells, scal, iso = z[name + "/in_cells"], z[name + "/in_scalars"], float(z[name + "/iso"])
+    idx = P.build_index(cells, scal)
+    mesh, st, tw = P.extract_isosurface_mesh(idx, iso)
+    h = ref.build(cells, scal)
+    ri = ref.extract_iso(h, iso, 0)
+    assert st.fat_triangle_count == ri["stats"]["fat_triangle_count"]
+    assert mesh.vertices.shape == ri["verts"].shape
+    assert (mesh.vertices.view(np.uint64) == ri["verts"].view(np.uint64)).all()
+    assert (mesh.triangles == ri["tris"]).all()
+    # a second call reuses the cached soup and mesh
+    mesh2, _, _ = P.extract_isosurface_mesh(idx, iso)
+    assert (mesh2.triangles == mesh.triangles).all()
+    ref.free(h)
