@@ -131,7 +131,8 @@ DATA_DESC = {
     "c3": "synthetic (GPU generator: 6-level octree toward a turbulent-noise zero set, soup order)",
     "c4": "synthetic (GPU generator: vortex-tube brick AMR, bijective-hash soup order)",
     "c5": "synthetic (GPU generator: brick AMR, generator order)",
-    "deep": "synthetic (GPU generator: 13-level octree toward a landing-gear surface, soup order)",
+    "deep": "synthetic (GPU generator: 13-level octree toward a landing-gear surface, 2-cell level bands, soup order)",
+    "deep_thin": "synthetic (GPU generator: 13-level octree toward a landing-gear surface, 1-cell level bands, soup order)",
 }
 
 
@@ -147,7 +148,7 @@ def make_workload(cfg_name, device):
     import torch
     gen = getattr(synth, cfg["kind"])
     if cfg["kind"] in ("octree_noise", "octree_sdf"):  # GPU generators: device tensors
-        cells, scal = gen(*cfg["args"], device=device)
+        cells, scal = gen(*cfg["args"], device=device, **cfg.get("kwargs", {}))
         return cells, scal, dict(level_cells=torch.bincount(cells[:, 3].long()).tolist())
     cells, scal = gen(*cfg["args"])
     return (torch.from_numpy(cells).to(device), torch.from_numpy(scal).to(device), {})

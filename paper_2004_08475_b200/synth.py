@@ -206,7 +206,7 @@ def octree_noise(root=(48, 48, 48), levels=6, seed=3, k=0.45, base=0.02, shuffle
     return cells, scal
 
 
-def landing_gear_sdf(c, scale):
+def landing_gear_sdf(c, scale, size=1.0):
     """signed distance (finest units, FP64) to a landing-gear-like body: a
     main strut, a side brace, an axle and two wheels (tori) -- the shape
     class of the paper's 13-level NASA landing gear.
@@ -214,6 +214,10 @@ def landing_gear_sdf(c, scale):
     import torch
     S = float(scale)
     x, y, z = c[:, 0], c[:, 1], c[:, 2]
+    # the body scaled by `size` about the domain's centre line
+    x = 0.5 * S + (x - 0.5 * S) / size
+    y = 0.5 * S + (y - 0.5 * S) / size
+    z = 0.5 * S + (z - 0.5 * S) / size
 
     def capsule(ax, ay, az, bx, by, bz, r):
         px, py, pz = x - ax, y - ay, z - az
@@ -232,11 +236,11 @@ def landing_gear_sdf(c, scale):
                                  0.022 * S))                             # axle
     for sy in (-0.15, 0.15):                                             # wheels
         d = torch.minimum(d, torus_y(cx, cy + sy * S, 0.30 * S, 0.10 * S, 0.045 * S))
-    return d
+    return d * size
 
 
 def octree_sdf(root=(3, 2, 2), levels=13, k=0.9, seed=13, shuffle=True, device="cuda",
-               noise=0.0):
+               noise=0.0, size=1.0):
     """DEEP config: an octree of `levels` levels (0..levels-1) over a root
     grid of coarsest cells, refined toward a landing-gear surface
     (landing_gear_sdf) -- a cell is split while its centre lies within k
@@ -258,7 +262,7 @@ def octree_sdf(root=(3, 2, 2), levels=13, k=0.9, seed=13, shuffle=True, device="
     while True:
         w = 1 << L
         ctr = cur.to(torch.float64) + 0.5 * w
-        f = landing_gear_sdf(ctr, scale)
+        f = landing_gear_sdf(ctr, scale, size)
         if noise:
             f = f + noise * torch.sin(ctr[:, 0] * 0.013 + ph[0]) * \
                 torch.sin(ctr[:, 1] * 0.011 + ph[1]) * torch.sin(ctr[:, 2] * 0.017 + ph[2])
@@ -296,6 +300,11 @@ CONFIGS = {
                dual_only=True, knobs=C5_KNOBS),
     # DEEP: a 13-level octree (levels 0..12) refined toward a landing-gear
     # surface (the paper's 13-level NASA landing gear shape class), soup
-    # order, iso 0 on the signed distance -- a sparse 47-bit key space
-    "deep": dict(kind="octree_sdf", args=((3, 2, 2), 13, 0.9), iso=0.0),
+    # order, iso 0 on the signed distance -- a sparse 44-bit key space; a
+    # cell splits within 2 widths of the surface (AMR codes keep a buffer of
+    # a few cells per level band)
+    "deep": dict(kind="octree_sdf", args=((3, 2, 2), 13, 2.0), kwargs=dict(size=0.67), iso=0.0),
+    # the same with a one-cell band per level (k = 0.9): nearly every cell
+    # at a level transition -- the lookup stress case
+    "deep_thin": dict(kind="octree_sdf", args=((3, 2, 2), 13, 0.9), iso=0.0),
 }
