@@ -172,6 +172,11 @@ def run_amrx(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1 or args.force_dist:
+        if "WORLD_SIZE" not in os.environ:  # --force-dist without a launcher: one rank
+            os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0",
+                              MASTER_ADDR="127.0.0.1", MASTER_PORT=str(free_port()))
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=dev)
     iso = iso_of(args.config)
 
@@ -640,6 +645,7 @@ def spawn_ranks(n, argv):
     lines show the rank count; returns the launcher's exit code"""
     env = dict(os.environ)
     env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout carries the one JSON line
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
            "--master-port", str(free_port()), os.path.abspath(__file__), *argv]
@@ -689,6 +695,7 @@ def main():
         sys.exit(spawn_ranks(args.gpus, sys.argv[1:]))
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if args.selftest:
         selftest(args)
         return

@@ -303,7 +303,7 @@ CONFIGS = {
     # order, iso 0 on the signed distance -- a sparse 44-bit key space; a
     # cell splits within 2 widths of the surface (AMR codes keep a buffer of
     # a few cells per level band)
-    "deep": dict(kind="octree_sdf", args=((3, 2, 2), 13, 2.0), kwargs=dict(size=0.67), iso=0.0),
+    "deep": dict(kind="octree_sdf", args=((6, 4, 4), 13, 2.0), kwargs=dict(size=0.335), iso=0.0),
     # the same with a one-cell band per level (k = 0.9): nearly every cell
     # at a level transition -- the lookup stress case
     "deep_thin": dict(kind="octree_sdf", args=((3, 2, 2), 13, 0.9), iso=0.0),
