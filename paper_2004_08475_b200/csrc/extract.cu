@@ -286,6 +286,7 @@ struct Smem {
   // cursors (cur, end) for duals and triangles
   unsigned long long acc[kWarps][8];
   uint64_t chunk[kWarps][4];
+  uint4 mk[kWarps][32];  // compacted runtime loop: per-lane mark bits (ok, miss, fin, low)
 };
 
 /// slot-numbered corner mask -> table row (mc::to_table_case, mc_tables.cpp:324-330)
@@ -708,6 +709,95 @@ __device__ __forceinline__ void resolve_marks(const KArgs &a, Smem &sm, int warp
   }
 }
 
+/// index of the r-th (0-based) set bit of mask (mask has more than r bits)
+__device__ __forceinline__ uint32_t nth_set_bit(uint32_t mask, uint32_t r)
+{
+  uint32_t pos = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1) {
+    const uint32_t cand = pos + uint32_t(step);
+    const uint32_t below = cand >= 32 ? mask : mask & ((1u << cand) - 1u);
+    if (uint32_t(__popc(below)) <= r) pos = cand;
+  }
+  return pos;
+}
+
+/*! resolve_marks with the warp's work compacted: the (lane, point) pairs of
+    every lane's `todo` are numbered by a warp scan and dealt out one per lane,
+    so the lookups (hint level + finer, then the coarser levels in snap's
+    order, locator.cpp:122-134) run with every lane busy instead of the warp
+    looping as long as its busiest lane.  A worker reads its owner's stencil
+    through shuffles, writes the result into the owner's shared-memory column
+    and ORs the point's class into the owner's mark words. */
+template <bool DIGITS>
+__device__ __forceinline__ void resolve_marks_compact(const KArgs &a, Smem &sm, int warp,
+                                                      int lane, const Cell &c,
+                                                      const Stencil &st, uint32_t self,
+                                                      uint32_t todo, Marks &m)
+{
+  const uint32_t cnt = __popc(todo);
+  const uint32_t incl = warp_incl_scan(cnt);
+  const uint32_t total = __shfl_sync(kFull, incl, 31);
+  dbg_sum(a.s, kDbgRuntime, cnt);
+  if (total == 0) return;
+  sm.mk[warp][lane] = make_uint4(0, 0, 0, 0);
+  __syncwarp();
+  for (uint32_t base = 0; base < total; base += 32) {
+    const uint32_t i = base + uint32_t(lane);
+    // owner = the number of lanes whose inclusive count is <= i
+    uint32_t owner = 0;
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1) {
+      const uint32_t v = __shfl_sync(kFull, incl, int(owner) + step - 1);
+      if (v <= i) owner += uint32_t(step);
+    }
+    owner = owner > 31u ? 31u : owner;
+    const bool have = i < total;
+    const uint32_t otodo = __shfl_sync(kFull, todo, int(owner));
+    const uint32_t oexcl = __shfl_sync(kFull, incl - cnt, int(owner));
+    Stencil ost;
+    ost.k0 = shfl_u64(st.k0, int(owner));
+    ost.sx = shfl_u64(st.sx, int(owner));
+    ost.sy = shfl_u64(st.sy, int(owner));
+    ost.sz = shfl_u64(st.sz, int(owner));
+    ost.inrange = __shfl_sync(kFull, st.inrange, int(owner));
+    const int olevel = __shfl_sync(kFull, c.level, int(owner));
+    const uint32_t oself = __shfl_sync(kFull, self, int(owner));
+    if (!have) continue;
+    const int p = int(nth_set_bit(otodo, i - oexcl));
+    uint64_t q[1] = {stencil_key<DIGITS>(ost, p)};
+    const bool v[1] = {((ost.inrange >> p) & 1u) != 0};
+    int64_t out[1] = {-1};
+    int lvl[1] = {olevel};
+    batch_find<1, true>(a.s, q, v, out, lvl);
+    const uint32_t coarser = a.g.level_mask & ~((2u << olevel) - 1);
+    if (out[0] < 0 && coarser) {
+      const Hit h = probe_coarser(a, olevel, ost, p, coarser);
+      out[0] = h.id;
+      lvl[0] = h.level;
+    }
+    sm.id[warp][p][owner] = uint32_t(out[0]);
+    sm.lev[warp][p][owner] = uint8_t(lvl[0]);
+    const uint32_t bit = 1u << p;
+    unsigned int *mk = &sm.mk[warp][owner].x;
+    if (out[0] < 0)
+      atomicOr(mk + 1, bit);
+    else if (lvl[0] < olevel)
+      atomicOr(mk + 2, bit);
+    else if (lvl[0] == olevel && uint32_t(out[0]) < oself)
+      atomicOr(mk + 3, bit);
+    else
+      atomicOr(mk, bit);
+  }
+  __syncwarp();
+  const uint4 w = sm.mk[warp][lane];
+  m.ok |= w.x;
+  m.miss |= w.y;
+  m.fin |= w.z;
+  m.low |= w.w;
+  __syncwarp();
+}
+
 template <bool EMIT_DUAL, bool EMIT_TRI, bool F32, int LOOKUP>
 #ifndef AMRX_MINB
 #define AMRX_MINB 4  // CTAs per SM the register budget is sized for (64 regs)
@@ -805,7 +895,13 @@ extract_kernel(const __grid_constant__ KArgs a)
           dbg_sum(a.s, kDbgFastPend, __popc(pend));
           need |= pend;
         }
-        resolve_marks<EMIT_TRI>(a, sm, warp, lane, c, st, self, need, m);
+#ifndef AMRX_COMPACT
+#define AMRX_COMPACT 1
+#endif
+        if (AMRX_COMPACT)
+          resolve_marks_compact<EMIT_TRI>(a, sm, warp, lane, c, st, self, need, m);
+        else
+          resolve_marks<EMIT_TRI>(a, sm, warp, lane, c, st, self, need, m);
       }
       // corners in order d = 0..7 are ascending stencil points, so the
       // first failing corner is the lowest failing bit
