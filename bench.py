@@ -367,7 +367,7 @@ def run_amrx(args):
         n * 16 / world + tris * 72 / world
     achieved = alg_bytes / (kern_ms / 1000.0) / 1e9
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r02_traffic.json")
     if os.path.exists(tpath):
         try:
             traffic = json.load(open(tpath)).get(args.config)
@@ -421,8 +421,9 @@ def run_amrx(args):
                                 "(CUDA events around both launches)"), "peak_kind": kind,
                      "alg_bytes_per_launch": alg_bytes,
                      "note": ("not bandwidth bound: extract_kernel issues instructions on "
-                              "78% of cycles (ALU pipe 67%) at 3.0% of DRAM peak "
-                              "(profiles/r01_extract_c4_ncu.txt)")},
+                              "74% of cycles at 4.1% of DRAM peak; mc_jobs_kernel waits on "
+                              "the corner-scalar loads (long scoreboard) at 26% of DRAM peak "
+                              "(profiles/r02_extract_c4_ncu.txt)")},
         "weld": weld_info if weld_ms is not None else None,
         "cpu_baseline": cpu,
         "e2e": e2e,

@@ -434,6 +434,7 @@ KeyGeom make_geometry(const int64_t mn[3], const int64_t mx[3],
   g.nlevels = 0;
   for (int l = 0; l <= kMaxLevel; l++)
     if ((level_mask >> l) & 1u) g.levels[g.nlevels++] = int8_t(l);
+  for (int a = 0; a < 3; a++) g.umax[a] = uint64_t(g.mx[a] - g.mn[a]) >> g.shift;
   if (g.total > 64) {
     // two-word keys (wide.cuh): an exact-key table, per-level probes
     g.wide = 1;
@@ -460,7 +461,10 @@ KeyGeom make_geometry(const int64_t mn[3], const int64_t mx[3],
                                                                           : kOccHash;
   }
   g.dir_bits = g.occ == kOccNone ? directory_bits(g, n) : occ_bits;
-  g.dir_shift = g.total - g.dir_bits;
+  // records: buckets of 32 key values whatever the width (a key space of
+  // fewer than 5 bits is one bucket), so lookups shift by a constant
+  g.dir_shift = g.occ == kOccNone ? g.total - g.dir_bits : kOccShift;
+
   g.aligned = 1;
   for (int a = 0; a < 3; a++)
     if (mn[a] & ((int64_t(1) << hi_level) - 1)) g.aligned = 0;

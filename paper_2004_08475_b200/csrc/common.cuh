@@ -64,6 +64,7 @@ struct KeyGeom {
   int32_t lbits;        // width of the level field
   int32_t total;        // key bits in use
   int32_t sh[3];        // left shift of the x/y/z fields
+  uint64_t umax[3];     // largest field value per axis ((mx - mn) >> shift)
   int32_t dir_bits;     // directory has 2^dir_bits + 1 entries
   int32_t dir_shift;    // bucket = key >> dir_shift
   uint32_t level_mask;  // bit l set iff level l present
@@ -234,7 +235,7 @@ __host__ __device__ inline Stencil make_stencil(const KeyGeom &g, uint64_t key, 
       continue;
     }
     const uint64_t u = (key >> g.sh[a]) & ((uint64_t(1) << g.bits[a]) - 1);
-    const uint64_t umax = uint64_t(g.mx[a] - g.mn[a]) >> g.shift;
+    const uint64_t umax = g.umax[a];
     *step[a] = wu << g.sh[a];
     if (u < wu) out |= m_minus[a];
     if (u + wu > umax) out |= m_plus[a];
@@ -421,7 +422,7 @@ __device__ __forceinline__ int64_t occ_resolve(uint64_t q, uint2 r, uint32_t lma
 
 __device__ __forceinline__ uint2 ldg_rec(const SearchCtx &s, uint64_t q)
 {
-  const uint64_t b = q >> s.dir_shift;
+  const uint64_t b = q >> kOccShift;  // (KeyGeom::dir_shift is kOccShift for records)
   if (!AMRX_BOUND(b - s.rec_lo < s.rec_cnt, kChkRecord)) return make_uint2(0, 0);
   return __ldg(s.rec + b);
 }

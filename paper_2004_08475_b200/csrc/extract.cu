@@ -735,11 +735,11 @@ __device__ __forceinline__ void resolve_marks_compact(const KArgs &a, Smem &sm, 
                                                       const Stencil &st, uint32_t self,
                                                       uint32_t todo, Marks &m)
 {
+  if (!__any_sync(kFull, todo != 0)) return;
   const uint32_t cnt = __popc(todo);
   const uint32_t incl = warp_incl_scan(cnt);
   const uint32_t total = __shfl_sync(kFull, incl, 31);
   dbg_sum(a.s, kDbgRuntime, cnt);
-  if (total == 0) return;
   sm.mk[warp][lane] = make_uint4(0, 0, 0, 0);
   __syncwarp();
   for (uint32_t base = 0; base < total; base += 32) {
