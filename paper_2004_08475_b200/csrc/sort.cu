@@ -95,6 +95,19 @@ __global__ void digit_offsets_kernel(const unsigned int *hist, int passes,
   }
 }
 
+#ifndef AMRX_SORT_LB
+#define AMRX_SORT_LB 8
+#endif
+constexpr int kLookBack = AMRX_SORT_LB;
+#ifndef AMRX_SORT_MINB
+#define AMRX_SORT_MINB 2
+#endif
+#ifndef AMRX_SORT_RANK_OR
+#define AMRX_SORT_RANK_OR 1  // C4 ingest 44.7 -> 43.6 ms (MATCH.ANY latency)
+#endif
+#ifndef AMRX_SORT_SF
+#define AMRX_SORT_SF 1  // C4 ingest 49.5 -> 44.7 ms with kLookBack 8
+#endif
 #ifndef AMRX_SORT_WHIST16
 #define AMRX_SORT_WHIST16 1  // C4 ingest 49.9 -> 48.8 ms (u32 counts: more shared-memory traffic)
 #endif
@@ -122,7 +135,7 @@ struct PassSmem {
     for scattering a payload that is still arriving). */
 enum { kPassPlain = 0, kPassGather = 1, kPassInverse = 2 };
 template <int MODE, typename V>
-__global__ void __launch_bounds__(kSortThreads)
+__global__ void __launch_bounds__(kSortThreads, AMRX_SORT_MINB)
 onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
                      const V *__restrict__ vals_in,
                      uint64_t *__restrict__ keys_out,
@@ -140,6 +153,11 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
   for (int i = threadIdx.x; i < kSortWarps * kDigits; i += kSortThreads)
     (&sm.whist[0][0])[i] = 0;
   for (int i = threadIdx.x; i < kDigits; i += kSortThreads) sm.hist[i] = 0;
+#if AMRX_SORT_RANK_OR
+  for (int i = threadIdx.x; i < kSortWarps * kDigits; i += kSortThreads)
+    reinterpret_cast<uint32_t *>(sm.keys)[i] = 0;
+#endif
+
   __syncthreads();
   const uint32_t tile = sm.tile;
   const uint64_t base = uint64_t(tile) * kSortTile;
@@ -169,15 +187,33 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
   if (digit_thread) st_relaxed(me, (tile == 0 ? kFlagPre : kFlagAgg) | sm.hist[threadIdx.x]);
   // warp multisplit: rank within (warp, digit) in input order
   const uint32_t lt = lanemask_lt();
+#if AMRX_SORT_RANK_OR
+  // peer masks by shared-memory OR (per warp and digit, in the key
+  // buffer's space: it is only written by the shuffle after the ranking)
+  static_assert(sizeof(sm.keys) >= sizeof(uint32_t) * kSortWarps * kDigits, "mask space");
+  uint32_t *pmask = reinterpret_cast<uint32_t *>(sm.keys) + warp * kDigits;
+#endif
 #pragma unroll
   for (int t = 0; t < kSortItems; t++) {
+#if AMRX_SORT_RANK_OR
+    uint32_t peers = 0;
+    if (dig[t] < kDigits) atomicOr(pmask + dig[t], 1u << lane);
+    __syncwarp();
+    if (dig[t] < kDigits) peers = pmask[dig[t]];
+#else
     const uint32_t peers = __match_any_sync(kFull, dig[t]);
+#endif
     const bool leader = (__ffs(peers) - 1) == lane;
     uint32_t before = 0;
     if (dig[t] < kDigits) before = sm.whist[warp][dig[t]];
     rank[t] = before + __popc(peers & lt);
     __syncwarp();
-    if (leader && dig[t] < kDigits) sm.whist[warp][dig[t]] = WhistT(before + __popc(peers));
+    if (leader && dig[t] < kDigits) {
+      sm.whist[warp][dig[t]] = WhistT(before + __popc(peers));
+#if AMRX_SORT_RANK_OR
+      pmask[dig[t]] = 0;
+#endif
+    }
     __syncwarp();
   }
   __syncthreads();
@@ -217,28 +253,48 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
       sm.bexcl[threadIdx.x] = x - total + (warp ? sm.wsum[warp - 1] : 0u);
   }
 
+#if AMRX_SORT_SF
+  // the shuffle needs only tile-local offsets: done before the look-back,
+  // the keys and values leave the registers before it
+  __syncthreads();
+  // local shuffle into digit order
+#pragma unroll
+  for (int t = 0; t < kSortItems; t++)
+    if (dig[t] < kDigits) {
+      const uint32_t pos = sm.bexcl[dig[t]] + sm.whist[warp][dig[t]] + rank[t];
+      sm.keys[pos] = k[t];
+      sm.vals[pos] = v[t];
+    }
+#endif
   // decoupled look-back per digit (the aggregate went out before the
   // ranking): sum the predecessors' until an inclusive prefix appears
   if (digit_thread) {
     const int d = threadIdx.x;
     unsigned long long excl = 0;
     if (tile != 0) {
+      // AMRX_SORT_LB predecessors per round trip: the walk back to the
+      // nearest inclusive prefix costs ~1/LB of the dependent L2 loads
+      // (tile 0 always holds an inclusive prefix, so the walk ends there)
       int64_t j = int64_t(tile) - 1;
-      while (true) {
-        unsigned long long s;
-        do {
-          s = ld_relaxed(state + uint64_t(j) * kDigits + d);
-        } while ((s & ~kValMask) == 0);
-        excl += s & kValMask;
-        if ((s & ~kValMask) == kFlagPre) break;
-        j--;
+      for (bool done = false; !done;) {
+        unsigned long long s[kLookBack];
+#pragma unroll
+        for (int q = 0; q < kLookBack; q++)
+          s[q] = j - q >= 0 ? ld_relaxed(state + uint64_t(j - q) * kDigits + d) : 0ull;
+#pragma unroll
+        for (int q = 0; q < kLookBack; q++) {
+          if (done || (s[q] & ~kValMask) == 0) break;  // not published yet: poll again from j
+          excl += s[q] & kValMask;
+          done = (s[q] & ~kValMask) == kFlagPre;
+          j--;
+        }
       }
       st_relaxed(me, kFlagPre | (excl + total));
     }
     sm.gofs[d] = digit_start[d] + excl;
   }
   __syncthreads();
-
+#if !AMRX_SORT_SF
   // local shuffle into digit order
 #pragma unroll
   for (int t = 0; t < kSortItems; t++)
@@ -248,6 +304,7 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
       sm.vals[pos] = v[t];
     }
   __syncthreads();
+#endif
   const uint64_t valid = n - base < uint64_t(kSortTile) ? n - base : kSortTile;
   if (MODE == kPassInverse) {
     for (int pos = threadIdx.x; pos < int(valid); pos += kSortThreads) {
