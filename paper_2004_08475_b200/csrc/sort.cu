@@ -9,6 +9,7 @@
 #include "internal.h"
 
 #include <algorithm>
+#include <cstddef>
 #include <type_traits>
 #include <vector>
 
@@ -102,8 +103,9 @@ constexpr int kLookBack = AMRX_SORT_LB;
 #ifndef AMRX_SORT_MINB
 #define AMRX_SORT_MINB 2
 #endif
-#ifndef AMRX_SORT_RANK_OR
-#define AMRX_SORT_RANK_OR 1  // C4 ingest 44.7 -> 43.6 ms (MATCH.ANY latency)
+// peer masks by shared-memory OR, not MATCH.ANY (its latency): C4 ingest 44.7 -> 43.6 ms
+#ifndef AMRX_SORT_DB
+#define AMRX_SORT_DB 0
 #endif
 #ifndef AMRX_SORT_SF
 #define AMRX_SORT_SF 1  // C4 ingest 49.5 -> 44.7 ms with kLookBack 8
@@ -150,13 +152,26 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
   if (threadIdx.x == 0) sm.tile = atomicAdd(ticket, 1u);
-  for (int i = threadIdx.x; i < kSortWarps * kDigits; i += kSortThreads)
-    (&sm.whist[0][0])[i] = 0;
+  // peer masks (per warp and digit) live in the key/value buffers' space,
+  // which only the shuffle after the ranking writes; two alternating sets
+  // when they fit (then a warp needs two barriers per item instead of three)
+  constexpr int kMaskWords = kSortWarps * kDigits;
+  constexpr bool kTwoSets =
+    AMRX_SORT_DB != 0 && sizeof(sm.keys) + sizeof(sm.vals) >= 2 * 4 * size_t(kMaskWords);
+  static_assert(sizeof(sm.keys) >= 4 * size_t(kMaskWords), "mask space");
+  static_assert(offsetof(PassSmem<V>, vals) == sizeof(sm.keys), "keys, vals adjacent");
+  // zero the per-warp counts and the peer masks with 16-byte stores
+  {
+    constexpr int kW = int(sizeof(sm.whist) / 16);
+    uint4 *w = reinterpret_cast<uint4 *>(&sm.whist[0][0]);
+#pragma unroll
+    for (int i = threadIdx.x; i < kW; i += kSortThreads) w[i] = make_uint4(0, 0, 0, 0);
+    constexpr int kM = (kTwoSets ? 2 : 1) * kMaskWords * 4 / 16;
+    uint4 *m = reinterpret_cast<uint4 *>(sm.keys);
+#pragma unroll
+    for (int i = threadIdx.x; i < kM; i += kSortThreads) m[i] = make_uint4(0, 0, 0, 0);
+  }
   for (int i = threadIdx.x; i < kDigits; i += kSortThreads) sm.hist[i] = 0;
-#if AMRX_SORT_RANK_OR
-  for (int i = threadIdx.x; i < kSortWarps * kDigits; i += kSortThreads)
-    reinterpret_cast<uint32_t *>(sm.keys)[i] = 0;
-#endif
 
   __syncthreads();
   const uint32_t tile = sm.tile;
@@ -187,34 +202,27 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
   if (digit_thread) st_relaxed(me, (tile == 0 ? kFlagPre : kFlagAgg) | sm.hist[threadIdx.x]);
   // warp multisplit: rank within (warp, digit) in input order
   const uint32_t lt = lanemask_lt();
-#if AMRX_SORT_RANK_OR
-  // peer masks by shared-memory OR (per warp and digit, in the key
-  // buffer's space: it is only written by the shuffle after the ranking)
-  static_assert(sizeof(sm.keys) >= sizeof(uint32_t) * kSortWarps * kDigits, "mask space");
   uint32_t *pmask = reinterpret_cast<uint32_t *>(sm.keys) + warp * kDigits;
-#endif
 #pragma unroll
   for (int t = 0; t < kSortItems; t++) {
-#if AMRX_SORT_RANK_OR
+    uint32_t *pm = pmask + ((kTwoSets && (t & 1)) ? kMaskWords : 0);
+    const bool valid = dig[t] < kDigits;
     uint32_t peers = 0;
-    if (dig[t] < kDigits) atomicOr(pmask + dig[t], 1u << lane);
+    if (valid) atomicOr(pm + dig[t], 1u << lane);
     __syncwarp();
-    if (dig[t] < kDigits) peers = pmask[dig[t]];
-#else
-    const uint32_t peers = __match_any_sync(kFull, dig[t]);
-#endif
-    const bool leader = (__ffs(peers) - 1) == lane;
     uint32_t before = 0;
-    if (dig[t] < kDigits) before = sm.whist[warp][dig[t]];
+    if (valid) {
+      peers = pm[dig[t]];
+      before = sm.whist[warp][dig[t]];
+    }
     rank[t] = before + __popc(peers & lt);
     __syncwarp();
-    if (leader && dig[t] < kDigits) {
+    if (valid && (__ffs(peers) - 1) == lane) {  // the digit's leader
       sm.whist[warp][dig[t]] = WhistT(before + __popc(peers));
-#if AMRX_SORT_RANK_OR
-      pmask[dig[t]] = 0;
-#endif
+      pm[dig[t]] = 0;
     }
-    __syncwarp();
+    // with one mask set the clear must land before the next item's OR
+    if (!kTwoSets) __syncwarp();
   }
   __syncthreads();
 
