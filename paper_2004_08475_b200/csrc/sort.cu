@@ -9,7 +9,6 @@
 #include "internal.h"
 
 #include <algorithm>
-#include <cstddef>
 #include <type_traits>
 #include <vector>
 
@@ -104,9 +103,6 @@ constexpr int kLookBack = AMRX_SORT_LB;
 #define AMRX_SORT_MINB 2
 #endif
 // peer masks by shared-memory OR, not MATCH.ANY (its latency): C4 ingest 44.7 -> 43.6 ms
-#ifndef AMRX_SORT_DB
-#define AMRX_SORT_DB 0
-#endif
 #ifndef AMRX_SORT_SF
 #define AMRX_SORT_SF 1  // C4 ingest 49.5 -> 44.7 ms with kLookBack 8
 #endif
@@ -152,21 +148,18 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
   if (threadIdx.x == 0) sm.tile = atomicAdd(ticket, 1u);
-  // peer masks (per warp and digit) live in the key/value buffers' space,
-  // which only the shuffle after the ranking writes; two alternating sets
-  // when they fit (then a warp needs two barriers per item instead of three)
+  // peer masks (per warp and digit) live in the key buffer's space, which
+  // only the shuffle after the ranking writes (two alternating mask sets, to
+  // drop one warp barrier per item, measured slower: 42.5 -> 43.0 ms)
   constexpr int kMaskWords = kSortWarps * kDigits;
-  constexpr bool kTwoSets =
-    AMRX_SORT_DB != 0 && sizeof(sm.keys) + sizeof(sm.vals) >= 2 * 4 * size_t(kMaskWords);
   static_assert(sizeof(sm.keys) >= 4 * size_t(kMaskWords), "mask space");
-  static_assert(offsetof(PassSmem<V>, vals) == sizeof(sm.keys), "keys, vals adjacent");
   // zero the per-warp counts and the peer masks with 16-byte stores
   {
     constexpr int kW = int(sizeof(sm.whist) / 16);
     uint4 *w = reinterpret_cast<uint4 *>(&sm.whist[0][0]);
 #pragma unroll
     for (int i = threadIdx.x; i < kW; i += kSortThreads) w[i] = make_uint4(0, 0, 0, 0);
-    constexpr int kM = (kTwoSets ? 2 : 1) * kMaskWords * 4 / 16;
+    constexpr int kM = kMaskWords * 4 / 16;
     uint4 *m = reinterpret_cast<uint4 *>(sm.keys);
 #pragma unroll
     for (int i = threadIdx.x; i < kM; i += kSortThreads) m[i] = make_uint4(0, 0, 0, 0);
@@ -205,24 +198,22 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
   uint32_t *pmask = reinterpret_cast<uint32_t *>(sm.keys) + warp * kDigits;
 #pragma unroll
   for (int t = 0; t < kSortItems; t++) {
-    uint32_t *pm = pmask + ((kTwoSets && (t & 1)) ? kMaskWords : 0);
     const bool valid = dig[t] < kDigits;
     uint32_t peers = 0;
-    if (valid) atomicOr(pm + dig[t], 1u << lane);
+    if (valid) atomicOr(pmask + dig[t], 1u << lane);
     __syncwarp();
     uint32_t before = 0;
     if (valid) {
-      peers = pm[dig[t]];
+      peers = pmask[dig[t]];
       before = sm.whist[warp][dig[t]];
     }
     rank[t] = before + __popc(peers & lt);
     __syncwarp();
     if (valid && (__ffs(peers) - 1) == lane) {  // the digit's leader
       sm.whist[warp][dig[t]] = WhistT(before + __popc(peers));
-      pm[dig[t]] = 0;
+      pmask[dig[t]] = 0;
     }
-    // with one mask set the clear must land before the next item's OR
-    if (!kTwoSets) __syncwarp();
+    __syncwarp();  // the clear lands before the next item's OR
   }
   __syncthreads();
 
