@@ -33,6 +33,8 @@ struct PrepassAcc {
     with the bounds/level reductions of locator.cpp:70-89.  The first bad
     record in INPUT order wins (atomicMin on its position), so the host can
     name "record n" exactly like the serial loop. */
+constexpr int kPrepassItems = 4;
+
 __global__ void __launch_bounds__(kThreads)
 prepass_kernel(const int4 *__restrict__ cells, uint64_t n, PrepassAcc *acc)
 {
@@ -41,24 +43,35 @@ prepass_kernel(const int4 *__restrict__ cells, uint64_t n, PrepassAcc *acc)
   long long hi[3] = {LLONG_MIN, LLONG_MIN, LLONG_MIN};
   unsigned int mask = 0;
   unsigned long long bad = ~0ull;
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
-       r += stride) {
-    const int4 c = __ldg(cells + r);
-    const int v[3] = {c.x, c.y, c.z};
-    bool ok = c.w >= 0 && c.w <= kMaxLevel;
-    if (ok) {
-      const int64_t w = int64_t(1) << c.w;
+  // kPrepassItems loads in flight per thread (strided by the block size)
+  constexpr int U = kPrepassItems;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * U;
+  for (uint64_t r0 = uint64_t(blockIdx.x) * blockDim.x * U + threadIdx.x; r0 < n;
+       r0 += stride) {
+    int4 cs[U];
 #pragma unroll
-      for (int a = 0; a < 3; a++) {
-        ok = ok && anchor_mask(v[a], c.w) == v[a];
-        mn[a] = min(mn[a], v[a]);
-        mx[a] = max(mx[a], v[a]);
-        hi[a] = max(hi[a], (long long)(v[a] + w));
+    for (int u = 0; u < U; u++)
+      if (r0 + u * blockDim.x < n) cs[u] = __ldg(cells + r0 + u * blockDim.x);
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint64_t r = r0 + u * blockDim.x;
+      if (r >= n) break;
+      const int4 c = cs[u];
+      const int v[3] = {c.x, c.y, c.z};
+      bool ok = c.w >= 0 && c.w <= kMaxLevel;
+      if (ok) {
+        const int64_t w = int64_t(1) << c.w;
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+          ok = ok && anchor_mask(v[a], c.w) == v[a];
+          mn[a] = min(mn[a], v[a]);
+          mx[a] = max(mx[a], v[a]);
+          hi[a] = max(hi[a], (long long)(v[a] + w));
+        }
+        mask |= 1u << c.w;
       }
-      mask |= 1u << c.w;
+      if (!ok && r < bad) bad = r;
     }
-    if (!ok && r < bad) bad = r;
   }
   // warp reduce, then one atomic per warp
 #pragma unroll
@@ -102,6 +115,8 @@ pack_kernel(const int4 *__restrict__ cells, uint64_t n, const KeyGeom g,
     cells: per-block shared histograms flushed once; a key's successor
     comes from the next lane (whole warps step together), or is packed again
     at a warp's last lane */
+constexpr int kPackRuns = 4;
+
 __global__ void __launch_bounds__(kThreads)
 pack_hist_kernel(const int4 *__restrict__ cells, uint64_t n, const KeyGeom g,
                  uint64_t *__restrict__ keys, uint32_t *__restrict__ idx,
@@ -113,29 +128,49 @@ pack_hist_kernel(const int4 *__restrict__ cells, uint64_t n, const KeyGeom g,
   __syncthreads();
   const int lane = threadIdx.x & 31;
   unsigned long long desc = 0, eq = 0;
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); base < n;
+  // a warp takes kPackRuns runs of 32 consecutive cells per step, all loads
+  // issued first; a run's last key compares with the next run's first
+  constexpr int U = kPackRuns;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * U;
+  for (uint64_t base = (uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u)) * U; base < n;
        base += stride) {
-    const uint64_t r = base + lane;
-    const bool in = r < n;
-    uint64_t k = 0;
-    if (in) {
-      const int4 c = __ldg(cells + r);
-      k = pack_unchecked(g, c.x, c.y, c.z, c.w);
-      keys[r] = k;
-      if (idx) idx[r] = uint32_t(r);
+    int4 c[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint64_t r = base + u * 32 + lane;
+      if (r < n) c[u] = __ldg(cells + r);
+    }
+    int4 tail = make_int4(0, 0, 0, 0);
+    const uint64_t after = base + U * 32;  // the first cell past the warp's runs
+    if (lane == 31 && after < n) tail = __ldg(cells + after);
+    uint64_t k[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint64_t r = base + u * 32 + lane;
+      k[u] = 0;
+      if (r < n) {
+        k[u] = pack_unchecked(g, c[u].x, c[u].y, c[u].z, c[u].w);
+        keys[r] = k[u];
+        if (idx) idx[r] = uint32_t(r);
 #pragma unroll 1
-      for (int p = 0; p < passes; p++)
-        atomicAdd(&h[p][(k >> (p * kSortRadixBits)) & (kSortDigits - 1)], 1u);
+        for (int p = 0; p < passes; p++)
+          atomicAdd(&h[p][(k[u] >> (p * kSortRadixBits)) & (kSortDigits - 1)], 1u);
+      }
     }
-    uint64_t nxt = __shfl_down_sync(kFull, (unsigned long long)k, 1);
-    if (lane == 31 && r + 1 < n) {
-      const int4 c = __ldg(cells + r + 1);
-      nxt = pack_unchecked(g, c.x, c.y, c.z, c.w);
-    }
-    if (in && r + 1 < n) {
-      desc += k > nxt;
-      eq += k == nxt;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint64_t r = base + u * 32 + lane;
+      uint64_t nxt = __shfl_down_sync(kFull, (unsigned long long)k[u], 1);
+      if (u + 1 < U) {
+        const uint64_t first = __shfl_sync(kFull, (unsigned long long)k[u + 1 < U ? u + 1 : u], 0);
+        if (lane == 31) nxt = first;
+      } else if (lane == 31 && after < n) {
+        nxt = pack_unchecked(g, tail.x, tail.y, tail.z, tail.w);
+      }
+      if (r + 1 < n) {
+        desc += k[u] > nxt;
+        eq += k[u] == nxt;
+      }
     }
   }
 #pragma unroll
@@ -428,16 +463,35 @@ rec_build_kernel(const uint64_t *__restrict__ keys, uint64_t n, int dir_shift,
                  uint64_t entries, const uint32_t *__restrict__ tile_start,
                  uint2 *__restrict__ rec, unsigned long long *order2)
 {
-  __shared__ uint32_t bits[kRecTile];
-  __shared__ uint32_t cnt[kRecTile];
+  __shared__ __align__(16) uint32_t bits[kRecTile];
+  __shared__ __align__(16) uint32_t cnt[kRecTile];
   __shared__ uint32_t wsum[32];
   const uint64_t t = blockIdx.x;
-  for (int j = threadIdx.x; j < kRecTile; j += kRecThreads) {
-    bits[j] = 0;
-    cnt[j] = 0;
+  const uint64_t lo = tile_start[t], hi = tile_start[t + 1];
+  const uint64_t r0 = t << kRecTileLog;  // records are relative to rec_lo
+  if (lo == hi) {
+    // no key in these buckets (most tiles of a sparse level): every record
+    // is {lo, 0}, two per 16-byte store
+    const uint4 z = make_uint4(uint32_t(lo), 0u, uint32_t(lo), 0u);
+    if (r0 + kRecTile <= entries) {
+      uint4 *dst = reinterpret_cast<uint4 *>(rec + r0);
+#pragma unroll
+      for (int j = threadIdx.x; j < kRecTile / 2; j += kRecThreads) dst[j] = z;
+    } else {
+      for (int j = threadIdx.x; j < kRecTile; j += kRecThreads)
+        if (r0 + j < entries) rec[r0 + j] = make_uint2(uint32_t(lo), 0u);
+    }
+    return;
+  }
+  {
+    uint4 *zb = reinterpret_cast<uint4 *>(bits), *zc = reinterpret_cast<uint4 *>(cnt);
+#pragma unroll
+    for (int j = threadIdx.x; j < kRecTile / 4; j += kRecThreads) {
+      zb[j] = make_uint4(0, 0, 0, 0);
+      zc[j] = make_uint4(0, 0, 0, 0);
+    }
   }
   __syncthreads();
-  const uint64_t lo = tile_start[t], hi = tile_start[t + 1];
   const int lane = threadIdx.x & 31;
   unsigned long long desc = 0, eq = 0;
   // whole warps step together so the match below sees all lanes
@@ -498,9 +552,18 @@ rec_build_kernel(const uint64_t *__restrict__ keys, uint64_t n, int dir_shift,
     run += c[j];
   }
   __syncthreads();
-  const uint64_t r0 = t << kRecTileLog;  // records are relative to rec_lo
-  for (int j = threadIdx.x; j < kRecTile; j += kRecThreads)  // coalesced
-    if (r0 + j < entries) rec[r0 + j] = make_uint2(cnt[j], bits[j]);
+  if (r0 + kRecTile <= entries) {  // coalesced, two records per 16-byte store
+    uint4 *dst = reinterpret_cast<uint4 *>(rec + r0);
+#pragma unroll
+    for (int j = threadIdx.x; j < kRecTile / 2; j += kRecThreads) {
+      const uint2 c = reinterpret_cast<const uint2 *>(cnt)[j];
+      const uint2 b = reinterpret_cast<const uint2 *>(bits)[j];
+      dst[j] = make_uint4(c.x, b.x, c.y, b.y);
+    }
+  } else {
+    for (int j = threadIdx.x; j < kRecTile; j += kRecThreads)
+      if (r0 + j < entries) rec[r0 + j] = make_uint2(cnt[j], bits[j]);
+  }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     desc += __shfl_xor_sync(kFull, desc, off);
