@@ -313,10 +313,10 @@ __device__ __forceinline__ double centre(int64_t anchor, int level)
     endpoints are runtime corner numbers: they are re-read through it from
     shared memory rather than kept in dynamically indexed arrays, which
     would live in local memory). */
-template <bool F32, bool GAPS = true, typename Corner>
+template <bool F32, bool GAPS = true, typename Corner, typename TCache>
 __device__ __forceinline__ int mc_core(const double *scal, const uint64_t *rows, const Cell &c,
                                        int delta, double iso, void *out, uint64_t at,
-                                       uint64_t cap, uint32_t &err, Corner corner)
+                                       uint64_t cap, uint32_t &err, Corner corner, TCache tcache)
 {
   const int64_t w = int64_t(1) << c.level;
   int mask = 0;
@@ -327,13 +327,15 @@ __device__ __forceinline__ int mc_core(const double *scal, const uint64_t *rows,
   const int ntab = int(word & 15);
   if (ntab == 0) return 0;
 
-  const auto edge_point = [&](int e, double (&pt)[3]) {
+  // an edge's endpoints, the lower CellId first (contour.cpp:42-44)
+  const auto ends_of = [&](int e, int &u, int &v, uint2 &cu, uint2 &cv) {
     const uint32_t ends = e < 8 ? uint32_t(AMRX_MC_EDGE_LO >> (8 * e))
                                 : uint32_t(AMRX_MC_EDGE_HI >> (8 * (e - 8)));
-    int u = int(ends & 15), v = int((ends >> 4) & 15);
-    uint2 cu = corner(u), cv = corner(v);  // (id, level)
-    if (cu.x == cv.x) err |= 1u;  // collapsed edge selected (contour.cpp:67-70)
-    if (cv.x < cu.x) {            // lower CellId first (contour.cpp:42-44)
+    u = int(ends & 15);
+    v = int((ends >> 4) & 15);
+    cu = corner(u);  // (id, level)
+    cv = corner(v);
+    if (cv.x < cu.x) {
       const int t = u;
       u = v;
       v = t;
@@ -341,8 +343,29 @@ __device__ __forceinline__ int mc_core(const double *scal, const uint64_t *rows,
       cu = cv;
       cv = tc;
     }
-    const double vu = __ldg(scal + cu.x), vv = __ldg(scal + cv.x);
-    const double t = __ddiv_rn(__dsub_rn(iso, vu), __dsub_rn(vv, vu));
+  };
+  // the interpolation parameter of each distinct edge the case's triangles
+  // use (contour.cpp:30-50), computed once: a vertex shared by two triangles
+  // is the same arithmetic on the same operands, so the same bits
+  {
+    uint32_t used = 0;
+    for (int q = 0; q < 3 * ntab; q++) used |= 1u << ((word >> (4 + 4 * q)) & 15);
+    for (; used; used &= used - 1) {
+      const int e = __ffs(used) - 1;
+      int u, v;
+      uint2 cu, cv;
+      ends_of(e, u, v, cu, cv);
+      if (cu.x == cv.x) err |= 1u;  // collapsed edge selected (contour.cpp:67-70)
+      const double vu = __ldg(scal + cu.x), vv = __ldg(scal + cv.x);
+      tcache(e) = __ddiv_rn(__dsub_rn(iso, vu), __dsub_rn(vv, vu));
+    }
+  }
+
+  const auto edge_point = [&](int e, double (&pt)[3]) {
+    int u, v;
+    uint2 cu, cv;
+    ends_of(e, u, v, cu, cv);
+    const double t = tcache(e);
     const int ou[3] = {((u & 1) + (delta & 1)) - 1, (((u >> 1) & 1) + ((delta >> 1) & 1)) - 1,
                        (((u >> 2) & 1) + ((delta >> 2) & 1)) - 1};
     const int ov[3] = {((v & 1) + (delta & 1)) - 1, (((v >> 1) & 1) + ((delta >> 1) & 1)) - 1,
@@ -421,6 +444,7 @@ mc_jobs_kernel(const __grid_constant__ McArgs a)
   __shared__ uint64_t rows[256];
   __shared__ uint32_t jid[8][kMcThreads];
   __shared__ uint8_t jlev[8][kMcThreads];
+  __shared__ double tcs[12][kMcThreads];  // per edge interpolation parameter
   for (int i = threadIdx.x; i < 256; i += kMcThreads) rows[i] = c_mc_rows[table_row(uint32_t(i))];
   __syncthreads();
   const uint64_t n = std::min<uint64_t>(*(volatile unsigned long long *)(a.out + 10), a.job_cap);
@@ -440,7 +464,8 @@ mc_jobs_kernel(const __grid_constant__ McArgs a)
     const uint32_t meta = job.meta;
     const int wrote = mc_core<F32>(a.scal, rows, c, int(meta & 7), a.iso, a.xyz, job.out,
                                    a.tri_cap, err,
-                                   [&](int d) { return make_uint2(jid[d][t], jlev[d][t]); });
+                                   [&](int d) { return make_uint2(jid[d][t], jlev[d][t]); },
+                                   [&](int e) -> double & { return tcs[e][t]; });
     const uint32_t deficit = (meta >> 8) - uint32_t(wrote);
     if (deficit) atomicSub(a.tile_tri_cnt + job.tile, deficit);
     wrote_sum += uint64_t(wrote);
@@ -1605,6 +1630,7 @@ __global__ void __launch_bounds__(256)
 wide_extract_kernel(const __grid_constant__ WArgs a)
 {
   __shared__ uint64_t rows[256];
+  __shared__ double tcs[DUAL ? 1 : 12][256];  // per edge interpolation parameter
   if (!DUAL) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) rows[i] = c_mc_rows[table_row(uint32_t(i))];
     __syncthreads();
@@ -1636,7 +1662,8 @@ wide_extract_kernel(const __grid_constant__ WArgs a)
         const uint64_t at = WRITE ? a.tri_off[r] + nt : 0;
         nt += uint32_t(mc_core<F32, false>(a.scal, rows, c, delta, a.iso,
                                            WRITE ? a.xyz : nullptr, at, WRITE ? a.tri_cap : 0,
-                                           err, [&](int d) { return make_uint2(ids[d], lev[d]); }));
+                                           err, [&](int d) { return make_uint2(ids[d], lev[d]); },
+                                           [&](int e) -> double & { return tcs[e][threadIdx.x]; }));
       }
     }
     if (!WRITE) {
