@@ -440,6 +440,10 @@ constexpr int kRecTile = 1 << kRecTileLog;
 #define AMRX_REC_THREADS 256  // C4 ingest: 256 49.8 ms, 512 50.4, 1024 52.2
 #endif
 constexpr int kRecThreads = AMRX_REC_THREADS;
+#ifndef AMRX_REC_UNROLL
+#define AMRX_REC_UNROLL 2  // C4 records 5.85 -> 5.49 ms (4: 5.98, 8: 9.23)
+#endif
+constexpr int kRecUnroll = AMRX_REC_UNROLL;
 
 /// tile_start[t] = first position whose bucket >= rec_lo + t * kRecTile,
 /// t in [0, tiles]; rec_lo is a multiple of kRecTile and no key lies below it
@@ -494,28 +498,39 @@ rec_build_kernel(const uint64_t *__restrict__ keys, uint64_t n, int dir_shift,
   __syncthreads();
   const int lane = threadIdx.x & 31;
   unsigned long long desc = 0, eq = 0;
-  // whole warps step together so the match below sees all lanes
-  for (uint64_t base = lo + (threadIdx.x & ~31u); base < hi; base += kRecThreads) {
-    const uint64_t i = base + lane;
-    const bool in = i < hi;
-    const uint64_t k = in ? ldg_u64(keys + i) : 0;
-    if (in && i + 1 < n) {
-      const uint64_t k1 = ldg_u64(keys + i + 1);
-      desc += k > k1;
-      eq += k == k1;
-    }
-    const uint32_t b = in ? uint32_t(k >> dir_shift) & (kRecTile - 1) : 0xffffffffu;
-    const uint32_t peers = __match_any_sync(kFull, b);
-    uint32_t v = in ? 1u << (uint32_t(k) & 31u) : 0u;
+  // whole warps step together so the match below sees all lanes;
+  // kRecUnroll runs of 32 keys per warp and step, their loads issued first
+  constexpr int U = kRecUnroll;
+  for (uint64_t base = lo + (threadIdx.x & ~31u); base < hi; base += kRecThreads * U) {
+    uint64_t kk[U], k1[U];
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {  // segmented OR over the run
-      const uint32_t y = __shfl_down_sync(kFull, v, off);
-      const uint32_t bo = __shfl_down_sync(kFull, b, off);
-      if (lane + off < 32 && bo == b) v |= y;
+    for (int u = 0; u < U; u++) {
+      const uint64_t i = base + u * kRecThreads + lane;
+      kk[u] = i < hi ? ldg_u64(keys + i) : 0;
+      k1[u] = i < hi && i + 1 < n ? ldg_u64(keys + i + 1) : 0;
     }
-    if (in && (__ffs(peers) - 1) == lane) {
-      atomicOr(&bits[b], v);
-      atomicAdd(&cnt[b], uint32_t(__popc(peers)));
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint64_t i = base + u * kRecThreads + lane;
+      const bool in = i < hi;
+      const uint64_t k = kk[u];
+      if (in && i + 1 < n) {
+        desc += k > k1[u];
+        eq += k == k1[u];
+      }
+      const uint32_t b = in ? uint32_t(k >> dir_shift) & (kRecTile - 1) : 0xffffffffu;
+      const uint32_t peers = __match_any_sync(kFull, b);
+      uint32_t v = in ? 1u << (uint32_t(k) & 31u) : 0u;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {  // segmented OR over the run
+        const uint32_t y = __shfl_down_sync(kFull, v, off);
+        const uint32_t bo = __shfl_down_sync(kFull, b, off);
+        if (lane + off < 32 && bo == b) v |= y;
+      }
+      if (in && (__ffs(peers) - 1) == lane) {
+        atomicOr(&bits[b], v);
+        atomicAdd(&cnt[b], uint32_t(__popc(peers)));
+      }
     }
   }
   __syncthreads();
