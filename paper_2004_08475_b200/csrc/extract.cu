@@ -175,7 +175,8 @@ sign_bits_kernel(const double *__restrict__ scal, uint64_t n, double iso,
 
 /*! the triangle variant of reorder_kernel: a tile's staging block holds
     up[t] reserved slots of which cnt[t] are triangles; when slivers left
-    gaps (rare: cnt < up) the warp compacts the block while moving it */
+    gaps (cnt < up) the warp compacts the block while moving it, 32 slots at
+    a time: a ballot of the kept slots, then one flat copy of their words */
 __global__ void __launch_bounds__(256)
 reorder_tri_kernel(const uint32_t *__restrict__ cnt, const uint32_t *__restrict__ up,
                    const uint64_t *__restrict__ src_off, const uint64_t *__restrict__ dst_off,
@@ -183,6 +184,7 @@ reorder_tri_kernel(const uint32_t *__restrict__ cnt, const uint32_t *__restrict_
                    uint32_t *__restrict__ dst, uint64_t dst_base, uint64_t dst_cap,
                    uint64_t src_n)
 {
+  __shared__ uint8_t s_kept[8][32];
   const int lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
   for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < tiles; t += warps) {
@@ -199,17 +201,23 @@ reorder_tri_kernel(const uint32_t *__restrict__ cnt, const uint32_t *__restrict_
     uint64_t done = 0;
     const int gw = gap_word(words);
     const uint32_t gm = gap_mark(words);
+    const int wib = threadIdx.x >> 5;
     for (uint32_t i0 = 0; i0 < u; i0 += 32) {
       const uint32_t i = i0 + lane;
       const bool ok = i < u && __ldg(src + (so + i) * words + gw) != gm;
-      uint32_t bal = __ballot_sync(kFull, ok);
-      while (bal) {  // the kept slots of this chunk, in order
-        const int l = __ffs(bal) - 1;
-        bal &= bal - 1;
-        const uint64_t d = d0 + done++;
-        if (d < dst_cap && lane < words)
-          dst[d * words + lane] = __ldg(src + (so + i0 + l) * words + lane);
+      const uint32_t bal = __ballot_sync(kFull, ok);
+      // the kept slots of this chunk in order (rank -> lane), then one
+      // flat copy of their words across the warp
+      if (ok) s_kept[wib][__popc(bal & lanemask_lt())] = uint8_t(lane);
+      __syncwarp();
+      const uint32_t kept = __popc(bal), nw = kept * uint32_t(words);
+      for (uint32_t w = lane; w < nw; w += 32) {
+        const uint32_t j = w / uint32_t(words), c = w - j * uint32_t(words);
+        const uint64_t d = d0 + done + j;
+        if (d < dst_cap) dst[d * words + c] = __ldg(src + (so + i0 + s_kept[wib][j]) * words + c);
       }
+      done += kept;
+      __syncwarp();
     }
   }
 }
