@@ -562,25 +562,6 @@ __host__ __device__ constexpr int base_of(int delta)
   return (delta & 1) + 3 * ((delta >> 1) & 1) + 9 * (delta >> 2);
 }
 
-/// classify one resolved point (dual.cpp:60-67: missing, finer, lower key, ok)
-__device__ __forceinline__ void mark_point(Smem &sm, int warp, int lane, const Cell &c,
-                                           uint32_t self, int p, int64_t id, int lev,
-                                           Marks &m)
-{
-  const uint32_t bit = 1u << p;
-  if (!AMRX_BOUND(p >= 0 && p < 27, kChkSmem)) return;
-  if (id < 0)
-    m.miss |= bit;
-  else if (lev < c.level)
-    m.fin |= bit;
-  else if (lev == c.level && uint32_t(id) < self)
-    m.low |= bit;
-  else
-    m.ok |= bit;
-  sm.id[warp][p][lane] = uint32_t(id);
-  sm.lev[warp][p][lane] = uint8_t(lev);
-}
-
 constexpr uint32_t kFast0 = kCorner0Points & ~(1u << 13);  // 0 1 3 4 9 10 12
 constexpr uint32_t kFast1 = kCube << 13 & ~(1u << 13);       // 14 16 17 22 23 25 26
 
@@ -688,60 +669,6 @@ __device__ __forceinline__ void fast_batch(const KArgs &a, Smem &sm, int warp, i
                             need, m, pend);
 }
 
-/*! resolve the stencil points in `todo` into the marks: two per lane
-    at a time with their lookups in lock-step (batch_find), in snap's probe
-    order (locator.cpp:122-134): hint level + finer in one lookup, then the
-    coarser candidate levels (probe_coarser).  A loop over runtime point
-    indices: unrolling it per point was measured slower for the iso kernel
-    (the hot code outgrows the instruction cache next to marching cubes). */
-template <bool DIGITS>
-__device__ __forceinline__ void resolve_marks(const KArgs &a, Smem &sm, int warp, int lane,
-                                              const Cell &c, const Stencil &st,
-                                              uint32_t self, uint32_t todo, Marks &m)
-{
-#ifndef AMRX_SLOW_K
-#define AMRX_SLOW_K 2  // measured best: K = 1 +1%, K = 3 +13% (before the fast batches)
-#endif
-  constexpr int K = AMRX_SLOW_K;
-  // present levels coarser than the hint: what a miss probes next
-  const uint32_t coarser = a.g.level_mask & ~((2u << c.level) - 1);
-  dbg_sum(a.s, kDbgRuntime, __popc(todo));
-  while (__any_sync(kFull, todo != 0)) {
-    uint64_t q[K];
-    bool v[K];
-    int64_t out[K];
-    int lvl[K], pk[K];
-#pragma unroll
-    for (int k = 0; k < K; k++) {
-      pk[k] = -1;
-      v[k] = false;
-      out[k] = -1;
-      lvl[k] = c.level;
-      q[k] = 0;
-      if (todo) {
-        const int p = __ffs(todo) - 1;
-        todo &= todo - 1;
-        pk[k] = p;
-        // at the hint level the point is its own anchor: key = cell key +
-        // packed steps, valid iff inside the stored range
-        v[k] = (st.inrange >> p) & 1u;
-        q[k] = stencil_key<DIGITS>(st, p);
-      }
-    }
-    batch_find<K, true>(a.s, q, v, out, lvl);
-#pragma unroll
-    for (int k = 0; k < K; k++)
-      if (pk[k] >= 0) {
-        if (out[k] < 0 && coarser) {
-          const Hit h = probe_coarser(a, c.level, st, pk[k], coarser);
-          out[k] = h.id;
-          lvl[k] = h.level;
-        }
-        mark_point(sm, warp, lane, c, self, pk[k], out[k], lvl[k], m);
-      }
-  }
-}
-
 /// index of the r-th (0-based) set bit of mask (mask has more than r bits)
 __device__ __forceinline__ uint32_t nth_set_bit(uint32_t mask, uint32_t r)
 {
@@ -755,11 +682,13 @@ __device__ __forceinline__ uint32_t nth_set_bit(uint32_t mask, uint32_t r)
   return pos;
 }
 
-/*! resolve_marks with the warp's work compacted: the (lane, point) pairs of
-    every lane's `todo` are numbered by a warp scan and dealt out one per lane,
-    so the lookups (hint level + finer, then the coarser levels in snap's
-    order, locator.cpp:122-134) run with every lane busy instead of the warp
-    looping as long as its busiest lane.  A worker reads its owner's stencil
+/*! resolve the stencil points in `todo` into the marks (classes of
+    dual.cpp:60-67: missing, finer, lower key, ok), with the warp's work
+    compacted: the (lane, point) pairs of every lane's `todo` are numbered by
+    a warp scan and dealt out one per lane, so the lookups (hint level +
+    finer, then the coarser levels in snap's order, locator.cpp:122-134) run
+    with every lane busy instead of the warp looping as long as its busiest
+    lane (the per-lane loop it replaced: C4 extraction 60.1 -> 44.9 ms).  A worker reads its owner's stencil
     through shuffles, writes the result into the owner's shared-memory column
     and ORs the point's class into the owner's mark words. */
 template <bool DIGITS>
@@ -928,13 +857,7 @@ extract_kernel(const __grid_constant__ KArgs a)
           dbg_sum(a.s, kDbgFastPend, __popc(pend));
           need |= pend;
         }
-#ifndef AMRX_COMPACT
-#define AMRX_COMPACT 1
-#endif
-        if (AMRX_COMPACT)
-          resolve_marks_compact<EMIT_TRI>(a, sm, warp, lane, c, st, self, need, m);
-        else
-          resolve_marks<EMIT_TRI>(a, sm, warp, lane, c, st, self, need, m);
+        resolve_marks_compact<EMIT_TRI>(a, sm, warp, lane, c, st, self, need, m);
       }
       // corners in order d = 0..7 are ascending stencil points, so the
       // first failing corner is the lowest failing bit

@@ -1,11 +1,13 @@
-// Stable LSD radix sort of (u64 key, u32 value) pairs, onesweep style:
-// one histogram sweep for every digit pass up front, then per 8-bit pass a
-// single kernel that ranks a tile in shared memory (warp __match_any_sync
-// multisplit), obtains the tile's global digit offsets through a decoupled
-// look-back over its predecessors, and scatters digit-sorted runs so the
-// stores coalesce.  Replaces the std::sort over a permutation in
-// build_index (proj/src/locator.cpp:52-68); stability keeps duplicate keys
-// in input order exactly like its (key, input index) comparator.
+// Stable LSD radix sort of (u64 key, u32 or u64 value) pairs, onesweep
+// style: the digit histograms of every pass up front (counted while the keys
+// are packed, or by one sweep), then per 9-bit pass a single kernel that
+// ranks a tile in shared memory (warp multisplit with peer masks built by
+// shared-memory OR), shuffles it into digit order, obtains the tile's global
+// digit offsets through a decoupled look-back over its predecessors, and
+// scatters digit-sorted runs so the stores coalesce.  Replaces the std::sort
+// over a permutation in build_index (proj/src/locator.cpp:52-68); stability
+// keeps duplicate keys in input order exactly like its (key, input index)
+// comparator.
 #include "internal.h"
 
 #include <algorithm>
@@ -103,9 +105,6 @@ constexpr int kLookBack = AMRX_SORT_LB;
 #define AMRX_SORT_MINB 2
 #endif
 // peer masks by shared-memory OR, not MATCH.ANY (its latency): C4 ingest 44.7 -> 43.6 ms
-#ifndef AMRX_SORT_SF
-#define AMRX_SORT_SF 1  // C4 ingest 49.5 -> 44.7 ms with kLookBack 8
-#endif
 #ifndef AMRX_SORT_WHIST16
 #define AMRX_SORT_WHIST16 1  // C4 ingest 49.9 -> 48.8 ms (u32 counts: more shared-memory traffic)
 #endif
@@ -252,9 +251,9 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
       sm.bexcl[threadIdx.x] = x - total + (warp ? sm.wsum[warp - 1] : 0u);
   }
 
-#if AMRX_SORT_SF
   // the shuffle needs only tile-local offsets: done before the look-back,
-  // the keys and values leave the registers before it
+  // the keys and values leave the registers before it (with the 8-wide
+  // look-back: C4 ingest 49.5 -> 44.7 ms)
   __syncthreads();
   // local shuffle into digit order
 #pragma unroll
@@ -264,7 +263,6 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
       sm.keys[pos] = k[t];
       sm.vals[pos] = v[t];
     }
-#endif
   // decoupled look-back per digit (the aggregate went out before the
   // ranking): sum the predecessors' until an inclusive prefix appears
   if (digit_thread) {
@@ -293,17 +291,6 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
     sm.gofs[d] = digit_start[d] + excl;
   }
   __syncthreads();
-#if !AMRX_SORT_SF
-  // local shuffle into digit order
-#pragma unroll
-  for (int t = 0; t < kSortItems; t++)
-    if (dig[t] < kDigits) {
-      const uint32_t pos = sm.bexcl[dig[t]] + sm.whist[warp][dig[t]] + rank[t];
-      sm.keys[pos] = k[t];
-      sm.vals[pos] = v[t];
-    }
-  __syncthreads();
-#endif
   const uint64_t valid = n - base < uint64_t(kSortTile) ? n - base : kSortTile;
   if (MODE == kPassInverse) {
     for (int pos = threadIdx.x; pos < int(valid); pos += kSortThreads) {
