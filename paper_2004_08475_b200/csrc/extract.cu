@@ -773,6 +773,7 @@ extract_kernel(const __grid_constant__ KArgs a)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem &sm = *reinterpret_cast<Smem *>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr bool kNeighbours = LOOKUP == kOccHash;  // see the k-neighbour shortcut below
   if (EMIT_TRI) {
     // indexed by the slot-numbered corner mask directly (table_row applied
     // once here instead of per dual)
@@ -804,6 +805,11 @@ extract_kernel(const __grid_constant__ KArgs a)
     const uint32_t self = uint32_t(cell);
     const uint64_t kself =
       valid && AMRX_BOUND(cell < a.s.n, kChkKey) ? ldg_u64(a.s.keys + cell) : 0;
+    // the sorted neighbours of the tile's end lanes (the others are lanes)
+    uint64_t kedge = 0;
+    if (kNeighbours && valid && lane == 0 && cell > 0) kedge = ldg_u64(a.s.keys + cell - 1);
+    if (kNeighbours && valid && lane == 31 && cell + 1 < a.s.n)
+      kedge = ldg_u64(a.s.keys + cell + 1);
     const Cell c = unpack(a.g, kself);
     const Stencil st = make_stencil(a.g, kself, c.level);
 
@@ -817,6 +823,32 @@ extract_kernel(const __grid_constant__ KArgs a)
         sm.id[warp][13][lane] = self;
         sm.lev[warp][13][lane] = uint8_t(c.level);
         need &= ~(1u << 13);
+      }
+      if (kNeighbours) {
+        // points 4 and 22, (0, 0, -w) and (0, 0, +w): when the sorted
+        // neighbour's key is the stencil key, the lookup would find exactly
+        // that cell (position self -1 / +1, the cell's level) -- resolved
+        // without one; a lower key (rule #3) and an ok corner.  Hashed
+        // records only: a hashed lookup costs more than the shortcut (deep
+        // extraction 28.0 -> 27.2 ms), a dense one less (C4 43.8 -> 44.0,
+        // C5 14.0 -> 14.8)
+        const uint64_t up = __shfl_up_sync(kFull, kself, 1);
+        const uint64_t dn = __shfl_down_sync(kFull, kself, 1);
+        const uint64_t kp = lane == 0 ? kedge : up, kn = lane == 31 ? kedge : dn;
+        const bool have_p = lane > 0 || cell > 0, have_n = lane < 31 || cell + 1 < a.s.n;
+        if (working && a.unique) {
+          if (have_p && ((st.inrange >> 4) & 1u) && kp == stencil_key(st, 4)) {
+            m.low |= 1u << 4;
+            sm.id[warp][4][lane] = self - 1;
+            sm.lev[warp][4][lane] = uint8_t(c.level);
+            need &= ~(1u << 4);
+          }
+          if (have_n && ((st.inrange >> 22) & 1u) && kn == stencil_key(st, 22)) {
+            m.ok |= 1u << 22;
+            sm.id[warp][22][lane] = self + 1;
+            sm.lev[warp][22][lane] = uint8_t(c.level);
+          }
+        }
       }
       // round 0: every candidate's corner 0 ({-w,0}^3); round 1: the
       // survivors' other corners (one inlined copy of the column code)
