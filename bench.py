@@ -388,6 +388,26 @@ def run_amrx(args):
         torch.cuda.empty_cache()
         P.release_cached_memory()
         e2e = e2e_single(P, hcells, hscal, iso, cap, duals_full, n, local, sh, args)
+        if not args.e2e_single_only:
+            try:
+                pipe = e2e_pipelined(P, hcells, hscal, iso, cap, n, local, sh, args)
+            except Exception as exc:  # device memory: keep the single-step line
+                pipe = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+            e2e["pipelined"] = pipe
+            if "ms_per_step" in pipe and pipe["ms_per_step"] < e2e["ms_per_step"]:
+                # the headline e2e is the steady state of consecutive steps
+                e2e["single_step"] = {k: e2e[k] for k in ("value", "ms_per_step",
+                                                           "triangles_per_s")}
+                e2e["value"] = duals_full / (pipe["ms_per_step"] / 1000.0)
+                e2e["triangles_per_s"] = pipe["triangles"] / (pipe["ms_per_step"] / 1000.0)
+                e2e["ms_per_step"] = pipe["ms_per_step"]
+                e2e["steps"] = pipe["steps"]
+                e2e["mode"] = ("steady state of consecutive steps: build_index from the pinned "
+                               "host input, extract_isosurface into a device soup, its download "
+                               "overlapping the next step's upload (full-duplex host link); "
+                               "every step's H2D and D2H in the timed region, the timer stops "
+                               "after the last download; single_step = one step alone with a "
+                               "pinned host soup")
         del hcells, hscal
 
     line = {
@@ -498,6 +518,56 @@ def e2e_single(P, hcells, hscal, iso, cap, duals_full, n, local, sh, args):
             "ms_per_step": ms_e2e, "triangles_per_s": nt / (ms_e2e / 1000.0),
             "h2d_bytes_per_step": int(n * 16 + n * 8), "d2h_bytes_per_step": int(nt * 72),
             "steps": k2, "link": link}
+
+
+def e2e_pipelined(P, hcells, hscal, iso, cap, n, local, sh, args):
+    """steady-state e2e of consecutive steps through the same public calls:
+    build_index from pinned host input, extract_isosurface into one of two
+    device soups, then that soup's download on a side stream -- which runs
+    while the next step uploads its input (the host link is full duplex).
+    Every step's H2D (24 B/cell) and D2H (72 B/triangle) is inside the timed
+    region; the timer stops after the last download."""
+    import torch
+    dev = torch.device("cuda", local)
+    hout = torch.empty((cap, 9), dtype=torch.float64, pin_memory=True)
+    dsoup = [torch.empty((cap, 9), dtype=torch.float64, device=dev) for _ in range(2)]
+    main = torch.cuda.ExternalStream(sh, device=dev) if sh else torch.cuda.current_stream(dev)
+    down = torch.cuda.Stream(device=dev)
+    done = [None, None]
+
+    def step(i):
+        b = i & 1
+        if done[b] is not None:  # the soup buffer's previous download
+            main.wait_event(done[b])
+        ix = P.build_index(hcells, hscal, device=local, stream=sh, lookup=args.lookup)
+        r = P.extract_isosurface(ix, P.IsoParams(iso=iso), out=dsoup[b])
+        ix.close()
+        nt = len(r.fat)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        down.wait_event(ev)
+        with torch.cuda.stream(down):
+            hout[:nt].copy_(dsoup[b][:nt], non_blocking=True)
+            done[b] = torch.cuda.Event()
+            done[b].record(down)
+        return nt
+
+    step(0)
+    torch.cuda.synchronize(dev)
+    k2 = max(2, min(args.steps, 4))
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(main)
+    t0 = time.perf_counter()
+    for i in range(k2):
+        nt = step(i)
+    main.wait_stream(down)
+    e1.record(main)
+    torch.cuda.synchronize(dev)
+    ms = max(e0.elapsed_time(e1) / k2, 1000 * (time.perf_counter() - t0) / k2)
+    del hout, dsoup
+    return {"ms_per_step": ms, "steps": k2, "triangles": nt,
+            "h2d_bytes_per_step": int(n * 24), "d2h_bytes_per_step": int(nt * 72)}
 
 
 # ------------------------------------------------------------ CPU baseline
@@ -683,6 +753,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=12_000_000)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-single-only", action="store_true",
+                    help="skip the steady-state (pipelined) e2e measurement")
     ap.add_argument("--dist-mode", default="partition", choices=["partition", "replicate"],
                     help="multi-GPU build: distributed sort + exchange, or rank-0 sort + broadcast")
     ap.add_argument("--lookup", default=None, choices=["records", "hash", "directory"],
