@@ -307,10 +307,13 @@ __device__ __forceinline__ int table_row(uint32_t mask)
   return row;
 }
 
-/// centre of the corner cell: anchor + half width, in double (core.hpp:113-118)
+/// centre of the corner cell: anchor + half width, in double (core.hpp:113-118).
+/// The reference's double(anchor) + 0.5 * 2^level is exact (|anchor| < 2^32,
+/// level <= 30), so it equals (2 * anchor + 2^level) converted once and
+/// halved -- the same bits with one conversion and one multiply
 __device__ __forceinline__ double centre(int64_t anchor, int level)
 {
-  return __dadd_rn(double(anchor), __dmul_rn(0.5, double(int64_t(1) << level)));
+  return __dmul_rn(0.5, double(2 * anchor + (int64_t(1) << level)));
 }
 
 /*! marching cubes over one accepted dual (contour.cpp:52-87): write its
