@@ -28,7 +28,7 @@ constexpr int kDigits = 1 << kRadixBits;
 constexpr int kSortThreads = AMRX_SORT_THREADS;
 constexpr int kSortWarps = kSortThreads / 32;
 #ifndef AMRX_SORT_ITEMS
-#define AMRX_SORT_ITEMS 8
+#define AMRX_SORT_ITEMS 9  // C4 ingest: 8 40.4 ms, 9 38.0, 10 40.8 (spills), 12 / 16 at 1 CTA/SM 41.7 / 43.6
 #endif
 constexpr int kSortItems = AMRX_SORT_ITEMS;  // keys per thread
 constexpr int kSortTile = kSortThreads * kSortItems;
@@ -98,7 +98,7 @@ __global__ void digit_offsets_kernel(const unsigned int *hist, int passes,
 }
 
 #ifndef AMRX_SORT_LB
-#define AMRX_SORT_LB 8
+#define AMRX_SORT_LB 4  // with 9 keys per thread: 2 37.9, 3 37.6, 4 37.5, 6 37.7, 8 38.0
 #endif
 constexpr int kLookBack = AMRX_SORT_LB;
 #ifndef AMRX_SORT_MINB
@@ -113,8 +113,13 @@ using WhistT = std::conditional_t<AMRX_SORT_WHIST16 != 0, uint16_t, uint32_t>;
 
 template <typename V>
 struct PassSmem {
-  uint64_t keys[kSortTile];
-  V vals[kSortTile];
+  union {
+    struct {
+      uint64_t keys[kSortTile];
+      V vals[kSortTile];
+    };
+    uint32_t pmasks[kSortWarps * kDigits];  // ranking's peer masks (before the shuffle)
+  };
   WhistT whist[kSortWarps][kDigits];  // per-warp counts -> warp offsets
   uint32_t bexcl[kDigits];              // tile-local digit start
   uint32_t hist[kDigits];               // tile digit counts (early publish)
@@ -151,7 +156,6 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
   // only the shuffle after the ranking writes (two alternating mask sets, to
   // drop one warp barrier per item, measured slower: 42.5 -> 43.0 ms)
   constexpr int kMaskWords = kSortWarps * kDigits;
-  static_assert(sizeof(sm.keys) >= 4 * size_t(kMaskWords), "mask space");
   // zero the per-warp counts and the peer masks with 16-byte stores
   {
     constexpr int kW = int(sizeof(sm.whist) / 16);
@@ -159,7 +163,7 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
 #pragma unroll
     for (int i = threadIdx.x; i < kW; i += kSortThreads) w[i] = make_uint4(0, 0, 0, 0);
     constexpr int kM = kMaskWords * 4 / 16;
-    uint4 *m = reinterpret_cast<uint4 *>(sm.keys);
+    uint4 *m = reinterpret_cast<uint4 *>(sm.pmasks);
 #pragma unroll
     for (int i = threadIdx.x; i < kM; i += kSortThreads) m[i] = make_uint4(0, 0, 0, 0);
   }
@@ -194,7 +198,7 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
   if (digit_thread) st_relaxed(me, (tile == 0 ? kFlagPre : kFlagAgg) | sm.hist[threadIdx.x]);
   // warp multisplit: rank within (warp, digit) in input order
   const uint32_t lt = lanemask_lt();
-  uint32_t *pmask = reinterpret_cast<uint32_t *>(sm.keys) + warp * kDigits;
+  uint32_t *pmask = sm.pmasks + warp * kDigits;
 #pragma unroll
   for (int t = 0; t < kSortItems; t++) {
     const bool valid = dig[t] < kDigits;
