@@ -451,6 +451,13 @@ constexpr int kMcThreads = AMRX_MC_THREADS;
     thread: every lane busy (inside extract_kernel only the few lanes of a
     tile that own a crossing dual were), and its own register budget.  A
     job's corner ids and levels sit in this thread's shared-memory column. */
+struct McSmem {
+  double tcs[12][kMcThreads];
+  uint64_t rows[256];
+  uint32_t jid[8][kMcThreads];
+  uint8_t jlev[8][kMcThreads];
+};
+
 template <bool F32>
 #ifndef AMRX_MC_MINB
 #define AMRX_MC_MINB 4
@@ -458,10 +465,12 @@ template <bool F32>
 __global__ void __launch_bounds__(kMcThreads, AMRX_MC_MINB)
 mc_jobs_kernel(const __grid_constant__ McArgs a)
 {
-  __shared__ uint64_t rows[256];
-  __shared__ uint32_t jid[8][kMcThreads];
-  __shared__ uint8_t jlev[8][kMcThreads];
-  __shared__ double tcs[12][kMcThreads];  // per edge interpolation parameter
+  extern __shared__ __align__(16) unsigned char mc_smem_raw[];
+  McSmem &ms = *reinterpret_cast<McSmem *>(mc_smem_raw);
+  uint64_t *rows = ms.rows;
+  auto &jid = ms.jid;
+  auto &jlev = ms.jlev;
+  auto &tcs = ms.tcs;  // per edge interpolation parameter
   for (int i = threadIdx.x; i < 256; i += kMcThreads) rows[i] = c_mc_rows[table_row(uint32_t(i))];
   __syncthreads();
   const uint64_t n = std::min<uint64_t>(*(volatile unsigned long long *)(a.out + 10), a.job_cap);
@@ -1440,11 +1449,14 @@ ExtractResult run_extract(const ExtractRequest &r, cudaStream_t st)
     });
     res.launches += 1;
     if (T && tri_stage) {
-      const int mgrid = device_sm_count() * 8;
-      if (F)
-        mc_jobs_kernel<true><<<mgrid, kMcThreads, 0, st>>>(m);
-      else
-        mc_jobs_kernel<false><<<mgrid, kMcThreads, 0, st>>>(m);
+      const int mgrid = device_sm_count() * std::max(1, 2048 / kMcThreads);
+      if (F) {
+        ensure_smem_attr(reinterpret_cast<const void *>(mc_jobs_kernel<true>), sizeof(McSmem));
+        mc_jobs_kernel<true><<<mgrid, kMcThreads, sizeof(McSmem), st>>>(m);
+      } else {
+        ensure_smem_attr(reinterpret_cast<const void *>(mc_jobs_kernel<false>), sizeof(McSmem));
+        mc_jobs_kernel<false><<<mgrid, kMcThreads, sizeof(McSmem), st>>>(m);
+      }
       AMRX_LAUNCH_CHECK();
       res.launches += 1;
     }
