@@ -167,12 +167,23 @@ __global__ void __launch_bounds__(256)
 sign_bits_kernel(const double *__restrict__ scal, uint64_t n, double iso,
                  uint32_t *__restrict__ bits)
 {
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u);
+  // a warp takes 4 consecutive 32-value words per step, loads first
+  constexpr int U = 4;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * U;
+  for (uint64_t base = (uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u)) * U;
        base < n; base += stride) {
-    const uint64_t r = base + (threadIdx.x & 31);
-    const uint32_t word = __ballot_sync(kFull, r < n && __ldg(scal + r) > iso);
-    if ((threadIdx.x & 31) == 0) bits[base >> 5] = word;
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint64_t r = base + 32 * u + (threadIdx.x & 31);
+      v[u] = r < n ? __ldg(scal + r) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint64_t r = base + 32 * u + (threadIdx.x & 31);
+      const uint32_t word = __ballot_sync(kFull, r < n && v[u] > iso);
+      if ((threadIdx.x & 31) == 0 && base + 32 * u < n) bits[(base >> 5) + u] = word;
+    }
   }
 }
 
