@@ -12,12 +12,15 @@ namespace amrx {
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef AMRX_GRID_BLOCKS
+#define AMRX_GRID_BLOCKS 32
+#endif
 
 int grid_for(uint64_t n, int threads, int per_thread = 1)
 {
   const uint64_t blocks = (n + uint64_t(threads) * per_thread - 1) /
                           (uint64_t(threads) * per_thread);
-  const uint64_t cap = uint64_t(device_sm_count()) * 32;
+  const uint64_t cap = uint64_t(device_sm_count()) * AMRX_GRID_BLOCKS;  // blocks per SM
   return int(std::max<uint64_t>(1, std::min(blocks, cap)));
 }
 
