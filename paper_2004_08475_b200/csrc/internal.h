@@ -147,7 +147,10 @@ constexpr int kSortMaxPasses = 8;
 
 /// occupancy records are built per tile of 2^kRecTileLog buckets; a
 /// partition's first bucket is a multiple of the tile
-constexpr int kRecTileLog = 12;
+#ifndef AMRX_REC_TILE_LOG
+#define AMRX_REC_TILE_LOG 12
+#endif
+constexpr int kRecTileLog = AMRX_REC_TILE_LOG;
 
 /// key = pack(cell), idx = position (idx may be null).  With hist (device,
 /// kSortMaxPasses x kSortDigits u32, zeroed here) the same pass counts the
