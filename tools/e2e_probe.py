@@ -1,5 +1,8 @@
-"""Break down the host-buffer (e2e) path on the C4 workload: build_index from
-pinned host arrays, extract into a pinned host buffer.  GPU only."""
+"""Break down the host-buffer (e2e) path: build_index from pinned host arrays,
+extract into a pinned host buffer.  GPU only.
+
+python tools/e2e_probe.py [scale]          C4 bricks at a scale
+python tools/e2e_probe.py --config NAME    a bench configuration"""
 import os
 import sys
 import time
@@ -12,30 +15,37 @@ from paper_2004_08475_b200 import synth  # noqa: E402
 
 
 def main():
-    scale = float(sys.argv[1]) if len(sys.argv) > 1 else 1.0
-    b3 = [max(1, int(round(x * scale))) for x in (512, 256, 256)]
-    k = list(synth.C4_KNOBS)
-    k[1] *= scale
-    k[2] *= scale
-    ds = synth.bricks(b3, seed=1, shuffle=True, knobs=k, holes=synth.body_holes(b3))
-    n = len(ds)
-    hc = torch.empty(ds.cells.shape, dtype=torch.int32, pin_memory=True)
-    hs = torch.empty(ds.scalars.shape, dtype=torch.float64, pin_memory=True)
-    hc.copy_(ds.cells)
-    hs.copy_(ds.scalars)
+    iso = synth.C4_ISO
+    if len(sys.argv) > 2 and sys.argv[1] == "--config":
+        import bench
+        cells, scal, _ = bench.make_workload(sys.argv[2], torch.device("cuda", 0))
+        iso = bench.iso_of(sys.argv[2])
+    else:
+        scale = float(sys.argv[1]) if len(sys.argv) > 1 else 1.0
+        b3 = [max(1, int(round(x * scale))) for x in (512, 256, 256)]
+        k = list(synth.C4_KNOBS)
+        k[1] *= scale
+        k[2] *= scale
+        ds = synth.bricks(b3, seed=1, shuffle=True, knobs=k, holes=synth.body_holes(b3))
+        cells, scal = ds.cells, ds.scalars
+    n = len(cells)
+    hc = torch.empty(cells.shape, dtype=torch.int32, pin_memory=True)
+    hs = torch.empty(scal.shape, dtype=torch.float64, pin_memory=True)
+    hc.copy_(cells)
+    hs.copy_(scal)
     t = time.perf_counter()
     torch.cuda.synchronize()
-    probe = P.build_index(ds.cells, ds.scalars)
-    ntri = len(P.extract_isosurface(probe, P.IsoParams(iso=synth.C4_ISO)).fat)
+    probe = P.build_index(cells, scal)
+    ntri = len(P.extract_isosurface(probe, P.IsoParams(iso=iso)).fat)
     probe.close()
     hout = torch.empty((int(ntri * 1.05) + 1024, 9), dtype=torch.float64, pin_memory=True)
     print(f"cells {n} tris {ntri} setup {time.perf_counter() - t:.2f}s", flush=True)
-    for rep in range(3):
+    for rep in range(5):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         ix = P.build_index(hc, hs)
         t1 = time.perf_counter()
-        r = P.extract_isosurface(ix, P.IsoParams(iso=synth.C4_ISO), out=hout)
+        r = P.extract_isosurface(ix, P.IsoParams(iso=iso), out=hout)
         t2 = time.perf_counter()
         ix.close()
         t3 = time.perf_counter()
