@@ -441,7 +441,7 @@ def run_amrx(args):
                                 "(CUDA events around both launches)"), "peak_kind": kind,
                      "alg_bytes_per_launch": alg_bytes,
                      "note": ("not bandwidth bound: extract_kernel issues instructions on "
-                              "74% of cycles at 4.1% of DRAM peak; mc_jobs_kernel waits on "
+                              "78% of cycles at 4% of DRAM peak; mc_jobs_kernel waits on "
                               "the corner-scalar loads (long scoreboard) at 26% of DRAM peak "
                               "(profiles/r02_extract_c4_ncu.txt)")},
         "weld": weld_info if weld_ms is not None else None,
