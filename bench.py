@@ -520,7 +520,7 @@ def e2e_single(P, hcells, hscal, iso, cap, duals_full, n, local, sh, args):
             "steps": k2, "link": link}
 
 
-def e2e_pipelined(P, hcells, hscal, iso, cap, n, local, sh, args):
+def e2e_pipelined(P, hcells, hscal, iso, cap, n, local, sh, args, keep=False):
     """steady-state e2e of consecutive steps through the same public calls:
     build_index from pinned host input, extract_isosurface into one of two
     device soups, then that soup's download on a side stream -- which runs
@@ -565,9 +565,12 @@ def e2e_pipelined(P, hcells, hscal, iso, cap, n, local, sh, args):
     e1.record(main)
     torch.cuda.synchronize(dev)
     ms = max(e0.elapsed_time(e1) / k2, 1000 * (time.perf_counter() - t0) / k2)
+    res = {"ms_per_step": ms, "steps": k2, "triangles": nt,
+           "h2d_bytes_per_step": int(n * 24), "d2h_bytes_per_step": int(nt * 72)}
+    if keep:  # tests: the last step's downloaded soup
+        res["_soup"] = hout[:nt].clone()
     del hout, dsoup
-    return {"ms_per_step": ms, "steps": k2, "triangles": nt,
-            "h2d_bytes_per_step": int(n * 24), "d2h_bytes_per_step": int(nt * 72)}
+    return res
 
 
 # ------------------------------------------------------------ CPU baseline
