@@ -528,7 +528,7 @@ void setup_stream(amrx_index *ix, const amrx_index_opts *opts)
 
 /// bring the device-side lookup structure + padding up for sorted keys;
 /// ix->order receives {descents, equal pairs, longest hash probe}
-void finalize_index(amrx_index *ix)
+void finalize_index(amrx_index *ix, const uint32_t *tile_starts = nullptr)
 {
   cudaStream_t st = ix->stream;
   pad_keys(ix->keys.as<uint64_t>(), ix->n, st);
@@ -540,7 +540,7 @@ void finalize_index(amrx_index *ix)
   if (ix->g.occ == kOccDense) {
     ix->rec.reserve((ix->rec_n ? ix->rec_n + 1 : entries) * sizeof(uint2), st);
     build_directory(ix->keys.as<uint64_t>(), ix->n, ix->g, nullptr, ix->rec.as<uint2>(), order,
-                    ix->scratch, st, ix->rec_lo, ix->rec_n);
+                    ix->scratch, st, ix->rec_lo, ix->rec_n, ix->rec_n ? nullptr : tile_starts);
     ix->info.lookup_entries = ix->rec_n ? ix->rec_n + 1 : entries;
   } else if (ix->g.occ == kOccHash) {
     const uint64_t buckets = hash_count(ix->keys.as<uint64_t>(), ix->n, ix->g, order,
@@ -999,6 +999,8 @@ void create_impl(const int32_t *cells4, const double *scalars, uint64_t n_cells,
     ingest_pack(cells_d, n, ix->g, ix->keys.as<uint64_t>(), idx, st, digit_hist,
                 (ix->g.total + kSortRadixBits - 1) / kSortRadixBits, order2);
 
+    TileStarts tstarts;  // record-tile starts from the sort's last pass
+    DevBuf tstarts_buf;
     uint64_t desc = 0, eq = 0;
     uint32_t *rank = nullptr;
     bool scatter_pending = false;
@@ -1025,13 +1027,22 @@ void create_impl(const int32_t *cells4, const double *scalars, uint64_t n_cells,
       keys_alt.reserve((n + kKeyPad) * sizeof(uint64_t), st);
       int passes = 0;
       bool in_alt = false;
+      if (ix->searchable && ix->g.occ == kOccDense) {
+        // dense records of the whole index: the last pass finds the record
+        // tiles' first positions (no separate sweep over the sorted keys)
+        tstarts.tiles = ((uint64_t(1) << ix->g.dir_bits) + 1 + (uint64_t(1) << kRecTileLog) - 1) >>
+                        kRecTileLog;
+        tstarts_buf.reserve(size_t(tstarts.tiles + 1) * 4, st);
+        tstarts.starts = tstarts_buf.as<uint32_t>();
+        tstarts.shift = ix->g.dir_shift;
+      }
       if (aux) {
         // arriving scalars: the last pass leaves the inverse permutation
         // for the chunk scatters
         auto *idx_alt = static_cast<uint32_t *>(l_ialt.get(kWsIdxAlt, n * 4, st));
         in_alt = radix_sort_pairs(ix->keys.as<uint64_t>(), idx, keys_alt.as<uint64_t>(),
                                   idx_alt, n, ix->g.total, sort_scratch, st, &passes, nullptr,
-                                  nullptr, nullptr, &rank, digit_hist);
+                                  nullptr, nullptr, &rank, digit_hist, &tstarts);
       } else {
         // resident scalars: the sort's 64-bit payload from the first pass
         // on (coalesced reads in input order; no gather, no positions)
@@ -1041,7 +1052,7 @@ void create_impl(const int32_t *cells4, const double *scalars, uint64_t n_cells,
                                       reinterpret_cast<const uint64_t *>(sc_d),
                                       ix->scal.as<uint64_t>(), keys_alt.as<uint64_t>(),
                                       scal_alt.as<uint64_t>(), n, ix->g.total, sort_scratch, st,
-                                      &passes, digit_hist);
+                                      &passes, digit_hist, &tstarts);
         if (in_alt) {
           std::swap(ix->scal.ptr, scal_alt.ptr);
           std::swap(ix->scal.bytes, scal_alt.bytes);
@@ -1057,7 +1068,7 @@ void create_impl(const int32_t *cells4, const double *scalars, uint64_t n_cells,
     }
     nvtxRangePop();
     nvtxRangePushA("lookup structure");
-    finalize_index(ix.get());
+    finalize_index(ix.get(), tstarts.filled ? tstarts.starts : nullptr);
     nvtxRangePop();
     if (scatter_pending) {
       for (int c = 0; c < kScalChunks; c++) {

@@ -884,7 +884,8 @@ void pad_keys(uint64_t *keys, uint64_t n, cudaStream_t st)
 
 void build_directory(const uint64_t *keys, uint64_t n, const KeyGeom &g,
                      uint32_t *dir, uint2 *rec, unsigned long long *order2,
-                     DevBuf &scratch, cudaStream_t st, uint64_t rec_lo, uint64_t rec_n)
+                     DevBuf &scratch, cudaStream_t st, uint64_t rec_lo, uint64_t rec_n,
+                     const uint32_t *tile_starts)
 {
   uint64_t entries = (uint64_t(1) << g.dir_bits) + 1;
   AMRX_CUDA(cudaMemsetAsync(order2, 0, 16, st));
@@ -892,12 +893,15 @@ void build_directory(const uint64_t *keys, uint64_t n, const KeyGeom &g,
     if (rec_n) entries = rec_n + 1;
     const uint64_t tiles = (entries + kRecTile - 1) / kRecTile;
     DevBuf starts;
-    starts.reserve(size_t(tiles + 1) * sizeof(uint32_t), st);
-    rec_tile_start_kernel<<<grid_for(n + 1, kThreads, 4), kThreads, 0, st>>>(
-      keys, n, g.dir_shift, rec_lo, tiles, starts.as<uint32_t>());
-    AMRX_LAUNCH_CHECK();
+    if (!tile_starts) {  // else the sort's last pass found them (rec_lo = 0)
+      starts.reserve(size_t(tiles + 1) * sizeof(uint32_t), st);
+      rec_tile_start_kernel<<<grid_for(n + 1, kThreads, 4), kThreads, 0, st>>>(
+        keys, n, g.dir_shift, rec_lo, tiles, starts.as<uint32_t>());
+      AMRX_LAUNCH_CHECK();
+      tile_starts = starts.as<uint32_t>();
+    }
     rec_build_kernel<<<unsigned(tiles), kRecThreads, 0, st>>>(
-      keys, n, g.dir_shift, entries, starts.as<uint32_t>(), rec, order2);
+      keys, n, g.dir_shift, entries, tile_starts, rec, order2);
     AMRX_LAUNCH_CHECK();
     return;
   }

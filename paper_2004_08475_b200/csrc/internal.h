@@ -187,7 +187,17 @@ void pad_keys(uint64_t *keys, uint64_t n, cudaStream_t st);
 void build_directory(const uint64_t *keys, uint64_t n, const KeyGeom &g,
                      uint32_t *dir, uint2 *rec, unsigned long long *order2,
                      DevBuf &scratch, cudaStream_t st, uint64_t rec_lo = 0,
-                     uint64_t rec_n = 0);
+                     uint64_t rec_n = 0, const uint32_t *tile_starts = nullptr);
+
+/// the record tiles' first key positions, found by the sort's last pass
+/// (dense records of a whole index): starts[t] = first position whose key
+/// >> shift >> kRecTileLog >= t, t in [0, tiles]; filled by the sort
+struct TileStarts {
+  uint32_t *starts = nullptr;  // tiles + 1 entries (device)
+  int shift = 0;
+  uint64_t tiles = 0;
+  bool filled = false;
+};
 
 /// hashed records: distinct buckets of the sorted keys (synchronises);
 /// order2 (device, 2 x u64) receives the keys' descents and equal pairs
@@ -231,7 +241,7 @@ bool radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
                       void *scratch, cudaStream_t st, int *passes_run,
                       const double *gsrc = nullptr, double *gdst = nullptr,
                       cudaEvent_t gsrc_ready = nullptr, uint32_t **rank_out = nullptr,
-                      const unsigned int *hist_in = nullptr);
+                      const unsigned int *hist_in = nullptr, TileStarts *ts = nullptr);
 
 /// radix_sort_pairs with a 64-bit payload that enters from vals_src (read
 /// by the first pass only: e.g. the caller's scalars in input order) and
@@ -240,7 +250,7 @@ bool radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
 bool radix_sort_pairs_u64(uint64_t *keys, const uint64_t *vals_src, uint64_t *vals,
                           uint64_t *keys_alt, uint64_t *vals_alt, uint64_t n, int key_bits,
                           void *scratch, cudaStream_t st, int *passes_run,
-                          const unsigned int *hist_in = nullptr);
+                          const unsigned int *hist_in = nullptr, TileStarts *ts = nullptr);
 
 /// out[rank[i]] = in[i] for i in [0, n) (a payload chunk into key order)
 void scatter_f64(const uint32_t *rank, const double *in, double *out, uint64_t n,

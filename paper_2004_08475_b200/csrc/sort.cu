@@ -144,12 +144,28 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
                      V *__restrict__ vals_out, uint64_t n, int shift,
                      const unsigned long long *__restrict__ digit_start,
                      unsigned long long *state, unsigned int *ticket,
-                     const double *__restrict__ gsrc, double *__restrict__ gdst)
+                     const double *__restrict__ gsrc, double *__restrict__ gdst,
+                     uint32_t *__restrict__ ts, int ts_shift, uint64_t ts_tiles)
 {
   static_assert(MODE == kPassPlain || sizeof(V) == 4, "gather/inverse carry u32 values");
+
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PassSmem<V> &sm = *reinterpret_cast<PassSmem<V> *>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // the record tiles' first positions (last pass only, ts non-null): a key
+  // whose smem predecessor is in its digit run knows its global
+  // predecessor (dst - 1) and writes the tiles between the two exactly; a
+  // run's first key only bounds its own tile (atomicMin) -- the empty tiles
+  // in between are filled by tile_starts_fix_kernel
+  const auto tile_start_note = [&](int pos, uint64_t kk, uint32_t d, uint64_t dst) {
+    const uint64_t tcur = min((kk >> ts_shift) >> kRecTileLog, ts_tiles);
+    if (pos > int(sm.bexcl[d])) {
+      const uint64_t tprev = min((sm.keys[pos - 1] >> ts_shift) >> kRecTileLog, ts_tiles);
+      for (uint64_t t = tprev + 1; t <= tcur; t++) ts[t] = uint32_t(dst);
+    } else {
+      atomicMin(ts + tcur, uint32_t(dst));
+    }
+  };
 
   if (threadIdx.x == 0) sm.tile = atomicAdd(ticket, 1u);
   // peer masks (per warp and digit) live in the key buffer's space, which
@@ -304,6 +320,7 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
       if (!AMRX_BOUND(dst < n && uint64_t(sm.vals[pos]) < n, kChkSort)) continue;
       keys_out[dst] = kk;
       vals_out[sm.vals[pos]] = V(dst);
+      if (ts) tile_start_note(pos, kk, d, dst);
     }
     return;
   }
@@ -338,6 +355,33 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
     if (!AMRX_BOUND(dst < n, kChkSort)) continue;
     keys_out[dst] = kk;
     vals_out[dst] = sm.vals[pos];
+    if (ts) tile_start_note(pos, kk, d, dst);
+  }
+}
+
+/// tile starts after the last pass: a reverse running minimum (the empty
+/// tiles take the next tile's start; never-seen entries are 0xFFFFFFFF),
+/// the sentinel entry is n.  One block: each thread a contiguous segment.
+__global__ void __launch_bounds__(1024) tile_starts_fix_kernel(uint32_t *ts, uint64_t m, uint32_t n)
+{
+  __shared__ uint32_t seg[1024];
+  const uint64_t per = (m + 1023) / 1024;
+  const uint64_t lo = min(m, uint64_t(threadIdx.x) * per), hi = min(m, lo + per);
+  const auto at = [&](uint64_t i) { return i == m - 1 ? min(ts[i], n) : ts[i]; };
+  uint32_t run = 0xFFFFFFFFu;
+  for (uint64_t i = lo; i < hi; i++) run = min(run, at(i));
+  seg[threadIdx.x] = run;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {  // reverse inclusive min-scan of the segments
+    const uint32_t v = threadIdx.x + off < 1024 ? seg[threadIdx.x + off] : 0xFFFFFFFFu;
+    __syncthreads();
+    seg[threadIdx.x] = min(seg[threadIdx.x], v);
+    __syncthreads();
+  }
+  uint32_t carry = threadIdx.x + 1 < 1024 ? seg[threadIdx.x + 1] : 0xFFFFFFFFu;
+  for (uint64_t i = hi; i-- > lo;) {
+    carry = min(carry, at(i));
+    ts[i] = carry;
   }
 }
 
@@ -358,8 +402,9 @@ template <typename V>
 bool sort_impl(uint64_t *keys, const V *vals_src, V *vals, uint64_t *keys_alt, V *vals_alt,
                uint64_t n, int key_bits, void *scratch, cudaStream_t st, int *passes_run,
                const double *gsrc, double *gdst, cudaEvent_t gsrc_ready, uint32_t **rank_out,
-               const unsigned int *hist_in)
+               const unsigned int *hist_in, TileStarts *tstarts)
 {
+  if (tstarts) tstarts->filled = false;
   if (passes_run) *passes_run = 0;
   if (rank_out) *rank_out = nullptr;
   if (n <= 1 || key_bits <= 0) return false;
@@ -414,33 +459,48 @@ bool sort_impl(uint64_t *keys, const V *vals_src, V *vals, uint64_t *keys_alt, V
   uint64_t *kin = keys, *kout = keys_alt;
   V *vin = vals, *vout = vals_alt;
   int run = 0;
+  const bool want_ts = tstarts && tstarts->starts && last >= 0 && !gsrc;
   for (int p = 0; p < passes; p++) {
     if (trivial[p]) continue;
     AMRX_CUDA(cudaMemsetAsync(state, 0, state_bytes, st));
     AMRX_CUDA(cudaMemsetAsync(ticket, 0, 4, st));
     const V *src = run == 0 ? vals_src : vin;
+    uint32_t *ts = nullptr;
+    int ts_shift = 0;
+    uint64_t ts_tiles = 0;
+    if (want_ts && p == last) {
+      AMRX_CUDA(cudaMemsetAsync(tstarts->starts, 0xff, (tstarts->tiles + 1) * 4, st));
+      ts = tstarts->starts;
+      ts_shift = tstarts->shift;
+      ts_tiles = tstarts->tiles;
+    }
     if constexpr (sizeof(V) == 4) {
       if (rank_out && p == last) {
         onesweep_pass_kernel<kPassInverse, uint32_t><<<unsigned(tiles), kSortThreads, smem, st>>>(
           kin, src, kout, vout, n, p * kRadixBits, offs + size_t(p) * kDigits,
-          state, ticket, nullptr, nullptr);
+          state, ticket, nullptr, nullptr, ts, ts_shift, ts_tiles);
         *rank_out = vout;
       } else if (gsrc && p == last) {
         if (gsrc_ready) AMRX_CUDA(cudaStreamWaitEvent(st, gsrc_ready, 0));
         onesweep_pass_kernel<kPassGather, uint32_t><<<unsigned(tiles), kSortThreads, smem, st>>>(
           kin, src, kout, vout, n, p * kRadixBits, offs + size_t(p) * kDigits,
-          state, ticket, gsrc, gdst);
+          state, ticket, gsrc, gdst, nullptr, 0, 0);
       } else {
         onesweep_pass_kernel<kPassPlain, V><<<unsigned(tiles), kSortThreads, smem, st>>>(
           kin, src, kout, vout, n, p * kRadixBits, offs + size_t(p) * kDigits,
-          state, ticket, nullptr, nullptr);
+          state, ticket, nullptr, nullptr, ts, ts_shift, ts_tiles);
       }
     } else {
       onesweep_pass_kernel<kPassPlain, V><<<unsigned(tiles), kSortThreads, smem, st>>>(
         kin, src, kout, vout, n, p * kRadixBits, offs + size_t(p) * kDigits,
-        state, ticket, nullptr, nullptr);
+        state, ticket, nullptr, nullptr, ts, ts_shift, ts_tiles);
     }
     AMRX_LAUNCH_CHECK();
+    if (ts) {
+      tile_starts_fix_kernel<<<1, 1024, 0, st>>>(ts, ts_tiles + 1, uint32_t(n));
+      AMRX_LAUNCH_CHECK();
+      tstarts->filled = true;
+    }
     std::swap(kin, kout);
     std::swap(vin, vout);
     run++;
@@ -461,19 +521,19 @@ bool radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt,
                       uint32_t *vals_alt, uint64_t n, int key_bits,
                       void *scratch, cudaStream_t st, int *passes_run,
                       const double *gsrc, double *gdst, cudaEvent_t gsrc_ready,
-                      uint32_t **rank_out, const unsigned int *hist_in)
+                      uint32_t **rank_out, const unsigned int *hist_in, TileStarts *ts)
 {
   return sort_impl<uint32_t>(keys, vals, vals, keys_alt, vals_alt, n, key_bits, scratch, st,
-                             passes_run, gsrc, gdst, gsrc_ready, rank_out, hist_in);
+                             passes_run, gsrc, gdst, gsrc_ready, rank_out, hist_in, ts);
 }
 
 bool radix_sort_pairs_u64(uint64_t *keys, const uint64_t *vals_src, uint64_t *vals,
                           uint64_t *keys_alt, uint64_t *vals_alt, uint64_t n, int key_bits,
                           void *scratch, cudaStream_t st, int *passes_run,
-                          const unsigned int *hist_in)
+                          const unsigned int *hist_in, TileStarts *ts)
 {
   return sort_impl<uint64_t>(keys, vals_src, vals, keys_alt, vals_alt, n, key_bits, scratch,
-                             st, passes_run, nullptr, nullptr, nullptr, nullptr, hist_in);
+                             st, passes_run, nullptr, nullptr, nullptr, nullptr, hist_in, ts);
 }
 
 }  // namespace amrx
