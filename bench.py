@@ -554,7 +554,7 @@ def e2e_pipelined(P, hcells, hscal, iso, cap, n, local, sh, args, keep=False):
 
     step(0)
     torch.cuda.synchronize(dev)
-    k2 = max(2, min(args.steps, 4))
+    k2 = max(2, min(args.steps, 8))
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(main)
