@@ -941,8 +941,8 @@ void build_hash(const uint64_t *keys, uint64_t n, const KeyGeom &g, ulonglong4 *
 #ifndef AMRX_HASH_GRID_BLOCKS
 #define AMRX_HASH_GRID_BLOCKS 128  // deep hash build 2.98 (32) -> 2.76 ms (512: 4.57)
 #endif
-  hash_build_kernel<<<grid_for(n, kThreads, 4, AMRX_HASH_GRID_BLOCKS), kThreads, 0, st>>>(keys, n, g.dir_shift, tab,
-                                                                   buckets - 1, max_probe);
+  hash_build_kernel<<<grid_for(n, kThreads, 4, AMRX_HASH_GRID_BLOCKS), kThreads, 0, st>>>(
+    keys, n, g.dir_shift, tab, buckets - 1, max_probe);
   AMRX_LAUNCH_CHECK();
 }
 
