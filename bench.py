@@ -542,8 +542,8 @@ def e2e_pipelined(P, hcells, hscal, iso, cap, n, local, sh, args, keep=False):
 
     def step(i):
         b = i & 1
-        if done[b] is not None:  # the soup buffer's previous download
-            main.wait_event(done[b])
+        if done[b] is not None:  # the soup buffer's previous download (long done by now)
+            done[b].synchronize()
         ix = P.build_index(hcells, hscal, device=local, stream=sh, lookup=args.lookup)
         r = P.extract_isosurface(ix, P.IsoParams(iso=iso), out=dsoup[b])
         ix.close()
