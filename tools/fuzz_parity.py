@@ -3,7 +3,7 @@ from the reference's own generators (slots with level jumps up to 5, octrees
 of several fields), shuffled, built on the GPU; the dual mesh, the fat soup
 bits, the four counters and the welded mesh must equal the reference library's.
 
-python tools/fuzz_parity.py [count] [seed0]"""
+python tools/fuzz_parity.py [count] [seed0] [records|hash|directory]"""
 import os
 import sys
 
@@ -19,6 +19,7 @@ import oracles  # noqa: E402
 def main():
     count = int(sys.argv[1]) if len(sys.argv) > 1 else 100
     seed0 = int(sys.argv[2]) if len(sys.argv) > 2 else 1000
+    lookup = sys.argv[3] if len(sys.argv) > 3 else None  # forced lookup structure
     R = oracles.reference()
     kinds = ["sphere", "linear", "rsine"]
     bad = 0
@@ -45,7 +46,7 @@ def main():
         perm = rng.permutation(len(cells))
         # an iso that ties with stored scalars half of the time (strict > rule)
         iso = float(scal[rng.integers(0, len(scal))]) if s % 4 < 2 else float(rng.normal())
-        idx = P.build_index(cells[perm], scal[perm])
+        idx = P.build_index(cells[perm], scal[perm], lookup=lookup)
         d = P.extract_dual_mesh(idx)
         rd = R.extract_dual(h)
         r = P.extract_isosurface(idx, P.IsoParams(iso=iso))
