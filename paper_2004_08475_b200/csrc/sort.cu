@@ -361,28 +361,58 @@ onesweep_pass_kernel(const uint64_t *__restrict__ keys_in,
 
 /// tile starts after the last pass: a reverse running minimum (the empty
 /// tiles take the next tile's start; never-seen entries are 0xFFFFFFFF),
-/// the sentinel entry is n.  One block: each thread a contiguous segment.
-__global__ void __launch_bounds__(1024) tile_starts_fix_kernel(uint32_t *ts, uint64_t m, uint32_t n)
+/// the sentinel entry is n.  Two launches over chunks of 1024 entries: the
+/// chunk minima, then each chunk's reverse scan seeded with the minimum of
+/// the chunks after it.
+constexpr int kFixChunk = 1024;
+
+__device__ __forceinline__ uint32_t ts_at(const uint32_t *ts, uint64_t i, uint64_t m, uint32_t n)
 {
-  __shared__ uint32_t seg[1024];
-  const uint64_t per = (m + 1023) / 1024;
-  const uint64_t lo = min(m, uint64_t(threadIdx.x) * per), hi = min(m, lo + per);
-  const auto at = [&](uint64_t i) { return i == m - 1 ? min(ts[i], n) : ts[i]; };
-  uint32_t run = 0xFFFFFFFFu;
-  for (uint64_t i = lo; i < hi; i++) run = min(run, at(i));
-  seg[threadIdx.x] = run;
+  return i >= m ? 0xFFFFFFFFu : (i == m - 1 ? min(ts[i], n) : ts[i]);
+}
+
+__global__ void __launch_bounds__(kFixChunk) tile_starts_min_kernel(const uint32_t *ts, uint64_t m,
+                                                                   uint32_t n, uint32_t *cmin)
+{
+  __shared__ uint32_t wmin[kFixChunk / 32];
+  const uint64_t i = uint64_t(blockIdx.x) * kFixChunk + threadIdx.x;
+  uint32_t v = ts_at(ts, i, m, n);
+  v = __reduce_min_sync(kFull, v);
+  if ((threadIdx.x & 31) == 0) wmin[threadIdx.x >> 5] = v;
   __syncthreads();
-  for (int off = 1; off < 1024; off <<= 1) {  // reverse inclusive min-scan of the segments
-    const uint32_t v = threadIdx.x + off < 1024 ? seg[threadIdx.x + off] : 0xFFFFFFFFu;
-    __syncthreads();
-    seg[threadIdx.x] = min(seg[threadIdx.x], v);
-    __syncthreads();
+  if (threadIdx.x < 32) {
+    v = __reduce_min_sync(kFull, wmin[threadIdx.x]);
+    if (threadIdx.x == 0) cmin[blockIdx.x] = v;
   }
-  uint32_t carry = threadIdx.x + 1 < 1024 ? seg[threadIdx.x + 1] : 0xFFFFFFFFu;
-  for (uint64_t i = hi; i-- > lo;) {
-    carry = min(carry, at(i));
-    ts[i] = carry;
+}
+
+__global__ void __launch_bounds__(kFixChunk) tile_starts_fix_kernel(uint32_t *ts, uint64_t m,
+                                                                   uint32_t n, const uint32_t *cmin,
+                                                                   uint32_t chunks)
+{
+  __shared__ uint32_t wsum[kFixChunk / 32];
+  __shared__ uint32_t carry_s;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // carry: the minimum over the chunks after this one
+  if (warp == 0) {
+    uint32_t c = 0xFFFFFFFFu;
+    for (uint32_t j = blockIdx.x + 1 + lane; j < chunks; j += 32) c = min(c, cmin[j]);
+    c = __reduce_min_sync(kFull, c);
+    if (lane == 0) carry_s = c;
   }
+  const uint64_t i = uint64_t(blockIdx.x) * kFixChunk + threadIdx.x;
+  uint32_t x = ts_at(ts, i, m, n);
+  // reverse inclusive min-scan over the chunk: within the warp, then across
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_down_sync(kFull, x, off);
+    if (lane + off < 32) x = min(x, y);
+  }
+  if (lane == 0) wsum[warp] = x;  // the warp's minimum
+  __syncthreads();
+  uint32_t later = carry_s;
+  for (int w = warp + 1; w < kFixChunk / 32; w++) later = min(later, wsum[w]);
+  if (i < m) ts[i] = min(x, later);
 }
 
 }  // namespace
@@ -497,7 +527,13 @@ bool sort_impl(uint64_t *keys, const V *vals_src, V *vals, uint64_t *keys_alt, V
     }
     AMRX_LAUNCH_CHECK();
     if (ts) {
-      tile_starts_fix_kernel<<<1, 1024, 0, st>>>(ts, ts_tiles + 1, uint32_t(n));
+      const uint64_t m = ts_tiles + 1;
+      const uint32_t chunks = uint32_t((m + kFixChunk - 1) / kFixChunk);
+      // the look-back state is free after the last pass: the chunk minima
+      uint32_t *cmin = reinterpret_cast<uint32_t *>(state);
+      tile_starts_min_kernel<<<chunks, kFixChunk, 0, st>>>(ts, m, uint32_t(n), cmin);
+      AMRX_LAUNCH_CHECK();
+      tile_starts_fix_kernel<<<chunks, kFixChunk, 0, st>>>(ts, m, uint32_t(n), cmin, chunks);
       AMRX_LAUNCH_CHECK();
       tstarts->filled = true;
     }
